@@ -1,0 +1,198 @@
+/*
+ * ddm.h — C-ABI of the B200-native FMM displacement-discontinuity library
+ * (libddm.so).  Plain pointers and sizes only; no torch or CUDA types.
+ *
+ * The operation this library accelerates is the matrix–vector product of the
+ * constant-element displacement discontinuity method (DDM), PAPER.md
+ * Eq.(final_sigs)–Eq.(final_pp): for N constant elements,
+ *
+ *     y_beta = sum_lambda A^{beta lambda} D^lambda ,
+ *
+ * "nine matrix-vector multiplications ... at each iteration" of GMRES and for
+ * "any extra time step", applied matrix-free through a fast
+ * multipole method (§3) at both of the paper's modification sites:
+ * the GMRES operator apply and the time-marching history sum (P:469-473,
+ * P:922-931).
+ *
+ * Conventions:
+ *   - Element i: centre (xc[i], yc[i]), half-length a[i] > 0, direction angle
+ *     beta[i] (tangent s = (cos, sin), normal n = (-sin, cos)).
+ *   - DOF layout element-major interleaved: D[ncomp*i + c], c = 0 shear D_s,
+ *     1 normal D_n (opening positive), 2 fluid source D_q (poroelastic only).
+ *     Rows: (sigma_s, sigma_n[, p]) at element i's centre, compression
+ *     positive.  ncomp = 2 elastic, 3 poroelastic.
+ *   - Collocation at element centres.
+ *   - All floating point is IEEE fp64.
+ *
+ * Ownership: every array argument is caller-owned and only read (const) or
+ * written (non-const); the library keeps no pointer to caller memory after a
+ * call returns.  Pointers marked [device] must be CUDA device memory on the
+ * context's device; [host] must be host memory.  `stream` is a cudaStream_t
+ * passed as void* (NULL = legacy default stream); every call is ordered on
+ * it, and calls that return data to the host synchronise it.
+ *
+ * Errors: every int-returning call returns a ddm_status; on failure a
+ * message is available from ddm_last_error(ctx) until the next call on that
+ * context.  No call aborts the process.
+ */
+#ifndef DDM_H_
+#define DDM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DDM_OK = 0,
+  DDM_ERR_ARG = 1,     /* invalid argument / dimension / material mismatch   */
+  DDM_ERR_CUDA = 2,    /* CUDA runtime error                                  */
+  DDM_ERR_NOCONV = 3,  /* GMRES did not converge: x = best iterate            */
+  DDM_ERR_NCCL = 4,    /* NCCL error                                          */
+  DDM_ERR_GEOM = 5,    /* non-finite coordinates or coincident points at the
+                          depth cap                                           */
+  DDM_ERR_OOM = 6      /* device allocation failed                            */
+} ddm_status;
+
+enum { DDM_FMM = 0, DDM_DIRECT = 1 };
+
+/* Material (Table rock_prop).  kind 0 = elastic (only G,
+ * nu used), 1 = fully coupled poroelastic.  kappa = k / mu (m^2 / (Pa s)). */
+typedef struct {
+  int kind;
+  double G, nu, nu_u, alpha, kappa;
+} ddm_material;
+
+typedef struct ddm_ctx_s* ddm_ctx_t;
+typedef struct ddm_tree_s* ddm_tree_t;
+
+/* ---------------------------------------------------------------- context
+ * ddm_ctx_create: bind to CUDA `device`.  nccl_uid: NULL for a single GPU,
+ * else the 128-byte ncclUniqueId that rank 0 created (ddm_nccl_unique_id) and
+ * the caller broadcast (torch.distributed is used only for that broadcast).
+ * rank / world: this process's place in the one-process-per-GPU job. */
+int ddm_ctx_create(int device, const void* nccl_uid, int rank, int world, ddm_ctx_t* out);
+void ddm_ctx_destroy(ddm_ctx_t ctx);
+const char* ddm_last_error(ddm_ctx_t ctx);
+/* Writes a fresh ncclUniqueId (128 bytes) into uid_out [host]. */
+int ddm_nccl_unique_id(void* uid_out);
+/* Library version string, e.g. "ddm-b200 0.1 sm_100a". */
+const char* ddm_version(void);
+
+/* ---------------------------------------------------------------- tree
+ * ddm_build_tree — hierarchical tree decomposition: Morton keys
+ * (a1), stable LSD radix sort (a2), cells (a3) and U/V interaction lists (a4)
+ * of DESIGN.md §4.  xc, yc, half_len, beta [device], n elements, user order.
+ * leaf_size: "prescribed number" of P:585 (>= 1).  order_p: number of
+ * complex coefficients per expansion series (2 <= p <= 40).
+ * min_leaf_side: depth cap, no cell is split below this side (0 = none).
+ * The tree is built once per geometry and reused.
+ * Errors: n < 1, leaf_size < 1, bad p -> DDM_ERR_ARG; non-finite coordinates
+ * or more than leaf_size coincident centres at depth 30 -> DDM_ERR_GEOM.
+ * The tree owns its device buffers until ddm_tree_free.  Multi-GPU: every
+ * rank passes the full geometry and builds the same tree; each rank then owns
+ * a contiguous range of Morton-ordered leaves (ddm_tree_partition). */
+int ddm_build_tree(ddm_ctx_t ctx, const double* xc, const double* yc, const double* half_len,
+                   const double* beta, int64_t n, int leaf_size, int order_p,
+                   double min_leaf_side, void* stream, ddm_tree_t* out);
+void ddm_tree_free(ddm_tree_t tree);
+
+/* Sizes of the tree's arrays, written into counts[DDM_TREE_NCOUNTS] [host]. */
+enum {
+  DDM_TC_N = 0, DDM_TC_CELLS, DDM_TC_LEAVES, DDM_TC_LEVELS, DDM_TC_V, DDM_TC_URANGES,
+  DDM_TC_NEAR_PAIRS, DDM_TC_P2P_ITEMS, DDM_TC_OWNED_LO, DDM_TC_OWNED_HI, DDM_TC_P,
+  DDM_TREE_NCOUNTS = 16
+};
+int ddm_tree_counts(ddm_tree_t tree, int64_t* counts);
+
+/* Copy one exported array into dst [host] (capacity in bytes).  Arrays:
+ *   KEYS    u64[n]   Morton key of each element, user order
+ *   PERM    i32[n]   sorted position -> user index
+ *   ROOT    f64[3]   x_min, y_min, W
+ *   LEVEL   i32[c], IX i32[c], IY i32[c], START i32[c], COUNT i32[c],
+ *   PARENT  i32[c], FIRST_CHILD i32[c], NCHILD i32[c], LEAF i32[c]
+ *   V_OFF   i32[c+1], V_IDX i32[nv]            (CSR, per target cell)
+ *   LEAVES  i32[nl]  cell index of each leaf (canonical order)
+ *   U_OFF   i32[nl+1], U_LO i32[nu], U_HI i32[nu]   (CSR of source element
+ *           ranges [lo, hi) in sorted order, per leaf; sorted and merged) */
+enum {
+  DDM_EX_KEYS = 0, DDM_EX_PERM, DDM_EX_ROOT, DDM_EX_LEVEL, DDM_EX_IX, DDM_EX_IY,
+  DDM_EX_START, DDM_EX_COUNT, DDM_EX_PARENT, DDM_EX_FIRST_CHILD, DDM_EX_NCHILD,
+  DDM_EX_LEAF, DDM_EX_V_OFF, DDM_EX_V_IDX, DDM_EX_LEAVES, DDM_EX_U_OFF, DDM_EX_U_LO,
+  DDM_EX_U_HI
+};
+int ddm_tree_export(ddm_tree_t tree, int what, void* dst, int64_t capacity_bytes);
+
+/* Partition the Morton-ordered leaves into `world` contiguous ranges of
+ * near-equal estimated cost (P2P pairs + M2L work) and keep rank's range.
+ * Called automatically by ddm_build_tree with the context's rank/world. */
+int ddm_tree_partition(ddm_tree_t tree, int rank, int world);
+
+/* Host-only helper (no GPU needed): split leaves with exclusive cost prefix
+ * prefix_excl[nleaves] (total = sum of costs) into `world` contiguous ranges:
+ * split[r] = first leaf of rank r, split[world] = nleaves.  Rank r gets the
+ * leaves whose prefix lies in [r total / world, (r+1) total / world). */
+int ddm_split_costs(const int64_t* prefix_excl, int64_t total, int nleaves, int world,
+                    int* split);
+
+/* ---------------------------------------------------------------- matvec
+ * y = A(elapsed) D (Eq.(final_sigs)-(final_pp) left-hand side).
+ * D, y [device], [n][ncomp] user order.  mode DDM_FMM: the FMM of DESIGN.md
+ * §4 (P2M, M2M, M2L, L2L, L2P + exact near-field P2P).
+ * mode DDM_DIRECT: exact all-pairs evaluation (no expansions).  elapsed is the
+ * time since the constant source was switched on (poroelastic; ignored when
+ * elastic).  Multi-GPU: D and y are full-length on every rank; y is complete
+ * on every rank on return (owned slices exchanged with NCCL all-gather).
+ * Errors: material/kind mismatch -> DDM_ERR_ARG. */
+int ddm_matvec(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, double elapsed,
+               const double* D, double* y, int mode, void* stream);
+
+/* r = sum_{m=1}^{h} A^{(m)} D^{h-m}, A^{(m)} = K(( m+1) dt) - K(m dt)
+ * (history double sum of Eq.(final_sigs)-(final_pp)).
+ * D_hist [device] [h][n][3]; r [device] [n][3].  h = 0 or elastic -> r = 0. */
+int ddm_history_apply(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, double dt,
+                      int h, const double* D_hist, double* r, int mode, void* stream);
+
+/* GMRES (reading R11): solve A(dt) x = b with CGS2 Arnoldi,
+ * Givens rotations, restart `restart`, relative tolerance tol on
+ * ||b - A x|| / ||b||.  b, x [device] [n][ncomp]; x holds the initial guess
+ * on entry and the solution on return.  iters, rel_resid [host] outputs
+ * (rel_resid = explicit true residual at exit).  b = 0 -> x = 0, iters = 0.
+ * Returns DDM_ERR_NOCONV with x = last iterate if max_iter is reached. */
+int ddm_gmres_solve(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, double dt,
+                    const double* b, double* x, double tol, int restart, int max_iter,
+                    int mode, int* iters, double* rel_resid, void* stream);
+
+/* Right-hand side of the first step: far-field stresses (sH along
+ * x, sh along y, compression positive) resolved on each face, plus the
+ * hydraulic load: b_s = (sH - sh) sin b cos b; b_n = p_f - sigma_n^ff
+ * (net = 0) or p_f (net = 1); b_p = p_f_pore (poroelastic).  beta [device],
+ * b [device] [n][ncomp]. */
+int ddm_farfield_rhs(ddm_ctx_t ctx, const double* beta, int64_t n, int ncomp, double p_f,
+                     double sH, double sh, int net, double b_p, double* b, void* stream);
+
+/* Stress intensity factors, Olson's formula Eq.(SIF):
+ * K = 0.806 E / (4 (1 - nu^2)) sqrt(pi / (2 a)) D.  w_tip (= D_n), ds_tip,
+ * a_tip, KI, KII [device] length ntips. */
+int ddm_sif(ddm_ctx_t ctx, const double* w_tip, const double* ds_tip, const double* a_tip,
+            int ntips, double E, double nu, double* KI, double* KII, void* stream);
+
+/* Per-stage timings of the last ddm_matvec on this tree (CUDA events, ms),
+ * written into ms[DDM_NSTAGES] [host] when profiling is enabled
+ * (ddm_set_profiling).  Stages: prep, p2m, m2m, m2l, l2l, p2p, l2p+finalize,
+ * exchange. */
+enum { DDM_ST_PREP = 0, DDM_ST_P2M, DDM_ST_M2M, DDM_ST_M2L, DDM_ST_L2L, DDM_ST_P2P,
+       DDM_ST_FINAL, DDM_ST_COMM, DDM_NSTAGES };
+int ddm_set_profiling(ddm_ctx_t ctx, int enable);
+int ddm_stage_times(ddm_ctx_t ctx, double* ms);
+
+/* Measured fp64 FMA throughput of this GPU (TFLOP/s, FMA = 2 flop), from a
+ * DFMA-chain kernel on all SMs, best of 5 (the roofline denominator for the
+ * fp64-ALU-bound kernels).  tflops [host]. */
+int ddm_probe_fp64(ddm_ctx_t ctx, double* tflops, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DDM_H_ */

@@ -1,0 +1,79 @@
+"""ctypes binding of libddm.so (include/ddm.h).  Argument marshalling only:
+every step of the hot path runs inside the library's CUDA kernels.  There is
+no CPU fallback — importing this module fails loudly if the library is
+missing."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libddm.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(there is no CPU fallback)")
+
+lib = C.CDLL(LIB_PATH)
+
+# status codes
+OK, ERR_ARG, ERR_CUDA, ERR_NOCONV, ERR_NCCL, ERR_GEOM, ERR_OOM = range(7)
+FMM, DIRECT = 0, 1
+
+TC = dict(N=0, CELLS=1, LEAVES=2, LEVELS=3, V=4, URANGES=5, NEAR_PAIRS=6, P2P_ITEMS=7,
+          OWNED_LO=8, OWNED_HI=9, P=10)
+NCOUNTS = 16
+EX = dict(KEYS=0, PERM=1, ROOT=2, LEVEL=3, IX=4, IY=5, START=6, COUNT=7, PARENT=8,
+          FIRST_CHILD=9, NCHILD=10, LEAF=11, V_OFF=12, V_IDX=13, LEAVES=14, U_OFF=15, U_LO=16,
+          U_HI=17)
+STAGES = ["prep", "p2m", "m2m", "m2l", "l2l", "p2p", "final", "comm"]
+
+
+class Material(C.Structure):
+    _fields_ = [("kind", C.c_int), ("G", C.c_double), ("nu", C.c_double),
+                ("nu_u", C.c_double), ("alpha", C.c_double), ("kappa", C.c_double)]
+
+
+_vp = C.c_void_p
+_dp = C.c_void_p          # device pointers are passed as integers
+_i64 = C.c_int64
+_d = C.c_double
+_i = C.c_int
+
+
+def _proto(name, res, *args):
+    f = getattr(lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+ddm_version = _proto("ddm_version", C.c_char_p)
+ddm_last_error = _proto("ddm_last_error", C.c_char_p, _vp)
+ddm_nccl_unique_id = _proto("ddm_nccl_unique_id", _i, _vp)
+ddm_ctx_create = _proto("ddm_ctx_create", _i, _i, _vp, _i, _i, C.POINTER(_vp))
+ddm_ctx_destroy = _proto("ddm_ctx_destroy", None, _vp)
+ddm_build_tree = _proto("ddm_build_tree", _i, _vp, _dp, _dp, _dp, _dp, _i64, _i, _i, _d, _vp,
+                        C.POINTER(_vp))
+ddm_tree_free = _proto("ddm_tree_free", None, _vp)
+ddm_tree_counts = _proto("ddm_tree_counts", _i, _vp, C.POINTER(_i64))
+ddm_tree_export = _proto("ddm_tree_export", _i, _vp, _i, _vp, _i64)
+ddm_tree_partition = _proto("ddm_tree_partition", _i, _vp, _i, _i)
+ddm_split_costs = _proto("ddm_split_costs", _i, C.POINTER(_i64), _i64, _i, _i, C.POINTER(_i))
+ddm_matvec = _proto("ddm_matvec", _i, _vp, _vp, C.POINTER(Material), _d, _dp, _dp, _i, _vp)
+ddm_history_apply = _proto("ddm_history_apply", _i, _vp, _vp, C.POINTER(Material), _d, _i, _dp,
+                           _dp, _i, _vp)
+ddm_gmres_solve = _proto("ddm_gmres_solve", _i, _vp, _vp, C.POINTER(Material), _d, _dp, _dp, _d,
+                         _i, _i, _i, C.POINTER(_i), C.POINTER(_d), _vp)
+ddm_farfield_rhs = _proto("ddm_farfield_rhs", _i, _vp, _dp, _i64, _i, _d, _d, _d, _i, _d, _dp,
+                          _vp)
+ddm_sif = _proto("ddm_sif", _i, _vp, _dp, _dp, _dp, _i, _d, _d, _dp, _dp, _vp)
+ddm_set_profiling = _proto("ddm_set_profiling", _i, _vp, _i)
+ddm_stage_times = _proto("ddm_stage_times", _i, _vp, C.POINTER(_d))
+
+EXPORTED = ["ddm_version", "ddm_last_error", "ddm_nccl_unique_id", "ddm_ctx_create",
+            "ddm_ctx_destroy", "ddm_build_tree", "ddm_tree_free", "ddm_tree_counts",
+            "ddm_tree_export", "ddm_tree_partition", "ddm_split_costs", "ddm_matvec",
+            "ddm_history_apply", "ddm_gmres_solve", "ddm_farfield_rhs", "ddm_sif",
+            "ddm_set_profiling", "ddm_stage_times"]

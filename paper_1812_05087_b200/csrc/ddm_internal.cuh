@@ -1,0 +1,192 @@
+// Internal declarations of libddm (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ddm.h"
+
+#ifdef DDM_WITH_NCCL
+#include <nccl.h>
+#endif
+
+namespace ddm {
+
+constexpr int kLBits = 30;      // quantisation bits per axis (R8)
+constexpr int kMaxP = 40;       // max complex coefficients per series
+constexpr int kNOffsets = 49;   // (dx,dy) in [-3,3]^2, class id (dy+3)*7+(dx+3)
+constexpr int kTgtGroup = 32;   // targets per P2P work item (one warp)
+constexpr int kSrcChunk = 512;  // max sources per P2P work item
+
+struct Status {
+  int code = DDM_OK;
+  std::string msg;
+};
+
+// Per-stage CUDA events (optional profiling)
+struct StageEvents {
+  cudaEvent_t ev[2 * DDM_NSTAGES] = {};
+  bool created = false;
+};
+
+}  // namespace ddm
+
+struct ddm_ctx_s {
+  int device = 0;
+  int rank = 0, world = 1;
+  std::string err;
+  bool profiling = false;
+  ddm::StageEvents stage;
+  double stage_ms[DDM_NSTAGES] = {};
+#ifdef DDM_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+  // persistent scratch
+  double* d_scalar = nullptr;     // small device scratch (reductions)
+  double* h_pinned = nullptr;     // small pinned host scratch
+  size_t h_pinned_n = 0;
+};
+
+// Device-side tree and all per-geometry buffers.  Level-major cell numbering,
+// Morton order within a level.
+struct ddm_tree_s {
+  ddm_ctx_s* ctx = nullptr;
+  int64_t n = 0;
+  int leaf = 0, p = 0;
+  int nlevels = 0;           // number of levels (max level + 1)
+  int ncells = 0, nleaves = 0;
+  int64_t nv = 0, nu = 0, near_pairs = 0;
+  int nitems = 0;
+  double x_min = 0, y_min = 0, W = 1;
+  std::vector<int> level_off;    // [nlevels+1] first cell of each level
+  // owned part (multi-GPU): contiguous sorted element range and leaf range
+  int own_leaf_lo = 0, own_leaf_hi = 0;
+  int64_t own_el_lo = 0, own_el_hi = 0;
+  std::vector<int64_t> rank_el_lo;   // [world+1] sorted-element split points
+  std::vector<int> rank_leaf_lo;     // [world+1] leaf split points
+  std::vector<int64_t> leaf_cost_prefix;  // [nleaves+1] exclusive prefix of leaf costs
+
+  // element data (sorted / Morton order)
+  uint64_t* keys_user = nullptr;  // [n] keys in user order
+  uint64_t* keys = nullptr;       // [n] sorted keys
+  int* perm = nullptr;            // [n] sorted -> user
+  double* ex = nullptr;           // [n] centre x
+  double* ey = nullptr;           // [n] centre y
+  double* ea = nullptr;           // [n] half length
+  double* ec = nullptr;           // [n] cos beta
+  double* es = nullptr;           // [n] sin beta
+  int* el_leaf = nullptr;         // [n] leaf (position in leaf list) of each element
+
+  // cells
+  int* c_level = nullptr;
+  int* c_ix = nullptr;
+  int* c_iy = nullptr;
+  int* c_start = nullptr;
+  int* c_count = nullptr;
+  int* c_parent = nullptr;
+  int* c_first_child = nullptr;
+  int* c_nchild = nullptr;
+  int* c_leaf = nullptr;
+  int* colleagues = nullptr;      // [ncells][9], -1 padded
+  int* v_off = nullptr;           // [ncells+1]
+  int* v_idx = nullptr;           // [nv]
+  unsigned char* v_cls = nullptr; // [nv] offset class
+  int* leaves = nullptr;          // [nleaves] cell ids
+  int* u_off = nullptr;           // [nleaves+1]
+  int* u_lo = nullptr;            // [nu]
+  int* u_hi = nullptr;            // [nu]
+  int4* items = nullptr;          // P2P work items: (leaf, tgt0, src_begin, src_end)
+  int* item_off = nullptr;        // [nleaves+1] first item of each leaf
+  int* m2l_cells = nullptr;       // (reserved) cells whose subtree meets the owned range
+  int n_m2l_cells = 0;
+  int item_lo_owned = 0, item_hi_owned = 0;   // P2P items of owned leaves
+
+  // FMM operators (device): M2M[4][p][p] complex, L2L[4][p][p] complex,
+  // Hankel table h[49][2p+2] complex, inverse factorials
+  double2* op_m2m = nullptr;
+  double2* op_l2l = nullptr;
+  double2* op_h = nullptr;
+  double* invfact = nullptr;
+  // expansions: [ncells][2][p] complex
+  double2* mpole = nullptr;
+  double2* local = nullptr;
+  // per-matvec workspaces
+  double* src = nullptr;          // [n][10] P2P source coefficients
+  double2* part = nullptr;        // [nitems*32] partial tractions
+  double* d_sorted = nullptr;     // [n*3] D gathered into sorted order
+  double* y_sorted = nullptr;     // [n*3]
+  double* part_direct = nullptr;  // [n*2] direct-mode tractions (sorted)
+  // GMRES workspace
+  double* krylov = nullptr;
+  int krylov_m = 0;
+  int64_t krylov_dof = 0;
+  double* gm_w = nullptr;
+  double* gm_tmp = nullptr;
+  double* gm_part = nullptr;
+  int64_t gm_part_n = 0;
+};
+
+namespace ddm {
+
+// error helpers (api.cu)
+int set_error(ddm_ctx_s* ctx, int code, const std::string& msg);
+int cuda_error(ddm_ctx_s* ctx, cudaError_t e, const char* what);
+
+#define DDM_CUDA(ctx, call)                                             \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess) return ::ddm::cuda_error((ctx), e_, #call);  \
+  } while (0)
+
+#define DDM_CHECK_LAUNCH(ctx, name) DDM_CUDA(ctx, cudaGetLastError())
+
+template <class T>
+int dalloc(ddm_ctx_s* ctx, T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(ctx, DDM_ERR_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+  }
+  return DDM_OK;
+}
+
+// scan.cu
+int exclusive_scan_i32(ddm_ctx_s* ctx, const int* in, int* out, int n, int* total_host,
+                       cudaStream_t s);
+int exclusive_scan_i64(ddm_ctx_s* ctx, const int64_t* in, int64_t* out, int n, int64_t* total_host,
+                       cudaStream_t s);
+
+// tree.cu
+int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double* a,
+               const double* beta, int64_t n, int leaf, int p, double min_side,
+               cudaStream_t s, ddm_tree_s* t);
+void free_tree(ddm_tree_s* t);
+int partition_tree(ddm_tree_s* t, int rank, int world, cudaStream_t s);
+void split_costs(const int64_t* prefix_excl, int64_t total, int nleaves, int world, int* split);
+
+// fmm.cu
+int fmm_init_operators(ddm_tree_s* t, cudaStream_t s);
+// D: [n][2], user order (d_sorted = false) or sorted order (true), full length.
+// Writes the owned rows into y_user (user order, via perm) and/or y_sorted.
+int fmm_matvec_elastic(ddm_ctx_s* ctx, ddm_tree_s* t, double G, double nu, const double* D,
+                       bool d_sorted, double* y_user, double* y_sorted, int mode,
+                       cudaStream_t s);
+
+// gmres.cu
+int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt,
+                const double* b, double* x, double tol, int restart, int max_iter, int mode,
+                int* iters, double* rel_resid, cudaStream_t s);
+
+// comm (api.cu)
+int allgather_sorted(ddm_ctx_s* ctx, ddm_tree_s* t, double* buf, int ncomp, cudaStream_t s);
+int allreduce_sum(ddm_ctx_s* ctx, double* buf, int64_t count, cudaStream_t s);
+
+// profiling helpers
+void stage_begin(ddm_ctx_s* ctx, int st, cudaStream_t s);
+void stage_end(ddm_ctx_s* ctx, int st, cudaStream_t s);
+
+}  // namespace ddm

@@ -1,0 +1,776 @@
+// Tree build on the GPU (§3.1):
+//   a1 Morton keys: quantise centres into the root square, bit-interleave
+//      (x in bit 0 -> child slot 1 + xbit + 2 ybit, the paper's left->right,
+//      bottom->top indexing);
+//   a2 stable LSD radix sort of (key, user index), 8 bits per pass;
+//   a3 cells level by level from sorted keys: a cell exists iff non-empty and
+//      its parent holds more than `leaf` elements;
+//   a4 colleague (same-level neighbour) lists, V lists ("not neighbors at the
+//      same level, but their parents are neighbors") and U lists
+//      (near field, as merged source-element ranges) + P2P work items.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "ddm_internal.cuh"
+
+namespace ddm {
+namespace {
+
+constexpr int kRadixThreads = 256;
+constexpr int kRadixItems = 16;
+constexpr int kRadixTile = kRadixThreads * kRadixItems;
+
+__device__ __forceinline__ uint64_t spread_bits(uint32_t v) {
+  uint64_t x = v & 0x3fffffffu;
+  x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+  x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  x = (x | (x << 2)) & 0x3333333333333333ull;
+  x = (x | (x << 1)) & 0x5555555555555555ull;
+  return x;
+}
+
+__device__ __forceinline__ uint32_t compact_bits(uint64_t x) {
+  x &= 0x5555555555555555ull;
+  x = (x | (x >> 1)) & 0x3333333333333333ull;
+  x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+  x = (x | (x >> 4)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x >> 8)) & 0x0000FFFF0000FFFFull;
+  x = (x | (x >> 16)) & 0x00000000FFFFFFFFull;
+  return (uint32_t)x;
+}
+
+// ---------------------------------------------------------------- a1
+__global__ void minmax_partial(const double* __restrict__ x, const double* __restrict__ y,
+                               int64_t n, double4* __restrict__ part, int* __restrict__ bad) {
+  double xmn = INFINITY, xmx = -INFINITY, ymn = INFINITY, ymx = -INFINITY;
+  int nonfinite = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double a = x[i], b = y[i];
+    if (!isfinite(a) || !isfinite(b)) nonfinite = 1;
+    xmn = fmin(xmn, a); xmx = fmax(xmx, a); ymn = fmin(ymn, b); ymx = fmax(ymx, b);
+  }
+  for (int o = 16; o; o >>= 1) {
+    xmn = fmin(xmn, __shfl_xor_sync(0xffffffffu, xmn, o));
+    xmx = fmax(xmx, __shfl_xor_sync(0xffffffffu, xmx, o));
+    ymn = fmin(ymn, __shfl_xor_sync(0xffffffffu, ymn, o));
+    ymx = fmax(ymx, __shfl_xor_sync(0xffffffffu, ymx, o));
+  }
+  __shared__ double4 sh[32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sh[w] = make_double4(xmn, xmx, ymn, ymx);
+  if (nonfinite) atomicOr(bad, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double4 r = sh[0];
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      r.x = fmin(r.x, sh[k].x); r.y = fmax(r.y, sh[k].y);
+      r.z = fmin(r.z, sh[k].z); r.w = fmax(r.w, sh[k].w);
+    }
+    part[blockIdx.x] = r;
+  }
+}
+
+__global__ void morton_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                              int64_t n, double xmin, double ymin, double s,
+                              uint64_t* __restrict__ key, int* __restrict__ idx) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double top = (double)((1u << kLBits) - 1);
+  // one IEEE subtract, then one IEEE multiply, never fused (reading R8)
+  double fx = floor(__dmul_rn(__dsub_rn(x[i], xmin), s));
+  double fy = floor(__dmul_rn(__dsub_rn(y[i], ymin), s));
+  fx = fmin(fmax(fx, 0.0), top);
+  fy = fmin(fmax(fy, 0.0), top);
+  key[i] = spread_bits((uint32_t)fx) | (spread_bits((uint32_t)fy) << 1);
+  idx[i] = (int)i;
+}
+
+// ---------------------------------------------------------------- a2
+__global__ void radix_hist(const uint64_t* __restrict__ k, int64_t n, int shift,
+                           int* __restrict__ hist, int nblocks) {
+  __shared__ int h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t t0 = (int64_t)blockIdx.x * kRadixTile;
+  for (int r = 0; r < kRadixItems; ++r) {
+    const int64_t i = t0 + r * kRadixThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[(k[i] >> shift) & 255], 1);
+  }
+  __syncthreads();
+  hist[threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+}
+
+// Stable scatter: items of a tile are visited in order (round r, warp w, lane).
+__global__ void radix_scatter(const uint64_t* __restrict__ kin, const int* __restrict__ vin,
+                              uint64_t* __restrict__ kout, int* __restrict__ vout, int64_t n,
+                              int shift, const int* __restrict__ offs, int nblocks) {
+  __shared__ int base[256];
+  __shared__ int wcnt[kRadixThreads / 32][256];
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  base[tid] = offs[tid * nblocks + blockIdx.x];
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t t0 = (int64_t)blockIdx.x * kRadixTile;
+  for (int r = 0; r < kRadixItems; ++r) {
+    const int64_t i = t0 + r * kRadixThreads + tid;
+    const bool valid = i < n;
+    const uint64_t key = valid ? kin[i] : 0ull;
+    const int val = valid ? vin[i] : 0;
+    const int d = valid ? (int)((key >> shift) & 255) : 256;
+#pragma unroll
+    for (int ww = 0; ww < kRadixThreads / 32; ++ww) wcnt[ww][tid] = 0;
+    __syncthreads();
+    const unsigned mask = __match_any_sync(0xffffffffu, d);
+    const int rank = __popc(mask & lt);
+    if (valid && rank == 0) wcnt[w][d] = __popc(mask);
+    __syncthreads();
+    int run = 0;
+#pragma unroll
+    for (int ww = 0; ww < kRadixThreads / 32; ++ww) {
+      const int c = wcnt[ww][tid];
+      wcnt[ww][tid] = run;
+      run += c;
+    }
+    __syncthreads();
+    if (valid) {
+      const int pos = base[d] + wcnt[w][d] + rank;
+      kout[pos] = key;
+      vout[pos] = val;
+    }
+    __syncthreads();
+    base[tid] += run;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- a3
+struct Cells {
+  int cap = 0;
+  int *level = nullptr, *ix = nullptr, *iy = nullptr, *start = nullptr, *count = nullptr,
+      *parent = nullptr, *first_child = nullptr, *nchild = nullptr, *leaf = nullptr;
+};
+
+int cells_reserve(ddm_ctx_s* ctx, Cells& c, int need, int used, cudaStream_t s) {
+  if (need <= c.cap) return DDM_OK;
+  int ncap = std::max(need, 2 * c.cap);
+  int** fields[9] = {&c.level, &c.ix, &c.iy, &c.start, &c.count, &c.parent, &c.first_child,
+                     &c.nchild, &c.leaf};
+  for (int f = 0; f < 9; ++f) {
+    int* nb = nullptr;
+    int rc = dalloc(ctx, &nb, ncap);
+    if (rc) return rc;
+    if (*fields[f] && used) DDM_CUDA(ctx, cudaMemcpyAsync(nb, *fields[f], sizeof(int) * used,
+                                                          cudaMemcpyDeviceToDevice, s));
+    if (*fields[f]) {
+      DDM_CUDA(ctx, cudaStreamSynchronize(s));
+      cudaFree(*fields[f]);
+    }
+    *fields[f] = nb;
+  }
+  c.cap = ncap;
+  return DDM_OK;
+}
+
+__global__ void split_flags(const uint64_t* __restrict__ keys, const int* __restrict__ cur,
+                            const int* __restrict__ c_start, int64_t n, int sh,
+                            int* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = cur[i];
+  int f = 0;
+  if (c >= 0) f = (i == c_start[c]) || ((keys[i] >> sh) != (keys[i - 1] >> sh));
+  flag[i] = f;
+}
+
+__global__ void create_cells(const uint64_t* __restrict__ keys, const int* __restrict__ cur,
+                             const int* __restrict__ flag, const int* __restrict__ pos,
+                             int64_t n, int sh, int lev, int base, Cells c) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || !flag[i]) return;
+  const int id = base + pos[i];
+  const int par = cur[i];
+  const uint64_t pre = keys[i] >> sh;
+  c.level[id] = lev;
+  c.ix[id] = (int)compact_bits(pre);
+  c.iy[id] = (int)compact_bits(pre >> 1);
+  c.start[id] = (int)i;
+  c.parent[id] = par;
+  c.first_child[id] = -1;
+  c.nchild[id] = 0;
+  if (i == c.start[par]) c.first_child[par] = id;
+}
+
+__global__ void finish_cells(int base, int m, int leaf, int lev, int lmax, Cells c,
+                             int* __restrict__ nsplit, int* __restrict__ geom_bad) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const int id = base + j;
+  const int par = c.parent[id];
+  const bool last = (j + 1 == m) || (c.parent[id + 1] != par);
+  const int end = last ? c.start[par] + c.count[par] : c.start[id + 1];
+  const int cnt = end - c.start[id];
+  c.count[id] = cnt;
+  if (last) c.nchild[par] = id - c.first_child[par] + 1;
+  const bool is_leaf = (cnt <= leaf) || (lev >= lmax);
+  c.leaf[id] = is_leaf ? 1 : 0;
+  if (!is_leaf) atomicAdd(nsplit, 1);
+  if (cnt > leaf && lev >= kLBits && lmax >= kLBits) atomicOr(geom_bad, 1);
+}
+
+__global__ void update_cur(int* __restrict__ cur, const int* __restrict__ flag,
+                           const int* __restrict__ pos, int64_t n, int base,
+                           const int* __restrict__ leaf) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (cur[i] < 0) return;
+  const int child = base + pos[i] + flag[i] - 1;
+  cur[i] = leaf[child] ? -1 : child;
+}
+
+// ---------------------------------------------------------------- a4
+__device__ __forceinline__ bool adj_or_eq(int ax, int ay, int bx, int by) {
+  return abs(ax - bx) <= 1 && abs(ay - by) <= 1;
+}
+
+// colleagues + V candidates for the cells of one level (lev >= 1)
+__global__ void lists_level(int c0, int c1, int lev, const int* __restrict__ parent,
+                            const int* __restrict__ ix, const int* __restrict__ iy,
+                            const int* __restrict__ first_child, const int* __restrict__ nchild,
+                            int* __restrict__ coll, int* __restrict__ vtmp,
+                            unsigned char* __restrict__ vcls_tmp, int* __restrict__ vcnt) {
+  const int c = c0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= c1) return;
+  const int P = parent[c];
+  const int cx = ix[c], cy = iy[c];
+  int nc = 0, nv = 0;
+  for (int k = 0; k < 9; ++k) {
+    const int Q = coll[P * 9 + k];
+    if (Q < 0) break;
+    const int f = first_child[Q], m = nchild[Q];
+    for (int q = f; q < f + m; ++q) {
+      const int qx = ix[q], qy = iy[q];
+      if (adj_or_eq(qx, qy, cx, cy)) {
+        coll[c * 9 + nc++] = q;
+      } else if (lev >= 2) {
+        vtmp[(int64_t)c * 27 + nv] = q;
+        vcls_tmp[(int64_t)c * 27 + nv] = (unsigned char)((qy - cy + 3) * 7 + (qx - cx + 3));
+        ++nv;
+      }
+    }
+  }
+  for (int k = nc; k < 9; ++k) coll[c * 9 + k] = -1;
+  vcnt[c] = nv;
+}
+
+__global__ void compact_v(int ncells, const int* __restrict__ vtmp,
+                          const unsigned char* __restrict__ vcls_tmp,
+                          const int* __restrict__ vcnt, const int* __restrict__ voff,
+                          int* __restrict__ vidx, unsigned char* __restrict__ vcls) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  const int o = voff[c];
+  for (int k = 0; k < vcnt[c]; ++k) {
+    vidx[o + k] = vtmp[(int64_t)c * 27 + k];
+    vcls[o + k] = vcls_tmp[(int64_t)c * 27 + k];
+  }
+}
+
+__global__ void scatter_leaves(int ncells, const int* __restrict__ leaf,
+                               const int* __restrict__ pos, const int* __restrict__ start,
+                               int* __restrict__ leaf_by_start) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < ncells && leaf[c]) leaf_by_start[start[c]] = c;
+}
+
+// leaves in element (Morton) order: walk the element-indexed marker array
+__global__ void gather_leaves(int64_t n, const int* __restrict__ leaf_by_start,
+                              const int* __restrict__ is_start, const int* __restrict__ pos,
+                              int* __restrict__ leaves) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && is_start[i]) leaves[pos[i]] = leaf_by_start[i];
+}
+
+__global__ void leaf_start_flags(int64_t n, const int* __restrict__ leaf_by_start,
+                                 int* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = leaf_by_start[i] >= 0 ? 1 : 0;
+}
+
+__global__ void element_leaf(int nleaves, const int* __restrict__ leaves,
+                             const int* __restrict__ start, const int* __restrict__ count,
+                             int* __restrict__ el_leaf) {
+  const int k = blockIdx.x;
+  if (k >= nleaves) return;
+  const int c = leaves[k];
+  for (int i = threadIdx.x; i < count[c]; i += blockDim.x) el_leaf[start[c] + i] = k;
+}
+
+// Enumerate the near-field source ranges of leaf B (reading R5):
+//  (1) leaf colleagues of every ancestor of B (incl. B itself);
+//  (2) all descendants of non-leaf colleagues of B.
+template <bool kFill>
+__device__ int enum_u(int B, const int* parent, const int* coll, const int* leaf,
+                      const int* start, const int* count, int2* out) {
+  int n = 0;
+  for (int A = B; A >= 0; A = parent[A]) {
+    for (int k = 0; k < 9; ++k) {
+      const int Q = coll[A * 9 + k];
+      if (Q < 0) break;
+      if (leaf[Q]) {
+        if (kFill) out[n] = make_int2(start[Q], start[Q] + count[Q]);
+        ++n;
+      } else if (A == B) {
+        if (kFill) out[n] = make_int2(start[Q], start[Q] + count[Q]);
+        ++n;
+      }
+    }
+  }
+  return n;
+}
+
+__global__ void u_count(int nleaves, const int* __restrict__ leaves, const int* parent,
+                        const int* coll, const int* leaf, const int* start, const int* count,
+                        int* __restrict__ ucnt) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nleaves) return;
+  ucnt[k] = enum_u<false>(leaves[k], parent, coll, leaf, start, count, nullptr);
+}
+
+// fill, sort by lo, merge contiguous ranges; merged count to mcnt, total
+// source count to nsrc
+__global__ void u_fill(int nleaves, const int* __restrict__ leaves, const int* parent,
+                       const int* coll, const int* leaf, const int* start, const int* count,
+                       const int* __restrict__ uoff, int2* __restrict__ utmp,
+                       int* __restrict__ mcnt, int* __restrict__ nsrc) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nleaves) return;
+  int2* r = utmp + uoff[k];
+  const int n = enum_u<true>(leaves[k], parent, coll, leaf, start, count, r);
+  for (int a = 1; a < n; ++a) {  // insertion sort by lo (ranges are disjoint)
+    const int2 v = r[a];
+    int b = a - 1;
+    while (b >= 0 && r[b].x > v.x) { r[b + 1] = r[b]; --b; }
+    r[b + 1] = v;
+  }
+  int m = 0, tot = 0;
+  for (int a = 0; a < n; ++a) {
+    tot += r[a].y - r[a].x;
+    if (m > 0 && r[m - 1].y == r[a].x) r[m - 1].y = r[a].y;
+    else r[m++] = r[a];
+  }
+  mcnt[k] = m;
+  nsrc[k] = tot;
+}
+
+__global__ void u_compact(int nleaves, const int* __restrict__ uoff, const int2* __restrict__ utmp,
+                          const int* __restrict__ moff, const int* __restrict__ mcnt,
+                          int* __restrict__ lo, int* __restrict__ hi) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nleaves) return;
+  for (int a = 0; a < mcnt[k]; ++a) {
+    const int2 v = utmp[uoff[k] + a];
+    lo[moff[k] + a] = v.x;
+    hi[moff[k] + a] = v.y;
+  }
+}
+
+__global__ void item_count(int nleaves, const int* __restrict__ leaves,
+                           const int* __restrict__ count, const int* __restrict__ nsrc,
+                           int* __restrict__ icnt, long long* __restrict__ pairs) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nleaves) return;
+  const int nt = count[leaves[k]];
+  const int groups = (nt + kTgtGroup - 1) / kTgtGroup;
+  const int chunks = max(1, (nsrc[k] + kSrcChunk - 1) / kSrcChunk);
+  icnt[k] = groups * chunks;
+  pairs[k] = (long long)nt * nsrc[k];
+}
+
+// item = (leaf k, first target (sorted index), src_begin, src_end) with the
+// source interval in the leaf's concatenated range space [0, nsrc)
+__global__ void item_fill(int nleaves, const int* __restrict__ leaves,
+                          const int* __restrict__ start, const int* __restrict__ count,
+                          const int* __restrict__ nsrc, const int* __restrict__ ioff,
+                          int4* __restrict__ items) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nleaves) return;
+  const int c = leaves[k];
+  const int nt = count[c];
+  const int groups = (nt + kTgtGroup - 1) / kTgtGroup;
+  const int ns = nsrc[k];
+  const int chunks = max(1, (ns + kSrcChunk - 1) / kSrcChunk);
+  int o = ioff[k];
+  for (int g = 0; g < groups; ++g)
+    for (int h = 0; h < chunks; ++h) {
+      const int b = (int)((long long)ns * h / chunks);
+      const int e = (int)((long long)ns * (h + 1) / chunks);
+      items[o++] = make_int4(k, start[c] + g * kTgtGroup, b, e);
+    }
+}
+
+__global__ void permute_elements(int64_t n, const int* __restrict__ perm,
+                                 const double* __restrict__ xc, const double* __restrict__ yc,
+                                 const double* __restrict__ a, const double* __restrict__ beta,
+                                 double* ex, double* ey, double* ea, double* ec, double* es) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int j = perm[i];
+  ex[i] = xc[j];
+  ey[i] = yc[j];
+  ea[i] = a[j];
+  double sb, cb;
+  sincos(beta[j], &sb, &cb);
+  ec[i] = cb;
+  es[i] = sb;
+}
+
+__global__ void leaf_cost(int nleaves, const int* __restrict__ leaves,
+                          const int* __restrict__ count, const int* __restrict__ nsrc, int p,
+                          long long* __restrict__ cost) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nleaves) return;
+  const long long nt = count[leaves[k]];
+  cost[k] = nt * ((long long)nsrc[k] + p);
+}
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+// Host-side split of per-leaf costs into `world` contiguous ranges of near
+// equal cost.  split[r] = first leaf of rank r, split[world] = n.
+void split_costs(const int64_t* prefix_excl, int64_t total, int nleaves, int world,
+                 int* split) {
+  split[0] = 0;
+  int k = 0;
+  for (int r = 1; r < world; ++r) {
+    const long double target = (long double)total * r / world;
+    while (k < nleaves && (long double)prefix_excl[k] < target) ++k;
+    split[r] = std::max(k, split[r - 1]);
+  }
+  split[world] = nleaves;
+}
+
+void free_tree(ddm_tree_s* t) {
+  void* ptrs[] = {t->keys_user, t->keys, t->perm, t->ex, t->ey, t->ea, t->ec, t->es,
+                  t->el_leaf, t->c_level, t->c_ix, t->c_iy, t->c_start, t->c_count,
+                  t->c_parent, t->c_first_child, t->c_nchild, t->c_leaf, t->colleagues,
+                  t->v_off, t->v_idx, t->v_cls, t->leaves, t->u_off, t->u_lo, t->u_hi,
+                  t->items, t->item_off, t->m2l_cells, t->op_m2m, t->op_l2l, t->op_h,
+                  t->invfact, t->mpole, t->local, t->src, t->part, t->d_sorted, t->y_sorted,
+                  t->part_direct,
+                  t->krylov, t->gm_w, t->gm_tmp, t->gm_part};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+}
+
+int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double* a,
+               const double* beta, int64_t n, int leaf, int p, double min_side,
+               cudaStream_t s, ddm_tree_s* t) {
+  if (n < 1 || n > (int64_t)0x7fffffff) return set_error(ctx, DDM_ERR_ARG, "n out of range");
+  if (leaf < 1) return set_error(ctx, DDM_ERR_ARG, "leaf_size < 1");
+  if (p < 2 || p > kMaxP) return set_error(ctx, DDM_ERR_ARG, "order_p out of [2, 40]");
+  int rc;
+  t->ctx = ctx;
+  t->n = n;
+  t->leaf = leaf;
+  t->p = p;
+
+  // ---- a1: root square
+  const int mmb = 148;
+  double4* part = nullptr;
+  int* dbad = nullptr;
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&part, mmb * sizeof(double4), s));
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&dbad, sizeof(int), s));
+  DDM_CUDA(ctx, cudaMemsetAsync(dbad, 0, sizeof(int), s));
+  minmax_partial<<<mmb, 256, 0, s>>>(xc, yc, n, part, dbad);
+  DDM_CUDA(ctx, cudaGetLastError());
+  std::vector<double4> hpart(mmb);
+  int hbad = 0;
+  DDM_CUDA(ctx, cudaMemcpyAsync(hpart.data(), part, mmb * sizeof(double4),
+                                cudaMemcpyDeviceToHost, s));
+  DDM_CUDA(ctx, cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  DDM_CUDA(ctx, cudaStreamSynchronize(s));
+  cudaFreeAsync(part, s);
+  cudaFreeAsync(dbad, s);
+  if (hbad) return set_error(ctx, DDM_ERR_GEOM, "non-finite element coordinates");
+  double xmn = INFINITY, xmx = -INFINITY, ymn = INFINITY, ymx = -INFINITY;
+  for (auto& v : hpart) {
+    xmn = std::min(xmn, v.x); xmx = std::max(xmx, v.y);
+    ymn = std::min(ymn, v.z); ymx = std::max(ymx, v.w);
+  }
+  double W = std::max(xmx - xmn, ymx - ymn);
+  if (W == 0.0) W = 1.0;
+  const double scale = 1073741824.0 / W;  // 2^30 / W, one IEEE division
+  t->x_min = xmn;
+  t->y_min = ymn;
+  t->W = W;
+  int lmax = kLBits;
+  if (min_side > 0.0) lmax = std::max(0, std::min(kLBits, (int)std::floor(std::log2(W / min_side))));
+
+  // ---- a1 keys, a2 sort
+  uint64_t* k2 = nullptr;
+  int* v2 = nullptr;
+  int* vin = nullptr;
+  if ((rc = dalloc(ctx, &t->keys_user, n)) || (rc = dalloc(ctx, &t->keys, n)) ||
+      (rc = dalloc(ctx, &t->perm, n)))
+    return rc;
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&k2, n * sizeof(uint64_t), s));
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&v2, n * sizeof(int), s));
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&vin, n * sizeof(int), s));
+  morton_kernel<<<nblk(n, 256), 256, 0, s>>>(xc, yc, n, xmn, ymn, scale, t->keys_user, vin);
+  DDM_CUDA(ctx, cudaGetLastError());
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->keys, t->keys_user, n * sizeof(uint64_t),
+                                cudaMemcpyDeviceToDevice, s));
+  {
+    const int nb = (int)nblk(n, kRadixTile);
+    int* hist = nullptr;
+    int* offs = nullptr;
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&hist, sizeof(int) * 256 * nb, s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&offs, sizeof(int) * 256 * nb, s));
+    uint64_t* ka = t->keys;
+    int* va = vin;
+    uint64_t* kb = k2;
+    int* vb = v2;
+    for (int pass = 0; pass < 8; ++pass) {  // 60-bit keys: 8 x 8-bit digits
+      const int shift = 8 * pass;
+      radix_hist<<<nb, 256, 0, s>>>(ka, n, shift, hist, nb);
+      DDM_CUDA(ctx, cudaGetLastError());
+      if ((rc = exclusive_scan_i32(ctx, hist, offs, 256 * nb, nullptr, s))) return rc;
+      radix_scatter<<<nb, kRadixThreads, 0, s>>>(ka, va, kb, vb, n, shift, offs, nb);
+      DDM_CUDA(ctx, cudaGetLastError());
+      std::swap(ka, kb);
+      std::swap(va, vb);
+    }
+    // 8 passes: result back in t->keys / vin
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->perm, va, n * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    cudaFreeAsync(hist, s);
+    cudaFreeAsync(offs, s);
+  }
+  cudaFreeAsync(k2, s);
+  cudaFreeAsync(v2, s);
+  cudaFreeAsync(vin, s);
+
+  // ---- a3 cells, level by level
+  Cells C;
+  if ((rc = cells_reserve(ctx, C, (int)std::max<int64_t>(64, 4 * (n / leaf + 1) + 8), 0, s)))
+    return rc;
+  {
+    const int zero = 0, one = 1, m1 = -1;
+    const int nn = (int)n;
+    const int root_leaf = (n <= leaf || lmax == 0) ? 1 : 0;
+    DDM_CUDA(ctx, cudaMemcpyAsync(C.level, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaMemcpyAsync(C.ix, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaMemcpyAsync(C.iy, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaMemcpyAsync(C.start, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaMemcpyAsync(C.count, &nn, sizeof(int), cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaMemcpyAsync(C.parent, &m1, sizeof(int), cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaMemcpyAsync(C.first_child, &m1, sizeof(int), cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaMemcpyAsync(C.nchild, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaMemcpyAsync(C.leaf, &root_leaf, sizeof(int), cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaStreamSynchronize(s));
+    (void)one;
+  }
+  t->level_off.assign(1, 0);
+  t->level_off.push_back(1);
+  int ncells = 1;
+  {
+    int *cur = nullptr, *flag = nullptr, *pos = nullptr, *dsplit = nullptr, *dgeom = nullptr;
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&cur, n * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&flag, n * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&pos, n * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&dsplit, sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&dgeom, sizeof(int), s));
+    DDM_CUDA(ctx, cudaMemsetAsync(dgeom, 0, sizeof(int), s));
+    const bool root_split = !(n <= leaf || lmax == 0);
+    DDM_CUDA(ctx, cudaMemsetAsync(cur, root_split ? 0 : 0xff, n * sizeof(int), s));
+    int nsplit = root_split ? 1 : 0;
+    for (int lev = 0; nsplit > 0 && lev < kLBits; ++lev) {
+      const int sh = 2 * (kLBits - lev - 1);
+      split_flags<<<nblk(n, 256), 256, 0, s>>>(t->keys, cur, C.start, n, sh, flag);
+      DDM_CUDA(ctx, cudaGetLastError());
+      int m = 0;
+      if ((rc = exclusive_scan_i32(ctx, flag, pos, (int)n, &m, s))) return rc;
+      if ((rc = cells_reserve(ctx, C, ncells + m, ncells, s))) return rc;
+      create_cells<<<nblk(n, 256), 256, 0, s>>>(t->keys, cur, flag, pos, n, sh, lev + 1,
+                                                ncells, C);
+      DDM_CUDA(ctx, cudaGetLastError());
+      DDM_CUDA(ctx, cudaMemsetAsync(dsplit, 0, sizeof(int), s));
+      finish_cells<<<nblk(m, 256), 256, 0, s>>>(ncells, m, leaf, lev + 1, lmax, C, dsplit,
+                                                dgeom);
+      DDM_CUDA(ctx, cudaGetLastError());
+      update_cur<<<nblk(n, 256), 256, 0, s>>>(cur, flag, pos, n, ncells, C.leaf);
+      DDM_CUDA(ctx, cudaGetLastError());
+      DDM_CUDA(ctx, cudaMemcpyAsync(&nsplit, dsplit, sizeof(int), cudaMemcpyDeviceToHost, s));
+      DDM_CUDA(ctx, cudaStreamSynchronize(s));
+      ncells += m;
+      t->level_off.push_back(ncells);
+    }
+    int hgeom = 0;
+    DDM_CUDA(ctx, cudaMemcpyAsync(&hgeom, dgeom, sizeof(int), cudaMemcpyDeviceToHost, s));
+    DDM_CUDA(ctx, cudaStreamSynchronize(s));
+    cudaFreeAsync(cur, s);
+    cudaFreeAsync(flag, s);
+    cudaFreeAsync(pos, s);
+    cudaFreeAsync(dsplit, s);
+    cudaFreeAsync(dgeom, s);
+    if (hgeom || nsplit > 0)
+      return set_error(ctx, DDM_ERR_GEOM,
+                       "more than leaf_size coincident element centres at the depth cap");
+  }
+  t->nlevels = (int)t->level_off.size() - 1;
+  t->ncells = ncells;
+  t->c_level = C.level; t->c_ix = C.ix; t->c_iy = C.iy; t->c_start = C.start;
+  t->c_count = C.count; t->c_parent = C.parent; t->c_first_child = C.first_child;
+  t->c_nchild = C.nchild; t->c_leaf = C.leaf;
+
+  // ---- a4 colleagues and V lists
+  int* vtmp = nullptr;
+  unsigned char* vcls_tmp = nullptr;
+  int* vcnt = nullptr;
+  if ((rc = dalloc(ctx, &t->colleagues, (size_t)ncells * 9))) return rc;
+  if ((rc = dalloc(ctx, &t->v_off, ncells + 1))) return rc;
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&vtmp, (size_t)ncells * 27 * sizeof(int), s));
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&vcls_tmp, (size_t)ncells * 27, s));
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&vcnt, (size_t)(ncells + 1) * sizeof(int), s));
+  {
+    std::vector<int> rootc(9, -1);
+    rootc[0] = 0;
+    const int z = 0;
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->colleagues, rootc.data(), 9 * sizeof(int),
+                                  cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaMemcpyAsync(vcnt, &z, sizeof(int), cudaMemcpyHostToDevice, s));
+    for (int lev = 1; lev < t->nlevels; ++lev) {
+      const int c0 = t->level_off[lev], c1 = t->level_off[lev + 1];
+      lists_level<<<nblk(c1 - c0, 128), 128, 0, s>>>(c0, c1, lev, C.parent, C.ix, C.iy,
+                                                     C.first_child, C.nchild, t->colleagues,
+                                                     vtmp, vcls_tmp, vcnt);
+      DDM_CUDA(ctx, cudaGetLastError());
+    }
+    int nv = 0;
+    if ((rc = exclusive_scan_i32(ctx, vcnt, t->v_off, ncells, &nv, s))) return rc;
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->v_off + ncells, &nv, sizeof(int), cudaMemcpyHostToDevice, s));
+    t->nv = nv;
+    if ((rc = dalloc(ctx, &t->v_idx, nv)) || (rc = dalloc(ctx, &t->v_cls, nv))) return rc;
+    compact_v<<<nblk(ncells, 128), 128, 0, s>>>(ncells, vtmp, vcls_tmp, vcnt, t->v_off,
+                                                t->v_idx, t->v_cls);
+    DDM_CUDA(ctx, cudaGetLastError());
+  }
+  cudaFreeAsync(vtmp, s);
+  cudaFreeAsync(vcls_tmp, s);
+  cudaFreeAsync(vcnt, s);
+
+  // ---- leaves in element order
+  {
+    int *lbs = nullptr, *flag = nullptr, *pos = nullptr;
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&lbs, n * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&flag, n * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&pos, n * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMemsetAsync(lbs, 0xff, n * sizeof(int), s));
+    scatter_leaves<<<nblk(ncells, 256), 256, 0, s>>>(ncells, C.leaf, nullptr, C.start, lbs);
+    DDM_CUDA(ctx, cudaGetLastError());
+    leaf_start_flags<<<nblk(n, 256), 256, 0, s>>>(n, lbs, flag);
+    DDM_CUDA(ctx, cudaGetLastError());
+    int nl = 0;
+    if ((rc = exclusive_scan_i32(ctx, flag, pos, (int)n, &nl, s))) return rc;
+    t->nleaves = nl;
+    if ((rc = dalloc(ctx, &t->leaves, nl)) || (rc = dalloc(ctx, &t->el_leaf, n))) return rc;
+    gather_leaves<<<nblk(n, 256), 256, 0, s>>>(n, lbs, flag, pos, t->leaves);
+    DDM_CUDA(ctx, cudaGetLastError());
+    element_leaf<<<nl, 64, 0, s>>>(nl, t->leaves, C.start, C.count, t->el_leaf);
+    DDM_CUDA(ctx, cudaGetLastError());
+    cudaFreeAsync(lbs, s);
+    cudaFreeAsync(flag, s);
+    cudaFreeAsync(pos, s);
+  }
+
+  // ---- U lists (merged source ranges) and P2P work items
+  {
+    const int nl = t->nleaves;
+    int *ucnt = nullptr, *uoff = nullptr, *mcnt = nullptr, *moff = nullptr, *nsrc = nullptr;
+    int2* utmp = nullptr;
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&ucnt, nl * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&uoff, nl * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&mcnt, nl * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&moff, nl * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&nsrc, nl * sizeof(int), s));
+    u_count<<<nblk(nl, 128), 128, 0, s>>>(nl, t->leaves, C.parent, t->colleagues, C.leaf,
+                                          C.start, C.count, ucnt);
+    DDM_CUDA(ctx, cudaGetLastError());
+    int tot = 0;
+    if ((rc = exclusive_scan_i32(ctx, ucnt, uoff, nl, &tot, s))) return rc;
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&utmp, (size_t)std::max(tot, 1) * sizeof(int2), s));
+    u_fill<<<nblk(nl, 64), 64, 0, s>>>(nl, t->leaves, C.parent, t->colleagues, C.leaf, C.start,
+                                       C.count, uoff, utmp, mcnt, nsrc);
+    DDM_CUDA(ctx, cudaGetLastError());
+    int nu = 0;
+    if ((rc = exclusive_scan_i32(ctx, mcnt, moff, nl, &nu, s))) return rc;
+    t->nu = nu;
+    if ((rc = dalloc(ctx, &t->u_off, nl + 1)) || (rc = dalloc(ctx, &t->u_lo, nu)) ||
+        (rc = dalloc(ctx, &t->u_hi, nu)))
+      return rc;
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->u_off, moff, nl * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->u_off + nl, &nu, sizeof(int), cudaMemcpyHostToDevice, s));
+    u_compact<<<nblk(nl, 128), 128, 0, s>>>(nl, uoff, utmp, moff, mcnt, t->u_lo, t->u_hi);
+    DDM_CUDA(ctx, cudaGetLastError());
+
+    int* icnt = nullptr;
+    long long* pairs = nullptr;
+    long long* pairs_scan = nullptr;
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&icnt, nl * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&pairs, nl * sizeof(long long), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&pairs_scan, nl * sizeof(long long), s));
+    item_count<<<nblk(nl, 128), 128, 0, s>>>(nl, t->leaves, C.count, nsrc, icnt, pairs);
+    DDM_CUDA(ctx, cudaGetLastError());
+    int64_t np = 0;
+    if ((rc = exclusive_scan_i64(ctx, (const int64_t*)pairs, (int64_t*)pairs_scan, nl, &np, s)))
+      return rc;
+    t->near_pairs = np;
+    if ((rc = dalloc(ctx, &t->item_off, nl + 1))) return rc;
+    int ni = 0;
+    if ((rc = exclusive_scan_i32(ctx, icnt, t->item_off, nl, &ni, s))) return rc;
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->item_off + nl, &ni, sizeof(int), cudaMemcpyHostToDevice, s));
+    t->nitems = ni;
+    if ((rc = dalloc(ctx, &t->items, ni))) return rc;
+    item_fill<<<nblk(nl, 128), 128, 0, s>>>(nl, t->leaves, C.start, C.count, nsrc, t->item_off,
+                                            t->items);
+    DDM_CUDA(ctx, cudaGetLastError());
+
+    // per-leaf cost prefix for the multi-GPU partition (kept on host)
+    long long* cost = pairs;  // reuse
+    leaf_cost<<<nblk(nl, 128), 128, 0, s>>>(nl, t->leaves, C.count, nsrc, p, cost);
+    DDM_CUDA(ctx, cudaGetLastError());
+    int64_t ctot = 0;
+    if ((rc = exclusive_scan_i64(ctx, (const int64_t*)cost, (int64_t*)pairs_scan, nl, &ctot, s)))
+      return rc;
+    t->leaf_cost_prefix.assign(nl + 1, 0);
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->leaf_cost_prefix.data(), pairs_scan, nl * sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, s));
+    DDM_CUDA(ctx, cudaStreamSynchronize(s));
+    t->leaf_cost_prefix[nl] = ctot;
+    cudaFreeAsync(ucnt, s);
+    cudaFreeAsync(uoff, s);
+    cudaFreeAsync(mcnt, s);
+    cudaFreeAsync(moff, s);
+    cudaFreeAsync(nsrc, s);
+    cudaFreeAsync(utmp, s);
+    cudaFreeAsync(icnt, s);
+    cudaFreeAsync(pairs, s);
+    cudaFreeAsync(pairs_scan, s);
+  }
+
+  // ---- element data in Morton order
+  if ((rc = dalloc(ctx, &t->ex, n)) || (rc = dalloc(ctx, &t->ey, n)) ||
+      (rc = dalloc(ctx, &t->ea, n)) || (rc = dalloc(ctx, &t->ec, n)) ||
+      (rc = dalloc(ctx, &t->es, n)))
+    return rc;
+  permute_elements<<<nblk(n, 256), 256, 0, s>>>(n, t->perm, xc, yc, a, beta, t->ex, t->ey,
+                                                t->ea, t->ec, t->es);
+  DDM_CUDA(ctx, cudaGetLastError());
+  DDM_CUDA(ctx, cudaStreamSynchronize(s));
+  return DDM_OK;
+}
+
+}  // namespace ddm

@@ -1,0 +1,228 @@
+"""GPU matvec (direct and FMM), GMRES, SIF and history vs the oracle.
+
+Bars (BASELINE.json north_star): DIRECT <= 1e-12, FMM <= 1e-8 (relative L2),
+GMRES solution and SIF <= 1e-6."""
+import numpy as np
+import pytest
+
+from oracle import elastic as OE
+from oracle import sif as OS
+from synth import CONFIGS, make_config, random_dd
+from synth.geometry import Geometry
+
+from ._util import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+G0, NU0 = 8e9, 0.25
+
+
+@pytest.fixture(scope="module")
+def ddm():
+    import torch
+    import paper_1812_05087_b200 as D
+    ctx = D.Context(0)
+    return D, ctx, torch
+
+
+_cache = {}
+
+
+def _setup(D, ctx, torch, cfg, leaf=None, p=20):
+    key = (cfg if isinstance(cfg, int) else id(cfg), leaf, p)
+    if key not in _cache:
+        g = make_config(cfg) if isinstance(cfg, int) else cfg
+        c = CONFIGS[cfg] if isinstance(cfg, int) else {"leaf": 32}
+        f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+        tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta),
+                      leaf_size=leaf or c["leaf"], order_p=p)
+        _cache[key] = (g, tree)
+    return _cache[key]
+
+
+_dense = {}
+
+
+def _A(cfg):
+    if cfg not in _dense:
+        _dense[cfg] = OE.assemble_dense(make_config(cfg), G0, NU0)
+    return _dense[cfg]
+
+
+def _mv(D, ctx, torch, tree, Dv, mode, p=None):
+    mat = D.material(0, G0, NU0)
+    y = D.matvec(ctx, tree, mat, torch.tensor(Dv, device="cuda"), mode=mode)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_direct_parity(ddm, cfg):
+    D, ctx, torch = ddm
+    g, tree = _setup(D, ctx, torch, cfg)
+    Dv = random_dd(g.n, 2, 100 + cfg)
+    y = _mv(D, ctx, torch, tree, Dv, "direct")
+    ref = OE.matvec_dense(_A(cfg), Dv)
+    assert rel_l2(y, ref) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_fmm_parity_random_vector(ddm, cfg):
+    D, ctx, torch = ddm
+    g, tree = _setup(D, ctx, torch, cfg)
+    Dv = random_dd(g.n, 2, 100 + cfg)
+    y = _mv(D, ctx, torch, tree, Dv, "fmm")
+    ref = OE.matvec_dense(_A(cfg), Dv)
+    assert rel_l2(y, ref) <= 1e-8
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_fmm_parity_solution_vector(ddm, cfg):
+    # the oracle's solution vector: near and far fields cancel, so the far
+    # field's truncation error is amplified.  Reading R7:
+    # parity on this vector is stated at p* = CONFIGS[cfg]["p_star"] = 28.
+    D, ctx, torch = ddm
+    g, tree = _setup(D, ctx, torch, cfg, p=CONFIGS[cfg]["p_star"])
+    A = _A(cfg)
+    b = OE.farfield_rhs(g, CONFIGS[cfg]["load"])
+    x = np.linalg.solve(A, b.reshape(-1)).reshape(-1, 2)
+    y = _mv(D, ctx, torch, tree, x, "fmm")
+    assert rel_l2(y, b) <= 1e-8
+
+
+def test_fmm_parity_cfg4_geometry_elastic(ddm):
+    D, ctx, torch = ddm
+    g, tree = _setup(D, ctx, torch, 4)
+    Dv = random_dd(g.n, 2, 104)
+    A = OE.assemble_dense(g, G0, NU0)
+    y = _mv(D, ctx, torch, tree, Dv, "fmm")
+    assert rel_l2(y, OE.matvec_dense(A, Dv)) <= 1e-8
+    yd = _mv(D, ctx, torch, tree, Dv, "direct")
+    assert rel_l2(yd, OE.matvec_dense(A, Dv)) <= 1e-12
+
+
+def test_fmm_parity_cfg5_sampled_rows(ddm):
+    # full size (N = 1e6, leaf 64, p = 20), in the launch configuration bench.py
+    # times; the oracle evaluates sampled rows one by one against all sources
+    D, ctx, torch = ddm
+    g, tree = _setup(D, ctx, torch, 5)
+    Dv = random_dd(g.n, 2, CONFIGS[5]["d_seed"])
+    y = _mv(D, ctx, torch, tree, Dv, "fmm")
+    rows = np.random.default_rng(5).choice(g.n, 48, replace=False)
+    ref = OE.matvec_rows(g, G0, NU0, Dv, rows)
+    assert rel_l2(y[rows], ref) <= 1e-8
+    # and deterministic: a second call is bitwise identical
+    y2 = _mv(D, ctx, torch, tree, Dv, "fmm")
+    assert np.array_equal(y, y2)
+
+
+def test_fmm_order_convergence(ddm):
+    # error falls with p (controllable error) on the solution vector of cfg 2
+    D, ctx, torch = ddm
+    g = make_config(2)
+    A = _A(2)
+    b = OE.farfield_rhs(g, CONFIGS[2]["load"])
+    x = np.linalg.solve(A, b.reshape(-1)).reshape(-1, 2)
+    errs = []
+    for p in (8, 14, 20, 28):
+        _, tree = _setup(D, ctx, torch, 2, p=p)
+        errs.append(rel_l2(_mv(D, ctx, torch, tree, x, "fmm"), b))
+    assert errs[0] > errs[1] > errs[2] >= errs[3] * 0.999
+    assert errs[3] <= 1e-9
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 31, 33])
+def test_small_and_single_leaf_equal_direct(ddm, n):
+    D, ctx, torch = ddm
+    rng = np.random.default_rng(n)
+    x = rng.uniform(0, 10, n)
+    y = rng.uniform(0, 10, n)
+    g = Geometry(x, y, np.full(n, 0.01), rng.uniform(0, np.pi, n), np.zeros(n, int),
+                 np.zeros((1, 2), int))
+    _, tree = _setup(D, ctx, torch, g, leaf=64)
+    Dv = rng.uniform(-1, 1, (n, 2))
+    A = OE.assemble_dense(g, G0, NU0)
+    ref = OE.matvec_dense(A, Dv)
+    assert rel_l2(_mv(D, ctx, torch, tree, Dv, "fmm"), ref) <= 1e-12
+    assert rel_l2(_mv(D, ctx, torch, tree, Dv, "direct"), ref) <= 1e-12
+
+
+def test_matvec_linearity_and_zero(ddm):
+    D, ctx, torch = ddm
+    g, tree = _setup(D, ctx, torch, 2)
+    u = random_dd(g.n, 2, 7)
+    v = random_dd(g.n, 2, 8)
+    yu = _mv(D, ctx, torch, tree, u, "fmm")
+    yv = _mv(D, ctx, torch, tree, v, "fmm")
+    yw = _mv(D, ctx, torch, tree, 2.5 * u + v, "fmm")
+    assert rel_l2(yw, 2.5 * yu + yv) <= 1e-12
+    assert not _mv(D, ctx, torch, tree, np.zeros((g.n, 2)), "fmm").any()
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_gmres_parity_and_sif(ddm, cfg):
+    D, ctx, torch = ddm
+    g, tree = _setup(D, ctx, torch, cfg, p=CONFIGS[cfg]["p_star"])
+    c = CONFIGS[cfg]
+    load = c["load"]
+    mat = D.material(0, G0, NU0)
+    beta = torch.tensor(g.beta, device="cuda")
+    b = D.farfield_rhs(ctx, beta, 2, load["p_f"], load["sH"], load["sh"], net=False)
+    bref = OE.farfield_rhs(g, load)
+    assert rel_l2(b.cpu().numpy(), bref) <= 1e-15
+    x, it, rr = D.gmres_solve(ctx, tree, mat, b, tol=c["tol"])
+    torch.cuda.synchronize()
+    xs = x.cpu().numpy()
+    x_lu = np.linalg.solve(_A(cfg), bref.reshape(-1)).reshape(-1, 2)
+    assert rr <= c["tol"] and it > 0
+    assert rel_l2(xs, x_lu) <= 1e-6
+    # SIF (Eq.SIF) at both tips of every fracture
+    tips = g.tips.reshape(-1)
+    E = 2 * G0 * (1 + NU0)
+    ti = torch.tensor(tips, device="cuda", dtype=torch.long)
+    KI, KII = D.sif(ctx, x[ti, 1].contiguous(), x[ti, 0].contiguous(),
+                    torch.tensor(g.half_len[tips], device="cuda"), E, NU0)
+    KIo, KIIo = OS.sif(x_lu[tips, 1], x_lu[tips, 0], g.half_len[tips], E, NU0)
+    assert rel_l2(KI.cpu().numpy(), KIo) <= 1e-6
+    if cfg == 2:
+        assert rel_l2(KII.cpu().numpy(), KIIo) <= 1e-6
+    if cfg == 1:   # Sneddon through the GPU path
+        w = OE.sneddon_opening(g.xc, 1.0, 1e6, 20e9, NU0)
+        assert abs(xs[100, 1] / w[100] - 1) < 0.01
+
+
+def test_gmres_special_cases(ddm):
+    D, ctx, torch = ddm
+    g, tree = _setup(D, ctx, torch, 1)
+    mat = D.material(0, G0, NU0)
+    b = torch.zeros((g.n, 2), dtype=torch.float64, device="cuda")
+    x0 = torch.ones_like(b)
+    x, it, rr = D.gmres_solve(ctx, tree, mat, b, x=x0)
+    assert it == 0 and not x.any().item()
+    b = torch.tensor(random_dd(g.n, 2, 3) * 1e10, device="cuda")
+    with pytest.raises(D.NoConvergence):
+        D.gmres_solve(ctx, tree, mat, b, tol=1e-14, max_iter=3)
+    x, it, rr = D.gmres_solve(ctx, tree, mat, b, tol=1e-14, max_iter=3, raise_noconv=False)
+    assert it == 3 and rr > 1e-14
+
+
+def test_history_elastic_and_empty(ddm):
+    D, ctx, torch = ddm
+    g, tree = _setup(D, ctx, torch, 2)
+    mat = D.material(0, G0, NU0)
+    Dh = torch.ones((3, g.n, 3), dtype=torch.float64, device="cuda")
+    r = D.history_apply(ctx, tree, mat, 10.0, Dh)
+    assert not r.any().item()
+    r = D.history_apply(ctx, tree, mat, 10.0, Dh[:0])
+    assert not r.any().item()
+
+
+def test_bad_arguments(ddm):
+    D, ctx, torch = ddm
+    g, tree = _setup(D, ctx, torch, 1)
+    Dv = torch.zeros((g.n, 2), dtype=torch.float64, device="cuda")
+    with pytest.raises(D.DDMError) as e:
+        D.matvec(ctx, tree, D.material(0, -1.0, 0.25), Dv)
+    assert e.value.code == 1
+    with pytest.raises(D.DDMError):
+        D.matvec(ctx, tree, D.material(0, G0, 0.25), Dv, mode=7)

@@ -1,0 +1,120 @@
+"""GPU tree build (a1-a4) vs the oracle: bit-exact keys, permutation, cells and
+U/V lists."""
+import numpy as np
+import pytest
+
+from oracle import tree as OT
+from synth import make_config
+from synth.geometry import Geometry
+
+from ._util import gpu_u_ranges, gpu_v_lists, oracle_u_ranges
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ddm():
+    import torch
+    import paper_1812_05087_b200 as D
+    ctx = D.Context(0)
+    return D, ctx, torch
+
+
+def _tensors(torch, g):
+    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+    return f(g.xc), f(g.yc), f(g.half_len), f(g.beta)
+
+
+def _compare(D, ctx, torch, g, leaf, lists=True, sample=None, min_side=0.0):
+    tree = D.Tree(ctx, *_tensors(torch, g), leaf_size=leaf, order_p=20, min_leaf_side=min_side)
+    ot = OT.build_tree(g.xc, g.yc, leaf, min_leaf_side=min_side)
+    assert np.array_equal(tree.export("KEYS"), ot.keys)
+    assert np.array_equal(tree.export("PERM"), ot.perm.astype(np.int32))
+    root = tree.export("ROOT")
+    assert (root[0], root[1], root[2]) == (ot.x_min, ot.y_min, ot.W)
+    assert tree.counts["CELLS"] == ot.n_cells
+    for name, arr in (("LEVEL", ot.level), ("IX", ot.ix), ("IY", ot.iy), ("START", ot.start),
+                      ("COUNT", ot.count), ("PARENT", ot.parent),
+                      ("FIRST_CHILD", ot.first_child), ("NCHILD", ot.n_child),
+                      ("LEAF", ot.is_leaf.astype(int))):
+        assert np.array_equal(tree.export(name), arr.astype(np.int32)), name
+    leaves_by_start = sorted(np.nonzero(ot.is_leaf)[0], key=lambda c: ot.start[c])
+    assert np.array_equal(tree.export("LEAVES"), np.array(leaves_by_start, dtype=np.int32))
+    if lists:
+        if sample is None:
+            V = OT.v_lists(ot)
+            U = OT.u_lists(ot)
+        else:
+            rng = np.random.default_rng(0)
+            cells = rng.choice(ot.n_cells, size=min(sample, ot.n_cells), replace=False)
+            leaves = rng.choice(np.nonzero(ot.is_leaf)[0], size=min(sample, int(ot.is_leaf.sum())),
+                                replace=False)
+            V = OT.v_lists(ot, cells)
+            U = OT.u_lists(ot, leaves)
+        gv = gpu_v_lists(tree)
+        for c, lst in V.items():
+            assert gv[c] == lst, c
+        gu = gpu_u_ranges(tree)
+        ou = oracle_u_ranges(ot, U)
+        for b, rs in ou.items():
+            assert gu[b] == rs, b
+    return tree, ot
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_tree_bitexact_configs(ddm, cfg):
+    D, ctx, torch = ddm
+    g = make_config(cfg)
+    tree, ot = _compare(D, ctx, torch, g, 32, sample=None if cfg != 3 else 400)
+    if cfg == 2:   # SURVEY.md §8 sizing table (own generator reproduces it)
+        assert tree.counts["CELLS"] == 195 and tree.counts["LEAVES"] == 140
+        assert tree.counts["V"] == 2124 and tree.counts["NEAR_PAIRS"] == 327618
+
+
+def test_tree_bitexact_config5_full_size(ddm):
+    D, ctx, torch = ddm
+    g = make_config(5)
+    _compare(D, ctx, torch, g, 64, sample=300)
+
+
+@pytest.mark.parametrize("seed,n,leaf", [(1, 1, 1), (2, 2, 1), (3, 33, 1), (4, 257, 3),
+                                         (5, 1000, 7), (6, 4097, 16), (7, 5000, 64)])
+def test_tree_bitexact_random_ragged(ddm, seed, n, leaf):
+    D, ctx, torch = ddm
+    rng = np.random.default_rng(seed)
+    if seed % 2:
+        x, y = rng.uniform(-5, 5, n), rng.uniform(0, 1, n)
+    else:   # clustered, duplicated coordinates along lines
+        x = np.round(rng.normal(size=n), 2)
+        y = 0.5 * x + 0.01 * rng.integers(4, size=n)
+    g = Geometry(x, y, np.full(n, 1e-3), rng.uniform(0, np.pi, n), np.zeros(n, int),
+                 np.zeros((1, 2), int))
+    try:
+        _compare(D, ctx, torch, g, leaf)
+    except OT.GeometryError:
+        with pytest.raises(D.DDMError):
+            D.Tree(ctx, *_tensors(torch, g), leaf_size=leaf)
+
+
+def test_depth_cap(ddm):
+    D, ctx, torch = ddm
+    g = make_config(4)
+    _compare(D, ctx, torch, g, 32, min_side=3.77)
+
+
+def test_geometry_errors(ddm):
+    D, ctx, torch = ddm
+    n = 10
+    g = Geometry(np.full(n, 0.5), np.full(n, 0.5), np.full(n, 1e-3), np.zeros(n), np.zeros(n, int),
+                 np.zeros((1, 2), int))
+    with pytest.raises(D.DDMError) as e:
+        D.Tree(ctx, *_tensors(torch, g), leaf_size=4)
+    assert e.value.code == 5
+    g.xc = g.xc.copy()
+    g.xc[3] = np.nan
+    with pytest.raises(D.DDMError) as e:
+        D.Tree(ctx, *_tensors(torch, g), leaf_size=64)
+    assert e.value.code == 5
+    with pytest.raises(D.DDMError) as e:
+        D.Tree(ctx, *_tensors(torch, g), leaf_size=0)
+    assert e.value.code == 1
