@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark: FMM DDM matvec on config 5 (N = 1e6 elastic elements, leaf 64,
+p = 20) — BASELINE.json metric "FMM DDM matvec interactions/s and GMRES solve
+time (fp64) vs roofline, 1/2/4/8 GPU".
+
+A step is one FMM matvec y = A D (prep, P2M, M2M, M2L, L2L, P2P, L2P+finalize;
+the tree is built once per geometry, and timed separately).
+value = dense-equivalent interactions/s = N^2 per matvec (whole job).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  (N > 1: launched by torchrun, one rank per GPU, NCCL)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("FMM DDM matvec interactions/s and GMRES solve time (fp64) vs roofline, "
+          "1/2/4/8 GPU")
+UNIT = "interactions/s"
+FLOP_PER_PAIR = 64          # P2P pair update, FMA = 2 flop
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, local, world
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.f = tempfile.NamedTemporaryFile(prefix="clocks", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) >= 9:
+                for k, nm in enumerate(names):
+                    if r[5 + k].strip().lower() == "active":
+                        reasons.add(nm)
+        loaded = [v for v in sm if v > 300] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def cpu_baseline_oracle(g, mat, Dv, rows: int):
+    """The oracle (numpy, fp64, as it stands) on a bounded sample: `rows` target
+    rows of config 5 against all N sources (oracle/elastic.matvec_rows)."""
+    from oracle import elastic as OE
+    idx = np.random.default_rng(1234).choice(g.n, rows, replace=False)
+    t0 = time.perf_counter()
+    OE.matvec_rows(g, mat["G"], mat["nu"], Dv, idx)
+    dt = time.perf_counter() - t0
+    return rows * g.n / dt, dt
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the host cores, rank 0 only."""
+    rank, _, world = _dist()
+    if rank != 0:
+        return
+    from synth import CONFIGS, make_config, random_dd
+    c = CONFIGS[args.config]
+    g = make_config(args.config)
+    Dv = random_dd(g.n, 2, c["d_seed"])
+    rows = args.ref_rows
+    for _ in range(args.warmup):
+        cpu_baseline_oracle(g, c["material"], Dv, max(1, rows // 4))
+    times = []
+    for _ in range(args.steps):
+        v, dt = cpu_baseline_oracle(g, c["material"], Dv, rows)
+        times.append(dt)
+    tot = sum(times)
+    value = args.steps * rows * g.n / tot
+    sample = (f"{rows} seeded target rows x all {g.n} sources per step "
+              f"(oracle.elastic.matvec_rows, numpy fp64)")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": c["name"], "N": g.n, "leaf": c["leaf"], "p": c["p"]},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1812_05087_b200 as D
+    from synth import CONFIGS, make_config, random_dd
+
+    rank, local, world = _dist()
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    uid = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [D.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    ctx = D.Context(local, rank, world, uid)
+    c = CONFIGS[args.config]
+    p = args.p or c["p"]
+    g = make_config(args.config)
+    n = g.n
+    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
+    xc, yc, hl, be = f(g.xc), f(g.yc), f(g.half_len), f(g.beta)
+    mat = D.material_from_dict(c["material"])
+    stream = torch.cuda.current_stream()
+
+    # tree (built once per geometry)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    tree = D.Tree(ctx, xc, yc, hl, be, leaf_size=c["leaf"], order_p=p)
+    e1.record()
+    torch.cuda.synchronize()
+    tree_ms = e0.elapsed_time(e1)
+    cnt = tree.counts
+
+    Dv_host = random_dd(n, 2, c["d_seed"])
+    Dd = f(Dv_host)
+    y = torch.empty_like(Dd)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    for _ in range(args.warmup):
+        D.matvec(ctx, tree, mat, Dd, y)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K matvecs, L2 flushed between steps (outside the events)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    for k in range(args.steps):
+        flush.zero_()
+        starts[k].record()
+        D.matvec(ctx, tree, mat, Dd, y)
+        ends[k].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    value = args.steps * float(n) * float(n) / (tot_ms * 1e-3)
+
+    # ---- end to end: pinned host D -> device, matvec, device -> pinned host y
+    hD = torch.from_numpy(Dv_host).pin_memory()
+    hy = torch.empty_like(hD).pin_memory()
+    Dd2 = torch.empty_like(Dd)
+    for _ in range(2):
+        Dd2.copy_(hD, non_blocking=True)
+        D.matvec(ctx, tree, mat, Dd2, y)
+        hy.copy_(y, non_blocking=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ee0.record()
+    for _ in range(args.steps):
+        Dd2.copy_(hD, non_blocking=True)
+        D.matvec(ctx, tree, mat, Dd2, y)
+        hy.copy_(y, non_blocking=True)
+    ee1.record()
+    torch.cuda.synchronize()
+    e2e_ms = ee0.elapsed_time(ee1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = args.steps * float(n) * float(n) / (e2e_ms * 1e-3)
+
+    # ---- per-stage CUDA events (separate instrumented run) for the roofline
+    ctx.set_profiling(True)
+    stages = {k: 0.0 for k in ("prep", "p2m", "m2m", "m2l", "l2l", "p2p", "final", "comm")}
+    nprof = max(3, min(args.steps, 10))
+    for _ in range(nprof):
+        flush.zero_()
+        D.matvec(ctx, tree, mat, Dd, y)
+        torch.cuda.synchronize()
+        for k, v in ctx.stage_times().items():
+            stages[k] += v / nprof
+    ctx.set_profiling(False)
+    fp64_peak = ctx_probe_fp64(ctx)
+    owned_pairs = cnt["NEAR_PAIRS"] / world   # approx. per rank for N > 1
+    p2p_ms = stages["p2p"]
+    achieved = owned_pairs * FLOP_PER_PAIR / (p2p_ms * 1e-3) / 1e12
+    levels = cnt["LEVELS"]
+    launches_per_step = 1 + 1 + max(0, levels - 3) + 1 + max(0, levels - 3) + 1 + 1
+    if world > 1:
+        launches_per_step += 2
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic",
+           "config": {"workload": c["name"], "N": n, "leaf": c["leaf"], "p": p,
+                      "elements_per_fracture": 100, "fractures": 10000, "box_m": 2000,
+                      "parallelism": f"morton-leaf-partition x{world}",
+                      "l2": "flushed between steps (256 MiB write, outside the step events)",
+                      "tree_build_ms": tree_ms, "cells": cnt["CELLS"], "leaves": cnt["LEAVES"],
+                      "levels": levels, "v_pairs": cnt["V"], "near_pairs": cnt["NEAR_PAIRS"]},
+           "stage_ms": stages,
+           "roofline": {"bound": "alu", "kernel": "p2p_kernel (fp64 pipe)",
+                        "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                        "frac": achieved / fp64_peak if fp64_peak else None,
+                        "traffic": None,
+                        "peak_source": "measured DFMA-chain probe (ddm_probe_fp64) on this GPU",
+                        "flop_per_pair": FLOP_PER_PAIR,
+                        "p2p_share_of_step": p2p_ms / ms_per_step},
+           "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(hD.numel() * 8),
+                   "d2h_bytes_per_step": int(hy.numel() * 8),
+                   "ms_per_step": e2e_ms / args.steps},
+           "gpu_launches": launches_per_step * args.steps,
+           "clocks": clocks}
+
+    if rank == 0 and world == 1 and not args.no_extras:
+        # GMRES solve time on config 2 (the metric's second half), at p and p*
+        out["gmres"] = gmres_extra(D, ctx, torch, dev)
+        gv, gdt = cpu_baseline_oracle(g, c["material"], Dv_host, args.cpu_rows)
+        out["cpu_baseline"] = {"value": gv, "unit": UNIT, "cores": 1, "kind": "oracle",
+                               "sample": f"{args.cpu_rows} seeded target rows x all {n} sources "
+                                         f"(oracle.elastic.matvec_rows, numpy fp64, {gdt:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def ctx_probe_fp64(ctx) -> float:
+    import ctypes as C
+    from paper_1812_05087_b200 import _lib as L
+    import torch
+    v = C.c_double(0.0)
+    rc = L.lib.ddm_probe_fp64(ctx._h, C.byref(v), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    return v.value if rc == 0 else None
+
+
+def gmres_extra(D, ctx, torch, dev):
+    from synth import CONFIGS, make_config
+    res = {}
+    g = make_config(2)
+    c = CONFIGS[2]
+    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
+    mat = D.material_from_dict(c["material"])
+    for p in (c["p"], c["p_star"]):
+        tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=c["leaf"],
+                      order_p=p)
+        ld = c["load"]
+        b = D.farfield_rhs(ctx, f(g.beta), 2, ld["p_f"], ld["sH"], ld["sh"])
+        D.gmres_solve(ctx, tree, mat, b, tol=c["tol"])   # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x, it, rr = D.gmres_solve(ctx, tree, mat, b, tol=c["tol"])
+        torch.cuda.synchronize()
+        res[f"cfg2_p{p}"] = {"solve_ms": 1e3 * (time.perf_counter() - t0), "iters": it,
+                             "rel_resid": rr}
+        tree.free()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--p", type=int, default=0)
+    ap.add_argument("--cpu-rows", type=int, default=64)
+    ap.add_argument("--ref-rows", type=int, default=16)
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
