@@ -17,7 +17,7 @@ namespace ddm {
 constexpr int kLBits = 30;      // quantisation bits per axis (R8)
 constexpr int kMaxP = 40;       // max complex coefficients per series
 constexpr int kNOffsets = 49;   // (dx,dy) in [-3,3]^2, class id (dy+3)*7+(dx+3)
-constexpr int kTgtGroup = 32;   // targets per P2P work item (one warp)
+constexpr int kTgtGroup = 8;    // targets per P2P work item (one warp, 32/nt source slices)
 constexpr int kSrcChunk = 512;  // max sources per P2P work item
 
 struct Status {
@@ -107,7 +107,8 @@ struct ddm_tree_s {
   // Hankel table h[49][2p+2] complex, inverse factorials
   double2* op_m2m = nullptr;
   double2* op_l2l = nullptr;
-  double2* op_h = nullptr;
+  double2* op_h = nullptr;        // M2L rotations e^{-ik theta} [49][p+2]
+  double* op_R = nullptr;         // M2L real Hankel entries [49][2p+2]
   double* invfact = nullptr;
   // expansions: [ncells][2][p] complex
   double2* mpole = nullptr;

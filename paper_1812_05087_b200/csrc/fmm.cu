@@ -41,6 +41,22 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return fma(r, fma(e, e, e), r);
 }
 
+// Block-wide global -> shared copy with 8 loads in flight per thread (a plain
+// strided loop waits one L2 round trip per element).
+template <class T>
+__device__ __forceinline__ void block_copy(T* __restrict__ dst, const T* __restrict__ src, int n) {
+  const int step = blockDim.x;
+  int f = threadIdx.x;
+  for (; f + 7 * step < n; f += 8 * step) {
+    T v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = src[f + k * step];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dst[f + k * step] = v[k];
+  }
+  for (; f < n; f += step) dst[f] = src[f];
+}
+
 struct CellGeom {
   double x_min, y_min, W;
   __device__ __forceinline__ double side(int lev) const { return ldexp(W, -lev); }
@@ -130,6 +146,11 @@ __device__ __forceinline__ double2 acc_to_traction(const P2PAcc& a, double gc, d
 }
 
 // ------------------------------------------------------------ P2P (near field)
+// One warp per work item (leaf k, group of nt <= kTgtGroup targets, interval
+// of the leaf's concatenated source ranges).  The 32 lanes are split into
+// S = 32 / nt source slices: lane l evaluates target l % nt against the
+// sources j = l / nt (mod S) of each 32-source batch staged in shared memory;
+// the S slice partials are then summed in a fixed order (deterministic).
 constexpr int kP2PWarps = 4;
 
 __global__ void __launch_bounds__(kP2PWarps * 32)
@@ -141,6 +162,7 @@ p2p_kernel(int item_lo, int item_hi, const int4* __restrict__ items,
            const double* __restrict__ ey, const double* __restrict__ ec,
            const double* __restrict__ es, double gc, double2* __restrict__ part) {
   __shared__ double sh[kP2PWarps][32 * 10];
+  __shared__ double red[kP2PWarps][3][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* ssrc = sh[w];
   for (int it = item_lo + blockIdx.x * kP2PWarps + w; it < item_hi;
@@ -148,11 +170,12 @@ p2p_kernel(int item_lo, int item_hi, const int4* __restrict__ items,
     const int4 item = items[it];
     const int k = item.x;
     const int c = leaves[k];
-    const int tend = c_start[c] + c_count[c];
-    const int ti = item.y + lane;
-    const bool tvalid = ti < tend;
-    double zx = 0.0, zy = 0.0;
-    if (tvalid) { zx = ex[ti]; zy = ey[ti]; }
+    const int nt = min(kTgtGroup, c_start[c] + c_count[c] - item.y);
+    const int S = 32 / nt;
+    const int tl = lane % nt, slice = lane / nt;
+    const bool active = slice < S;
+    const int ti = item.y + tl;
+    const double zx = ex[ti], zy = ey[ti];
     P2PAcc acc;
     // cursor into the leaf's concatenated source ranges
     int r = u_off[k];
@@ -161,7 +184,6 @@ p2p_kernel(int item_lo, int item_hi, const int4* __restrict__ items,
     while (r < rend && roff >= u_hi[r] - u_lo[r]) { roff -= u_hi[r] - u_lo[r]; ++r; }
     for (int t = item.z; t < item.w; t += 32) {
       const int nb = min(32, item.w - t);
-      // lane-local source of this batch
       if (lane < nb) {
         int rr = r, q = roff + lane;
         while (q >= u_hi[rr] - u_lo[rr]) { q -= u_hi[rr] - u_lo[rr]; ++rr; }
@@ -171,14 +193,32 @@ p2p_kernel(int item_lo, int item_hi, const int4* __restrict__ items,
         for (int f = 0; f < 5; ++f) d[f] = g[f];
       }
       __syncwarp();
-      for (int j = 0; j < nb; ++j) pair_update(acc, zx, zy, ssrc + j * 10);
+      if (active) {
+#pragma unroll 4
+        for (int j = slice; j < nb; j += S) pair_update(acc, zx, zy, ssrc + j * 10);
+      }
       __syncwarp();
       roff += nb;
       while (r < rend && roff >= u_hi[r] - u_lo[r]) { roff -= u_hi[r] - u_lo[r]; ++r; }
     }
-    double2 T = make_double2(0.0, 0.0);
-    if (tvalid) T = acc_to_traction(acc, gc, ec[ti], es[ti]);
-    part[(int64_t)it * 32 + lane] = T;
+    red[w][0][lane] = acc.phi;
+    red[w][1][lane] = acc.psi.x;
+    red[w][2][lane] = acc.psi.y;
+    __syncwarp();
+    if (lane < kTgtGroup) {
+      double2 T = make_double2(0.0, 0.0);
+      if (lane < nt) {
+        P2PAcc tot;
+        for (int s2 = 0; s2 < S; ++s2) {
+          tot.phi += red[w][0][lane + s2 * nt];
+          tot.psi.x += red[w][1][lane + s2 * nt];
+          tot.psi.y += red[w][2][lane + s2 * nt];
+        }
+        T = acc_to_traction(tot, gc, ec[ti], es[ti]);
+      }
+      part[(int64_t)it * kTgtGroup + lane] = T;
+    }
+    __syncwarp();
   }
 }
 
@@ -224,8 +264,8 @@ p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ 
            const double* __restrict__ es, double2* __restrict__ mpole) {
   extern __shared__ double2 p2m_sh[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int stride = (p + 1) | 1;                 // odd row stride in double2 units
-  double2* buf = p2m_sh + (size_t)w * 32 * stride * 2;   // [32][stride] x {alpha, gamma}
+  double2* buf = p2m_sh + (size_t)w * 32 * 17;     // [32 elements][16 (+1 pad)] per chunk
+  const int nchunk = (p + 7) / 8;
   for (int k = blockIdx.x * kP2MWarps + w; k < nleaves; k += gridDim.x * kP2MWarps) {
     const int c = leaves[k];
     const int lev = c_level[c];
@@ -233,8 +273,11 @@ p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ 
     const double is = 1.0 / s;
     const double2 z0 = cg.centre(lev, c_ix[c], c_iy[c]);
     const int e0 = c_start[c], ne = c_count[c];
-    double2 acc_a[2], acc_g[2];
-    acc_a[0] = acc_a[1] = acc_g[0] = acc_g[1] = make_double2(0.0, 0.0);
+    // lane < 16 owns column `lane` of every 8-coefficient chunk:
+    // column j < 8 -> alpha slot 8 ch + j, column j >= 8 -> gamma slot 8 ch + j - 8
+    double2 acc[kMaxP / 8];
+#pragma unroll
+    for (int q = 0; q < kMaxP / 8; ++q) acc[q] = make_double2(0.0, 0.0);
     for (int r0 = 0; r0 < ne; r0 += 32) {
       const int i = e0 + r0 + lane;
       const bool valid = r0 + lane < ne;
@@ -257,45 +300,48 @@ p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ 
       double2 pw1 = make_double2(1.0, 0.0), pw2 = pw1;
       double2 Pm1 = make_double2(0.0, 0.0);   // P_{n-2}
       double2 Pm = make_double2(0.0, 0.0);    // P_{n-1}
-      for (int n = 1; n <= p; ++n) {
-        // P_{n-1}: for n = 1 it is P_0 = 0; then advance powers
-        if (n >= 2) {
-          pw1 = cmul(pw1, z1);
-          pw2 = cmul(pw2, z2);
-          Pm1 = Pm;
-          Pm = csub(pw2, pw1);
-        }
-        const double2 alpha = cmul(B, Pm);
-        double2 gam = cmul(Q, Pm);
-        double2 t = cscale(cmul(A, Pm1), (double)(n - 1));
-        cmac(t, cscale(rr, (double)(n - 2)), Pm);
-        cmac(gam, B, t);
-        buf[lane * stride * 2 + (n - 1)] = alpha;
-        buf[lane * stride * 2 + stride + (n - 1)] = gam;
-      }
-      __syncwarp();
-      // lane = coefficient index: sum the rows in element order
-      for (int cc = 0; cc < 2; ++cc) {
-        const int n = lane + 32 * cc;
-        if (n < p) {
-          double2 sa = acc_a[cc], sg = acc_g[cc];
-          const int rows = min(32, ne - r0);
-          for (int e = 0; e < rows; ++e) {
-            sa = cadd(sa, buf[e * stride * 2 + n]);
-            sg = cadd(sg, buf[e * stride * 2 + stride + n]);
+      const int rows = min(32, ne - r0);
+#pragma unroll
+      for (int ch = 0; ch < kMaxP / 8; ++ch) {
+        if (ch < nchunk) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int n = 8 * ch + j + 1;        // coefficient index (slot n - 1)
+            double2 alpha = make_double2(0.0, 0.0), gam = alpha;
+            if (n <= p) {
+              if (n >= 2) {
+                pw1 = cmul(pw1, z1);
+                pw2 = cmul(pw2, z2);
+                Pm1 = Pm;
+                Pm = csub(pw2, pw1);
+              }
+              alpha = cmul(B, Pm);
+              gam = cmul(Q, Pm);
+              double2 t = cscale(cmul(A, Pm1), (double)(n - 1));
+              cmac(t, cscale(rr, (double)(n - 2)), Pm);
+              cmac(gam, B, t);
+            }
+            buf[lane * 17 + j] = alpha;
+            buf[lane * 17 + 8 + j] = gam;
           }
-          acc_a[cc] = sa;
-          acc_g[cc] = sg;
+          __syncwarp();
+          // column (lane & 15), rows of half (lane >> 4), fixed order
+          const int col = lane & 15, h0 = (lane >> 4) * 16;
+          double2 sum = make_double2(0.0, 0.0);
+          for (int e = h0; e < min(rows, h0 + 16); ++e) sum = cadd(sum, buf[e * 17 + col]);
+          sum.x += __shfl_down_sync(0xffffffffu, sum.x, 16);
+          sum.y += __shfl_down_sync(0xffffffffu, sum.y, 16);
+          acc[ch] = cadd(acc[ch], sum);
+          __syncwarp();
         }
       }
-      __syncwarp();
     }
     double2* out = mpole + (size_t)c * 2 * p;
-    for (int cc = 0; cc < 2; ++cc) {
-      const int n = lane + 32 * cc;
-      if (n < p) {
-        out[n] = acc_a[cc];
-        out[p + n] = acc_g[cc];
+    if (lane < 16) {
+#pragma unroll
+      for (int ch = 0; ch < kMaxP / 8; ++ch) {
+        const int slot = 8 * ch + (lane & 7);
+        if (ch < nchunk && slot < p) out[(lane < 8 ? 0 : p) + slot] = acc[ch];
       }
     }
   }
@@ -305,6 +351,8 @@ p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ 
 // parent P at level lev (non-leaf): sum over children q of
 //   alpha^P_m = sum_n MT_q[n][m] alpha^q_n,  gamma^P_m = sum_n MT_q[n][m] c^q_n,
 //   c_n = gamma_n - (n-1) conj(e)/s_c alpha_{n-1},  e = z_P - z_q.
+// Warp per parent; the four quadrant operators live in shared memory and the
+// children are accumulated in independent chains (ILP), summed in child order.
 constexpr int kM2MWarps = 4;
 
 __global__ void __launch_bounds__(kM2MWarps * 32)
@@ -312,52 +360,55 @@ m2m_kernel(int c0, int c1, const int* __restrict__ c_leaf, const int* __restrict
            const int* __restrict__ c_iy, const int* __restrict__ first_child,
            const int* __restrict__ nchild, int p, const double2* __restrict__ opT,
            double2* __restrict__ mpole) {
-  __shared__ double2 sh[kM2MWarps][2 * (kMaxP + 1)];
+  extern __shared__ double2 m2m_sh[];
+  double2* ops = m2m_sh;                                   // [4][p][p]
+  block_copy(ops, opT, 4 * p * p);
+  __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* sa = sh[w];
-  double2* scv = sh[w] + (kMaxP + 1);
+  double2* xa = m2m_sh + 4 * p * p + (size_t)w * 8 * p;   // [4][p]
+  double2* xc = xa + 4 * p;                                // [4][p]
   for (int c = c0 + blockIdx.x * kM2MWarps + w; c < c1; c += gridDim.x * kM2MWarps) {
     if (c_leaf[c]) continue;
-    double2 acc_a[2], acc_g[2];
-    acc_a[0] = acc_a[1] = acc_g[0] = acc_g[1] = make_double2(0.0, 0.0);
     const int f = first_child[c], nc = nchild[c];
-    for (int q = f; q < f + nc; ++q) {
-      const int quad = (c_ix[q] & 1) + 2 * (c_iy[q] & 1);
-      // conj(e)/s_c with e = z_P - z_q = -((xb-1/2) + i (yb-1/2)) s_c
-      const double2 eb = make_double2(-((c_ix[q] & 1) - 0.5), ((c_iy[q] & 1) - 0.5));
-      const double2* mq = mpole + (size_t)q * 2 * p;
-      for (int n = lane; n < p; n += 32) sa[n] = mq[n];
-      __syncwarp();
-      for (int n = lane; n < p; n += 32) {
-        double2 cv = mq[p + n];
-        if (n >= 1) cmac(cv, cscale(eb, -(double)n), sa[n - 1]);
-        scv[n] = cv;
-      }
-      __syncwarp();
-      const double2* M = opT + (size_t)quad * p * p;
-      for (int cc = 0; cc < 2; ++cc) {
-        const int m = lane + 32 * cc;
-        if (m < p) {
-          double2 a = acc_a[cc], g = acc_g[cc];
-          for (int n = 0; n <= m; ++n) {
-            const double2 t = M[(size_t)n * p + m];
-            cmac(a, t, sa[n]);
-            cmac(g, t, scv[n]);
-          }
-          acc_a[cc] = a;
-          acc_g[cc] = g;
+    int quad[4];
+    for (int i = 0; i < 4; ++i) {
+      quad[i] = 0;
+      if (i < nc) {
+        const int q = f + i;
+        const int xb = c_ix[q] & 1, yb = c_iy[q] & 1;
+        quad[i] = xb + 2 * yb;
+        // conj(e)/s_c with e = z_P - z_q = -((xb-1/2) + i (yb-1/2)) s_c
+        const double2 eb = make_double2(-(xb - 0.5), (yb - 0.5));
+        const double2* mq = mpole + (size_t)q * 2 * p;
+        for (int n = lane; n < p; n += 32) {
+          xa[i * p + n] = mq[n];
+          double2 cv = mq[p + n];
+          if (n >= 1) cmac(cv, cscale(eb, -(double)n), mq[n - 1]);
+          xc[i * p + n] = cv;
         }
       }
-      __syncwarp();
     }
+    __syncwarp();
     double2* out = mpole + (size_t)c * 2 * p;
-    for (int cc = 0; cc < 2; ++cc) {
-      const int m = lane + 32 * cc;
-      if (m < p) {
-        out[m] = acc_a[cc];
-        out[p + m] = acc_g[cc];
+    for (int m = lane; m < p; m += 32) {
+      double2 a[4], g[4];
+      for (int i = 0; i < 4; ++i) a[i] = g[i] = make_double2(0.0, 0.0);
+      for (int n = 0; n <= m; ++n) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i < nc) {
+            const double2 t = ops[(quad[i] * p + n) * p + m];
+            cmac(a[i], t, xa[i * p + n]);
+            cmac(g[i], t, xc[i * p + n]);
+          }
+        }
       }
+      double2 sa = a[0], sg = g[0];
+      for (int i = 1; i < 4; ++i) { sa = cadd(sa, a[i]); sg = cadd(sg, g[i]); }
+      out[m] = sa;
+      out[p + m] = sg;
     }
+    __syncwarp();
   }
 }
 
@@ -366,56 +417,96 @@ m2m_kernel(int c0, int c1, const int* __restrict__ c_leaf, const int* __restrict
 // h_k = (k-1)! delta^-k (table per offset class),
 //   l_m = (-1)^m/m! sum_{n=1..p} [alpha_n/(n-1)!] h_{n+m}
 //   g_m = (-1)^m/m! sum_{n=1..p+1} [c_n/(n-1)!] h_{n+m},  c_n = gamma_n - (n-1) conj(delta) alpha_{n-1}
+// Rotated form: with delta = rho e^{i theta},
+//   delta^-(n+m) = R_{n+m} e^{-i n theta} e^{-i m theta} / (n+m-1)!,
+//   R_k = (k-1)! rho^-k (real), so each pair costs two real-Hankel sums over
+//   rotated inputs plus one output rotation.  Tables per offset class:
+//   rot[o][k] = e^{-i k theta}, R[o][k]; the next source's expansion is
+//   prefetched into registers while the current one is applied.
 constexpr int kM2LWarps = 8;
 
 __global__ void __launch_bounds__(kM2LWarps * 32)
 m2l_kernel(int c0, int c1, const int* __restrict__ v_off, const int* __restrict__ v_idx,
-           const unsigned char* __restrict__ v_cls, int p, const double2* __restrict__ htab,
-           const double* __restrict__ invfact, const double2* __restrict__ mpole,
-           double2* __restrict__ local) {
+           const unsigned char* __restrict__ v_cls, int p, const double* __restrict__ rtab,
+           const double2* __restrict__ rottab, const double* __restrict__ invfact,
+           const double2* __restrict__ mpole, double2* __restrict__ local) {
   extern __shared__ double2 m2l_sh[];
-  const int hs = 2 * p + 2;                          // entries per class
-  double2* sh_h = m2l_sh;                            // [49][hs]
-  double2* wbuf = m2l_sh + kNOffsets * hs;           // per warp [2][p+2]
-  for (int f = threadIdx.x; f < kNOffsets * hs; f += blockDim.x) sh_h[f] = htab[f];
+  const int rs = 2 * p + 2;                          // R entries per class
+  const int qs = p + 2;                              // rotation entries per class
+  double2* sh_rot = m2l_sh;                          // [49][qs]
+  double* sh_R = reinterpret_cast<double*>(m2l_sh + kNOffsets * qs);   // [49][rs]
+  double2* wbuf = m2l_sh + kNOffsets * qs + (kNOffsets * rs + 1) / 2;
+  block_copy(sh_rot, rottab, kNOffsets * qs);
+  block_copy(sh_R, rtab, kNOffsets * rs);
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* sa = wbuf + (size_t)w * 2 * (p + 2);
-  double2* scv = sa + (p + 2);
+  double2* sa = wbuf + (size_t)w * (3 * p + 2);      // raw alpha [p]
+  double2* ap = sa + p;                               // rotated/scaled alpha [p]
+  double2* cp = ap + p;                               // rotated/scaled c [p+1]
   for (int c = c0 + blockIdx.x * kM2LWarps + w; c < c1; c += gridDim.x * kM2LWarps) {
     double2 al[2], ag[2];
     al[0] = al[1] = ag[0] = ag[1] = make_double2(0.0, 0.0);
     const int vb = v_off[c], ve = v_off[c + 1];
+    double2 na[2], ng[2];
+    if (vb < ve) {
+      const double2* ma = mpole + (size_t)v_idx[vb] * 2 * p;
+      for (int cc = 0; cc < 2; ++cc) {
+        const int n = lane + 32 * cc;
+        na[cc] = n < p ? ma[n] : make_double2(0.0, 0.0);
+        ng[cc] = n < p ? ma[p + n] : make_double2(0.0, 0.0);
+      }
+    }
     for (int v = vb; v < ve; ++v) {
-      const int a = v_idx[v];
       const int cls = v_cls[v];
+      const double2 xa0 = na[0], xa1 = na[1], xg0 = ng[0], xg1 = ng[1];
+      if (v + 1 < ve) {   // prefetch the next source
+        const double2* ma = mpole + (size_t)v_idx[v + 1] * 2 * p;
+        for (int cc = 0; cc < 2; ++cc) {
+          const int n = lane + 32 * cc;
+          if (n < p) {
+            na[cc] = ma[n];
+            ng[cc] = ma[p + n];
+          }
+        }
+      }
       const int dxs = cls % 7 - 3, dys = cls / 7 - 3;   // source - target in cells
-      const double2 dconj = make_double2(-(double)dxs, (double)dys);  // conj(delta), delta = -(dx + i dy)
-      const double2* ma = mpole + (size_t)a * 2 * p;
-      for (int n = lane; n < p; n += 32) sa[n] = ma[n];
+      const double2 dconj = make_double2(-(double)dxs, (double)dys);  // conj(delta)
+      const double2* rot = sh_rot + cls * qs;
+      const double* R = sh_R + cls * rs;
+      if (lane < p) sa[lane] = xa0;
+      if (lane + 32 < p) sa[lane + 32] = xa1;
       __syncwarp();
-      for (int n = lane; n <= p; n += 32) {   // slot n <-> c_{n+1}
-        double2 cv = (n < p) ? ma[p + n] : make_double2(0.0, 0.0);
-        if (n >= 1) cmac(cv, cscale(dconj, -(double)n), sa[n - 1]);
-        scv[n] = cscale(cv, invfact[n]);
+      for (int cc = 0; cc < 2; ++cc) {   // slot n <-> coefficient n + 1
+        const int n = lane + 32 * cc;
+        if (n <= p) {
+          double2 cv = (n < p) ? (cc ? xg1 : xg0) : make_double2(0.0, 0.0);
+          if (n >= 1) cmac(cv, cscale(dconj, -(double)n), sa[n - 1]);
+          const double2 r = cscale(rot[n + 1], invfact[n]);
+          cp[n] = cmul(cv, r);
+          if (n < p) ap[n] = cmul(cc ? xa1 : xa0, r);
+        }
       }
       __syncwarp();
-      for (int n = lane; n < p; n += 32) sa[n] = cscale(sa[n], invfact[n]);
-      __syncwarp();
-      const double2* h = sh_h + cls * hs;
       for (int cc = 0; cc < 2; ++cc) {
         const int m = lane + 32 * cc;
         if (m < p) {
-          double2 l = al[cc], g = ag[cc];
-          // h index k = n + m with n = slot + 1
+          double2 sl = make_double2(0.0, 0.0), sg = sl;
+          const double* Rm = R + 1 + m;
+#pragma unroll 4
           for (int n = 0; n < p; ++n) {
-            const double2 hk = h[n + 1 + m];
-            cmac(l, sa[n], hk);
-            cmac(g, scv[n], hk);
+            const double rk = Rm[n];
+            const double2 a = ap[n], g = cp[n];
+            sl.x = fma(a.x, rk, sl.x);
+            sl.y = fma(a.y, rk, sl.y);
+            sg.x = fma(g.x, rk, sg.x);
+            sg.y = fma(g.y, rk, sg.y);
           }
-          cmac(g, scv[p], h[p + 1 + m]);
-          al[cc] = l;
-          ag[cc] = g;
+          const double rk = Rm[p];
+          sg.x = fma(cp[p].x, rk, sg.x);
+          sg.y = fma(cp[p].y, rk, sg.y);
+          const double2 ro = rot[m];
+          cmac(al[cc], sl, ro);
+          cmac(ag[cc], sg, ro);
         }
       }
       __syncwarp();
@@ -435,41 +526,66 @@ m2l_kernel(int c0, int c1, const int* __restrict__ v_off, const int* __restrict_
 // ------------------------------------------------------------ L2L (a8)
 // child c += shift of parent P:  g_k = gamma_k + (k+1) conj(eps) lambda_{k+1},
 //   lambda^c_k += sum_m LT_q[m][k] lambda^P_m,  gamma^c_k += sum_m LT_q[m][k] g_m
+// Warp per parent P (non-leaf, level lev-1): shifts P's local expansion to
+// each of its children (independent chains), operators in shared memory.
 constexpr int kL2LWarps = 4;
 
 __global__ void __launch_bounds__(kL2LWarps * 32)
-l2l_kernel(int c0, int c1, const int* __restrict__ c_parent, const int* __restrict__ c_ix,
-           const int* __restrict__ c_iy, int p, const double2* __restrict__ opT,
+l2l_kernel(int c0, int c1, const int* __restrict__ c_leaf, const int* __restrict__ c_ix,
+           const int* __restrict__ c_iy, const int* __restrict__ first_child,
+           const int* __restrict__ nchild, int p, const double2* __restrict__ opT,
            double2* __restrict__ local) {
-  __shared__ double2 sh[kL2LWarps][2 * (kMaxP + 1)];
+  extern __shared__ double2 l2l_sh[];
+  double2* ops = l2l_sh;                                     // [4][p][p]
+  block_copy(ops, opT, 4 * p * p);
+  __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* sl = sh[w];
-  double2* sg = sh[w] + (kMaxP + 1);
-  for (int c = c0 + blockIdx.x * kL2LWarps + w; c < c1; c += gridDim.x * kL2LWarps) {
-    const int P = c_parent[c];
-    const int xb = c_ix[c] & 1, yb = c_iy[c] & 1;
-    const int quad = xb + 2 * yb;
-    const double2 epsb = make_double2(0.5 * (xb - 0.5), -0.5 * (yb - 0.5));  // conj(eps)
+  double2* sl = l2l_sh + 4 * p * p + (size_t)w * 2 * p;
+  double2* sgv = sl + p;
+  for (int P = c0 + blockIdx.x * kL2LWarps + w; P < c1; P += gridDim.x * kL2LWarps) {
+    if (c_leaf[P]) continue;
     const double2* lp = local + (size_t)P * 2 * p;
-    for (int m = lane; m < p; m += 32) sl[m] = lp[m];
-    __syncwarp();
     for (int m = lane; m < p; m += 32) {
-      double2 g = lp[p + m];
-      if (m + 1 < p) cmac(g, cscale(epsb, (double)(m + 1)), sl[m + 1]);
-      sg[m] = g;
+      sl[m] = lp[m];
+      sgv[m] = lp[p + m];
     }
     __syncwarp();
-    const double2* L = opT + (size_t)quad * p * p;
-    double2* out = local + (size_t)c * 2 * p;
+    const int f = first_child[P], nc = nchild[P];
+    int quad[4];
+    double2 epsb[4];
+    for (int i = 0; i < 4; ++i) {
+      const int q = f + min(i, nc - 1);
+      const int xb = c_ix[q] & 1, yb = c_iy[q] & 1;
+      quad[i] = xb + 2 * yb;
+      epsb[i] = make_double2(0.5 * (xb - 0.5), -0.5 * (yb - 0.5));  // conj(eps)
+    }
     for (int k = lane; k < p; k += 32) {
-      double2 l = out[k], g = out[p + k];
+      double2 l[4], g[4];
+      for (int i = 0; i < 4; ++i) l[i] = g[i] = make_double2(0.0, 0.0);
       for (int m = k; m < p; ++m) {
-        const double2 t = L[(size_t)m * p + k];
-        cmac(l, t, sl[m]);
-        cmac(g, t, sg[m]);
+        const double2 lm = sl[m];
+        const double2 gm = sgv[m];
+        const double2 lm1 = (m + 1 < p) ? sl[m + 1] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i < nc) {
+            // g_m = gamma_m + (m+1) conj(eps) lambda_{m+1}
+            double2 gv = gm;
+            cmac(gv, cscale(epsb[i], (double)(m + 1)), lm1);
+            const double2 t = ops[(quad[i] * p + m) * p + k];
+            cmac(l[i], t, lm);
+            cmac(g[i], t, gv);
+          }
+        }
       }
-      out[k] = l;
-      out[p + k] = g;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i < nc) {
+          double2* out = local + (size_t)(f + i) * 2 * p;
+          out[k] = cadd(out[k], l[i]);
+          out[p + k] = cadd(out[p + k], g[i]);
+        }
+      }
     }
     __syncwarp();
   }
@@ -499,7 +615,7 @@ __global__ void finalize_kernel(int64_t e_lo, int64_t e_hi, int ncomp,
   const int nch = (item_off[k + 1] - i0) / ngroups;
   const int g = slot / kTgtGroup, ln = slot % kTgtGroup;
   double2 T = make_double2(0.0, 0.0);
-  for (int h = 0; h < nch; ++h) T = cadd(T, part[(int64_t)(i0 + g * nch + h) * 32 + ln]);
+  for (int h = 0; h < nch; ++h) T = cadd(T, part[(int64_t)(i0 + g * nch + h) * kTgtGroup + ln]);
   const int lev = c_level[c];
   if (lev >= 2) {
     const double s = cg.side(lev);
@@ -564,7 +680,7 @@ int ensure_workspace(ddm_ctx_s* ctx, ddm_tree_s* t) {
     if ((rc = dalloc(ctx, &t->mpole, (size_t)t->ncells * 2 * t->p))) return rc;
     if ((rc = dalloc(ctx, &t->local, (size_t)t->ncells * 2 * t->p))) return rc;
     if ((rc = dalloc(ctx, &t->src, (size_t)t->n * 10))) return rc;
-    if ((rc = dalloc(ctx, &t->part, (size_t)t->nitems * 32))) return rc;
+    if ((rc = dalloc(ctx, &t->part, (size_t)t->nitems * kTgtGroup))) return rc;
     if ((rc = dalloc(ctx, &t->d_sorted, (size_t)t->n * 3))) return rc;
     if ((rc = dalloc(ctx, &t->y_sorted, (size_t)t->n * 3))) return rc;
     if ((rc = dalloc(ctx, &t->part_direct, (size_t)t->n * 2))) return rc;
@@ -615,22 +731,29 @@ int fmm_init_operators(ddm_tree_s* t, cudaStream_t s) {
         l2l[(size_t)q * p * p + (size_t)m * p + k] = v;
       }
   }
+  // M2L tables per offset class: rot[o][k] = e^{-i k theta} (k = 0..p+1) and
+  // R[o][k] = (k-1)! rho^-k (k = 1..2p+1), delta = -(dx + i dy) = rho e^{i theta}
+  std::vector<double> R((size_t)kNOffsets * (2 * p + 2), 0.0);
+  V rot((size_t)kNOffsets * (p + 2), make_double2(0.0, 0.0));
   for (int o = 0; o < kNOffsets; ++o) {
     const int dx = o % 7 - 3, dy = o / 7 - 3;
-    for (int k = 0; k < 2 * p + 2; ++k) h[(size_t)o * (2 * p + 2) + k] = make_double2(0.0, 0.0);
     if (std::max(std::abs(dx), std::abs(dy)) < 2) continue;
-    // 1/delta = conj(delta)/|delta|^2, delta = -(dx + i dy)
-    const double d2 = (double)dx * dx + (double)dy * dy;
-    const double ir = -dx / d2, ii = dy / d2;
-    double fact = 1.0;  // (k-1)!
+    const double rho = std::sqrt((double)dx * dx + (double)dy * dy);
+    const double er = -dx / rho, ei = dy / rho;   // e^{-i theta} = conj(delta)/rho
     double pr = 1.0, pi = 0.0;
-    for (int k = 1; k <= 2 * p + 1; ++k) {
-      const double nr = pr * ir - pi * ii, ni = pr * ii + pi * ir;
+    for (int k = 0; k < p + 2; ++k) {
+      rot[(size_t)o * (p + 2) + k] = make_double2(pr, pi);
+      const double nr = pr * er - pi * ei, ni = pr * ei + pi * er;
       pr = nr; pi = ni;
+    }
+    double fact = 1.0, rp = 1.0;
+    for (int k = 1; k <= 2 * p + 1; ++k) {
       if (k >= 2) fact *= (k - 1);
-      h[(size_t)o * (2 * p + 2) + k] = make_double2(fact * pr, fact * pi);
+      rp /= rho;
+      R[(size_t)o * (2 * p + 2) + k] = fact * rp;
     }
   }
+  h = rot;
   std::vector<double> inv(2 * p + 2);
   double f = 1.0;
   for (int k = 0; k < 2 * p + 2; ++k) {
@@ -639,8 +762,11 @@ int fmm_init_operators(ddm_tree_s* t, cudaStream_t s) {
   }
   int rc;
   if ((rc = dalloc(ctx, &t->op_m2m, m2m.size())) || (rc = dalloc(ctx, &t->op_l2l, l2l.size())) ||
-      (rc = dalloc(ctx, &t->op_h, h.size())) || (rc = dalloc(ctx, &t->invfact, inv.size())))
+      (rc = dalloc(ctx, &t->op_h, h.size())) || (rc = dalloc(ctx, &t->invfact, inv.size())) ||
+      (rc = dalloc(ctx, &t->op_R, R.size())))
     return rc;
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->op_R, R.data(), R.size() * sizeof(double),
+                                cudaMemcpyHostToDevice, s));
   DDM_CUDA(ctx, cudaMemcpyAsync(t->op_m2m, m2m.data(), m2m.size() * sizeof(double2),
                                 cudaMemcpyHostToDevice, s));
   DDM_CUDA(ctx, cudaMemcpyAsync(t->op_l2l, l2l.data(), l2l.size() * sizeof(double2),
@@ -690,8 +816,7 @@ int fmm_matvec_elastic(ddm_ctx_s* ctx, ddm_tree_s* t, double G, double nu, const
   // ---- upward pass: P2M on all leaves, M2M finest -> level 2
   stage_begin(ctx, DDM_ST_P2M, s);
   {
-    const int stride = (p + 1) | 1;
-    const size_t shm = (size_t)kP2MWarps * 32 * stride * 2 * sizeof(double2);
+    const size_t shm = (size_t)kP2MWarps * 32 * 17 * sizeof(double2);
     if (shm > 48 * 1024)
       DDM_CUDA(ctx, cudaFuncSetAttribute(p2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)shm));
@@ -704,13 +829,19 @@ int fmm_matvec_elastic(ddm_ctx_s* ctx, ddm_tree_s* t, double G, double nu, const
   }
   stage_end(ctx, DDM_ST_P2M, s);
   stage_begin(ctx, DDM_ST_M2M, s);
-  for (int lev = t->nlevels - 2; lev >= 2; --lev) {
-    const int c0 = t->level_off[lev], c1 = t->level_off[lev + 1];
-    const int nb = std::min(nblk(c1 - c0, kM2MWarps), 148u * 8);
-    m2m_kernel<<<nb, kM2MWarps * 32, 0, s>>>(c0, c1, t->c_leaf, t->c_ix, t->c_iy,
-                                             t->c_first_child, t->c_nchild, p, t->op_m2m,
-                                             t->mpole);
-    DDM_CUDA(ctx, cudaGetLastError());
+  {
+    const size_t shm = ((size_t)4 * p * p + (size_t)kM2MWarps * 8 * p) * sizeof(double2);
+    if (shm > 48 * 1024)
+      DDM_CUDA(ctx, cudaFuncSetAttribute(m2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)shm));
+    for (int lev = t->nlevels - 2; lev >= 2; --lev) {
+      const int c0 = t->level_off[lev], c1 = t->level_off[lev + 1];
+      const int nb = std::min(nblk(c1 - c0, kM2MWarps), 148u * 4);
+      m2m_kernel<<<nb, kM2MWarps * 32, shm, s>>>(c0, c1, t->c_leaf, t->c_ix, t->c_iy,
+                                                 t->c_first_child, t->c_nchild, p, t->op_m2m,
+                                                 t->mpole);
+      DDM_CUDA(ctx, cudaGetLastError());
+    }
   }
   stage_end(ctx, DDM_ST_M2M, s);
 
@@ -718,24 +849,32 @@ int fmm_matvec_elastic(ddm_ctx_s* ctx, ddm_tree_s* t, double G, double nu, const
   stage_begin(ctx, DDM_ST_M2L, s);
   if (t->nlevels > 2) {
     const int c0 = t->level_off[2], c1 = t->ncells;
-    const size_t shm = ((size_t)kNOffsets * (2 * p + 2) + (size_t)kM2LWarps * 2 * (p + 2)) *
-                       sizeof(double2);
+    const size_t shm = ((size_t)kNOffsets * (p + 2) + ((size_t)kNOffsets * (2 * p + 2) + 1) / 2 +
+                        (size_t)kM2LWarps * (3 * p + 2)) * sizeof(double2);
     if (shm > 48 * 1024)
       DDM_CUDA(ctx, cudaFuncSetAttribute(m2l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)shm));
-    const int nb = std::min(nblk(c1 - c0, kM2LWarps), 148u * 2);
+    const int nb = std::min(nblk(c1 - c0, kM2LWarps), 148u * 4);
     m2l_kernel<<<nb, kM2LWarps * 32, shm, s>>>(c0, c1, t->v_off, t->v_idx, t->v_cls, p,
-                                               t->op_h, t->invfact, t->mpole, t->local);
+                                               t->op_R, t->op_h, t->invfact, t->mpole, t->local);
     DDM_CUDA(ctx, cudaGetLastError());
   }
   stage_end(ctx, DDM_ST_M2L, s);
   stage_begin(ctx, DDM_ST_L2L, s);
-  for (int lev = 3; lev < t->nlevels; ++lev) {
-    const int c0 = t->level_off[lev], c1 = t->level_off[lev + 1];
-    const int nb = std::min(nblk(c1 - c0, kL2LWarps), 148u * 8);
-    l2l_kernel<<<nb, kL2LWarps * 32, 0, s>>>(c0, c1, t->c_parent, t->c_ix, t->c_iy, p,
-                                             t->op_l2l, t->local);
-    DDM_CUDA(ctx, cudaGetLastError());
+  {
+    const size_t shm = ((size_t)4 * p * p + (size_t)kL2LWarps * 2 * p) * sizeof(double2);
+    if (shm > 48 * 1024)
+      DDM_CUDA(ctx, cudaFuncSetAttribute(l2l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)shm));
+    // parents at level lev (>= 2) push to their children at lev + 1
+    for (int lev = 2; lev + 1 < t->nlevels; ++lev) {
+      const int c0 = t->level_off[lev], c1 = t->level_off[lev + 1];
+      const int nb = std::min(nblk(c1 - c0, kL2LWarps), 148u * 4);
+      l2l_kernel<<<nb, kL2LWarps * 32, shm, s>>>(c0, c1, t->c_leaf, t->c_ix, t->c_iy,
+                                                 t->c_first_child, t->c_nchild, p, t->op_l2l,
+                                                 t->local);
+      DDM_CUDA(ctx, cudaGetLastError());
+    }
   }
   stage_end(ctx, DDM_ST_L2L, s);
 
