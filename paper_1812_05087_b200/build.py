@@ -13,7 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libddm.so")
-SOURCES = ["api.cu", "scan.cu", "tree.cu", "fmm.cu", "gmres.cu"]
+SOURCES = ["api.cu", "scan.cu", "tree.cu", "fmm.cu", "expansions.cu", "p2p.cu", "gmres.cu"]
+HEADERS = ["ddm_internal.cuh", "kcommon.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -37,8 +38,8 @@ def _nccl_dirs():
 
 def build(verbose: bool = False, force: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "ddm_internal.cuh"), os.path.join(ROOT, "include", "ddm.h"),
-                   __file__]
+    deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [
+        os.path.join(ROOT, "include", "ddm.h"), __file__]
     if (not force and os.path.exists(LIB)
             and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps)):
         return LIB

@@ -1,0 +1,72 @@
+// Device helpers shared by the FMM kernels (complex fp64 arithmetic, fast
+// reciprocal, block copies, cell geometry) and the launcher declarations.
+#pragma once
+#include "ddm_internal.cuh"
+
+namespace ddm {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// acc += a * b
+__device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
+// 1/x for x > 0 normal: MUFU.RCP64H seed + cubic Newton refinement (error ~e^3)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
+// Block-wide global -> shared copy with 8 loads in flight per thread.
+template <class T>
+__device__ __forceinline__ void block_copy(T* __restrict__ dst, const T* __restrict__ src, int n) {
+  const int step = blockDim.x;
+  int f = threadIdx.x;
+  for (; f + 7 * step < n; f += 8 * step) {
+    T v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = src[f + k * step];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dst[f + k * step] = v[k];
+  }
+  for (; f < n; f += step) dst[f] = src[f];
+}
+
+struct CellGeom {
+  double x_min, y_min, W;
+  __device__ __forceinline__ double side(int lev) const { return ldexp(W, -lev); }
+  __device__ __forceinline__ double2 centre(int lev, int ix, int iy) const {
+    const double s = ldexp(W, -lev);
+    return make_double2(x_min + (ix + 0.5) * s, y_min + (iy + 0.5) * s);
+  }
+};
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// ---- launchers (expansions.cu): upward / downward passes
+int launch_p2m(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
+               cudaStream_t s);
+int launch_m2m_level(ddm_ctx_s* ctx, ddm_tree_s* t, int lev, cudaStream_t s);
+int launch_m2l(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
+int launch_l2l_level(ddm_ctx_s* ctx, ddm_tree_s* t, int lev, cudaStream_t s);
+int launch_finalize(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, int ncomp, double gc,
+                    double* y_user, double* y_sorted, cudaStream_t s);
+
+// ---- launchers (p2p.cu): near field
+int launch_prep_sources(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D,
+                        int ncomp, cudaStream_t s);
+int launch_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, double gc,
+               cudaStream_t s);
+int launch_direct(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, int ncomp, double gc,
+                  double* y_user, double* y_sorted, cudaStream_t s);
+
+}  // namespace ddm
