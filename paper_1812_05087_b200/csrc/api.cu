@@ -220,6 +220,19 @@ int ddm_ctx_create(int device, const void* nccl_uid, int rank, int world, ddm_ct
     *out = ctx;
     return rc;
   }
+  {
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    if ((e = cudaStreamCreateWithPriority(&ctx->s_hi, cudaStreamNonBlocking, hi_prio)) != cudaSuccess ||
+        (e = cudaStreamCreateWithPriority(&ctx->s_lo, cudaStreamNonBlocking, lo_prio)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_far, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_near, cudaEventDisableTiming)) != cudaSuccess) {
+      int rc = cuda_error(ctx, e, "stream/event creation");
+      *out = ctx;
+      return rc;
+    }
+  }
   if (world > 1) {
 #ifdef DDM_WITH_NCCL
     if (!nccl_uid) {
@@ -249,6 +262,10 @@ void ddm_ctx_destroy(ddm_ctx_t ctx) {
 #endif
   if (ctx->stage.created)
     for (auto& ev : ctx->stage.ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : {ctx->ev_fork, ctx->ev_far, ctx->ev_near})
+    if (ev) cudaEventDestroy(ev);
+  for (cudaStream_t st : {ctx->s_hi, ctx->s_lo})
+    if (st) cudaStreamDestroy(st);
   if (ctx->d_scalar) cudaFree(ctx->d_scalar);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   delete ctx;

@@ -43,6 +43,10 @@ struct ddm_ctx_s {
 #ifdef DDM_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
+  // fork/join streams: the far-field chain (latency bound) runs on s_hi, the
+  // near field (P2P, throughput bound) concurrently on s_lo
+  cudaStream_t s_hi = nullptr, s_lo = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_far = nullptr, ev_near = nullptr;
   // persistent scratch
   double* d_scalar = nullptr;     // small device scratch (reductions)
   double* h_pinned = nullptr;     // small pinned host scratch

@@ -149,29 +149,42 @@ int fmm_matvec_elastic(ddm_ctx_s* ctx, ddm_tree_s* t, double G, double nu, const
     return rc;
   }
 
-  // upward pass: P2M on all leaves, M2M finest -> level 2 (replicated on all ranks)
-  stage_begin(ctx, DDM_ST_P2M, s);
-  if ((rc = launch_p2m(ctx, t, perm_in, D, ncomp, s))) return rc;
-  stage_end(ctx, DDM_ST_P2M, s);
-  stage_begin(ctx, DDM_ST_M2M, s);
-  for (int lev = t->nlevels - 2; lev >= 2; --lev)
-    if ((rc = launch_m2m_level(ctx, t, lev, s))) return rc;
-  stage_end(ctx, DDM_ST_M2M, s);
-
-  // downward pass: M2L at every level >= 2 (one launch), L2L top-down
-  stage_begin(ctx, DDM_ST_M2L, s);
-  if ((rc = launch_m2l(ctx, t, s))) return rc;
-  stage_end(ctx, DDM_ST_M2L, s);
-  stage_begin(ctx, DDM_ST_L2L, s);
-  for (int lev = 2; lev + 1 < t->nlevels; ++lev)
-    if ((rc = launch_l2l_level(ctx, t, lev, s))) return rc;
-  stage_end(ctx, DDM_ST_L2L, s);
+  // fork: the near field (P2P, throughput bound) runs on the low-priority
+  // stream concurrently with the latency-bound far-field chain on the
+  // high-priority stream; both only read `src` / D and write disjoint buffers.
+  DDM_CUDA(ctx, cudaEventRecord(ctx->ev_fork, s));
+  cudaStream_t sf = ctx->s_hi, sn = ctx->s_lo;
+  DDM_CUDA(ctx, cudaStreamWaitEvent(sf, ctx->ev_fork, 0));
+  DDM_CUDA(ctx, cudaStreamWaitEvent(sn, ctx->ev_fork, 0));
 
   // near field: P2P work items of the owned leaves
-  stage_begin(ctx, DDM_ST_P2P, s);
-  if ((rc = launch_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, gc, s))) return rc;
-  stage_end(ctx, DDM_ST_P2P, s);
+  stage_begin(ctx, DDM_ST_P2P, sn);
+  if ((rc = launch_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, gc, sn))) return rc;
+  stage_end(ctx, DDM_ST_P2P, sn);
+  DDM_CUDA(ctx, cudaEventRecord(ctx->ev_near, sn));
 
+  // upward pass: P2M on all leaves, M2M finest -> level 2 (replicated on all ranks)
+  stage_begin(ctx, DDM_ST_P2M, sf);
+  if ((rc = launch_p2m(ctx, t, perm_in, D, ncomp, sf))) return rc;
+  stage_end(ctx, DDM_ST_P2M, sf);
+  stage_begin(ctx, DDM_ST_M2M, sf);
+  for (int lev = t->nlevels - 2; lev >= 2; --lev)
+    if ((rc = launch_m2m_level(ctx, t, lev, sf))) return rc;
+  stage_end(ctx, DDM_ST_M2M, sf);
+
+  // downward pass: M2L at every level >= 2 (one launch), L2L top-down
+  stage_begin(ctx, DDM_ST_M2L, sf);
+  if ((rc = launch_m2l(ctx, t, sf))) return rc;
+  stage_end(ctx, DDM_ST_M2L, sf);
+  stage_begin(ctx, DDM_ST_L2L, sf);
+  for (int lev = 2; lev + 1 < t->nlevels; ++lev)
+    if ((rc = launch_l2l_level(ctx, t, lev, sf))) return rc;
+  stage_end(ctx, DDM_ST_L2L, sf);
+  DDM_CUDA(ctx, cudaEventRecord(ctx->ev_far, sf));
+
+  // join
+  DDM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_near, 0));
+  DDM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_far, 0));
   stage_begin(ctx, DDM_ST_FINAL, s);
   rc = launch_finalize(ctx, t, lo, hi, ncomp, gc, y_user, y_sorted, s);
   stage_end(ctx, DDM_ST_FINAL, s);

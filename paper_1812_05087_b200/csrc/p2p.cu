@@ -201,7 +201,9 @@ int launch_prep_sources(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const
 int launch_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, double gc,
                cudaStream_t s) {
   if (item_hi <= item_lo) return DDM_OK;
-  const int nb = std::min(nblk(item_hi - item_lo, kP2PWarps), 148u * 16);
+  // short-lived blocks (4 items each): slots free up continuously, so the
+  // high-priority far-field kernels interleave with the near field
+  const unsigned nb = nblk(item_hi - item_lo, kP2PWarps);
   p2p_kernel<<<nb, kP2PWarps * 32, 0, s>>>(item_lo, item_hi, t->items, t->u_off, t->u_lo,
                                            t->u_hi, t->leaves, t->c_start, t->c_count, t->src,
                                            t->ex, t->ey, t->ec, t->es, gc, t->part);
