@@ -8,7 +8,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libddm.so")
+# DDM_LIB: alternative build of the same library (tuning experiments only)
+LIB_PATH = os.environ.get("DDM_LIB") or os.path.join(_HERE, "libddm.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

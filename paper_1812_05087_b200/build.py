@@ -36,20 +36,24 @@ def _nccl_dirs():
     return None, None
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile every .cu for sm_100a and link libddm.so.  `defines`/`out` are
+    for tuning experiments (variant builds of the same sources)."""
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [
         os.path.join(ROOT, "include", "ddm.h"), __file__]
-    if (not force and os.path.exists(LIB)
-            and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps)):
-        return LIB
+    target = out or LIB
+    if (not force and not defines and os.path.exists(target)
+            and os.path.getmtime(target) >= max(os.path.getmtime(d) for d in deps)):
+        return target
     nvcc = _nvcc()
     inc, lib = _nccl_dirs()
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
+    common += [f"-D{d}" for d in defines]
     if inc:
         common += ["-DDDM_WITH_NCCL", "-I", inc]
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build") if not out else out + ".objs"
     os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):
@@ -64,14 +68,14 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
         objs = list(ex.map(compile_one, srcs))
-    link = [nvcc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs]
+    link = [nvcc, *ARCH, "-shared", "-o", target + ".tmp", *objs]
     if lib:
         link += ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

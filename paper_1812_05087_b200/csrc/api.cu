@@ -2,6 +2,7 @@
 // history, GMRES, loads, SIF, multi-GPU exchange.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -221,6 +222,8 @@ int ddm_ctx_create(int device, const void* nccl_uid, int rank, int world, ddm_ct
     return rc;
   }
   {
+    const char* ser = getenv("DDM_SERIAL");
+    ctx->serial = ser && ser[0] == '1';
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
     if ((e = cudaStreamCreateWithPriority(&ctx->s_hi, cudaStreamNonBlocking, hi_prio)) != cudaSuccess ||

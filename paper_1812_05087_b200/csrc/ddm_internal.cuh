@@ -46,6 +46,7 @@ struct ddm_ctx_s {
   // fork/join streams: the far-field chain (latency bound) runs on s_hi, the
   // near field (P2P, throughput bound) concurrently on s_lo
   cudaStream_t s_hi = nullptr, s_lo = nullptr;
+  bool serial = false;            // DDM_SERIAL=1: everything on the caller's stream (profiling)
   cudaEvent_t ev_fork = nullptr, ev_far = nullptr, ev_near = nullptr;
   // persistent scratch
   double* d_scalar = nullptr;     // small device scratch (reductions)
@@ -106,6 +107,13 @@ struct ddm_tree_s {
   int* m2l_cells = nullptr;       // (reserved) cells whose subtree meets the owned range
   int n_m2l_cells = 0;
   int item_lo_owned = 0, item_hi_owned = 0;   // P2P items of owned leaves
+  // persistent-pass scheduling (expansions.cu)
+  int* up_list = nullptr;         // non-leaf cells of level >= 2, deepest level first
+  int n_up = 0;
+  int* ready_up = nullptr;        // [ncells] multipole-ready flags (epoch tagged)
+  int* ready_down = nullptr;      // [ncells] local-final flags (epoch tagged)
+  int* tickets = nullptr;         // [2] work counters (upward, downward)
+  int epoch = 0;
 
   // FMM operators (device): M2M[4][p][p] complex, L2L[4][p][p] complex,
   // Hankel table h[49][2p+2] complex, inverse factorials

@@ -9,6 +9,14 @@
 // and likewise for Psi~ = Psi + conj(z0) Phi'.  The factor i G C,
 // C = 1/(4 pi (1 - nu)), is applied once, at evaluation.
 //
+// Scheduling: each pass is ONE persistent launch.  Warps take
+// cells in topological order from an atomic ticket counter (upward: all leaves
+// (P2M), then non-leaf cells deepest level first (M2M); downward: cells of
+// level >= 2 top-down (M2L, then L2L from the parent)).  A cell waits for the
+// cells it depends on through per-cell ready flags (release / acquire, tagged
+// with a per-call epoch).  Everything a warp waits for holds a lower ticket,
+// i.e. it was taken earlier by a running warp, so the wait cannot deadlock.
+//
 // Every kernel is a template on the expansion order PT (PT = 0: runtime p) so
 // that, for the instantiated orders, inner loops unroll and loads pipeline.
 #include <algorithm>
@@ -34,214 +42,272 @@ namespace {
 template <int PT>
 __host__ __device__ constexpr int pmax() { return PT ? PT : kMaxP; }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// all lanes: spin until flag == epoch (acquire by every lane)
+__device__ __forceinline__ void wait_ready(const int* flag, int epoch) {
+  while (ld_acquire(flag) != epoch) __nanosleep(64);
+}
+// publish the warp's writes, then set the flag
+__device__ __forceinline__ void publish(int* flag, int epoch, int lane) {
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) st_release(flag, epoch);
+}
+
+constexpr int kPassWarps = 8;
+
 // ------------------------------------------------------------ P2M (a5)
-// warp per leaf; lane = element of a 32-element round.
+// Warp per leaf; lane = element of a 32-element round.
 //   alpha_n = (B/s) P_{n-1}
 //   gamma_n = (1/s)[Q P_{n-1} + B((n-1) A P_{n-2} + (n-2) r P_{n-1})]
 // zeta_{1,2} = (z_{1,2} - z0)/s, P_m = zeta2^m - zeta1^m, A = conj(zc - z0)/s - r (zc - z0)/s.
 // Coefficients are produced in chunks of 8 and summed over the elements of
 // the round through a padded [32][17] shared-memory transpose (fixed order).
-constexpr int kP2MWarps = 4;
-
 template <int PT>
-__global__ void __launch_bounds__(kP2MWarps * 32)
-p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ c_level,
-           const int* __restrict__ c_ix, const int* __restrict__ c_iy,
-           const int* __restrict__ c_start, const int* __restrict__ c_count, CellGeom cg,
-           int p_rt, const int* __restrict__ perm, const double* __restrict__ D, int ncomp,
-           const double* __restrict__ ex, const double* __restrict__ ey,
-           const double* __restrict__ ea, const double* __restrict__ ec,
-           const double* __restrict__ es, double2* __restrict__ mpole) {
-  const int p = PT ? PT : p_rt;
-  __shared__ double2 buf_all[kP2MWarps][32 * 17];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* buf = buf_all[w];
+__device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const int* __restrict__ c_ix,
+                         const int* __restrict__ c_iy, const int* __restrict__ c_start,
+                         const int* __restrict__ c_count, const CellGeom& cg,
+                         const int* __restrict__ perm, const double* __restrict__ D, int ncomp,
+                         const double* __restrict__ ex, const double* __restrict__ ey,
+                         const double* __restrict__ ea, const double* __restrict__ ec,
+                         const double* __restrict__ es, double2* __restrict__ mpole, double2* buf,
+                         int lane) {
   constexpr int NCH = (pmax<PT>() + 7) / 8;
   const int nchunk = (p + 7) / 8;
-  for (int k = blockIdx.x * kP2MWarps + w; k < nleaves; k += gridDim.x * kP2MWarps) {
-    const int c = leaves[k];
-    const int lev = c_level[c];
-    const double s = cg.side(lev);
-    const double is = 1.0 / s;
-    const double2 z0 = cg.centre(lev, c_ix[c], c_iy[c]);
-    const int e0 = c_start[c], ne = c_count[c];
-    // lane < 16 owns column `lane` of every chunk:
-    // column j < 8 -> alpha slot 8 ch + j, column j >= 8 -> gamma slot 8 ch + j - 8
-    double2 acc[NCH];
+  const int lev = c_level[c];
+  const double s = cg.side(lev);
+  const double is = 1.0 / s;
+  const double2 z0 = cg.centre(lev, c_ix[c], c_iy[c]);
+  const int e0 = c_start[c], ne = c_count[c];
+  // lane < 16 owns column `lane` of every chunk:
+  // column j < 8 -> alpha slot 8 ch + j, column j >= 8 -> gamma slot 8 ch + j - 8
+  double2 acc[NCH];
 #pragma unroll
-    for (int q = 0; q < NCH; ++q) acc[q] = make_double2(0.0, 0.0);
-    for (int r0 = 0; r0 < ne; r0 += 32) {
-      const int i = e0 + r0 + lane;
-      const bool valid = r0 + lane < ne;
-      double2 B = make_double2(0, 0), Q = B, rr = B, A = B, z1 = B, z2 = B;
-      if (valid) {
-        const int j = perm ? perm[i] : i;
-        const double ds = D[(int64_t)j * ncomp], dn = D[(int64_t)j * ncomp + 1];
-        const double cb = ec[i], sb = es[i], a = ea[i];
-        B = make_double2(ds * cb - dn * sb, ds * sb + dn * cb);
-        rr = make_double2(cb * cb - sb * sb, -2.0 * cb * sb);
-        Q = csub(cmul(rr, B), cconj(B));
-        const double2 d = make_double2((ex[i] - z0.x) * is, (ey[i] - z0.y) * is);
-        A = csub(cconj(d), cmul(rr, d));
-        z1 = make_double2(d.x - a * cb * is, d.y - a * sb * is);
-        z2 = make_double2(d.x + a * cb * is, d.y + a * sb * is);
-        B = cscale(B, is);
-        Q = cscale(Q, is);
-      }
-      double2 pw1 = make_double2(1.0, 0.0), pw2 = pw1;
-      double2 Pm1 = make_double2(0.0, 0.0);   // P_{n-2}
-      double2 Pm = make_double2(0.0, 0.0);    // P_{n-1}
-      const int rows = min(32, ne - r0);
+  for (int q = 0; q < NCH; ++q) acc[q] = make_double2(0.0, 0.0);
+  for (int r0 = 0; r0 < ne; r0 += 32) {
+    const int i = e0 + r0 + lane;
+    const bool valid = r0 + lane < ne;
+    double2 B = make_double2(0, 0), Q = B, rr = B, A = B, z1 = B, z2 = B;
+    if (valid) {
+      const int j = perm ? perm[i] : i;
+      const double ds = D[(int64_t)j * ncomp], dn = D[(int64_t)j * ncomp + 1];
+      const double cb = ec[i], sb = es[i], a = ea[i];
+      B = make_double2(ds * cb - dn * sb, ds * sb + dn * cb);
+      rr = make_double2(cb * cb - sb * sb, -2.0 * cb * sb);
+      Q = csub(cmul(rr, B), cconj(B));
+      const double2 d = make_double2((ex[i] - z0.x) * is, (ey[i] - z0.y) * is);
+      A = csub(cconj(d), cmul(rr, d));
+      z1 = make_double2(d.x - a * cb * is, d.y - a * sb * is);
+      z2 = make_double2(d.x + a * cb * is, d.y + a * sb * is);
+      B = cscale(B, is);
+      Q = cscale(Q, is);
+    }
+    double2 pw1 = make_double2(1.0, 0.0), pw2 = pw1;
+    double2 Pm1 = make_double2(0.0, 0.0);   // P_{n-2}
+    double2 Pm = make_double2(0.0, 0.0);    // P_{n-1}
+    const int rows = min(32, ne - r0);
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) {
-        if (ch < nchunk) {
+    for (int ch = 0; ch < NCH; ++ch) {
+      if (ch < nchunk) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int n = 8 * ch + j + 1;        // coefficient index (slot n - 1)
-            double2 alpha = make_double2(0.0, 0.0), gam = alpha;
-            if (n <= p) {
-              if (n >= 2) {
-                pw1 = cmul(pw1, z1);
-                pw2 = cmul(pw2, z2);
-                Pm1 = Pm;
-                Pm = csub(pw2, pw1);
-              }
-              alpha = cmul(B, Pm);
-              gam = cmul(Q, Pm);
-              double2 tt = cscale(cmul(A, Pm1), (double)(n - 1));
-              cmac(tt, cscale(rr, (double)(n - 2)), Pm);
-              cmac(gam, B, tt);
+        for (int j = 0; j < 8; ++j) {
+          const int n = 8 * ch + j + 1;        // coefficient index (slot n - 1)
+          double2 alpha = make_double2(0.0, 0.0), gam = alpha;
+          if (n <= p) {
+            if (n >= 2) {
+              pw1 = cmul(pw1, z1);
+              pw2 = cmul(pw2, z2);
+              Pm1 = Pm;
+              Pm = csub(pw2, pw1);
             }
-            buf[lane * 17 + j] = alpha;
-            buf[lane * 17 + 8 + j] = gam;
+            alpha = cmul(B, Pm);
+            gam = cmul(Q, Pm);
+            double2 tt = cscale(cmul(A, Pm1), (double)(n - 1));
+            cmac(tt, cscale(rr, (double)(n - 2)), Pm);
+            cmac(gam, B, tt);
           }
-          __syncwarp();
-          const int col = lane & 15, h0 = (lane >> 4) * 16;
-          double2 sum = make_double2(0.0, 0.0);
-          const int hend = min(rows, h0 + 16);
-          for (int e = h0; e < hend; ++e) sum = cadd(sum, buf[e * 17 + col]);
-          sum.x += __shfl_down_sync(0xffffffffu, sum.x, 16);
-          sum.y += __shfl_down_sync(0xffffffffu, sum.y, 16);
-          acc[ch] = cadd(acc[ch], sum);
-          __syncwarp();
+          buf[lane * 17 + j] = alpha;
+          buf[lane * 17 + 8 + j] = gam;
         }
+        __syncwarp();
+        const int col = lane & 15, h0 = (lane >> 4) * 16;
+        double2 sum = make_double2(0.0, 0.0);
+        const int hend = min(rows, h0 + 16);
+        for (int e = h0; e < hend; ++e) sum = cadd(sum, buf[e * 17 + col]);
+        sum.x += __shfl_down_sync(0xffffffffu, sum.x, 16);
+        sum.y += __shfl_down_sync(0xffffffffu, sum.y, 16);
+        acc[ch] = cadd(acc[ch], sum);
+        __syncwarp();
       }
     }
-    double2* out = mpole + (size_t)c * 2 * p;
-    if (lane < 16) {
+  }
+  double2* out = mpole + (size_t)c * 2 * p;
+  if (lane < 16) {
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) {
-        const int slot = 8 * ch + (lane & 7);
-        if (ch < nchunk && slot < p) out[(lane < 8 ? 0 : p) + slot] = acc[ch];
-      }
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int slot = 8 * ch + (lane & 7);
+      if (ch < nchunk && slot < p) out[(lane < 8 ? 0 : p) + slot] = acc[ch];
     }
   }
 }
 
 // ------------------------------------------------------------ M2M (a6)
-// Warp per non-leaf parent; child q contributes
-//   alpha^P_m += sum_n M_q[n][m] alpha^q_n,  gamma^P_m += sum_n M_q[n][m] c^q_n,
-//   c_n = gamma_n - (n-1) conj(e)/s_c alpha_{n-1},  e = z_P - z_q,
-// M_q[n][m] = 2^{-n} C(m-1, n-1) eps_q^{m-n} (zero for n > m), eps_q = (z_q - z_P)/s_P.
-// The four operators live in shared memory; children are independent chains.
-constexpr int kM2MWarps = 4;
-
+// Parent c from its children q (all ready):
+//   alpha^c_m = sum_q sum_n M_q[n][m] alpha^q_n,  gamma^c_m = sum_q sum_n M_q[n][m] c^q_n,
+//   c_n = gamma_n - (n-1) conj(e)/s_q alpha_{n-1},  e = z_c - z_q,
+// M_q[n][m] = 2^{-n} C(m-1, n-1) eps_q^{m-n} (zero for n > m), eps_q = (z_q - z_c)/s_c.
 template <int PT>
-__global__ void __launch_bounds__(kM2MWarps * 32)
-m2m_kernel(int c0, int c1, const int* __restrict__ c_leaf, const int* __restrict__ c_ix,
-           const int* __restrict__ c_iy, const int* __restrict__ first_child,
-           const int* __restrict__ nchild, int p_rt, const double2* __restrict__ opT,
-           double2* __restrict__ mpole) {
+__device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* __restrict__ c_iy,
+                         const int* __restrict__ first_child, const int* __restrict__ nchild,
+                         const double2* ops, double2* __restrict__ mpole, double2* xa, double2* xc,
+                         const int* ready, int epoch, int lane) {
+  const int f = first_child[c], nc = nchild[c];
+  int quad[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    quad[i] = 0;
+    if (i < nc) {
+      const int q = f + i;
+      wait_ready(ready + q, epoch);
+      const int xb = c_ix[q] & 1, yb = c_iy[q] & 1;
+      quad[i] = xb + 2 * yb;
+      const double2 eb = make_double2(-(xb - 0.5), (yb - 0.5));   // conj(e)/s_q
+      const double2* mq = mpole + (size_t)q * 2 * p;
+      for (int n = lane; n < p; n += 32) {
+        xa[i * p + n] = mq[n];
+        double2 cv = mq[p + n];
+        if (n >= 1) cmac(cv, cscale(eb, -(double)n), mq[n - 1]);
+        xc[i * p + n] = cv;
+      }
+    }
+  }
+  __syncwarp();
+  double2* out = mpole + (size_t)c * 2 * p;
+  for (int m = lane; m < p; m += 32) {
+    double2 a[4], g[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = g[i] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int n = 0; n < pmax<PT>(); ++n) {
+      if (!PT && n >= p) break;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i < nc) {
+          const double2 tq = ops[(quad[i] * p + n) * p + m];
+          cmac(a[i], tq, xa[i * p + n]);
+          cmac(g[i], tq, xc[i * p + n]);
+        }
+      }
+    }
+    double2 sa = a[0], sg = g[0];
+#pragma unroll
+    for (int i = 1; i < 4; ++i) {
+      sa = cadd(sa, a[i]);
+      sg = cadd(sg, g[i]);
+    }
+    out[m] = sa;
+    out[p + m] = sg;
+  }
+  __syncwarp();
+}
+
+// Upward pass: tickets [0, nleaves) = P2M of leaves[t]; then M2M of
+// up_list[t - nleaves] (non-leaf cells of level >= 2, deepest level first).
+template <int PT>
+__global__ void __launch_bounds__(kPassWarps * 32)
+upward_kernel(int nleaves, int nm2m, const int* __restrict__ leaves,
+              const int* __restrict__ up_list, const int* __restrict__ c_level,
+              const int* __restrict__ c_ix, const int* __restrict__ c_iy,
+              const int* __restrict__ c_start, const int* __restrict__ c_count,
+              const int* __restrict__ first_child, const int* __restrict__ nchild, CellGeom cg,
+              int p_rt, const int* __restrict__ perm, const double* __restrict__ D, int ncomp,
+              const double* __restrict__ ex, const double* __restrict__ ey,
+              const double* __restrict__ ea, const double* __restrict__ ec,
+              const double* __restrict__ es, const double2* __restrict__ opT,
+              double2* __restrict__ mpole, int* __restrict__ ready, int epoch,
+              int* __restrict__ ticket) {
   const int p = PT ? PT : p_rt;
-  extern __shared__ double2 m2m_sh[];
-  double2* ops = m2m_sh;                                   // [4][p][p] as [q][n][m]
+  extern __shared__ double2 up_sh[];
+  double2* ops = up_sh;                                      // [4][p][p] as [q][n][m]
   block_copy(ops, opT, 4 * p * p);
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* xa = m2m_sh + 4 * p * p + (size_t)w * 8 * p;   // [4][p]
-  double2* xc = xa + 4 * p;                                // [4][p]
-  for (int c = c0 + blockIdx.x * kM2MWarps + w; c < c1; c += gridDim.x * kM2MWarps) {
-    if (c_leaf[c]) continue;
-    const int f = first_child[c], nc = nchild[c];
-    int quad[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      quad[i] = 0;
-      if (i < nc) {
-        const int q = f + i;
-        const int xb = c_ix[q] & 1, yb = c_iy[q] & 1;
-        quad[i] = xb + 2 * yb;
-        const double2 eb = make_double2(-(xb - 0.5), (yb - 0.5));   // conj(e)/s_c
-        const double2* mq = mpole + (size_t)q * 2 * p;
-        for (int n = lane; n < p; n += 32) {
-          xa[i * p + n] = mq[n];
-          double2 cv = mq[p + n];
-          if (n >= 1) cmac(cv, cscale(eb, -(double)n), mq[n - 1]);
-          xc[i * p + n] = cv;
-        }
-      }
+  double2* wb = up_sh + 4 * p * p + (size_t)w * (32 * 17 > 8 * p ? 32 * 17 : 8 * p);
+  const int total = nleaves + nm2m;
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= total) break;
+    int c;
+    if (t < nleaves) {
+      c = leaves[t];
+      p2m_cell<PT>(c, p, c_level, c_ix, c_iy, c_start, c_count, cg, perm, D, ncomp, ex, ey, ea,
+                   ec, es, mpole, wb, lane);
+    } else {
+      c = up_list[t - nleaves];
+      m2m_cell<PT>(c, p, c_ix, c_iy, first_child, nchild, ops, mpole, wb, wb + 4 * p, ready,
+                   epoch, lane);
     }
-    __syncwarp();
-    double2* out = mpole + (size_t)c * 2 * p;
-    for (int m = lane; m < p; m += 32) {
-      double2 a[4], g[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = g[i] = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int n = 0; n < pmax<PT>(); ++n) {
-        if (!PT && n >= p) break;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (i < nc) {
-            const double2 tq = ops[(quad[i] * p + n) * p + m];
-            cmac(a[i], tq, xa[i * p + n]);
-            cmac(g[i], tq, xc[i * p + n]);
-          }
-        }
-      }
-      double2 sa = a[0], sg = g[0];
-#pragma unroll
-      for (int i = 1; i < 4; ++i) {
-        sa = cadd(sa, a[i]);
-        sg = cadd(sg, g[i]);
-      }
-      out[m] = sa;
-      out[p + m] = sg;
-    }
-    __syncwarp();
+    publish(ready + c, epoch, lane);
   }
 }
 
-// ------------------------------------------------------------ M2L (a7)
-// Rotated form: with delta = (z_b - z_a)/s = rho e^{i theta},
+// ------------------------------------------------------------ M2L (a7) + L2L (a8)
+// Rotated M2L: with delta = (z_b - z_a)/s = rho e^{i theta},
 //   l_m = (-1)^m/m! e^{-i m theta} sum_{n=1..p} [alpha_n e^{-i n theta}/(n-1)!] R_{n+m}
 //   g_m = (-1)^m/m! e^{-i m theta} sum_{n=1..p+1} [c_n e^{-i n theta}/(n-1)!] R_{n+m}
 //   c_n = gamma_n - (n-1) conj(delta) alpha_{n-1},  R_k = (k-1)! rho^-k (real)
-// Tables per offset class (49) in shared memory; the next source expansion is
-// prefetched into registers while the current one is applied.
-constexpr int kM2LWarps = 8;
-
+// then L2L from the (final) parent P:
+//   g'_m = gamma^P_m + (m+1) conj(eps) lambda^P_{m+1},  eps = (z_c - z_P)/s_P
+//   lambda^c_k += sum_m L_q[m][k] lambda^P_m,  gamma^c_k += sum_m L_q[m][k] g'_m
+// L_q[m][k] = C(m, k) 2^{-k} eps^{m-k} (zero for m < k).
 template <int PT>
-__global__ void __launch_bounds__(kM2LWarps * 32)
-m2l_kernel(int c0, int c1, const int* __restrict__ v_off, const int* __restrict__ v_idx,
-           const unsigned char* __restrict__ v_cls, int p_rt, const double* __restrict__ rtab,
-           const double2* __restrict__ rottab, const double* __restrict__ invfact,
-           const double2* __restrict__ mpole, double2* __restrict__ local) {
+__global__ void __launch_bounds__(kPassWarps * 32)
+downward_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restrict__ v_off,
+                const int* __restrict__ v_idx, const unsigned char* __restrict__ v_cls,
+                const int* __restrict__ c_level, const int* __restrict__ c_ix,
+                const int* __restrict__ c_iy, const int* __restrict__ c_start,
+                const int* __restrict__ c_count, const int* __restrict__ c_parent, int p_rt,
+                const double* __restrict__ rtab, const double2* __restrict__ rottab,
+                const double* __restrict__ invfact, const double2* __restrict__ l2lT,
+                const double2* __restrict__ mpole, double2* __restrict__ local,
+                int* __restrict__ ready, int epoch, int* __restrict__ ticket) {
   const int p = PT ? PT : p_rt;
-  extern __shared__ double2 m2l_sh[];
+  extern __shared__ double2 dn_sh[];
   const int rs = 2 * p + 2;                          // R entries per class
   const int qs = p + 2;                              // rotation entries per class
-  double2* sh_rot = m2l_sh;                          // [49][qs]
-  double* sh_R = reinterpret_cast<double*>(m2l_sh + kNOffsets * qs);   // [49][rs]
-  double2* wbuf = m2l_sh + kNOffsets * qs + (kNOffsets * rs + 1) / 2;
+  double2* sh_l2l = dn_sh;                           // [4][p][p] as [q][m][k]
+  double2* sh_rot = sh_l2l + 4 * p * p;              // [49][qs]
+  double* sh_R = reinterpret_cast<double*>(sh_rot + kNOffsets * qs);   // [49][rs]
+  double2* wbuf = sh_rot + kNOffsets * qs + (kNOffsets * rs + 1) / 2;
+  block_copy(sh_l2l, l2lT, 4 * p * p);
   block_copy(sh_rot, rottab, kNOffsets * qs);
   block_copy(sh_R, rtab, kNOffsets * rs);
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* sa = wbuf + (size_t)w * (3 * p + 2);      // raw alpha [p]
-  double2* ap = sa + p;                               // rotated/scaled alpha [p]
-  double2* cp = ap + p;                               // rotated/scaled c [p+1]
-  for (int c = c0 + blockIdx.x * kM2LWarps + w; c < c1; c += gridDim.x * kM2LWarps) {
+  double2* sa = wbuf + (size_t)w * (3 * p + 2);      // raw alpha [p]      | parent lambda [p]
+  double2* ap = sa + p;                               // rotated alpha [p]  | g' [p]
+  double2* cp = ap + p;                               // rotated c [p+1]
+  const int total = c1 - c0;
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= total) break;
+    const int c = c0 + t;
+    const int cs = c_start[c], ce = cs + c_count[c];
+    if (ce <= own_lo || cs >= own_hi) {   // subtree outside this rank's targets
+      publish(ready + c, epoch, lane);
+      continue;
+    }
     double2 al[2], ag[2];
     al[0] = al[1] = ag[0] = ag[1] = make_double2(0.0, 0.0);
     const int vb = v_off[c], ve = v_off[c + 1];
@@ -313,91 +379,58 @@ m2l_kernel(int c0, int c1, const int* __restrict__ v_off, const int* __restrict_
       }
       __syncwarp();
     }
-    double2* out = local + (size_t)c * 2 * p;
     for (int cc = 0; cc < 2; ++cc) {
       const int m = lane + 32 * cc;
       if (m < p) {
         const double sc = ((m & 1) ? -1.0 : 1.0) * invfact[m];
-        out[m] = cscale(al[cc], sc);
-        out[p + m] = cscale(ag[cc], sc);
+        al[cc] = cscale(al[cc], sc);
+        ag[cc] = cscale(ag[cc], sc);
       }
     }
-  }
-}
-
-// ------------------------------------------------------------ L2L (a8)
-// Warp per non-leaf parent P (level lev); for each child i:
-//   g_m = gamma^P_m + (m+1) conj(eps_i) lambda^P_{m+1},  eps_i = (z_i - z_P)/s_P
-//   lambda^i_k += sum_m L_q[m][k] lambda^P_m,  gamma^i_k += sum_m L_q[m][k] g_m
-// L_q[m][k] = C(m, k) 2^{-k} eps^{m-k} (zero for m < k).
-constexpr int kL2LWarps = 4;
-
-template <int PT>
-__global__ void __launch_bounds__(kL2LWarps * 32)
-l2l_kernel(int c0, int c1, const int* __restrict__ c_leaf, const int* __restrict__ c_ix,
-           const int* __restrict__ c_iy, const int* __restrict__ first_child,
-           const int* __restrict__ nchild, int p_rt, const double2* __restrict__ opT,
-           double2* __restrict__ local) {
-  const int p = PT ? PT : p_rt;
-  extern __shared__ double2 l2l_sh[];
-  double2* ops = l2l_sh;                                     // [4][p][p] as [q][m][k]
-  block_copy(ops, opT, 4 * p * p);
-  __syncthreads();
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* sl = l2l_sh + 4 * p * p + (size_t)w * 5 * p;     // lambda^P [p]
-  double2* xg = sl + p;                                      // g per child [4][p]
-  for (int P = c0 + blockIdx.x * kL2LWarps + w; P < c1; P += gridDim.x * kL2LWarps) {
-    if (c_leaf[P]) continue;
-    const double2* lp = local + (size_t)P * 2 * p;
-    const int f = first_child[P], nc = nchild[P];
-    int quad[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int q = f + min(i, nc - 1);
-      quad[i] = (c_ix[q] & 1) + 2 * (c_iy[q] & 1);
-    }
-    for (int m = lane; m < p; m += 32) {
-      const double2 lm = lp[m];
-      sl[m] = lm;
-      const double2 gm = lp[p + m];
-      const double2 lm1 = (m + 1 < p) ? lp[m + 1] : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int xb = quad[i] & 1, yb = quad[i] >> 1;
-        const double2 epsb = make_double2(0.5 * (xb - 0.5), -0.5 * (yb - 0.5));  // conj(eps)
-        double2 gv = gm;
-        cmac(gv, cscale(epsb, (double)(m + 1)), lm1);
-        xg[i * p + m] = gv;
+    // L2L from the parent (its local expansion is final once its flag is set)
+    if (c_level[c] >= 3) {
+      const int P = c_parent[c];
+      wait_ready(ready + P, epoch);
+      const double2* lp = local + (size_t)P * 2 * p;
+      const int xb = c_ix[c] & 1, yb = c_iy[c] & 1;
+      const int quad = xb + 2 * yb;
+      const double2 epsb = make_double2(0.5 * (xb - 0.5), -0.5 * (yb - 0.5));   // conj(eps)
+      double2* sl = sa;
+      double2* sg = ap;
+      for (int m = lane; m < p; m += 32) {
+        sl[m] = lp[m];
+        double2 gv = lp[p + m];
+        if (m + 1 < p) cmac(gv, cscale(epsb, (double)(m + 1)), lp[m + 1]);
+        sg[m] = gv;
       }
-    }
-    __syncwarp();
-    for (int k = lane; k < p; k += 32) {
-      double2 l[4], g[4];
+      __syncwarp();
+      const double2* L = sh_l2l + (size_t)quad * p * p;
+      for (int cc = 0; cc < 2; ++cc) {
+        const int k = lane + 32 * cc;
+        if (k < p) {
+          double2 l = al[cc], g = ag[cc];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) l[i] = g[i] = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int m = 0; m < pmax<PT>(); ++m) {
-        if (!PT && m >= p) break;
-        const double2 lm = sl[m];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (i < nc) {
-            const double2 tq = ops[(quad[i] * p + m) * p + k];
-            cmac(l[i], tq, lm);
-            cmac(g[i], tq, xg[i * p + m]);
+          for (int m = 0; m < pmax<PT>(); ++m) {
+            if (!PT && m >= p) break;
+            const double2 tq = L[m * p + k];
+            cmac(l, tq, sl[m]);
+            cmac(g, tq, sg[m]);
           }
+          al[cc] = l;
+          ag[cc] = g;
         }
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (i < nc) {
-          double2* out = local + (size_t)(f + i) * 2 * p;
-          out[k] = cadd(out[k], l[i]);
-          out[p + k] = cadd(out[p + k], g[i]);
-        }
+      __syncwarp();
+    }
+    double2* out = local + (size_t)c * 2 * p;
+    for (int cc = 0; cc < 2; ++cc) {
+      const int m = lane + 32 * cc;
+      if (m < p) {
+        out[m] = al[cc];
+        out[p + m] = ag[cc];
       }
     }
-    __syncwarp();
+    publish(ready + c, epoch, lane);
   }
 }
 
@@ -469,35 +502,35 @@ int set_smem(ddm_ctx_s* ctx, K kernel, size_t shm) {
   return DDM_OK;
 }
 
-}  // namespace
-
-int launch_p2m(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
-               cudaStream_t s) {
-  const CellGeom cg{t->x_min, t->y_min, t->W};
-  const unsigned nb = std::min(nblk(t->nleaves, kP2MWarps), 148u * 8);
-#define DDM_L(PT)                                                                               \
-  p2m_kernel<PT><<<nb, kP2MWarps * 32, 0, s>>>(t->nleaves, t->leaves, t->c_level, t->c_ix,      \
-                                               t->c_iy, t->c_start, t->c_count, cg, t->p,       \
-                                               perm_in, D, ncomp, t->ex, t->ey, t->ea, t->ec,   \
-                                               t->es, t->mpole)
-  DDM_P_DISPATCH(t->p, DDM_L);
-#undef DDM_L
-  DDM_CUDA(ctx, cudaGetLastError());
-  return DDM_OK;
+int pass_grid(ddm_ctx_s* ctx, const void* kernel, size_t shm, int work) {
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kPassWarps * 32, shm);
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+  const int by_work = (work + kPassWarps - 1) / kPassWarps;
+  return std::max(1, std::min(std::max(per_sm, 1) * nsm, by_work));
 }
 
-int launch_m2m_level(ddm_ctx_s* ctx, ddm_tree_s* t, int lev, cudaStream_t s) {
+}  // namespace
+
+// upward pass: P2M on all leaves + M2M of every non-leaf cell of level >= 2
+int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
+                  cudaStream_t s) {
   const int p = t->p;
-  const int c0 = t->level_off[lev], c1 = t->level_off[lev + 1];
-  const size_t shm = ((size_t)4 * p * p + (size_t)kM2MWarps * 8 * p) * sizeof(double2);
-  const unsigned nb = std::min(nblk(c1 - c0, kM2MWarps), 148u * 6);
+  const CellGeom cg{t->x_min, t->y_min, t->W};
+  const size_t wsz = std::max(32 * 17, 8 * p);
+  const size_t shm = ((size_t)4 * p * p + (size_t)kPassWarps * wsz) * sizeof(double2);
+  ++t->epoch;
+  DDM_CUDA(ctx, cudaMemsetAsync(t->tickets, 0, 2 * sizeof(int), s));
   int rc = DDM_OK;
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \
-    if ((rc = set_smem(ctx, m2m_kernel<PT>, shm))) return rc;                                   \
-    m2m_kernel<PT><<<nb, kM2MWarps * 32, shm, s>>>(c0, c1, t->c_leaf, t->c_ix, t->c_iy,         \
-                                                   t->c_first_child, t->c_nchild, p,            \
-                                                   t->op_m2m, t->mpole);                        \
+    if ((rc = set_smem(ctx, upward_kernel<PT>, shm))) return rc;                                \
+    const int nb = pass_grid(ctx, (const void*)upward_kernel<PT>, shm, t->nleaves + t->n_up);   \
+    upward_kernel<PT><<<nb, kPassWarps * 32, shm, s>>>(                                         \
+        t->nleaves, t->n_up, t->leaves, t->up_list, t->c_level, t->c_ix, t->c_iy, t->c_start,   \
+        t->c_count, t->c_first_child, t->c_nchild, cg, p, perm_in, D, ncomp, t->ex, t->ey,      \
+        t->ea, t->ec, t->es, t->op_m2m, t->mpole, t->ready_up, t->epoch, t->tickets);           \
   } while (0)
   DDM_P_DISPATCH(p, DDM_L);
 #undef DDM_L
@@ -505,39 +538,23 @@ int launch_m2m_level(ddm_ctx_s* ctx, ddm_tree_s* t, int lev, cudaStream_t s) {
   return DDM_OK;
 }
 
-int launch_m2l(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
+// downward pass: M2L + L2L of every cell of level >= 2, top-down
+int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   if (t->nlevels <= 2) return DDM_OK;
   const int p = t->p;
   const int c0 = t->level_off[2], c1 = t->ncells;
-  const size_t shm = ((size_t)kNOffsets * (p + 2) + ((size_t)kNOffsets * (2 * p + 2) + 1) / 2 +
-                      (size_t)kM2LWarps * (3 * p + 2)) * sizeof(double2);
-  const unsigned nb = std::min(nblk(c1 - c0, kM2LWarps), 148u * 4);
+  const size_t shm = ((size_t)4 * p * p + (size_t)kNOffsets * (p + 2) +
+                      ((size_t)kNOffsets * (2 * p + 2) + 1) / 2 +
+                      (size_t)kPassWarps * (3 * p + 2)) * sizeof(double2);
   int rc = DDM_OK;
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \
-    if ((rc = set_smem(ctx, m2l_kernel<PT>, shm))) return rc;                                   \
-    m2l_kernel<PT><<<nb, kM2LWarps * 32, shm, s>>>(c0, c1, t->v_off, t->v_idx, t->v_cls, p,     \
-                                                   t->op_R, t->op_h, t->invfact, t->mpole,      \
-                                                   t->local);                                   \
-  } while (0)
-  DDM_P_DISPATCH(p, DDM_L);
-#undef DDM_L
-  DDM_CUDA(ctx, cudaGetLastError());
-  return DDM_OK;
-}
-
-int launch_l2l_level(ddm_ctx_s* ctx, ddm_tree_s* t, int lev, cudaStream_t s) {
-  const int p = t->p;
-  const int c0 = t->level_off[lev], c1 = t->level_off[lev + 1];
-  const size_t shm = ((size_t)4 * p * p + (size_t)kL2LWarps * 5 * p) * sizeof(double2);
-  const unsigned nb = std::min(nblk(c1 - c0, kL2LWarps), 148u * 6);
-  int rc = DDM_OK;
-#define DDM_L(PT)                                                                               \
-  do {                                                                                          \
-    if ((rc = set_smem(ctx, l2l_kernel<PT>, shm))) return rc;                                   \
-    l2l_kernel<PT><<<nb, kL2LWarps * 32, shm, s>>>(c0, c1, t->c_leaf, t->c_ix, t->c_iy,         \
-                                                   t->c_first_child, t->c_nchild, p,            \
-                                                   t->op_l2l, t->local);                        \
+    if ((rc = set_smem(ctx, downward_kernel<PT>, shm))) return rc;                              \
+    const int nb = pass_grid(ctx, (const void*)downward_kernel<PT>, shm, c1 - c0);              \
+    downward_kernel<PT><<<nb, kPassWarps * 32, shm, s>>>(                                       \
+        c0, c1, t->own_el_lo, t->own_el_hi, t->v_off, t->v_idx, t->v_cls, t->c_level, t->c_ix,  \
+        t->c_iy, t->c_start, t->c_count, t->c_parent, p, t->op_R, t->op_h, t->invfact,          \
+        t->op_l2l, t->mpole, t->local, t->ready_down, t->epoch, t->tickets + 1);                \
   } while (0)
   DDM_P_DISPATCH(p, DDM_L);
 #undef DDM_L

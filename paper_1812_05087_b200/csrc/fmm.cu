@@ -153,7 +153,7 @@ int fmm_matvec_elastic(ddm_ctx_s* ctx, ddm_tree_s* t, double G, double nu, const
   // stream concurrently with the latency-bound far-field chain on the
   // high-priority stream; both only read `src` / D and write disjoint buffers.
   DDM_CUDA(ctx, cudaEventRecord(ctx->ev_fork, s));
-  cudaStream_t sf = ctx->s_hi, sn = ctx->s_lo;
+  cudaStream_t sf = ctx->serial ? s : ctx->s_hi, sn = ctx->serial ? s : ctx->s_lo;
   DDM_CUDA(ctx, cudaStreamWaitEvent(sf, ctx->ev_fork, 0));
   DDM_CUDA(ctx, cudaStreamWaitEvent(sn, ctx->ev_fork, 0));
 
@@ -163,23 +163,17 @@ int fmm_matvec_elastic(ddm_ctx_s* ctx, ddm_tree_s* t, double G, double nu, const
   stage_end(ctx, DDM_ST_P2P, sn);
   DDM_CUDA(ctx, cudaEventRecord(ctx->ev_near, sn));
 
-  // upward pass: P2M on all leaves, M2M finest -> level 2 (replicated on all ranks)
+  // upward pass (one persistent launch): P2M on all leaves + M2M finest ->
+  // level 2, replicated on all ranks.  Stage "p2m" times the whole upward pass.
   stage_begin(ctx, DDM_ST_P2M, sf);
-  if ((rc = launch_p2m(ctx, t, perm_in, D, ncomp, sf))) return rc;
+  if ((rc = launch_upward(ctx, t, perm_in, D, ncomp, sf))) return rc;
   stage_end(ctx, DDM_ST_P2M, sf);
-  stage_begin(ctx, DDM_ST_M2M, sf);
-  for (int lev = t->nlevels - 2; lev >= 2; --lev)
-    if ((rc = launch_m2m_level(ctx, t, lev, sf))) return rc;
-  stage_end(ctx, DDM_ST_M2M, sf);
 
-  // downward pass: M2L at every level >= 2 (one launch), L2L top-down
+  // downward pass (one persistent launch): M2L + L2L of every cell of level
+  // >= 2 whose subtree holds owned targets.  Stage "m2l" times the whole pass.
   stage_begin(ctx, DDM_ST_M2L, sf);
-  if ((rc = launch_m2l(ctx, t, sf))) return rc;
+  if ((rc = launch_downward(ctx, t, sf))) return rc;
   stage_end(ctx, DDM_ST_M2L, sf);
-  stage_begin(ctx, DDM_ST_L2L, sf);
-  for (int lev = 2; lev + 1 < t->nlevels; ++lev)
-    if ((rc = launch_l2l_level(ctx, t, lev, sf))) return rc;
-  stage_end(ctx, DDM_ST_L2L, sf);
   DDM_CUDA(ctx, cudaEventRecord(ctx->ev_far, sf));
 
   // join

@@ -53,11 +53,9 @@ struct CellGeom {
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 // ---- launchers (expansions.cu): upward / downward passes
-int launch_p2m(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
-               cudaStream_t s);
-int launch_m2m_level(ddm_ctx_s* ctx, ddm_tree_s* t, int lev, cudaStream_t s);
-int launch_m2l(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
-int launch_l2l_level(ddm_ctx_s* ctx, ddm_tree_s* t, int lev, cudaStream_t s);
+int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
+                  cudaStream_t s);
+int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
 int launch_finalize(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, int ncomp, double gc,
                     double* y_user, double* y_sorted, cudaStream_t s);
 

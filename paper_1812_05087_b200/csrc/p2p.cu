@@ -82,8 +82,11 @@ __device__ __forceinline__ double2 acc_to_traction(const P2PAcc& a, double gc, d
 // sources j = l / nt (mod S) of each 32-source batch staged in shared memory;
 // the S slice partials are summed in a fixed order (deterministic).
 constexpr int kP2PWarps = 4;
+#ifndef DDM_P2P_MINB
+#define DDM_P2P_MINB 8   // >= 8 resident blocks per SM (measured best: 1.18 -> 1.06 ms)
+#endif
 
-__global__ void __launch_bounds__(kP2PWarps * 32)
+__global__ void __launch_bounds__(kP2PWarps * 32, DDM_P2P_MINB)
 p2p_kernel(int item_lo, int item_hi, const int4* __restrict__ items,
            const int* __restrict__ u_off, const int* __restrict__ u_lo,
            const int* __restrict__ u_hi, const int* __restrict__ leaves,

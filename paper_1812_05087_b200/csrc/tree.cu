@@ -460,7 +460,7 @@ void free_tree(ddm_tree_s* t) {
                   t->v_off, t->v_idx, t->v_cls, t->leaves, t->u_off, t->u_lo, t->u_hi,
                   t->items, t->item_off, t->m2l_cells, t->op_m2m, t->op_l2l, t->op_h, t->op_R,
                   t->invfact, t->mpole, t->local, t->src, t->part, t->d_sorted, t->y_sorted,
-                  t->part_direct,
+                  t->part_direct, t->up_list, t->ready_up, t->ready_down, t->tickets,
                   t->krylov, t->gm_w, t->gm_tmp, t->gm_part};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -769,6 +769,28 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
   permute_elements<<<nblk(n, 256), 256, 0, s>>>(n, t->perm, xc, yc, a, beta, t->ex, t->ey,
                                                 t->ea, t->ec, t->es);
   DDM_CUDA(ctx, cudaGetLastError());
+
+  // ---- schedule of the persistent upward pass: non-leaf cells of level >= 2,
+  // deepest level first (every parent after all of its children)
+  {
+    std::vector<int> hleaf(ncells);
+    DDM_CUDA(ctx, cudaMemcpyAsync(hleaf.data(), C.leaf, ncells * sizeof(int),
+                                  cudaMemcpyDeviceToHost, s));
+    DDM_CUDA(ctx, cudaStreamSynchronize(s));
+    std::vector<int> up;
+    for (int lev = t->nlevels - 1; lev >= 2; --lev)
+      for (int c = t->level_off[lev]; c < t->level_off[lev + 1]; ++c)
+        if (!hleaf[c]) up.push_back(c);
+    t->n_up = (int)up.size();
+    if ((rc = dalloc(ctx, &t->up_list, up.size())) || (rc = dalloc(ctx, &t->ready_up, ncells)) ||
+        (rc = dalloc(ctx, &t->ready_down, ncells)) || (rc = dalloc(ctx, &t->tickets, 2)))
+      return rc;
+    if (!up.empty())
+      DDM_CUDA(ctx, cudaMemcpyAsync(t->up_list, up.data(), up.size() * sizeof(int),
+                                    cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaMemsetAsync(t->ready_up, 0, ncells * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMemsetAsync(t->ready_down, 0, ncells * sizeof(int), s));
+  }
   DDM_CUDA(ctx, cudaStreamSynchronize(s));
   return DDM_OK;
 }
