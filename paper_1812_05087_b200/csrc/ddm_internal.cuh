@@ -17,8 +17,12 @@ namespace ddm {
 constexpr int kLBits = 30;      // quantisation bits per axis (R8)
 constexpr int kMaxP = 40;       // max complex coefficients per series
 constexpr int kNOffsets = 49;   // (dx,dy) in [-3,3]^2, class id (dy+3)*7+(dx+3)
-constexpr int kTgtGroup = 8;    // targets per P2P work item (one warp, 32/nt source slices)
+#ifndef DDM_TGT_GROUP
+#define DDM_TGT_GROUP 16
+#endif
+constexpr int kTgtGroup = DDM_TGT_GROUP;   // targets per P2P work item (one warp)
 constexpr int kSrcChunk = 512;  // max sources per P2P work item
+constexpr int kSrcStride = 12;  // doubles per P2P source record
 
 struct Status {
   int code = DDM_OK;

@@ -26,7 +26,7 @@ int ensure_workspace(ddm_ctx_s* ctx, ddm_tree_s* t) {
   if (!t->mpole) {
     if ((rc = dalloc(ctx, &t->mpole, (size_t)t->ncells * 2 * t->p))) return rc;
     if ((rc = dalloc(ctx, &t->local, (size_t)t->ncells * 2 * t->p))) return rc;
-    if ((rc = dalloc(ctx, &t->src, (size_t)t->n * 10))) return rc;
+    if ((rc = dalloc(ctx, &t->src, (size_t)t->n * kSrcStride))) return rc;
     if ((rc = dalloc(ctx, &t->part, (size_t)t->nitems * kTgtGroup))) return rc;
     if ((rc = dalloc(ctx, &t->d_sorted, (size_t)t->n * 3))) return rc;
     if ((rc = dalloc(ctx, &t->y_sorted, (size_t)t->n * 3))) return rc;

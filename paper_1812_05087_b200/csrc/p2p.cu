@@ -10,8 +10,9 @@ namespace ddm {
 namespace {
 
 // Per element (sorted order), from the DDs (D_s, D_n) and geometry:
-//   e = e^{i beta}, B = (D_s + i D_n) e, r = conj(e)^2, Q' = Q - 2 B r = -(r B + conj B)
-//   src = {z1, z2, r, B/2, Q'}  (10 doubles)
+//   e = e^{i beta}, B = (D_s + i D_n) e, r = conj(e)^2, Bh = B/2,
+//   Q' = Q - 2 B r = -(r B + conj B), P1 = Bh (r - 1), P2 = i Bh (r + 1)
+//   src = {z1, z2, P1, P2, Bh, Q'}  (12 doubles, kSrcStride)
 __global__ void prep_sources(int64_t n, int ncomp, const int* __restrict__ perm,
                              const double* __restrict__ D, const double* __restrict__ ex,
                              const double* __restrict__ ey, const double* __restrict__ ea,
@@ -27,18 +28,24 @@ __global__ void prep_sources(int64_t n, int ncomp, const int* __restrict__ perm,
   const double2 r = make_double2(c * c - s * s, -2.0 * c * s);
   const double2 rB = cmul(r, B);
   const double2 Qp = make_double2(-(rB.x + B.x), -(rB.y - B.y));
-  double2* o = reinterpret_cast<double2*>(src + i * 10);
+  const double2 Bh = make_double2(0.5 * B.x, 0.5 * B.y);
+  const double2 P1 = cmul(Bh, make_double2(r.x - 1.0, r.y));
+  const double2 T2 = cmul(Bh, make_double2(r.x + 1.0, r.y));
+  double2* o = reinterpret_cast<double2*>(src + i * kSrcStride);
   o[0] = make_double2(ex[i] - a * c, ey[i] - a * s);
   o[1] = make_double2(ex[i] + a * c, ey[i] + a * s);
-  o[2] = r;
-  o[3] = make_double2(0.5 * B.x, 0.5 * B.y);
-  o[4] = Qp;
+  o[2] = P1;
+  o[3] = make_double2(-T2.y, T2.x);    // P2 = i Bh (r + 1)
+  o[4] = Bh;
+  o[5] = Qp;
 }
 
-// Contribution of source element (z1, z2, r, Bh, Q') to the target at z:
+// Contribution of source element (z1, z2, P1, P2, Bh, Q') to the target at z:
 //   r1 = 1/(z - z1), r2 = 1/(z - z2), I2 = r2 - r1, I3 = I2 (r1 + r2)/2
 //   Phi           += i G C B I2                 -> phi += Im(Bh I2)
 //   zb Phi' + Psi += i G C I2 [Q' + B (r D - conj D)(r1 + r2)/2],  D = z - zc
+// with Bh (r D2 - conj D2) = dx P1 + dy P2 for D2 = 2 D = dx + i dy.
+// 36 fp64-pipe instructions + 1 MUFU.RCP64H; r1, r2 share one reciprocal.
 struct P2PAcc {
   double phi = 0.0;
   double2 psi = make_double2(0.0, 0.0);
@@ -51,19 +58,17 @@ __device__ __forceinline__ void pair_update(P2PAcc& acc, double zx, double zy, c
   const double n2 = fma(w2x, w2x, w2y * w2y);
   const double inv = fast_rcp(n1 * n2);
   const double i1 = n2 * inv, i2 = n1 * inv;
-  const double2 r1 = make_double2(w1x * i1, -w1y * i1);
-  const double2 r2 = make_double2(w2x * i2, -w2y * i2);
-  const double2 I2 = csub(r2, r1);
-  const double2 S = cadd(r1, r2);
+  const double r1x = w1x * i1, r1y = -w1y * i1;        // r1 = conj(w1)/|w1|^2
+  const double I2x = fma(w2x, i2, -r1x), I2y = fma(-w2y, i2, -r1y);   // r2 - r1
+  const double Sx = fma(w2x, i2, r1x), Sy = fma(-w2y, i2, r1y);       // r2 + r1
   const double dx = w1x + w2x, dy = w1y + w2y;   // 2 (z - zc)
-  // X = r * D2 - conj(D2)
-  const double2 X = make_double2(fma(sp[4], dx, fma(-sp[5], dy, -dx)),
-                                 fma(sp[4], dy, fma(sp[5], dx, dy)));
-  const double2 BX = cmul(make_double2(sp[6], sp[7]), X);   // (B/2) X = B (r D - conj D)
-  double2 V = make_double2(sp[8], sp[9]);
-  cmac(V, BX, S);
-  cmac(acc.psi, I2, V);
-  acc.phi = fma(sp[6], I2.y, fma(sp[7], I2.x, acc.phi));
+  const double BXx = fma(dx, sp[4], dy * sp[6]);
+  const double BXy = fma(dx, sp[5], dy * sp[7]);
+  const double Vx = fma(BXx, Sx, fma(-BXy, Sy, sp[10]));
+  const double Vy = fma(BXx, Sy, fma(BXy, Sx, sp[11]));
+  acc.psi.x = fma(I2x, Vx, fma(-I2y, Vy, acc.psi.x));
+  acc.psi.y = fma(I2x, Vy, fma(I2y, Vx, acc.psi.y));
+  acc.phi = fma(sp[8], I2y, fma(sp[9], I2x, acc.phi));
 }
 
 // traction (sigma_s, sigma_n) at a target with direction (ct, st):
@@ -77,14 +82,17 @@ __device__ __forceinline__ double2 acc_to_traction(const P2PAcc& a, double gc, d
 }
 
 // One warp per work item (leaf k, group of nt <= kTgtGroup targets, interval
-// of the leaf's concatenated source ranges).  The 32 lanes are split into
-// S = 32 / nt source slices: lane l evaluates target l % nt against the
-// sources j = l / nt (mod S) of each 32-source batch staged in shared memory;
-// the S slice partials are summed in a fixed order (deterministic).
+// of the leaf's concatenated source ranges).  Each lane owns kTPL targets
+// (independent chains sharing every source load); the tp = ceil(nt/kTPL)
+// lane-target slots are replicated over S = 32 / tp source slices: lane l
+// takes slot l % tp and the sources j = l / tp (mod S).  Source records are
+// read through L1 (the tp lanes of a slice broadcast one record).  The S slice
+// partials are summed in a fixed order (deterministic results).
 constexpr int kP2PWarps = 4;
 #ifndef DDM_P2P_MINB
-#define DDM_P2P_MINB 8   // >= 8 resident blocks per SM (measured best: 1.18 -> 1.06 ms)
+#define DDM_P2P_MINB 6
 #endif
+constexpr int kTPL = kTgtGroup / 8;   // targets per lane (2)
 
 __global__ void __launch_bounds__(kP2PWarps * 32, DDM_P2P_MINB)
 p2p_kernel(int item_lo, int item_hi, const int4* __restrict__ items,
@@ -94,59 +102,70 @@ p2p_kernel(int item_lo, int item_hi, const int4* __restrict__ items,
            const double* __restrict__ src, const double* __restrict__ ex,
            const double* __restrict__ ey, const double* __restrict__ ec,
            const double* __restrict__ es, double gc, double2* __restrict__ part) {
-  __shared__ double sh[kP2PWarps][32 * 10];
-  __shared__ double red[kP2PWarps][3][32];
+  __shared__ double red[kP2PWarps][3][32 * kTPL];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* ssrc = sh[w];
   for (int it = item_lo + blockIdx.x * kP2PWarps + w; it < item_hi;
        it += gridDim.x * kP2PWarps) {
     const int4 item = items[it];
     const int k = item.x;
     const int c = leaves[k];
     const int nt = min(kTgtGroup, c_start[c] + c_count[c] - item.y);
-    const int S = 32 / nt;
-    const int tl = lane % nt, slice = lane / nt;
+    const int tp = (nt + kTPL - 1) / kTPL;
+    const int S = 32 / tp;
+    const int tl = lane % tp, slice = lane / tp;
     const bool active = slice < S;
-    const int ti = item.y + tl;
-    const double zx = ex[ti], zy = ey[ti];
-    P2PAcc acc;
-    // cursor into the leaf's concatenated source ranges
-    int r = u_off[k];
-    const int rend = u_off[k + 1];
-    int roff = item.z;
-    while (r < rend && roff >= u_hi[r] - u_lo[r]) { roff -= u_hi[r] - u_lo[r]; ++r; }
-    for (int t = item.z; t < item.w; t += 32) {
-      const int nb = min(32, item.w - t);
-      if (lane < nb) {
-        int rr = r, q = roff + lane;
-        while (q >= u_hi[rr] - u_lo[rr]) { q -= u_hi[rr] - u_lo[rr]; ++rr; }
-        const double2* g = reinterpret_cast<const double2*>(src + (int64_t)(u_lo[rr] + q) * 10);
-        double2* d = reinterpret_cast<double2*>(ssrc + lane * 10);
+    double zx[kTPL], zy[kTPL];
+    P2PAcc acc[kTPL];
 #pragma unroll
-        for (int f = 0; f < 5; ++f) d[f] = g[f];
-      }
-      __syncwarp();
-      if (active) {
-#pragma unroll 4
-        for (int j = slice; j < nb; j += S) pair_update(acc, zx, zy, ssrc + j * 10);
-      }
-      __syncwarp();
-      roff += nb;
-      while (r < rend && roff >= u_hi[r] - u_lo[r]) { roff -= u_hi[r] - u_lo[r]; ++r; }
+    for (int q = 0; q < kTPL; ++q) {
+      const int ti = item.y + min(tl * kTPL + q, nt - 1);
+      zx[q] = ex[ti];
+      zy[q] = ey[ti];
     }
-    red[w][0][lane] = acc.phi;
-    red[w][1][lane] = acc.psi.x;
-    red[w][2][lane] = acc.psi.y;
+    if (active) {
+      int pos = 0;   // position in the concatenated range space
+      for (int r = u_off[k], rend = u_off[k + 1]; r < rend && pos < item.w; ++r) {
+        const int lo = u_lo[r], len = u_hi[r] - lo;
+        const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
+        const double* base = src + (int64_t)lo * kSrcStride;
+#pragma unroll 2
+        for (int j = b + slice; j < e; j += S) {
+          double sp[kSrcStride];
+          const double2* g = reinterpret_cast<const double2*>(base + (int64_t)j * kSrcStride);
+#pragma unroll
+          for (int f = 0; f < kSrcStride / 2; ++f) {
+            const double2 v = __ldg(g + f);
+            sp[2 * f] = v.x;
+            sp[2 * f + 1] = v.y;
+          }
+#pragma unroll
+          for (int q = 0; q < kTPL; ++q) pair_update(acc[q], zx[q], zy[q], sp);
+        }
+        pos += len;
+      }
+    }
+    // slot of (target t, slice s) = t + s * tp * kTPL
+#pragma unroll
+    for (int q = 0; q < kTPL; ++q) {
+      const int sl = tl * kTPL + q + slice * tp * kTPL;
+      if (active) {
+        red[w][0][sl] = acc[q].phi;
+        red[w][1][sl] = acc[q].psi.x;
+        red[w][2][sl] = acc[q].psi.y;
+      }
+    }
     __syncwarp();
     if (lane < kTgtGroup) {
       double2 T = make_double2(0.0, 0.0);
       if (lane < nt) {
         P2PAcc tot;
         for (int s2 = 0; s2 < S; ++s2) {
-          tot.phi += red[w][0][lane + s2 * nt];
-          tot.psi.x += red[w][1][lane + s2 * nt];
-          tot.psi.y += red[w][2][lane + s2 * nt];
+          const int sl = lane + s2 * tp * kTPL;
+          tot.phi += red[w][0][sl];
+          tot.psi.x += red[w][1][sl];
+          tot.psi.y += red[w][2][sl];
         }
+        const int ti = item.y + lane;
         T = acc_to_traction(tot, gc, ec[ti], es[ti]);
       }
       part[(int64_t)it * kTgtGroup + lane] = T;
@@ -164,7 +183,7 @@ direct_kernel(int64_t n, int64_t t_lo, int64_t t_hi, int ncomp, const double* __
               const double* __restrict__ ec, const double* __restrict__ es, double gc,
               const int* __restrict__ perm, double* __restrict__ y_user,
               double* __restrict__ y_sorted) {
-  __shared__ double ssrc[kDirThreads * 10];
+  __shared__ double ssrc[kDirThreads * kSrcStride];
   const int64_t ti = t_lo + blockIdx.x * (int64_t)kDirThreads + threadIdx.x;
   const bool tvalid = ti < t_hi;
   double zx = 0.0, zy = 0.0;
@@ -173,10 +192,11 @@ direct_kernel(int64_t n, int64_t t_lo, int64_t t_hi, int ncomp, const double* __
   for (int64_t j0 = 0; j0 < n; j0 += kDirThreads) {
     const int nb = (int)min((int64_t)kDirThreads, n - j0);
     __syncthreads();
-    for (int f = threadIdx.x; f < nb * 5; f += kDirThreads)
-      reinterpret_cast<double2*>(ssrc)[f] = reinterpret_cast<const double2*>(src + j0 * 10)[f];
+    for (int f = threadIdx.x; f < nb * kSrcStride / 2; f += kDirThreads)
+      reinterpret_cast<double2*>(ssrc)[f] =
+          reinterpret_cast<const double2*>(src + j0 * kSrcStride)[f];
     __syncthreads();
-    for (int j = 0; j < nb; ++j) pair_update(acc, zx, zy, ssrc + j * 10);
+    for (int j = 0; j < nb; ++j) pair_update(acc, zx, zy, ssrc + j * kSrcStride);
   }
   if (!tvalid) return;
   const double2 T = acc_to_traction(acc, gc, ec[ti], es[ti]);
