@@ -20,6 +20,7 @@
 // Every kernel is a template on the expansion order PT (PT = 0: runtime p) so
 // that, for the instantiated orders, inner loops unroll and loads pipeline.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kcommon.cuh"
 
@@ -508,6 +509,13 @@ int pass_grid(ddm_ctx_s* ctx, const void* kernel, size_t shm, int work) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
   const int by_work = (work + kPassWarps - 1) / kPassWarps;
+  // DDM_PASS_BLOCKS_PER_SM caps the persistent grid so the concurrent near
+  // field keeps SM slots (0 = occupancy limit)
+  static const int cap = [] {
+    const char* e = getenv("DDM_PASS_BLOCKS_PER_SM");
+    return e ? atoi(e) : 0;
+  }();
+  if (cap > 0) per_sm = std::min(per_sm, cap);
   return std::max(1, std::min(std::max(per_sm, 1) * nsm, by_work));
 }
 
