@@ -50,7 +50,7 @@ class Clocks:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -235,7 +235,9 @@ def run_ours(args):
     p2p_ms = stages["p2p"]
     achieved = owned_pairs * FLOP_PER_PAIR / (p2p_ms * 1e-3) / 1e12
     levels = cnt["LEVELS"]
-    launches_per_step = 1 + 1 + max(0, levels - 3) + 1 + max(0, levels - 3) + 1 + 1
+    # prep_sources, p2p_kernel, upward_kernel, downward_kernel, finalize_kernel
+    # (+ unpack_allgather and scatter_user when the rows are exchanged)
+    launches_per_step = 5
     if world > 1:
         launches_per_step += 2
 
@@ -312,7 +314,7 @@ def gmres_extra(D, ctx, torch, dev):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=5)
