@@ -6,13 +6,17 @@
 #include <cstring>
 #include <new>
 
-#include "ddm_internal.cuh"
+#include "kcommon.cuh"
 
 namespace ddm {
 
 int set_error(ddm_ctx_s* ctx, int code, const std::string& msg) {
   if (ctx) ctx->err = msg;
   return code;
+}
+
+int cuda_error_if(ddm_ctx_s* ctx, cudaError_t e, const char* what) {
+  return e == cudaSuccess ? DDM_OK : cuda_error(ctx, e, what);
 }
 
 int cuda_error(ddm_ctx_s* ctx, cudaError_t e, const char* what) {
@@ -83,8 +87,6 @@ __global__ void dfma_probe_kernel(int iters, double a, double b, double* out) {
   for (int k = 0; k < 8; ++k) s += x[k];
   if (s == 1.2345e-300) out[0] = s;   // keep the chains alive
 }
-
-inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 int check_material(ddm_ctx_s* ctx, const ddm_material* m) {
   if (!m) return set_error(ctx, DDM_ERR_ARG, "material is NULL");
@@ -220,6 +222,13 @@ int ddm_ctx_create(int device, const void* nccl_uid, int rank, int world, ddm_ct
     int rc = cuda_error(ctx, e, "cudaMalloc(scratch)");
     *out = ctx;
     return rc;
+  }
+  {
+    int rc = poro_init_tables(ctx);
+    if (rc) {
+      *out = ctx;
+      return rc;
+    }
   }
   {
     const char* ser = getenv("DDM_SERIAL");
@@ -393,39 +402,66 @@ int ddm_matvec(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double elap
   if (rc) return rc;
   if (mode != DDM_FMM && mode != DDM_DIRECT) return set_error(ctx, DDM_ERR_ARG, "bad mode");
   cudaStream_t s = (cudaStream_t)stream;
-  if (mat->kind != 0)
-    return set_error(ctx, DDM_ERR_ARG, "poroelastic matvec not available in this build");
-  (void)elapsed;
-  if (ctx->world == 1) return fmm_matvec_elastic(ctx, t, mat->G, mat->nu, D, false, y, nullptr,
-                                                 mode, s);
-  rc = fmm_matvec_elastic(ctx, t, mat->G, mat->nu, D, false, nullptr, t->y_sorted, mode, s);
+  const int ncomp = mat->kind == 1 ? 3 : 2;
+  if (ctx->world == 1) return fmm_matvec(ctx, t, mat, elapsed, D, false, y, nullptr, mode, s);
+  rc = fmm_matvec(ctx, t, mat, elapsed, D, false, nullptr, t->y_sorted, mode, s);
   if (rc) return rc;
-  {
-    stage_begin(ctx, DDM_ST_COMM, s);
-    rc = allgather_sorted(ctx, t, t->y_sorted, 2, s);
-    if (rc) return rc;
-    stage_end(ctx, DDM_ST_COMM, s);
-    scatter_user<<<nblk(t->n, 256), 256, 0, s>>>(t->n, 2, t->perm, t->y_sorted, y);
-    DDM_CUDA(ctx, cudaGetLastError());
-  }
+  stage_begin(ctx, DDM_ST_COMM, s);
+  rc = allgather_sorted(ctx, t, t->y_sorted, ncomp, s);
+  if (rc) return rc;
+  stage_end(ctx, DDM_ST_COMM, s);
+  scatter_user<<<nblk(t->n, 256), 256, 0, s>>>(t->n, ncomp, t->perm, t->y_sorted, y);
+  DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;
 }
 
+// E_j = D^(h+1-j) - D^(h-j) with D^h = D^(-1) = 0   (telescoped lag kernels)
+__global__ void lag_difference(int64_t len, int h, int j, const double* __restrict__ Dh,
+                               double* __restrict__ E) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  const int a = h + 1 - j, b = h - j;
+  const double va = (a >= 0 && a < h) ? Dh[(int64_t)a * len + i] : 0.0;
+  const double vb = (b >= 0 && b < h) ? Dh[(int64_t)b * len + i] : 0.0;
+  E[i] = va - vb;
+}
+
+__global__ void axpy_kernel(int64_t len, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < len) y[i] += x[i];
+}
+
+// r = sum_{m=1}^{h} [K((m+1) dt) - K(m dt)] D^(h-m)
+//   = sum_{j=1}^{h+1} K(j dt) (D^(h+1-j) - D^(h-j))   (D^h = D^(-1) = 0)
+// i.e. h+1 continuous-source matvecs, each with its own elapsed time.
 int ddm_history_apply(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double dt, int h,
                       const double* D_hist, double* r, int mode, void* stream) {
   if (!ctx || !t || !r) return ctx ? set_error(ctx, DDM_ERR_ARG, "NULL argument") : DDM_ERR_ARG;
   int rc = check_material(ctx, mat);
   if (rc) return rc;
   if (h < 0 || !(dt > 0)) return set_error(ctx, DDM_ERR_ARG, "need h >= 0 and dt > 0");
+  if (mode != DDM_FMM && mode != DDM_DIRECT) return set_error(ctx, DDM_ERR_ARG, "bad mode");
   cudaStream_t s = (cudaStream_t)stream;
-  if (h == 0 || mat->kind == 0) {
-    // empty sum / elastic lag kernels vanish identically (R10)
-    DDM_CUDA(ctx, cudaMemsetAsync(r, 0, (size_t)t->n * 3 * sizeof(double), s));
-    return DDM_OK;
+  const int64_t len = t->n * 3;
+  DDM_CUDA(ctx, cudaMemsetAsync(r, 0, (size_t)len * sizeof(double), s));
+  if (h == 0 || mat->kind == 0) return DDM_OK;   // empty sum / elastic (R10)
+  if (!D_hist) return set_error(ctx, DDM_ERR_ARG, "NULL D_hist");
+  double* E = nullptr;
+  double* y = nullptr;
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&E, len * sizeof(double), s));
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&y, len * sizeof(double), s));
+  for (int j = 1; j <= h + 1 && !rc; ++j) {
+    lag_difference<<<nblk(len, 256), 256, 0, s>>>(len, h, j, D_hist, E);
+    rc = cuda_error_if(ctx, cudaGetLastError(), "lag_difference");
+    if (!rc) rc = ddm_matvec(ctx, t, mat, j * dt, E, y, mode, stream);
+    if (!rc) {
+      axpy_kernel<<<nblk(len, 256), 256, 0, s>>>(len, y, r);
+      rc = cuda_error_if(ctx, cudaGetLastError(), "axpy");
+    }
   }
-  (void)D_hist;
-  (void)mode;
-  return set_error(ctx, DDM_ERR_ARG, "poroelastic history not available in this build");
+  cudaFreeAsync(E, s);
+  cudaFreeAsync(y, s);
+  return rc;
 }
 
 int ddm_gmres_solve(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double dt,
@@ -436,8 +472,8 @@ int ddm_gmres_solve(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double
   if (rc) return rc;
   if (!(tol > 0) || restart < 1 || max_iter < 0)
     return set_error(ctx, DDM_ERR_ARG, "need tol > 0, restart >= 1, max_iter >= 0");
-  if (mat->kind != 0)
-    return set_error(ctx, DDM_ERR_ARG, "poroelastic GMRES not available in this build");
+  if (mat->kind == 1 && !(dt > 0))
+    return set_error(ctx, DDM_ERR_ARG, "poroelastic GMRES needs dt > 0");
   return gmres_solve(ctx, t, mat, dt, b, x, tol, restart, max_iter, mode, iters, rel_resid,
                      (cudaStream_t)stream);
 }

@@ -69,6 +69,7 @@ struct ddm_tree_s {
   int64_t nv = 0, nu = 0, near_pairs = 0;
   int nitems = 0;
   double x_min = 0, y_min = 0, W = 1;
+  double a_max = 0;              // largest element half-length
   std::vector<int> level_off;    // [nlevels+1] first cell of each level
   // owned part (multi-GPU): contiguous sorted element range and leaf range
   int own_leaf_lo = 0, own_leaf_hi = 0;
@@ -150,6 +151,7 @@ namespace ddm {
 // error helpers (api.cu)
 int set_error(ddm_ctx_s* ctx, int code, const std::string& msg);
 int cuda_error(ddm_ctx_s* ctx, cudaError_t e, const char* what);
+int cuda_error_if(ddm_ctx_s* ctx, cudaError_t e, const char* what);
 
 #define DDM_CUDA(ctx, call)                                             \
   do {                                                                  \
@@ -187,11 +189,12 @@ void split_costs(const int64_t* prefix_excl, int64_t total, int nleaves, int wor
 
 // fmm.cu
 int fmm_init_operators(ddm_tree_s* t, cudaStream_t s);
-// D: [n][2], user order (d_sorted = false) or sorted order (true), full length.
-// Writes the owned rows into y_user (user order, via perm) and/or y_sorted.
-int fmm_matvec_elastic(ddm_ctx_s* ctx, ddm_tree_s* t, double G, double nu, const double* D,
-                       bool d_sorted, double* y_user, double* y_sorted, int mode,
-                       cudaStream_t s);
+// D: [n][ncomp], user order (d_sorted = false) or sorted order (true), full
+// length.  Writes the owned rows into y_user (user order, via perm) and/or
+// y_sorted.  ncomp = 2 (elastic) or 3 (poroelastic, elapsed = tau).
+int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double elapsed,
+               const double* D, bool d_sorted, double* y_user, double* y_sorted, int mode,
+               cudaStream_t s);
 
 // gmres.cu
 int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt,

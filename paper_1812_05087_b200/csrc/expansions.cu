@@ -79,7 +79,7 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
                          const double* __restrict__ ex, const double* __restrict__ ey,
                          const double* __restrict__ ea, const double* __restrict__ ec,
                          const double* __restrict__ es, double2* __restrict__ mpole, double2* buf,
-                         int lane) {
+                         int lane, const PoroFar& pf) {
   constexpr int NCH = (pmax<PT>() + 7) / 8;
   const int nchunk = (p + 7) / 8;
   const int lev = c_level[c];
@@ -96,6 +96,10 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
     const int i = e0 + r0 + lane;
     const bool valid = r0 + lane < ne;
     double2 B = make_double2(0, 0), Q = B, rr = B, A = B, z1 = B, z2 = B;
+    // poroelastic far field: B-part of Phi and Psi~ scaled by
+    // fu, plus Wm conj(e) I2 and Wc B I4 in Psi~ (iGC factored out)
+    double2 Wme = make_double2(0, 0), Bc = Wme;
+    double fu = 1.0;
     if (valid) {
       const int j = perm ? perm[i] : i;
       const double ds = D[(int64_t)j * ncomp], dn = D[(int64_t)j * ncomp + 1];
@@ -107,10 +111,20 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
       A = csub(cconj(d), cmul(rr, d));
       z1 = make_double2(d.x - a * cb * is, d.y - a * sb * is);
       z2 = make_double2(d.x + a * cb * is, d.y + a * sb * is);
+      if (pf.on) {
+        const double qf = -D[(int64_t)j * ncomp + 2];          // J: q_formula = -q_ABI
+        const double mu = -(pf.eta / pf.S) * dn;
+        const double wm = (pf.eta * mu / M_PI + pf.eta * qf * pf.ct / (M_PI * pf.kappa)) / pf.gc;
+        // (wm / i) conj(e) / s, and 48 eta k_p c tau B / s^3
+        Wme = cscale(cmul(make_double2(0.0, -wm), make_double2(cb, -sb)), is);
+        Bc = cscale(B, 48.0 * pf.eta * pf.kp * pf.ct * is * is * is);
+        fu = pf.fu;
+      }
       B = cscale(B, is);
       Q = cscale(Q, is);
     }
     double2 pw1 = make_double2(1.0, 0.0), pw2 = pw1;
+    double2 Pm2 = make_double2(0.0, 0.0);   // P_{n-3}
     double2 Pm1 = make_double2(0.0, 0.0);   // P_{n-2}
     double2 Pm = make_double2(0.0, 0.0);    // P_{n-1}
     const int rows = min(32, ne - r0);
@@ -125,14 +139,19 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
             if (n >= 2) {
               pw1 = cmul(pw1, z1);
               pw2 = cmul(pw2, z2);
+              Pm2 = Pm1;
               Pm1 = Pm;
               Pm = csub(pw2, pw1);
             }
-            alpha = cmul(B, Pm);
+            alpha = cscale(cmul(B, Pm), fu);
             gam = cmul(Q, Pm);
             double2 tt = cscale(cmul(A, Pm1), (double)(n - 1));
             cmac(tt, cscale(rr, (double)(n - 2)), Pm);
-            cmac(gam, B, tt);
+            cmac(gam, cscale(B, fu), tt);
+            if (pf.on) {
+              cmac(gam, Wme, Pm);
+              if (n >= 4) cmac(gam, cscale(Bc, (n - 1) * (n - 2) / 6.0), Pm2);
+            }
           }
           buf[lane * 17 + j] = alpha;
           buf[lane * 17 + 8 + j] = gam;
@@ -233,7 +252,7 @@ upward_kernel(int nleaves, int nm2m, const int* __restrict__ leaves,
               const double* __restrict__ ea, const double* __restrict__ ec,
               const double* __restrict__ es, const double2* __restrict__ opT,
               double2* __restrict__ mpole, int* __restrict__ ready, int epoch,
-              int* __restrict__ ticket) {
+              int* __restrict__ ticket, PoroFar pf) {
   const int p = PT ? PT : p_rt;
   extern __shared__ double2 up_sh[];
   double2* ops = up_sh;                                      // [4][p][p] as [q][n][m]
@@ -251,7 +270,7 @@ upward_kernel(int nleaves, int nm2m, const int* __restrict__ leaves,
     if (t < nleaves) {
       c = leaves[t];
       p2m_cell<PT>(c, p, c_level, c_ix, c_iy, c_start, c_count, cg, perm, D, ncomp, ex, ey, ea,
-                   ec, es, mpole, wb, lane);
+                   ec, es, mpole, wb, lane, pf);
     } else {
       c = up_list[t - nleaves];
       m2m_cell<PT>(c, p, c_ix, c_iy, first_child, nchild, ops, mpole, wb, wb + 4 * p, ready,
@@ -444,9 +463,9 @@ __global__ void finalize_kernel(int64_t e_lo, int64_t e_hi, int ncomp,
                                 const int* __restrict__ c_level, const int* __restrict__ c_ix,
                                 const int* __restrict__ c_iy, const int* __restrict__ c_start,
                                 const int* __restrict__ c_count,
-                                const int* __restrict__ item_off, const double2* __restrict__ part,
+                                const int* __restrict__ item_off, const double* __restrict__ part,
                                 const double2* __restrict__ local, CellGeom cg, int p_rt,
-                                double gc, const double* __restrict__ ex,
+                                double gc, PoroFar pf, const double* __restrict__ ex,
                                 const double* __restrict__ ey, const double* __restrict__ ec,
                                 const double* __restrict__ es, const int* __restrict__ perm,
                                 double* __restrict__ y_user, double* __restrict__ y_sorted) {
@@ -461,7 +480,13 @@ __global__ void finalize_kernel(int64_t e_lo, int64_t e_hi, int ncomp,
   const int nch = (item_off[k + 1] - i0) / ngroups;
   const int g = slot / kTgtGroup, ln = slot % kTgtGroup;
   double2 T = make_double2(0.0, 0.0);
-  for (int h = 0; h < nch; ++h) T = cadd(T, part[(int64_t)(i0 + g * nch + h) * kTgtGroup + ln]);
+  double pr = 0.0;
+  for (int h = 0; h < nch; ++h) {
+    const double* pp = part + ((int64_t)(i0 + g * nch + h) * kTgtGroup + ln) * ncomp;
+    T.x += pp[0];
+    T.y += pp[1];
+    if (ncomp == 3) pr += pp[2];
+  }
   const int lev = c_level[c];
   if (lev >= 2) {
     const double s = cg.side(lev);
@@ -484,15 +509,19 @@ __global__ void finalize_kernel(int64_t e_lo, int64_t e_hi, int ncomp,
     const double2 t2 = cmul(e2, W);
     T.x += t2.y;
     T.y += t2.x - 2.0 * gc * phi.y;
+    // far pore pressure p = -4 k_p Re(i G C Phi)/fu (formula sign), ABI p = -that
+    if (pf.on) pr -= 4.0 * pf.kp * gc * phi.y / pf.fu;
   }
   if (y_sorted) {
     y_sorted[i * ncomp + 0] = T.x;
     y_sorted[i * ncomp + 1] = T.y;
+    if (ncomp == 3) y_sorted[i * ncomp + 2] = pr;
   }
   if (y_user) {
     const int j = perm[i];
     y_user[(int64_t)j * ncomp + 0] = T.x;
     y_user[(int64_t)j * ncomp + 1] = T.y;
+    if (ncomp == 3) y_user[(int64_t)j * ncomp + 2] = pr;
   }
 }
 
@@ -526,7 +555,7 @@ int pass_grid(ddm_ctx_s* ctx, const void* kernel, size_t shm, int work) {
 
 // upward pass: P2M on all leaves + M2M of every non-leaf cell of level >= 2
 int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
-                  cudaStream_t s) {
+                  const PoroFar& pf, cudaStream_t s) {
   const int p = t->p;
   const CellGeom cg{t->x_min, t->y_min, t->W};
   const size_t wsz = std::max(32 * 17, 8 * p);
@@ -541,7 +570,7 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
     upward_kernel<PT><<<nb, kPassWarps * 32, shm, s>>>(                                         \
         t->nleaves, t->n_up, t->leaves, t->up_list, t->c_level, t->c_ix, t->c_iy, t->c_start,   \
         t->c_count, t->c_first_child, t->c_nchild, cg, p, perm_in, D, ncomp, t->ex, t->ey,      \
-        t->ea, t->ec, t->es, t->op_m2m, t->mpole, t->ready_up, t->epoch, t->tickets);           \
+        t->ea, t->ec, t->es, t->op_m2m, t->mpole, t->ready_up, t->epoch, t->tickets, pf);       \
   } while (0)
   DDM_P_DISPATCH(p, DDM_L);
 #undef DDM_L
@@ -574,15 +603,16 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
 }
 
 int launch_finalize(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, int ncomp, double gc,
-                    double* y_user, double* y_sorted, cudaStream_t s) {
+                    const PoroFar& pf, double* y_user, double* y_sorted, cudaStream_t s) {
   if (hi <= lo) return DDM_OK;
   const CellGeom cg{t->x_min, t->y_min, t->W};
   const unsigned nb = nblk(hi - lo, 128);
 #define DDM_L(PT)                                                                               \
   finalize_kernel<PT><<<nb, 128, 0, s>>>(lo, hi, ncomp, t->el_leaf, t->leaves, t->c_level,      \
                                          t->c_ix, t->c_iy, t->c_start, t->c_count, t->item_off, \
-                                         t->part, t->local, cg, t->p, gc, t->ex, t->ey, t->ec,  \
-                                         t->es, t->perm, y_user, y_sorted)
+                                         reinterpret_cast<const double*>(t->part), t->local, cg, \
+                                         t->p, gc, pf, t->ex, t->ey, t->ec, t->es, t->perm,     \
+                                         y_user, y_sorted)
   DDM_P_DISPATCH(t->p, DDM_L);
 #undef DDM_L
   DDM_CUDA(ctx, cudaGetLastError());

@@ -27,7 +27,7 @@ int ensure_workspace(ddm_ctx_s* ctx, ddm_tree_s* t) {
     if ((rc = dalloc(ctx, &t->mpole, (size_t)t->ncells * 2 * t->p))) return rc;
     if ((rc = dalloc(ctx, &t->local, (size_t)t->ncells * 2 * t->p))) return rc;
     if ((rc = dalloc(ctx, &t->src, (size_t)t->n * kSrcStride))) return rc;
-    if ((rc = dalloc(ctx, &t->part, (size_t)t->nitems * kTgtGroup))) return rc;
+    if ((rc = dalloc(ctx, &t->part, (size_t)t->nitems * kTgtGroup * 2))) return rc;  // <= 4 doubles/slot
     if ((rc = dalloc(ctx, &t->d_sorted, (size_t)t->n * 3))) return rc;
     if ((rc = dalloc(ctx, &t->y_sorted, (size_t)t->n * 3))) return rc;
   }
@@ -125,26 +125,48 @@ int fmm_init_operators(ddm_tree_s* t, cudaStream_t s) {
   return DDM_OK;
 }
 
-// Elastic matvec.  D: [n][2], user order (d_sorted = false) or sorted order,
-// full length on every rank.  Writes the owned rows into y_user (user order)
+// Matvec y = A(elapsed) D.  D: [n][ncomp], user order
+// (d_sorted = false) or sorted order, full length on every rank; ncomp = 2
+// elastic, 3 poroelastic.  Writes the owned rows into y_user (user order)
 // and/or y_sorted (sorted order).
-int fmm_matvec_elastic(ddm_ctx_s* ctx, ddm_tree_s* t, double G, double nu, const double* D,
-                       bool d_sorted, double* y_user, double* y_sorted, int mode,
-                       cudaStream_t s) {
+int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double elapsed,
+               const double* D, bool d_sorted, double* y_user, double* y_sorted, int mode,
+               cudaStream_t s) {
   int rc = ensure_workspace(ctx, t);
   if (rc) return rc;
-  const int ncomp = 2;
-  const double gc = G / (4.0 * M_PI * (1.0 - nu));
+  const bool poro = mat->kind == 1;
+  const int ncomp = poro ? 3 : 2;
+  const double gc = mat->G / (4.0 * M_PI * (1.0 - mat->nu));
   const int64_t lo = t->own_el_lo, hi = t->own_el_hi;
   const int* perm_in = d_sorted ? nullptr : t->perm;
+  PoroParams PP;
+  PoroFar pf;
+  if (poro) {
+    if (!(elapsed > 0)) return set_error(ctx, DDM_ERR_ARG, "poroelastic matvec needs elapsed > 0");
+    PP = poro_params(mat, elapsed);
+    pf = poro_far(PP);
+    if (mode == DDM_FMM && t->nlevels > 2) {
+      // the far field is the r >> sqrt(c tau) form: every V pair must be
+      // separated by more than R_c = sqrt(160 c tau) (u > 40)
+      const double smin = std::ldexp(t->W, -(t->nlevels - 1));
+      const double sep = smin - 2.0 * t->a_max;
+      if (sep <= 0 || sep * sep / (4.0 * PP.ct) <= 40.0)
+        return set_error(ctx, DDM_ERR_ARG,
+                         "tree too fine for the poroelastic far field at this elapsed time: build "
+                         "it with min_leaf_side >= sqrt(160 c tau) + 2 max(a)");
+    }
+  }
 
   stage_begin(ctx, DDM_ST_PREP, s);
-  if ((rc = launch_prep_sources(ctx, t, perm_in, D, ncomp, s))) return rc;
+  rc = poro ? launch_poro_prep(ctx, t, perm_in, D, s)
+            : launch_prep_sources(ctx, t, perm_in, D, ncomp, s);
+  if (rc) return rc;
   stage_end(ctx, DDM_ST_PREP, s);
 
   if (mode == DDM_DIRECT) {
     stage_begin(ctx, DDM_ST_P2P, s);
-    rc = launch_direct(ctx, t, lo, hi, ncomp, gc, y_user, y_sorted, s);
+    rc = poro ? launch_poro_direct(ctx, t, lo, hi, PP, y_user, y_sorted, s)
+              : launch_direct(ctx, t, lo, hi, ncomp, gc, y_user, y_sorted, s);
     stage_end(ctx, DDM_ST_P2P, s);
     return rc;
   }
@@ -159,14 +181,16 @@ int fmm_matvec_elastic(ddm_ctx_s* ctx, ddm_tree_s* t, double G, double nu, const
 
   // near field: P2P work items of the owned leaves
   stage_begin(ctx, DDM_ST_P2P, sn);
-  if ((rc = launch_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, gc, sn))) return rc;
+  rc = poro ? launch_poro_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, PP, sn)
+            : launch_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, gc, sn);
+  if (rc) return rc;
   stage_end(ctx, DDM_ST_P2P, sn);
   DDM_CUDA(ctx, cudaEventRecord(ctx->ev_near, sn));
 
   // upward pass (one persistent launch): P2M on all leaves + M2M finest ->
   // level 2, replicated on all ranks.  Stage "p2m" times the whole upward pass.
   stage_begin(ctx, DDM_ST_P2M, sf);
-  if ((rc = launch_upward(ctx, t, perm_in, D, ncomp, sf))) return rc;
+  if ((rc = launch_upward(ctx, t, perm_in, D, ncomp, pf, sf))) return rc;
   stage_end(ctx, DDM_ST_P2M, sf);
 
   // downward pass (one persistent launch): M2L + L2L of every cell of level
@@ -180,7 +204,7 @@ int fmm_matvec_elastic(ddm_ctx_s* ctx, ddm_tree_s* t, double G, double nu, const
   DDM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_near, 0));
   DDM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_far, 0));
   stage_begin(ctx, DDM_ST_FINAL, s);
-  rc = launch_finalize(ctx, t, lo, hi, ncomp, gc, y_user, y_sorted, s);
+  rc = launch_finalize(ctx, t, lo, hi, ncomp, gc, pf, y_user, y_sorted, s);
   stage_end(ctx, DDM_ST_FINAL, s);
   return rc;
 }

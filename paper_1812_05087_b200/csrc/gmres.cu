@@ -133,8 +133,7 @@ struct Gm {
 int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt,
                 const double* b_user, double* x_user, double tol, int restart, int max_iter,
                 int mode, int* iters_out, double* rel_out, cudaStream_t s) {
-  (void)dt;
-  const int ncomp = 2;
+  const int ncomp = mat->kind == 1 ? 3 : 2;
   const int64_t n = t->n;
   const int64_t nfull = n * ncomp;
   const int64_t lo = t->own_el_lo * ncomp;
@@ -174,7 +173,7 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   DDM_CUDA(ctx, cudaGetLastError());
 
   auto apply = [&](const double* vfull) -> int {
-    return fmm_matvec_elastic(ctx, t, mat->G, mat->nu, vfull, true, nullptr, wf, mode, s);
+    return fmm_matvec(ctx, t, mat, dt, vfull, true, nullptr, wf, mode, s);
   };
   std::vector<double> hh(2 * (m + 1) + 1);
   auto fetch = [&](int cnt) -> int {

@@ -52,12 +52,43 @@ struct CellGeom {
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// Biot constants of a poroelastic material at elapsed time tau (poro.cu)
+struct PoroParams {
+  double G = 0, C = 0, eta = 0, kp = 0, S = 0, kappa = 0, c = 0, ct = 0;
+};
+PoroParams poro_params(const ddm_material* m, double tau);
+int poro_init_tables(ddm_ctx_s* ctx);
+
+// far-field (expansion) weights of the poroelastic kernel, r >> sqrt(c tau)
+// (DESIGN.md §4.13): Phi scaled by fu = 1 + 2 eta k_p = (1-nu)/(1-nu_u); Psi~
+// gains the monopole / fluid-source I2 terms and the c tau I4 term; L2P reads
+// p = -4 k_p Re(Phi_total)/fu (formula sign; ABI p = -that).
+struct PoroFar {
+  int on = 0;
+  double fu = 1.0, eta = 0, kp = 0, S = 0, kappa = 0, ct = 0, gc = 1.0;
+};
+inline PoroFar poro_far(const PoroParams& P) {
+  PoroFar f;
+  f.on = 1;
+  f.fu = 1.0 + 2.0 * P.eta * P.kp;
+  f.eta = P.eta; f.kp = P.kp; f.S = P.S; f.kappa = P.kappa; f.ct = P.ct; f.gc = P.G * P.C;
+  return f;
+}
+
+int launch_poro_prep(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D,
+                     cudaStream_t s);
+int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, const PoroParams& P,
+                    cudaStream_t s);
+int launch_poro_direct(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi,
+                       const PoroParams& P, double* y_user, double* y_sorted, cudaStream_t s);
+
 // ---- launchers (expansions.cu): upward / downward passes
+struct PoroFar;
 int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
-                  cudaStream_t s);
+                  const PoroFar& pf, cudaStream_t s);
 int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
 int launch_finalize(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, int ncomp, double gc,
-                    double* y_user, double* y_sorted, cudaStream_t s);
+                    const PoroFar& pf, double* y_user, double* y_sorted, cudaStream_t s);
 
 // ---- launchers (p2p.cu): near field
 int launch_prep_sources(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D,

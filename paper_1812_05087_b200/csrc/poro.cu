@@ -1,0 +1,476 @@
+// Fully coupled poroelastic continuous-source kernel on the GPU (DESIGN.md
+// §4.13; PAPER.md Eq.(int_sigs)-(int_pp) P:319-375, Eq.(final_sigs)-(final_pp)
+// P:389-449).  Plane strain Biot theory, tension-positive stress, CS-convention
+// DDs, physical pore pressure; the ABI sign map J = diag(1, 1, -1) is applied
+// at the boundary of this file (source q and output p negated).
+//
+// Element influence = drained Kolosov–Muskhelishvili (closed form, nu)
+//   + sigma^p = 2 eta (Phi_,ij - p delta_ij) and p, integrated along the
+//     element with the fixed rule: panels graded away from the nearest point
+//     (each <= max(r, sqrt(c tau)) / 4), 8-point Gauss–Legendre per panel,
+//     E1 log singularity removed analytically when the target is on the
+//     element; analytic far form when u_min = dist^2 / (4 c tau) > 40.
+// Point kernels (per unit length, omega = w/|w|, u = |w|^2/(4 c tau)):
+//   p       = Re(K ob^2) f2(u)/(4 c tau) + mu e^-u/(4 pi c tau) + q E1(u)/(4 pi kappa)
+//   d2Phi   = K ob^4 g2(u)/(4 c tau) - e^-u Re(K ob^2) ob^2/(16 c tau)
+//             - mu f2(u) ob^2/(16 pi c tau) - q h2(u) ob^2/(16 pi kappa)
+//   K = -4 k_p i G C B e, B = (Ds + i Dn) e, mu = -(eta/S) Dn
+//   T^p = sigma_n + i sigma_s = -eta p + e^{2 i bt} (-4 eta d2Phi)
+#include <cmath>
+
+#include "kcommon.cuh"
+
+namespace ddm {
+namespace {
+
+__constant__ double c_gl_x[8];
+__constant__ double c_gl_w[8];
+
+constexpr double kUFar = 40.0;
+constexpr double kPanelFraction = 0.25;
+constexpr double kEulerGamma = 0.57721566490153286061;
+
+struct PoroConst {
+  double G, C, eta, kp, S, kappa, c, ct;   // ct = c tau
+  double gc;                              // G C
+};
+
+// f2 = (1 - (1+u)e^-u)/u, g2 = (-1/4 - e^-u/2 + 3(1-e^-u)/(4u))/u, h2 = (1-e^-u)/u
+// power-series coefficients (powers of u, ascending), filled by poro_init_tables:
+//   f2 = sum_{k>=2} (-1)^k (k-1) u^(k-1)/k!,  g2 = sum_{k>=1} (-1)^k (1-2k) u^(k-1)/(4 (k+1)!),
+//   h2 = sum_{k>=0} (-u)^k/(k+1)!
+constexpr int kNSeries = 25;
+__constant__ double c_f2[kNSeries];
+__constant__ double c_g2[kNSeries];
+__constant__ double c_h2[8];
+
+__device__ __forceinline__ void fgh(double u, double& f2, double& g2, double& h2, double& eu) {
+  eu = exp(-u);
+  if (u < 1.0) {
+    double sf = 0.0, sg = 0.0;
+#pragma unroll
+    for (int k = kNSeries - 1; k >= 0; --k) {
+      sf = fma(sf, u, c_f2[k]);
+      sg = fma(sg, u, c_g2[k]);
+    }
+    f2 = sf;
+    g2 = sg;
+  } else {
+    f2 = (1.0 - (1.0 + u) * eu) / u;
+    g2 = (-0.25 - 0.5 * eu + 0.75 * (-expm1(-u)) / u) / u;
+  }
+  if (u < 1e-3) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 7; k >= 0; --k) s = fma(s, u, c_h2[k]);
+    h2 = s;
+  } else {
+    h2 = -expm1(-u) / u;
+  }
+}
+
+// Ein(u) = E1(u) + gamma + ln u = sum_{k>=1} (-1)^{k+1} u^k / (k k!)  (u <= 2)
+__device__ double ein_series(double u) {
+  double term = u, sum = 0.0;
+  for (int k = 1; k < 60; ++k) {
+    const double t = term / k;
+    sum += t;
+    if (fabs(t) < 1e-17 * fabs(sum)) break;
+    term *= -u / (k + 1);
+  }
+  return sum;
+}
+
+// E1(u), u > 0: series below 1, modified Lentz continued fraction above
+__device__ double expint_e1(double u) {
+  if (u <= 1.0) return ein_series(u) - kEulerGamma - log(u);
+  // E1(u) = e^-u / (u + 1 - 1/(u + 3 - 4/(u + 5 - ...)))
+  const double tiny = 1e-300;
+  double b = u + 1.0, c = 1.0 / tiny, d = 1.0 / b, h = d;
+  for (int i = 1; i < 200; ++i) {
+    const double an = -(double)i * i;
+    b += 2.0;
+    d = 1.0 / (an * d + b);
+    c = b + an / c;
+    const double del = c * d;
+    h *= del;
+    if (fabs(del - 1.0) < 1e-16) break;
+  }
+  return h * exp(-u);
+}
+
+// point kernel: adds w_q * (p, d2Phi) of the unit-length point source at offset w
+__device__ __forceinline__ void point_add(double wx, double wy, double wq, const PoroConst& k,
+                                          double2 K, double mu, double q, bool q_split,
+                                          double& p_acc, double2& d2_acc) {
+  const double r2 = fma(wx, wx, wy * wy);
+  const double u = r2 / (4.0 * k.ct);
+  const double ir = rsqrt(r2);
+  // ob = conj(omega)
+  const double obx = wx * ir, oby = -wy * ir;
+  const double2 ob2 = make_double2(obx * obx - oby * oby, 2.0 * obx * oby);
+  const double2 ob4 = cmul(ob2, ob2);
+  double f2, g2, h2, eu;
+  fgh(u, f2, g2, h2, eu);
+  const double2 Kob2 = cmul(K, ob2);
+  const double ReK = Kob2.x;
+  double p = ReK * f2 / (4.0 * k.ct) + mu * eu / (4.0 * M_PI * k.ct);
+  const double2 Kob4 = cmul(K, ob4);
+  double2 d2 = make_double2(Kob4.x * g2 / (4.0 * k.ct), Kob4.y * g2 / (4.0 * k.ct));
+  const double cb = eu * ReK / (16.0 * k.ct) + mu * f2 / (16.0 * M_PI * k.ct);
+  d2.x -= cb * ob2.x;
+  d2.y -= cb * ob2.y;
+  if (q != 0.0) {
+    const double e1 = q_split ? (expint_e1(u) + kEulerGamma + log(u)) : expint_e1(u);
+    p += q * e1 / (4.0 * M_PI * k.kappa);
+    const double cq = q * h2 / (16.0 * M_PI * k.kappa);
+    d2.x -= cq * ob2.x;
+    d2.y -= cq * ob2.y;
+  }
+  p_acc = fma(wq, p, p_acc);
+  d2_acc.x = fma(wq, d2.x, d2_acc.x);
+  d2_acc.y = fma(wq, d2.y, d2_acc.y);
+}
+
+// integral of (-gamma - ln(s^2/(4 c tau))) ds over [s0, s1], 0 <= s0 < s1
+__device__ __forceinline__ double e1_log_part(double s0, double s1, double ct) {
+  auto prim = [&](double s) {
+    if (s == 0.0) return 0.0;
+    return -kEulerGamma * s - (2.0 * (s * log(s) - s) - s * log(4.0 * ct));
+  };
+  return prim(s1) - prim(s0);
+}
+
+}  // namespace
+
+// Poroelastic influence of one source element on one target (tension-positive
+// traction T = sigma_n + i sigma_s and physical p, CS-convention DDs):
+// the sigma^p + p part only (the drained part is added by the caller).
+__device__ void poro_element(double2 zt, double2 zc, double2 e, double a, double Ds, double Dn,
+                             double q, const PoroConst& k, double2 e2t, double2& T, double& p) {
+  const double lt = sqrt(k.ct);
+  const double rx = zt.x - zc.x, ry = zt.y - zc.y;
+  const double sstar = rx * e.x + ry * e.y;          // Re((zt - zc) conj(e))
+  const double dperp = fabs(-rx * e.y + ry * e.x);   // |Im(...)|
+  const double dist = (fabs(sstar) <= a) ? dperp : hypot(dperp, fabs(sstar) - a);
+  const double2 B = make_double2(Ds * e.x - Dn * e.y, Ds * e.y + Dn * e.x);
+  const double mu = -(k.eta / k.S) * Dn;
+  if (dist * dist / (4.0 * k.ct) > kUFar) {
+    // analytic far form: Phi^p = 2 eta k_p Phi^D, Psi^p = 2 eta k_p 2 i G C B Ibar3
+    //   + (eta mu/pi + eta q c tau/(pi kappa)) conj(e) I2 + 48 eta k_p c tau i G C B I4
+    const double2 z1 = make_double2(zc.x - a * e.x, zc.y - a * e.y);
+    const double2 z2 = make_double2(zc.x + a * e.x, zc.y + a * e.y);
+    const double2 w1 = make_double2(zt.x - z1.x, zt.y - z1.y);
+    const double2 w2 = make_double2(zt.x - z2.x, zt.y - z2.y);
+    auto inv = [](double2 w) {
+      const double n = fma(w.x, w.x, w.y * w.y);
+      return make_double2(w.x / n, -w.y / n);
+    };
+    const double2 r1 = inv(w1), r2 = inv(w2);
+    const double2 I2 = csub(r2, r1);
+    const double2 r12 = cmul(r1, r1), r22 = cmul(r2, r2);
+    const double2 I3 = cscale(csub(r22, r12), 0.5);
+    const double2 I4 = cscale(csub(cmul(r22, r2), cmul(r12, r1)), 1.0 / 3.0);
+    const double2 rr = make_double2(e.x * e.x - e.y * e.y, -2.0 * e.x * e.y);   // conj(e)^2
+    const double2 dz = make_double2(zt.x - zc.x, zt.y - zc.y);
+    double2 X = make_double2(zc.x, -zc.y);
+    cmac(X, rr, dz);
+    const double2 I3b = csub(cmul(X, I3), cmul(rr, I2));
+    const double2 iGC = make_double2(0.0, k.gc);
+    const double2 iGCB = cmul(iGC, B);
+    const double ekp = 2.0 * k.eta * k.kp;
+    const double2 PhiD = cmul(iGCB, I2);
+    const double2 Phi = cscale(PhiD, ekp);
+    const double2 dPhi = cscale(cmul(iGCB, I3), -2.0 * ekp);
+    const double wm = k.eta * mu / M_PI + k.eta * q * k.ct / (M_PI * k.kappa);
+    double2 Psi = cscale(cmul(iGCB, I3b), 2.0 * ekp);
+    cmac(Psi, cscale(make_double2(e.x, -e.y), wm), I2);
+    cmac(Psi, cscale(iGCB, 48.0 * k.eta * k.kp * k.ct), I4);
+    double2 Wv = Psi;
+    cmac(Wv, make_double2(zt.x, -zt.y), dPhi);
+    const double2 t2 = cmul(e2t, Wv);
+    T = make_double2(2.0 * Phi.x + t2.x, t2.y);
+    p = -k.kp * 4.0 * PhiD.x;
+    return;
+  }
+  // near rule
+  const double2 K = cscale(cmul(make_double2(0.0, k.gc), cmul(B, e)), -4.0 * k.kp);
+  const bool on_line = (dperp == 0.0) && (fabs(sstar) < a);
+  const double s0c = fmin(fmax(sstar, -a), a);
+  double pacc = 0.0;
+  double2 d2acc = make_double2(0.0, 0.0);
+  for (int side = 0; side < 2; ++side) {
+    const double other = side ? a : -a;
+    const double sign = side ? 1.0 : -1.0;
+    if ((other - s0c) * sign <= 0.0) continue;
+    double s = s0c;
+    int guard = 0;
+    while ((other - s) * sign > 0.0 && guard++ < 4096) {
+      const double r = hypot(dperp, s - sstar);
+      double snext = s + sign * kPanelFraction * fmax(r, lt);
+      if ((other - snext) * sign <= 0.0) snext = other;
+      const double mid = 0.5 * (s + snext), half = 0.5 * fabs(snext - s);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const double sq = mid + half * c_gl_x[g];
+        const double wx = zt.x - (zc.x + sq * e.x), wy = zt.y - (zc.y + sq * e.y);
+        point_add(wx, wy, half * c_gl_w[g], k, K, mu, q, on_line, pacc, d2acc);
+      }
+      s = snext;
+    }
+    if (on_line && q != 0.0) {
+      const double len = fabs(other - sstar);
+      pacc += q * e1_log_part(0.0, len, k.ct) / (4.0 * M_PI * k.kappa);
+    }
+  }
+  p = pacc;
+  const double2 t2 = cmul(e2t, make_double2(-4.0 * k.eta * d2acc.x, -4.0 * k.eta * d2acc.y));
+  T = make_double2(-k.eta * pacc + t2.x, t2.y);
+}
+
+namespace {
+
+// drained elastic KM influence (tension-positive traction T = sigma_n + i sigma_s)
+__device__ __forceinline__ double2 drained_traction(double2 zt, double2 zc, double2 e, double a,
+                                                    double Ds, double Dn, double gc, double2 e2t) {
+  const double2 B = make_double2(Ds * e.x - Dn * e.y, Ds * e.y + Dn * e.x);
+  const double2 rr = make_double2(e.x * e.x - e.y * e.y, -2.0 * e.x * e.y);
+  const double2 Q = csub(cmul(rr, B), make_double2(B.x, -B.y));
+  const double2 z1 = make_double2(zc.x - a * e.x, zc.y - a * e.y);
+  const double2 z2 = make_double2(zc.x + a * e.x, zc.y + a * e.y);
+  const double2 w1 = make_double2(zt.x - z1.x, zt.y - z1.y);
+  const double2 w2 = make_double2(zt.x - z2.x, zt.y - z2.y);
+  const double n1 = fma(w1.x, w1.x, w1.y * w1.y), n2 = fma(w2.x, w2.x, w2.y * w2.y);
+  const double2 r1 = make_double2(w1.x / n1, -w1.y / n1), r2 = make_double2(w2.x / n2, -w2.y / n2);
+  const double2 I2 = csub(r2, r1);
+  const double2 I3 = cscale(csub(cmul(r2, r2), cmul(r1, r1)), 0.5);
+  const double2 dz = make_double2(zt.x - zc.x, zt.y - zc.y);
+  double2 X = make_double2(zc.x, -zc.y);
+  cmac(X, rr, dz);
+  const double2 I3b = csub(cmul(X, I3), cmul(rr, I2));
+  const double2 iGC = make_double2(0.0, gc);
+  const double2 Phi = cmul(iGC, cmul(B, I2));
+  const double2 dPhi = cscale(cmul(iGC, cmul(B, I3)), -2.0);
+  double2 Psi = cmul(Q, I2);
+  cmac(Psi, cscale(B, 2.0), I3b);
+  Psi = cmul(iGC, Psi);
+  double2 Wv = Psi;
+  cmac(Wv, make_double2(zt.x, -zt.y), dPhi);
+  const double2 t2 = cmul(e2t, Wv);
+  return make_double2(2.0 * Phi.x + t2.x, t2.y);
+}
+
+// full 3x3 action of one source (Ds, Dn, q ABI) on one target: adds
+// (sigma_s, sigma_n, p) in ABI convention
+__device__ __forceinline__ void poro_pair(double2 zt, double2 e2t, const double* sp,
+                                          const PoroConst& k, double& os, double& on,
+                                          double& op) {
+  const double2 zc = make_double2(sp[0], sp[1]);
+  const double2 e = make_double2(sp[2], sp[3]);
+  const double a = sp[4];
+  const double Ds = sp[5], Dn = sp[6], q = -sp[7];   // J: q_formula = -q_ABI
+  const double2 Td = drained_traction(zt, zc, e, a, Ds, Dn, k.gc, e2t);
+  double2 Tp;
+  double p;
+  poro_element(zt, zc, e, a, Ds, Dn, q, k, e2t, Tp, p);
+  os += Td.y + Tp.y;
+  on += Td.x + Tp.x;
+  op -= p;                                             // J: p_ABI = -p_formula
+}
+
+constexpr int kPoroStride = 8;   // {zc, e, a, Ds, Dn, q}
+
+__global__ void poro_prep(int64_t n, const int* __restrict__ perm, const double* __restrict__ D,
+                          const double* __restrict__ ex, const double* __restrict__ ey,
+                          const double* __restrict__ ea, const double* __restrict__ ec,
+                          const double* __restrict__ es, double* __restrict__ src) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int j = perm ? perm[i] : (int)i;
+  double* o = src + i * kPoroStride;
+  o[0] = ex[i];
+  o[1] = ey[i];
+  o[2] = ec[i];
+  o[3] = es[i];
+  o[4] = ea[i];
+  o[5] = D[(int64_t)j * 3 + 0];
+  o[6] = D[(int64_t)j * 3 + 1];
+  o[7] = D[(int64_t)j * 3 + 2];
+}
+
+// near field: warp per item (<= kTgtGroup targets); lane = (target, slice)
+__global__ void __launch_bounds__(128)
+poro_p2p_kernel(int item_lo, int item_hi, const int4* __restrict__ items,
+                const int* __restrict__ u_off, const int* __restrict__ u_lo,
+                const int* __restrict__ u_hi, const int* __restrict__ leaves,
+                const int* __restrict__ c_start, const int* __restrict__ c_count,
+                const double* __restrict__ src, const double* __restrict__ ex,
+                const double* __restrict__ ey, const double* __restrict__ ec,
+                const double* __restrict__ es, PoroConst k, double* __restrict__ part3) {
+  __shared__ double red[4][3][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int it = item_lo + blockIdx.x * 4 + w; it < item_hi; it += gridDim.x * 4) {
+    const int4 item = items[it];
+    const int kk = item.x;
+    const int c = leaves[kk];
+    const int nt = min(kTgtGroup, c_start[c] + c_count[c] - item.y);
+    const int S = 32 / nt;
+    const int tl = lane % nt, slice = lane / nt;
+    const bool active = slice < S;
+    const int ti = item.y + tl;
+    const double2 zt = make_double2(ex[ti], ey[ti]);
+    const double ct = ec[ti], st = es[ti];
+    const double2 e2t = make_double2(ct * ct - st * st, 2.0 * ct * st);
+    double os = 0.0, on = 0.0, op = 0.0;
+    if (active) {
+      int pos = 0;
+      for (int r = u_off[kk], rend = u_off[kk + 1]; r < rend && pos < item.w; ++r) {
+        const int lo = u_lo[r], len = u_hi[r] - lo;
+        const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
+        for (int j = b + slice; j < e; j += S)
+          poro_pair(zt, e2t, src + (int64_t)(lo + j) * kPoroStride, k, os, on, op);
+        pos += len;
+      }
+      red[w][0][lane] = os;
+      red[w][1][lane] = on;
+      red[w][2][lane] = op;
+    }
+    __syncwarp();
+    if (lane < kTgtGroup) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      if (lane < nt)
+        for (int q = 0; q < S; ++q) {
+          s0 += red[w][0][lane + q * nt];
+          s1 += red[w][1][lane + q * nt];
+          s2 += red[w][2][lane + q * nt];
+        }
+      double* o = part3 + ((int64_t)it * kTgtGroup + lane) * 3;
+      o[0] = s0;
+      o[1] = s1;
+      o[2] = s2;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void poro_direct_kernel(int64_t n, int64_t t_lo, int64_t t_hi,
+                                   const double* __restrict__ src, const double* __restrict__ ex,
+                                   const double* __restrict__ ey, const double* __restrict__ ec,
+                                   const double* __restrict__ es, PoroConst k,
+                                   const int* __restrict__ perm, double* __restrict__ y_user,
+                                   double* __restrict__ y_sorted) {
+  const int64_t ti = t_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (ti >= t_hi) return;
+  const double2 zt = make_double2(ex[ti], ey[ti]);
+  const double ct = ec[ti], st = es[ti];
+  const double2 e2t = make_double2(ct * ct - st * st, 2.0 * ct * st);
+  double os = 0.0, on = 0.0, op = 0.0;
+  for (int64_t j = 0; j < n; ++j) poro_pair(zt, e2t, src + j * kPoroStride, k, os, on, op);
+  if (y_sorted) {
+    y_sorted[ti * 3] = os;
+    y_sorted[ti * 3 + 1] = on;
+    y_sorted[ti * 3 + 2] = op;
+  }
+  if (y_user) {
+    const int j = perm[ti];
+    y_user[(int64_t)j * 3] = os;
+    y_user[(int64_t)j * 3 + 1] = on;
+    y_user[(int64_t)j * 3 + 2] = op;
+  }
+}
+
+}  // namespace
+
+PoroParams poro_params(const ddm_material* m, double tau) {
+  PoroParams P;
+  const double G = m->G, nu = m->nu, nuu = m->nu_u, al = m->alpha;
+  const double M = 2 * G * (nuu - nu) / (al * al * (1 - 2 * nuu) * (1 - 2 * nu));
+  P.S = al * al * (1 - 2 * nu) / (2 * G * (1 - nu)) + 1.0 / M;
+  P.c = m->kappa / P.S;
+  P.eta = al * (1 - 2 * nu) / (2 * (1 - nu));
+  P.kp = al * (1 - 2 * nu) / (2 * G * P.S);
+  P.kappa = m->kappa;
+  P.G = G;
+  P.C = 1.0 / (4.0 * M_PI * (1.0 - nu));
+  P.ct = P.c * tau;
+  return P;
+}
+
+int poro_init_tables(ddm_ctx_s* ctx) {
+  // 8-point Gauss–Legendre nodes/weights on [-1, 1] by Newton on P_8
+  double x[8], wts[8];
+  const int n = 8;
+  for (int i = 0; i < n; ++i) {
+    double z = cos(M_PI * (i + 0.75) / (n + 0.5)), pp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p1 = 1.0, p2 = 0.0;
+      for (int j = 1; j <= n; ++j) {
+        const double p3 = p2;
+        p2 = p1;
+        p1 = ((2.0 * j - 1.0) * z * p2 - (j - 1.0) * p3) / j;
+      }
+      pp = n * (z * p1 - p2) / (z * z - 1.0);
+      const double z1 = z;
+      z = z1 - p1 / pp;
+      if (fabs(z - z1) < 1e-16) break;
+    }
+    x[i] = z;
+    wts[i] = 2.0 / ((1.0 - z * z) * pp * pp);
+  }
+  DDM_CUDA(ctx, cudaMemcpyToSymbol(c_gl_x, x, sizeof(x)));
+  DDM_CUDA(ctx, cudaMemcpyToSymbol(c_gl_w, wts, sizeof(wts)));
+  double f2[kNSeries] = {}, g2[kNSeries] = {}, h2[8] = {};
+  double fact = 1.0;                       // k!
+  for (int k = 1; k <= kNSeries + 1; ++k) {
+    fact *= k;
+    const double sgn = (k & 1) ? -1.0 : 1.0;
+    if (k >= 2 && k - 1 < kNSeries) f2[k - 1] = sgn * (k - 1) / fact;
+    if (k - 1 < kNSeries) g2[k - 1] = sgn * (1 - 2 * k) / (4.0 * fact * (k + 1));
+  }
+  fact = 1.0;
+  for (int k = 0; k < 8; ++k) {
+    fact *= (k + 1);                       // (k+1)!
+    h2[k] = ((k & 1) ? -1.0 : 1.0) / fact;
+  }
+  DDM_CUDA(ctx, cudaMemcpyToSymbol(c_f2, f2, sizeof(f2)));
+  DDM_CUDA(ctx, cudaMemcpyToSymbol(c_g2, g2, sizeof(g2)));
+  DDM_CUDA(ctx, cudaMemcpyToSymbol(c_h2, h2, sizeof(h2)));
+  return DDM_OK;
+}
+
+static PoroConst to_const(const PoroParams& P) {
+  PoroConst k;
+  k.G = P.G; k.C = P.C; k.eta = P.eta; k.kp = P.kp; k.S = P.S; k.kappa = P.kappa; k.c = P.c;
+  k.ct = P.ct; k.gc = P.G * P.C;
+  return k;
+}
+
+int launch_poro_prep(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D,
+                     cudaStream_t s) {
+  poro_prep<<<nblk(t->n, 256), 256, 0, s>>>(t->n, perm_in, D, t->ex, t->ey, t->ea, t->ec, t->es,
+                                             t->src);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, const PoroParams& P,
+                    cudaStream_t s) {
+  if (item_hi <= item_lo) return DDM_OK;
+  poro_p2p_kernel<<<nblk(item_hi - item_lo, 4), 128, 0, s>>>(
+      item_lo, item_hi, t->items, t->u_off, t->u_lo, t->u_hi, t->leaves, t->c_start, t->c_count,
+      t->src, t->ex, t->ey, t->ec, t->es, to_const(P), reinterpret_cast<double*>(t->part));
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+int launch_poro_direct(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi,
+                       const PoroParams& P, double* y_user, double* y_sorted, cudaStream_t s) {
+  if (hi <= lo) return DDM_OK;
+  poro_direct_kernel<<<nblk(hi - lo, 64), 64, 0, s>>>(t->n, lo, hi, t->src, t->ex, t->ey, t->ec,
+                                                      t->es, to_const(P), t->perm, y_user,
+                                                      y_sorted);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+}  // namespace ddm

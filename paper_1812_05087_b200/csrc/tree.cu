@@ -504,6 +504,16 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
   double W = std::max(xmx - xmn, ymx - ymn);
   if (W == 0.0) W = 1.0;
   const double scale = 1073741824.0 / W;  // 2^30 / W, one IEEE division
+  {
+    std::vector<double> ha(n);
+    DDM_CUDA(ctx, cudaMemcpy(ha.data(), a, n * sizeof(double), cudaMemcpyDeviceToHost));
+    t->a_max = 0.0;
+    for (double v : ha) {
+      if (!(std::isfinite(v) && v > 0))
+        return set_error(ctx, DDM_ERR_GEOM, "element half-lengths must be finite and > 0");
+      t->a_max = std::max(t->a_max, v);
+    }
+  }
   t->x_min = xmn;
   t->y_min = ymn;
   t->W = W;

@@ -1,0 +1,149 @@
+"""GPU poroelastic path vs the oracle: direct matvec,
+FMM matvec, GMRES and the history sum."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import history as OH
+from oracle import poro as OP
+from synth import CONFIGS, make_config, random_dd
+from synth.geometry import Geometry
+
+from ._util import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+MAT = CONFIGS[3]["material"]
+
+
+@pytest.fixture(scope="module")
+def ddm():
+    import torch
+    import paper_1812_05087_b200 as D
+    ctx = D.Context(0)
+    return D, ctx, torch
+
+
+def _rc(tau, g):
+    k = OP.constants(MAT["G"], MAT["nu"], MAT["nu_u"], MAT["alpha"], MAT["kappa"])
+    return math.sqrt(160 * k["c"] * tau) + 2 * g.half_len.max()
+
+
+def _tree(D, ctx, torch, g, leaf=32, p=20, min_side=0.0):
+    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+    return D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=leaf, order_p=p,
+                  min_leaf_side=min_side)
+
+
+def _mv(D, ctx, torch, tree, Dv, mode, tau):
+    mat = D.material_from_dict(MAT)
+    y = D.matvec(ctx, tree, mat, torch.tensor(Dv, device="cuda"), mode=mode, elapsed=tau)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+_dense = {}
+
+
+def _A(cfg, tau):
+    key = (cfg, tau)
+    if key not in _dense:
+        _dense[key] = OP.assemble_dense(make_config(cfg), MAT, tau)
+    return _dense[key]
+
+
+def test_poro_direct_parity_cfg4(ddm):
+    D, ctx, torch = ddm
+    g = make_config(4)
+    tau = CONFIGS[4]["dt"]
+    tree = _tree(D, ctx, torch, g)
+    Dv = random_dd(g.n, 3, 104)
+    Dv[:, 2] *= 1e-9          # fluid-source rates (m^2/s per m) of a plausible size
+    y = _mv(D, ctx, torch, tree, Dv, "direct", tau)
+    ref = (_A(4, tau) @ Dv.reshape(-1)).reshape(-1, 3)
+    for c in range(3):        # each row block on its own scale
+        assert rel_l2(y[:, c], ref[:, c]) <= 1e-12, c
+
+
+def test_poro_fmm_parity_cfg4(ddm):
+    D, ctx, torch = ddm
+    g = make_config(4)
+    tau = CONFIGS[4]["dt"]
+    tree = _tree(D, ctx, torch, g, p=28, min_side=_rc(tau, g))
+    Dv = random_dd(g.n, 3, 104)
+    Dv[:, 2] *= 1e-9
+    y = _mv(D, ctx, torch, tree, Dv, "fmm", tau)
+    ref = (_A(4, tau) @ Dv.reshape(-1)).reshape(-1, 3)
+    for c in range(3):
+        assert rel_l2(y[:, c], ref[:, c]) <= 1e-8, c
+
+
+def test_poro_fmm_rejects_too_fine_tree(ddm):
+    D, ctx, torch = ddm
+    g = make_config(4)
+    tree = _tree(D, ctx, torch, g, leaf=4)
+    Dv = random_dd(g.n, 3, 1)
+    with pytest.raises(D.DDMError):
+        _mv(D, ctx, torch, tree, Dv, "fmm", 1e4)
+    with pytest.raises(D.DDMError):
+        _mv(D, ctx, torch, tree, Dv, "direct", 0.0)
+
+
+def test_poro_sampled_rows_cfg3(ddm):
+    # full-size config 3 (N = 20000, 3 unknowns per element) on sampled rows
+    D, ctx, torch = ddm
+    g = make_config(3)
+    tau = CONFIGS[3]["dt"]
+    tree = _tree(D, ctx, torch, g, p=CONFIGS[3]["p_star"], min_side=_rc(tau, g))
+    Dv = random_dd(g.n, 3, 103)
+    Dv[:, 2] *= 1e-9
+    y = _mv(D, ctx, torch, tree, Dv, "fmm", tau)
+    rows = np.random.default_rng(3).choice(g.n, 12, replace=False)
+    ref = OP.matvec_rows(g, MAT, tau, Dv, rows)
+    for c in range(3):
+        assert rel_l2(y[rows, c], ref[:, c]) <= 1e-8, c
+
+
+def test_poro_gmres_cfg4(ddm):
+    D, ctx, torch = ddm
+    g = make_config(4)
+    c = CONFIGS[4]
+    tau = c["dt"]
+    ld = c["load"]
+    tree = _tree(D, ctx, torch, g, p=28, min_side=_rc(tau, g))
+    mat = D.material_from_dict(MAT)
+    beta = torch.tensor(g.beta, device="cuda")
+    b = D.farfield_rhs(ctx, beta, 3, ld["p_f"], ld["sH"], ld["sh"], net=False,
+                       b_p=ld["p_f"] - ld["p0"])
+    bref = OH.poro_rhs(g, ld)
+    assert rel_l2(b.cpu().numpy(), bref) <= 1e-15
+    x, it, rr = D.gmres_solve(ctx, tree, mat, b, dt=tau, tol=1e-10, restart=2000, max_iter=6000)
+    x_lu = np.linalg.solve(_A(4, tau), bref.reshape(-1)).reshape(-1, 3)
+    xs = x.cpu().numpy()
+    assert rr <= 1e-10
+    for comp in range(3):
+        assert rel_l2(xs[:, comp], x_lu[:, comp]) <= 1e-6, comp
+
+
+def test_poro_history_small(ddm):
+    D, ctx, torch = ddm
+    rng = np.random.default_rng(9)
+    n = 24
+    t = np.linspace(0, 1, n + 1)
+    xc = 0.5 * (t[1:] + t[:-1]) * 3.0
+    g = Geometry(np.concatenate([xc[:12], xc[:12] + 0.1]), np.concatenate([0 * xc[:12], 0.4 + 0 * xc[:12]]),
+                 np.full(n, 0.0625), np.zeros(n), np.repeat([0, 1], 12), np.array([[0, 11], [12, 23]]))
+    dt = 60.0
+    h = 3
+    Dh = rng.uniform(-1e-3, 1e-3, (h, n, 3))
+    Dh[:, :, 2] *= 1e-9
+    mat = dict(MAT, kind=1)
+    ref = OH.history_sum(g, mat, dt, Dh)
+    tree = _tree(D, ctx, torch, g, leaf=4)
+    r = D.history_apply(ctx, tree, D.material_from_dict(MAT), dt,
+                        torch.tensor(Dh, device="cuda"), mode="direct")
+    torch.cuda.synchronize()
+    r = r.cpu().numpy()
+    for c in range(3):
+        assert rel_l2(r[:, c], ref[:, c]) <= 1e-11, c
