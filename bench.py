@@ -220,7 +220,9 @@ def run_ours(args):
     e2e_value = args.steps * float(n) * float(n) / (e2e_ms * 1e-3)
 
     # ---- per-stage CUDA events (separate instrumented run) for the roofline
-    ctx.set_profiling(True)
+    # serial schedule: every stage's events bracket that stage's kernels alone
+    # (in the timed step the near field overlaps the far-field chain)
+    ctx.set_profiling(True, serial=True)
     stages = {k: 0.0 for k in ("prep", "p2m", "m2m", "m2l", "l2l", "p2p", "final", "comm")}
     nprof = max(3, min(args.steps, 10))
     for _ in range(nprof):
@@ -255,10 +257,15 @@ def run_ours(args):
            "roofline": {"bound": "alu", "kernel": "p2p_kernel (fp64 pipe)",
                         "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                         "frac": achieved / fp64_peak if fp64_peak else None,
-                        "traffic": None,
+                        "traffic": _ncu_traffic("p2p_kernel"),
+                        "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one "
+                                          "ncu --set full capture (profiles/ncu_traffic.json)",
                         "peak_source": "measured DFMA-chain probe (ddm_probe_fp64) on this GPU",
                         "flop_per_pair": FLOP_PER_PAIR,
-                        "p2p_share_of_step": p2p_ms / ms_per_step},
+                        "kernel_ms": p2p_ms,
+                        "kernel_ms_source": "CUDA events on the launching stream, serial "
+                                            "instrumented matvecs after the timed region",
+                        "p2p_share_of_serial_step": p2p_ms / sum(stages.values())},
            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(hD.numel() * 8),
                    "d2h_bytes_per_step": int(hy.numel() * 8),
                    "ms_per_step": e2e_ms / args.steps},
@@ -277,6 +284,16 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    summary (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh)[kernel]["dram_bytes"]
+    except Exception:
+        return None
 
 
 def ctx_probe_fp64(ctx) -> float:

@@ -83,8 +83,10 @@ class Context:
         except Exception:
             pass
 
-    def set_profiling(self, on: bool = True):
-        self.check(L.ddm_set_profiling(self._h, 1 if on else 0))
+    def set_profiling(self, on: bool = True, serial: bool = False):
+        """Per-stage CUDA events; serial=True also runs every stage on the
+        caller's stream one after another (clean per-kernel durations)."""
+        self.check(L.ddm_set_profiling(self._h, (2 if serial else 1) if on else 0))
 
     def stage_times(self) -> dict:
         arr = (C.c_double * 8)()

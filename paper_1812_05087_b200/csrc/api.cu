@@ -232,7 +232,7 @@ int ddm_ctx_create(int device, const void* nccl_uid, int rank, int world, ddm_ct
   }
   {
     const char* ser = getenv("DDM_SERIAL");
-    ctx->serial = ser && ser[0] == '1';
+    ctx->serial = ctx->serial_env = ser && ser[0] == '1';
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
     if ((e = cudaStreamCreateWithPriority(&ctx->s_hi, cudaStreamNonBlocking, hi_prio)) != cudaSuccess ||
@@ -290,6 +290,8 @@ int ddm_set_profiling(ddm_ctx_t ctx, int enable) {
     ctx->stage.created = true;
   }
   ctx->profiling = enable != 0;
+  // mode 2: serial schedule, so every stage's events bracket that stage alone
+  ctx->serial = enable == 2 ? true : ctx->serial_env;
   return DDM_OK;
 }
 

@@ -51,6 +51,7 @@ struct ddm_ctx_s {
   // near field (P2P, throughput bound) concurrently on s_lo
   cudaStream_t s_hi = nullptr, s_lo = nullptr;
   bool serial = false;            // DDM_SERIAL=1: everything on the caller's stream (profiling)
+  bool serial_env = false;        // the DDM_SERIAL setting (restored when profiling mode 2 ends)
   cudaEvent_t ev_fork = nullptr, ev_far = nullptr, ev_near = nullptr;
   // persistent scratch
   double* d_scalar = nullptr;     // small device scratch (reductions)
@@ -120,13 +121,14 @@ struct ddm_tree_s {
   int* tickets = nullptr;         // [2] work counters (upward, downward)
   int epoch = 0;
 
-  // FMM operators (device): M2M[4][p][p] complex, L2L[4][p][p] complex,
-  // Hankel table h[49][2p+2] complex, inverse factorials
-  double2* op_m2m = nullptr;
-  double2* op_l2l = nullptr;
-  double2* op_h = nullptr;        // M2L rotations e^{-ik theta} [49][p+2]
-  double* op_R = nullptr;         // M2L real Hankel entries [49][2p+2]
-  double* invfact = nullptr;
+  // FMM operators (device, fmm.cu fmm_init_operators): every translation is
+  // pre-scale (complex powers) x real Pascal matrix x post-scale
+  double* op_pas = nullptr;       // [p][p]    C(m,k) at m*p+k      (L2L, lane k)
+  double* op_pasT = nullptr;      // [p][p]    C(m,n) at n*p+m      (M2M, lane m)
+  double* op_pm2l = nullptr;      // [p+1][p]  C(m+n,n) at n*p+m    (M2L, runtime-p path)
+  double2* op_w = nullptr;        // [49][p+2] w^k, w = 1/delta      (M2L offset classes)
+  double2* op_eps = nullptr;      // [4][p+2]  eps_q^k               (M2M / L2L quadrants)
+  double2* op_e2i = nullptr;      // [4][p+2]  (2 eps_q)^-k
   // expansions: [ncells][2][p] complex
   double2* mpole = nullptr;
   double2* local = nullptr;

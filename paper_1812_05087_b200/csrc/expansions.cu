@@ -36,7 +36,6 @@ namespace {
     case 24: F(24); break;                \
     case 28: F(28); break;                \
     case 32: F(32); break;                \
-    case 40: F(40); break;                \
     default: F(0); break;                 \
   }
 
@@ -179,16 +178,20 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
 }
 
 // ------------------------------------------------------------ M2M (a6)
-// Parent c from its children q (all ready):
-//   alpha^c_m = sum_q sum_n M_q[n][m] alpha^q_n,  gamma^c_m = sum_q sum_n M_q[n][m] c^q_n,
-//   c_n = gamma_n - (n-1) conj(e)/s_q alpha_{n-1},  e = z_c - z_q,
-// M_q[n][m] = 2^{-n} C(m-1, n-1) eps_q^{m-n} (zero for n > m), eps_q = (z_q - z_c)/s_c.
+// Parent c from its children q (all ready), separable form (fmm.cu):
+//   c^q_{n+1} = gamma^q_{n+1} - n conj(e)/s_q alpha^q_n,   e = z_c - z_q
+//   xa^q_n = (2 eps_q)^{-(n+1)} alpha^q_{n+1},  xc^q_n = (2 eps_q)^{-(n+1)} c^q_{n+1}
+//   alpha^c_{m+1} = sum_q eps_q^{m+1} sum_n C(m, n) xa^q_n     (gamma^c likewise from xc)
+// Lane m reads the real Pascal entry C(m, n) (consecutive per lane) and the
+// pre-scaled child coefficients (shared-memory broadcasts).
 template <int PT>
 __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* __restrict__ c_iy,
                          const int* __restrict__ first_child, const int* __restrict__ nchild,
-                         const double2* ops, double2* __restrict__ mpole, double2* xa, double2* xc,
-                         const int* ready, int epoch, int lane) {
+                         const double* pasT, const double2* eps, const double2* e2i,
+                         double2* __restrict__ mpole, double2* xa, double2* xc, const int* ready,
+                         int epoch, int lane) {
   const int f = first_child[c], nc = nchild[c];
+  const int pw = p + 2;
   int quad[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -200,11 +203,14 @@ __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* 
       quad[i] = xb + 2 * yb;
       const double2 eb = make_double2(-(xb - 0.5), (yb - 0.5));   // conj(e)/s_q
       const double2* mq = mpole + (size_t)q * 2 * p;
+      const double2* Ei = e2i + quad[i] * pw;
       for (int n = lane; n < p; n += 32) {
-        xa[i * p + n] = mq[n];
+        const double2 an = mq[n];
         double2 cv = mq[p + n];
         if (n >= 1) cmac(cv, cscale(eb, -(double)n), mq[n - 1]);
-        xc[i * p + n] = cv;
+        const double2 sc = Ei[n + 1];
+        xa[i * p + n] = cmul(an, sc);
+        xc[i * p + n] = cmul(cv, sc);
       }
     }
   }
@@ -217,20 +223,26 @@ __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* 
 #pragma unroll
     for (int n = 0; n < pmax<PT>(); ++n) {
       if (!PT && n >= p) break;
+      const double cm = pasT[n * p + m];   // C(m, n)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         if (i < nc) {
-          const double2 tq = ops[(quad[i] * p + n) * p + m];
-          cmac(a[i], tq, xa[i * p + n]);
-          cmac(g[i], tq, xc[i * p + n]);
+          const double2 x = xa[i * p + n], y = xc[i * p + n];
+          a[i].x = fma(x.x, cm, a[i].x);
+          a[i].y = fma(x.y, cm, a[i].y);
+          g[i].x = fma(y.x, cm, g[i].x);
+          g[i].y = fma(y.y, cm, g[i].y);
         }
       }
     }
-    double2 sa = a[0], sg = g[0];
+    double2 sa = make_double2(0.0, 0.0), sg = sa;
 #pragma unroll
-    for (int i = 1; i < 4; ++i) {
-      sa = cadd(sa, a[i]);
-      sg = cadd(sg, g[i]);
+    for (int i = 0; i < 4; ++i) {
+      if (i < nc) {
+        const double2 em = eps[quad[i] * pw + m + 1];
+        cmac(sa, a[i], em);
+        cmac(sg, g[i], em);
+      }
     }
     out[m] = sa;
     out[p + m] = sg;
@@ -250,16 +262,23 @@ upward_kernel(int nleaves, int nm2m, const int* __restrict__ leaves,
               int p_rt, const int* __restrict__ perm, const double* __restrict__ D, int ncomp,
               const double* __restrict__ ex, const double* __restrict__ ey,
               const double* __restrict__ ea, const double* __restrict__ ec,
-              const double* __restrict__ es, const double2* __restrict__ opT,
+              const double* __restrict__ es, const double* __restrict__ pasT_g,
+              const double2* __restrict__ eps_g, const double2* __restrict__ e2i_g,
               double2* __restrict__ mpole, int* __restrict__ ready, int epoch,
               int* __restrict__ ticket, PoroFar pf) {
   const int p = PT ? PT : p_rt;
+  const int pw = p + 2;
   extern __shared__ double2 up_sh[];
-  double2* ops = up_sh;                                      // [4][p][p] as [q][n][m]
-  block_copy(ops, opT, 4 * p * p);
+  double2* eps = up_sh;                                       // [4][pw]
+  double2* e2i = eps + 4 * pw;                                // [4][pw]
+  double* pasT = reinterpret_cast<double*>(e2i + 4 * pw);     // [p][p] C(m,n) at n*p+m
+  double2* wbase = e2i + 4 * pw + (p * p + 1) / 2;
+  block_copy(eps, eps_g, 4 * pw);
+  block_copy(e2i, e2i_g, 4 * pw);
+  block_copy(pasT, pasT_g, p * p);
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* wb = up_sh + 4 * p * p + (size_t)w * (32 * 17 > 8 * p ? 32 * 17 : 8 * p);
+  double2* wb = wbase + (size_t)w * (32 * 17 > 8 * p ? 32 * 17 : 8 * p);
   const int total = nleaves + nm2m;
   for (;;) {
     int t = 0;
@@ -273,22 +292,23 @@ upward_kernel(int nleaves, int nm2m, const int* __restrict__ leaves,
                    ec, es, mpole, wb, lane, pf);
     } else {
       c = up_list[t - nleaves];
-      m2m_cell<PT>(c, p, c_ix, c_iy, first_child, nchild, ops, mpole, wb, wb + 4 * p, ready,
-                   epoch, lane);
+      m2m_cell<PT>(c, p, c_ix, c_iy, first_child, nchild, pasT, eps, e2i, mpole, wb, wb + 4 * p,
+                   ready, epoch, lane);
     }
     publish(ready + c, epoch, lane);
   }
 }
 
 // ------------------------------------------------------------ M2L (a7) + L2L (a8)
-// Rotated M2L: with delta = (z_b - z_a)/s = rho e^{i theta},
-//   l_m = (-1)^m/m! e^{-i m theta} sum_{n=1..p} [alpha_n e^{-i n theta}/(n-1)!] R_{n+m}
-//   g_m = (-1)^m/m! e^{-i m theta} sum_{n=1..p+1} [c_n e^{-i n theta}/(n-1)!] R_{n+m}
-//   c_n = gamma_n - (n-1) conj(delta) alpha_{n-1},  R_k = (k-1)! rho^-k (real)
-// then L2L from the (final) parent P:
+// M2L of V pair (target c, source b), delta = (z_c - z_b)/s, w = 1/delta:
+//   c_{n+1} = gamma_{n+1} - n conj(delta) alpha_n                 (Psi~ coupling)
+//   ap_n = w^{n+1} alpha_{n+1},  cp_n = w^{n+1} c_{n+1}           (pre-scale, lane n)
+//   lambda_m += (-w)^m sum_n C(m+n, n) ap_n,  g_m += (-w)^m sum_n C(m+n, n) cp_n
+// The real Pascal row C(m+n, n) of lane m is class independent: it lives in
+// registers (PT <= 32), so the inner loop reads only the two broadcast
+// coefficients per n from shared memory.  Then L2L from the (final) parent P:
 //   g'_m = gamma^P_m + (m+1) conj(eps) lambda^P_{m+1},  eps = (z_c - z_P)/s_P
-//   lambda^c_k += sum_m L_q[m][k] lambda^P_m,  gamma^c_k += sum_m L_q[m][k] g'_m
-// L_q[m][k] = C(m, k) 2^{-k} eps^{m-k} (zero for m < k).
+//   lambda^c_k += (2 eps)^{-k} sum_m C(m, k) eps^m lambda^P_m   (gamma^c likewise from g')
 template <int PT>
 __global__ void __launch_bounds__(kPassWarps * 32)
 downward_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restrict__ v_off,
@@ -296,26 +316,44 @@ downward_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __res
                 const int* __restrict__ c_level, const int* __restrict__ c_ix,
                 const int* __restrict__ c_iy, const int* __restrict__ c_start,
                 const int* __restrict__ c_count, const int* __restrict__ c_parent, int p_rt,
-                const double* __restrict__ rtab, const double2* __restrict__ rottab,
-                const double* __restrict__ invfact, const double2* __restrict__ l2lT,
-                const double2* __restrict__ mpole, double2* __restrict__ local,
-                int* __restrict__ ready, int epoch, int* __restrict__ ticket) {
+                const double2* __restrict__ w_g, const double2* __restrict__ eps_g,
+                const double2* __restrict__ e2i_g, const double* __restrict__ pas_g,
+                const double* __restrict__ pm2l_g, const double2* __restrict__ mpole,
+                double2* __restrict__ local, int* __restrict__ ready, int epoch,
+                int* __restrict__ ticket) {
   const int p = PT ? PT : p_rt;
+  constexpr bool REG = PT > 0 && PT <= 32;   // Pascal row in registers, one output per lane
+  constexpr int NCC = REG ? 1 : 2;           // outputs per lane: m = lane + 32 cc
+  const int pw = p + 2;
   extern __shared__ double2 dn_sh[];
-  const int rs = 2 * p + 2;                          // R entries per class
-  const int qs = p + 2;                              // rotation entries per class
-  double2* sh_l2l = dn_sh;                           // [4][p][p] as [q][m][k]
-  double2* sh_rot = sh_l2l + 4 * p * p;              // [49][qs]
-  double* sh_R = reinterpret_cast<double*>(sh_rot + kNOffsets * qs);   // [49][rs]
-  double2* wbuf = sh_rot + kNOffsets * qs + (kNOffsets * rs + 1) / 2;
-  block_copy(sh_l2l, l2lT, 4 * p * p);
-  block_copy(sh_rot, rottab, kNOffsets * qs);
-  block_copy(sh_R, rtab, kNOffsets * rs);
+  double2* sh_w = dn_sh;                                        // [49][pw]
+  double2* sh_eps = sh_w + kNOffsets * pw;                      // [4][pw]
+  double2* sh_e2i = sh_eps + 4 * pw;                            // [4][pw]
+  double* sh_pas = reinterpret_cast<double*>(sh_e2i + 4 * pw);  // [p][p] C(m,k) at m*p+k
+  double* sh_pm2l = sh_pas + p * p;                             // [p+1][p] (runtime-p path)
+  const int ndbl = p * p + (REG ? 0 : (p + 1) * p);
+  double2* wbuf = sh_e2i + 4 * pw + (ndbl + 1) / 2;
+  block_copy(sh_w, w_g, kNOffsets * pw);
+  block_copy(sh_eps, eps_g, 4 * pw);
+  block_copy(sh_e2i, e2i_g, 4 * pw);
+  block_copy(sh_pas, pas_g, p * p);
+  if (!REG) block_copy(sh_pm2l, pm2l_g, (p + 1) * p);
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* sa = wbuf + (size_t)w * (3 * p + 2);      // raw alpha [p]      | parent lambda [p]
-  double2* ap = sa + p;                               // rotated alpha [p]  | g' [p]
-  double2* cp = ap + p;                               // rotated c [p+1]
+  double2* sa = wbuf + (size_t)w * (3 * p + 1);      // raw alpha [p]      | eps^m lambda^P [p]
+  double2* ap = sa + p;                               // pre-scaled alpha [p] | eps^m g' [p]
+  double2* cp = ap + p;                               // pre-scaled c [p+1]
+  // lane m's M2L Pascal row C(m+n, n), n = 0..PT (exact integers up to 2^53)
+  double prow[REG ? PT + 1 : 1];
+  if (REG) {
+    double cb = 1.0;
+    prow[0] = 1.0;
+#pragma unroll
+    for (int n = 1; n < (REG ? PT + 1 : 1); ++n) {
+      cb = cb * (double)(lane + n) / (double)n;
+      prow[n] = cb;
+    }
+  }
   const int total = c1 - c0;
   for (;;) {
     int t = 0;
@@ -328,14 +366,17 @@ downward_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __res
       publish(ready + c, epoch, lane);
       continue;
     }
-    double2 al[2], ag[2];
-    al[0] = al[1] = ag[0] = ag[1] = make_double2(0.0, 0.0);
+    double2 al[NCC], ag[NCC];
+#pragma unroll
+    for (int cc = 0; cc < NCC; ++cc) al[cc] = ag[cc] = make_double2(0.0, 0.0);
     const int vb = v_off[c], ve = v_off[c + 1];
-    double2 na[2], ng[2];
-    na[0] = na[1] = ng[0] = ng[1] = make_double2(0.0, 0.0);
+    double2 na[NCC], ng[NCC];
+#pragma unroll
+    for (int cc = 0; cc < NCC; ++cc) na[cc] = ng[cc] = make_double2(0.0, 0.0);
     if (vb < ve) {
       const double2* ma = mpole + (size_t)v_idx[vb] * 2 * p;
-      for (int cc = 0; cc < 2; ++cc) {
+#pragma unroll
+      for (int cc = 0; cc < NCC; ++cc) {
         const int n = lane + 32 * cc;
         if (n < p) {
           na[cc] = ma[n];
@@ -345,10 +386,16 @@ downward_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __res
     }
     for (int v = vb; v < ve; ++v) {
       const int cls = v_cls[v];
-      const double2 xa0 = na[0], xa1 = na[1], xg0 = ng[0], xg1 = ng[1];
+      double2 xa[NCC], xg[NCC];
+#pragma unroll
+      for (int cc = 0; cc < NCC; ++cc) {
+        xa[cc] = na[cc];
+        xg[cc] = ng[cc];
+      }
       if (v + 1 < ve) {   // prefetch the next source
         const double2* ma = mpole + (size_t)v_idx[v + 1] * 2 * p;
-        for (int cc = 0; cc < 2; ++cc) {
+#pragma unroll
+        for (int cc = 0; cc < NCC; ++cc) {
           const int n = lane + 32 * cc;
           if (n < p) {
             na[cc] = ma[n];
@@ -358,54 +405,56 @@ downward_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __res
       }
       const int dxs = cls % 7 - 3, dys = cls / 7 - 3;   // source - target in cells
       const double2 dconj = make_double2(-(double)dxs, (double)dys);  // conj(delta)
-      const double2* rot = sh_rot + cls * qs;
-      const double* R = sh_R + cls * rs;
-      if (lane < p) sa[lane] = xa0;
-      if (lane + 32 < p) sa[lane + 32] = xa1;
+      const double2* W = sh_w + cls * pw;
+#pragma unroll
+      for (int cc = 0; cc < NCC; ++cc) {
+        const int n = lane + 32 * cc;
+        if (n < p) sa[n] = xa[cc];
+      }
       __syncwarp();
-      for (int cc = 0; cc < 2; ++cc) {   // slot n <-> coefficient n + 1
+      // pre-scale (slot n <-> coefficient n + 1); lane p also forms c_{p+1}
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
         const int n = lane + 32 * cc;
         if (n <= p) {
-          double2 cv = (n < p) ? (cc ? xg1 : xg0) : make_double2(0.0, 0.0);
+          const bool in = n < p;
+          double2 cv = make_double2(0.0, 0.0), av = cv;
+          if (in) {
+            cv = (cc == 0 || !REG) ? xg[cc < NCC ? cc : 0] : cv;
+            av = (cc == 0 || !REG) ? xa[cc < NCC ? cc : 0] : av;
+          }
           if (n >= 1) cmac(cv, cscale(dconj, -(double)n), sa[n - 1]);
-          const double2 rr = cscale(rot[n + 1], invfact[n]);
-          cp[n] = cmul(cv, rr);
-          if (n < p) ap[n] = cmul(cc ? xa1 : xa0, rr);
+          const double2 wn = W[n + 1];
+          cp[n] = cmul(cv, wn);
+          if (in) ap[n] = cmul(av, wn);
         }
       }
       __syncwarp();
-      for (int cc = 0; cc < 2; ++cc) {
+#pragma unroll
+      for (int cc = 0; cc < NCC; ++cc) {
         const int m = lane + 32 * cc;
         if (m < p) {
           double2 sl = make_double2(0.0, 0.0), sg = sl;
-          const double* Rm = R + 1 + m;
 #pragma unroll
           for (int n = 0; n < pmax<PT>(); ++n) {
             if (!PT && n >= p) break;
-            const double rk = Rm[n];
+            const double pc = REG ? prow[REG ? n : 0] : sh_pm2l[n * p + m];
             const double2 a = ap[n], g = cp[n];
-            sl.x = fma(a.x, rk, sl.x);
-            sl.y = fma(a.y, rk, sl.y);
-            sg.x = fma(g.x, rk, sg.x);
-            sg.y = fma(g.y, rk, sg.y);
+            sl.x = fma(a.x, pc, sl.x);
+            sl.y = fma(a.y, pc, sl.y);
+            sg.x = fma(g.x, pc, sg.x);
+            sg.y = fma(g.y, pc, sg.y);
           }
-          const double rk = Rm[p];
-          sg.x = fma(cp[p].x, rk, sg.x);
-          sg.y = fma(cp[p].y, rk, sg.y);
-          const double2 ro = rot[m];
-          cmac(al[cc], sl, ro);
-          cmac(ag[cc], sg, ro);
+          const double pc = REG ? prow[REG ? PT : 0] : sh_pm2l[p * p + m];
+          sg.x = fma(cp[p].x, pc, sg.x);
+          sg.y = fma(cp[p].y, pc, sg.y);
+          double2 wm = W[m];
+          if (m & 1) wm = make_double2(-wm.x, -wm.y);
+          cmac(al[cc], sl, wm);
+          cmac(ag[cc], sg, wm);
         }
       }
       __syncwarp();
-    }
-    for (int cc = 0; cc < 2; ++cc) {
-      const int m = lane + 32 * cc;
-      if (m < p) {
-        const double sc = ((m & 1) ? -1.0 : 1.0) * invfact[m];
-        al[cc] = cscale(al[cc], sc);
-        ag[cc] = cscale(ag[cc], sc);
-      }
     }
     // L2L from the parent (its local expansion is final once its flag is set)
     if (c_level[c] >= 3) {
@@ -415,35 +464,43 @@ downward_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __res
       const int xb = c_ix[c] & 1, yb = c_iy[c] & 1;
       const int quad = xb + 2 * yb;
       const double2 epsb = make_double2(0.5 * (xb - 0.5), -0.5 * (yb - 0.5));   // conj(eps)
-      double2* sl = sa;
-      double2* sg = ap;
+      const double2* E = sh_eps + quad * pw;
+      const double2* Ei = sh_e2i + quad * pw;
+      double2* xl = sa;
+      double2* xg = ap;
       for (int m = lane; m < p; m += 32) {
-        sl[m] = lp[m];
         double2 gv = lp[p + m];
         if (m + 1 < p) cmac(gv, cscale(epsb, (double)(m + 1)), lp[m + 1]);
-        sg[m] = gv;
+        const double2 em = E[m];
+        xl[m] = cmul(lp[m], em);
+        xg[m] = cmul(gv, em);
       }
       __syncwarp();
-      const double2* L = sh_l2l + (size_t)quad * p * p;
-      for (int cc = 0; cc < 2; ++cc) {
+#pragma unroll
+      for (int cc = 0; cc < NCC; ++cc) {
         const int k = lane + 32 * cc;
         if (k < p) {
-          double2 l = al[cc], g = ag[cc];
+          double2 l = make_double2(0.0, 0.0), g = l;
 #pragma unroll
           for (int m = 0; m < pmax<PT>(); ++m) {
             if (!PT && m >= p) break;
-            const double2 tq = L[m * p + k];
-            cmac(l, tq, sl[m]);
-            cmac(g, tq, sg[m]);
+            const double pc = sh_pas[m * p + k];   // C(m, k)
+            const double2 x = xl[m], y = xg[m];
+            l.x = fma(x.x, pc, l.x);
+            l.y = fma(x.y, pc, l.y);
+            g.x = fma(y.x, pc, g.x);
+            g.y = fma(y.y, pc, g.y);
           }
-          al[cc] = l;
-          ag[cc] = g;
+          const double2 ek = Ei[k];
+          cmac(al[cc], l, ek);
+          cmac(ag[cc], g, ek);
         }
       }
       __syncwarp();
     }
     double2* out = local + (size_t)c * 2 * p;
-    for (int cc = 0; cc < 2; ++cc) {
+#pragma unroll
+    for (int cc = 0; cc < NCC; ++cc) {
       const int m = lane + 32 * cc;
       if (m < p) {
         out[m] = al[cc];
@@ -559,7 +616,8 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
   const int p = t->p;
   const CellGeom cg{t->x_min, t->y_min, t->W};
   const size_t wsz = std::max(32 * 17, 8 * p);
-  const size_t shm = ((size_t)4 * p * p + (size_t)kPassWarps * wsz) * sizeof(double2);
+  const size_t shm = ((size_t)8 * (p + 2) + (size_t)(p * p + 1) / 2 + (size_t)kPassWarps * wsz) *
+                     sizeof(double2);
   ++t->epoch;
   DDM_CUDA(ctx, cudaMemsetAsync(t->tickets, 0, 2 * sizeof(int), s));
   int rc = DDM_OK;
@@ -570,7 +628,8 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
     upward_kernel<PT><<<nb, kPassWarps * 32, shm, s>>>(                                         \
         t->nleaves, t->n_up, t->leaves, t->up_list, t->c_level, t->c_ix, t->c_iy, t->c_start,   \
         t->c_count, t->c_first_child, t->c_nchild, cg, p, perm_in, D, ncomp, t->ex, t->ey,      \
-        t->ea, t->ec, t->es, t->op_m2m, t->mpole, t->ready_up, t->epoch, t->tickets, pf);       \
+        t->ea, t->ec, t->es, t->op_pasT, t->op_eps, t->op_e2i, t->mpole, t->ready_up, t->epoch, \
+        t->tickets, pf);                                                                        \
   } while (0)
   DDM_P_DISPATCH(p, DDM_L);
 #undef DDM_L
@@ -583,9 +642,10 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   if (t->nlevels <= 2) return DDM_OK;
   const int p = t->p;
   const int c0 = t->level_off[2], c1 = t->ncells;
-  const size_t shm = ((size_t)4 * p * p + (size_t)kNOffsets * (p + 2) +
-                      ((size_t)kNOffsets * (2 * p + 2) + 1) / 2 +
-                      (size_t)kPassWarps * (3 * p + 2)) * sizeof(double2);
+  const bool reg = (p == 8 || p == 12 || p == 16 || p == 20 || p == 24 || p == 28 || p == 32);
+  const size_t ndbl = (size_t)p * p + (reg ? 0 : (size_t)(p + 1) * p);
+  const size_t shm = ((size_t)(kNOffsets + 8) * (p + 2) + (ndbl + 1) / 2 +
+                      (size_t)kPassWarps * (3 * p + 1)) * sizeof(double2);
   int rc = DDM_OK;
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \
@@ -593,8 +653,8 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     const int nb = pass_grid(ctx, (const void*)downward_kernel<PT>, shm, c1 - c0);              \
     downward_kernel<PT><<<nb, kPassWarps * 32, shm, s>>>(                                       \
         c0, c1, t->own_el_lo, t->own_el_hi, t->v_off, t->v_idx, t->v_cls, t->c_level, t->c_ix,  \
-        t->c_iy, t->c_start, t->c_count, t->c_parent, p, t->op_R, t->op_h, t->invfact,          \
-        t->op_l2l, t->mpole, t->local, t->ready_down, t->epoch, t->tickets + 1);                \
+        t->c_iy, t->c_start, t->c_count, t->c_parent, p, t->op_w, t->op_eps, t->op_e2i,         \
+        t->op_pas, t->op_pm2l, t->mpole, t->local, t->ready_down, t->epoch, t->tickets + 1);    \
   } while (0)
   DDM_P_DISPATCH(p, DDM_L);
 #undef DDM_L

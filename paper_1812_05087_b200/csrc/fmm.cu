@@ -36,90 +36,72 @@ int ensure_workspace(ddm_ctx_s* ctx, ddm_tree_s* t) {
 
 }  // namespace
 
-// Translation operators (host, fp64), uploaded once per tree:
-//   M2M_q[m][n] = 2^-n C(m-1, n-1) eps^(m-n)   (n <= m), eps = (z_q - z_P)/s_P
-//   L2L_q[k][m] = C(m, k) 2^-k eps^(m-k)         (m >= k)
-//   M2L: rot[o][k] = e^{-i k theta}, R[o][k] = (k-1)! rho^-k for the 49 offset
-//        classes o = (dy+3)*7 + (dx+3), delta = -(dx + i dy) = rho e^{i theta}
-// stored transposed ([n][m] resp. [m][k]) for coalesced lane = output access.
+// Translation operators (host, fp64), uploaded once per tree.  Every
+// translation of DESIGN.md §4 factors as  post-scale x (real Pascal matrix) x
+// pre-scale  (the binomial expansions of Eq.(m2m), Eq.(m2l), Eq.(l2l) with the
+// offset powers pulled out of the sums):
+//   M2M  alpha^P_{m+1} = eps^{m+1} sum_n C(m, n) (2 eps)^{-(n+1)} alpha^q_{n+1}
+//   M2L  lambda_m      = (-w)^m    sum_n C(m+n, n) w^{n+1} alpha_{n+1}
+//   L2L  l^c_k         = (2 eps)^{-k} sum_m C(m, k) eps^m lambda^P_m
+// eps = (z_child - z_parent)/s_parent (4 quadrants), w = 1/delta with
+// delta = (z_target - z_source)/s = -(dx + i dy) for the 49 offset classes
+// o = (dy+3)*7 + (dx+3) (classes with max(|dx|,|dy|) < 2 are unused).
 int fmm_init_operators(ddm_tree_s* t, cudaStream_t s) {
   ddm_ctx_s* ctx = t->ctx;
   const int p = t->p;
   typedef std::vector<double2> V;
-  V m2m((size_t)4 * p * p), l2l((size_t)4 * p * p);
-  auto cpow = [](double re, double im, int k) {
-    double a = 1.0, b = 0.0;
-    for (int i = 0; i < k; ++i) {
-      const double na = a * re - b * im, nb = a * im + b * re;
-      a = na;
-      b = nb;
+  std::vector<double> pas((size_t)p * p), pasT((size_t)p * p), pm2l((size_t)(p + 1) * p);
+  for (int m = 0; m < p; ++m)
+    for (int k = 0; k < p; ++k) {
+      pas[(size_t)m * p + k] = binom(m, k);
+      pasT[(size_t)k * p + m] = binom(m, k);
     }
-    return make_double2(a, b);
+  for (int n = 0; n <= p; ++n)
+    for (int m = 0; m < p; ++m) pm2l[(size_t)n * p + m] = binom(m + n, n);
+  auto cmulh = [](double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
   };
+  const int pw = p + 2;
+  V eps((size_t)4 * pw), e2i((size_t)4 * pw), w((size_t)kNOffsets * pw, make_double2(0.0, 0.0));
   for (int q = 0; q < 4; ++q) {
-    const double ex_ = 0.5 * ((q & 1) - 0.5), ey_ = 0.5 * ((q >> 1) - 0.5);
-    for (int m = 1; m <= p; ++m)
-      for (int n = 1; n <= p; ++n) {
-        double2 v = make_double2(0.0, 0.0);
-        if (n <= m) {
-          const double2 e = cpow(ex_, ey_, m - n);
-          const double f = std::ldexp(1.0, -n) * binom(m - 1, n - 1);
-          v = make_double2(f * e.x, f * e.y);
-        }
-        m2m[(size_t)q * p * p + (size_t)(n - 1) * p + (m - 1)] = v;
-      }
-    for (int k = 0; k < p; ++k)
-      for (int m = 0; m < p; ++m) {
-        double2 v = make_double2(0.0, 0.0);
-        if (m >= k) {
-          const double2 e = cpow(ex_, ey_, m - k);
-          const double f = std::ldexp(1.0, -k) * binom(m, k);
-          v = make_double2(f * e.x, f * e.y);
-        }
-        l2l[(size_t)q * p * p + (size_t)m * p + k] = v;
-      }
+    const double2 e = make_double2(0.5 * ((q & 1) - 0.5), 0.5 * ((q >> 1) - 0.5));
+    const double n2 = 4.0 * (e.x * e.x + e.y * e.y);
+    const double2 ie = make_double2(2.0 * e.x / n2, -2.0 * e.y / n2);   // 1/(2 eps)
+    double2 a = make_double2(1.0, 0.0), b = a;
+    for (int k = 0; k < pw; ++k) {
+      eps[(size_t)q * pw + k] = a;
+      e2i[(size_t)q * pw + k] = b;
+      a = cmulh(a, e);
+      b = cmulh(b, ie);
+    }
   }
-  std::vector<double> R((size_t)kNOffsets * (2 * p + 2), 0.0);
-  V rot((size_t)kNOffsets * (p + 2), make_double2(0.0, 0.0));
   for (int o = 0; o < kNOffsets; ++o) {
     const int dx = o % 7 - 3, dy = o / 7 - 3;
     if (std::max(std::abs(dx), std::abs(dy)) < 2) continue;
-    const double rho = std::sqrt((double)dx * dx + (double)dy * dy);
-    const double er = -dx / rho, ei = dy / rho;   // e^{-i theta} = conj(delta)/rho
-    double pr = 1.0, pi = 0.0;
-    for (int k = 0; k < p + 2; ++k) {
-      rot[(size_t)o * (p + 2) + k] = make_double2(pr, pi);
-      const double nr = pr * er - pi * ei, ni = pr * ei + pi * er;
-      pr = nr;
-      pi = ni;
+    const double r2 = (double)dx * dx + (double)dy * dy;
+    const double2 wo = make_double2(-dx / r2, dy / r2);   // 1/delta = conj(delta)/|delta|^2
+    double2 a = make_double2(1.0, 0.0);
+    for (int k = 0; k < pw; ++k) {
+      w[(size_t)o * pw + k] = a;
+      a = cmulh(a, wo);
     }
-    double fact = 1.0, rp = 1.0;
-    for (int k = 1; k <= 2 * p + 1; ++k) {
-      if (k >= 2) fact *= (k - 1);
-      rp /= rho;
-      R[(size_t)o * (2 * p + 2) + k] = fact * rp;
-    }
-  }
-  std::vector<double> inv(2 * p + 2);
-  double f = 1.0;
-  for (int k = 0; k < 2 * p + 2; ++k) {
-    if (k >= 1) f *= k;
-    inv[k] = 1.0 / f;
   }
   int rc;
-  if ((rc = dalloc(ctx, &t->op_m2m, m2m.size())) || (rc = dalloc(ctx, &t->op_l2l, l2l.size())) ||
-      (rc = dalloc(ctx, &t->op_h, rot.size())) || (rc = dalloc(ctx, &t->invfact, inv.size())) ||
-      (rc = dalloc(ctx, &t->op_R, R.size())))
+  if ((rc = dalloc(ctx, &t->op_pas, pas.size())) || (rc = dalloc(ctx, &t->op_pasT, pasT.size())) ||
+      (rc = dalloc(ctx, &t->op_pm2l, pm2l.size())) || (rc = dalloc(ctx, &t->op_w, w.size())) ||
+      (rc = dalloc(ctx, &t->op_eps, eps.size())) || (rc = dalloc(ctx, &t->op_e2i, e2i.size())))
     return rc;
-  DDM_CUDA(ctx, cudaMemcpyAsync(t->op_R, R.data(), R.size() * sizeof(double),
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->op_pas, pas.data(), pas.size() * sizeof(double),
                                 cudaMemcpyHostToDevice, s));
-  DDM_CUDA(ctx, cudaMemcpyAsync(t->op_m2m, m2m.data(), m2m.size() * sizeof(double2),
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->op_pasT, pasT.data(), pasT.size() * sizeof(double),
                                 cudaMemcpyHostToDevice, s));
-  DDM_CUDA(ctx, cudaMemcpyAsync(t->op_l2l, l2l.data(), l2l.size() * sizeof(double2),
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->op_pm2l, pm2l.data(), pm2l.size() * sizeof(double),
                                 cudaMemcpyHostToDevice, s));
-  DDM_CUDA(ctx, cudaMemcpyAsync(t->op_h, rot.data(), rot.size() * sizeof(double2),
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->op_w, w.data(), w.size() * sizeof(double2),
                                 cudaMemcpyHostToDevice, s));
-  DDM_CUDA(ctx, cudaMemcpyAsync(t->invfact, inv.data(), inv.size() * sizeof(double),
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->op_eps, eps.data(), eps.size() * sizeof(double2),
+                                cudaMemcpyHostToDevice, s));
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->op_e2i, e2i.data(), e2i.size() * sizeof(double2),
                                 cudaMemcpyHostToDevice, s));
   DDM_CUDA(ctx, cudaStreamSynchronize(s));
   return DDM_OK;

@@ -147,3 +147,90 @@ def test_poro_history_small(ddm):
     r = r.cpu().numpy()
     for c in range(3):
         assert rel_l2(r[:, c], ref[:, c]) <= 1e-11, c
+
+
+def _lags(cfg, dt, h):
+    """A^(m) = K((m+1) dt) - K(m dt), m = 1..h (oracle, reading R10); [0] unused."""
+    K = [None] + [_A(cfg, j * dt) for j in range(1, h + 2)]
+    return [None] + [K[m + 1] - K[m] for m in range(1, h + 1)]
+
+
+def test_poro_history_fmm_and_direct_cfg4(ddm):
+    # a13: r_h = sum_{m=1}^{h} A^(m) D^(h-m) (P:400-405, P:922-929) on config 4's
+    # geometry, h = 3, against the oracle's direct double sum
+    D, ctx, torch = ddm
+    g = make_config(4)
+    dt = CONFIGS[4]["dt"]
+    h = 3
+    rng = np.random.default_rng(44)
+    Dh = rng.uniform(-1e-3, 1e-3, (h, g.n, 3))
+    Dh[:, :, 2] *= 1e-9
+    ref = OH.history_sum(g, dict(MAT, kind=1), dt, Dh, _lags(4, dt, h))
+    mat = D.material_from_dict(MAT)
+    Dt = torch.tensor(Dh, device="cuda")
+    tree_d = _tree(D, ctx, torch, g)
+    r_dir = D.history_apply(ctx, tree_d, mat, dt, Dt, mode="direct").cpu().numpy()
+    tree_f = _tree(D, ctx, torch, g, p=28, min_side=_rc((h + 1) * dt, g))
+    r_fmm = D.history_apply(ctx, tree_f, mat, dt, Dt, mode="fmm").cpu().numpy()
+    for c in range(3):
+        assert rel_l2(r_dir[:, c], ref[:, c]) <= 1e-11, ("direct", c)
+        assert rel_l2(r_fmm[:, c], ref[:, c]) <= 1e-8, ("fmm", c)
+
+
+def test_poro_history_causal_and_single_element(ddm):
+    # S:441-443, S:474: h = 1 uses only A^(1) D^0; a single element reduces to
+    # its 3x3 self blocks; rerunning a prefix reproduces it bitwise
+    D, ctx, torch = ddm
+    dt = 60.0
+    g1 = Geometry(np.array([0.0]), np.array([0.0]), np.array([0.25]), np.array([0.3]),
+                  np.array([0]), np.array([[0, 0]]))
+    D1 = np.array([[[2e-4, -1e-4, 3e-10]], [[-1e-4, 5e-4, 1e-10]]])
+    ref = OH.history_sum(g1, dict(MAT, kind=1), dt, D1)
+    mat = D.material_from_dict(MAT)
+    tree = _tree(D, ctx, torch, g1, leaf=1)
+    r = D.history_apply(ctx, tree, mat, dt, torch.tensor(D1, device="cuda"), mode="fmm")
+    r = r.cpu().numpy()
+    for c in range(3):
+        assert rel_l2(r[:, c], ref[:, c]) <= 1e-11, c
+    g = make_config(4)
+    tree4 = _tree(D, ctx, torch, g, p=20, min_side=_rc(4 * dt, g))
+    Dh = torch.tensor(np.random.default_rng(5).uniform(-1e-3, 1e-3, (3, g.n, 3)), device="cuda")
+    a = D.history_apply(ctx, tree4, mat, dt, Dh[:2].contiguous()).cpu().numpy()
+    D.history_apply(ctx, tree4, mat, dt, Dh)
+    b = D.history_apply(ctx, tree4, mat, dt, Dh[:2].contiguous()).cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+def test_poro_gmres_cfg3_full_size(ddm):
+    # config 3 at full size (N = 20000, 60000 unknowns): GMRES through the FMM;
+    # the oracle checks the true residual b - A x on sampled rows (it cannot
+    # hold the 29 GB dense matrix), plus the physics of the 5-fracture case:
+    # mirror symmetry about the middle fracture (S:476) and the stress shadow
+    # (outer fractures open more than inner ones, P:1262-1265)
+    D, ctx, torch = ddm
+    g = make_config(3)
+    c = CONFIGS[3]
+    tau = c["dt"]
+    ld = c["load"]
+    tree = _tree(D, ctx, torch, g, p=c["p_star"], min_side=_rc(tau, g))
+    mat = D.material_from_dict(MAT)
+    beta = torch.tensor(g.beta, device="cuda")
+    b = D.farfield_rhs(ctx, beta, 3, ld["p_f"], ld["sH"], ld["sh"], net=True,
+                       b_p=ld["sh"] + ld["p_f"] - ld["p0"])
+    bref = OH.poro_rhs(g, ld)
+    assert rel_l2(b.cpu().numpy(), bref) <= 1e-15
+    x, it, rr = D.gmres_solve(ctx, tree, mat, b, dt=tau, tol=1e-10, restart=3000, max_iter=6000)
+    xs = x.cpu().numpy()
+    assert rr <= 1e-10
+    rows = np.random.default_rng(33).choice(g.n, 24, replace=False)
+    Ax = OP.matvec_rows(g, MAT, tau, xs, rows)
+    scale = np.linalg.norm(bref[rows])          # b_s = 0 here: one scale for all rows
+    for comp in range(3):
+        res = np.linalg.norm(Ax[:, comp] - bref[rows, comp]) / scale
+        assert res <= 1e-6, (comp, res)
+    nel = 4000
+    w = xs[:, 1].reshape(5, nel)                       # opening per fracture
+    assert np.abs(w - w[::-1]).max() <= 1e-6 * np.abs(w).max()
+    mid = nel // 2
+    centre = w[:, mid - 1:mid + 1].mean(axis=1)
+    assert centre[0] > centre[1] and centre[0] > centre[2] and centre[4] > centre[3]
