@@ -237,9 +237,10 @@ def run_ours(args):
     p2p_ms = stages["p2p"]
     achieved = owned_pairs * FLOP_PER_PAIR / (p2p_ms * 1e-3) / 1e12
     levels = cnt["LEVELS"]
-    # prep_sources, p2p_kernel, upward_kernel, downward_kernel, finalize_kernel
+    # prep_sources, p2p_kernel, p2m_kernel, m2m_kernel, m2l_kernel, l2l_kernel,
+    # finalize_kernel
     # (+ unpack_allgather and scatter_user when the rows are exchanged)
-    launches_per_step = 5
+    launches_per_step = 7
     if world > 1:
         launches_per_step += 2
 

@@ -116,8 +116,9 @@ struct ddm_tree_s {
   // persistent-pass scheduling (expansions.cu)
   int* up_list = nullptr;         // non-leaf cells of level >= 2, deepest level first
   int n_up = 0;
+  std::vector<int> up_level_off;  // [2 (nlevels+1)]: level l = up_list[off[2l], off[2l+1])
   int* ready_up = nullptr;        // [ncells] multipole-ready flags (epoch tagged)
-  int* ready_down = nullptr;      // [ncells] local-final flags (epoch tagged)
+  int* ready_down = nullptr;      // [2 ncells] local-final flags | M2L-done flags (epoch tagged)
   int* tickets = nullptr;         // [2] work counters (upward, downward)
   int epoch = 0;
 

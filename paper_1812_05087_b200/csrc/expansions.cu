@@ -9,18 +9,19 @@
 // and likewise for Psi~ = Psi + conj(z0) Phi'.  The factor i G C,
 // C = 1/(4 pi (1 - nu)), is applied once, at evaluation.
 //
-// Scheduling: each pass is ONE persistent launch.  Warps take
-// cells in topological order from an atomic ticket counter (upward: all leaves
-// (P2M), then non-leaf cells deepest level first (M2M); downward: cells of
-// level >= 2 top-down (M2L, then L2L from the parent)).  A cell waits for the
-// cells it depends on through per-cell ready flags (release / acquire, tagged
-// with a per-call epoch).  Everything a warp waits for holds a lower ticket,
-// i.e. it was taken earlier by a running warp, so the wait cannot deadlock.
+// Scheduling: P2M (warp per leaf) and M2L (warp per cell)
+// have no dependencies and run as plain grids; M2M and L2L are launched one
+// tree level at a time (M2M deepest level first, L2L top-down), so every
+// dependency is a kernel boundary: no flags, no atomics, no spinning.  On the
+// high-priority stream these short launches interleave with the concurrent
+// near field (fmm.cu).
 //
 // Every kernel is a template on the expansion order PT (PT = 0: runtime p) so
 // that, for the instantiated orders, inner loops unroll and loads pipeline.
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "kcommon.cuh"
 
@@ -41,25 +42,6 @@ namespace {
 
 template <int PT>
 __host__ __device__ constexpr int pmax() { return PT ? PT : kMaxP; }
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// all lanes: spin until flag == epoch (acquire by every lane)
-__device__ __forceinline__ void wait_ready(const int* flag, int epoch) {
-  while (ld_acquire(flag) != epoch) __nanosleep(64);
-}
-// publish the warp's writes, then set the flag
-__device__ __forceinline__ void publish(int* flag, int epoch, int lane) {
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) st_release(flag, epoch);
-}
 
 constexpr int kPassWarps = 8;
 
@@ -122,6 +104,14 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
       B = cscale(B, is);
       Q = cscale(Q, is);
     }
+    // per-element weights of the power sums (elastic: fu = 1, Wme = Bc = 0):
+    //   alpha_n = ub P_{n-1},  gamma_n = y_n P_{n-1} + (n-1) x P_{n-2} [+ Bc (n-1)(n-2)/6 P_{n-3}]
+    //   ub = fu B, wr = fu B r, x = fu B A, y_n = Q + (n-2) wr + Wme (y_1 = Q - wr + Wme)
+    const double2 ub = cscale(B, fu);
+    const double2 wr = cmul(ub, rr);
+    const double2 xw = cmul(ub, A);
+    double2 yn = cadd(csub(Q, wr), Wme);
+    double2 xn = make_double2(0.0, 0.0);     // (n-1) x
     double2 pw1 = make_double2(1.0, 0.0), pw2 = pw1;
     double2 Pm2 = make_double2(0.0, 0.0);   // P_{n-3}
     double2 Pm1 = make_double2(0.0, 0.0);   // P_{n-2}
@@ -142,15 +132,12 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
               Pm1 = Pm;
               Pm = csub(pw2, pw1);
             }
-            alpha = cscale(cmul(B, Pm), fu);
-            gam = cmul(Q, Pm);
-            double2 tt = cscale(cmul(A, Pm1), (double)(n - 1));
-            cmac(tt, cscale(rr, (double)(n - 2)), Pm);
-            cmac(gam, cscale(B, fu), tt);
-            if (pf.on) {
-              cmac(gam, Wme, Pm);
-              if (n >= 4) cmac(gam, cscale(Bc, (n - 1) * (n - 2) / 6.0), Pm2);
-            }
+            alpha = cmul(ub, Pm);
+            gam = cmul(yn, Pm);
+            cmac(gam, xn, Pm1);
+            if (pf.on && n >= 4) cmac(gam, cscale(Bc, (n - 1) * (n - 2) / 6.0), Pm2);
+            yn = cadd(yn, wr);
+            xn = cadd(xn, xw);
           }
           buf[lane * 17 + j] = alpha;
           buf[lane * 17 + 8 + j] = gam;
@@ -188,8 +175,7 @@ template <int PT>
 __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* __restrict__ c_iy,
                          const int* __restrict__ first_child, const int* __restrict__ nchild,
                          const double* pasT, const double2* eps, const double2* e2i,
-                         double2* __restrict__ mpole, double2* xa, double2* xc, const int* ready,
-                         int epoch, int lane) {
+                         double2* __restrict__ mpole, double2* xa, double2* xc, int lane) {
   const int f = first_child[c], nc = nchild[c];
   const int pw = p + 2;
   int quad[4];
@@ -198,7 +184,6 @@ __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* 
     quad[i] = 0;
     if (i < nc) {
       const int q = f + i;
-      wait_ready(ready + q, epoch);
       const int xb = c_ix[q] & 1, yb = c_iy[q] & 1;
       quad[i] = xb + 2 * yb;
       const double2 eb = make_double2(-(xb - 0.5), (yb - 0.5));   // conj(e)/s_q
@@ -250,22 +235,33 @@ __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* 
   __syncwarp();
 }
 
-// Upward pass: tickets [0, nleaves) = P2M of leaves[t]; then M2M of
-// up_list[t - nleaves] (non-leaf cells of level >= 2, deepest level first).
+// P2M of every leaf: no dependencies, warp per leaf (grid-stride).
 template <int PT>
 __global__ void __launch_bounds__(kPassWarps * 32)
-upward_kernel(int nleaves, int nm2m, const int* __restrict__ leaves,
-              const int* __restrict__ up_list, const int* __restrict__ c_level,
-              const int* __restrict__ c_ix, const int* __restrict__ c_iy,
-              const int* __restrict__ c_start, const int* __restrict__ c_count,
-              const int* __restrict__ first_child, const int* __restrict__ nchild, CellGeom cg,
-              int p_rt, const int* __restrict__ perm, const double* __restrict__ D, int ncomp,
-              const double* __restrict__ ex, const double* __restrict__ ey,
-              const double* __restrict__ ea, const double* __restrict__ ec,
-              const double* __restrict__ es, const double* __restrict__ pasT_g,
-              const double2* __restrict__ eps_g, const double2* __restrict__ e2i_g,
-              double2* __restrict__ mpole, int* __restrict__ ready, int epoch,
-              int* __restrict__ ticket, PoroFar pf) {
+p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ c_level,
+           const int* __restrict__ c_ix, const int* __restrict__ c_iy,
+           const int* __restrict__ c_start, const int* __restrict__ c_count, CellGeom cg,
+           int p_rt, const double* __restrict__ D, int ncomp, const double* __restrict__ ex,
+           const double* __restrict__ ey, const double* __restrict__ ea,
+           const double* __restrict__ ec, const double* __restrict__ es,
+           double2* __restrict__ mpole, PoroFar pf) {
+  const int p = PT ? PT : p_rt;
+  extern __shared__ double2 p2m_sh[];   // [kPassWarps][32 * 17] transposition buffers
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = blockIdx.x * kPassWarps + w; k < nleaves; k += gridDim.x * kPassWarps)
+    p2m_cell<PT>(leaves[k], p, c_level, c_ix, c_iy, c_start, c_count, cg, nullptr, D, ncomp, ex,
+                 ey, ea, ec, es, mpole, p2m_sh + w * 32 * 17, lane, pf);
+}
+
+// M2M of the non-leaf cells up_list[u0, u1) of ONE level (launched deepest
+// level first: every child is final when its parent's level runs).
+template <int PT>
+__global__ void __launch_bounds__(kPassWarps * 32)
+m2m_level_kernel(int u0, int u1, const int* __restrict__ up_list, const int* __restrict__ c_ix,
+                 const int* __restrict__ c_iy, const int* __restrict__ first_child,
+                 const int* __restrict__ nchild, int p_rt, const double* __restrict__ pasT_g,
+                 const double2* __restrict__ eps_g, const double2* __restrict__ e2i_g,
+                 double2* __restrict__ mpole) {
   const int p = PT ? PT : p_rt;
   const int pw = p + 2;
   extern __shared__ double2 up_sh[];
@@ -278,236 +274,322 @@ upward_kernel(int nleaves, int nm2m, const int* __restrict__ leaves,
   block_copy(pasT, pasT_g, p * p);
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* wb = wbase + (size_t)w * (32 * 17 > 8 * p ? 32 * 17 : 8 * p);
-  const int total = nleaves + nm2m;
-  for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(ticket, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= total) break;
-    int c;
-    if (t < nleaves) {
-      c = leaves[t];
-      p2m_cell<PT>(c, p, c_level, c_ix, c_iy, c_start, c_count, cg, perm, D, ncomp, ex, ey, ea,
-                   ec, es, mpole, wb, lane, pf);
-    } else {
-      c = up_list[t - nleaves];
-      m2m_cell<PT>(c, p, c_ix, c_iy, first_child, nchild, pasT, eps, e2i, mpole, wb, wb + 4 * p,
-                   ready, epoch, lane);
-    }
-    publish(ready + c, epoch, lane);
-  }
+  double2* wb = wbase + (size_t)w * 8 * p;
+  for (int k = u0 + blockIdx.x * kPassWarps + w; k < u1; k += gridDim.x * kPassWarps)
+    m2m_cell<PT>(up_list[k], p, c_ix, c_iy, first_child, nchild, pasT, eps, e2i, mpole, wb,
+                 wb + 4 * p, lane);
 }
 
 // ------------------------------------------------------------ M2L (a7) + L2L (a8)
 // M2L of V pair (target c, source b), delta = (z_c - z_b)/s, w = 1/delta:
 //   c_{n+1} = gamma_{n+1} - n conj(delta) alpha_n                 (Psi~ coupling)
-//   ap_n = w^{n+1} alpha_{n+1},  cp_n = w^{n+1} c_{n+1}           (pre-scale, lane n)
+//   ap_n = w^{n+1} alpha_{n+1},  cp_n = w^{n+1} c_{n+1}           (pre-scale)
 //   lambda_m += (-w)^m sum_n C(m+n, n) ap_n,  g_m += (-w)^m sum_n C(m+n, n) cp_n
-// The real Pascal row C(m+n, n) of lane m is class independent: it lives in
-// registers (PT <= 32), so the inner loop reads only the two broadcast
-// coefficients per n from shared memory.  Then L2L from the (final) parent P:
+// The Pascal matrix C(m+n, n) is the same for every pair and offset class, so
+// the middle step is one real GEMM per target cell:
+//   Y[m][col] = sum_n P[m][n] X[n][col],  col = 4 v + (ap.re, ap.im, cp.re, cp.im)
+// run on the fp64 tensor pipe (mma.sync m8n8k4 f64 = DMMA.8x8x4: same fp64 peak
+// as DFMA on B200, scripts/micro/dmma.cu, at 1/8 of the issued instructions).
+// Then L2L from the (final) parent P:
 //   g'_m = gamma^P_m + (m+1) conj(eps) lambda^P_{m+1},  eps = (z_c - z_P)/s_P
 //   lambda^c_k += (2 eps)^{-k} sum_m C(m, k) eps^m lambda^P_m   (gamma^c likewise from g')
+
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int kM2LBatch = 4;     // V pairs per pipelined batch (2 DMMA n-tiles)
+
+// Tensor-core M2L of cell c's V list [vb, ve) (PT <= 32).  Per batch of
+// kM2LBatch pairs: (1) every lane loads the source coefficients of its
+// ceil(batch x KB / 32) (pair, n) items at once (all loads in flight), then
+// writes the pre-scaled X[col][n] (col = 4 pair + (ap.re, ap.im, cp.re,
+// cp.im)); (2) the warp runs Y = P X on DMMA (two pairs = one 8-column
+// n-tile) and post-scales.  Lane l owns output rows m = 8 i + l/4 of series
+// (l%4)%2 for pair parity (l%4)/2; the parities are summed at the end.
+// Results go to out_l[m], out_g[m] (m < p).
+constexpr int kXStride = 36;   // doubles per X column (>= p+1; = 4 mod 16: conflict-free fragments)
+
 template <int PT>
-__global__ void __launch_bounds__(kPassWarps * 32)
-downward_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restrict__ v_off,
-                const int* __restrict__ v_idx, const unsigned char* __restrict__ v_cls,
-                const int* __restrict__ c_level, const int* __restrict__ c_ix,
-                const int* __restrict__ c_iy, const int* __restrict__ c_start,
-                const int* __restrict__ c_count, const int* __restrict__ c_parent, int p_rt,
-                const double2* __restrict__ w_g, const double2* __restrict__ eps_g,
-                const double2* __restrict__ e2i_g, const double* __restrict__ pas_g,
-                const double* __restrict__ pm2l_g, const double2* __restrict__ mpole,
-                double2* __restrict__ local, int* __restrict__ ready, int epoch,
-                int* __restrict__ ticket) {
+__device__ void m2l_cell_tc(int vb, int ve, const int* __restrict__ v_idx,
+                            const unsigned char* __restrict__ v_cls,
+                            const double2* __restrict__ mpole, const double2* __restrict__ w_g,
+                            const double* sh_afr, double* X, double2* out_l, double2* out_g,
+                            int lane) {
+  constexpr int p = PT, pw = PT + 2, P2 = 2 * PT;
+  constexpr int MT = (PT + 7) / 8, KS = (PT + 4) / 4, KB = 4 * KS;
+  constexpr int ITEMS = (kM2LBatch * KB + 31) / 32;
+  double2 acc[MT];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) acc[i] = make_double2(0.0, 0.0);
+  const int q = lane >> 2, j = lane & 3;
+  for (int vc = vb; vc < ve; vc += 32) {   // V lists hold <= 27 entries
+    const int K = min(32, ve - vc);
+    int my_src = 0, my_cls = 0;
+    if (lane < K) {
+      my_src = v_idx[vc + lane];
+      my_cls = v_cls[vc + lane];
+    }
+    for (int b0 = 0; b0 < K; b0 += kM2LBatch) {
+      const int nb = min(kM2LBatch, K - b0);
+      // phase 1: loads of all items first
+      double2 ra[ITEMS], rg[ITEMS], rp[ITEMS], rw[ITEMS];
+      int rn[ITEMS], rv[ITEMS], rc[ITEMS];
+#pragma unroll
+      for (int r = 0; r < ITEMS; ++r) {
+        const int it = r * 32 + lane;
+        const int v = min(it / KB, kM2LBatch - 1), n = it - v * KB;
+        const int src = __shfl_sync(0xffffffffu, my_src, (b0 + v) & 31);
+        const int cls = __shfl_sync(0xffffffffu, my_cls, (b0 + v) & 31);
+        rn[r] = n;
+        rv[r] = v;
+        rc[r] = cls;
+        const bool ok = v < nb && it < kM2LBatch * KB;
+        const double2* ma = mpole + (size_t)src * P2;
+        const double2 z = make_double2(0.0, 0.0);
+        ra[r] = (ok && n < p) ? __ldg(ma + n) : z;
+        rg[r] = (ok && n < p) ? __ldg(ma + p + n) : z;
+        rp[r] = (ok && n >= 1 && n <= p) ? __ldg(ma + n - 1) : z;
+        rw[r] = (ok && n <= p) ? __ldg(w_g + cls * pw + n + 1) : z;
+      }
+#pragma unroll
+      for (int r = 0; r < ITEMS; ++r) {
+        const int n = rn[r], v = rv[r];
+        if (v < nb && r * 32 + lane < kM2LBatch * KB) {
+          const double2 av = cmul(ra[r], rw[r]);
+          double2 cv = rg[r];
+          const int cls = rc[r];
+          const double2 dconj = make_double2(-(double)(cls % 7 - 3), (double)(cls / 7 - 3));
+          cmac(cv, cscale(dconj, -(double)n), rp[r]);
+          cv = cmul(cv, rw[r]);
+          double* xc = X + (size_t)(4 * v) * kXStride + n;
+          xc[0] = av.x;
+          xc[kXStride] = av.y;
+          xc[2 * kXStride] = cv.x;
+          xc[3 * kXStride] = cv.y;
+        }
+      }
+      __syncwarp();
+      // phase 2: Y = P X on DMMA, two pairs (8 columns) per n-tile; post-scale
+      for (int t = 0; t < (nb + 1) >> 1; ++t) {
+        double d[MT][2];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) d[i][0] = d[i][1] = 0.0;
+        const double* xb = X + (size_t)(8 * t + q) * kXStride + j;
+#pragma unroll
+        for (int sk = 0; sk < KS; ++sk) {
+          const double bv = xb[4 * sk];
+#pragma unroll
+          for (int i = 0; i < MT; ++i)
+            dmma_884(d[i][0], d[i][1], sh_afr[(i * KS + sk) * 32 + lane], bv);
+        }
+        // lane holds rows m = 8 i + q, columns 8 t + 2 j + {0, 1}: pair 2 t + j/2,
+        // series j % 2, (re, im)
+        const int vloc = 2 * t + (j >> 1);
+        const int cls = __shfl_sync(0xffffffffu, my_cls, (b0 + vloc) & 31);
+        if (vloc < nb) {
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            const int m = 8 * i + q;
+            double2 wm = __ldg(w_g + cls * pw + min(m, p));
+            if (m & 1) wm = make_double2(-wm.x, -wm.y);
+            cmac(acc[i], make_double2(d[i][0], d[i][1]), wm);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  // sum the two pair parities (lanes l and l ^ 2), lanes with j < 2 write
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, 2);
+    acc[i].y += __shfl_xor_sync(0xffffffffu, acc[i].y, 2);
+    const int m = 8 * i + q;
+    if (j < 2 && m < p) (j == 0 ? out_l : out_g)[m] = acc[i];
+  }
+}
+
+// Runtime-p fallback M2L (DFMA, lane = m, Pascal entries from shared memory).
+__device__ void m2l_cell_dfma(int p, int vb, int ve, const int* __restrict__ v_idx,
+                              const unsigned char* __restrict__ v_cls,
+                              const double2* __restrict__ mpole, const double2* sh_w,
+                              const double* sh_pm2l, double2* sa, double2* ap, double2* cp,
+                              double2* out_l, double2* out_g, int lane) {
+  const int pw = p + 2;
+  double2 al[2], ag[2];
+  al[0] = al[1] = ag[0] = ag[1] = make_double2(0.0, 0.0);
+  for (int v = vb; v < ve; ++v) {
+    const int cls = v_cls[v];
+    const double2* ma = mpole + (size_t)v_idx[v] * 2 * p;
+    const int dxs = cls % 7 - 3, dys = cls / 7 - 3;
+    const double2 dconj = make_double2(-(double)dxs, (double)dys);
+    const double2* W = sh_w + cls * pw;
+    for (int n = lane; n < p; n += 32) sa[n] = ma[n];
+    __syncwarp();
+    for (int n = lane; n <= p; n += 32) {
+      double2 cv = n < p ? ma[p + n] : make_double2(0.0, 0.0);
+      if (n >= 1) cmac(cv, cscale(dconj, -(double)n), sa[n - 1]);
+      const double2 wn = W[n + 1];
+      cp[n] = cmul(cv, wn);
+      if (n < p) ap[n] = cmul(sa[n], wn);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      const int m = lane + 32 * cc;
+      if (m < p) {
+        double2 sl = make_double2(0.0, 0.0), sg = sl;
+        for (int n = 0; n < p; ++n) {
+          const double pc = sh_pm2l[n * p + m];
+          sl.x = fma(ap[n].x, pc, sl.x);
+          sl.y = fma(ap[n].y, pc, sl.y);
+          sg.x = fma(cp[n].x, pc, sg.x);
+          sg.y = fma(cp[n].y, pc, sg.y);
+        }
+        const double pc = sh_pm2l[p * p + m];
+        sg.x = fma(cp[p].x, pc, sg.x);
+        sg.y = fma(cp[p].y, pc, sg.y);
+        double2 wm = W[m];
+        if (m & 1) wm = make_double2(-wm.x, -wm.y);
+        cmac(al[cc], sl, wm);
+        cmac(ag[cc], sg, wm);
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    const int m = lane + 32 * cc;
+    if (m < p) {
+      out_l[m] = al[cc];
+      out_g[m] = ag[cc];
+    }
+  }
+  __syncwarp();
+}
+
+// M2L of every cell of level >= 2 whose subtree holds owned targets: no
+// dependencies (all multipoles are final), warp per cell (grid-stride).
+template <int PT>
+__global__ void __launch_bounds__(kPassWarps * 32, 2)
+m2l_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restrict__ v_off,
+           const int* __restrict__ v_idx, const unsigned char* __restrict__ v_cls,
+           const int* __restrict__ c_start, const int* __restrict__ c_count, int p_rt,
+           const double2* __restrict__ w_g, const double* __restrict__ pm2l_g,
+           const double2* __restrict__ mpole, double2* __restrict__ local) {
   const int p = PT ? PT : p_rt;
-  constexpr bool REG = PT > 0 && PT <= 32;   // Pascal row in registers, one output per lane
-  constexpr int NCC = REG ? 1 : 2;           // outputs per lane: m = lane + 32 cc
+  constexpr bool TC = PT > 0 && PT <= 32;   // tensor-core M2L
+  constexpr int MT = TC ? (PT + 7) / 8 : 1, KS = TC ? (PT + 4) / 4 : 1;
   const int pw = p + 2;
   extern __shared__ double2 dn_sh[];
-  double2* sh_w = dn_sh;                                        // [49][pw]
-  double2* sh_eps = sh_w + kNOffsets * pw;                      // [4][pw]
+  // dfma: W [49][pw] | C(m+n,n) [p+1][p] at n*p+m | per warp sa, ap, cp
+  // tc:   A fragments [MT][KS][32] | per warp X [4 kM2LBatch][kXStride] doubles
+  double2* sh_w = dn_sh;
+  const int nw2 = TC ? 0 : kNOffsets * pw;
+  double* sh_pm2l = reinterpret_cast<double*>(sh_w + nw2);
+  const int ndbl = TC ? MT * KS * 32 : (p + 1) * p;
+  double2* wbuf = sh_w + nw2 + (ndbl + 1) / 2;
+  if (!TC) block_copy(sh_w, w_g, kNOffsets * pw);
+  if (TC) {
+    // A fragments of the Pascal matrix P[m][n] = C(m+n, n) (m < p, n <= p, else 0):
+    // fragment (i, s), lane l holds P[8 i + l/4][4 s + l%4]
+    for (int e = threadIdx.x; e < MT * KS * 32; e += blockDim.x) {
+      const int l = e & 31, f = e >> 5, i = f / KS, sk = f - i * KS;
+      const int m = 8 * i + (l >> 2), n = 4 * sk + (l & 3);
+      sh_pm2l[e] = (m < p && n <= p) ? pm2l_g[n * p + m] : 0.0;
+    }
+  } else {
+    block_copy(sh_pm2l, pm2l_g, (p + 1) * p);
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t wstride = TC ? (size_t)2 * kM2LBatch * kXStride : 3 * (size_t)p + 1;
+  double2* ring = wbuf + (size_t)w * wstride;
+  for (int c = c0 + blockIdx.x * kPassWarps + w; c < c1; c += gridDim.x * kPassWarps) {
+    const int cs = c_start[c], ce = cs + c_count[c];
+    if (ce <= own_lo || cs >= own_hi) continue;   // subtree outside this rank's targets
+    double2* out = local + (size_t)c * 2 * p;
+    const int vb = v_off[c], ve = v_off[c + 1];
+    if constexpr (TC) {
+      m2l_cell_tc<PT>(vb, ve, v_idx, v_cls, mpole, w_g, sh_pm2l, reinterpret_cast<double*>(ring),
+                      out, out + p, lane);
+    } else {
+      m2l_cell_dfma(p, vb, ve, v_idx, v_cls, mpole, sh_w, sh_pm2l, ring, ring + p, ring + 2 * p,
+                    out, out + p, lane);
+    }
+  }
+}
+
+// L2L of the cells [c0, c1) of ONE level >= 3 whose subtree holds owned
+// targets: local[c] (its M2L result) += L2L(parent's final local).  Launched
+// top-down, one level at a time.
+template <int PT>
+__global__ void __launch_bounds__(kPassWarps * 32)
+l2l_level_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restrict__ c_ix,
+                 const int* __restrict__ c_iy, const int* __restrict__ c_start,
+                 const int* __restrict__ c_count, const int* __restrict__ c_parent, int p_rt,
+                 const double2* __restrict__ eps_g, const double2* __restrict__ e2i_g,
+                 const double* __restrict__ pas_g, double2* __restrict__ local) {
+  const int p = PT ? PT : p_rt;
+  const int pw = p + 2;
+  extern __shared__ double2 l2_sh[];
+  double2* sh_eps = l2_sh;                                      // [4][pw]
   double2* sh_e2i = sh_eps + 4 * pw;                            // [4][pw]
   double* sh_pas = reinterpret_cast<double*>(sh_e2i + 4 * pw);  // [p][p] C(m,k) at m*p+k
-  double* sh_pm2l = sh_pas + p * p;                             // [p+1][p] (runtime-p path)
-  const int ndbl = p * p + (REG ? 0 : (p + 1) * p);
-  double2* wbuf = sh_e2i + 4 * pw + (ndbl + 1) / 2;
-  block_copy(sh_w, w_g, kNOffsets * pw);
+  double2* wbuf = sh_e2i + 4 * pw + (p * p + 1) / 2;
   block_copy(sh_eps, eps_g, 4 * pw);
   block_copy(sh_e2i, e2i_g, 4 * pw);
   block_copy(sh_pas, pas_g, p * p);
-  if (!REG) block_copy(sh_pm2l, pm2l_g, (p + 1) * p);
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* sa = wbuf + (size_t)w * (3 * p + 1);      // raw alpha [p]      | eps^m lambda^P [p]
-  double2* ap = sa + p;                               // pre-scaled alpha [p] | eps^m g' [p]
-  double2* cp = ap + p;                               // pre-scaled c [p+1]
-  // lane m's M2L Pascal row C(m+n, n), n = 0..PT (exact integers up to 2^53)
-  double prow[REG ? PT + 1 : 1];
-  if (REG) {
-    double cb = 1.0;
-    prow[0] = 1.0;
-#pragma unroll
-    for (int n = 1; n < (REG ? PT + 1 : 1); ++n) {
-      cb = cb * (double)(lane + n) / (double)n;
-      prow[n] = cb;
-    }
-  }
-  const int total = c1 - c0;
-  for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(ticket, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= total) break;
-    const int c = c0 + t;
+  double2* xl = wbuf + (size_t)w * 2 * p;
+  double2* xg = xl + p;
+  for (int c = c0 + blockIdx.x * kPassWarps + w; c < c1; c += gridDim.x * kPassWarps) {
     const int cs = c_start[c], ce = cs + c_count[c];
-    if (ce <= own_lo || cs >= own_hi) {   // subtree outside this rank's targets
-      publish(ready + c, epoch, lane);
-      continue;
+    if (ce <= own_lo || cs >= own_hi) continue;   // no owned target below c
+    const int P = c_parent[c];
+    const double2* lp = local + (size_t)P * 2 * p;
+    const int xb = c_ix[c] & 1, yb = c_iy[c] & 1;
+    const int quad = xb + 2 * yb;
+    const double2 epsb = make_double2(0.5 * (xb - 0.5), -0.5 * (yb - 0.5));   // conj(eps)
+    const double2* E = sh_eps + quad * pw;
+    const double2* Ei = sh_e2i + quad * pw;
+    for (int m = lane; m < p; m += 32) {
+      double2 gv = lp[p + m];
+      if (m + 1 < p) cmac(gv, cscale(epsb, (double)(m + 1)), lp[m + 1]);
+      const double2 em = E[m];
+      xl[m] = cmul(lp[m], em);
+      xg[m] = cmul(gv, em);
     }
-    double2 al[NCC], ag[NCC];
-#pragma unroll
-    for (int cc = 0; cc < NCC; ++cc) al[cc] = ag[cc] = make_double2(0.0, 0.0);
-    const int vb = v_off[c], ve = v_off[c + 1];
-    double2 na[NCC], ng[NCC];
-#pragma unroll
-    for (int cc = 0; cc < NCC; ++cc) na[cc] = ng[cc] = make_double2(0.0, 0.0);
-    if (vb < ve) {
-      const double2* ma = mpole + (size_t)v_idx[vb] * 2 * p;
-#pragma unroll
-      for (int cc = 0; cc < NCC; ++cc) {
-        const int n = lane + 32 * cc;
-        if (n < p) {
-          na[cc] = ma[n];
-          ng[cc] = ma[p + n];
-        }
-      }
-    }
-    for (int v = vb; v < ve; ++v) {
-      const int cls = v_cls[v];
-      double2 xa[NCC], xg[NCC];
-#pragma unroll
-      for (int cc = 0; cc < NCC; ++cc) {
-        xa[cc] = na[cc];
-        xg[cc] = ng[cc];
-      }
-      if (v + 1 < ve) {   // prefetch the next source
-        const double2* ma = mpole + (size_t)v_idx[v + 1] * 2 * p;
-#pragma unroll
-        for (int cc = 0; cc < NCC; ++cc) {
-          const int n = lane + 32 * cc;
-          if (n < p) {
-            na[cc] = ma[n];
-            ng[cc] = ma[p + n];
-          }
-        }
-      }
-      const int dxs = cls % 7 - 3, dys = cls / 7 - 3;   // source - target in cells
-      const double2 dconj = make_double2(-(double)dxs, (double)dys);  // conj(delta)
-      const double2* W = sh_w + cls * pw;
-#pragma unroll
-      for (int cc = 0; cc < NCC; ++cc) {
-        const int n = lane + 32 * cc;
-        if (n < p) sa[n] = xa[cc];
-      }
-      __syncwarp();
-      // pre-scale (slot n <-> coefficient n + 1); lane p also forms c_{p+1}
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int n = lane + 32 * cc;
-        if (n <= p) {
-          const bool in = n < p;
-          double2 cv = make_double2(0.0, 0.0), av = cv;
-          if (in) {
-            cv = (cc == 0 || !REG) ? xg[cc < NCC ? cc : 0] : cv;
-            av = (cc == 0 || !REG) ? xa[cc < NCC ? cc : 0] : av;
-          }
-          if (n >= 1) cmac(cv, cscale(dconj, -(double)n), sa[n - 1]);
-          const double2 wn = W[n + 1];
-          cp[n] = cmul(cv, wn);
-          if (in) ap[n] = cmul(av, wn);
-        }
-      }
-      __syncwarp();
-#pragma unroll
-      for (int cc = 0; cc < NCC; ++cc) {
-        const int m = lane + 32 * cc;
-        if (m < p) {
-          double2 sl = make_double2(0.0, 0.0), sg = sl;
-#pragma unroll
-          for (int n = 0; n < pmax<PT>(); ++n) {
-            if (!PT && n >= p) break;
-            const double pc = REG ? prow[REG ? n : 0] : sh_pm2l[n * p + m];
-            const double2 a = ap[n], g = cp[n];
-            sl.x = fma(a.x, pc, sl.x);
-            sl.y = fma(a.y, pc, sl.y);
-            sg.x = fma(g.x, pc, sg.x);
-            sg.y = fma(g.y, pc, sg.y);
-          }
-          const double pc = REG ? prow[REG ? PT : 0] : sh_pm2l[p * p + m];
-          sg.x = fma(cp[p].x, pc, sg.x);
-          sg.y = fma(cp[p].y, pc, sg.y);
-          double2 wm = W[m];
-          if (m & 1) wm = make_double2(-wm.x, -wm.y);
-          cmac(al[cc], sl, wm);
-          cmac(ag[cc], sg, wm);
-        }
-      }
-      __syncwarp();
-    }
-    // L2L from the parent (its local expansion is final once its flag is set)
-    if (c_level[c] >= 3) {
-      const int P = c_parent[c];
-      wait_ready(ready + P, epoch);
-      const double2* lp = local + (size_t)P * 2 * p;
-      const int xb = c_ix[c] & 1, yb = c_iy[c] & 1;
-      const int quad = xb + 2 * yb;
-      const double2 epsb = make_double2(0.5 * (xb - 0.5), -0.5 * (yb - 0.5));   // conj(eps)
-      const double2* E = sh_eps + quad * pw;
-      const double2* Ei = sh_e2i + quad * pw;
-      double2* xl = sa;
-      double2* xg = ap;
-      for (int m = lane; m < p; m += 32) {
-        double2 gv = lp[p + m];
-        if (m + 1 < p) cmac(gv, cscale(epsb, (double)(m + 1)), lp[m + 1]);
-        const double2 em = E[m];
-        xl[m] = cmul(lp[m], em);
-        xg[m] = cmul(gv, em);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int cc = 0; cc < NCC; ++cc) {
-        const int k = lane + 32 * cc;
-        if (k < p) {
-          double2 l = make_double2(0.0, 0.0), g = l;
-#pragma unroll
-          for (int m = 0; m < pmax<PT>(); ++m) {
-            if (!PT && m >= p) break;
-            const double pc = sh_pas[m * p + k];   // C(m, k)
-            const double2 x = xl[m], y = xg[m];
-            l.x = fma(x.x, pc, l.x);
-            l.y = fma(x.y, pc, l.y);
-            g.x = fma(y.x, pc, g.x);
-            g.y = fma(y.y, pc, g.y);
-          }
-          const double2 ek = Ei[k];
-          cmac(al[cc], l, ek);
-          cmac(ag[cc], g, ek);
-        }
-      }
-      __syncwarp();
-    }
+    __syncwarp();
     double2* out = local + (size_t)c * 2 * p;
 #pragma unroll
-    for (int cc = 0; cc < NCC; ++cc) {
-      const int m = lane + 32 * cc;
-      if (m < p) {
-        out[m] = al[cc];
-        out[p + m] = ag[cc];
+    for (int cc = 0; cc < 2; ++cc) {
+      const int k = lane + 32 * cc;
+      if (k < p) {
+        double2 al = out[k], ag = out[p + k];
+        double2 l = make_double2(0.0, 0.0), g = l;
+#pragma unroll
+        for (int m = 0; m < pmax<PT>(); ++m) {
+          if (!PT && m >= p) break;
+          const double pc = sh_pas[m * p + k];   // C(m, k)
+          const double2 x = xl[m], y = xg[m];
+          l.x = fma(x.x, pc, l.x);
+          l.y = fma(x.y, pc, l.y);
+          g.x = fma(y.x, pc, g.x);
+          g.y = fma(y.y, pc, g.y);
+        }
+        const double2 ek = Ei[k];
+        cmac(al, l, ek);
+        cmac(ag, g, ek);
+        out[k] = al;
+        out[p + k] = ag;
       }
     }
-    publish(ready + c, epoch, lane);
+    __syncwarp();
   }
 }
 
@@ -582,23 +664,53 @@ __global__ void finalize_kernel(int64_t e_lo, int64_t e_hi, int ncomp,
   }
 }
 
+// Host-side launch configuration is cached per (kernel, shared-memory size,
+// device): the attribute and occupancy queries cost microseconds of host time
+// per call, which would otherwise sit between the kernels of every matvec.
+struct LaunchCfg {
+  const void* kernel;
+  size_t shm;
+  int device;
+  int per_sm, nsm;
+};
+std::mutex g_cfg_mu;
+std::vector<LaunchCfg> g_cfg;
+
 template <class K>
 int set_smem(ddm_ctx_s* ctx, K kernel, size_t shm) {
-  if (shm > 48 * 1024)
-    DDM_CUDA(ctx, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  if (shm <= 48 * 1024) return DDM_OK;
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  for (const auto& c : g_cfg)
+    if (c.kernel == (const void*)kernel && c.shm >= shm && c.device == ctx->device && c.per_sm < 0)
+      return DDM_OK;
+  DDM_CUDA(ctx, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  g_cfg.push_back({(const void*)kernel, shm, ctx->device, -1, 0});
   return DDM_OK;
 }
 
 int pass_grid(ddm_ctx_s* ctx, const void* kernel, size_t shm, int work) {
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kPassWarps * 32, shm);
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+  int per_sm = -1, nsm = 148;
+  {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    for (const auto& c : g_cfg)
+      if (c.kernel == kernel && c.shm == shm && c.device == ctx->device && c.per_sm >= 0) {
+        per_sm = c.per_sm;
+        nsm = c.nsm;
+        break;
+      }
+  }
+  if (per_sm < 0) {
+    per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kPassWarps * 32, shm);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    g_cfg.push_back({kernel, shm, ctx->device, per_sm, nsm});
+  }
   const int by_work = (work + kPassWarps - 1) / kPassWarps;
-  // DDM_PASS_BLOCKS_PER_SM caps the persistent grid so the concurrent near
-  // field keeps SM slots (0 = occupancy limit)
-  // default: 1 block per SM when the near field runs concurrently (measured
-  // best), the occupancy limit when everything is serial
+  // DDM_PASS_BLOCKS_PER_SM caps the grids of the pass kernels so the
+  // concurrent near field keeps SM slots (0 = occupancy limit); default: 1
+  // block per SM when the near field runs concurrently, the occupancy limit
+  // when everything is serial
   static const int env_cap = [] {
     const char* e = getenv("DDM_PASS_BLOCKS_PER_SM");
     return e ? atoi(e) : -1;
@@ -610,26 +722,34 @@ int pass_grid(ddm_ctx_s* ctx, const void* kernel, size_t shm, int work) {
 
 }  // namespace
 
-// upward pass: P2M on all leaves + M2M of every non-leaf cell of level >= 2
+// upward pass: P2M on all leaves, then M2M one level at a time (deepest
+// first), replicated on every rank
 int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
                   const PoroFar& pf, cudaStream_t s) {
+  (void)perm_in;   // D is in sorted order (prep gathered it)
   const int p = t->p;
   const CellGeom cg{t->x_min, t->y_min, t->W};
-  const size_t wsz = std::max(32 * 17, 8 * p);
-  const size_t shm = ((size_t)8 * (p + 2) + (size_t)(p * p + 1) / 2 + (size_t)kPassWarps * wsz) *
+  const size_t shm = ((size_t)8 * (p + 2) + (size_t)(p * p + 1) / 2 + (size_t)kPassWarps * 8 * p) *
                      sizeof(double2);
-  ++t->epoch;
-  DDM_CUDA(ctx, cudaMemsetAsync(t->tickets, 0, 2 * sizeof(int), s));
+  const size_t shp = (size_t)kPassWarps * 32 * 17 * sizeof(double2);
   int rc = DDM_OK;
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \
-    if ((rc = set_smem(ctx, upward_kernel<PT>, shm))) return rc;                                \
-    const int nb = pass_grid(ctx, (const void*)upward_kernel<PT>, shm, t->nleaves + t->n_up);   \
-    upward_kernel<PT><<<nb, kPassWarps * 32, shm, s>>>(                                         \
-        t->nleaves, t->n_up, t->leaves, t->up_list, t->c_level, t->c_ix, t->c_iy, t->c_start,   \
-        t->c_count, t->c_first_child, t->c_nchild, cg, p, perm_in, D, ncomp, t->ex, t->ey,      \
-        t->ea, t->ec, t->es, t->op_pasT, t->op_eps, t->op_e2i, t->mpole, t->ready_up, t->epoch, \
-        t->tickets, pf);                                                                        \
+    if ((rc = set_smem(ctx, p2m_kernel<PT>, shp))) return rc;                                   \
+    const int nb = pass_grid(ctx, (const void*)p2m_kernel<PT>, shp, t->nleaves);                \
+    p2m_kernel<PT><<<nb, kPassWarps * 32, shp, s>>>(t->nleaves, t->leaves, t->c_level, t->c_ix, \
+                                                    t->c_iy, t->c_start, t->c_count, cg, p, D,  \
+                                                    ncomp, t->ex, t->ey, t->ea, t->ec, t->es,   \
+                                                    t->mpole, pf);                              \
+    if ((rc = set_smem(ctx, m2m_level_kernel<PT>, shm))) return rc;                             \
+    for (int lev = t->nlevels - 1; lev >= 2; --lev) {                                           \
+      const int u0 = t->up_level_off[2 * lev], u1 = t->up_level_off[2 * lev + 1];               \
+      if (u1 <= u0) continue;                                                                   \
+      const int nb2 = pass_grid(ctx, (const void*)m2m_level_kernel<PT>, shm, u1 - u0);          \
+      m2m_level_kernel<PT><<<nb2, kPassWarps * 32, shm, s>>>(                                   \
+          u0, u1, t->up_list, t->c_ix, t->c_iy, t->c_first_child, t->c_nchild, p, t->op_pasT,    \
+          t->op_eps, t->op_e2i, t->mpole);                                                      \
+    }                                                                                           \
   } while (0)
   DDM_P_DISPATCH(p, DDM_L);
 #undef DDM_L
@@ -637,24 +757,36 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
   return DDM_OK;
 }
 
-// downward pass: M2L + L2L of every cell of level >= 2, top-down
+// downward pass: M2L of every cell of level >= 2, then L2L one level at a
+// time (top-down), both restricted to subtrees holding owned targets
 int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   if (t->nlevels <= 2) return DDM_OK;
   const int p = t->p;
   const int c0 = t->level_off[2], c1 = t->ncells;
-  const bool reg = (p == 8 || p == 12 || p == 16 || p == 20 || p == 24 || p == 28 || p == 32);
-  const size_t ndbl = (size_t)p * p + (reg ? 0 : (size_t)(p + 1) * p);
-  const size_t shm = ((size_t)(kNOffsets + 8) * (p + 2) + (ndbl + 1) / 2 +
-                      (size_t)kPassWarps * (3 * p + 1)) * sizeof(double2);
+  const bool tc = (p == 8 || p == 12 || p == 16 || p == 20 || p == 24 || p == 28 || p == 32);
+  const size_t ndbl = tc ? (size_t)((p + 7) / 8) * ((p + 4) / 4) * 32 : (size_t)(p + 1) * p;
+  const size_t wstride = tc ? (size_t)2 * kM2LBatch * kXStride : 3 * (size_t)p + 1;
+  const size_t shm = ((tc ? 0 : (size_t)kNOffsets * (p + 2)) + (ndbl + 1) / 2 +
+                      (size_t)kPassWarps * wstride) * sizeof(double2);
+  const size_t shm2 = ((size_t)8 * (p + 2) + (size_t)(p * p + 1) / 2 + (size_t)kPassWarps * 2 * p) *
+                      sizeof(double2);
   int rc = DDM_OK;
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \
-    if ((rc = set_smem(ctx, downward_kernel<PT>, shm))) return rc;                              \
-    const int nb = pass_grid(ctx, (const void*)downward_kernel<PT>, shm, c1 - c0);              \
-    downward_kernel<PT><<<nb, kPassWarps * 32, shm, s>>>(                                       \
-        c0, c1, t->own_el_lo, t->own_el_hi, t->v_off, t->v_idx, t->v_cls, t->c_level, t->c_ix,  \
-        t->c_iy, t->c_start, t->c_count, t->c_parent, p, t->op_w, t->op_eps, t->op_e2i,         \
-        t->op_pas, t->op_pm2l, t->mpole, t->local, t->ready_down, t->epoch, t->tickets + 1);    \
+    if ((rc = set_smem(ctx, m2l_kernel<PT>, shm))) return rc;                                   \
+    const int nb = pass_grid(ctx, (const void*)m2l_kernel<PT>, shm, c1 - c0);                   \
+    m2l_kernel<PT><<<nb, kPassWarps * 32, shm, s>>>(                                            \
+        c0, c1, t->own_el_lo, t->own_el_hi, t->v_off, t->v_idx, t->v_cls, t->c_start,           \
+        t->c_count, p, t->op_w, t->op_pm2l, t->mpole, t->local);                                \
+    if ((rc = set_smem(ctx, l2l_level_kernel<PT>, shm2))) return rc;                            \
+    for (int lev = 3; lev < t->nlevels; ++lev) {                                                \
+      const int a = t->level_off[lev], b = t->level_off[lev + 1];                               \
+      if (b <= a) continue;                                                                     \
+      const int nb2 = pass_grid(ctx, (const void*)l2l_level_kernel<PT>, shm2, b - a);           \
+      l2l_level_kernel<PT><<<nb2, kPassWarps * 32, shm2, s>>>(                                  \
+          a, b, t->own_el_lo, t->own_el_hi, t->c_ix, t->c_iy, t->c_start, t->c_count,           \
+          t->c_parent, p, t->op_eps, t->op_e2i, t->op_pas, t->local);                           \
+    }                                                                                           \
   } while (0)
   DDM_P_DISPATCH(p, DDM_L);
 #undef DDM_L

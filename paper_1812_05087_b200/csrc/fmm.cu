@@ -172,7 +172,8 @@ int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double el
   // upward pass (one persistent launch): P2M on all leaves + M2M finest ->
   // level 2, replicated on all ranks.  Stage "p2m" times the whole upward pass.
   stage_begin(ctx, DDM_ST_P2M, sf);
-  if ((rc = launch_upward(ctx, t, perm_in, D, ncomp, pf, sf))) return rc;
+  // (prep gathered D into sorted order: the upward pass reads it coalesced)
+  if ((rc = launch_upward(ctx, t, nullptr, perm_in ? t->d_sorted : D, ncomp, pf, sf))) return rc;
   stage_end(ctx, DDM_ST_P2M, sf);
 
   // downward pass (one persistent launch): M2L + L2L of every cell of level

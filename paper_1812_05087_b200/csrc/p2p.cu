@@ -17,12 +17,16 @@ __global__ void prep_sources(int64_t n, int ncomp, const int* __restrict__ perm,
                              const double* __restrict__ D, const double* __restrict__ ex,
                              const double* __restrict__ ey, const double* __restrict__ ea,
                              const double* __restrict__ ec, const double* __restrict__ es,
-                             double* __restrict__ src) {
+                             double* __restrict__ src, double* __restrict__ dsort) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int j = perm ? perm[i] : (int)i;
   const double ds = D[(int64_t)j * ncomp + 0];
   const double dn = D[(int64_t)j * ncomp + 1];
+  if (dsort) {   // D gathered into sorted order for the upward pass
+    dsort[i * ncomp + 0] = ds;
+    dsort[i * ncomp + 1] = dn;
+  }
   const double c = ec[i], s = es[i], a = ea[i];
   const double2 B = make_double2(ds * c - dn * s, ds * s + dn * c);
   const double2 r = make_double2(c * c - s * s, -2.0 * c * s);
@@ -216,7 +220,8 @@ direct_kernel(int64_t n, int64_t t_lo, int64_t t_hi, int ncomp, const double* __
 int launch_prep_sources(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D,
                         int ncomp, cudaStream_t s) {
   prep_sources<<<nblk(t->n, 256), 256, 0, s>>>(t->n, ncomp, perm_in, D, t->ex, t->ey, t->ea,
-                                                 t->ec, t->es, t->src);
+                                                 t->ec, t->es, t->src,
+                                                 perm_in ? t->d_sorted : nullptr);
   DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;
 }

@@ -283,7 +283,8 @@ constexpr int kPoroStride = 8;   // {zc, e, a, Ds, Dn, q}
 __global__ void poro_prep(int64_t n, const int* __restrict__ perm, const double* __restrict__ D,
                           const double* __restrict__ ex, const double* __restrict__ ey,
                           const double* __restrict__ ea, const double* __restrict__ ec,
-                          const double* __restrict__ es, double* __restrict__ src) {
+                          const double* __restrict__ es, double* __restrict__ src,
+                          double* __restrict__ dsort) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int j = perm ? perm[i] : (int)i;
@@ -293,9 +294,15 @@ __global__ void poro_prep(int64_t n, const int* __restrict__ perm, const double*
   o[2] = ec[i];
   o[3] = es[i];
   o[4] = ea[i];
-  o[5] = D[(int64_t)j * 3 + 0];
-  o[6] = D[(int64_t)j * 3 + 1];
-  o[7] = D[(int64_t)j * 3 + 2];
+  const double d0 = D[(int64_t)j * 3 + 0], d1 = D[(int64_t)j * 3 + 1], d2 = D[(int64_t)j * 3 + 2];
+  o[5] = d0;
+  o[6] = d1;
+  o[7] = d2;
+  if (dsort) {   // D gathered into sorted order for the upward pass
+    dsort[i * 3 + 0] = d0;
+    dsort[i * 3 + 1] = d1;
+    dsort[i * 3 + 2] = d2;
+  }
 }
 
 // near field: warp per item (<= kTgtGroup targets); lane = (target, slice)
@@ -448,7 +455,7 @@ static PoroConst to_const(const PoroParams& P) {
 int launch_poro_prep(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D,
                      cudaStream_t s) {
   poro_prep<<<nblk(t->n, 256), 256, 0, s>>>(t->n, perm_in, D, t->ex, t->ey, t->ea, t->ec, t->es,
-                                             t->src);
+                                             t->src, perm_in ? t->d_sorted : nullptr);
   DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;
 }

@@ -788,18 +788,22 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
                                   cudaMemcpyDeviceToHost, s));
     DDM_CUDA(ctx, cudaStreamSynchronize(s));
     std::vector<int> up;
-    for (int lev = t->nlevels - 1; lev >= 2; --lev)
+    t->up_level_off.assign(2 * (t->nlevels + 1), 0);
+    for (int lev = t->nlevels - 1; lev >= 2; --lev) {
+      t->up_level_off[2 * lev] = (int)up.size();
       for (int c = t->level_off[lev]; c < t->level_off[lev + 1]; ++c)
         if (!hleaf[c]) up.push_back(c);
+      t->up_level_off[2 * lev + 1] = (int)up.size();
+    }
     t->n_up = (int)up.size();
     if ((rc = dalloc(ctx, &t->up_list, up.size())) || (rc = dalloc(ctx, &t->ready_up, ncells)) ||
-        (rc = dalloc(ctx, &t->ready_down, ncells)) || (rc = dalloc(ctx, &t->tickets, 2)))
+        (rc = dalloc(ctx, &t->ready_down, 2 * (size_t)ncells)) || (rc = dalloc(ctx, &t->tickets, 2)))
       return rc;
     if (!up.empty())
       DDM_CUDA(ctx, cudaMemcpyAsync(t->up_list, up.data(), up.size() * sizeof(int),
                                     cudaMemcpyHostToDevice, s));
     DDM_CUDA(ctx, cudaMemsetAsync(t->ready_up, 0, ncells * sizeof(int), s));
-    DDM_CUDA(ctx, cudaMemsetAsync(t->ready_down, 0, ncells * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMemsetAsync(t->ready_down, 0, 2 * ncells * sizeof(int), s));
   }
   DDM_CUDA(ctx, cudaStreamSynchronize(s));
   return DDM_OK;
