@@ -223,7 +223,7 @@ def run_ours(args):
     # serial schedule: every stage's events bracket that stage's kernels alone
     # (in the timed step the near field overlaps the far-field chain)
     ctx.set_profiling(True, serial=True)
-    stages = {k: 0.0 for k in ("prep", "p2m", "m2m", "m2l", "l2l", "p2p", "final", "comm")}
+    stages = {k: 0.0 for k in ("prep", "p2m", "m2m", "m2l", "l2l", "l2p", "p2p", "final", "comm")}
     nprof = max(3, min(args.steps, 10))
     for _ in range(nprof):
         flush.zero_()

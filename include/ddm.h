@@ -180,13 +180,13 @@ int ddm_sif(ddm_ctx_t ctx, const double* w_tip, const double* ds_tip, const doub
 
 /* Per-stage timings of the last ddm_matvec on this tree (CUDA events, ms),
  * written into ms[DDM_NSTAGES] [host] when profiling is enabled
- * (ddm_set_profiling).  Stages: prep, p2m, m2m, m2l, l2l, p2p, l2p+finalize,
- * exchange.  enable = 0: off; 1: events on the normal schedule (the near
+ * (ddm_set_profiling).  Stages: prep, p2m, m2m, m2l, l2l, p2p, finalize (near +
+ * far sum and scatter), exchange, l2p.  enable = 0: off; 1: events on the normal schedule (the near
  * field runs concurrently with the far-field chain, so stage times overlap);
  * 2: events + serial schedule (every stage on the caller's stream, one after
  * another: each stage time is that stage's kernels alone, for rooflines). */
 enum { DDM_ST_PREP = 0, DDM_ST_P2M, DDM_ST_M2M, DDM_ST_M2L, DDM_ST_L2L, DDM_ST_P2P,
-       DDM_ST_FINAL, DDM_ST_COMM, DDM_NSTAGES };
+       DDM_ST_FINAL, DDM_ST_COMM, DDM_ST_L2P, DDM_NSTAGES };
 int ddm_set_profiling(ddm_ctx_t ctx, int enable);
 int ddm_stage_times(ddm_ctx_t ctx, double* ms);
 

@@ -28,7 +28,7 @@ NCOUNTS = 16
 EX = dict(KEYS=0, PERM=1, ROOT=2, LEVEL=3, IX=4, IY=5, START=6, COUNT=7, PARENT=8,
           FIRST_CHILD=9, NCHILD=10, LEAF=11, V_OFF=12, V_IDX=13, LEAVES=14, U_OFF=15, U_LO=16,
           U_HI=17)
-STAGES = ["prep", "p2m", "m2m", "m2l", "l2l", "p2p", "final", "comm"]
+STAGES = ["prep", "p2m", "m2m", "m2l", "l2l", "p2p", "final", "comm", "l2p"]
 
 
 class Material(C.Structure):

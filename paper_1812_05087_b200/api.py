@@ -89,7 +89,7 @@ class Context:
         self.check(L.ddm_set_profiling(self._h, (2 if serial else 1) if on else 0))
 
     def stage_times(self) -> dict:
-        arr = (C.c_double * 8)()
+        arr = (C.c_double * len(L.STAGES))()
         self.check(L.ddm_stage_times(self._h, arr))
         return dict(zip(L.STAGES, list(arr)))
 

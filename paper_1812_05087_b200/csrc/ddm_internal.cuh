@@ -21,7 +21,10 @@ constexpr int kNOffsets = 49;   // (dx,dy) in [-3,3]^2, class id (dy+3)*7+(dx+3)
 #define DDM_TGT_GROUP 16
 #endif
 constexpr int kTgtGroup = DDM_TGT_GROUP;   // targets per P2P work item (one warp)
-constexpr int kSrcChunk = 512;  // max sources per P2P work item
+#ifndef DDM_SRC_CHUNK
+#define DDM_SRC_CHUNK 512
+#endif
+constexpr int kSrcChunk = DDM_SRC_CHUNK;  // max sources per P2P work item
 constexpr int kSrcStride = 12;  // doubles per P2P source record
 
 struct Status {
@@ -113,6 +116,8 @@ struct ddm_tree_s {
   int* m2l_cells = nullptr;       // (reserved) cells whose subtree meets the owned range
   int n_m2l_cells = 0;
   int item_lo_owned = 0, item_hi_owned = 0;   // P2P items of owned leaves
+  int* p2p_order = nullptr;       // [item_hi_owned - item_lo_owned] owned items, most sources
+                                  // first (longest-processing-time order: no tail)
   // persistent-pass scheduling (expansions.cu)
   int* up_list = nullptr;         // non-leaf cells of level >= 2, deepest level first
   int n_up = 0;
@@ -138,6 +143,7 @@ struct ddm_tree_s {
   double2* part = nullptr;        // [nitems*32] partial tractions
   double* d_sorted = nullptr;     // [n*3] D gathered into sorted order
   double* y_sorted = nullptr;     // [n*3]
+  double* y_far = nullptr;        // [n*3] L2P far field of the owned elements (sorted order)
   double* part_direct = nullptr;  // [n*2] direct-mode tractions (sorted)
   // GMRES workspace
   double* krylov = nullptr;

@@ -593,22 +593,71 @@ l2l_level_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __re
   }
 }
 
-// ------------------------------------------------------------ L2P + finalize (a9, a11)
-// per owned sorted element: sum P2P partials in item order, add the far field
-// from the leaf's local expansion, write (sigma_s, sigma_n).
+// ------------------------------------------------------------ L2P (a9)
+// Thread per owned element (on the far-field stream, overlapping the near
+// field): Phi, Phi', Psi~ of the leaf's local series by Horner (the series are
+// read through L1: the threads of a leaf share them), projected onto the
+// element's frame: y_far[i] = (sigma_s, sigma_n[, p]) in sorted order.
+//   W = i G C (conj(u) Phi' + Psi~),  T = sigma_n + i sigma_s = 2 Re(i G C Phi) + e^{2 i b} W
 template <int PT>
+__global__ void __launch_bounds__(256)
+l2p_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int* __restrict__ el_leaf,
+           const int* __restrict__ leaves, const int* __restrict__ c_level,
+           const int* __restrict__ c_ix, const int* __restrict__ c_iy,
+           const double2* __restrict__ local, CellGeom cg, int p_rt, double gc, PoroFar pf,
+           const double* __restrict__ ex, const double* __restrict__ ey,
+           const double* __restrict__ ec, const double* __restrict__ es,
+           double* __restrict__ y_far) {
+  const int p = PT ? PT : p_rt;
+  const int64_t i = e_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= e_hi) return;
+  const int c = __ldg(leaves + __ldg(el_leaf + i));
+  const int lev = __ldg(c_level + c);
+  double t0 = 0.0, t1 = 0.0, pr = 0.0;
+  if (lev >= 2) {   // no far field above level 2
+    const double s = cg.side(lev), is = 1.0 / s;
+    const double2 z0 = cg.centre(lev, __ldg(c_ix + c), __ldg(c_iy + c));
+    const double2 u = make_double2((ex[i] - z0.x) * is, (ey[i] - z0.y) * is);
+    const double2* L = local + (size_t)c * 2 * p;
+    double2 phi = make_double2(0, 0), dphi = phi, psi = phi;
+#pragma unroll
+    for (int mm = pmax<PT>() - 1; mm >= 0; --mm) {
+      if (!PT && mm >= p) continue;
+      const double2 lm = __ldg(L + mm), gm = __ldg(L + p + mm);
+      if (mm >= 1) {   // dphi = dphi u + mm L[mm]
+        const double fm = (double)mm;
+        dphi = make_double2(fma(dphi.x, u.x, fma(-dphi.y, u.y, fm * lm.x)),
+                            fma(dphi.x, u.y, fma(dphi.y, u.x, fm * lm.y)));
+      }
+      phi = make_double2(fma(phi.x, u.x, fma(-phi.y, u.y, lm.x)),
+                         fma(phi.x, u.y, fma(phi.y, u.x, lm.y)));
+      psi = make_double2(fma(psi.x, u.x, fma(-psi.y, u.y, gm.x)),
+                         fma(psi.x, u.y, fma(psi.y, u.x, gm.y)));
+    }
+    const double2 wv = cadd(cmul(cconj(u), dphi), psi);
+    const double2 W = make_double2(-gc * wv.y, gc * wv.x);
+    const double ct = ec[i], st = es[i];
+    const double2 e2 = make_double2(ct * ct - st * st, 2.0 * ct * st);
+    const double2 t2 = cmul(e2, W);
+    t0 = t2.y;
+    t1 = t2.x - 2.0 * gc * phi.y;
+    // far pore pressure p = -4 k_p Re(i G C Phi)/fu (formula sign), ABI p = -that
+    if (pf.on) pr = -4.0 * pf.kp * gc * phi.y / pf.fu;
+  }
+  y_far[i * ncomp + 0] = t0;
+  y_far[i * ncomp + 1] = t1;
+  if (ncomp == 3) y_far[i * ncomp + 2] = pr;
+}
+
+// ------------------------------------------------------------ finalize (a11)
+// per owned sorted element: near field (sum of the P2P partials of its target
+// group, in item order) + far field (y_far), written in user and/or sorted order
 __global__ void finalize_kernel(int64_t e_lo, int64_t e_hi, int ncomp,
                                 const int* __restrict__ el_leaf, const int* __restrict__ leaves,
-                                const int* __restrict__ c_level, const int* __restrict__ c_ix,
-                                const int* __restrict__ c_iy, const int* __restrict__ c_start,
-                                const int* __restrict__ c_count,
+                                const int* __restrict__ c_start, const int* __restrict__ c_count,
                                 const int* __restrict__ item_off, const double* __restrict__ part,
-                                const double2* __restrict__ local, CellGeom cg, int p_rt,
-                                double gc, PoroFar pf, const double* __restrict__ ex,
-                                const double* __restrict__ ey, const double* __restrict__ ec,
-                                const double* __restrict__ es, const int* __restrict__ perm,
+                                const double* __restrict__ y_far, const int* __restrict__ perm,
                                 double* __restrict__ y_user, double* __restrict__ y_sorted) {
-  const int p = PT ? PT : p_rt;
   const int64_t i = e_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= e_hi) return;
   const int k = el_leaf[i];
@@ -618,48 +667,23 @@ __global__ void finalize_kernel(int64_t e_lo, int64_t e_hi, int ncomp,
   const int i0 = item_off[k];
   const int nch = (item_off[k + 1] - i0) / ngroups;
   const int g = slot / kTgtGroup, ln = slot % kTgtGroup;
-  double2 T = make_double2(0.0, 0.0);
-  double pr = 0.0;
+  double t0 = y_far[i * ncomp], t1 = y_far[i * ncomp + 1];
+  double pr = ncomp == 3 ? y_far[i * ncomp + 2] : 0.0;
   for (int h = 0; h < nch; ++h) {
     const double* pp = part + ((int64_t)(i0 + g * nch + h) * kTgtGroup + ln) * ncomp;
-    T.x += pp[0];
-    T.y += pp[1];
+    t0 += pp[0];
+    t1 += pp[1];
     if (ncomp == 3) pr += pp[2];
   }
-  const int lev = c_level[c];
-  if (lev >= 2) {
-    const double s = cg.side(lev);
-    const double2 z0 = cg.centre(lev, c_ix[c], c_iy[c]);
-    const double2 u = make_double2((ex[i] - z0.x) / s, (ey[i] - z0.y) / s);
-    const double2* L = local + (size_t)c * 2 * p;
-    double2 phi = make_double2(0, 0), dphi = phi, psi = phi;
-#pragma unroll
-    for (int mm = pmax<PT>() - 1; mm >= 0; --mm) {
-      if (!PT && mm >= p) continue;
-      if (mm >= 1) dphi = cadd(cmul(dphi, u), cscale(L[mm], (double)mm));
-      phi = cadd(cmul(phi, u), L[mm]);
-      psi = cadd(cmul(psi, u), L[p + mm]);
-    }
-    // W = i G C (conj(u) dPhi + Psi~), T += 2 Re(i G C Phi) + e^{2 i b} W
-    const double2 wv = cadd(cmul(cconj(u), dphi), psi);
-    const double2 W = make_double2(-gc * wv.y, gc * wv.x);
-    const double ct = ec[i], st = es[i];
-    const double2 e2 = make_double2(ct * ct - st * st, 2.0 * ct * st);
-    const double2 t2 = cmul(e2, W);
-    T.x += t2.y;
-    T.y += t2.x - 2.0 * gc * phi.y;
-    // far pore pressure p = -4 k_p Re(i G C Phi)/fu (formula sign), ABI p = -that
-    if (pf.on) pr -= 4.0 * pf.kp * gc * phi.y / pf.fu;
-  }
   if (y_sorted) {
-    y_sorted[i * ncomp + 0] = T.x;
-    y_sorted[i * ncomp + 1] = T.y;
+    y_sorted[i * ncomp + 0] = t0;
+    y_sorted[i * ncomp + 1] = t1;
     if (ncomp == 3) y_sorted[i * ncomp + 2] = pr;
   }
   if (y_user) {
     const int j = perm[i];
-    y_user[(int64_t)j * ncomp + 0] = T.x;
-    y_user[(int64_t)j * ncomp + 1] = T.y;
+    y_user[(int64_t)j * ncomp + 0] = t0;
+    y_user[(int64_t)j * ncomp + 1] = t1;
     if (ncomp == 3) y_user[(int64_t)j * ncomp + 2] = pr;
   }
 }
@@ -737,11 +761,14 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
   do {                                                                                          \
     if ((rc = set_smem(ctx, p2m_kernel<PT>, shp))) return rc;                                   \
     const int nb = pass_grid(ctx, (const void*)p2m_kernel<PT>, shp, t->nleaves);                \
+    stage_begin(ctx, DDM_ST_P2M, s);                                                            \
     p2m_kernel<PT><<<nb, kPassWarps * 32, shp, s>>>(t->nleaves, t->leaves, t->c_level, t->c_ix, \
                                                     t->c_iy, t->c_start, t->c_count, cg, p, D,  \
                                                     ncomp, t->ex, t->ey, t->ea, t->ec, t->es,   \
                                                     t->mpole, pf);                              \
+    stage_end(ctx, DDM_ST_P2M, s);                                                              \
     if ((rc = set_smem(ctx, m2m_level_kernel<PT>, shm))) return rc;                             \
+    stage_begin(ctx, DDM_ST_M2M, s);                                                            \
     for (int lev = t->nlevels - 1; lev >= 2; --lev) {                                           \
       const int u0 = t->up_level_off[2 * lev], u1 = t->up_level_off[2 * lev + 1];               \
       if (u1 <= u0) continue;                                                                   \
@@ -750,6 +777,7 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
           u0, u1, t->up_list, t->c_ix, t->c_iy, t->c_first_child, t->c_nchild, p, t->op_pasT,    \
           t->op_eps, t->op_e2i, t->mpole);                                                      \
     }                                                                                           \
+    stage_end(ctx, DDM_ST_M2M, s);                                                              \
   } while (0)
   DDM_P_DISPATCH(p, DDM_L);
 #undef DDM_L
@@ -775,10 +803,13 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   do {                                                                                          \
     if ((rc = set_smem(ctx, m2l_kernel<PT>, shm))) return rc;                                   \
     const int nb = pass_grid(ctx, (const void*)m2l_kernel<PT>, shm, c1 - c0);                   \
+    stage_begin(ctx, DDM_ST_M2L, s);                                                            \
     m2l_kernel<PT><<<nb, kPassWarps * 32, shm, s>>>(                                            \
         c0, c1, t->own_el_lo, t->own_el_hi, t->v_off, t->v_idx, t->v_cls, t->c_start,           \
         t->c_count, p, t->op_w, t->op_pm2l, t->mpole, t->local);                                \
+    stage_end(ctx, DDM_ST_M2L, s);                                                              \
     if ((rc = set_smem(ctx, l2l_level_kernel<PT>, shm2))) return rc;                            \
+    stage_begin(ctx, DDM_ST_L2L, s);                                                            \
     for (int lev = 3; lev < t->nlevels; ++lev) {                                                \
       const int a = t->level_off[lev], b = t->level_off[lev + 1];                               \
       if (b <= a) continue;                                                                     \
@@ -787,6 +818,7 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
           a, b, t->own_el_lo, t->own_el_hi, t->c_ix, t->c_iy, t->c_start, t->c_count,           \
           t->c_parent, p, t->op_eps, t->op_e2i, t->op_pas, t->local);                           \
     }                                                                                           \
+    stage_end(ctx, DDM_ST_L2L, s);                                                              \
   } while (0)
   DDM_P_DISPATCH(p, DDM_L);
 #undef DDM_L
@@ -794,19 +826,31 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   return DDM_OK;
 }
 
-int launch_finalize(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, int ncomp, double gc,
-                    const PoroFar& pf, double* y_user, double* y_sorted, cudaStream_t s) {
+// L2P of the owned elements into t->y_far (far-field stream)
+int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFar& pf,
+               cudaStream_t s) {
+  const int64_t lo = t->own_el_lo, hi = t->own_el_hi;
   if (hi <= lo) return DDM_OK;
   const CellGeom cg{t->x_min, t->y_min, t->W};
-  const unsigned nb = nblk(hi - lo, 128);
+  const unsigned nb = nblk(hi - lo, 256);
 #define DDM_L(PT)                                                                               \
-  finalize_kernel<PT><<<nb, 128, 0, s>>>(lo, hi, ncomp, t->el_leaf, t->leaves, t->c_level,      \
-                                         t->c_ix, t->c_iy, t->c_start, t->c_count, t->item_off, \
-                                         reinterpret_cast<const double*>(t->part), t->local, cg, \
-                                         t->p, gc, pf, t->ex, t->ey, t->ec, t->es, t->perm,     \
-                                         y_user, y_sorted)
+  l2p_kernel<PT><<<nb, 256, 0, s>>>(lo, hi, ncomp, t->el_leaf, t->leaves, t->c_level, t->c_ix,  \
+                                    t->c_iy, t->local, cg, t->p, gc, pf, t->ex, t->ey, t->ec,   \
+                                    t->es, t->y_far)
   DDM_P_DISPATCH(t->p, DDM_L);
 #undef DDM_L
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+int launch_finalize(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, int ncomp, double gc,
+                    const PoroFar& pf, double* y_user, double* y_sorted, cudaStream_t s) {
+  (void)gc;
+  (void)pf;
+  if (hi <= lo) return DDM_OK;
+  finalize_kernel<<<nblk(hi - lo, 256), 256, 0, s>>>(
+      lo, hi, ncomp, t->el_leaf, t->leaves, t->c_start, t->c_count, t->item_off,
+      reinterpret_cast<const double*>(t->part), t->y_far, t->perm, y_user, y_sorted);
   DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;
 }

@@ -30,6 +30,7 @@ int ensure_workspace(ddm_ctx_s* ctx, ddm_tree_s* t) {
     if ((rc = dalloc(ctx, &t->part, (size_t)t->nitems * kTgtGroup * 2))) return rc;  // <= 4 doubles/slot
     if ((rc = dalloc(ctx, &t->d_sorted, (size_t)t->n * 3))) return rc;
     if ((rc = dalloc(ctx, &t->y_sorted, (size_t)t->n * 3))) return rc;
+    if ((rc = dalloc(ctx, &t->y_far, (size_t)t->n * 3))) return rc;
   }
   return DDM_OK;
 }
@@ -169,18 +170,16 @@ int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double el
   stage_end(ctx, DDM_ST_P2P, sn);
   DDM_CUDA(ctx, cudaEventRecord(ctx->ev_near, sn));
 
-  // upward pass (one persistent launch): P2M on all leaves + M2M finest ->
-  // level 2, replicated on all ranks.  Stage "p2m" times the whole upward pass.
-  stage_begin(ctx, DDM_ST_P2M, sf);
-  // (prep gathered D into sorted order: the upward pass reads it coalesced)
+  // upward pass: P2M on all leaves, M2M level by level (replicated on all
+  // ranks); prep gathered D into sorted order, so it is read coalesced
   if ((rc = launch_upward(ctx, t, nullptr, perm_in ? t->d_sorted : D, ncomp, pf, sf))) return rc;
-  stage_end(ctx, DDM_ST_P2M, sf);
-
-  // downward pass (one persistent launch): M2L + L2L of every cell of level
-  // >= 2 whose subtree holds owned targets.  Stage "m2l" times the whole pass.
-  stage_begin(ctx, DDM_ST_M2L, sf);
+  // downward pass: M2L of every cell of level >= 2, L2L level by level (cells
+  // whose subtree holds owned targets)
   if ((rc = launch_downward(ctx, t, sf))) return rc;
-  stage_end(ctx, DDM_ST_M2L, sf);
+  // L2P of the owned leaves (far field at the targets), still on the far stream
+  stage_begin(ctx, DDM_ST_L2P, sf);
+  if ((rc = launch_l2p(ctx, t, ncomp, gc, pf, sf))) return rc;
+  stage_end(ctx, DDM_ST_L2P, sf);
   DDM_CUDA(ctx, cudaEventRecord(ctx->ev_far, sf));
 
   // join

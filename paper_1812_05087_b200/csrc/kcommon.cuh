@@ -87,6 +87,8 @@ struct PoroFar;
 int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
                   const PoroFar& pf, cudaStream_t s);
 int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
+int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFar& pf,
+               cudaStream_t s);
 int launch_finalize(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, int ncomp, double gc,
                     const PoroFar& pf, double* y_user, double* y_sorted, cudaStream_t s);
 

@@ -96,10 +96,13 @@ constexpr int kP2PWarps = 4;
 #ifndef DDM_P2P_MINB
 #define DDM_P2P_MINB 6
 #endif
-constexpr int kTPL = kTgtGroup / 8;   // targets per lane (2)
+#ifndef DDM_TPL
+#define DDM_TPL 2
+#endif
+constexpr int kTPL = DDM_TPL;   // targets per lane (independent chains sharing each source load)
 
 __global__ void __launch_bounds__(kP2PWarps * 32, DDM_P2P_MINB)
-p2p_kernel(int item_lo, int item_hi, const int4* __restrict__ items,
+p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ items,
            const int* __restrict__ u_off, const int* __restrict__ u_lo,
            const int* __restrict__ u_hi, const int* __restrict__ leaves,
            const int* __restrict__ c_start, const int* __restrict__ c_count,
@@ -108,8 +111,8 @@ p2p_kernel(int item_lo, int item_hi, const int4* __restrict__ items,
            const double* __restrict__ es, double gc, double2* __restrict__ part) {
   __shared__ double red[kP2PWarps][3][32 * kTPL];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int it = item_lo + blockIdx.x * kP2PWarps + w; it < item_hi;
-       it += gridDim.x * kP2PWarps) {
+  for (int oi = blockIdx.x * kP2PWarps + w; oi < nown; oi += gridDim.x * kP2PWarps) {
+    const int it = order[oi];
     const int4 item = items[it];
     const int k = item.x;
     const int c = leaves[k];
@@ -232,7 +235,8 @@ int launch_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, double g
   // short-lived blocks (4 items each): slots free up continuously, so the
   // high-priority far-field kernels interleave with the near field
   const unsigned nb = nblk(item_hi - item_lo, kP2PWarps);
-  p2p_kernel<<<nb, kP2PWarps * 32, 0, s>>>(item_lo, item_hi, t->items, t->u_off, t->u_lo,
+  p2p_kernel<<<nb, kP2PWarps * 32, 0, s>>>(item_hi - item_lo, t->p2p_order, t->items, t->u_off,
+                                           t->u_lo,
                                            t->u_hi, t->leaves, t->c_start, t->c_count, t->src,
                                            t->ex, t->ey, t->ec, t->es, gc, t->part);
   DDM_CUDA(ctx, cudaGetLastError());

@@ -307,7 +307,7 @@ __global__ void poro_prep(int64_t n, const int* __restrict__ perm, const double*
 
 // near field: warp per item (<= kTgtGroup targets); lane = (target, slice)
 __global__ void __launch_bounds__(128)
-poro_p2p_kernel(int item_lo, int item_hi, const int4* __restrict__ items,
+poro_p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ items,
                 const int* __restrict__ u_off, const int* __restrict__ u_lo,
                 const int* __restrict__ u_hi, const int* __restrict__ leaves,
                 const int* __restrict__ c_start, const int* __restrict__ c_count,
@@ -316,7 +316,8 @@ poro_p2p_kernel(int item_lo, int item_hi, const int4* __restrict__ items,
                 const double* __restrict__ es, PoroConst k, double* __restrict__ part3) {
   __shared__ double red[4][3][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int it = item_lo + blockIdx.x * 4 + w; it < item_hi; it += gridDim.x * 4) {
+  for (int oi = blockIdx.x * 4 + w; oi < nown; oi += gridDim.x * 4) {
+    const int it = order[oi];
     const int4 item = items[it];
     const int kk = item.x;
     const int c = leaves[kk];
@@ -464,7 +465,7 @@ int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, con
                     cudaStream_t s) {
   if (item_hi <= item_lo) return DDM_OK;
   poro_p2p_kernel<<<nblk(item_hi - item_lo, 4), 128, 0, s>>>(
-      item_lo, item_hi, t->items, t->u_off, t->u_lo, t->u_hi, t->leaves, t->c_start, t->c_count,
+      item_hi - item_lo, t->p2p_order, t->items, t->u_off, t->u_lo, t->u_hi, t->leaves, t->c_start, t->c_count,
       t->src, t->ex, t->ey, t->ec, t->es, to_const(P), reinterpret_cast<double*>(t->part));
   DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;

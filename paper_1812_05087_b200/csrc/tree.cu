@@ -458,8 +458,8 @@ void free_tree(ddm_tree_s* t) {
                   t->el_leaf, t->c_level, t->c_ix, t->c_iy, t->c_start, t->c_count,
                   t->c_parent, t->c_first_child, t->c_nchild, t->c_leaf, t->colleagues,
                   t->v_off, t->v_idx, t->v_cls, t->leaves, t->u_off, t->u_lo, t->u_hi,
-                  t->items, t->item_off, t->m2l_cells, t->op_pas, t->op_pasT, t->op_pm2l, t->op_w,
-                  t->op_eps, t->op_e2i, t->mpole, t->local, t->src, t->part, t->d_sorted, t->y_sorted,
+                  t->items, t->item_off, t->p2p_order, t->m2l_cells, t->op_pas, t->op_pasT, t->op_pm2l, t->op_w,
+                  t->op_eps, t->op_e2i, t->mpole, t->local, t->src, t->part, t->d_sorted, t->y_sorted, t->y_far,
                   t->part_direct, t->up_list, t->ready_up, t->ready_down, t->tickets,
                   t->krylov, t->gm_w, t->gm_tmp, t->gm_part};
   for (void* p : ptrs)
