@@ -174,28 +174,45 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
 template <int PT>
 __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* __restrict__ c_iy,
                          const int* __restrict__ first_child, const int* __restrict__ nchild,
-                         const double* pasT, const double2* eps, const double2* e2i,
-                         double2* __restrict__ mpole, double2* xa, double2* xc, int lane) {
+                         const double* __restrict__ pasT, const double2* __restrict__ eps,
+                         const double2* __restrict__ e2i, double2* __restrict__ mpole, double2* xa,
+                         double2* xc, int lane) {
   const int f = first_child[c], nc = nchild[c];
   const int pw = p + 2;
+  constexpr int NC = PT ? (PT + 31) / 32 : 2;   // coefficients per lane
+  // all children's coefficients in flight at once (lane n: slots n, n-1 of both series)
+  double2 an[4][NC], gn[4][NC], ap[4][NC];
   int quad[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    quad[i] = 0;
+    const int q = f + min(i, nc - 1);
+    quad[i] = (c_ix[q] & 1) + 2 * (c_iy[q] & 1);
+    const double2* mq = mpole + (size_t)q * 2 * p;
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+      const int n = lane + 32 * cc;
+      const bool ok = i < nc && n < p;
+      an[i][cc] = ok ? mq[n] : make_double2(0.0, 0.0);
+      gn[i][cc] = ok ? mq[p + n] : make_double2(0.0, 0.0);
+      ap[i][cc] = (ok && n >= 1) ? mq[n - 1] : make_double2(0.0, 0.0);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
     if (i < nc) {
-      const int q = f + i;
-      const int xb = c_ix[q] & 1, yb = c_iy[q] & 1;
-      quad[i] = xb + 2 * yb;
+      const int xb = quad[i] & 1, yb = quad[i] >> 1;
       const double2 eb = make_double2(-(xb - 0.5), (yb - 0.5));   // conj(e)/s_q
-      const double2* mq = mpole + (size_t)q * 2 * p;
       const double2* Ei = e2i + quad[i] * pw;
-      for (int n = lane; n < p; n += 32) {
-        const double2 an = mq[n];
-        double2 cv = mq[p + n];
-        if (n >= 1) cmac(cv, cscale(eb, -(double)n), mq[n - 1]);
-        const double2 sc = Ei[n + 1];
-        xa[i * p + n] = cmul(an, sc);
-        xc[i * p + n] = cmul(cv, sc);
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        const int n = lane + 32 * cc;
+        if (n < p) {
+          double2 cv = gn[i][cc];
+          cmac(cv, cscale(eb, -(double)n), ap[i][cc]);
+          const double2 sc = __ldg(Ei + n + 1);
+          xa[i * p + n] = cmul(an[i][cc], sc);
+          xc[i * p + n] = cmul(cv, sc);
+        }
       }
     }
   }
@@ -208,7 +225,7 @@ __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* 
 #pragma unroll
     for (int n = 0; n < pmax<PT>(); ++n) {
       if (!PT && n >= p) break;
-      const double cm = pasT[n * p + m];   // C(m, n)
+      const double cm = __ldg(pasT + n * p + m);   // C(m, n)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         if (i < nc) {
@@ -224,7 +241,7 @@ __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* 
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (i < nc) {
-        const double2 em = eps[quad[i] * pw + m + 1];
+        const double2 em = __ldg(eps + quad[i] * pw + m + 1);
         cmac(sa, a[i], em);
         cmac(sg, g[i], em);
       }
@@ -263,20 +280,11 @@ m2m_level_kernel(int u0, int u1, const int* __restrict__ up_list, const int* __r
                  const double2* __restrict__ eps_g, const double2* __restrict__ e2i_g,
                  double2* __restrict__ mpole) {
   const int p = PT ? PT : p_rt;
-  const int pw = p + 2;
-  extern __shared__ double2 up_sh[];
-  double2* eps = up_sh;                                       // [4][pw]
-  double2* e2i = eps + 4 * pw;                                // [4][pw]
-  double* pasT = reinterpret_cast<double*>(e2i + 4 * pw);     // [p][p] C(m,n) at n*p+m
-  double2* wbase = e2i + 4 * pw + (p * p + 1) / 2;
-  block_copy(eps, eps_g, 4 * pw);
-  block_copy(e2i, e2i_g, 4 * pw);
-  block_copy(pasT, pasT_g, p * p);
-  __syncthreads();
+  extern __shared__ double2 up_sh[];   // per warp: pre-scaled children [2][4][p]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* wb = wbase + (size_t)w * 8 * p;
+  double2* wb = up_sh + (size_t)w * 8 * p;
   for (int k = u0 + blockIdx.x * kPassWarps + w; k < u1; k += gridDim.x * kPassWarps)
-    m2m_cell<PT>(up_list[k], p, c_ix, c_iy, first_child, nchild, pasT, eps, e2i, mpole, wb,
+    m2m_cell<PT>(up_list[k], p, c_ix, c_iy, first_child, nchild, pasT_g, eps_g, e2i_g, mpole, wb,
                  wb + 4 * p, lane);
 }
 
@@ -320,7 +328,6 @@ __device__ void m2l_cell_tc(int vb, int ve, const int* __restrict__ v_idx,
                             int lane) {
   constexpr int p = PT, pw = PT + 2, P2 = 2 * PT;
   constexpr int MT = (PT + 7) / 8, KS = (PT + 4) / 4, KB = 4 * KS;
-  constexpr int ITEMS = (kM2LBatch * KB + 31) / 32;
   double2 acc[MT];
 #pragma unroll
   for (int i = 0; i < MT; ++i) acc[i] = make_double2(0.0, 0.0);
@@ -334,41 +341,42 @@ __device__ void m2l_cell_tc(int vb, int ve, const int* __restrict__ v_idx,
     }
     for (int b0 = 0; b0 < K; b0 += kM2LBatch) {
       const int nb = min(kM2LBatch, K - b0);
-      // phase 1: loads of all items first
-      double2 ra[ITEMS], rg[ITEMS], rp[ITEMS], rw[ITEMS];
-      int rn[ITEMS], rv[ITEMS], rc[ITEMS];
+      // phase 1: lane n (rounds of 32 over n < KB) loads slots n, n-1 of every
+      // pair of the batch at once (coalesced across lanes), then writes the
+      // pre-scaled X[4 v + comp][n]
+      constexpr int NR = (KB + 31) / 32;
 #pragma unroll
-      for (int r = 0; r < ITEMS; ++r) {
-        const int it = r * 32 + lane;
-        const int v = min(it / KB, kM2LBatch - 1), n = it - v * KB;
-        const int src = __shfl_sync(0xffffffffu, my_src, (b0 + v) & 31);
-        const int cls = __shfl_sync(0xffffffffu, my_cls, (b0 + v) & 31);
-        rn[r] = n;
-        rv[r] = v;
-        rc[r] = cls;
-        const bool ok = v < nb && it < kM2LBatch * KB;
-        const double2* ma = mpole + (size_t)src * P2;
-        const double2 z = make_double2(0.0, 0.0);
-        ra[r] = (ok && n < p) ? __ldg(ma + n) : z;
-        rg[r] = (ok && n < p) ? __ldg(ma + p + n) : z;
-        rp[r] = (ok && n >= 1 && n <= p) ? __ldg(ma + n - 1) : z;
-        rw[r] = (ok && n <= p) ? __ldg(w_g + cls * pw + n + 1) : z;
-      }
+      for (int rr = 0; rr < NR; ++rr) {
+        const int n = lane + 32 * rr;
+        double2 ra[kM2LBatch], rg[kM2LBatch], rp[kM2LBatch], rw[kM2LBatch];
+        int cl[kM2LBatch];
 #pragma unroll
-      for (int r = 0; r < ITEMS; ++r) {
-        const int n = rn[r], v = rv[r];
-        if (v < nb && r * 32 + lane < kM2LBatch * KB) {
-          const double2 av = cmul(ra[r], rw[r]);
-          double2 cv = rg[r];
-          const int cls = rc[r];
-          const double2 dconj = make_double2(-(double)(cls % 7 - 3), (double)(cls / 7 - 3));
-          cmac(cv, cscale(dconj, -(double)n), rp[r]);
-          cv = cmul(cv, rw[r]);
-          double* xc = X + (size_t)(4 * v) * kXStride + n;
-          xc[0] = av.x;
-          xc[kXStride] = av.y;
-          xc[2 * kXStride] = cv.x;
-          xc[3 * kXStride] = cv.y;
+        for (int v = 0; v < kM2LBatch; ++v) {
+          const int src = __shfl_sync(0xffffffffu, my_src, (b0 + v) & 31);
+          cl[v] = __shfl_sync(0xffffffffu, my_cls, (b0 + v) & 31);
+          const double2* ma = mpole + (size_t)src * P2;
+          const double2 z = make_double2(0.0, 0.0);
+          const bool ok = v < nb;
+          ra[v] = (ok && n < p) ? __ldg(ma + n) : z;
+          rg[v] = (ok && n < p) ? __ldg(ma + p + n) : z;
+          rp[v] = (ok && n >= 1 && n <= p) ? __ldg(ma + n - 1) : z;
+          rw[v] = (ok && n <= p) ? __ldg(w_g + cl[v] * pw + n + 1) : z;
+        }
+        if (n < KB) {
+#pragma unroll
+          for (int v = 0; v < kM2LBatch; ++v) {
+            const double2 av = cmul(ra[v], rw[v]);
+            double2 cv = rg[v];
+            const double2 dconj =
+                make_double2(-(double)(cl[v] % 7 - 3), (double)(cl[v] / 7 - 3));   // conj(delta)
+            cmac(cv, cscale(dconj, -(double)n), rp[v]);
+            cv = cmul(cv, rw[v]);
+            double* xc = X + (size_t)(4 * v) * kXStride + n;
+            xc[0] = av.x;
+            xc[kXStride] = av.y;
+            xc[2 * kXStride] = cv.x;
+            xc[3 * kXStride] = cv.y;
+          }
         }
       }
       __syncwarp();
@@ -535,54 +543,64 @@ l2l_level_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __re
                  const double* __restrict__ pas_g, double2* __restrict__ local) {
   const int p = PT ? PT : p_rt;
   const int pw = p + 2;
-  extern __shared__ double2 l2_sh[];
-  double2* sh_eps = l2_sh;                                      // [4][pw]
-  double2* sh_e2i = sh_eps + 4 * pw;                            // [4][pw]
-  double* sh_pas = reinterpret_cast<double*>(sh_e2i + 4 * pw);  // [p][p] C(m,k) at m*p+k
-  double2* wbuf = sh_e2i + 4 * pw + (p * p + 1) / 2;
-  block_copy(sh_eps, eps_g, 4 * pw);
-  block_copy(sh_e2i, e2i_g, 4 * pw);
-  block_copy(sh_pas, pas_g, p * p);
-  __syncthreads();
+  constexpr int NC = PT ? (PT + 31) / 32 : 2;   // coefficients per lane
+  extern __shared__ double2 l2_sh[];   // per warp: xl [p] | xg [p]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* xl = wbuf + (size_t)w * 2 * p;
+  double2* xl = l2_sh + (size_t)w * 2 * p;
   double2* xg = xl + p;
   for (int c = c0 + blockIdx.x * kPassWarps + w; c < c1; c += gridDim.x * kPassWarps) {
     const int cs = c_start[c], ce = cs + c_count[c];
     if (ce <= own_lo || cs >= own_hi) continue;   // no owned target below c
     const int P = c_parent[c];
     const double2* lp = local + (size_t)P * 2 * p;
-    const int xb = c_ix[c] & 1, yb = c_iy[c] & 1;
-    const int quad = xb + 2 * yb;
-    const double2 epsb = make_double2(0.5 * (xb - 0.5), -0.5 * (yb - 0.5));   // conj(eps)
-    const double2* E = sh_eps + quad * pw;
-    const double2* Ei = sh_e2i + quad * pw;
-    for (int m = lane; m < p; m += 32) {
-      double2 gv = lp[p + m];
-      if (m + 1 < p) cmac(gv, cscale(epsb, (double)(m + 1)), lp[m + 1]);
-      const double2 em = E[m];
-      xl[m] = cmul(lp[m], em);
-      xg[m] = cmul(gv, em);
+    double2* out = local + (size_t)c * 2 * p;
+    const int quad = (c_ix[c] & 1) + 2 * (c_iy[c] & 1);
+    // loads first: parent coefficients (slots m, m+1 of lambda, m of gamma) and
+    // this cell's own M2L result
+    double2 pl[NC], pl1[NC], pg[NC], ol[NC], og[NC];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+      const int m = lane + 32 * cc;
+      const bool ok = m < p;
+      const double2 z = make_double2(0.0, 0.0);
+      pl[cc] = ok ? lp[m] : z;
+      pl1[cc] = (ok && m + 1 < p) ? lp[m + 1] : z;
+      pg[cc] = ok ? lp[p + m] : z;
+      ol[cc] = ok ? out[m] : z;
+      og[cc] = ok ? out[p + m] : z;
+    }
+    const double2 epsb = make_double2(0.5 * ((quad & 1) - 0.5), -0.5 * ((quad >> 1) - 0.5));
+    const double2* E = eps_g + quad * pw;
+    const double2* Ei = e2i_g + quad * pw;
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+      const int m = lane + 32 * cc;
+      if (m < p) {
+        double2 gv = pg[cc];
+        cmac(gv, cscale(epsb, (double)(m + 1)), pl1[cc]);
+        const double2 em = __ldg(E + m);
+        xl[m] = cmul(pl[cc], em);
+        xg[m] = cmul(gv, em);
+      }
     }
     __syncwarp();
-    double2* out = local + (size_t)c * 2 * p;
 #pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
+    for (int cc = 0; cc < NC; ++cc) {
       const int k = lane + 32 * cc;
       if (k < p) {
-        double2 al = out[k], ag = out[p + k];
         double2 l = make_double2(0.0, 0.0), g = l;
 #pragma unroll
         for (int m = 0; m < pmax<PT>(); ++m) {
           if (!PT && m >= p) break;
-          const double pc = sh_pas[m * p + k];   // C(m, k)
+          const double pc = __ldg(pas_g + m * p + k);   // C(m, k)
           const double2 x = xl[m], y = xg[m];
           l.x = fma(x.x, pc, l.x);
           l.y = fma(x.y, pc, l.y);
           g.x = fma(y.x, pc, g.x);
           g.y = fma(y.y, pc, g.y);
         }
-        const double2 ek = Ei[k];
+        const double2 ek = __ldg(Ei + k);
+        double2 al = ol[cc], ag = og[cc];
         cmac(al, l, ek);
         cmac(ag, g, ek);
         out[k] = al;
@@ -753,8 +771,7 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
   (void)perm_in;   // D is in sorted order (prep gathered it)
   const int p = t->p;
   const CellGeom cg{t->x_min, t->y_min, t->W};
-  const size_t shm = ((size_t)8 * (p + 2) + (size_t)(p * p + 1) / 2 + (size_t)kPassWarps * 8 * p) *
-                     sizeof(double2);
+  const size_t shm = (size_t)kPassWarps * 8 * p * sizeof(double2);
   const size_t shp = (size_t)kPassWarps * 32 * 17 * sizeof(double2);
   int rc = DDM_OK;
 #define DDM_L(PT)                                                                               \
@@ -796,8 +813,7 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   const size_t wstride = tc ? (size_t)2 * kM2LBatch * kXStride : 3 * (size_t)p + 1;
   const size_t shm = ((tc ? 0 : (size_t)kNOffsets * (p + 2)) + (ndbl + 1) / 2 +
                       (size_t)kPassWarps * wstride) * sizeof(double2);
-  const size_t shm2 = ((size_t)8 * (p + 2) + (size_t)(p * p + 1) / 2 + (size_t)kPassWarps * 2 * p) *
-                      sizeof(double2);
+  const size_t shm2 = (size_t)kPassWarps * 2 * p * sizeof(double2);
   int rc = DDM_OK;
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \
