@@ -55,7 +55,8 @@ typedef enum {
   DDM_ERR_OOM = 6      /* device allocation failed                            */
 } ddm_status;
 
-enum { DDM_FMM = 0, DDM_DIRECT = 1 };
+enum { DDM_FMM = 0, DDM_DIRECT = 1,
+       DDM_HIST_PERLAG = 2 /* ddm_history_apply only: one FMM matvec per lag (the paper's scheme) */ };
 
 /* Material (Table rock_prop).  kind 0 = elastic (only G,
  * nu used), 1 = fully coupled poroelastic.  kappa = k / mu (m^2 / (Pa s)). */
@@ -148,9 +149,18 @@ int ddm_split_costs(const int64_t* prefix_excl, int64_t total, int nleaves, int 
 int ddm_matvec(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, double elapsed,
                const double* D, double* y, int mode, void* stream);
 
-/* r = sum_{m=1}^{h} A^{(m)} D^{h-m}, A^{(m)} = K(( m+1) dt) - K(m dt)
- * (history double sum of Eq.(final_sigs)-(final_pp)).
- * D_hist [device] [h][n][3]; r [device] [n][3].  h = 0 or elastic -> r = 0. */
+/* r = sum_{m=1}^{h} A^{(m)} D^{h-m}, A^{(m)} = K((m+1) dt) - K(m dt)
+ * (history double sum of Eq.(final_sigs)-(final_pp); P:922-929;
+ * reading R10).  D_hist [device] [h][n][3] user order (D^0 .. D^{h-1}, the
+ * caller's storage, only read); r [device] [n][3] user order, overwritten.
+ * h = 0 or elastic -> r = 0.  Written as r = sum_{j=1}^{h+1} K(j dt) E_j,
+ * E_j = D^{h+1-j} - D^{h-j}.  mode DDM_FMM: fast form -- one
+ * far-field pass of the tau-linear far weights on sum_{k<h} D^k plus one
+ * multi-lag near-field launch; needs a tree built with min_leaf_side >=
+ * sqrt(160 c (h+1) dt) + 2 max(a) (else DDM_ERR_ARG).  DDM_HIST_PERLAG: h+1
+ * FMM matvecs (the paper's one-FMM-per-previous-step scheme).
+ * DDM_DIRECT: h+1 exact all-pairs matvecs.  Multi-GPU: r complete on every
+ * rank. */
 int ddm_history_apply(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, double dt,
                       int h, const double* D_hist, double* r, int mode, void* stream);
 

@@ -154,7 +154,8 @@ class Tree:
 
 
 def _mode(mode) -> int:
-    return {"fmm": L.FMM, "direct": L.DIRECT}[mode] if isinstance(mode, str) else int(mode)
+    return ({"fmm": L.FMM, "direct": L.DIRECT, "perlag": L.HIST_PERLAG}[mode]
+            if isinstance(mode, str) else int(mode))
 
 
 def matvec(ctx: Context, tree: Tree, mat, D: torch.Tensor, y: torch.Tensor | None = None,
@@ -169,7 +170,9 @@ def matvec(ctx: Context, tree: Tree, mat, D: torch.Tensor, y: torch.Tensor | Non
 
 def history_apply(ctx, tree, mat, dt: float, D_hist: torch.Tensor, r: torch.Tensor | None = None,
                   mode="fmm", stream=None) -> torch.Tensor:
-    """ddm_history_apply: r = sum_{m=1}^{h} A^(m) D^(h-m); D_hist [h, n, 3]."""
+    """ddm_history_apply: r = sum_{m=1}^{h} A^(m) D^(h-m); D_hist [h, n, 3].
+    mode "fmm" = fast form (one far pass + multi-lag near field), "perlag" =
+    one FMM matvec per lag (the paper's scheme), "direct" = exact per lag."""
     h = D_hist.shape[0]
     if r is None:
         r = torch.empty((tree.n, 3), dtype=torch.float64, device=D_hist.device)

@@ -464,12 +464,26 @@ int ddm_history_apply(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, doub
   int rc = check_material(ctx, mat);
   if (rc) return rc;
   if (h < 0 || !(dt > 0)) return set_error(ctx, DDM_ERR_ARG, "need h >= 0 and dt > 0");
-  if (mode != DDM_FMM && mode != DDM_DIRECT) return set_error(ctx, DDM_ERR_ARG, "bad mode");
+  if (mode != DDM_FMM && mode != DDM_DIRECT && mode != DDM_HIST_PERLAG)
+    return set_error(ctx, DDM_ERR_ARG, "bad mode");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t len = t->n * 3;
   DDM_CUDA(ctx, cudaMemsetAsync(r, 0, (size_t)len * sizeof(double), s));
   if (h == 0 || mat->kind == 0) return DDM_OK;   // empty sum / elastic (R10)
   if (!D_hist) return set_error(ctx, DDM_ERR_ARG, "NULL D_hist");
+  if (mode == DDM_FMM) {   // fast form (f1)
+    if (ctx->world == 1) return fmm_history(ctx, t, mat, dt, h, D_hist, r, nullptr, s);
+    rc = fmm_history(ctx, t, mat, dt, h, D_hist, nullptr, t->y_sorted, s);
+    if (rc) return rc;
+    stage_begin(ctx, DDM_ST_COMM, s);
+    rc = allgather_sorted(ctx, t, t->y_sorted, 3, s);
+    if (rc) return rc;
+    stage_end(ctx, DDM_ST_COMM, s);
+    scatter_user<<<nblk(t->n, 256), 256, 0, s>>>(t->n, 3, t->perm, t->y_sorted, r);
+    DDM_CUDA(ctx, cudaGetLastError());
+    return DDM_OK;
+  }
+  const int mv_mode = mode == DDM_DIRECT ? DDM_DIRECT : DDM_FMM;
   double* E = nullptr;
   double* y = nullptr;
   DDM_CUDA(ctx, cudaMallocAsync((void**)&E, len * sizeof(double), s));
@@ -477,7 +491,7 @@ int ddm_history_apply(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, doub
   for (int j = 1; j <= h + 1 && !rc; ++j) {
     lag_difference<<<nblk(len, 256), 256, 0, s>>>(len, h, j, D_hist, E);
     rc = cuda_error_if(ctx, cudaGetLastError(), "lag_difference");
-    if (!rc) rc = ddm_matvec(ctx, t, mat, j * dt, E, y, mode, stream);
+    if (!rc) rc = ddm_matvec(ctx, t, mat, j * dt, E, y, mv_mode, stream);
     if (!rc) {
       axpy_kernel<<<nblk(len, 256), 256, 0, s>>>(len, y, r);
       rc = cuda_error_if(ctx, cudaGetLastError(), "axpy");

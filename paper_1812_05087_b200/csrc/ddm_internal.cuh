@@ -205,6 +205,10 @@ int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double el
                const double* D, bool d_sorted, double* y_user, double* y_sorted, int mode,
                cudaStream_t s);
 
+// fast history sum (poroelastic): r = sum_{m=1}^{h} A^(m) D^(h-m), D_hist user order
+int fmm_history(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt, int h,
+                const double* D_hist, double* y_user, double* y_sorted, cudaStream_t s);
+
 // gmres.cu
 int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt,
                 const double* b, double* x, double tol, int restart, int max_iter, int mode,

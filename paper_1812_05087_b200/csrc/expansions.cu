@@ -94,12 +94,16 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
       z2 = make_double2(d.x + a * cb * is, d.y + a * sb * is);
       if (pf.on) {
         const double qf = -D[(int64_t)j * ncomp + 2];          // J: q_formula = -q_ABI
-        const double mu = -(pf.eta / pf.S) * dn;
+        const double mu = pf.lin ? 0.0 : -(pf.eta / pf.S) * dn;
         const double wm = (pf.eta * mu / M_PI + pf.eta * qf * pf.ct / (M_PI * pf.kappa)) / pf.gc;
         // (wm / i) conj(e) / s, and 48 eta k_p c tau B / s^3
         Wme = cscale(cmul(make_double2(0.0, -wm), make_double2(cb, -sb)), is);
         Bc = cscale(B, 48.0 * pf.eta * pf.kp * pf.ct * is * is * is);
         fu = pf.fu;
+        if (pf.lin) {   // tau-linear part only: no Phi series, no drained Psi terms
+          fu = 0.0;
+          Q = make_double2(0.0, 0.0);
+        }
       }
       B = cscale(B, is);
       Q = cscale(Q, is);

@@ -191,4 +191,62 @@ int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double el
   return rc;
 }
 
+// Fast history sum:
+//   r = sum_{m=1}^{h} A^(m) D^(h-m) = sum_{j=1}^{h+1} K(j dt) E_j,  E_j = D^(h+1-j) - D^(h-j)
+// (reading R10).  Far field (V pairs, all separated beyond R_c((h+1) dt)): the
+// far form is affine in tau and sum_j E_j = 0, so it is ONE far pass of the
+// tau-linear weights at tau = dt on S = sum_j j E_j = sum_{k<h} D^k.  Near
+// field: one multi-lag launch (poro_hist_near_kernel).  D_hist [h][n][3] user
+// order; writes the owned rows into y_user and/or y_sorted.
+int fmm_history(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt, int h,
+                const double* D_hist, double* y_user, double* y_sorted, cudaStream_t s) {
+  int rc = ensure_workspace(ctx, t);
+  if (rc) return rc;
+  const PoroParams PP = poro_params(mat, dt);
+  if (t->nlevels > 2) {
+    const double ctmax = PP.c * ((h + 1) * dt);
+    const double smin = std::ldexp(t->W, -(t->nlevels - 1));
+    const double sep = smin - 2.0 * t->a_max;
+    if (sep <= 0 || sep * sep / (4.0 * ctmax) <= 40.0)
+      return set_error(ctx, DDM_ERR_ARG,
+                       "tree too fine for the poroelastic far field at the history's longest lag: "
+                       "build it with min_leaf_side >= sqrt(160 c (h+1) dt) + 2 max(a)");
+  }
+  const int64_t n = t->n;
+  double *Hs = nullptr, *Cs = nullptr, *Ctot = nullptr;
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&Hs, (size_t)n * (h + 2) * 3 * sizeof(double), s));
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&Cs, (size_t)n * (h + 1) * 3 * sizeof(double), s));
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&Ctot, (size_t)n * 3 * sizeof(double), s));
+  rc = launch_poro_hist_gather(ctx, t, h, D_hist, Hs, Cs, Ctot, s);
+  // source geometry records (the D fields hold S, unused by the near kernel)
+  if (!rc) rc = launch_poro_prep(ctx, t, nullptr, Ctot, s);
+  if (rc) return rc;
+  DDM_CUDA(ctx, cudaEventRecord(ctx->ev_fork, s));
+  cudaStream_t sf = ctx->serial ? s : ctx->s_hi, sn = ctx->serial ? s : ctx->s_lo;
+  DDM_CUDA(ctx, cudaStreamWaitEvent(sf, ctx->ev_fork, 0));
+  DDM_CUDA(ctx, cudaStreamWaitEvent(sn, ctx->ev_fork, 0));
+  stage_begin(ctx, DDM_ST_P2P, sn);
+  if ((rc = launch_poro_hist_near(ctx, t, PP, h, dt, Hs, Cs, sn))) return rc;
+  stage_end(ctx, DDM_ST_P2P, sn);
+  DDM_CUDA(ctx, cudaEventRecord(ctx->ev_near, sn));
+  PoroFar pf = poro_far(PP);
+  pf.lin = 1;   // tau-linear weights only, at tau = dt
+  const double gc = mat->G / (4.0 * M_PI * (1.0 - mat->nu));
+  if ((rc = launch_upward(ctx, t, nullptr, Ctot, 3, pf, sf))) return rc;
+  if ((rc = launch_downward(ctx, t, sf))) return rc;
+  stage_begin(ctx, DDM_ST_L2P, sf);
+  if ((rc = launch_l2p(ctx, t, 3, gc, pf, sf))) return rc;
+  stage_end(ctx, DDM_ST_L2P, sf);
+  DDM_CUDA(ctx, cudaEventRecord(ctx->ev_far, sf));
+  DDM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_near, 0));
+  DDM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_far, 0));
+  stage_begin(ctx, DDM_ST_FINAL, s);
+  rc = launch_finalize(ctx, t, t->own_el_lo, t->own_el_hi, 3, gc, pf, y_user, y_sorted, s);
+  stage_end(ctx, DDM_ST_FINAL, s);
+  cudaFreeAsync(Hs, s);
+  cudaFreeAsync(Cs, s);
+  cudaFreeAsync(Ctot, s);
+  return rc;
+}
+
 }  // namespace ddm

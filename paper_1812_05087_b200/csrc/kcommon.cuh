@@ -63,8 +63,11 @@ int poro_init_tables(ddm_ctx_s* ctx);
 // (DESIGN.md §4.13): Phi scaled by fu = 1 + 2 eta k_p = (1-nu)/(1-nu_u); Psi~
 // gains the monopole / fluid-source I2 terms and the c tau I4 term; L2P reads
 // p = -4 k_p Re(Phi_total)/fu (formula sign; ABI p = -that).
+// lin = 1: only the part proportional to c tau (the far form is affine in
+// tau: F(tau) = F0 + tau F1) -- the far field of the fast history sum, whose
+// tau-independent part cancels (sum_j E_j = 0).
 struct PoroFar {
-  int on = 0;
+  int on = 0, lin = 0;
   double fu = 1.0, eta = 0, kp = 0, S = 0, kappa = 0, ct = 0, gc = 1.0;
 };
 inline PoroFar poro_far(const PoroParams& P) {
@@ -79,6 +82,10 @@ int launch_poro_prep(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const do
                      cudaStream_t s);
 int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, const PoroParams& P,
                     cudaStream_t s);
+int launch_poro_hist_gather(ddm_ctx_s* ctx, ddm_tree_s* t, int h, const double* D_hist,
+                            double* Hs, double* Cs, double* Ctot, cudaStream_t s);
+int launch_poro_hist_near(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, int h, double dt,
+                          const double* Hs, const double* Cs, cudaStream_t s);
 int launch_poro_direct(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi,
                        const PoroParams& P, double* y_user, double* y_sorted, cudaStream_t s);
 

@@ -228,6 +228,53 @@ __device__ void poro_element(double2 zt, double2 zc, double2 e, double a, double
   T = make_double2(-k.eta * pacc + t2.x, t2.y);
 }
 
+// Far form of the poroelastic part, affine in tau: F(tau) = F0 + tau F1 (the
+// analytic branch of poro_element).  Returns F0(D0) + tau1 F1(D1) for two
+// source triples (formula convention), used by the fast history sum where
+// sum_{j <= j0} F(j dt) E_j = F0(sum E_j) + dt F1(sum j E_j).
+__device__ void poro_far_split(double2 zt, double2 zc, double2 e, double a, double Ds0, double Dn0,
+                               double Ds1, double Dn1, double q1, double tau1, const PoroConst& k,
+                               double2 e2t, double2& T, double& p) {
+  const double2 B0 = make_double2(Ds0 * e.x - Dn0 * e.y, Ds0 * e.y + Dn0 * e.x);
+  const double2 B1 = make_double2(Ds1 * e.x - Dn1 * e.y, Ds1 * e.y + Dn1 * e.x);
+  const double mu0 = -(k.eta / k.S) * Dn0;
+  const double2 z1 = make_double2(zc.x - a * e.x, zc.y - a * e.y);
+  const double2 z2 = make_double2(zc.x + a * e.x, zc.y + a * e.y);
+  const double2 w1 = make_double2(zt.x - z1.x, zt.y - z1.y);
+  const double2 w2 = make_double2(zt.x - z2.x, zt.y - z2.y);
+  auto inv = [](double2 w) {
+    const double n = fma(w.x, w.x, w.y * w.y);
+    return make_double2(w.x / n, -w.y / n);
+  };
+  const double2 r1 = inv(w1), r2 = inv(w2);
+  const double2 I2 = csub(r2, r1);
+  const double2 r12 = cmul(r1, r1), r22 = cmul(r2, r2);
+  const double2 I3 = cscale(csub(r22, r12), 0.5);
+  const double2 I4 = cscale(csub(cmul(r22, r2), cmul(r12, r1)), 1.0 / 3.0);
+  const double2 rr = make_double2(e.x * e.x - e.y * e.y, -2.0 * e.x * e.y);   // conj(e)^2
+  const double2 dz = make_double2(zt.x - zc.x, zt.y - zc.y);
+  double2 X = make_double2(zc.x, -zc.y);
+  cmac(X, rr, dz);
+  const double2 I3b = csub(cmul(X, I3), cmul(rr, I2));
+  const double2 iGC = make_double2(0.0, k.gc);
+  const double2 iGCB0 = cmul(iGC, B0), iGCB1 = cmul(iGC, B1);
+  const double ekp = 2.0 * k.eta * k.kp;
+  const double2 PhiD = cmul(iGCB0, I2);
+  const double2 Phi = cscale(PhiD, ekp);
+  const double2 dPhi = cscale(cmul(iGCB0, I3), -2.0 * ekp);
+  const double ct1 = k.c * tau1;
+  const double wm0 = k.eta * mu0 / M_PI;
+  const double wm1 = k.eta * q1 * ct1 / (M_PI * k.kappa);
+  double2 Psi = cscale(cmul(iGCB0, I3b), 2.0 * ekp);
+  cmac(Psi, cscale(make_double2(e.x, -e.y), wm0 + wm1), I2);
+  cmac(Psi, cscale(iGCB1, 48.0 * k.eta * k.kp * ct1), I4);
+  double2 Wv = Psi;
+  cmac(Wv, make_double2(zt.x, -zt.y), dPhi);
+  const double2 t2 = cmul(e2t, Wv);
+  T = make_double2(2.0 * Phi.x + t2.x, t2.y);
+  p = -k.kp * 4.0 * PhiD.x;
+}
+
 namespace {
 
 // drained elastic KM influence (tension-positive traction T = sigma_n + i sigma_s)
@@ -387,6 +434,147 @@ __global__ void poro_direct_kernel(int64_t n, int64_t t_lo, int64_t t_hi,
   }
 }
 
+// ---------------------------------------------------------------- fast history (f1)
+// D_hist [h][n][3] (user order, ABI) -> Hs[i][k'][3] (sorted element i,
+// k' = 0..h+1 holds D^(k'-1), D^-1 = D^h = 0) and Cs[i][k][3] = sum_{k''<k} D^k''
+// (k = 0..h).  Thread per (element, component).
+__global__ void hist_gather(int64_t n, int h, const int* __restrict__ perm,
+                            const double* __restrict__ Dh, double* __restrict__ Hs,
+                            double* __restrict__ Cs, double* __restrict__ Ctot) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n * 3) return;
+  const int64_t i = t / 3;
+  const int c = (int)(t - i * 3);
+  const int64_t j = perm[i];
+  double* H = Hs + i * (int64_t)(h + 2) * 3 + c;
+  double* C = Cs + i * (int64_t)(h + 1) * 3 + c;
+  H[0] = 0.0;
+  double acc = 0.0;
+  C[0] = 0.0;
+  for (int k = 0; k < h; ++k) {
+    const double d = Dh[((int64_t)k * n + j) * 3 + c];
+    H[(k + 1) * 3] = d;
+    acc += d;
+    C[(k + 1) * 3] = acc;
+  }
+  H[(h + 1) * 3] = 0.0;
+  Ctot[i * 3 + c] = acc;   // C[h] = sum_{k<h} D^k: source of the far pass (sorted)
+}
+
+// Near field of the history sum, one launch for all lags:
+//   r = sum_{j=1}^{h+1} K(j dt) E_j,  E_j = D^(h+1-j) - D^(h-j)
+// The drained part of K is tau independent and sum_j E_j = 0, so only the
+// poroelastic part is summed.  Per pair, lags j <= j0 (the far-form lags of
+// poro_element: dist^2 / (4 c j dt) > 40, the same decision as a per-lag
+// matvec) collapse to F0(S0) + dt F1(S1) with S0 = sum_{j<=j0} E_j = -D^(h-j0)
+// and S1 = sum_{j<=j0} j E_j = C[h] - C[h+1-j0] - j0 D^(h-j0); the remaining
+// lags use the near rule at tau = j dt.
+__global__ void __launch_bounds__(128)
+poro_hist_near_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ items,
+                      const int* __restrict__ u_off, const int* __restrict__ u_lo,
+                      const int* __restrict__ u_hi, const int* __restrict__ leaves,
+                      const int* __restrict__ c_start, const int* __restrict__ c_count,
+                      const double* __restrict__ src, const double* __restrict__ Hs,
+                      const double* __restrict__ Cs, int h, double dt,
+                      const double* __restrict__ ex, const double* __restrict__ ey,
+                      const double* __restrict__ ec, const double* __restrict__ es, PoroConst k,
+                      double* __restrict__ part3) {
+  __shared__ double red[4][3][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hs = (h + 2) * 3, cst = (h + 1) * 3;
+  for (int oi = blockIdx.x * 4 + w; oi < nown; oi += gridDim.x * 4) {
+    const int it = order[oi];
+    const int4 item = items[it];
+    const int kk = item.x;
+    const int c = leaves[kk];
+    const int nt = min(kTgtGroup, c_start[c] + c_count[c] - item.y);
+    const int S = 32 / nt;
+    const int tl = lane % nt, slice = lane / nt;
+    const bool active = slice < S;
+    const int ti = item.y + tl;
+    const double2 zt = make_double2(ex[ti], ey[ti]);
+    const double ctg = ec[ti], stg = es[ti];
+    const double2 e2t = make_double2(ctg * ctg - stg * stg, 2.0 * ctg * stg);
+    double os = 0.0, on = 0.0, op = 0.0;
+    if (active) {
+      int pos = 0;
+      for (int r = u_off[kk], rend = u_off[kk + 1]; r < rend && pos < item.w; ++r) {
+        const int lo = u_lo[r], len = u_hi[r] - lo;
+        const int b = max(item.z - pos, 0), e_ = min(item.w - pos, len);
+        for (int jj = b + slice; jj < e_; jj += S) {
+          const int sidx = lo + jj;
+          const double* sp = src + (int64_t)sidx * kPoroStride;
+          const double2 zc = make_double2(sp[0], sp[1]);
+          const double2 e = make_double2(sp[2], sp[3]);
+          const double a = sp[4];
+          const double* H = Hs + (int64_t)sidx * hs;
+          const double* C = Cs + (int64_t)sidx * cst;
+          // distance of the target to the segment (as poro_element)
+          const double rx = zt.x - zc.x, ry = zt.y - zc.y;
+          const double sstar = rx * e.x + ry * e.y;
+          const double dperp = fabs(-rx * e.y + ry * e.x);
+          const double dist = (fabs(sstar) <= a) ? dperp : hypot(dperp, fabs(sstar) - a);
+          const double d2 = dist * dist;
+          // j0 = number of leading far-form lags (monotone in j)
+          auto is_far = [&](int j) { return d2 / (4.0 * (k.c * (j * dt))) > kUFar; };
+          int j0 = (int)fmin((double)(h + 1), floor(d2 / (4.0 * kUFar * k.c * dt)));
+          j0 = max(j0, 0);
+          while (j0 < h + 1 && is_far(j0 + 1)) ++j0;
+          while (j0 > 0 && !is_far(j0)) --j0;
+          double2 T = make_double2(0.0, 0.0);
+          double p = 0.0;
+          if (j0 > 0) {
+            // S0 = -D^(h-j0) (k' = h-j0+1), S1 = C[h] - C[h+1-j0] - j0 D^(h-j0)
+            const double* Dj = H + (h - j0 + 1) * 3;
+            const double* Ch = C + h * 3;
+            const double* Cl = C + (h + 1 - j0) * 3;
+            const double s0s = -Dj[0], s0n = -Dj[1];
+            const double s1s = Ch[0] - Cl[0] - j0 * Dj[0];
+            const double s1n = Ch[1] - Cl[1] - j0 * Dj[1];
+            const double s1q = Ch[2] - Cl[2] - j0 * Dj[2];
+            poro_far_split(zt, zc, e, a, s0s, s0n, s1s, s1n, -s1q, dt, k, e2t, T, p);
+          }
+          for (int j = j0 + 1; j <= h + 1; ++j) {
+            const double* Da = H + (h + 2 - j) * 3;   // D^(h+1-j)
+            const double* Db = H + (h + 1 - j) * 3;   // D^(h-j)
+            PoroConst kj = k;
+            kj.ct = k.c * (j * dt);
+            double2 Tj;
+            double pj;
+            poro_element(zt, zc, e, a, Da[0] - Db[0], Da[1] - Db[1], -(Da[2] - Db[2]), kj, e2t, Tj,
+                         pj);
+            T.x += Tj.x;
+            T.y += Tj.y;
+            p += pj;
+          }
+          os += T.y;
+          on += T.x;
+          op -= p;   // J: p_ABI = -p_formula
+        }
+        pos += len;
+      }
+      red[w][0][lane] = os;
+      red[w][1][lane] = on;
+      red[w][2][lane] = op;
+    }
+    __syncwarp();
+    if (lane < kTgtGroup) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      if (lane < nt)
+        for (int q = 0; q < S; ++q) {
+          s0 += red[w][0][lane + q * nt];
+          s1 += red[w][1][lane + q * nt];
+          s2 += red[w][2][lane + q * nt];
+        }
+      double* o = part3 + ((int64_t)it * kTgtGroup + lane) * 3;
+      o[0] = s0;
+      o[1] = s1;
+      o[2] = s2;
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 PoroParams poro_params(const ddm_material* m, double tau) {
@@ -477,6 +665,25 @@ int launch_poro_direct(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi,
   poro_direct_kernel<<<nblk(hi - lo, 64), 64, 0, s>>>(t->n, lo, hi, t->src, t->ex, t->ey, t->ec,
                                                       t->es, to_const(P), t->perm, y_user,
                                                       y_sorted);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+int launch_poro_hist_gather(ddm_ctx_s* ctx, ddm_tree_s* t, int h, const double* D_hist,
+                            double* Hs, double* Cs, double* Ctot, cudaStream_t s) {
+  hist_gather<<<nblk(t->n * 3, 256), 256, 0, s>>>(t->n, h, t->perm, D_hist, Hs, Cs, Ctot);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+int launch_poro_hist_near(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, int h, double dt,
+                          const double* Hs, const double* Cs, cudaStream_t s) {
+  const int nown = t->item_hi_owned - t->item_lo_owned;
+  if (nown <= 0) return DDM_OK;
+  poro_hist_near_kernel<<<nblk(nown, 4), 128, 0, s>>>(
+      nown, t->p2p_order, t->items, t->u_off, t->u_lo, t->u_hi, t->leaves, t->c_start,
+      t->c_count, t->src, Hs, Cs, h, dt, t->ex, t->ey, t->ec, t->es, to_const(P),
+      reinterpret_cast<double*>(t->part));
   DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;
 }

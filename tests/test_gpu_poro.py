@@ -172,9 +172,45 @@ def test_poro_history_fmm_and_direct_cfg4(ddm):
     r_dir = D.history_apply(ctx, tree_d, mat, dt, Dt, mode="direct").cpu().numpy()
     tree_f = _tree(D, ctx, torch, g, p=28, min_side=_rc((h + 1) * dt, g))
     r_fmm = D.history_apply(ctx, tree_f, mat, dt, Dt, mode="fmm").cpu().numpy()
+    r_lag = D.history_apply(ctx, tree_f, mat, dt, Dt, mode="perlag").cpu().numpy()
     for c in range(3):
         assert rel_l2(r_dir[:, c], ref[:, c]) <= 1e-11, ("direct", c)
         assert rel_l2(r_fmm[:, c], ref[:, c]) <= 1e-8, ("fmm", c)
+        assert rel_l2(r_lag[:, c], ref[:, c]) <= 1e-8, ("perlag", c)
+
+
+def _subset(g, nfrac):
+    keep = g.frac_id < nfrac
+    return Geometry(g.xc[keep], g.yc[keep], g.half_len[keep], g.beta[keep], g.frac_id[keep],
+                    g.tips[:nfrac])
+
+
+def test_poro_fast_history_many_lags(ddm):
+    # f1: the fast history (one far pass + multi-lag near field)
+    # against the oracle's direct double sum over h = 12 lags, on 8 of config
+    # 4's fractures (400 elements): near pairs switch between the far form and
+    # the near rule at different lags, V pairs take the tau-linear far pass
+    D, ctx, torch = ddm
+    g = _subset(make_config(4), 8)
+    dt = CONFIGS[4]["dt"]
+    h = 12
+    rng = np.random.default_rng(412)
+    Dh = rng.uniform(-1e-3, 1e-3, (h, g.n, 3))
+    Dh[:, :, 2] *= 1e-9
+    K = [None] + [OP.assemble_dense(g, MAT, j * dt) for j in range(1, h + 2)]
+    lags = [None] + [K[m + 1] - K[m] for m in range(1, h + 1)]
+    ref = OH.history_sum(g, dict(MAT, kind=1), dt, Dh, lags)
+    mat = D.material_from_dict(MAT)
+    tree = _tree(D, ctx, torch, g, leaf=16, p=28, min_side=_rc((h + 1) * dt, g))
+    assert tree.counts["LEVELS"] >= 4
+    r = D.history_apply(ctx, tree, mat, dt, torch.tensor(Dh, device="cuda"), mode="fmm")
+    r = r.cpu().numpy()
+    for c in range(3):
+        assert rel_l2(r[:, c], ref[:, c]) <= 1e-8, c
+    # a tree finer than the longest lag's R_c is refused by the fast form
+    fine = _tree(D, ctx, torch, g, leaf=4)
+    with pytest.raises(D.DDMError):
+        D.history_apply(ctx, fine, mat, dt, torch.tensor(Dh, device="cuda"), mode="fmm")
 
 
 def test_poro_history_causal_and_single_element(ddm):
