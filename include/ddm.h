@@ -164,6 +164,13 @@ int ddm_matvec(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, double e
 int ddm_history_apply(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, double dt,
                       int h, const double* D_hist, double* r, int mode, void* stream);
 
+/* Right-hand side of step h of the time marching ("subtracting
+ * the effect of all previous time steps"): rhs = b - sum_{m=1}^{h} A^{(m)} D^{h-m}
+ * (ddm_history_apply with the same mode and errors).  b, rhs [device] [n][3]
+ * user order (may alias). */
+int ddm_history_rhs(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, double dt, int h,
+                    const double* D_hist, const double* b, double* rhs, int mode, void* stream);
+
 /* GMRES (reading R11): solve A(dt) x = b with CGS2 Arnoldi,
  * Givens rotations, restart `restart`, relative tolerance tol on
  * ||b - A x|| / ||b||.  b, x [device] [n][ncomp]; x holds the initial guess

@@ -14,6 +14,7 @@ from .api import (  # noqa: F401
     farfield_rhs,
     gmres_solve,
     history_apply,
+    history_rhs,
     material,
     material_from_dict,
     matvec,
@@ -21,5 +22,7 @@ from .api import (  # noqa: F401
     sif,
     split_costs,
 )
+
+from .march import march  # noqa: F401,E402
 
 __version__ = "0.1.0"

@@ -182,6 +182,18 @@ def history_apply(ctx, tree, mat, dt: float, D_hist: torch.Tensor, r: torch.Tens
     return r
 
 
+def history_rhs(ctx, tree, mat, dt: float, D_hist: torch.Tensor, b: torch.Tensor,
+                rhs: torch.Tensor | None = None, mode="fmm", stream=None) -> torch.Tensor:
+    """ddm_history_rhs: rhs = b - sum_{m=1}^{h} A^(m) D^(h-m) (P:922-929)."""
+    h = D_hist.shape[0]
+    if rhs is None:
+        rhs = torch.empty_like(b)
+    ptr = _dev(D_hist, "D_hist") if h > 0 else 0
+    ctx.check(L.ddm_history_rhs(ctx._h, tree._h, C.byref(mat), float(dt), int(h), ptr,
+                                _dev(b, "b"), _dev(rhs, "rhs"), _mode(mode), _stream_ptr(stream)))
+    return rhs
+
+
 def gmres_solve(ctx, tree, mat, b: torch.Tensor, x: torch.Tensor | None = None, dt: float = 0.0,
                 tol: float = 1e-10, restart: int = 2000, max_iter: int = 10000, mode="fmm",
                 stream=None, raise_noconv: bool = True):

@@ -450,6 +450,13 @@ __global__ void lag_difference(int64_t len, int h, int j, const double* __restri
   E[i] = va - vb;
 }
 
+// out = a - b (elementwise; out may alias a)
+__global__ void sub_kernel(int64_t len, const double* a, const double* __restrict__ b,
+                           double* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < len) out[i] = a[i] - b[i];
+}
+
 __global__ void axpy_kernel(int64_t len, const double* __restrict__ x, double* __restrict__ y) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < len) y[i] += x[i];
@@ -499,6 +506,22 @@ int ddm_history_apply(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, doub
   }
   cudaFreeAsync(E, s);
   cudaFreeAsync(y, s);
+  return rc;
+}
+
+int ddm_history_rhs(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double dt, int h,
+                    const double* D_hist, const double* b, double* rhs, int mode, void* stream) {
+  if (!ctx || !t || !b || !rhs) return ctx ? set_error(ctx, DDM_ERR_ARG, "NULL argument") : DDM_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t len = t->n * 3;
+  double* r = nullptr;
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&r, (size_t)len * sizeof(double), s));
+  int rc = ddm_history_apply(ctx, t, mat, dt, h, D_hist, r, mode, stream);
+  if (!rc) {
+    sub_kernel<<<nblk(len, 256), 256, 0, s>>>(len, b, r, rhs);
+    rc = cuda_error_if(ctx, cudaGetLastError(), "sub_kernel");
+  }
+  cudaFreeAsync(r, s);
   return rc;
 }
 

@@ -1,0 +1,37 @@
+"""FMPDDM time marching (PAPER.md Fig.(algorithm)): the host loop
+around the C-ABI calls.  At step h the right-hand side is the first-step load
+b minus the influence of all previous steps' solutions (ddm_history_rhs,
+P:922-929), then GMRES through the FMM solves A(dt) D^h = rhs.
+Argument marshalling only: every arithmetic step runs in libddm.so."""
+from __future__ import annotations
+
+import time
+
+import torch
+
+from . import api
+
+
+def march(ctx, tree, mat, dt: float, b: torch.Tensor, steps: int, tol: float = 1e-10,
+          restart: int = 2000, max_iter: int = 10000, history_mode: str = "fmm",
+          warm_start: bool = True, stream=None):
+    """Returns (D, stats): D [steps, n, 3] device tensor of the per-step
+    solutions D^0..D^{steps-1}; stats = per-step dicts (iters, rel_resid,
+    history_s, gmres_s) with host wall times around synchronised calls."""
+    n = tree.n
+    D = torch.zeros((steps, n, 3), dtype=torch.float64, device=b.device)
+    rhs = torch.empty_like(b)
+    stats = []
+    for h in range(steps):
+        t0 = time.perf_counter()
+        api.history_rhs(ctx, tree, mat, dt, D[:h], b, rhs, mode=history_mode, stream=stream)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if warm_start and h > 0:
+            D[h].copy_(D[h - 1])
+        _, it, rr = api.gmres_solve(ctx, tree, mat, rhs, x=D[h], dt=dt, tol=tol, restart=restart,
+                                    max_iter=max_iter, stream=stream)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        stats.append({"iters": it, "rel_resid": rr, "history_s": t1 - t0, "gmres_s": t2 - t1})
+    return D, stats

@@ -270,3 +270,26 @@ def test_poro_gmres_cfg3_full_size(ddm):
     mid = nel // 2
     centre = w[:, mid - 1:mid + 1].mean(axis=1)
     assert centre[0] > centre[1] and centre[0] > centre[2] and centre[4] > centre[3]
+
+
+def test_poro_march_vs_oracle(ddm):
+    # FMPDDM time marching (Fig.(algorithm)): history subtraction
+    # (fast form) + GMRES per step on 4 of config 4's fractures, 6 steps,
+    # against the oracle's direct marching (dense lags, LU per step)
+    D, ctx, torch = ddm
+    g = _subset(make_config(4), 4)
+    c = CONFIGS[4]
+    dt, steps, ld = c["dt"], 6, c["load"]
+    bref = OH.poro_rhs(g, ld)
+    ref = OH.march(g, dict(MAT, kind=1), dt, bref, steps)
+    mat = D.material_from_dict(MAT)
+    tree = _tree(D, ctx, torch, g, leaf=16, p=28, min_side=_rc((steps + 1) * dt, g))
+    b = torch.tensor(bref, device="cuda")
+    Dg, stats = D.march(ctx, tree, mat, dt, b, steps, tol=1e-11)
+    Dg = Dg.cpu().numpy()
+    assert all(s["rel_resid"] <= 1e-11 for s in stats)
+    for h in range(steps):
+        for comp in range(3):
+            assert rel_l2(Dg[h, :, comp], ref[h, :, comp]) <= 1e-6, (h, comp)
+    # the solution changes over time (poroelastic relaxation), so the history matters
+    assert rel_l2(Dg[-1], Dg[0]) > 1e-4
