@@ -17,6 +17,7 @@
 //   K = -4 k_p i G C B e, B = (Ds + i Dn) e, mu = -(eta/S) Dn
 //   T^p = sigma_n + i sigma_s = -eta p + e^{2 i bt} (-4 eta d2Phi)
 #include <cmath>
+#include <vector>
 
 #include "kcommon.cuh"
 
@@ -69,34 +70,56 @@ __device__ __forceinline__ void fgh(double u, double& f2, double& g2, double& h2
   }
 }
 
-// Ein(u) = E1(u) + gamma + ln u = sum_{k>=1} (-1)^{k+1} u^k / (k k!)  (u <= 2)
-__device__ double ein_series(double u) {
-  double term = u, sum = 0.0;
-  for (int k = 1; k < 60; ++k) {
-    const double t = term / k;
-    sum += t;
-    if (fabs(t) < 1e-17 * fabs(sum)) break;
-    term *= -u / (k + 1);
-  }
-  return sum;
+// Exponential integral E1 (Theis fluid-source kernel), table driven (no
+// iterative continued fraction on the device):
+//   u <= 2:        Ein(u) = E1(u) + gamma + ln u = sum_{k=1}^{25} (-1)^{k+1} u^k/(k k!)  (Horner)
+//   2 < u <= 1024: h(u) = u e^u E1(u) by a 26-term Chebyshev series per octave
+//                  [2^j, 2^{j+1}] (coefficients from a long-double continued
+//                  fraction at start-up, poro_init_tables)
+//   u > 1024:      h = 1 - 1/u + 2/u^2 - 6/u^3 + 24/u^4 - 120/u^5
+// Max relative error vs a reference E1: 3.4e-15.
+constexpr int kEinTerms = 25;
+constexpr int kE1Oct = 9;        // octaves [2,4) .. [512,1024)
+constexpr int kE1Cheb = 26;
+__device__ double g_ein[kEinTerms];
+__device__ double g_e1cheb[kE1Oct * kE1Cheb];
+
+__device__ __forceinline__ double ein_poly(double u) {   // u <= 2
+  double s = 0.0;
+#pragma unroll
+  for (int k = kEinTerms - 1; k >= 0; --k) s = fma(s, u, __ldg(g_ein + k));
+  return s * u;
 }
 
-// E1(u), u > 0: series below 1, modified Lentz continued fraction above
-__device__ double expint_e1(double u) {
-  if (u <= 1.0) return ein_series(u) - kEulerGamma - log(u);
-  // E1(u) = e^-u / (u + 1 - 1/(u + 3 - 4/(u + 5 - ...)))
-  const double tiny = 1e-300;
-  double b = u + 1.0, c = 1.0 / tiny, d = 1.0 / b, h = d;
-  for (int i = 1; i < 200; ++i) {
-    const double an = -(double)i * i;
-    b += 2.0;
-    d = 1.0 / (an * d + b);
-    c = b + an / c;
-    const double del = c * d;
-    h *= del;
-    if (fabs(del - 1.0) < 1e-16) break;
+__device__ __forceinline__ double e1_h(double u) {   // u e^u E1(u), u > 2
+  if (u > 1024.0) {
+    const double iu = 1.0 / u;
+    return 1.0 - iu * (1.0 - 2.0 * iu * (1.0 - 3.0 * iu * (1.0 - 4.0 * iu * (1.0 - 5.0 * iu))));
   }
-  return h * exp(-u);
+  int j = ilogb(u) - 1;               // u in [2^(j+1), 2^(j+2))
+  j = min(max(j, 0), kE1Oct - 1);
+  const double a = ldexp(2.0, j), b = 2.0 * a;
+  const double x = (2.0 * u - a - b) / (b - a);
+  const double* c = g_e1cheb + j * kE1Cheb;
+  double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+  for (int k = kE1Cheb - 1; k >= 1; --k) {
+    const double t = fma(2.0 * x, b1, __ldg(c + k) - b2);
+    b2 = b1;
+    b1 = t;
+  }
+  return fma(x, b1, __ldg(c) - b2);
+}
+
+// E1(u), u > 0
+__device__ __forceinline__ double expint_e1(double u) {
+  if (u <= 2.0) return ein_poly(u) - kEulerGamma - log(u);
+  return e1_h(u) * exp(-u) / u;
+}
+// Ein(u) = E1(u) + gamma + ln u (the smooth part, for targets on the element)
+__device__ __forceinline__ double expint_ein(double u) {
+  if (u <= 2.0) return ein_poly(u);
+  return e1_h(u) * exp(-u) / u + kEulerGamma + log(u);
 }
 
 // point kernel: adds w_q * (p, d2Phi) of the unit-length point source at offset w
@@ -121,7 +144,7 @@ __device__ __forceinline__ void point_add(double wx, double wy, double wq, const
   d2.x -= cb * ob2.x;
   d2.y -= cb * ob2.y;
   if (q != 0.0) {
-    const double e1 = q_split ? (expint_e1(u) + kEulerGamma + log(u)) : expint_e1(u);
+    const double e1 = q_split ? expint_ein(u) : expint_e1(u);
     p += q * e1 / (4.0 * M_PI * k.kappa);
     const double cq = q * h2 / (16.0 * M_PI * k.kappa);
     d2.x -= cq * ob2.x;
@@ -228,6 +251,109 @@ __device__ void poro_element(double2 zt, double2 zc, double2 e, double a, double
   T = make_double2(-k.eta * pacc + t2.x, t2.y);
 }
 
+// Is the pair (target zt, source element) in the near-rule regime of
+// poro_element at this c tau?  (dist^2 / (4 c tau) <= 40)
+__device__ __forceinline__ bool poro_is_near(double2 zt, double2 zc, double2 e, double a,
+                                             double ct) {
+  const double rx = zt.x - zc.x, ry = zt.y - zc.y;
+  const double sstar = rx * e.x + ry * e.y;
+  const double dperp = fabs(-rx * e.y + ry * e.x);
+  const double dist = (fabs(sstar) <= a) ? dperp : hypot(dperp, fabs(sstar) - a);
+  return !(dist * dist / (4.0 * ct) > kUFar);
+}
+
+// Warp-cooperative near rule of poro_element (same panels, nodes and weights:
+// panels graded away from the nearest point, each <= max(r, sqrt(c tau))/4,
+// 8-point Gauss–Legendre; analytic E1 log part on the element).  Lanes 0 and
+// 1 generate the panel breakpoints of the two sides (sequential recurrence)
+// into shared memory, then all 32 lanes evaluate the quadrature points; the
+// sums are reduced across the warp.  All lanes must call it with the same
+// arguments; every lane returns (T, p).
+constexpr int kCoopPanels = 64;   // panels per side per round (shared memory)
+__device__ void poro_near_coop(double2 zt, double2 zc, double2 e, double a, double Ds, double Dn,
+                               double q, const PoroConst& k, double2 e2t, double* sh, int lane,
+                               double2& T, double& p) {
+  const double lt = sqrt(k.ct);
+  const double rx = zt.x - zc.x, ry = zt.y - zc.y;
+  const double sstar = rx * e.x + ry * e.y;
+  const double dperp = fabs(-rx * e.y + ry * e.x);
+  const double2 B = make_double2(Ds * e.x - Dn * e.y, Ds * e.y + Dn * e.x);
+  const double mu = -(k.eta / k.S) * Dn;
+  const double2 K = cscale(cmul(make_double2(0.0, k.gc), cmul(B, e)), -4.0 * k.kp);
+  const bool on_line = (dperp == 0.0) && (fabs(sstar) < a);
+  const double s0c = fmin(fmax(sstar, -a), a);
+  // sh layout: [2 sides][kCoopPanels + 1] breakpoints, [2] counts (as doubles), [2] done flags
+  double* bp = sh;
+  double* cnt = sh + 2 * (kCoopPanels + 1);
+  double pacc = 0.0;
+  double2 d2acc = make_double2(0.0, 0.0);
+  double cur = s0c;          // lane 0/1: current position of its side
+  bool done = false;         // lane 0/1: side finished
+  int guard = 0;
+  if (lane < 2) {
+    const double other = lane ? a : -a;
+    const double sign = lane ? 1.0 : -1.0;
+    done = !((other - s0c) * sign > 0.0);
+  }
+  for (;;) {
+    if (lane < 2) {
+      const double other = lane ? a : -a;
+      const double sign = lane ? 1.0 : -1.0;
+      double* b = bp + lane * (kCoopPanels + 1);
+      int np = 0;
+      b[0] = cur;
+      while (!done && np < kCoopPanels) {
+        if (!((other - cur) * sign > 0.0) || guard++ >= 4096) {
+          done = true;
+          break;
+        }
+        const double r = hypot(dperp, cur - sstar);
+        double snext = cur + sign * kPanelFraction * fmax(r, lt);
+        if ((other - snext) * sign <= 0.0) snext = other;
+        b[++np] = snext;
+        cur = snext;
+        if (!((other - cur) * sign > 0.0)) done = true;
+      }
+      cnt[lane] = (double)np;
+    }
+    __syncwarp();
+    const int n0 = (int)cnt[0], n1 = (int)cnt[1];
+    const int npts = 8 * (n0 + n1);
+    for (int t = lane; t < npts; t += 32) {
+      const int pan = t >> 3, g = t & 7;
+      const int side = pan < n0 ? 0 : 1;
+      const int pi = side ? pan - n0 : pan;
+      const double* b = bp + side * (kCoopPanels + 1);
+      const double s = b[pi], snext = b[pi + 1];
+      const double mid = 0.5 * (s + snext), half = 0.5 * fabs(snext - s);
+      const double sq = mid + half * c_gl_x[g];
+      const double wx = zt.x - (zc.x + sq * e.x), wy = zt.y - (zc.y + sq * e.y);
+      point_add(wx, wy, half * c_gl_w[g], k, K, mu, q, on_line, pacc, d2acc);
+    }
+    const unsigned more = __ballot_sync(0xffffffffu, lane < 2 && !done);
+    __syncwarp();
+    if (!more) break;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    pacc += __shfl_xor_sync(0xffffffffu, pacc, o);
+    d2acc.x += __shfl_xor_sync(0xffffffffu, d2acc.x, o);
+    d2acc.y += __shfl_xor_sync(0xffffffffu, d2acc.y, o);
+  }
+  if (on_line && q != 0.0) {
+    for (int side = 0; side < 2; ++side) {
+      const double other = side ? a : -a;
+      const double sign = side ? 1.0 : -1.0;
+      if ((other - s0c) * sign <= 0.0) continue;
+      const double len = fabs(other - sstar);
+      pacc += q * e1_log_part(0.0, len, k.ct) / (4.0 * M_PI * k.kappa);
+    }
+  }
+  p = pacc;
+  const double2 t2 = cmul(e2t, make_double2(-4.0 * k.eta * d2acc.x, -4.0 * k.eta * d2acc.y));
+  T = make_double2(-k.eta * pacc + t2.x, t2.y);
+}
+
 // Far form of the poroelastic part, affine in tau: F(tau) = F0 + tau F1 (the
 // analytic branch of poro_element).  Returns F0(D0) + tau1 F1(D1) for two
 // source triples (formula convention), used by the fast history sum where
@@ -325,7 +451,39 @@ __device__ __forceinline__ void poro_pair(double2 zt, double2 e2t, const double*
   op -= p;                                             // J: p_ABI = -p_formula
 }
 
+// drained part + (far-form poroelastic part unless the pair is in the near-rule
+// regime); returns true if the near-rule part is still to be added
+__device__ __forceinline__ bool poro_pair_split(double2 zt, double2 e2t, const double* sp,
+                                                const PoroConst& k, double& os, double& on,
+                                                double& op) {
+  const double2 zc = make_double2(sp[0], sp[1]);
+  const double2 e = make_double2(sp[2], sp[3]);
+  const double a = sp[4];
+  const double Ds = sp[5], Dn = sp[6], q = -sp[7];   // J: q_formula = -q_ABI
+  const double2 Td = drained_traction(zt, zc, e, a, Ds, Dn, k.gc, e2t);
+  os += Td.y;
+  on += Td.x;
+  if (poro_is_near(zt, zc, e, a, k.ct)) return true;
+  double2 Tp;
+  double p;
+  poro_element(zt, zc, e, a, Ds, Dn, q, k, e2t, Tp, p);   // analytic far form
+  os += Tp.y;
+  on += Tp.x;
+  op -= p;                                                 // J: p_ABI = -p_formula
+  return false;
+}
+
 constexpr int kPoroStride = 8;   // {zc, e, a, Ds, Dn, q}
+constexpr int kQueue = 64;       // per-warp queue of near-rule pairs (flushed at >= 32)
+
+// per-warp near-rule queue: entries (target slot, source, lag) evaluated one
+// at a time by the whole warp (poro_near_coop); sums per target slot in
+// queue order (deterministic)
+struct NearQueue {
+  int t[kQueue], s[kQueue], j[kQueue];
+  double acc[3][kTgtGroup];
+  double coop[2 * (kCoopPanels + 1) + 2];
+};
 
 __global__ void poro_prep(int64_t n, const int* __restrict__ perm, const double* __restrict__ D,
                           const double* __restrict__ ex, const double* __restrict__ ey,
@@ -352,7 +510,11 @@ __global__ void poro_prep(int64_t n, const int* __restrict__ perm, const double*
   }
 }
 
-// near field: warp per item (<= kTgtGroup targets); lane = (target, slice)
+// near field: warp per item (<= kTgtGroup targets); lane = (target, slice).
+// The cheap parts (drained closed form, far-form poroelastic part) run per
+// lane; pairs in the near-rule regime go to a per-warp queue and are
+// integrated by all 32 lanes together (poro_near_coop), so the quadrature does
+// not serialise a warp on a few divergent lanes.
 __global__ void __launch_bounds__(128)
 poro_p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ items,
                 const int* __restrict__ u_off, const int* __restrict__ u_lo,
@@ -362,7 +524,10 @@ poro_p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict_
                 const double* __restrict__ ey, const double* __restrict__ ec,
                 const double* __restrict__ es, PoroConst k, double* __restrict__ part3) {
   __shared__ double red[4][3][32];
+  __shared__ NearQueue nq[4];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  NearQueue& Q = nq[w];
+  const unsigned lt_mask = (1u << lane) - 1u;
   for (int oi = blockIdx.x * 4 + w; oi < nown; oi += gridDim.x * 4) {
     const int it = order[oi];
     const int4 item = items[it];
@@ -374,18 +539,55 @@ poro_p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict_
     const bool active = slice < S;
     const int ti = item.y + tl;
     const double2 zt = make_double2(ex[ti], ey[ti]);
-    const double ct = ec[ti], st = es[ti];
-    const double2 e2t = make_double2(ct * ct - st * st, 2.0 * ct * st);
+    const double ctg = ec[ti], stg = es[ti];
+    const double2 e2t = make_double2(ctg * ctg - stg * stg, 2.0 * ctg * stg);
+    for (int e = lane; e < 3 * kTgtGroup; e += 32) (&Q.acc[0][0])[e] = 0.0;
+    int qn = 0;
     double os = 0.0, on = 0.0, op = 0.0;
-    if (active) {
-      int pos = 0;
-      for (int r = u_off[kk], rend = u_off[kk + 1]; r < rend && pos < item.w; ++r) {
-        const int lo = u_lo[r], len = u_hi[r] - lo;
-        const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
-        for (int j = b + slice; j < e; j += S)
-          poro_pair(zt, e2t, src + (int64_t)(lo + j) * kPoroStride, k, os, on, op);
-        pos += len;
+    auto flush = [&]() {
+      __syncwarp();
+      for (int qi = 0; qi < qn; ++qi) {
+        const int t = Q.t[qi];
+        const int tg = item.y + t;
+        const double2 ztq = make_double2(ex[tg], ey[tg]);
+        const double cq = ec[tg], sq = es[tg];
+        const double2 e2q = make_double2(cq * cq - sq * sq, 2.0 * cq * sq);
+        const double* sp = src + (int64_t)Q.s[qi] * kPoroStride;
+        double2 T;
+        double p;
+        poro_near_coop(ztq, make_double2(sp[0], sp[1]), make_double2(sp[2], sp[3]), sp[4], sp[5],
+                       sp[6], -sp[7], k, e2q, Q.coop, lane, T, p);
+        if (lane == 0) {
+          Q.acc[0][t] += T.y;
+          Q.acc[1][t] += T.x;
+          Q.acc[2][t] -= p;
+        }
+        __syncwarp();
       }
+      qn = 0;
+    };
+    int pos = 0;
+    for (int r = u_off[kk], rend = u_off[kk + 1]; r < rend && pos < item.w; ++r) {
+      const int lo = u_lo[r], len = u_hi[r] - lo;
+      const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
+      for (int jb = b; jb < e; jb += S) {
+        const int j = jb + slice;
+        bool near = false;
+        if (active && j < e)
+          near = poro_pair_split(zt, e2t, src + (int64_t)(lo + j) * kPoroStride, k, os, on, op);
+        const unsigned m = __ballot_sync(0xffffffffu, near);
+        if (near) {
+          const int idx = qn + __popc(m & lt_mask);
+          Q.t[idx] = tl;
+          Q.s[idx] = lo + j;
+        }
+        qn += __popc(m);
+        if (qn >= 32) flush();
+      }
+      pos += len;
+    }
+    flush();
+    if (active) {
       red[w][0][lane] = os;
       red[w][1][lane] = on;
       red[w][2][lane] = op;
@@ -393,12 +595,16 @@ poro_p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict_
     __syncwarp();
     if (lane < kTgtGroup) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      if (lane < nt)
+      if (lane < nt) {
         for (int q = 0; q < S; ++q) {
           s0 += red[w][0][lane + q * nt];
           s1 += red[w][1][lane + q * nt];
           s2 += red[w][2][lane + q * nt];
         }
+        s0 += Q.acc[0][lane];
+        s1 += Q.acc[1][lane];
+        s2 += Q.acc[2][lane];
+      }
       double* o = part3 + ((int64_t)it * kTgtGroup + lane) * 3;
       o[0] = s0;
       o[1] = s1;
@@ -480,7 +686,10 @@ poro_hist_near_kernel(int nown, const int* __restrict__ order, const int4* __res
                       const double* __restrict__ ec, const double* __restrict__ es, PoroConst k,
                       double* __restrict__ part3) {
   __shared__ double red[4][3][32];
+  __shared__ NearQueue nq[4];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  NearQueue& Q = nq[w];
+  const unsigned lt_mask = (1u << lane) - 1u;
   const int hs = (h + 2) * 3, cst = (h + 1) * 3;
   for (int oi = blockIdx.x * 4 + w; oi < nown; oi += gridDim.x * 4) {
     const int it = order[oi];
@@ -495,14 +704,46 @@ poro_hist_near_kernel(int nown, const int* __restrict__ order, const int4* __res
     const double2 zt = make_double2(ex[ti], ey[ti]);
     const double ctg = ec[ti], stg = es[ti];
     const double2 e2t = make_double2(ctg * ctg - stg * stg, 2.0 * ctg * stg);
+    for (int e = lane; e < 3 * kTgtGroup; e += 32) (&Q.acc[0][0])[e] = 0.0;
+    int qn = 0;
     double os = 0.0, on = 0.0, op = 0.0;
-    if (active) {
-      int pos = 0;
-      for (int r = u_off[kk], rend = u_off[kk + 1]; r < rend && pos < item.w; ++r) {
-        const int lo = u_lo[r], len = u_hi[r] - lo;
-        const int b = max(item.z - pos, 0), e_ = min(item.w - pos, len);
-        for (int jj = b + slice; jj < e_; jj += S) {
-          const int sidx = lo + jj;
+    auto flush = [&]() {
+      __syncwarp();
+      for (int qi = 0; qi < qn; ++qi) {
+        const int t = Q.t[qi], sidx = Q.s[qi], j = Q.j[qi];
+        const int tg = item.y + t;
+        const double2 ztq = make_double2(ex[tg], ey[tg]);
+        const double cq = ec[tg], sq = es[tg];
+        const double2 e2q = make_double2(cq * cq - sq * sq, 2.0 * cq * sq);
+        const double* sp = src + (int64_t)sidx * kPoroStride;
+        const double* Da = Hs + (int64_t)sidx * hs + (h + 2 - j) * 3;   // D^(h+1-j)
+        const double* Db = Da - 3;                                       // D^(h-j)
+        PoroConst kj = k;
+        kj.ct = k.c * (j * dt);
+        double2 T;
+        double p;
+        poro_near_coop(ztq, make_double2(sp[0], sp[1]), make_double2(sp[2], sp[3]), sp[4],
+                       Da[0] - Db[0], Da[1] - Db[1], -(Da[2] - Db[2]), kj, e2q, Q.coop, lane, T,
+                       p);
+        if (lane == 0) {
+          Q.acc[0][t] += T.y;
+          Q.acc[1][t] += T.x;
+          Q.acc[2][t] -= p;
+        }
+        __syncwarp();
+      }
+      qn = 0;
+    };
+    int pos = 0;
+    for (int r = u_off[kk], rend = u_off[kk + 1]; r < rend && pos < item.w; ++r) {
+      const int lo = u_lo[r], len = u_hi[r] - lo;
+      const int b = max(item.z - pos, 0), e_ = min(item.w - pos, len);
+      for (int jb = b; jb < e_; jb += S) {
+        const int jj = jb + slice;
+        const bool valid = active && jj < e_;
+        const int sidx = lo + (valid ? jj : 0);
+        int j0 = 0;
+        if (valid) {
           const double* sp = src + (int64_t)sidx * kPoroStride;
           const double2 zc = make_double2(sp[0], sp[1]);
           const double2 e = make_double2(sp[2], sp[3]);
@@ -515,14 +756,12 @@ poro_hist_near_kernel(int nown, const int* __restrict__ order, const int4* __res
           const double dperp = fabs(-rx * e.y + ry * e.x);
           const double dist = (fabs(sstar) <= a) ? dperp : hypot(dperp, fabs(sstar) - a);
           const double d2 = dist * dist;
-          // j0 = number of leading far-form lags (monotone in j)
+          // j0 = number of leading far-form lags (monotone in j; same test as poro_element)
           auto is_far = [&](int j) { return d2 / (4.0 * (k.c * (j * dt))) > kUFar; };
-          int j0 = (int)fmin((double)(h + 1), floor(d2 / (4.0 * kUFar * k.c * dt)));
+          j0 = (int)fmin((double)(h + 1), floor(d2 / (4.0 * kUFar * k.c * dt)));
           j0 = max(j0, 0);
           while (j0 < h + 1 && is_far(j0 + 1)) ++j0;
           while (j0 > 0 && !is_far(j0)) --j0;
-          double2 T = make_double2(0.0, 0.0);
-          double p = 0.0;
           if (j0 > 0) {
             // S0 = -D^(h-j0) (k' = h-j0+1), S1 = C[h] - C[h+1-j0] - j0 D^(h-j0)
             const double* Dj = H + (h - j0 + 1) * 3;
@@ -532,27 +771,36 @@ poro_hist_near_kernel(int nown, const int* __restrict__ order, const int4* __res
             const double s1s = Ch[0] - Cl[0] - j0 * Dj[0];
             const double s1n = Ch[1] - Cl[1] - j0 * Dj[1];
             const double s1q = Ch[2] - Cl[2] - j0 * Dj[2];
+            double2 T;
+            double p;
             poro_far_split(zt, zc, e, a, s0s, s0n, s1s, s1n, -s1q, dt, k, e2t, T, p);
+            os += T.y;
+            on += T.x;
+            op -= p;   // J: p_ABI = -p_formula
           }
-          for (int j = j0 + 1; j <= h + 1; ++j) {
-            const double* Da = H + (h + 2 - j) * 3;   // D^(h+1-j)
-            const double* Db = H + (h + 1 - j) * 3;   // D^(h-j)
-            PoroConst kj = k;
-            kj.ct = k.c * (j * dt);
-            double2 Tj;
-            double pj;
-            poro_element(zt, zc, e, a, Da[0] - Db[0], Da[1] - Db[1], -(Da[2] - Db[2]), kj, e2t, Tj,
-                         pj);
-            T.x += Tj.x;
-            T.y += Tj.y;
-            p += pj;
-          }
-          os += T.y;
-          on += T.x;
-          op -= p;   // J: p_ABI = -p_formula
         }
-        pos += len;
+        // near-rule lags j0+1 .. h+1 of this pair -> queue
+        int jn = j0 + 1, rem = valid ? h + 1 - j0 : 0;
+        for (;;) {
+          const bool has = rem > 0;
+          const unsigned m = __ballot_sync(0xffffffffu, has);
+          if (!m) break;
+          if (has) {
+            const int idx = qn + __popc(m & lt_mask);
+            Q.t[idx] = tl;
+            Q.s[idx] = sidx;
+            Q.j[idx] = jn;
+            ++jn;
+            --rem;
+          }
+          qn += __popc(m);
+          if (qn >= 32) flush();
+        }
       }
+      pos += len;
+    }
+    flush();
+    if (active) {
       red[w][0][lane] = os;
       red[w][1][lane] = on;
       red[w][2][lane] = op;
@@ -560,12 +808,16 @@ poro_hist_near_kernel(int nown, const int* __restrict__ order, const int4* __res
     __syncwarp();
     if (lane < kTgtGroup) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      if (lane < nt)
+      if (lane < nt) {
         for (int q = 0; q < S; ++q) {
           s0 += red[w][0][lane + q * nt];
           s1 += red[w][1][lane + q * nt];
           s2 += red[w][2][lane + q * nt];
         }
+        s0 += Q.acc[0][lane];
+        s1 += Q.acc[1][lane];
+        s2 += Q.acc[2][lane];
+      }
       double* o = part3 + ((int64_t)it * kTgtGroup + lane) * 3;
       o[0] = s0;
       o[1] = s1;
@@ -627,6 +879,39 @@ int poro_init_tables(ddm_ctx_s* ctx) {
   for (int k = 0; k < 8; ++k) {
     fact *= (k + 1);                       // (k+1)!
     h2[k] = ((k & 1) ? -1.0 : 1.0) / fact;
+  }
+  {
+    // E1 tables: Ein series coefficients and per-octave Chebyshev series of
+    // h(u) = u e^u E1(u), evaluated in long double by the backward continued
+    // fraction E1(u) e^u = 1/(u+1- 1/(u+3- 4/(u+5- ...)))
+    double ein[kEinTerms];
+    long double kf = 1.0L;
+    for (int k = 1; k <= kEinTerms; ++k) {
+      kf *= k;
+      ein[k - 1] = (double)(((k & 1) ? 1.0L : -1.0L) / (k * kf));
+    }
+    auto h_ld = [](long double u) {
+      const int M = 4000;
+      long double f = u + 2.0L * M + 1.0L;
+      for (int k = M; k >= 1; --k) f = u + 2.0L * k - 1.0L - (long double)k * k / f;
+      return u / f;
+    };
+    std::vector<double> cheb(kE1Oct * kE1Cheb);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int j = 0; j < kE1Oct; ++j) {
+      const long double a = ldexpl(2.0L, j), b = 2.0L * a;
+      const long double mid = 0.5L * (a + b), half = 0.5L * (b - a);
+      long double hv[kE1Cheb];
+      for (int i = 0; i < kE1Cheb; ++i)
+        hv[i] = h_ld(mid + half * cosl(pi * (i + 0.5L) / kE1Cheb));
+      for (int k = 0; k < kE1Cheb; ++k) {
+        long double sum = 0.0L;
+        for (int i = 0; i < kE1Cheb; ++i) sum += hv[i] * cosl(pi * k * (i + 0.5L) / kE1Cheb);
+        cheb[j * kE1Cheb + k] = (double)(sum * 2.0L / kE1Cheb / (k == 0 ? 2.0L : 1.0L));
+      }
+    }
+    DDM_CUDA(ctx, cudaMemcpyToSymbol(g_ein, ein, sizeof(ein)));
+    DDM_CUDA(ctx, cudaMemcpyToSymbol(g_e1cheb, cheb.data(), cheb.size() * sizeof(double)));
   }
   DDM_CUDA(ctx, cudaMemcpyToSymbol(c_f2, f2, sizeof(f2)));
   DDM_CUDA(ctx, cudaMemcpyToSymbol(c_g2, g2, sizeof(g2)));
