@@ -275,7 +275,7 @@ def run_ours(args):
 
     if rank == 0 and world == 1 and not args.no_extras:
         # GMRES solve time on config 2 (the metric's second half), at p and p*
-        out["gmres"] = gmres_extra(D, ctx, torch, dev)
+        out["gmres"] = gmres_extra(D, ctx, torch, dev, args.march_steps)
         gv, gdt = cpu_baseline_oracle(g, c["material"], Dv_host, args.cpu_rows)
         out["cpu_baseline"] = {"value": gv, "unit": UNIT, "cores": 1, "kind": "oracle",
                                "sample": f"{args.cpu_rows} seeded target rows x all {n} sources "
@@ -306,26 +306,88 @@ def ctx_probe_fp64(ctx) -> float:
     return v.value if rc == 0 else None
 
 
-def gmres_extra(D, ctx, torch, dev):
+def _poro_rc(c, g, tau):
+    """sqrt(160 c tau) + 2 max(a): the min leaf side for the poroelastic far field."""
+    m = c["material"]
+    G, nu, nuu, al, kap = m["G"], m["nu"], m["nu_u"], m["alpha"], m["kappa"]
+    M = 2 * G * (nuu - nu) / (al * al * (1 - 2 * nuu) * (1 - 2 * nu))
+    S = al * al * (1 - 2 * nu) / (2 * G * (1 - nu)) + 1 / M
+    return (160 * (kap / S) * tau) ** 0.5 + 2 * float(g.half_len.max())
+
+
+def gmres_extra(D, ctx, torch, dev, march_steps: int):
+    """The metric's second half: GMRES solve times (device-synchronised wall
+    clock around ddm_gmres_solve) on config 2 (elastic, p and p*) and config 3
+    (poroelastic, full size), poroelastic matvec times, and config 4 time
+    marching (history + GMRES per step) for the first `march_steps` steps,
+    with the history sum timed in the fast form and per lag at the last step."""
     from synth import CONFIGS, make_config
     res = {}
+    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
+
+    def timed(fn, reps=1):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            r = fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / reps * 1e3, r
+
     g = make_config(2)
     c = CONFIGS[2]
-    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
     mat = D.material_from_dict(c["material"])
     for p in (c["p"], c["p_star"]):
         tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=c["leaf"],
                       order_p=p)
         ld = c["load"]
         b = D.farfield_rhs(ctx, f(g.beta), 2, ld["p_f"], ld["sH"], ld["sh"])
-        D.gmres_solve(ctx, tree, mat, b, tol=c["tol"])   # warm-up
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        x, it, rr = D.gmres_solve(ctx, tree, mat, b, tol=c["tol"])
-        torch.cuda.synchronize()
-        res[f"cfg2_p{p}"] = {"solve_ms": 1e3 * (time.perf_counter() - t0), "iters": it,
-                             "rel_resid": rr}
+        ms, (x, it, rr) = timed(lambda: D.gmres_solve(ctx, tree, mat, b, tol=c["tol"]))
+        res[f"cfg2_p{p}"] = {"solve_ms": ms, "iters": it, "rel_resid": rr}
         tree.free()
+    # config 3: poroelastic, N = 20000 (60000 unknowns), one temporal element
+    g = make_config(3)
+    c = CONFIGS[3]
+    mat = D.material_from_dict(c["material"])
+    tau = c["dt"]
+    tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=c["leaf"],
+                  order_p=c["p_star"], min_leaf_side=_poro_rc(c, g, tau))
+    ld = c["load"]
+    b = D.farfield_rhs(ctx, f(g.beta), 3, ld["p_f"], ld["sH"], ld["sh"], net=True,
+                       b_p=ld["sh"] + ld["p_f"] - ld["p0"])
+    y = torch.empty_like(b)
+    mv_ms, _ = timed(lambda: D.matvec(ctx, tree, mat, b, y, elapsed=tau), reps=10)
+    ms, (x, it, rr) = timed(lambda: D.gmres_solve(ctx, tree, mat, b, dt=tau, tol=c["tol"],
+                                                   restart=3000, max_iter=6000))
+    res["cfg3_poro"] = {"solve_ms": ms, "iters": it, "rel_resid": rr, "matvec_ms": mv_ms,
+                        "p": c["p_star"], "near_pairs": tree.counts["NEAR_PAIRS"]}
+    tree.free()
+    # config 4: poroelastic time marching (first march_steps of the 200 steps)
+    g = make_config(4)
+    c = CONFIGS[4]
+    mat = D.material_from_dict(c["material"])
+    dt = c["dt"]
+    tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=c["leaf"],
+                  order_p=c["p"], min_leaf_side=_poro_rc(c, g, (c["steps"] + 1) * dt))
+    ld = c["load"]
+    b = D.farfield_rhs(ctx, f(g.beta), 3, ld["p_f"], ld["sH"], ld["sh"], net=False,
+                       b_p=ld["p_f"] - ld["p0"])
+    y = torch.empty_like(b)
+    mv_ms, _ = timed(lambda: D.matvec(ctx, tree, mat, b, y, elapsed=dt), reps=10)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    Dh, st = D.march(ctx, tree, mat, dt, b, march_steps, tol=c["tol"])
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    h = march_steps - 1
+    hf, _ = timed(lambda: D.history_apply(ctx, tree, mat, dt, Dh[:h], mode="fmm"))
+    hp, _ = timed(lambda: D.history_apply(ctx, tree, mat, dt, Dh[:h], mode="perlag"))
+    res["cfg4_march"] = {"steps": march_steps, "of_steps": c["steps"], "wall_s": wall,
+                         "gmres_iters": [s["iters"] for s in st],
+                         "gmres_s": sum(s["gmres_s"] for s in st),
+                         "history_s": sum(s["history_s"] for s in st), "matvec_ms": mv_ms,
+                         f"history_fast_h{h}_ms": hf, f"history_perlag_h{h}_ms": hp}
+    tree.free()
     return res
 
 
@@ -340,6 +402,7 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=64)
     ap.add_argument("--ref-rows", type=int, default=16)
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--march-steps", type=int, default=10)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
