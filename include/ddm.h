@@ -56,7 +56,8 @@ typedef enum {
 } ddm_status;
 
 enum { DDM_FMM = 0, DDM_DIRECT = 1,
-       DDM_HIST_PERLAG = 2 /* ddm_history_apply only: one FMM matvec per lag (the paper's scheme) */ };
+       DDM_HIST_PERLAG = 2, /* ddm_history_apply only: one FMM matvec per lag (the paper's scheme) */
+       DDM_GMRES_NO_PRECOND = 8 /* ddm_gmres_solve only, OR-ed into mode: plain GMRES */ };
 
 /* Material (Table rock_prop).  kind 0 = elastic (only G,
  * nu used), 1 = fully coupled poroelastic.  kappa = k / mu (m^2 / (Pa s)). */
@@ -173,7 +174,10 @@ int ddm_history_rhs(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, dou
 
 /* GMRES (reading R11): solve A(dt) x = b with CGS2 Arnoldi,
  * Givens rotations, restart `restart`, relative tolerance tol on
- * ||b - A x|| / ||b||.  b, x [device] [n][ncomp]; x holds the initial guess
+ * ||b - A x|| / ||b|| (the true residual: right preconditioning).  The
+ * operator is right-preconditioned by the inverse element self blocks
+ * (block Jacobi, 2x2 elastic / 3x3 poroelastic) unless
+ * DDM_GMRES_NO_PRECOND is OR-ed into mode (DDM_FMM or DDM_DIRECT).  b, x [device] [n][ncomp]; x holds the initial guess
  * on entry and the solution on return.  iters, rel_resid [host] outputs
  * (rel_resid = explicit true residual at exit).  b = 0 -> x = 0, iters = 0.
  * Returns DDM_ERR_NOCONV with x = last iterate if max_iter is reached. */

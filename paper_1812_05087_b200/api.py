@@ -196,14 +196,16 @@ def history_rhs(ctx, tree, mat, dt: float, D_hist: torch.Tensor, b: torch.Tensor
 
 def gmres_solve(ctx, tree, mat, b: torch.Tensor, x: torch.Tensor | None = None, dt: float = 0.0,
                 tol: float = 1e-10, restart: int = 2000, max_iter: int = 10000, mode="fmm",
-                stream=None, raise_noconv: bool = True):
-    """ddm_gmres_solve: returns (x, iters, rel_resid)."""
+                stream=None, raise_noconv: bool = True, precond: bool = True):
+    """ddm_gmres_solve: returns (x, iters, rel_resid).  precond: block-Jacobi
+    right preconditioning (inverse element self blocks); False = plain GMRES."""
     if x is None:
         x = torch.zeros_like(b)
     it = C.c_int(0)
     rr = C.c_double(0.0)
     rc = L.ddm_gmres_solve(ctx._h, tree._h, C.byref(mat), float(dt), _dev(b, "b"), _dev(x, "x"),
-                           float(tol), int(restart), int(max_iter), _mode(mode), C.byref(it),
+                           float(tol), int(restart), int(max_iter),
+                           _mode(mode) | (0 if precond else L.GMRES_NO_PRECOND), C.byref(it),
                            C.byref(rr), _stream_ptr(stream))
     if rc == L.ERR_NOCONV and not raise_noconv:
         return x, it.value, rr.value

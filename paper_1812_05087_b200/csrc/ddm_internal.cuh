@@ -145,6 +145,10 @@ struct ddm_tree_s {
   double* y_sorted = nullptr;     // [n*3]
   double* y_far = nullptr;        // [n*3] L2P far field of the owned elements (sorted order)
   double* part_direct = nullptr;  // [n*2] direct-mode tractions (sorted)
+  // GMRES block-Jacobi preconditioner: inverse self blocks [n][ncomp][ncomp]
+  // (sorted order) for the material / elapsed time in pc_key
+  double* pc = nullptr;
+  double pc_key[8] = {};
   // GMRES workspace
   double* krylov = nullptr;
   int krylov_m = 0;

@@ -10,9 +10,10 @@
 // least-squares problem is solved on the host.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <vector>
 
-#include "ddm_internal.cuh"
+#include "kcommon.cuh"
 
 namespace ddm {
 namespace {
@@ -95,7 +96,56 @@ __global__ void scatter_to_user(int64_t n, int ncomp, const int* __restrict__ pe
   for (int c = 0; c < ncomp; ++c) out[(int64_t)j * ncomp + c] = in[i * ncomp + c];
 }
 
-inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+// in place: blk[e] <- inverse(blk[e]) (ncomp x ncomp, row major); a singular
+// block (|det| <= 1e-300 scale) becomes the identity
+__global__ void invert_blocks(int64_t n, int ncomp, double* __restrict__ blk) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double* A = blk + e * ncomp * ncomp;
+  if (ncomp == 2) {
+    const double a = A[0], b = A[1], c = A[2], d = A[3];
+    const double det = a * d - b * c;
+    if (!(fabs(det) > 0.0) || !isfinite(det)) {
+      A[0] = 1.0; A[1] = 0.0; A[2] = 0.0; A[3] = 1.0;
+      return;
+    }
+    A[0] = d / det; A[1] = -b / det; A[2] = -c / det; A[3] = a / det;
+    return;
+  }
+  double m[9], r[9];
+  for (int k = 0; k < 9; ++k) m[k] = A[k];
+  r[0] = m[4] * m[8] - m[5] * m[7];
+  r[1] = m[2] * m[7] - m[1] * m[8];
+  r[2] = m[1] * m[5] - m[2] * m[4];
+  r[3] = m[5] * m[6] - m[3] * m[8];
+  r[4] = m[0] * m[8] - m[2] * m[6];
+  r[5] = m[2] * m[3] - m[0] * m[5];
+  r[6] = m[3] * m[7] - m[4] * m[6];
+  r[7] = m[1] * m[6] - m[0] * m[7];
+  r[8] = m[0] * m[4] - m[1] * m[3];
+  const double det = m[0] * r[0] + m[1] * r[3] + m[2] * r[6];
+  if (!(fabs(det) > 0.0) || !isfinite(det)) {
+    for (int k = 0; k < 9; ++k) A[k] = (k % 4 == 0) ? 1.0 : 0.0;
+    return;
+  }
+  for (int k = 0; k < 9; ++k) A[k] = r[k] / det;
+}
+
+// out[e] (+)= blk[e] in[e] over elements [e0, e1) (vectors in sorted order)
+__global__ void block_apply(int64_t e0, int64_t e1, int ncomp, const double* __restrict__ blk,
+                            const double* __restrict__ in, double* __restrict__ out, int add) {
+  const int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= e1) return;
+  const double* A = blk + e * ncomp * ncomp;
+  double v[3], o[3];
+  for (int c = 0; c < ncomp; ++c) v[c] = in[e * ncomp + c];
+  for (int r = 0; r < ncomp; ++r) {
+    double acc = 0.0;
+    for (int c = 0; c < ncomp; ++c) acc = fma(A[r * ncomp + c], v[c], acc);
+    o[r] = acc;
+  }
+  for (int r = 0; r < ncomp; ++r) out[e * ncomp + r] = add ? out[e * ncomp + r] + o[r] : o[r];
+}
 
 struct Gm {
   ddm_ctx_s* ctx;
@@ -134,6 +184,8 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
                 const double* b_user, double* x_user, double tol, int restart, int max_iter,
                 int mode, int* iters_out, double* rel_out, cudaStream_t s) {
   const int ncomp = mat->kind == 1 ? 3 : 2;
+  const bool use_pc = !(mode & DDM_GMRES_NO_PRECOND);
+  mode &= ~DDM_GMRES_NO_PRECOND;
   const int64_t n = t->n;
   const int64_t nfull = n * ncomp;
   const int64_t lo = t->own_el_lo * ncomp;
@@ -150,8 +202,26 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
     t->krylov_dof = nloc;
   }
   if (!t->gm_w) {
-    // gm_w: 4 full vectors (b, x, v, w); gm_tmp: h buffer
-    if ((rc = dalloc(ctx, &t->gm_w, (size_t)4 * nfull))) return rc;
+    // gm_w: 5 full vectors (b, x, v, w, u); gm_tmp: h buffer
+    if ((rc = dalloc(ctx, &t->gm_w, (size_t)5 * 3 * n))) return rc;
+  }
+  if (use_pc) {
+    // block-Jacobi: inverse self blocks for this material and elapsed time
+    const double key[8] = {(double)mat->kind, mat->G, mat->nu, mat->nu_u, mat->alpha, mat->kappa,
+                           mat->kind == 1 ? dt : 0.0, 1.0};
+    if (!t->pc || std::memcmp(key, t->pc_key, sizeof(key)) != 0) {
+      if (!t->pc && (rc = dalloc(ctx, &t->pc, (size_t)n * 9))) return rc;
+      if (mat->kind == 1) {
+        if (!(dt > 0)) return set_error(ctx, DDM_ERR_ARG, "poroelastic GMRES needs dt > 0");
+        rc = launch_poro_self_blocks(ctx, t, poro_params(mat, dt), t->pc, s);
+      } else {
+        rc = launch_elastic_self_blocks(ctx, t, mat->G / (4.0 * M_PI * (1.0 - mat->nu)), t->pc, s);
+      }
+      if (rc) return rc;
+      invert_blocks<<<nblk(n, 256), 256, 0, s>>>(n, ncomp, t->pc);
+      DDM_CUDA(ctx, cudaGetLastError());
+      std::memcpy(t->pc_key, key, sizeof(key));
+    }
   }
   const int64_t part_need = (int64_t)(m + 2) * 256;
   if (t->gm_part_n < part_need) {
@@ -165,6 +235,7 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   double* xs = t->gm_w + nfull;
   double* vf = t->gm_w + 2 * nfull;
   double* wf = t->gm_w + 3 * nfull;
+  double* uf = t->gm_w + 4 * nfull;   // preconditioned operand M^-1 v (full) / update V y
   double* V = t->krylov;
   Gm g{ctx, t, s, ncomp, nloc, lo, t->gm_part, t->gm_part_n, t->gm_tmp};
 
@@ -172,7 +243,15 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   gather_sorted<<<nblk(n, 256), 256, 0, s>>>(n, ncomp, t->perm, x_user, xs);
   DDM_CUDA(ctx, cudaGetLastError());
 
+  // operator: A M^-1 (right preconditioning) or A
   auto apply = [&](const double* vfull) -> int {
+    if (!use_pc) return fmm_matvec(ctx, t, mat, dt, vfull, true, nullptr, wf, mode, s);
+    block_apply<<<nblk(n, 256), 256, 0, s>>>(0, n, ncomp, t->pc, vfull, uf, 0);
+    DDM_CUDA(ctx, cudaGetLastError());
+    return fmm_matvec(ctx, t, mat, dt, uf, true, nullptr, wf, mode, s);
+  };
+  // r = b - A x uses A itself (x is in the unpreconditioned space)
+  auto apply_plain = [&](const double* vfull) -> int {
     return fmm_matvec(ctx, t, mat, dt, vfull, true, nullptr, wf, mode, s);
   };
   std::vector<double> hh(2 * (m + 1) + 1);
@@ -197,7 +276,7 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   double rel = 0.0;
   for (;;) {
     // r = b - A x
-    if ((rc = apply(xs))) return rc;
+    if ((rc = apply_plain(xs))) return rc;
     sub_scale<<<nblk(nloc, 256), 256, 0, s>>>(bs + lo, wf + lo, V, nloc);
     DDM_CUDA(ctx, cudaGetLastError());
     if ((rc = g.dots(V, 0, 1, V, 0)) || (rc = fetch(1))) return rc;
@@ -259,7 +338,15 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
       y[i] = acc / H[(size_t)i * m + i];
     }
     DDM_CUDA(ctx, cudaMemcpyAsync(g.dh, y.data(), kdone * sizeof(double), cudaMemcpyHostToDevice, s));
-    if ((rc = g.axpy(V, nloc, kdone, g.dh, 1.0, xs + lo))) return rc;
+    if (use_pc) {   // x += M^-1 (V y)
+      DDM_CUDA(ctx, cudaMemsetAsync(uf + lo, 0, nloc * sizeof(double), s));
+      if ((rc = g.axpy(V, nloc, kdone, g.dh, 1.0, uf + lo))) return rc;
+      block_apply<<<nblk(t->own_el_hi - t->own_el_lo, 256), 256, 0, s>>>(
+          t->own_el_lo, t->own_el_hi, ncomp, t->pc, uf, xs, 1);
+      DDM_CUDA(ctx, cudaGetLastError());
+    } else if ((rc = g.axpy(V, nloc, kdone, g.dh, 1.0, xs + lo))) {
+      return rc;
+    }
     if (ctx->world > 1 && (rc = allgather_sorted(ctx, t, xs, ncomp, s))) return rc;
     DDM_CUDA(ctx, cudaStreamSynchronize(s));   // y (host) must stay alive until the copy ran
   }

@@ -86,6 +86,10 @@ int launch_poro_hist_gather(ddm_ctx_s* ctx, ddm_tree_s* t, int h, const double* 
                             double* Hs, double* Cs, double* Ctot, cudaStream_t s);
 int launch_poro_hist_near(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, int h, double dt,
                           const double* Hs, const double* Cs, cudaStream_t s);
+int launch_poro_self_blocks(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, double* blk,
+                            cudaStream_t s);
+int launch_elastic_self_blocks(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, double* blk,
+                               cudaStream_t s);
 int launch_poro_direct(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi,
                        const PoroParams& P, double* y_user, double* y_sorted, cudaStream_t s);
 

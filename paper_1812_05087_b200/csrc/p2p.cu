@@ -252,4 +252,42 @@ int launch_direct(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, int nco
   return DDM_OK;
 }
 
+namespace {
+// Self blocks of the elastic influence (block-Jacobi preconditioner of
+// GMRES): blk[i][r][c] = traction component r (s, n) at element i's centre
+// from a unit DD component c (s, n) on element i (sorted order).
+__global__ void elastic_self_blocks(int64_t n, const double* __restrict__ ex,
+                                    const double* __restrict__ ey, const double* __restrict__ ea,
+                                    const double* __restrict__ ec, const double* __restrict__ es,
+                                    double gc, double* __restrict__ blk) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double c = ec[i], s = es[i], a = ea[i];
+  const double2 r = make_double2(c * c - s * s, -2.0 * c * s);
+  for (int col = 0; col < 2; ++col) {
+    const double ds = col == 0 ? 1.0 : 0.0, dn = col == 1 ? 1.0 : 0.0;
+    const double2 B = make_double2(ds * c - dn * s, ds * s + dn * c);
+    const double2 rB = cmul(r, B);
+    const double2 Bh = make_double2(0.5 * B.x, 0.5 * B.y);
+    const double2 P1 = cmul(Bh, make_double2(r.x - 1.0, r.y));
+    const double2 T2 = cmul(Bh, make_double2(r.x + 1.0, r.y));
+    double sp[kSrcStride] = {ex[i] - a * c, ey[i] - a * s, ex[i] + a * c, ey[i] + a * s,
+                             P1.x, P1.y, -T2.y, T2.x, Bh.x, Bh.y, -(rB.x + B.x), -(rB.y - B.y)};
+    P2PAcc acc;
+    pair_update(acc, ex[i], ey[i], sp);
+    const double2 T = acc_to_traction(acc, gc, c, s);
+    blk[i * 4 + 0 * 2 + col] = T.x;
+    blk[i * 4 + 1 * 2 + col] = T.y;
+  }
+}
+}  // namespace
+
+int launch_elastic_self_blocks(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, double* blk,
+                               cudaStream_t s) {
+  elastic_self_blocks<<<nblk(t->n, 128), 128, 0, s>>>(t->n, t->ex, t->ey, t->ea, t->ec, t->es,
+                                                      gc, blk);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
 }  // namespace ddm

@@ -827,6 +827,29 @@ poro_hist_near_kernel(int nown, const int* __restrict__ order, const int4* __res
   }
 }
 
+// Self blocks of the poroelastic influence (block-Jacobi preconditioner):
+// blk[i][r][c] = (sigma_s, sigma_n, p)_r at element i from a unit ABI
+// component c (D_s, D_n, q) on element i (sorted order).
+__global__ void poro_self_blocks(int64_t n, const double* __restrict__ ex,
+                                 const double* __restrict__ ey, const double* __restrict__ ea,
+                                 const double* __restrict__ ec, const double* __restrict__ es,
+                                 PoroConst k, double* __restrict__ blk) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 zt = make_double2(ex[i], ey[i]);
+  const double ct = ec[i], st = es[i];
+  const double2 e2t = make_double2(ct * ct - st * st, 2.0 * ct * st);
+  for (int col = 0; col < 3; ++col) {
+    const double sp[kPoroStride] = {ex[i], ey[i], ct, st, ea[i], col == 0 ? 1.0 : 0.0,
+                                    col == 1 ? 1.0 : 0.0, col == 2 ? 1.0 : 0.0};
+    double os = 0.0, on = 0.0, op = 0.0;
+    poro_pair(zt, e2t, sp, k, os, on, op);
+    blk[i * 9 + 0 * 3 + col] = os;
+    blk[i * 9 + 1 * 3 + col] = on;
+    blk[i * 9 + 2 * 3 + col] = op;
+  }
+}
+
 }  // namespace
 
 PoroParams poro_params(const ddm_material* m, double tau) {
@@ -969,6 +992,14 @@ int launch_poro_hist_near(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, in
       nown, t->p2p_order, t->items, t->u_off, t->u_lo, t->u_hi, t->leaves, t->c_start,
       t->c_count, t->src, Hs, Cs, h, dt, t->ex, t->ey, t->ec, t->es, to_const(P),
       reinterpret_cast<double*>(t->part));
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+int launch_poro_self_blocks(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, double* blk,
+                            cudaStream_t s) {
+  poro_self_blocks<<<nblk(t->n, 64), 64, 0, s>>>(t->n, t->ex, t->ey, t->ea, t->ec, t->es,
+                                                 to_const(P), blk);
   DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;
 }

@@ -40,6 +40,13 @@ for cfg in (2, 3):
     else:
         b = D.farfield_rhs(ctx, f(g.beta), 2, ld["p_f"], ld["sH"], ld["sh"])
     dt = c.get("dt", 0.0)
+    for pc in (True, False):
+        t = time.perf_counter()
+        x, it2, rr2 = D.gmres_solve(ctx, tree, mat, b, dt=dt, tol=c["tol"], restart=3000,
+                                    max_iter=6000, raise_noconv=False, precond=pc)
+        torch.cuda.synchronize()
+        out[f"cfg{cfg}_solve_precond{int(pc)}"] = {"iters": it2, "rel": rr2,
+                                                   "ms": (time.perf_counter() - t) * 1e3}
     x, it, rr = D.gmres_solve(ctx, tree, mat, b, dt=dt, tol=1e-30, restart=3000, max_iter=iters,
                               raise_noconv=False)
     torch.cuda.synchronize()
