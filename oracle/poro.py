@@ -32,7 +32,7 @@ physical pore pressure:
              sigma^p part: T^p = -eta p + e^{2 i b_t} (-4 eta d^2Phi/dw^2)
 The element influence = drained Crouch–Starfield (oracle/elastic.py, nu) +
 integral along the element of (T^p, p) by the fixed composite Gauss–Legendre
-rule of DESIGN.md §4.13 (8 nodes per panel, panels graded away from the nearest point, each <= max(r, sqrt(c tau))/4,
+rule of DESIGN.md R17, §4.5 (8 nodes per panel, panels graded away from the nearest point, each <= max(r, sqrt(c tau))/4,
 split at the foot of the perpendicular when the target lies on the element,
 where the log singularity of E1 is integrated analytically).  Beyond
 u_min = dist^2/(4 c tau) > 40 the transient terms are below 1e-17 and the
@@ -176,7 +176,7 @@ def _e1_line_integral(s0, s1, cscale):
 def _graded_edges(s0, s1, sfrom, sstar, dperp, lt):
     """Panel edges on [s0, s1] graded away from the nearest point sfrom: each
     panel is at most half of max(distance of its near end to the target,
-    sqrt(c tau)) times PANEL_FRACTION long."""
+    sqrt(c tau)) times PANEL_FRACTION long (R17, §4.5)."""
     pts = [sfrom]
     s = sfrom
     other = s1 if sfrom == s0 else s0

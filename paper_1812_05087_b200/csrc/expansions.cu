@@ -9,7 +9,7 @@
 // and likewise for Psi~ = Psi + conj(z0) Phi'.  The factor i G C,
 // C = 1/(4 pi (1 - nu)), is applied once, at evaluation.
 //
-// Scheduling (DESIGN.md §4.9): P2M (warp per leaf) and M2L (warp per cell)
+// Scheduling (DESIGN.md §4.4): P2M (warp per leaf) and M2L (warp per cell)
 // have no dependencies and run as plain grids; M2M and L2L are launched one
 // tree level at a time (M2M deepest level first, L2L top-down), so every
 // dependency is a kernel boundary: no flags, no atomics, no spinning.  On the
@@ -77,7 +77,7 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
     const int i = e0 + r0 + lane;
     const bool valid = r0 + lane < ne;
     double2 B = make_double2(0, 0), Q = B, rr = B, A = B, z1 = B, z2 = B;
-    // poroelastic far field (DESIGN.md §4.13): B-part of Phi and Psi~ scaled by
+    // poroelastic far field (DESIGN.md §4.5): B-part of Phi and Psi~ scaled by
     // fu, plus Wm conj(e) I2 and Wc B I4 in Psi~ (iGC factored out)
     double2 Wme = make_double2(0, 0), Bc = Wme;
     double fu = 1.0;

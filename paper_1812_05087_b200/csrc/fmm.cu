@@ -130,7 +130,7 @@ int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double el
     pf = poro_far(PP);
     if (mode == DDM_FMM && t->nlevels > 2) {
       // the far field is the r >> sqrt(c tau) form: every V pair must be
-      // separated by more than R_c = sqrt(160 c tau) (u > 40, DESIGN.md §4.13)
+      // separated by more than R_c = sqrt(160 c tau) (u > 40, DESIGN.md §4.5)
       const double smin = std::ldexp(t->W, -(t->nlevels - 1));
       const double sep = smin - 2.0 * t->a_max;
       if (sep <= 0 || sep * sep / (4.0 * PP.ct) <= 40.0)
@@ -191,7 +191,7 @@ int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double el
   return rc;
 }
 
-// Fast history sum (SURVEY §8f row f1; DESIGN.md §4.14):
+// Fast history sum (SURVEY §8f row f1; DESIGN.md §4.6):
 //   r = sum_{m=1}^{h} A^(m) D^(h-m) = sum_{j=1}^{h+1} K(j dt) E_j,  E_j = D^(h+1-j) - D^(h-j)
 // (reading R10).  Far field (V pairs, all separated beyond R_c((h+1) dt)): the
 // far form is affine in tau and sum_j E_j = 0, so it is ONE far pass of the

@@ -60,12 +60,12 @@ PoroParams poro_params(const ddm_material* m, double tau);
 int poro_init_tables(ddm_ctx_s* ctx);
 
 // far-field (expansion) weights of the poroelastic kernel, r >> sqrt(c tau)
-// (DESIGN.md §4.13): Phi scaled by fu = 1 + 2 eta k_p = (1-nu)/(1-nu_u); Psi~
+// (DESIGN.md §4.5): Phi scaled by fu = 1 + 2 eta k_p = (1-nu)/(1-nu_u); Psi~
 // gains the monopole / fluid-source I2 terms and the c tau I4 term; L2P reads
 // p = -4 k_p Re(Phi_total)/fu (formula sign; ABI p = -that).
 // lin = 1: only the part proportional to c tau (the far form is affine in
 // tau: F(tau) = F0 + tau F1) -- the far field of the fast history sum, whose
-// tau-independent part cancels (sum_j E_j = 0, DESIGN.md §4.14).
+// tau-independent part cancels (sum_j E_j = 0, DESIGN.md §4.6).
 struct PoroFar {
   int on = 0, lin = 0;
   double fu = 1.0, eta = 0, kp = 0, S = 0, kappa = 0, ct = 0, gc = 1.0;

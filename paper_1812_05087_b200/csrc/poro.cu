@@ -1,5 +1,5 @@
 // Fully coupled poroelastic continuous-source kernel on the GPU (DESIGN.md
-// §4.13; PAPER.md Eq.(int_sigs)-(int_pp) P:319-375, Eq.(final_sigs)-(final_pp)
+// §4.5; PAPER.md Eq.(int_sigs)-(int_pp) P:319-375, Eq.(final_sigs)-(final_pp)
 // P:389-449).  Plane strain Biot theory, tension-positive stress, CS-convention
 // DDs, physical pore pressure; the ABI sign map J = diag(1, 1, -1) is applied
 // at the boundary of this file (source q and output p negated).
@@ -77,7 +77,7 @@ __device__ __forceinline__ void fgh(double u, double& f2, double& g2, double& h2
 //                  [2^j, 2^{j+1}] (coefficients from a long-double continued
 //                  fraction at start-up, poro_init_tables)
 //   u > 1024:      h = 1 - 1/u + 2/u^2 - 6/u^3 + 24/u^4 - 120/u^5
-// Max relative error vs a reference E1: 3.4e-15 (DESIGN.md §4.13).
+// Max relative error vs a reference E1: 3.4e-15 (DESIGN.md §4.5).
 constexpr int kEinTerms = 25;
 constexpr int kE1Oct = 9;        // octaves [2,4) .. [512,1024)
 constexpr int kE1Cheb = 26;
