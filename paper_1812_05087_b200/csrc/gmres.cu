@@ -1,4 +1,4 @@
-// GMRES with the FMM operator ("a modified
+// GMRES with the FMM operator (DESIGN.md §4.1 row a12, §4.7; "a modified
 // version of GMRES with FMM for matrix-vector multiplication"; reading R11):
 // restarted GMRES, Arnoldi by classical Gram-Schmidt applied twice (CGS2),
 // Givens rotations, relative residual ||b - A x|| / ||b|| <= tol.
