@@ -251,6 +251,8 @@ int ddm_ctx_create(int device, const void* nccl_uid, int rank, int world, ddm_ct
     ctx->serial = ctx->serial_env = ser && ser[0] == '1';
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    if (const char* sw = getenv("DDM_PRIO_SWAP"))   // experiment: near field high priority
+      if (sw[0] == '1') std::swap(lo_prio, hi_prio);
     if ((e = cudaStreamCreateWithPriority(&ctx->s_hi, cudaStreamNonBlocking, hi_prio)) != cudaSuccess ||
         (e = cudaStreamCreateWithPriority(&ctx->s_lo, cudaStreamNonBlocking, lo_prio)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
