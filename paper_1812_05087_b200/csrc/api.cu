@@ -255,6 +255,7 @@ int ddm_ctx_create(int device, const void* nccl_uid, int rank, int world, ddm_ct
       if (sw[0] == '1') std::swap(lo_prio, hi_prio);
     if ((e = cudaStreamCreateWithPriority(&ctx->s_hi, cudaStreamNonBlocking, hi_prio)) != cudaSuccess ||
         (e = cudaStreamCreateWithPriority(&ctx->s_lo, cudaStreamNonBlocking, lo_prio)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&ctx->s_cap, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_far, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_near, cudaEventDisableTiming)) != cudaSuccess) {
@@ -294,7 +295,7 @@ void ddm_ctx_destroy(ddm_ctx_t ctx) {
     for (auto& ev : ctx->stage.ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : {ctx->ev_fork, ctx->ev_far, ctx->ev_near})
     if (ev) cudaEventDestroy(ev);
-  for (cudaStream_t st : {ctx->s_hi, ctx->s_lo})
+  for (cudaStream_t st : {ctx->s_hi, ctx->s_lo, ctx->s_cap})
     if (st) cudaStreamDestroy(st);
   if (ctx->d_scalar) cudaFree(ctx->d_scalar);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);

@@ -53,6 +53,7 @@ struct ddm_ctx_s {
   // fork/join streams: the far-field chain (latency bound) runs on s_hi, the
   // near field (P2P, throughput bound) concurrently on s_lo
   cudaStream_t s_hi = nullptr, s_lo = nullptr;
+  cudaStream_t s_cap = nullptr;   // capture stream of the matvec graphs (fmm.cu)
   bool serial = false;            // DDM_SERIAL=1: everything on the caller's stream (profiling)
   bool serial_env = false;        // the DDM_SERIAL setting (restored when profiling mode 2 ends)
   cudaEvent_t ev_fork = nullptr, ev_far = nullptr, ev_near = nullptr;
@@ -64,6 +65,29 @@ struct ddm_ctx_s {
 
 // Device-side tree and all per-geometry buffers.  Level-major cell numbering,
 // Morton order within a level.
+// arguments that determine a matvec's launch sequence (graph cache key)
+struct MatvecKey {
+  const double* D = nullptr;
+  double* y_user = nullptr;
+  double* y_sorted = nullptr;
+  cudaStream_t s = nullptr;
+  int mode = -1;
+  bool d_sorted = false, serial = false;
+  ddm_material mat = {};
+  double elapsed = 0.0;
+  bool operator==(const MatvecKey& o) const {
+    return D == o.D && y_user == o.y_user && y_sorted == o.y_sorted && s == o.s &&
+           mode == o.mode && d_sorted == o.d_sorted && serial == o.serial &&
+           mat.kind == o.mat.kind && mat.G == o.mat.G && mat.nu == o.mat.nu &&
+           mat.nu_u == o.mat.nu_u && mat.alpha == o.mat.alpha && mat.kappa == o.mat.kappa &&
+           elapsed == o.elapsed;
+  }
+};
+struct MatvecGraph {
+  MatvecKey key;
+  cudaGraphExec_t exec = nullptr;
+};
+
 struct ddm_tree_s {
   ddm_ctx_s* ctx = nullptr;
   int64_t n = 0;
@@ -145,6 +169,10 @@ struct ddm_tree_s {
   double* y_sorted = nullptr;     // [n*3]
   double* y_far = nullptr;        // [n*3] L2P far field of the owned elements (sorted order)
   double* part_direct = nullptr;  // [n*2] direct-mode tractions (sorted)
+  // matvec CUDA graphs (fmm.cu)
+  std::vector<MatvecGraph> graphs = std::vector<MatvecGraph>(4);
+  int graph_next = 0;
+  MatvecKey last_key;
   // GMRES block-Jacobi preconditioner: inverse self blocks [n][ncomp][ncomp]
   // (sorted order) for the material / elapsed time in pc_key
   double* pc = nullptr;

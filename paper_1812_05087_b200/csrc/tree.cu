@@ -464,6 +464,8 @@ void free_tree(ddm_tree_s* t) {
                   t->krylov, t->pc, t->gm_w, t->gm_tmp, t->gm_part};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (auto& g : t->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
 }
 
 int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double* a,
