@@ -29,7 +29,8 @@ sys.path.insert(0, ROOT)
 METRIC = ("FMM DDM matvec interactions/s and GMRES solve time (fp64) vs roofline, "
           "1/2/4/8 GPU")
 UNIT = "interactions/s"
-FLOP_PER_PAIR = 64          # P2P pair update, FMA = 2 flop
+FLOP_PER_PAIR = 57          # P2P pair update: 21 DFMA (2 flop) + 9 DMUL + 6 DADD
+FP64_INSTR_PER_PAIR = 36    # fp64-pipe instructions per pair (+ 1 MUFU.RCP64H on the XU)
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 
 
@@ -263,6 +264,10 @@ def run_ours(args):
                                           "ncu --set full capture (profiles/ncu_traffic.json)",
                         "peak_source": "measured DFMA-chain probe (ddm_probe_fp64) on this GPU",
                         "flop_per_pair": FLOP_PER_PAIR,
+                        "fp64_pipe_frac": (owned_pairs * FP64_INSTR_PER_PAIR / (p2p_ms * 1e-3)
+                                           / (fp64_peak * 1e12 / 2.0)) if fp64_peak else None,
+                        "fp64_pipe_frac_note": "fp64-pipe instructions issued / peak instruction "
+                                               "rate (peak TFLOP/s / 2 flop per DFMA)",
                         "kernel_ms": p2p_ms,
                         "kernel_ms_source": "CUDA events on the launching stream, serial "
                                             "instrumented matvecs after the timed region",
