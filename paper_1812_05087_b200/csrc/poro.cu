@@ -479,11 +479,130 @@ constexpr int kQueue = 64;       // per-warp queue of near-rule pairs (flushed a
 // per-warp near-rule queue: entries (target slot, source, lag) evaluated one
 // at a time by the whole warp (poro_near_coop); sums per target slot in
 // queue order (deterministic)
+constexpr int kBatchQ = 16;   // queue entries whose panels are generated in parallel
+constexpr int kBP = 32;       // panel breakpoints per side kept for a batched entry
 struct NearQueue {
   int t[kQueue], s[kQueue], j[kQueue];
   double acc[3][kTgtGroup];
-  double coop[2 * (kCoopPanels + 1) + 2];
+  double coop[2 * (kCoopPanels + 1) + 2];   // fallback (entries with > kBP panels a side)
+  double bp[kBatchQ][2][kBP + 1];
+  int np[kBatchQ][2];                       // panels per side, -1 = more than kBP
 };
+
+// One queued near-rule evaluation: target (zt, e2t), source element (zc, e,
+// a), source strengths (formula convention) and c tau.
+struct NearDesc {
+  double2 zt, e2t, zc, e;
+  double a, Ds, Dn, q, ct;
+};
+
+// Flush the queue: entries in batches of kBatchQ; lanes 2i, 2i+1 generate the
+// graded panels of entry i's two sides in parallel (the sequential recurrence
+// of poro_element), then the warp integrates the entries one at a time (32
+// lanes over the 8 x panels Gauss–Legendre nodes) and lane 0 adds the result
+// to the entry's target slot -- in queue order (deterministic).  desc(qi)
+// returns entry qi's NearDesc.
+template <class Desc>
+__device__ void near_queue_flush(NearQueue& Q, int qn, int lane, const PoroConst& k0,
+                                 const Desc& desc) {
+  __syncwarp();
+  for (int base = 0; base < qn; base += kBatchQ) {
+    const int ng = min(kBatchQ, qn - base);
+    {  // phase A: panel breakpoints, lane = (entry, side)
+      const int ei = lane >> 1, side = lane & 1;
+      if (ei < ng) {
+        const NearDesc d = desc(base + ei);
+        const double lt = sqrt(d.ct);
+        const double rx = d.zt.x - d.zc.x, ry = d.zt.y - d.zc.y;
+        const double sstar = rx * d.e.x + ry * d.e.y;
+        const double dperp = fabs(-rx * d.e.y + ry * d.e.x);
+        const double s0c = fmin(fmax(sstar, -d.a), d.a);
+        const double other = side ? d.a : -d.a;
+        const double sign = side ? 1.0 : -1.0;
+        double* b = Q.bp[ei][side];
+        double cur = s0c;
+        int np = 0;
+        b[0] = cur;
+        bool over = false;
+        if ((other - s0c) * sign > 0.0) {
+          while ((other - cur) * sign > 0.0) {
+            if (np == kBP) {
+              over = true;
+              break;
+            }
+            const double r = hypot(dperp, cur - sstar);
+            double snext = cur + sign * kPanelFraction * fmax(r, lt);
+            if ((other - snext) * sign <= 0.0) snext = other;
+            b[++np] = snext;
+            cur = snext;
+          }
+        }
+        Q.np[ei][side] = over ? -1 : np;
+      }
+    }
+    __syncwarp();
+    for (int ei = 0; ei < ng; ++ei) {   // phase B: the warp integrates entry ei
+      const NearDesc d = desc(base + ei);
+      PoroConst k = k0;
+      k.ct = d.ct;
+      double2 T;
+      double p;
+      const int n0 = Q.np[ei][0], n1 = Q.np[ei][1];
+      if (n0 < 0 || n1 < 0) {
+        poro_near_coop(d.zt, d.zc, d.e, d.a, d.Ds, d.Dn, d.q, k, d.e2t, Q.coop, lane, T, p);
+      } else {
+        const double rx = d.zt.x - d.zc.x, ry = d.zt.y - d.zc.y;
+        const double sstar = rx * d.e.x + ry * d.e.y;
+        const double dperp = fabs(-rx * d.e.y + ry * d.e.x);
+        const double2 B = make_double2(d.Ds * d.e.x - d.Dn * d.e.y, d.Ds * d.e.y + d.Dn * d.e.x);
+        const double mu = -(k.eta / k.S) * d.Dn;
+        const double2 K = cscale(cmul(make_double2(0.0, k.gc), cmul(B, d.e)), -4.0 * k.kp);
+        const bool on_line = (dperp == 0.0) && (fabs(sstar) < d.a);
+        const double s0c = fmin(fmax(sstar, -d.a), d.a);
+        double pacc = 0.0;
+        double2 d2acc = make_double2(0.0, 0.0);
+        const int npts = 8 * (n0 + n1);
+        for (int t = lane; t < npts; t += 32) {
+          const int pan = t >> 3, g = t & 7;
+          const int side = pan < n0 ? 0 : 1;
+          const int pi = side ? pan - n0 : pan;
+          const double* b = Q.bp[ei][side];
+          const double s0 = b[pi], s1 = b[pi + 1];
+          const double mid = 0.5 * (s0 + s1), half = 0.5 * fabs(s1 - s0);
+          const double sq = mid + half * c_gl_x[g];
+          const double wx = d.zt.x - (d.zc.x + sq * d.e.x), wy = d.zt.y - (d.zc.y + sq * d.e.y);
+          point_add(wx, wy, half * c_gl_w[g], k, K, mu, d.q, on_line, pacc, d2acc);
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          pacc += __shfl_xor_sync(0xffffffffu, pacc, o);
+          d2acc.x += __shfl_xor_sync(0xffffffffu, d2acc.x, o);
+          d2acc.y += __shfl_xor_sync(0xffffffffu, d2acc.y, o);
+        }
+        if (on_line && d.q != 0.0) {
+          for (int side = 0; side < 2; ++side) {
+            const double other = side ? d.a : -d.a;
+            const double sign = side ? 1.0 : -1.0;
+            if ((other - s0c) * sign <= 0.0) continue;
+            const double len = fabs(other - sstar);
+            pacc += d.q * e1_log_part(0.0, len, k.ct) / (4.0 * M_PI * k.kappa);
+          }
+        }
+        p = pacc;
+        const double2 t2 =
+            cmul(d.e2t, make_double2(-4.0 * k.eta * d2acc.x, -4.0 * k.eta * d2acc.y));
+        T = make_double2(-k.eta * pacc + t2.x, t2.y);
+      }
+      if (lane == 0) {
+        const int slot = Q.t[base + ei];
+        Q.acc[0][slot] += T.y;
+        Q.acc[1][slot] += T.x;
+        Q.acc[2][slot] -= p;   // J: p_ABI = -p_formula
+      }
+      __syncwarp();
+    }
+  }
+}
 
 __global__ void poro_prep(int64_t n, const int* __restrict__ perm, const double* __restrict__ D,
                           const double* __restrict__ ex, const double* __restrict__ ey,
@@ -544,26 +663,24 @@ poro_p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict_
     for (int e = lane; e < 3 * kTgtGroup; e += 32) (&Q.acc[0][0])[e] = 0.0;
     int qn = 0;
     double os = 0.0, on = 0.0, op = 0.0;
+    auto desc = [&](int qi) {
+      const int tg = item.y + Q.t[qi];
+      const double cq = ec[tg], sq = es[tg];
+      const double* sp = src + (int64_t)Q.s[qi] * kPoroStride;
+      NearDesc d;
+      d.zt = make_double2(ex[tg], ey[tg]);
+      d.e2t = make_double2(cq * cq - sq * sq, 2.0 * cq * sq);
+      d.zc = make_double2(sp[0], sp[1]);
+      d.e = make_double2(sp[2], sp[3]);
+      d.a = sp[4];
+      d.Ds = sp[5];
+      d.Dn = sp[6];
+      d.q = -sp[7];   // J: q_formula = -q_ABI
+      d.ct = k.ct;
+      return d;
+    };
     auto flush = [&]() {
-      __syncwarp();
-      for (int qi = 0; qi < qn; ++qi) {
-        const int t = Q.t[qi];
-        const int tg = item.y + t;
-        const double2 ztq = make_double2(ex[tg], ey[tg]);
-        const double cq = ec[tg], sq = es[tg];
-        const double2 e2q = make_double2(cq * cq - sq * sq, 2.0 * cq * sq);
-        const double* sp = src + (int64_t)Q.s[qi] * kPoroStride;
-        double2 T;
-        double p;
-        poro_near_coop(ztq, make_double2(sp[0], sp[1]), make_double2(sp[2], sp[3]), sp[4], sp[5],
-                       sp[6], -sp[7], k, e2q, Q.coop, lane, T, p);
-        if (lane == 0) {
-          Q.acc[0][t] += T.y;
-          Q.acc[1][t] += T.x;
-          Q.acc[2][t] -= p;
-        }
-        __syncwarp();
-      }
+      near_queue_flush(Q, qn, lane, k, desc);
       qn = 0;
     };
     int pos = 0;
@@ -707,31 +824,26 @@ poro_hist_near_kernel(int nown, const int* __restrict__ order, const int4* __res
     for (int e = lane; e < 3 * kTgtGroup; e += 32) (&Q.acc[0][0])[e] = 0.0;
     int qn = 0;
     double os = 0.0, on = 0.0, op = 0.0;
+    auto desc = [&](int qi) {
+      const int tg = item.y + Q.t[qi], sidx = Q.s[qi], j = Q.j[qi];
+      const double cq = ec[tg], sq = es[tg];
+      const double* sp = src + (int64_t)sidx * kPoroStride;
+      const double* Da = Hs + (int64_t)sidx * hs + (h + 2 - j) * 3;   // D^(h+1-j)
+      const double* Db = Da - 3;                                       // D^(h-j)
+      NearDesc d;
+      d.zt = make_double2(ex[tg], ey[tg]);
+      d.e2t = make_double2(cq * cq - sq * sq, 2.0 * cq * sq);
+      d.zc = make_double2(sp[0], sp[1]);
+      d.e = make_double2(sp[2], sp[3]);
+      d.a = sp[4];
+      d.Ds = Da[0] - Db[0];
+      d.Dn = Da[1] - Db[1];
+      d.q = -(Da[2] - Db[2]);   // J: q_formula = -q_ABI
+      d.ct = k.c * (j * dt);
+      return d;
+    };
     auto flush = [&]() {
-      __syncwarp();
-      for (int qi = 0; qi < qn; ++qi) {
-        const int t = Q.t[qi], sidx = Q.s[qi], j = Q.j[qi];
-        const int tg = item.y + t;
-        const double2 ztq = make_double2(ex[tg], ey[tg]);
-        const double cq = ec[tg], sq = es[tg];
-        const double2 e2q = make_double2(cq * cq - sq * sq, 2.0 * cq * sq);
-        const double* sp = src + (int64_t)sidx * kPoroStride;
-        const double* Da = Hs + (int64_t)sidx * hs + (h + 2 - j) * 3;   // D^(h+1-j)
-        const double* Db = Da - 3;                                       // D^(h-j)
-        PoroConst kj = k;
-        kj.ct = k.c * (j * dt);
-        double2 T;
-        double p;
-        poro_near_coop(ztq, make_double2(sp[0], sp[1]), make_double2(sp[2], sp[3]), sp[4],
-                       Da[0] - Db[0], Da[1] - Db[1], -(Da[2] - Db[2]), kj, e2q, Q.coop, lane, T,
-                       p);
-        if (lane == 0) {
-          Q.acc[0][t] += T.y;
-          Q.acc[1][t] += T.x;
-          Q.acc[2][t] -= p;
-        }
-        __syncwarp();
-      }
+      near_queue_flush(Q, qn, lane, k, desc);
       qn = 0;
     };
     int pos = 0;
