@@ -104,7 +104,7 @@ void ddm_tree_free(ddm_tree_t tree);
 enum {
   DDM_TC_N = 0, DDM_TC_CELLS, DDM_TC_LEAVES, DDM_TC_LEVELS, DDM_TC_V, DDM_TC_URANGES,
   DDM_TC_NEAR_PAIRS, DDM_TC_P2P_ITEMS, DDM_TC_OWNED_LO, DDM_TC_OWNED_HI, DDM_TC_P,
-  DDM_TREE_NCOUNTS = 16
+  DDM_TC_W, DDM_TC_W_MIN, DDM_TREE_NCOUNTS = 16
 };
 int ddm_tree_counts(ddm_tree_t tree, int64_t* counts);
 
@@ -117,12 +117,16 @@ int ddm_tree_counts(ddm_tree_t tree, int64_t* counts);
  *   V_OFF   i32[c+1], V_IDX i32[nv]            (CSR, per target cell)
  *   LEAVES  i32[nl]  cell index of each leaf (canonical order)
  *   U_OFF   i32[nl+1], U_LO i32[nu], U_HI i32[nu]   (CSR of source element
- *           ranges [lo, hi) in sorted order, per leaf; sorted and merged) */
+ *           ranges [lo, hi) in sorted order, per leaf; sorted and merged)
+ *   W_OFF   i32[nl+1], W_IDX i32[nw]   (CSR of M2P source cells per leaf,
+ *           ascending, the W split of R5: cells deeper than the
+ *           leaf, not touching it, with >= w_min elements; env DDM_W_MIN at
+ *           build time, default 24, 0 = no W lists) */
 enum {
   DDM_EX_KEYS = 0, DDM_EX_PERM, DDM_EX_ROOT, DDM_EX_LEVEL, DDM_EX_IX, DDM_EX_IY,
   DDM_EX_START, DDM_EX_COUNT, DDM_EX_PARENT, DDM_EX_FIRST_CHILD, DDM_EX_NCHILD,
   DDM_EX_LEAF, DDM_EX_V_OFF, DDM_EX_V_IDX, DDM_EX_LEAVES, DDM_EX_U_OFF, DDM_EX_U_LO,
-  DDM_EX_U_HI
+  DDM_EX_U_HI, DDM_EX_W_OFF, DDM_EX_W_IDX
 };
 int ddm_tree_export(ddm_tree_t tree, int what, void* dst, int64_t capacity_bytes);
 

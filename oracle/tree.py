@@ -26,7 +26,14 @@ Exact readings (R5/R8):
   V(b)          existing same-level a with parent(a) adjacent-or-equal to
                 parent(b) and a not adjacent-or-equal to b (levels >= 2).
   U(B), leaf B  leaves A whose ancestors at level min(lev A, lev B) are
-                adjacent-or-equal (includes B).  W/X-type pairs go to P2P.
+                adjacent-or-equal (includes B), minus the leaves below a W(B)
+                cell; X-type pairs go to P2P.
+  W(B), leaf B  (w_min > 0) cells D deeper than B whose
+                ancestor at B's level is adjacent-or-equal to B, with D not
+                touching B (closed boxes disjoint), every ancestor of D below
+                B's level touching B, and count(D) >= w_min: D's multipole is
+                evaluated at B's targets (M2P).  A non-touching D with fewer
+                than w_min elements stays in U (P2P is cheaper).
 Cell numbering is canonical: level-major, Morton prefix order within a level.
 """
 from __future__ import annotations
@@ -210,32 +217,89 @@ def v_lists(t: OracleTree, targets=None) -> dict:
     return out
 
 
-def u_lists(t: OracleTree, targets=None) -> dict:
-    """Brute force U(B) for each target leaf B: sorted canonical leaf indices."""
+def touching(a: Cell, b: Cell) -> bool:
+    """Closed boxes of cells at any levels intersect (share a point)."""
+    if a.level > b.level:
+        a, b = b, a
+    sh = b.level - a.level                 # b is the finer cell
+    lo_x, hi_x = a.ix << sh, (a.ix + 1) << sh
+    lo_y, hi_y = a.iy << sh, (a.iy + 1) << sh
+    return (lo_x <= b.ix + 1 and b.ix <= hi_x) and (lo_y <= b.iy + 1 and b.iy <= hi_y)
+
+
+def w_lists(t: OracleTree, w_min: int, targets=None) -> dict:
+    """Brute force W(B) for each target leaf B: sorted canonical cell indices
+    (definition in the module docstring; empty when w_min <= 0)."""
     leaves = [c for c in t.cells if c.leaf]
     tg = leaves if targets is None else [t.cells[i] for i in targets]
+    by_level = {}
+    for c in t.cells:
+        by_level.setdefault(c.level, []).append(c)
     out = {}
     for B in tg:
         lst = []
-        for A in leaves:
-            m = min(A.level, B.level)
-            if adjacent_or_equal(ancestor(A, m), ancestor(B, m)):
-                lst.append(A.index)
+        if w_min > 0:
+            # candidates: the cells whose ancestor at B's level is adjacent-or-equal
+            # to B, i.e. the proper descendants of those cells; test each one
+            for Q in by_level[B.level]:
+                if not adjacent_or_equal(Q, B):
+                    continue
+                stack = list(Q.children)
+                while stack:
+                    D = stack.pop()
+                    stack.extend(D.children)
+                    if len(D.points) < w_min or touching(D, B):
+                        continue
+                    E, ok = D.parent, True
+                    while E.level > B.level:
+                        ok = ok and touching(E, B)
+                        E = E.parent
+                    if ok:
+                        lst.append(D.index)
         out[B.index] = sorted(lst)
     return out
 
 
-def pair_coverage(t: OracleTree, U: dict, V: dict) -> np.ndarray:
+def u_lists(t: OracleTree, targets=None, w_min: int = 0) -> dict:
+    """Brute force U(B) for each target leaf B: sorted canonical leaf indices
+    (w_min > 0: without the leaves below a W(B) cell)."""
+    leaves = [c for c in t.cells if c.leaf]
+    tg = leaves if targets is None else [t.cells[i] for i in targets]
+    W = w_lists(t, w_min, [B.index for B in tg]) if w_min > 0 else {}
+    out = {}
+    for B in tg:
+        wset = set(W.get(B.index, []))
+        lst = []
+        for A in leaves:
+            m = min(A.level, B.level)
+            if adjacent_or_equal(ancestor(A, m), ancestor(B, m)):
+                c, under_w = A, False
+                while c is not None and c.level > B.level:
+                    under_w = under_w or c.index in wset
+                    c = c.parent
+                if not under_w:
+                    lst.append(A.index)
+        out[B.index] = sorted(lst)
+    return out
+
+
+def pair_coverage(t: OracleTree, U: dict, V: dict, W: dict | None = None) -> np.ndarray:
     """For every ordered pair of leaves (B target, A source) count how many
-    times it is handled: once by U(B), or once per level l where
-    anc_l(A) in V(anc_l(B)).  The partition property requires all ones."""
+    times it is handled: once by U(B), once per W(B) cell above-or-at A, or
+    once per level l where anc_l(A) in V(anc_l(B)).  The partition property
+    requires all ones."""
     leaves = [c for c in t.cells if c.leaf]
     Vs = {k: set(v) for k, v in V.items()}
     cnt = np.zeros((len(leaves), len(leaves)), dtype=np.int64)
     for i, B in enumerate(leaves):
         uset = set(U[B.index])
+        wset = set(W[B.index]) if W is not None else set()
         for j, A in enumerate(leaves):
             n = 1 if A.index in uset else 0
+            c = A
+            while c is not None:
+                n += 1 if c.index in wset else 0
+                c = c.parent
             for lev in range(2, min(A.level, B.level) + 1):
                 if ancestor(A, lev).index in Vs[ancestor(B, lev).index]:
                     n += 1

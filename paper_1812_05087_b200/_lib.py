@@ -24,11 +24,11 @@ FMM, DIRECT, HIST_PERLAG = 0, 1, 2
 GMRES_NO_PRECOND = 8
 
 TC = dict(N=0, CELLS=1, LEAVES=2, LEVELS=3, V=4, URANGES=5, NEAR_PAIRS=6, P2P_ITEMS=7,
-          OWNED_LO=8, OWNED_HI=9, P=10)
+          OWNED_LO=8, OWNED_HI=9, P=10, W=11, W_MIN=12)
 NCOUNTS = 16
 EX = dict(KEYS=0, PERM=1, ROOT=2, LEVEL=3, IX=4, IY=5, START=6, COUNT=7, PARENT=8,
           FIRST_CHILD=9, NCHILD=10, LEAF=11, V_OFF=12, V_IDX=13, LEAVES=14, U_OFF=15, U_LO=16,
-          U_HI=17)
+          U_HI=17, W_OFF=18, W_IDX=19)
 STAGES = ["prep", "p2m", "m2m", "m2l", "l2l", "p2p", "final", "comm", "l2p"]
 
 

@@ -377,6 +377,8 @@ int ddm_tree_counts(ddm_tree_t t, int64_t* c) {
   c[DDM_TC_OWNED_LO] = t->own_el_lo;
   c[DDM_TC_OWNED_HI] = t->own_el_hi;
   c[DDM_TC_P] = t->p;
+  c[DDM_TC_W] = t->nw;
+  c[DDM_TC_W_MIN] = t->w_min;
   return DDM_OK;
 }
 
@@ -409,6 +411,8 @@ int ddm_tree_export(ddm_tree_t t, int what, void* dst, int64_t cap) {
     case DDM_EX_U_OFF: src = t->u_off; bytes = ((size_t)t->nleaves + 1) * 4; break;
     case DDM_EX_U_LO: src = t->u_lo; bytes = t->nu * 4; break;
     case DDM_EX_U_HI: src = t->u_hi; bytes = t->nu * 4; break;
+    case DDM_EX_W_OFF: src = t->w_off; bytes = ((size_t)t->nleaves + 1) * 4; break;
+    case DDM_EX_W_IDX: src = t->w_idx; bytes = t->nw * 4; break;
     default: return set_error(ctx, DDM_ERR_ARG, "unknown export id");
   }
   if ((int64_t)bytes > cap) return set_error(ctx, DDM_ERR_ARG, "capacity too small");

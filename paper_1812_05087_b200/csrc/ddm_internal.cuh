@@ -135,6 +135,10 @@ struct ddm_tree_s {
   int* u_off = nullptr;           // [nleaves+1]
   int* u_lo = nullptr;            // [nu]
   int* u_hi = nullptr;            // [nu]
+  int* w_off = nullptr;           // [nleaves+1] W lists (M2P cells) of each leaf
+  int* w_idx = nullptr;           // [nw] canonical cell ids, ascending per leaf
+  int64_t nw = 0;
+  int w_min = 24;                 // W(B) cells hold >= w_min elements (DDM_W_MIN, 0 = off)
   int4* items = nullptr;          // P2P work items: (leaf, tgt0, src_begin, src_end)
   int* item_off = nullptr;        // [nleaves+1] first item of each leaf
   int* m2l_cells = nullptr;       // (reserved) cells whose subtree meets the owned range

@@ -626,20 +626,25 @@ __global__ void __launch_bounds__(256)
 l2p_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int* __restrict__ el_leaf,
            const int* __restrict__ leaves, const int* __restrict__ c_level,
            const int* __restrict__ c_ix, const int* __restrict__ c_iy,
-           const double2* __restrict__ local, CellGeom cg, int p_rt, double gc, PoroFar pf,
-           const double* __restrict__ ex, const double* __restrict__ ey,
-           const double* __restrict__ ec, const double* __restrict__ es,
-           double* __restrict__ y_far) {
+           const double2* __restrict__ local, const int* __restrict__ w_off,
+           const int* __restrict__ w_idx, const double2* __restrict__ mpole, CellGeom cg,
+           int p_rt, double gc, PoroFar pf, const double* __restrict__ ex,
+           const double* __restrict__ ey, const double* __restrict__ ec,
+           const double* __restrict__ es, double* __restrict__ y_far) {
   const int p = PT ? PT : p_rt;
   const int64_t i = e_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= e_hi) return;
-  const int c = __ldg(leaves + __ldg(el_leaf + i));
+  const int k = __ldg(el_leaf + i);
+  const int c = __ldg(leaves + k);
   const int lev = __ldg(c_level + c);
-  double t0 = 0.0, t1 = 0.0, pr = 0.0;
-  if (lev >= 2) {   // no far field above level 2
+  const double x = ex[i], y = ey[i];
+  // Phi and X = conj(u) dPhi/du + Psi~ summed over the local series and the
+  // multipoles of the leaf's W cells (each in its own normalised coordinate)
+  double2 phi_t = make_double2(0.0, 0.0), X_t = phi_t;
+  if (lev >= 2) {   // no local expansion above level 2
     const double s = cg.side(lev), is = 1.0 / s;
     const double2 z0 = cg.centre(lev, __ldg(c_ix + c), __ldg(c_iy + c));
-    const double2 u = make_double2((ex[i] - z0.x) * is, (ey[i] - z0.y) * is);
+    const double2 u = make_double2((x - z0.x) * is, (y - z0.y) * is);
     const double2* L = local + (size_t)c * 2 * p;
     double2 phi = make_double2(0, 0), dphi = phi, psi = phi;
 #pragma unroll
@@ -656,19 +661,47 @@ l2p_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int* __restrict__ el_lea
       psi = make_double2(fma(psi.x, u.x, fma(-psi.y, u.y, gm.x)),
                          fma(psi.x, u.y, fma(psi.y, u.x, gm.y)));
     }
-    const double2 wv = cadd(cmul(cconj(u), dphi), psi);
-    const double2 W = make_double2(-gc * wv.y, gc * wv.x);
-    const double ct = ec[i], st = es[i];
-    const double2 e2 = make_double2(ct * ct - st * st, 2.0 * ct * st);
-    const double2 t2 = cmul(e2, W);
-    t0 = t2.y;
-    t1 = t2.x - 2.0 * gc * phi.y;
-    // far pore pressure p = -4 k_p Re(i G C Phi)/fu (formula sign), ABI p = -that
-    if (pf.on) pr = -4.0 * pf.kp * gc * phi.y / pf.fu;
+    phi_t = phi;
+    X_t = cadd(cmul(cconj(u), dphi), psi);
   }
-  y_far[i * ncomp + 0] = t0;
-  y_far[i * ncomp + 1] = t1;
-  if (ncomp == 3) y_far[i * ncomp + 2] = pr;
+  // M2P (W list): the multipole of each W cell D at this target,
+  // in D's normalised coordinate u = (z - z_D)/s_D, v = 1/u:
+  //   Phi = v f(v), f = sum_{n>=1} a_n v^(n-1);  dPhi/du = -v^2 (f + v f');
+  //   Psi~ = v g(v), g = sum c_n v^(n-1)   (f, f', g by Horner)
+  for (int wi = __ldg(w_off + k), we = __ldg(w_off + k + 1); wi < we; ++wi) {
+    const int D = __ldg(w_idx + wi);
+    const int ld = __ldg(c_level + D);
+    const double isd = ldexp(1.0 / cg.W, ld);   // 1/s_D (exact power-of-two scaling)
+    const double2 zd = cg.centre(ld, __ldg(c_ix + D), __ldg(c_iy + D));
+    const double2 u = make_double2((x - zd.x) * isd, (y - zd.y) * isd);
+    const double inn = 1.0 / fma(u.x, u.x, u.y * u.y);
+    const double2 v = make_double2(u.x * inn, -u.y * inn);
+    const double2* M = mpole + (size_t)D * 2 * p;
+    double2 f = make_double2(0, 0), fd = f, g = f;
+#pragma unroll
+    for (int n = pmax<PT>(); n >= 1; --n) {
+      if (!PT && n > p) continue;
+      const double2 an = __ldg(M + n - 1), cn = __ldg(M + p + n - 1);
+      fd = make_double2(fma(fd.x, v.x, fma(-fd.y, v.y, f.x)), fma(fd.x, v.y, fma(fd.y, v.x, f.y)));
+      f = make_double2(fma(f.x, v.x, fma(-f.y, v.y, an.x)), fma(f.x, v.y, fma(f.y, v.x, an.y)));
+      g = make_double2(fma(g.x, v.x, fma(-g.y, v.y, cn.x)), fma(g.x, v.y, fma(g.y, v.x, cn.y)));
+    }
+    const double2 dPdv = cadd(f, cmul(v, fd));
+    const double2 v2 = cmul(v, v);
+    const double2 dPdu = make_double2(-(v2.x * dPdv.x - v2.y * dPdv.y),
+                                      -(v2.x * dPdv.y + v2.y * dPdv.x));
+    phi_t = cadd(phi_t, cmul(f, v));
+    X_t = cadd(X_t, cadd(cmul(cconj(u), dPdu), cmul(g, v)));
+  }
+  // W = i G C X, T = sigma_n + i sigma_s = 2 Re(i G C Phi) + e^{2 i b} W
+  const double2 W = make_double2(-gc * X_t.y, gc * X_t.x);
+  const double ct = ec[i], st = es[i];
+  const double2 e2 = make_double2(ct * ct - st * st, 2.0 * ct * st);
+  const double2 t2 = cmul(e2, W);
+  y_far[i * ncomp + 0] = t2.y;
+  y_far[i * ncomp + 1] = t2.x - 2.0 * gc * phi_t.y;
+  // far pore pressure p = -4 k_p Re(i G C Phi)/fu (formula sign), ABI p = -that
+  if (ncomp == 3) y_far[i * ncomp + 2] = pf.on ? -4.0 * pf.kp * gc * phi_t.y / pf.fu : 0.0;
 }
 
 // ------------------------------------------------------------ finalize (a11)
@@ -854,9 +887,11 @@ int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFa
   const CellGeom cg{t->x_min, t->y_min, t->W};
   const unsigned nb = nblk(hi - lo, 256);
 #define DDM_L(PT)                                                                               \
-  l2p_kernel<PT><<<nb, 256, 0, s>>>(lo, hi, ncomp, t->el_leaf, t->leaves, t->c_level, t->c_ix,  \
-                                    t->c_iy, t->local, cg, t->p, gc, pf, t->ex, t->ey, t->ec,   \
-                                    t->es, t->y_far)
+  do {                                                                                          \
+    l2p_kernel<PT><<<nb, 256, 0, s>>>(lo, hi, ncomp, t->el_leaf, t->leaves, t->c_level,         \
+                                      t->c_ix, t->c_iy, t->local, t->w_off, t->w_idx, t->mpole, \
+                                      cg, t->p, gc, pf, t->ex, t->ey, t->ec, t->es, t->y_far);  \
+  } while (0)
   DDM_P_DISPATCH(t->p, DDM_L);
 #undef DDM_L
   DDM_CUDA(ctx, cudaGetLastError());

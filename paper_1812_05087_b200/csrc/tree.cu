@@ -307,13 +307,32 @@ __global__ void element_leaf(int nleaves, const int* __restrict__ leaves,
   for (int i = threadIdx.x; i < count[c]; i += blockDim.x) el_leaf[start[c] + i] = k;
 }
 
-// Enumerate the near-field source ranges of leaf B (reading R5):
-//  (1) leaf colleagues of every ancestor of B (incl. B itself);
-//  (2) all descendants of non-leaf colleagues of B.
+// Enumerate the near field of leaf B (reading R5, W split of SURVEY §8f f3):
+//  (1) leaf colleagues of every ancestor of B (incl. B itself) -> U;
+//  (2) the subtrees of the non-leaf colleagues of B, walked: a cell touching
+//      B is descended (a touching leaf -> U); a non-touching cell D is
+//      well separated from B: D -> W (M2P) if count(D) >= w_min, else its
+//      whole subtree -> U.  w_min <= 0: (2) puts every subtree in U.
+// Returns the number of U ranges; *nw = number of W cells.
+__device__ __forceinline__ bool cells_touch(int la, int ixa, int iya, int lb, int ixb, int iyb) {
+  if (la > lb) {
+    const int t0 = la, t1 = ixa, t2 = iya;
+    la = lb; ixa = ixb; iya = iyb;
+    lb = t0; ixb = t1; iyb = t2;
+  }
+  const int sh = lb - la;   // b is the finer cell
+  const long long lx = (long long)ixa << sh, hx = (long long)(ixa + 1) << sh;
+  const long long ly = (long long)iya << sh, hy = (long long)(iya + 1) << sh;
+  return lx <= ixb + 1 && ixb <= hx && ly <= iyb + 1 && iyb <= hy;
+}
+
 template <bool kFill>
-__device__ int enum_u(int B, const int* parent, const int* coll, const int* leaf,
-                      const int* start, const int* count, int2* out) {
-  int n = 0;
+__device__ int enum_uw(int B, const int* parent, const int* coll, const int* leaf,
+                       const int* start, const int* count, const int* level, const int* ix,
+                       const int* iy, const int* first_child, const int* nchild, int w_min,
+                       int2* out, int* wout, int* nw) {
+  int n = 0, m = 0;
+  const int lB = level[B], xB = ix[B], yB = iy[B];
   for (int A = B; A >= 0; A = parent[A]) {
     for (int k = 0; k < 9; ++k) {
       const int Q = coll[A * 9 + k];
@@ -322,37 +341,76 @@ __device__ int enum_u(int B, const int* parent, const int* coll, const int* leaf
         if (kFill) out[n] = make_int2(start[Q], start[Q] + count[Q]);
         ++n;
       } else if (A == B) {
-        if (kFill) out[n] = make_int2(start[Q], start[Q] + count[Q]);
-        ++n;
+        if (w_min <= 0) {
+          if (kFill) out[n] = make_int2(start[Q], start[Q] + count[Q]);
+          ++n;
+          continue;
+        }
+        // walk Q's subtree (explicit stack, depth-first)
+        int stack[128];
+        int sp = 0;
+        for (int c = nchild[Q] - 1; c >= 0; --c) stack[sp++] = first_child[Q] + c;
+        while (sp > 0) {
+          const int D = stack[--sp];
+          if (cells_touch(lB, xB, yB, level[D], ix[D], iy[D])) {
+            if (leaf[D]) {
+              if (kFill) out[n] = make_int2(start[D], start[D] + count[D]);
+              ++n;
+            } else {
+              for (int c = nchild[D] - 1; c >= 0 && sp < 128; --c) stack[sp++] = first_child[D] + c;
+            }
+          } else if (count[D] >= w_min) {
+            if (kFill) wout[m] = D;
+            ++m;
+          } else {
+            if (kFill) out[n] = make_int2(start[D], start[D] + count[D]);
+            ++n;
+          }
+        }
       }
     }
   }
+  *nw = m;
   return n;
 }
 
 __global__ void u_count(int nleaves, const int* __restrict__ leaves, const int* parent,
                         const int* coll, const int* leaf, const int* start, const int* count,
-                        int* __restrict__ ucnt) {
+                        const int* level, const int* ix, const int* iy, const int* first_child,
+                        const int* nchild, int w_min, int* __restrict__ ucnt,
+                        int* __restrict__ wcnt) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nleaves) return;
-  ucnt[k] = enum_u<false>(leaves[k], parent, coll, leaf, start, count, nullptr);
+  int nw = 0;
+  ucnt[k] = enum_uw<false>(leaves[k], parent, coll, leaf, start, count, level, ix, iy,
+                           first_child, nchild, w_min, nullptr, nullptr, &nw);
+  wcnt[k] = nw;
 }
 
-// fill, sort by lo, merge contiguous ranges; merged count to mcnt, total
-// source count to nsrc
 __global__ void u_fill(int nleaves, const int* __restrict__ leaves, const int* parent,
                        const int* coll, const int* leaf, const int* start, const int* count,
-                       const int* __restrict__ uoff, int2* __restrict__ utmp,
-                       int* __restrict__ mcnt, int* __restrict__ nsrc) {
+                       const int* level, const int* ix, const int* iy, const int* first_child,
+                       const int* nchild, int w_min, const int* __restrict__ uoff,
+                       int2* __restrict__ utmp, int* __restrict__ mcnt, int* __restrict__ nsrc,
+                       const int* __restrict__ woff, int* __restrict__ widx) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nleaves) return;
   int2* r = utmp + uoff[k];
-  const int n = enum_u<true>(leaves[k], parent, coll, leaf, start, count, r);
+  int* w = widx + woff[k];
+  int nw = 0;
+  const int n = enum_uw<true>(leaves[k], parent, coll, leaf, start, count, level, ix, iy,
+                              first_child, nchild, w_min, r, w, &nw);
   for (int a = 1; a < n; ++a) {  // insertion sort by lo (ranges are disjoint)
     const int2 v = r[a];
     int b = a - 1;
     while (b >= 0 && r[b].x > v.x) { r[b + 1] = r[b]; --b; }
     r[b + 1] = v;
+  }
+  for (int a = 1; a < nw; ++a) {  // W cells in canonical (index) order
+    const int v = w[a];
+    int b = a - 1;
+    while (b >= 0 && w[b] > v) { w[b + 1] = w[b]; --b; }
+    w[b + 1] = v;
   }
   int m = 0, tot = 0;
   for (int a = 0; a < n; ++a) {
@@ -457,7 +515,7 @@ void free_tree(ddm_tree_s* t) {
   void* ptrs[] = {t->keys_user, t->keys, t->perm, t->ex, t->ey, t->ea, t->ec, t->es,
                   t->el_leaf, t->c_level, t->c_ix, t->c_iy, t->c_start, t->c_count,
                   t->c_parent, t->c_first_child, t->c_nchild, t->c_leaf, t->colleagues,
-                  t->v_off, t->v_idx, t->v_cls, t->leaves, t->u_off, t->u_lo, t->u_hi,
+                  t->v_off, t->v_idx, t->v_cls, t->leaves, t->u_off, t->u_lo, t->u_hi, t->w_off, t->w_idx,
                   t->items, t->item_off, t->p2p_order, t->m2l_cells, t->op_pas, t->op_pasT, t->op_pm2l, t->op_w,
                   t->op_eps, t->op_e2i, t->mpole, t->local, t->src, t->part, t->d_sorted, t->y_sorted, t->y_far,
                   t->part_direct, t->up_list, t->ready_up, t->ready_down, t->tickets,
@@ -698,7 +756,8 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
     cudaFreeAsync(pos, s);
   }
 
-  // ---- U lists (merged source ranges) and P2P work items
+  // ---- U lists (merged source ranges), W lists and P2P work items
+  if (const char* e = getenv("DDM_W_MIN")) t->w_min = atoi(e);
   {
     const int nl = t->nleaves;
     int *ucnt = nullptr, *uoff = nullptr, *mcnt = nullptr, *moff = nullptr, *nsrc = nullptr;
@@ -708,15 +767,27 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
     DDM_CUDA(ctx, cudaMallocAsync((void**)&mcnt, nl * sizeof(int), s));
     DDM_CUDA(ctx, cudaMallocAsync((void**)&moff, nl * sizeof(int), s));
     DDM_CUDA(ctx, cudaMallocAsync((void**)&nsrc, nl * sizeof(int), s));
+    int* wcnt = nullptr;
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&wcnt, nl * sizeof(int), s));
     u_count<<<nblk(nl, 128), 128, 0, s>>>(nl, t->leaves, C.parent, t->colleagues, C.leaf,
-                                          C.start, C.count, ucnt);
+                                          C.start, C.count, C.level, C.ix, C.iy, C.first_child,
+                                          C.nchild, t->w_min, ucnt, wcnt);
     DDM_CUDA(ctx, cudaGetLastError());
     int tot = 0;
     if ((rc = exclusive_scan_i32(ctx, ucnt, uoff, nl, &tot, s))) return rc;
     DDM_CUDA(ctx, cudaMallocAsync((void**)&utmp, (size_t)std::max(tot, 1) * sizeof(int2), s));
+    // W lists: offsets per leaf, cells
+    int nwt = 0;
+    if ((rc = dalloc(ctx, &t->w_off, nl + 1))) return rc;
+    if ((rc = exclusive_scan_i32(ctx, wcnt, t->w_off, nl, &nwt, s))) return rc;
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->w_off + nl, &nwt, sizeof(int), cudaMemcpyHostToDevice, s));
+    t->nw = nwt;
+    if ((rc = dalloc(ctx, &t->w_idx, std::max(nwt, 1)))) return rc;
     u_fill<<<nblk(nl, 64), 64, 0, s>>>(nl, t->leaves, C.parent, t->colleagues, C.leaf, C.start,
-                                       C.count, uoff, utmp, mcnt, nsrc);
+                                       C.count, C.level, C.ix, C.iy, C.first_child, C.nchild,
+                                       t->w_min, uoff, utmp, mcnt, nsrc, t->w_off, t->w_idx);
     DDM_CUDA(ctx, cudaGetLastError());
+    cudaFreeAsync(wcnt, s);
     int nu = 0;
     if ((rc = exclusive_scan_i32(ctx, mcnt, moff, nl, &nu, s))) return rc;
     t->nu = nu;

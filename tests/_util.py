@@ -48,3 +48,10 @@ def rel_l2(a, b) -> float:
     b = np.asarray(b, dtype=np.float64).ravel()
     nb = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+def gpu_w_lists(tree) -> dict:
+    leaves = tree.export("LEAVES")
+    off = tree.export("W_OFF")
+    idx = tree.export("W_IDX")
+    return {int(leaves[k]): [int(v) for v in idx[off[k]:off[k + 1]]] for k in range(leaves.size)}

@@ -7,7 +7,7 @@ from oracle import tree as OT
 from synth import make_config
 from synth.geometry import Geometry
 
-from ._util import gpu_u_ranges, gpu_v_lists, oracle_u_ranges
+from ._util import gpu_w_lists, gpu_u_ranges, gpu_v_lists, oracle_u_ranges
 
 pytestmark = pytest.mark.gpu
 
@@ -41,16 +41,19 @@ def _compare(D, ctx, torch, g, leaf, lists=True, sample=None, min_side=0.0):
     leaves_by_start = sorted(np.nonzero(ot.is_leaf)[0], key=lambda c: ot.start[c])
     assert np.array_equal(tree.export("LEAVES"), np.array(leaves_by_start, dtype=np.int32))
     if lists:
+        wm = tree.counts["W_MIN"]
         if sample is None:
             V = OT.v_lists(ot)
-            U = OT.u_lists(ot)
+            U = OT.u_lists(ot, w_min=wm)
+            Wl = OT.w_lists(ot, wm)
         else:
             rng = np.random.default_rng(0)
             cells = rng.choice(ot.n_cells, size=min(sample, ot.n_cells), replace=False)
             leaves = rng.choice(np.nonzero(ot.is_leaf)[0], size=min(sample, int(ot.is_leaf.sum())),
                                 replace=False)
             V = OT.v_lists(ot, cells)
-            U = OT.u_lists(ot, leaves)
+            U = OT.u_lists(ot, leaves, w_min=wm)
+            Wl = OT.w_lists(ot, wm, leaves)
         gv = gpu_v_lists(tree)
         for c, lst in V.items():
             assert gv[c] == lst, c
@@ -58,6 +61,9 @@ def _compare(D, ctx, torch, g, leaf, lists=True, sample=None, min_side=0.0):
         ou = oracle_u_ranges(ot, U)
         for b, rs in ou.items():
             assert gu[b] == rs, b
+        gw = gpu_w_lists(tree)
+        for b, lst in Wl.items():
+            assert gw[b] == lst, b
     return tree, ot
 
 
@@ -66,9 +72,11 @@ def test_tree_bitexact_configs(ddm, cfg):
     D, ctx, torch = ddm
     g = make_config(cfg)
     tree, ot = _compare(D, ctx, torch, g, 32, sample=None if cfg != 3 else 400)
-    if cfg == 2:   # SURVEY.md §8 sizing table (own generator reproduces it)
+    if cfg == 2:   # SURVEY.md §8 sizing table (own generator reproduces it); the W split
+        # (w_min = 24, the library default) moves 20964 of its 327618 near pairs to M2P
         assert tree.counts["CELLS"] == 195 and tree.counts["LEAVES"] == 140
-        assert tree.counts["V"] == 2124 and tree.counts["NEAR_PAIRS"] == 327618
+        assert tree.counts["W_MIN"] == 24
+        assert tree.counts["V"] == 2124 and tree.counts["NEAR_PAIRS"] == 306654
 
 
 def test_tree_bitexact_config5_full_size(ddm):

@@ -94,6 +94,13 @@ def test_pair_coverage_on_random_trees():
         U, V = T.u_lists(t), T.v_lists(t)
         cov = T.pair_coverage(t, U, V)
         assert (cov == 1).all(), trial
+        # the W split (M2P cells) keeps the partition property
+        wm = int(rng.integers(1, 4))
+        Uw, Ww = T.u_lists(t, w_min=wm), T.w_lists(t, wm)
+        assert (T.pair_coverage(t, Uw, V, Ww) == 1).all(), (trial, wm)
+        for b, lst in Ww.items():   # W cells never touch their target leaf
+            for d in lst:
+                assert not T.touching(t.cells[d], t.cells[b])
         # every element sits in exactly one leaf; leaves hold <= leaf points
         assert t.count[t.is_leaf].sum() == n
         assert (t.count[t.is_leaf] <= leaf).all()
