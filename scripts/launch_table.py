@@ -9,8 +9,9 @@ hdr = rows[0]
 ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
 recs = [(r[ki], float(r[vi].replace(",", ""))) for r in rows[1:]]
 last = max(i for i, (k, _) in enumerate(recs) if "prep_sources" in k or "poro_prep" in k)
+end = next((i for i in range(last, len(recs)) if "finalize" in recs[i][0]), len(recs) - 1)
 agg = collections.OrderedDict()
-for k, v in recs[last:]:
+for k, v in recs[last:end + 1]:
     name = k.split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
     name = name.replace("unnamed>::", "")
     a = agg.setdefault(name, [0, 0.0])
