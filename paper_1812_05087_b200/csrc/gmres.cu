@@ -53,7 +53,8 @@ __global__ void reduce_parts(const double* __restrict__ part, int nvec, int nb,
   if (lane == 0) out[i] = s;
 }
 
-// w[j] += sign * sum_i V[i * ld + j] c[i]
+// w[j] += sign * sum_i V[i * ld + j] c[i]: eight independent accumulators
+// per thread (eight loads of the basis in flight), summed in a fixed order
 __global__ void multi_axpy(const double* __restrict__ V, int64_t ld, int nvec,
                            const double* __restrict__ c, double sign, double* __restrict__ w,
                            int64_t len) {
@@ -62,8 +63,15 @@ __global__ void multi_axpy(const double* __restrict__ V, int64_t ld, int nvec,
   __syncthreads();
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < len;
        j += (int64_t)gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int i = 0; i < nvec; ++i) acc = fma(V[(int64_t)i * ld + j], sc[i], acc);
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    const double* v = V + j;
+    int i = 0;
+    for (; i + 8 <= nvec; i += 8) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = fma(__ldg(v + (int64_t)(i + q) * ld), sc[i + q], a[q]);
+    }
+    for (int q = 0; i < nvec; ++i, ++q) a[q] = fma(__ldg(v + (int64_t)i * ld), sc[i], a[q]);
+    const double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     w[j] = fma(sign, acc, w[j]);
   }
 }
