@@ -226,3 +226,38 @@ def test_bad_arguments(ddm):
     assert e.value.code == 1
     with pytest.raises(D.DDMError):
         D.matvec(ctx, tree, D.material(0, G0, 0.25), Dv, mode=7)
+
+
+def test_gmres_plain_and_restarted(ddm):
+    # R11/R20: the plain method (no preconditioner) and a short restart both
+    # reach the LU solution; right preconditioning keeps the true residual test
+    D, ctx, torch = ddm
+    g, tree = _setup(D, ctx, torch, 2, p=CONFIGS[2]["p_star"])
+    c = CONFIGS[2]
+    load = c["load"]
+    mat = D.material(0, G0, NU0)
+    b = D.farfield_rhs(ctx, torch.tensor(g.beta, device="cuda"), 2, load["p_f"], load["sH"],
+                       load["sh"])
+    x_lu = np.linalg.solve(_A(2), OE.farfield_rhs(g, load).reshape(-1)).reshape(-1, 2)
+    x0, it0, _ = D.gmres_solve(ctx, tree, mat, b, tol=1e-10, precond=False)
+    x1, it1, rr1 = D.gmres_solve(ctx, tree, mat, b, tol=1e-10, restart=40, max_iter=5000)
+    x2, it2, _ = D.gmres_solve(ctx, tree, mat, b, tol=1e-10)
+    for x in (x0, x1, x2):
+        assert rel_l2(x.cpu().numpy(), x_lu) <= 1e-6
+    assert it1 > it2 and rr1 <= 1e-10 and it2 < it0   # restarts cost iterations; block Jacobi saves
+
+
+def test_no_w_lists_reproduce_survey_sizes_and_parity(ddm, monkeypatch):
+    # DDM_W_MIN=0 turns the W split off: the lists are the SURVEY §8 table's
+    # (R5 without W: 327618 near pairs for config 2) and the FMM still matches
+    # the dense oracle
+    D, ctx, torch = ddm
+    monkeypatch.setenv("DDM_W_MIN", "0")
+    g = make_config(2)
+    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+    tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=32, order_p=20)
+    assert tree.counts["W"] == 0 and tree.counts["W_MIN"] == 0
+    assert tree.counts["NEAR_PAIRS"] == 327618
+    Dv = random_dd(g.n, 2, 102)
+    y = _mv(D, ctx, torch, tree, Dv, "fmm")
+    assert rel_l2(y, OE.matvec_dense(_A(2), Dv)) <= 1e-8
