@@ -322,6 +322,20 @@ constexpr int kM2LBatch = 4;     // V pairs per pipelined batch (2 DMMA n-tiles)
 // n-tile) and post-scales.  Lane l owns output rows m = 8 i + l/4 of series
 // (l%4)%2 for pair parity (l%4)/2; the parities are summed at the end.
 // Results go to out_l[m], out_g[m] (m < p).
+// conj(delta) of the 49 offset classes, delta = -(dx + i dy) (fmm.cu), i.e.
+// conj(delta) = (-dx, dy) with dx = o % 7 - 3, dy = o / 7 - 3
+__constant__ double2 c_dconj[kNOffsets] = {
+#define DDM_DC(o) {-(double)((o) % 7 - 3), (double)((o) / 7 - 3)}
+    DDM_DC(0), DDM_DC(1), DDM_DC(2), DDM_DC(3), DDM_DC(4), DDM_DC(5), DDM_DC(6),
+    DDM_DC(7), DDM_DC(8), DDM_DC(9), DDM_DC(10), DDM_DC(11), DDM_DC(12), DDM_DC(13),
+    DDM_DC(14), DDM_DC(15), DDM_DC(16), DDM_DC(17), DDM_DC(18), DDM_DC(19), DDM_DC(20),
+    DDM_DC(21), DDM_DC(22), DDM_DC(23), DDM_DC(24), DDM_DC(25), DDM_DC(26), DDM_DC(27),
+    DDM_DC(28), DDM_DC(29), DDM_DC(30), DDM_DC(31), DDM_DC(32), DDM_DC(33), DDM_DC(34),
+    DDM_DC(35), DDM_DC(36), DDM_DC(37), DDM_DC(38), DDM_DC(39), DDM_DC(40), DDM_DC(41),
+    DDM_DC(42), DDM_DC(43), DDM_DC(44), DDM_DC(45), DDM_DC(46), DDM_DC(47), DDM_DC(48)
+#undef DDM_DC
+};
+
 constexpr int kXStride = 36;   // doubles per X column (>= p+1; = 4 mod 16: conflict-free fragments)
 
 template <int PT>
@@ -352,29 +366,32 @@ __device__ void m2l_cell_tc(int vb, int ve, const int* __restrict__ v_idx,
 #pragma unroll
       for (int rr = 0; rr < NR; ++rr) {
         const int n = lane + 32 * rr;
-        double2 ra[kM2LBatch], rg[kM2LBatch], rp[kM2LBatch], rw[kM2LBatch];
-        int cl[kM2LBatch];
+        // lane constants: which of slots n, n-1 exist; -n as a double
+        const bool in_a = n < p, in_p = n >= 1 && n <= p, in_w = n <= p;
+        const int na_ = in_a ? n : 0, np_ = in_p ? n - 1 : 0, nw_ = in_w ? n + 1 : 0;
+        const double mn = -(double)n;
+        double2 ra[kM2LBatch], rg[kM2LBatch], rp[kM2LBatch], rw[kM2LBatch], dc[kM2LBatch];
 #pragma unroll
         for (int v = 0; v < kM2LBatch; ++v) {
           const int src = __shfl_sync(0xffffffffu, my_src, (b0 + v) & 31);
-          cl[v] = __shfl_sync(0xffffffffu, my_cls, (b0 + v) & 31);
-          const double2* ma = mpole + (size_t)src * P2;
-          const double2 z = make_double2(0.0, 0.0);
-          const bool ok = v < nb;
-          ra[v] = (ok && n < p) ? __ldg(ma + n) : z;
-          rg[v] = (ok && n < p) ? __ldg(ma + p + n) : z;
-          rp[v] = (ok && n >= 1 && n <= p) ? __ldg(ma + n - 1) : z;
-          rw[v] = (ok && n <= p) ? __ldg(w_g + cl[v] * pw + n + 1) : z;
+          const int cl = __shfl_sync(0xffffffffu, my_cls, (b0 + v) & 31);
+          const double2* ma = mpole + (size_t)src * P2;   // src = 0 for v >= nb: valid memory
+          ra[v] = __ldg(ma + na_);
+          rg[v] = __ldg(ma + p + na_);
+          rp[v] = __ldg(ma + np_);
+          rw[v] = __ldg(w_g + cl * pw + nw_);
+          dc[v] = c_dconj[cl];   // conj(delta) of the class (constant-cache broadcast)
         }
         if (n < KB) {
+          const double2 z = make_double2(0.0, 0.0);
 #pragma unroll
           for (int v = 0; v < kM2LBatch; ++v) {
-            const double2 av = cmul(ra[v], rw[v]);
-            double2 cv = rg[v];
-            const double2 dconj =
-                make_double2(-(double)(cl[v] % 7 - 3), (double)(cl[v] / 7 - 3));   // conj(delta)
-            cmac(cv, cscale(dconj, -(double)n), rp[v]);
-            cv = cmul(cv, rw[v]);
+            const bool ok = v < nb;
+            const double2 wv = (ok && in_w) ? rw[v] : z;
+            const double2 av = in_a ? cmul(ra[v], wv) : z;
+            double2 cv = in_a ? rg[v] : z;
+            if (in_p) cmac(cv, cscale(dc[v], mn), rp[v]);
+            cv = cmul(cv, wv);
             double* xc = X + (size_t)(4 * v) * kXStride + n;
             xc[0] = av.x;
             xc[kXStride] = av.y;
