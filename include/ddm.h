@@ -57,7 +57,11 @@ typedef enum {
 
 enum { DDM_FMM = 0, DDM_DIRECT = 1,
        DDM_HIST_PERLAG = 2, /* ddm_history_apply only: one FMM matvec per lag (the paper's scheme) */
-       DDM_GMRES_NO_PRECOND = 8 /* ddm_gmres_solve only, OR-ed into mode: plain GMRES */ };
+       DDM_GMRES_NO_PRECOND = 8, /* ddm_gmres_solve only, OR-ed into mode: plain GMRES */
+       DDM_BBFMM = 16 /* ddm_matvec / ddm_gmres_solve, elastic: the paper's Chebyshev
+                         (bbFMM) far field with n nodes per dimension, mode =
+                         DDM_BBFMM_MODE(n), 2 <= n <= 8 */ };
+#define DDM_BBFMM_MODE(n) (DDM_BBFMM | ((n) << 8))
 
 /* Material (Table rock_prop).  kind 0 = elastic (only G,
  * nu used), 1 = fully coupled poroelastic.  kappa = k / mu (m^2 / (Pa s)). */
@@ -146,7 +150,15 @@ int ddm_split_costs(const int64_t* prefix_excl, int64_t total, int nleaves, int 
  * y = A(elapsed) D (Eq.(final_sigs)-(final_pp) left-hand side).
  * D, y [device], [n][ncomp] user order.  mode DDM_FMM: the FMM of DESIGN.md
  * §4 (P2M, M2M, M2L, L2L, L2P + exact near-field P2P).
- * mode DDM_DIRECT: exact all-pairs evaluation (no expansions).  elapsed is the
+ * mode DDM_DIRECT: exact all-pairs evaluation (no expansions).
+ * mode DDM_BBFMM_MODE(n) (elastic only): the same tree, lists and exact near
+ * field, far field by the paper's black-box FMM -- Chebyshev interpolation
+ * with n x n nodes per cell (S_n), node weights (Eq.(p2l),
+ * Eq.(m2m)), kernel at node pairs (Eq.(m2l)), interpolation down the tree
+ * (Eq.(l2l)) and at the targets; DESIGN.md §4.9.  Accuracy is the
+ * interpolation's (n = 3: ~1e-4, n = 6: ~1e-6 relative), not the series'.
+ * Errors: n outside [2, 8] or a poroelastic material -> DDM_ERR_ARG.
+ * elapsed is the
  * time since the constant source was switched on (poroelastic; ignored when
  * elastic).  Multi-GPU: D and y are full-length on every rank; y is complete
  * on every rank on return (owned slices exchanged with NCCL all-gather).

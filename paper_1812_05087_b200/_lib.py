@@ -22,6 +22,7 @@ lib = C.CDLL(LIB_PATH)
 OK, ERR_ARG, ERR_CUDA, ERR_NOCONV, ERR_NCCL, ERR_GEOM, ERR_OOM = range(7)
 FMM, DIRECT, HIST_PERLAG = 0, 1, 2
 GMRES_NO_PRECOND = 8
+BBFMM = 16   # | n << 8: Chebyshev (bbFMM) far field with n nodes per dimension
 
 TC = dict(N=0, CELLS=1, LEAVES=2, LEVELS=3, V=4, URANGES=5, NEAR_PAIRS=6, P2P_ITEMS=7,
           OWNED_LO=8, OWNED_HI=9, P=10, W=11, W_MIN=12)

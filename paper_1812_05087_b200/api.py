@@ -155,8 +155,14 @@ class Tree:
 
 
 def _mode(mode) -> int:
-    return ({"fmm": L.FMM, "direct": L.DIRECT, "perlag": L.HIST_PERLAG}[mode]
-            if isinstance(mode, str) else int(mode))
+    """"fmm" (complex-variable series), "direct", "perlag" (history), or
+    "bbfmm<n>" (the paper's Chebyshev far field with n nodes per dimension,
+    e.g. "bbfmm3", "bbfmm6"; elastic)."""
+    if not isinstance(mode, str):
+        return int(mode)
+    if mode.startswith("bbfmm"):
+        return L.BBFMM | (int(mode[5:]) << 8)
+    return {"fmm": L.FMM, "direct": L.DIRECT, "perlag": L.HIST_PERLAG}[mode]
 
 
 def matvec(ctx: Context, tree: Tree, mat, D: torch.Tensor, y: torch.Tensor | None = None,

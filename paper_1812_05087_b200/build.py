@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libddm.so")
 SOURCES = ["api.cu", "scan.cu", "tree.cu", "fmm.cu", "expansions.cu", "p2p.cu", "poro.cu",
-           "gmres.cu"]
+           "gmres.cu", "bbfmm.cu"]
 HEADERS = ["ddm_internal.cuh", "kcommon.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -425,7 +425,10 @@ int ddm_matvec(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double elap
   if (!ctx || !t || !D || !y) return ctx ? set_error(ctx, DDM_ERR_ARG, "NULL argument") : DDM_ERR_ARG;
   int rc = check_material(ctx, mat);
   if (rc) return rc;
-  if (mode != DDM_FMM && mode != DDM_DIRECT) return set_error(ctx, DDM_ERR_ARG, "bad mode");
+  if (mode != DDM_FMM && mode != DDM_DIRECT &&
+      !((mode & 0xff) == DDM_BBFMM && ((mode >> 8) & 0xff) >= 2 && ((mode >> 8) & 0xff) <= 8 &&
+        (mode >> 16) == 0))
+    return set_error(ctx, DDM_ERR_ARG, "bad mode");
   cudaStream_t s = (cudaStream_t)stream;
   const int ncomp = mat->kind == 1 ? 3 : 2;
   if (ctx->world == 1) return fmm_matvec(ctx, t, mat, elapsed, D, false, y, nullptr, mode, s);

@@ -173,6 +173,10 @@ struct ddm_tree_s {
   double* y_sorted = nullptr;     // [n*3]
   double* y_far = nullptr;        // [n*3] L2P far field of the owned elements (sorted order)
   double* part_direct = nullptr;  // [n*2] direct-mode tractions (sorted)
+  // bbFMM far field (bbfmm.cu): node weights W and node values F, [ncells][3][bb_n^2] complex
+  double2* bb_w = nullptr;
+  double2* bb_f = nullptr;
+  int bb_n = 0;
   // matvec CUDA graphs (fmm.cu)
   std::vector<MatvecGraph> graphs = std::vector<MatvecGraph>(4);
   int graph_next = 0;
@@ -244,6 +248,11 @@ int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double el
 // fast history sum (poroelastic): r = sum_{m=1}^{h} A^(m) D^(h-m), D_hist user order
 int fmm_history(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt, int h,
                 const double* D_hist, double* y_user, double* y_sorted, cudaStream_t s);
+
+// bbfmm.cu: Chebyshev far field with n nodes per dimension (mode DDM_BBFMM)
+int bb_prepare(ddm_ctx_s* ctx, ddm_tree_s* t, int n);
+int launch_bb_far(ddm_ctx_s* ctx, ddm_tree_s* t, int n, const double* D, int ncomp, double gc,
+                  cudaStream_t s);
 
 // gmres.cu
 int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt,

@@ -209,6 +209,14 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
     }
   }
 
+  // Chebyshev far field (f2, bbfmm.cu): mode DDM_BBFMM | n << 8, elastic
+  const bool bb = (mode & DDM_BBFMM) != 0;
+  const int bb_n = (mode >> 8) & 0xff;
+  if (bb) {
+    if (poro) return set_error(ctx, DDM_ERR_ARG, "the bbFMM far field is elastic only");
+    if ((rc = bb_prepare(ctx, t, bb_n))) return rc;
+  }
+
   stage_begin(ctx, DDM_ST_PREP, s);
   rc = poro ? launch_poro_prep(ctx, t, perm_in, D, s)
             : launch_prep_sources(ctx, t, perm_in, D, ncomp, s);
@@ -239,6 +247,9 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
   stage_end(ctx, DDM_ST_P2P, sn);
   DDM_CUDA(ctx, cudaEventRecord(ctx->ev_near, sn));
 
+  if (bb) {
+    if ((rc = launch_bb_far(ctx, t, bb_n, perm_in ? t->d_sorted : D, ncomp, gc, sf))) return rc;
+  } else {
   // upward pass: P2M on all leaves, M2M level by level (replicated on all
   // ranks); prep gathered D into sorted order, so it is read coalesced
   if ((rc = launch_upward(ctx, t, nullptr, perm_in ? t->d_sorted : D, ncomp, pf, sf))) return rc;
@@ -249,6 +260,7 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
   stage_begin(ctx, DDM_ST_L2P, sf);
   if ((rc = launch_l2p(ctx, t, ncomp, gc, pf, sf))) return rc;
   stage_end(ctx, DDM_ST_L2P, sf);
+  }
   DDM_CUDA(ctx, cudaEventRecord(ctx->ev_far, sf));
 
   // join
