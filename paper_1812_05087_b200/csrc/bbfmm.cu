@@ -35,20 +35,8 @@ __constant__ double c_bbX[kBBMaxN + 1][kBBMaxN];               // [n][i] xbar_i
 __constant__ double c_bbGx[kBBMaxN + 1][kBBMaxN];              // [n][g] Gauss-Legendre nodes
 __constant__ double c_bbGw[kBBMaxN + 1][kBBMaxN];              // [n][g] Gauss-Legendre weights
 
-// T_0..T_{N-1} at x, then S_n(xbar_i, x) for the given row of T_k(xbar_i)
-template <int N>
-__device__ __forceinline__ double card1(const double (&Trow)[N], double x) {
-  double s = 0.0, tkm = 1.0, tk = x;
-#pragma unroll
-  for (int k = 1; k < N; ++k) {
-    s = fma(Trow[k], tk, s);
-    const double tn = fma(2.0 * x, tk, -tkm);
-    tkm = tk;
-    tk = tn;
-  }
-  return (1.0 + 2.0 * s) * (1.0 / N);
-}
-
+// S_n(xbar_i, x) for i < N: T_0..T_{N-1}(x) by the recurrence, then the
+// sums against T_k(xbar_i)
 template <int N>
 __device__ __forceinline__ void card_all(double x, double (&S)[N]) {
   double T[N];
@@ -70,8 +58,17 @@ __device__ __forceinline__ bool owns(int cs, int cn, int64_t lo, int64_t hi) {
 }
 
 // ---------------------------------------------------------------- P2M
-// thread = (leaf, node m = i N + k): the three weights of node m summed over
-// the leaf's elements and their N Gauss-Legendre points (Eq.(p2l))
+// warp per leaf (Eq.(p2l)).  The leaf's (element, Gauss-Legendre point)
+// pairs are taken 32 at a time: phase 1, lane = pair: the 1D cardinal values
+// S_n(xbar_i, xi), S_n(xbar_k, eta) of its point and its three densities
+// (times the quadrature weight) into shared memory; phase 2, lane = node
+// m = i N + k (two rounds when N^2 > 32): W_m += sum_pairs Sx_i Sy_k c_pair.
+template <int N>
+struct BBP2MSmem {
+  double sx[32][N], sy[32][N];
+  double2 c1[32], c2[32], c3[32];
+};
+
 template <int N>
 __global__ void __launch_bounds__(128)
 bb_p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ c_level,
@@ -82,56 +79,122 @@ bb_p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict
               const double* __restrict__ ec, const double* __restrict__ es, double gc,
               double2* __restrict__ bbw) {
   constexpr int NN = N * N;
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int k = (int)(gid / NN);
+  constexpr int NR = (NN + 31) / 32;
+  __shared__ BBP2MSmem<N> sm_all[4];
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (k >= nleaves) return;
-  const int m = (int)(gid % NN), mi = m / N, mk = m % N;
-  double Tx[N], Ty[N];
-#pragma unroll
-  for (int q = 0; q < N; ++q) {
-    Tx[q] = c_bbT[N][mi][q];
-    Ty[q] = c_bbT[N][mk][q];
-  }
+  BBP2MSmem<N>& sm = sm_all[threadIdx.x >> 5];
   const int c = leaves[k];
   const int lev = c_level[c];
   const double hs = 0.5 * cg.side(lev), ihs = 1.0 / hs;
   const double2 z0 = cg.centre(lev, c_ix[c], c_iy[c]);
-  double2 w1 = make_double2(0, 0), w2 = w1, w3 = w1;
-  for (int e = c_start[c], e1 = e + c_count[c]; e < e1; ++e) {
-    const double ds = D[(int64_t)e * ncomp], dn = D[(int64_t)e * ncomp + 1];
-    const double cb = ec[e], sb = es[e], a = ea[e];
-    const double2 eb = make_double2(cb, sb);
-    const double2 B = make_double2(ds * cb - dn * sb, ds * sb + dn * cb);
-    const double2 r = make_double2(cb * cb - sb * sb, -2.0 * cb * sb);
-    const double2 Q = csub(cmul(r, B), cconj(B));
-    const double2 Be = cmul(B, eb), Qe = cmul(Q, eb);
-    const double xc = (ex[e] - z0.x) * ihs, yc = (ey[e] - z0.y) * ihs;
-    const double ax = a * cb * ihs, ay = a * sb * ihs;
-    double2 s1 = make_double2(0, 0), s3 = s1;   // sum S w, sum S w conj(zeta - c)/hs
+  const int e0 = c_start[c], npair = c_count[c] * N;
+  double2 w1[NR], w2[NR], w3[NR];
 #pragma unroll
-    for (int g = 0; g < N; ++g) {
-      const double tg = c_bbGx[N][g];
-      const double xi = fma(tg, ax, xc), eta = fma(tg, ay, yc);
-      const double S = c_bbGw[N][g] * card1<N>(Tx, xi) * card1<N>(Ty, eta);
-      s1.x += S;
-      s3.x = fma(S, xi, s3.x);
-      s3.y = fma(-S, eta, s3.y);
+  for (int r = 0; r < NR; ++r) w1[r] = w2[r] = w3[r] = make_double2(0, 0);
+  for (int p0 = 0; p0 < npair; p0 += 32) {
+    const int pr = p0 + lane;
+    if (pr < npair) {
+      const int e = e0 + pr / N, g = pr % N;
+      const double ds = D[(int64_t)e * ncomp], dn = D[(int64_t)e * ncomp + 1];
+      const double cb = ec[e], sb = es[e], a = ea[e];
+      const double2 eb = make_double2(cb, sb);
+      const double2 B = make_double2(ds * cb - dn * sb, ds * sb + dn * cb);
+      const double2 r = make_double2(cb * cb - sb * sb, -2.0 * cb * sb);
+      const double2 Q = csub(cmul(r, B), cconj(B));
+      const double tg = c_bbGx[N][g], wa = c_bbGw[N][g] * a;
+      const double xi = fma(tg, a * cb * ihs, (ex[e] - z0.x) * ihs);
+      const double eta = fma(tg, a * sb * ihs, (ey[e] - z0.y) * ihs);
+      double Sx[N], Sy[N];
+      card_all<N>(xi, Sx);
+      card_all<N>(eta, Sy);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        sm.sx[lane][i] = Sx[i];
+        sm.sy[lane][i] = Sy[i];
+      }
+      // densities / (i gc) times wg a:  Be, Qe, 2 Be conj(zeta - c) = 2 hs Be (xi - i eta)
+      const double2 Be = cmul(B, eb);
+      sm.c1[lane] = cscale(Be, wa);
+      sm.c2[lane] = cscale(cmul(Q, eb), wa);
+      sm.c3[lane] = cscale(cmul(Be, make_double2(xi, -eta)), 2.0 * hs * wa);
     }
-    // sum_g wg a S (rho / (i gc)):  w1 += a s1 Be, w2 += a s1 Qe, w3 += 2 a hs s3 Be
-    w1 = cadd(w1, cscale(Be, a * s1.x));
-    w2 = cadd(w2, cscale(Qe, a * s1.x));
-    w3 = cadd(w3, cscale(cmul(s3, Be), 2.0 * a * hs));
+    __syncwarp();
+    const int np = min(32, npair - p0);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int m = lane + 32 * r;
+      if (m < NN) {
+        const int mi = m / N, mk = m % N;
+        for (int q = 0; q < np; ++q) {
+          const double S = sm.sx[q][mi] * sm.sy[q][mk];
+          const double2 v1 = sm.c1[q], v2 = sm.c2[q], v3 = sm.c3[q];
+          w1[r].x = fma(S, v1.x, w1[r].x); w1[r].y = fma(S, v1.y, w1[r].y);
+          w2[r].x = fma(S, v2.x, w2[r].x); w2[r].y = fma(S, v2.y, w2[r].y);
+          w3[r].x = fma(S, v3.x, w3[r].x); w3[r].y = fma(S, v3.y, w3[r].y);
+        }
+      }
+    }
+    __syncwarp();
   }
   // times i gc
   double2* W = bbw + (size_t)c * 3 * NN;
-  W[m] = make_double2(-gc * w1.y, gc * w1.x);
-  W[NN + m] = make_double2(-gc * w2.y, gc * w2.x);
-  W[2 * NN + m] = make_double2(-gc * w3.y, gc * w3.x);
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int m = lane + 32 * r;
+    if (m < NN) {
+      W[m] = make_double2(-gc * w1[r].y, gc * w1[r].x);
+      W[NN + m] = make_double2(-gc * w2[r].y, gc * w2[r].x);
+      W[2 * NN + m] = make_double2(-gc * w3[r].y, gc * w3[r].x);
+    }
+  }
 }
 
-// ---------------------------------------------------------------- M2M
-// thread = (parent cell of one level, node): Eq.(m2m), the third weight
-// re-centred on the parent (w3 += 2 conj(c_child - c_parent) w1)
+// ---------------------------------------------------------------- M2M / L2L
+// Both are the 2D interpolation between a parent's nodes and a child's nodes,
+// a product of two 1D N x N matrices (c_bbS), applied separably (2 N^3 per
+// density instead of N^4) by one warp per cell through shared memory.
+template <int N>
+struct BBTransSmem {
+  double2 a[3][N * N], b[3][N * N];
+};
+
+// dst[d][i*N + l] = sum_k M[i][k] src[d][k*N + l]   (first index)   when FIRST,
+// dst[d][i*N + l] = sum_k M[l][k] src[d][i*N + k]   (second index)  otherwise;
+// M(i, k) = S[h][i][k] (M2M, parent node i <- child node k) or S[h][k][i] (L2L)
+template <int N, bool FIRST, bool TRANS>
+__device__ __forceinline__ void bb_pass(const double (*S)[N][N], int h, const double2 (*src)[N * N],
+                                        double2 (*dst)[N * N], int lane) {
+  constexpr int NN = N * N;
+  for (int m = lane; m < NN; m += 32) {
+    const int i = m / N, l = m % N;
+    const int row = FIRST ? i : l;
+    double2 t[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const double M = TRANS ? S[h][k][row] : S[h][row][k];
+      const int q = FIRST ? k * N + l : i * N + k;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        t[d].x = fma(M, src[d][q].x, t[d].x);
+        t[d].y = fma(M, src[d][q].y, t[d].y);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) dst[d][m] = t[d];
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void bb_stage_S(double (*sS)[N][N]) {
+  for (int f = threadIdx.x; f < 2 * N * N; f += blockDim.x)
+    sS[f / (N * N)][(f / N) % N][f % N] = c_bbS[N][f / (N * N)][(f / N) % N][f % N];
+  __syncthreads();
+}
+
+// warp per parent of one level (Eq.(m2m)); the third weight re-centred on
+// the parent: w3 += 2 conj(c_child - c_parent) w1
 template <int N>
 __global__ void __launch_bounds__(128)
 bb_m2m_level_kernel(int u0, int u1, const int* __restrict__ up_list,
@@ -139,49 +202,50 @@ bb_m2m_level_kernel(int u0, int u1, const int* __restrict__ up_list,
                     const int* __restrict__ c_iy, const int* __restrict__ c_first_child,
                     const int* __restrict__ c_nchild, CellGeom cg, double2* __restrict__ bbw) {
   constexpr int NN = N * N;
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int idx = (int)(gid / NN);
-  if (u0 + idx >= u1) return;
-  const int m = (int)(gid % NN), mi = m / N, mj = m % N;
-  const int P = up_list[u0 + idx];
+  __shared__ double sS[2][N][N];
+  __shared__ BBTransSmem<N> sm_all[4];
+  bb_stage_S<N>(sS);
+  const int lane = threadIdx.x & 31;
+  const int idx = u0 + blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (idx >= u1) return;
+  BBTransSmem<N>& sm = sm_all[threadIdx.x >> 5];
+  const int P = up_list[idx];
   const double q4 = 0.25 * cg.side(c_level[P]);
-  double2 a1 = make_double2(0, 0), a2 = a1, a3 = a1;
+  constexpr int NR = (NN + 31) / 32;
+  double2 acc[3][NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[0][r] = acc[1][r] = acc[2][r] = make_double2(0, 0);
   for (int q = c_first_child[P], q1 = q + c_nchild[P]; q < q1; ++q) {
     const int hx = c_ix[q] & 1, hy = c_iy[q] & 1;
-    double Sx[N], Sy[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      Sx[k] = c_bbS[N][hx][mi][k];
-      Sy[k] = c_bbS[N][hy][mj][k];
-    }
-    const double2* Wq = bbw + (size_t)q * 3 * NN;
-    double2 s1 = make_double2(0, 0), s2 = s1, s3 = s1;
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      double2 t1 = make_double2(0, 0), t2 = t1, t3 = t1;
-#pragma unroll
-      for (int l = 0; l < N; ++l) {
-        const int mc = k * N + l;
-        const double S = Sy[l];
-        const double2 v1 = Wq[mc], v2 = Wq[NN + mc], v3 = Wq[2 * NN + mc];
-        t1.x = fma(S, v1.x, t1.x); t1.y = fma(S, v1.y, t1.y);
-        t2.x = fma(S, v2.x, t2.x); t2.y = fma(S, v2.y, t2.y);
-        t3.x = fma(S, v3.x, t3.x); t3.y = fma(S, v3.y, t3.y);
-      }
-      s1.x = fma(Sx[k], t1.x, s1.x); s1.y = fma(Sx[k], t1.y, s1.y);
-      s2.x = fma(Sx[k], t2.x, s2.x); s2.y = fma(Sx[k], t2.y, s2.y);
-      s3.x = fma(Sx[k], t3.x, s3.x); s3.y = fma(Sx[k], t3.y, s3.y);
-    }
     // 2 conj(c_q - c_P) = 2 q4 ((2hx - 1) - i (2hy - 1))
     const double2 sh = make_double2(2.0 * q4 * (2 * hx - 1), -2.0 * q4 * (2 * hy - 1));
-    a1 = cadd(a1, s1);
-    a2 = cadd(a2, s2);
-    a3 = cadd(a3, cadd(s3, cmul(sh, s1)));
+    const double2* Wq = bbw + (size_t)q * 3 * NN;
+    for (int m = lane; m < NN; m += 32) {
+      const double2 v1 = Wq[m];
+      sm.a[0][m] = v1;
+      sm.a[1][m] = Wq[NN + m];
+      sm.a[2][m] = cadd(Wq[2 * NN + m], cmul(sh, v1));
+    }
+    __syncwarp();
+    bb_pass<N, true, false>(sS, hx, sm.a, sm.b, lane);    // parent x-node <- child x-node
+    __syncwarp();
+    bb_pass<N, false, false>(sS, hy, sm.b, sm.a, lane);   // parent y-node <- child y-node
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int m = lane + 32 * r;
+      if (m < NN)
+        for (int d = 0; d < 3; ++d) acc[d][r] = cadd(acc[d][r], sm.a[d][m]);
+    }
+    __syncwarp();
   }
   double2* W = bbw + (size_t)P * 3 * NN;
-  W[m] = a1;
-  W[NN + m] = a2;
-  W[2 * NN + m] = a3;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int m = lane + 32 * r;
+    if (m < NN)
+      for (int d = 0; d < 3; ++d) W[d * NN + m] = acc[d][r];
+  }
 }
 
 // node-pair kernel sums of one source cell's weights at the point u (units of
@@ -250,8 +314,9 @@ bb_m2l_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restr
 }
 
 // ---------------------------------------------------------------- L2L
-// thread = (cell of one level >= 3 holding owned targets, node): Eq.(l2l),
-// Psi~ re-centred on the child (Psi~_c = Psi~_P + conj(c_c - c_P) Phi')
+// warp per cell of one level >= 3 holding owned targets (Eq.(l2l)): the
+// parent's node values, Psi~ re-centred on the child (Psi~ + conj(c_c - c_P)
+// Phi'), interpolated at the child's nodes and added to its M2L result
 template <int N>
 __global__ void __launch_bounds__(128)
 bb_l2l_level_kernel(int a, int b, int64_t own_lo, int64_t own_hi, const int* __restrict__ c_level,
@@ -259,44 +324,34 @@ bb_l2l_level_kernel(int a, int b, int64_t own_lo, int64_t own_hi, const int* __r
                     const int* __restrict__ c_start, const int* __restrict__ c_count,
                     const int* __restrict__ c_parent, CellGeom cg, double2* __restrict__ bbf) {
   constexpr int NN = N * N;
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int c = a + (int)(gid / NN);
+  __shared__ double sS[2][N][N];
+  __shared__ BBTransSmem<N> sm_all[4];
+  bb_stage_S<N>(sS);
+  const int lane = threadIdx.x & 31;
+  const int c = a + blockIdx.x * 4 + (threadIdx.x >> 5);
   if (c >= b) return;
   if (!owns(c_start[c], c_count[c], own_lo, own_hi)) return;
-  const int m = (int)(gid % NN), mk = m / N, ml = m % N;
+  BBTransSmem<N>& sm = sm_all[threadIdx.x >> 5];
   const int P = c_parent[c];
   const int hx = c_ix[c] & 1, hy = c_iy[c] & 1;
-  double Sx[N], Sy[N];
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    Sx[i] = c_bbS[N][hx][i][mk];
-    Sy[i] = c_bbS[N][hy][i][ml];
-  }
-  const double2* FP = bbf + (size_t)P * 3 * NN;
-  double2 s1 = make_double2(0, 0), s2 = s1, s3 = s1;
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    double2 t1 = make_double2(0, 0), t2 = t1, t3 = t1;
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-      const int mp = i * N + j;
-      const double S = Sy[j];
-      const double2 v1 = FP[mp], v2 = FP[NN + mp], v3 = FP[2 * NN + mp];
-      t1.x = fma(S, v1.x, t1.x); t1.y = fma(S, v1.y, t1.y);
-      t2.x = fma(S, v2.x, t2.x); t2.y = fma(S, v2.y, t2.y);
-      t3.x = fma(S, v3.x, t3.x); t3.y = fma(S, v3.y, t3.y);
-    }
-    s1.x = fma(Sx[i], t1.x, s1.x); s1.y = fma(Sx[i], t1.y, s1.y);
-    s2.x = fma(Sx[i], t2.x, s2.x); s2.y = fma(Sx[i], t2.y, s2.y);
-    s3.x = fma(Sx[i], t3.x, s3.x); s3.y = fma(Sx[i], t3.y, s3.y);
-  }
   // conj(c_c - c_P) = s_c/2 ((2hx - 1) - i (2hy - 1))
   const double hc = 0.5 * cg.side(c_level[c]);
   const double2 sh = make_double2(hc * (2 * hx - 1), -hc * (2 * hy - 1));
+  const double2* FP = bbf + (size_t)P * 3 * NN;
+  for (int m = lane; m < NN; m += 32) {
+    const double2 v2 = FP[NN + m];
+    sm.a[0][m] = FP[m];
+    sm.a[1][m] = v2;
+    sm.a[2][m] = cadd(FP[2 * NN + m], cmul(sh, v2));
+  }
+  __syncwarp();
+  bb_pass<N, true, true>(sS, hx, sm.a, sm.b, lane);    // child x-node <- parent x-node
+  __syncwarp();
+  bb_pass<N, false, true>(sS, hy, sm.b, sm.a, lane);   // child y-node <- parent y-node
+  __syncwarp();
   double2* F = bbf + (size_t)c * 3 * NN;
-  F[m] = cadd(F[m], s1);
-  F[NN + m] = cadd(F[NN + m], s2);
-  F[2 * NN + m] = cadd(F[2 * NN + m], cadd(s3, cmul(sh, s2)));
+  for (int m = lane; m < NN; m += 32)
+    for (int d = 0; d < 3; ++d) F[d * NN + m] = cadd(F[d * NN + m], sm.a[d][m]);
 }
 
 // ---------------------------------------------------------------- L2P + W
@@ -471,7 +526,7 @@ int launch_bb_far(ddm_ctx_s* ctx, ddm_tree_s* t, int n, const double* D, int nco
 #define DDM_L(NT)                                                                               \
   do {                                                                                          \
     stage_begin(ctx, DDM_ST_P2M, s);                                                            \
-    bb_p2m_kernel<NT><<<nblk((int64_t)t->nleaves * NN, 128), 128, 0, s>>>(                      \
+    bb_p2m_kernel<NT><<<nblk(t->nleaves, 4), 128, 0, s>>>(                      \
         t->nleaves, t->leaves, t->c_level, t->c_ix, t->c_iy, t->c_start, t->c_count, cg, D,     \
         ncomp, t->ex, t->ey, t->ea, t->ec, t->es, gc, t->bb_w);                                 \
     stage_end(ctx, DDM_ST_P2M, s);                                                              \
@@ -479,7 +534,7 @@ int launch_bb_far(ddm_ctx_s* ctx, ddm_tree_s* t, int n, const double* D, int nco
     for (int lev = t->nlevels - 1; lev >= 2; --lev) {                                           \
       const int u0 = t->up_level_off[2 * lev], u1 = t->up_level_off[2 * lev + 1];               \
       if (u1 <= u0) continue;                                                                   \
-      bb_m2m_level_kernel<NT><<<nblk((int64_t)(u1 - u0) * NN, 128), 128, 0, s>>>(               \
+      bb_m2m_level_kernel<NT><<<nblk(u1 - u0, 4), 128, 0, s>>>(               \
           u0, u1, t->up_list, t->c_level, t->c_ix, t->c_iy, t->c_first_child, t->c_nchild, cg,  \
           t->bb_w);                                                                             \
     }                                                                                           \
@@ -495,7 +550,7 @@ int launch_bb_far(ddm_ctx_s* ctx, ddm_tree_s* t, int n, const double* D, int nco
       for (int lev = 3; lev < t->nlevels; ++lev) {                                              \
         const int a = t->level_off[lev], b = t->level_off[lev + 1];                             \
         if (b <= a) continue;                                                                   \
-        bb_l2l_level_kernel<NT><<<nblk((int64_t)(b - a) * NN, 128), 128, 0, s>>>(               \
+        bb_l2l_level_kernel<NT><<<nblk(b - a, 4), 128, 0, s>>>(               \
             a, b, lo, hi, t->c_level, t->c_ix, t->c_iy, t->c_start, t->c_count, t->c_parent,    \
             cg, t->bb_f);                                                                       \
       }                                                                                         \
