@@ -279,6 +279,9 @@ def run_ours(args):
            "clocks": clocks}
 
     if rank == 0 and world == 1 and not args.no_extras:
+        # the paper's own far field (Chebyshev bbFMM, NCheb3 / NCheb6) on the
+        # same tree and input
+        out["bbfmm"] = bbfmm_extra(D, ctx, torch, tree, mat, Dd, y, flush, cnt, fp64_peak)
         # GMRES solve time on config 2 (the metric's second half), at p and p*
         out["gmres"] = gmres_extra(D, ctx, torch, dev, args.march_steps)
         gv, gdt = cpu_baseline_oracle(g, c["material"], Dv_host, args.cpu_rows)
@@ -318,6 +321,55 @@ def _poro_rc(c, g, tau):
     M = 2 * G * (nuu - nu) / (al * al * (1 - 2 * nuu) * (1 - 2 * nu))
     S = al * al * (1 - 2 * nu) / (2 * G * (1 - nu)) + 1 / M
     return (160 * (kap / S) * tau) ** 0.5 + 2 * float(g.half_len.max())
+
+
+# fp64-pipe instructions per node pair of bb_m2l_kernel<6> (DFMA + DMUL + DADD
+# of the fully unrolled node loop / 36, cuobjdump -sass)
+BB_M2L_INSTR_PER_NODE_PAIR = 33
+
+
+def bbfmm_extra(D, ctx, torch, tree, mat, Dd, y, flush, cnt, fp64_peak, reps: int = 20):
+    """Matvec time of the bbFMM far field at n = 3 and 6 (the paper's NCheb3 /
+    NCheb6) on the bench workload: CUDA events around `reps`
+    matvecs (L2 flushed before each, outside the events), serial per-stage
+    times, the relative L2 difference from the p = 20 series matvec (whose own
+    error is ~1e-10), and the fp64-pipe fraction of the dominant kernel (M2L)."""
+    ref = torch.empty_like(Dd)
+    D.matvec(ctx, tree, mat, Dd, ref)
+    res = {}
+    for n in (3, 6):
+        mode = f"bbfmm{n}"
+        for _ in range(3):
+            D.matvec(ctx, tree, mat, Dd, y, mode=mode)
+        torch.cuda.synchronize()
+        tot = 0.0
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            D.matvec(ctx, tree, mat, Dd, y, mode=mode)
+            e1.record()
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        err = (torch.linalg.norm(y - ref) / torch.linalg.norm(ref)).item()
+        ctx.set_profiling(True, serial=True)
+        st = {}
+        for _ in range(3):
+            flush.zero_()
+            D.matvec(ctx, tree, mat, Dd, y, mode=mode)
+            torch.cuda.synchronize()
+            for k, v in ctx.stage_times().items():
+                st[k] = st.get(k, 0.0) + v / 3
+        ctx.set_profiling(False)
+        node_pairs = cnt["V"] * (n * n) ** 2
+        r = {"ms_per_matvec": tot / reps, "rel_diff_vs_series_p20": err,
+             "serial_stage_ms": {k: v for k, v in st.items() if v > 0},
+             "m2l_node_pairs": node_pairs}
+        if n == 6 and fp64_peak and st.get("m2l"):
+            r["m2l_fp64_pipe_frac"] = (node_pairs * BB_M2L_INSTR_PER_NODE_PAIR
+                                       / (st["m2l"] * 1e-3) / (fp64_peak * 1e12 / 2.0))
+        res[mode] = r
+    return res
 
 
 def gmres_extra(D, ctx, torch, dev, march_steps: int):

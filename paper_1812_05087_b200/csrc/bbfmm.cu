@@ -256,18 +256,26 @@ template <int N>
 __device__ __forceinline__ void node_sums(double2 u, const double2* __restrict__ Wb, double2& t1,
                                           double2& t3, double2& t2a, double2& t2b) {
   constexpr int NN = N * N;
-#pragma unroll 4
-  for (int mm = 0; mm < NN; ++mm) {
-    const double dx = u.x - c_bbX[N][mm / N], dy = u.y - c_bbX[N][mm % N];
-    const double r = fast_rcp(fma(dx, dx, dy * dy));
-    const double2 inv = make_double2(dx * r, -dy * r);
-    const double2 inv2 = make_double2(fma(inv.x, inv.x, -inv.y * inv.y), 2.0 * inv.x * inv.y);
-    const double2 inv3 = cmul(inv2, inv);
-    const double2 v1 = Wb[mm], v2 = Wb[NN + mm], v3 = Wb[2 * NN + mm];
-    cmac(t1, inv2, v1);
-    cmac(t3, inv3, v1);
-    cmac(t2a, inv2, v2);
-    cmac(t2b, inv3, v3);
+  double dyk[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) dyk[k] = u.y - c_bbX[N][k];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const double dx = u.x - c_bbX[N][i], dx2 = dx * dx;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int mm = i * N + k;
+      const double dy = dyk[k];
+      const double r = fast_rcp(fma(dy, dy, dx2));
+      const double2 inv = make_double2(dx * r, -dy * r);
+      const double2 inv2 = make_double2(fma(inv.x, inv.x, -inv.y * inv.y), 2.0 * inv.x * inv.y);
+      const double2 inv3 = cmul(inv2, inv);
+      const double2 v1 = Wb[mm], v2 = Wb[NN + mm], v3 = Wb[2 * NN + mm];
+      cmac(t1, inv2, v1);
+      cmac(t3, inv3, v1);
+      cmac(t2a, inv2, v2);
+      cmac(t2b, inv3, v3);
+    }
   }
 }
 
