@@ -58,6 +58,8 @@ typedef enum {
 enum { DDM_FMM = 0, DDM_DIRECT = 1,
        DDM_HIST_PERLAG = 2, /* ddm_history_apply only: one FMM matvec per lag (the paper's scheme) */
        DDM_GMRES_NO_PRECOND = 8, /* ddm_gmres_solve only, OR-ed into mode: plain GMRES */
+       DDM_GMRES_PC_POINT = 32,  /* ddm_gmres_solve only, OR-ed into mode: point-block
+                                    Jacobi (element self blocks) instead of leaf blocks */
        DDM_BBFMM = 16 /* ddm_matvec / ddm_gmres_solve, elastic: the paper's Chebyshev
                          (bbFMM) far field with n nodes per dimension, mode =
                          DDM_BBFMM_MODE(n), 2 <= n <= 8 */ };
@@ -188,15 +190,29 @@ int ddm_history_apply(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, d
 int ddm_history_rhs(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, double dt, int h,
                     const double* D_hist, const double* b, double* rhs, int mode, void* stream);
 
-/* GMRES (reading R11): solve A(dt) x = b with CGS2 Arnoldi,
- * Givens rotations, restart `restart`, relative tolerance tol on
- * ||b - A x|| / ||b|| (the true residual: right preconditioning).  The
- * operator is right-preconditioned by the inverse element self blocks
- * (block Jacobi, 2x2 elastic / 3x3 poroelastic) unless
- * DDM_GMRES_NO_PRECOND is OR-ed into mode (DDM_FMM or DDM_DIRECT).  b, x [device] [n][ncomp]; x holds the initial guess
+/* GMRES (reading R11): solve A(dt) x = b with classical
+ * Gram-Schmidt Arnoldi (second pass when the first cancels more than half of
+ * ||w||^2), Givens rotations, restart `restart`, relative tolerance tol on
+ * ||b - A x|| / ||b|| (the true residual: right preconditioning; a cycle
+ * whose estimate reaches tol is continued, not restarted, until the true
+ * residual does).  Preconditioner: by default leaf-block
+ * Jacobi -- the exact dense blocks of chunks of <= 32 consecutive elements
+ * of one leaf (the strongest couplings: neighbours on the same fracture),
+ * inverted once per material / dt; DDM_GMRES_PC_POINT OR-ed into mode: the
+ * element self blocks (2x2 elastic / 3x3 poroelastic); DDM_GMRES_NO_PRECOND:
+ * none.  The operator mode is DDM_FMM, DDM_DIRECT or DDM_BBFMM_MODE(n).
+ * b, x [device] [n][ncomp]; x holds the initial guess
  * on entry and the solution on return.  iters, rel_resid [host] outputs
  * (rel_resid = explicit true residual at exit).  b = 0 -> x = 0, iters = 0.
  * Returns DDM_ERR_NOCONV with x = last iterate if max_iter is reached. */
+/* y = M^-1 x, the GMRES preconditioner on its own: kind 1
+ * point-block Jacobi (inverse element self blocks), kind 2 leaf-block Jacobi
+ * (inverse dense blocks of <= 32 consecutive elements of one leaf; chunks as
+ * documented at ddm_gmres_solve).  x, y [device] [n][ncomp] user order.
+ * Errors: kind not 1/2, poroelastic with dt <= 0 -> DDM_ERR_ARG. */
+int ddm_precond_apply(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, double dt,
+                      const double* x, double* y, int kind, void* stream);
+
 int ddm_gmres_solve(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, double dt,
                     const double* b, double* x, double tol, int restart, int max_iter,
                     int mode, int* iters, double* rel_resid, void* stream);

@@ -19,6 +19,7 @@ from .api import (  # noqa: F401
     material_from_dict,
     matvec,
     nccl_unique_id,
+    precond_apply,
     sif,
     split_costs,
 )

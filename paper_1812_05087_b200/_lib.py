@@ -22,6 +22,7 @@ lib = C.CDLL(LIB_PATH)
 OK, ERR_ARG, ERR_CUDA, ERR_NOCONV, ERR_NCCL, ERR_GEOM, ERR_OOM = range(7)
 FMM, DIRECT, HIST_PERLAG = 0, 1, 2
 GMRES_NO_PRECOND = 8
+GMRES_PC_POINT = 32   # point-block Jacobi instead of the default leaf blocks
 BBFMM = 16   # | n << 8: Chebyshev (bbFMM) far field with n nodes per dimension
 
 TC = dict(N=0, CELLS=1, LEAVES=2, LEVELS=3, V=4, URANGES=5, NEAR_PAIRS=6, P2P_ITEMS=7,
@@ -71,6 +72,8 @@ ddm_history_rhs = _proto("ddm_history_rhs", _i, _vp, _vp, C.POINTER(Material), _
                          _dp, _i, _vp)
 ddm_gmres_solve = _proto("ddm_gmres_solve", _i, _vp, _vp, C.POINTER(Material), _d, _dp, _dp, _d,
                          _i, _i, _i, C.POINTER(_i), C.POINTER(_d), _vp)
+ddm_precond_apply = _proto("ddm_precond_apply", _i, _vp, _vp, C.POINTER(Material), _d, _dp, _dp,
+                           _i, _vp)
 ddm_farfield_rhs = _proto("ddm_farfield_rhs", _i, _vp, _dp, _i64, _i, _d, _d, _d, _i, _d, _dp,
                           _vp)
 ddm_sif = _proto("ddm_sif", _i, _vp, _dp, _dp, _dp, _i, _d, _d, _dp, _dp, _vp)
@@ -80,5 +83,6 @@ ddm_stage_times = _proto("ddm_stage_times", _i, _vp, C.POINTER(_d))
 EXPORTED = ["ddm_version", "ddm_last_error", "ddm_nccl_unique_id", "ddm_ctx_create",
             "ddm_ctx_destroy", "ddm_build_tree", "ddm_tree_free", "ddm_tree_counts",
             "ddm_tree_export", "ddm_tree_partition", "ddm_split_costs", "ddm_matvec",
-            "ddm_history_apply", "ddm_history_rhs", "ddm_gmres_solve", "ddm_farfield_rhs", "ddm_sif",
+            "ddm_history_apply", "ddm_history_rhs", "ddm_gmres_solve", "ddm_precond_apply",
+            "ddm_farfield_rhs", "ddm_sif",
             "ddm_set_profiling", "ddm_stage_times"]

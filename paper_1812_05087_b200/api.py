@@ -201,18 +201,42 @@ def history_rhs(ctx, tree, mat, dt: float, D_hist: torch.Tensor, b: torch.Tensor
     return rhs
 
 
+def _pc_flags(precond) -> int:
+    if precond is None or precond is False:
+        return L.GMRES_NO_PRECOND
+    if precond is True or precond == "leaf":
+        return 0
+    if precond == "point":
+        return L.GMRES_PC_POINT
+    raise ValueError(f"precond must be 'leaf', 'point' or False, not {precond!r}")
+
+
+def precond_apply(ctx, tree, mat, x: torch.Tensor, y: torch.Tensor | None = None, dt: float = 0.0,
+                  kind="leaf", stream=None) -> torch.Tensor:
+    """ddm_precond_apply: y = M^-1 x for the GMRES preconditioner ("leaf" or
+    "point" block Jacobi), user order."""
+    if y is None:
+        y = torch.empty_like(x)
+    ctx.check(L.ddm_precond_apply(ctx._h, tree._h, C.byref(mat), float(dt), _dev(x, "x"),
+                                  _dev(y, "y"), {"point": 1, "leaf": 2}[kind],
+                                  _stream_ptr(stream)))
+    return y
+
+
 def gmres_solve(ctx, tree, mat, b: torch.Tensor, x: torch.Tensor | None = None, dt: float = 0.0,
                 tol: float = 1e-10, restart: int = 2000, max_iter: int = 10000, mode="fmm",
-                stream=None, raise_noconv: bool = True, precond: bool = True):
-    """ddm_gmres_solve: returns (x, iters, rel_resid).  precond: block-Jacobi
-    right preconditioning (inverse element self blocks); False = plain GMRES."""
+                stream=None, raise_noconv: bool = True, precond="leaf"):
+    """ddm_gmres_solve: returns (x, iters, rel_resid).  precond: right
+    preconditioning by block Jacobi -- "leaf" (or True, default): inverse dense
+    blocks of <= 32 consecutive elements of one leaf; "point": inverse element
+    self blocks; False / None: plain GMRES."""
     if x is None:
         x = torch.zeros_like(b)
     it = C.c_int(0)
     rr = C.c_double(0.0)
     rc = L.ddm_gmres_solve(ctx._h, tree._h, C.byref(mat), float(dt), _dev(b, "b"), _dev(x, "x"),
                            float(tol), int(restart), int(max_iter),
-                           _mode(mode) | (0 if precond else L.GMRES_NO_PRECOND), C.byref(it),
+                           _mode(mode) | _pc_flags(precond), C.byref(it),
                            C.byref(rr), _stream_ptr(stream))
     if rc == L.ERR_NOCONV and not raise_noconv:
         return x, it.value, rr.value

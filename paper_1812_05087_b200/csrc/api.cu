@@ -529,6 +529,16 @@ int ddm_history_rhs(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double
   return rc;
 }
 
+int ddm_precond_apply(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double dt,
+                      const double* x, double* y, int kind, void* stream) {
+  if (!ctx || !t || !x || !y) return ctx ? set_error(ctx, DDM_ERR_ARG, "NULL argument") : DDM_ERR_ARG;
+  int rc = check_material(ctx, mat);
+  if (rc) return rc;
+  if (kind != 1 && kind != 2) return set_error(ctx, DDM_ERR_ARG, "kind must be 1 or 2");
+  if (mat->kind == 1 && !(dt > 0)) return set_error(ctx, DDM_ERR_ARG, "poroelastic needs dt > 0");
+  return precond_apply_user(ctx, t, mat, dt, kind, x, y, (cudaStream_t)stream);
+}
+
 int ddm_gmres_solve(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double dt,
                     const double* b, double* x, double tol, int restart, int max_iter, int mode,
                     int* iters, double* rel_resid, void* stream) {

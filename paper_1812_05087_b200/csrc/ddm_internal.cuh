@@ -26,6 +26,7 @@ constexpr int kTgtGroup = DDM_TGT_GROUP;   // targets per P2P work item (one war
 #endif
 constexpr int kSrcChunk = DDM_SRC_CHUNK;  // max sources per P2P work item
 constexpr int kSrcStride = 12;  // doubles per P2P source record
+constexpr int kPcChunk = 32;    // max elements per leaf-block preconditioner block
 
 struct Status {
   int code = DDM_OK;
@@ -185,6 +186,15 @@ struct ddm_tree_s {
   // (sorted order) for the material / elapsed time in pc_key
   double* pc = nullptr;
   double pc_key[8] = {};
+  // leaf-block Jacobi (default GMRES preconditioner): chunks of <= kPcChunk
+  // consecutive sorted elements of one leaf, inverse blocks column-major
+  int2* pc_chunks = nullptr;      // [pc_nchunks] (first sorted element, count)
+  int64_t* pc_off = nullptr;      // [pc_nchunks] block offsets (doubles), for ncomp = pc_off_ncomp
+  int pc_nchunks = 0, pc_off_ncomp = 0;
+  int pc_q_lo = 0, pc_q_hi = 0;   // chunks of the owned elements
+  double* pcl = nullptr;
+  int64_t pcl_n = 0;
+  double pcl_key[8] = {};
   // GMRES workspace
   double* krylov = nullptr;
   int krylov_m = 0;
@@ -258,6 +268,10 @@ int launch_bb_far(ddm_ctx_s* ctx, ddm_tree_s* t, int n, const double* D, int nco
 int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt,
                 const double* b, double* x, double tol, int restart, int max_iter, int mode,
                 int* iters, double* rel_resid, cudaStream_t s);
+
+// y = M^-1 x (user order): kind 1 point-block, 2 leaf-block Jacobi
+int precond_apply_user(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt,
+                       int kind, const double* x_user, double* y_user, cudaStream_t s);
 
 // comm (api.cu)
 int allgather_sorted(ddm_ctx_s* ctx, ddm_tree_s* t, double* buf, int ncomp, cudaStream_t s);

@@ -1,15 +1,21 @@
 // GMRES with the FMM operator (DESIGN.md §4.1 row a12, §4.7; "a modified
 // version of GMRES with FMM for matrix-vector multiplication"; reading R11):
-// restarted GMRES, Arnoldi by classical Gram-Schmidt applied twice (CGS2),
+// restarted GMRES, Arnoldi by classical Gram-Schmidt with selective
+// reorthogonalisation (a second CGS pass when the first cancelled more than
+// half of ||w||^2: Daniel-Gragg-Kaufman-Stewart criterion),
 // Givens rotations, relative residual ||b - A x|| / ||b|| <= tol.
 //
 // Vectors live in Morton-sorted order; each rank keeps its owned rows
 // [own_el_lo, own_el_hi) of every Krylov vector.  Per iteration: one all-gather
-// of the new basis vector (multi-GPU only), the matvec, two batched dot passes
-// (each one all-reduce of k+1 partial dots) and one norm.  The small Hessenberg
+// of the new basis vector (multi-GPU only), the matvec, one batched dot pass
+// (one all-reduce of k+1 partial dots) and two norms, plus a second dot pass
+// when reorthogonalisation is needed.  The small Hessenberg
 // least-squares problem is solved on the host.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -155,6 +161,121 @@ __global__ void block_apply(int64_t e0, int64_t e1, int ncomp, const double* __r
   for (int r = 0; r < ncomp; ++r) out[e * ncomp + r] = add ? out[e * ncomp + r] + o[r] : o[r];
 }
 
+// In place: the chunk's dense block (row-major, d = ncomp * count) becomes
+// its inverse, stored column-major (coalesced rows in chunk_apply).  Rows are
+// equilibrated first (the poroelastic rows mix tractions and pressures of
+// very different scale), then Gauss-Jordan with partial pivoting in shared
+// memory: A^-1 = (R A)^-1 R.  A singular block becomes the identity.
+__global__ void __launch_bounds__(256)
+chunk_invert(const int2* __restrict__ chunks, const int64_t* __restrict__ off, int ncomp,
+             double* __restrict__ blk) {
+  extern __shared__ double sm[];
+  const int d = ncomp * chunks[blockIdx.x].y;
+  double* A = sm;
+  double* rs = A + d * d;
+  double* colk = rs + d;
+  __shared__ int piv[kPcChunk * 3];
+  __shared__ int singular;
+  double* B = blk + off[blockIdx.x];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int f = tid; f < d * d; f += nt) A[f] = B[f];
+  if (tid == 0) singular = 0;
+  __syncthreads();
+  for (int r = tid; r < d; r += nt) {
+    double mx = 0.0;
+    for (int j = 0; j < d; ++j) mx = fmax(mx, fabs(A[r * d + j]));
+    const double sc = mx > 0.0 ? 1.0 / mx : 1.0;
+    rs[r] = sc;
+    for (int j = 0; j < d; ++j) A[r * d + j] *= sc;
+  }
+  __syncthreads();
+  for (int k = 0; k < d; ++k) {
+    if (tid < 32) {   // pivot: argmax_{i >= k} |A[i][k]| (lowest index on ties)
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + tid; i < d; i += 32) {
+        const double v = fabs(A[i * d + k]);
+        if (v > best) { best = v; bi = i; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tid == 0) {
+        piv[k] = bi;
+        if (!(best > 0.0)) singular = 1;
+      }
+    }
+    __syncthreads();
+    if (singular) break;
+    const int p = piv[k];
+    if (p != k)
+      for (int j = tid; j < d; j += nt) {
+        const double t = A[k * d + j];
+        A[k * d + j] = A[p * d + j];
+        A[p * d + j] = t;
+      }
+    __syncthreads();
+    const double ip = 1.0 / A[k * d + k];
+    for (int i = tid; i < d; i += nt) colk[i] = A[i * d + k];
+    __syncthreads();
+    for (int j = tid; j < d; j += nt) A[k * d + j] = (j == k ? 1.0 : A[k * d + j]) * ip;
+    __syncthreads();
+    for (int f = tid; f < d * d; f += nt) {
+      const int i = f / d, j = f % d;
+      if (i == k) continue;
+      A[f] = (j == k ? 0.0 : A[f]) - colk[i] * A[k * d + j];
+    }
+    __syncthreads();
+  }
+  if (singular) {
+    for (int f = tid; f < d * d; f += nt) B[f] = (f / d == f % d) ? 1.0 : 0.0;
+    return;
+  }
+  for (int k = d - 1; k >= 0; --k) {   // undo the row interchanges as column swaps
+    const int p = piv[k];
+    if (p != k)
+      for (int i = tid; i < d; i += nt) {
+        const double t = A[i * d + k];
+        A[i * d + k] = A[i * d + p];
+        A[i * d + p] = t;
+      }
+    __syncthreads();
+  }
+  // (R A)^-1 R: column c scaled by rs[c]; stored column-major
+  for (int f = tid; f < d * d; f += nt) {
+    const int c = f / d, r = f % d;
+    B[f] = A[r * d + c] * rs[c];
+  }
+}
+
+// y (+)= blockdiag(inv) x over the chunks [q0, q0 + gridDim.x) (sorted order)
+__global__ void __launch_bounds__(128)
+chunk_apply(const int2* __restrict__ chunks, const int64_t* __restrict__ off, int q0, int ncomp,
+            const double* __restrict__ inv, const double* __restrict__ x, double* __restrict__ y,
+            int add) {
+  __shared__ double xs[kPcChunk * 3];
+  const int q = q0 + blockIdx.x;
+  const int2 ch = chunks[q];
+  const int d = ncomp * ch.y;
+  const int64_t b0 = (int64_t)ch.x * ncomp;
+  const double* Ai = inv + off[q];
+  for (int t = threadIdx.x; t < d; t += blockDim.x) xs[t] = x[b0 + t];
+  __syncthreads();
+  for (int r = threadIdx.x; r < d; r += blockDim.x) {
+    double a0 = 0.0, a1 = 0.0;
+    int c = 0;
+    for (; c + 1 < d; c += 2) {
+      a0 = fma(Ai[(size_t)c * d + r], xs[c], a0);
+      a1 = fma(Ai[(size_t)(c + 1) * d + r], xs[c + 1], a1);
+    }
+    if (c < d) a0 = fma(Ai[(size_t)c * d + r], xs[c], a0);
+    const double v = a0 + a1;
+    y[b0 + r] = add ? y[b0 + r] + v : v;
+  }
+}
+
 struct Gm {
   ddm_ctx_s* ctx;
   ddm_tree_s* t;
@@ -188,12 +309,146 @@ struct Gm {
 
 }  // namespace
 
+// Chunks of the leaf-block preconditioner: each leaf's sorted element range
+// split into ceil(count / kPcChunk) near-equal consecutive chunks; block
+// offsets for ncomp components.  Owned chunks: [pc_q_lo, pc_q_hi).
+static int pc_build_chunks(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, cudaStream_t s) {
+  if (t->pc_chunks && t->pc_off_ncomp == ncomp) return DDM_OK;
+  std::vector<int> leaves(t->nleaves), start(t->ncells), count(t->ncells);
+  DDM_CUDA(ctx, cudaMemcpyAsync(leaves.data(), t->leaves, t->nleaves * sizeof(int),
+                                cudaMemcpyDeviceToHost, s));
+  DDM_CUDA(ctx, cudaMemcpyAsync(start.data(), t->c_start, t->ncells * sizeof(int),
+                                cudaMemcpyDeviceToHost, s));
+  DDM_CUDA(ctx, cudaMemcpyAsync(count.data(), t->c_count, t->ncells * sizeof(int),
+                                cudaMemcpyDeviceToHost, s));
+  DDM_CUDA(ctx, cudaStreamSynchronize(s));
+  std::vector<std::pair<int, int>> lr;
+  for (int c : leaves) lr.push_back({start[c], count[c]});
+  std::sort(lr.begin(), lr.end());
+  std::vector<int2> ch;
+  std::vector<int64_t> off;
+  int64_t tot = 0;
+  t->pc_q_lo = -1;
+  t->pc_q_hi = 0;
+  for (const auto& l : lr) {
+    const int nc = (l.second + kPcChunk - 1) / kPcChunk;
+    for (int q = 0; q < nc; ++q) {
+      const int a = l.first + (int)((int64_t)l.second * q / nc);
+      const int b = l.first + (int)((int64_t)l.second * (q + 1) / nc);
+      if (a >= t->own_el_lo && a < t->own_el_hi) {
+        if (t->pc_q_lo < 0) t->pc_q_lo = (int)ch.size();
+        t->pc_q_hi = (int)ch.size() + 1;
+      }
+      ch.push_back(make_int2(a, b - a));
+      off.push_back(tot);
+      tot += (int64_t)(ncomp * (b - a)) * (ncomp * (b - a));
+    }
+  }
+  if (t->pc_q_lo < 0) t->pc_q_lo = t->pc_q_hi = 0;
+  if (t->pc_chunks) cudaFree(t->pc_chunks);
+  if (t->pc_off) cudaFree(t->pc_off);
+  if (t->pcl) cudaFree(t->pcl);
+  t->pc_chunks = nullptr;
+  t->pc_off = nullptr;
+  t->pcl = nullptr;
+  int rc;
+  if ((rc = dalloc(ctx, &t->pc_chunks, ch.size())) || (rc = dalloc(ctx, &t->pc_off, off.size())) ||
+      (rc = dalloc(ctx, &t->pcl, (size_t)tot)))
+    return rc;
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->pc_chunks, ch.data(), ch.size() * sizeof(int2),
+                                cudaMemcpyHostToDevice, s));
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->pc_off, off.data(), off.size() * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, s));
+  DDM_CUDA(ctx, cudaStreamSynchronize(s));
+  t->pc_nchunks = (int)ch.size();
+  t->pc_off_ncomp = ncomp;
+  t->pcl_n = tot;
+  std::memset(t->pcl_key, 0, sizeof(t->pcl_key));
+  return DDM_OK;
+}
+
+// leaf-block inverses for this material / dt (cached on the tree)
+static int pc_leaf_blocks(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt,
+                          cudaStream_t s) {
+  const int ncomp = mat->kind == 1 ? 3 : 2;
+  int rc = pc_build_chunks(ctx, t, ncomp, s);
+  if (rc) return rc;
+  const double key[8] = {(double)mat->kind, mat->G, mat->nu, mat->nu_u, mat->alpha, mat->kappa,
+                         mat->kind == 1 ? dt : 0.0, 2.0};
+  if (std::memcmp(key, t->pcl_key, sizeof(key)) == 0) return DDM_OK;
+  if (mat->kind == 1) {
+    if (!(dt > 0)) return set_error(ctx, DDM_ERR_ARG, "poroelastic GMRES needs dt > 0");
+    rc = launch_poro_chunk_blocks(ctx, t, poro_params(mat, dt), t->pc_nchunks, t->pc_chunks,
+                                  t->pc_off, t->pcl, s);
+  } else {
+    rc = launch_elastic_chunk_blocks(ctx, t, mat->G / (4.0 * M_PI * (1.0 - mat->nu)),
+                                     t->pc_nchunks, t->pc_chunks, t->pc_off, t->pcl, s);
+  }
+  if (rc) return rc;
+  const int dmax = ncomp * kPcChunk;
+  const size_t shm = ((size_t)dmax * dmax + 2 * dmax) * sizeof(double);
+  DDM_CUDA(ctx, cudaFuncSetAttribute(chunk_invert, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)shm));
+  chunk_invert<<<t->pc_nchunks, 256, shm, s>>>(t->pc_chunks, t->pc_off, ncomp, t->pcl);
+  DDM_CUDA(ctx, cudaGetLastError());
+  std::memcpy(t->pcl_key, key, sizeof(key));
+  return DDM_OK;
+}
+
+int precond_apply(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt, int kind,
+                  const double* x_sorted, double* y_sorted, cudaStream_t s) {
+  const int ncomp = mat->kind == 1 ? 3 : 2;
+  int rc;
+  if (kind == 1) {
+    const double key[8] = {(double)mat->kind, mat->G, mat->nu, mat->nu_u, mat->alpha, mat->kappa,
+                           mat->kind == 1 ? dt : 0.0, 1.0};
+    if (!t->pc || std::memcmp(key, t->pc_key, sizeof(key)) != 0) {
+      if (!t->pc && (rc = dalloc(ctx, &t->pc, (size_t)t->n * 9))) return rc;
+      rc = mat->kind == 1
+               ? launch_poro_self_blocks(ctx, t, poro_params(mat, dt), t->pc, s)
+               : launch_elastic_self_blocks(ctx, t, mat->G / (4.0 * M_PI * (1.0 - mat->nu)), t->pc, s);
+      if (rc) return rc;
+      invert_blocks<<<nblk(t->n, 256), 256, 0, s>>>(t->n, ncomp, t->pc);
+      DDM_CUDA(ctx, cudaGetLastError());
+      std::memcpy(t->pc_key, key, sizeof(key));
+    }
+    block_apply<<<nblk(t->n, 256), 256, 0, s>>>(0, t->n, ncomp, t->pc, x_sorted, y_sorted, 0);
+  } else {
+    if ((rc = pc_leaf_blocks(ctx, t, mat, dt, s))) return rc;
+    chunk_apply<<<t->pc_nchunks, 128, 0, s>>>(t->pc_chunks, t->pc_off, 0, ncomp, t->pcl, x_sorted,
+                                              y_sorted, 0);
+  }
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+// y = M^-1 x in user order (ddm_precond_apply)
+int precond_apply_user(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt,
+                       int kind, const double* x_user, double* y_user, cudaStream_t s) {
+  const int ncomp = mat->kind == 1 ? 3 : 2;
+  const int64_t n = t->n;
+  double *xs = nullptr, *ys = nullptr;
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&xs, (size_t)n * ncomp * sizeof(double), s));
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&ys, (size_t)n * ncomp * sizeof(double), s));
+  gather_sorted<<<nblk(n, 256), 256, 0, s>>>(n, ncomp, t->perm, x_user, xs);
+  int rc = precond_apply(ctx, t, mat, dt, kind, xs, ys, s);
+  if (!rc) {
+    scatter_to_user<<<nblk(n, 256), 256, 0, s>>>(n, ncomp, t->perm, ys, y_user);
+    rc = cuda_error_if(ctx, cudaGetLastError(), "scatter_to_user");
+  }
+  cudaFreeAsync(xs, s);
+  cudaFreeAsync(ys, s);
+  if (!rc) rc = cuda_error_if(ctx, cudaStreamSynchronize(s), "precond_apply");
+  return rc;
+}
+
 int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt,
                 const double* b_user, double* x_user, double tol, int restart, int max_iter,
                 int mode, int* iters_out, double* rel_out, cudaStream_t s) {
   const int ncomp = mat->kind == 1 ? 3 : 2;
   const bool use_pc = !(mode & DDM_GMRES_NO_PRECOND);
-  mode &= ~DDM_GMRES_NO_PRECOND;
+  const bool pc_point = (mode & DDM_GMRES_PC_POINT) != 0;
+  mode &= ~(DDM_GMRES_NO_PRECOND | DDM_GMRES_PC_POINT);
   const int64_t n = t->n;
   const int64_t nfull = n * ncomp;
   const int64_t lo = t->own_el_lo * ncomp;
@@ -210,27 +465,11 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
     t->krylov_dof = nloc;
   }
   if (!t->gm_w) {
-    // gm_w: 5 full vectors (b, x, v, w, u); gm_tmp: h buffer
-    if ((rc = dalloc(ctx, &t->gm_w, (size_t)5 * 3 * n))) return rc;
+    // gm_w: 6 full vectors (b, x, v, w, u, trial x); gm_tmp: h buffer
+    if ((rc = dalloc(ctx, &t->gm_w, (size_t)6 * 3 * n))) return rc;
   }
-  if (use_pc) {
-    // block-Jacobi: inverse self blocks for this material and elapsed time
-    const double key[8] = {(double)mat->kind, mat->G, mat->nu, mat->nu_u, mat->alpha, mat->kappa,
-                           mat->kind == 1 ? dt : 0.0, 1.0};
-    if (!t->pc || std::memcmp(key, t->pc_key, sizeof(key)) != 0) {
-      if (!t->pc && (rc = dalloc(ctx, &t->pc, (size_t)n * 9))) return rc;
-      if (mat->kind == 1) {
-        if (!(dt > 0)) return set_error(ctx, DDM_ERR_ARG, "poroelastic GMRES needs dt > 0");
-        rc = launch_poro_self_blocks(ctx, t, poro_params(mat, dt), t->pc, s);
-      } else {
-        rc = launch_elastic_self_blocks(ctx, t, mat->G / (4.0 * M_PI * (1.0 - mat->nu)), t->pc, s);
-      }
-      if (rc) return rc;
-      invert_blocks<<<nblk(n, 256), 256, 0, s>>>(n, ncomp, t->pc);
-      DDM_CUDA(ctx, cudaGetLastError());
-      std::memcpy(t->pc_key, key, sizeof(key));
-    }
-  }
+  if (use_pc && mat->kind == 1 && !(dt > 0))
+    return set_error(ctx, DDM_ERR_ARG, "poroelastic GMRES needs dt > 0");
   const int64_t part_need = (int64_t)(m + 2) * 256;
   if (t->gm_part_n < part_need) {
     if (t->gm_part) cudaFree(t->gm_part);
@@ -244,6 +483,7 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   double* vf = t->gm_w + 2 * nfull;
   double* wf = t->gm_w + 3 * nfull;
   double* uf = t->gm_w + 4 * nfull;   // preconditioned operand M^-1 v (full) / update V y
+  double* xt = t->gm_w + 5 * nfull;   // trial iterate (true-residual check)
   double* V = t->krylov;
   Gm g{ctx, t, s, ncomp, nloc, lo, t->gm_part, t->gm_part_n, t->gm_tmp};
 
@@ -254,8 +494,8 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   // operator: A M^-1 (right preconditioning) or A
   auto apply = [&](const double* vfull) -> int {
     if (!use_pc) return fmm_matvec(ctx, t, mat, dt, vfull, true, nullptr, wf, mode, s);
-    block_apply<<<nblk(n, 256), 256, 0, s>>>(0, n, ncomp, t->pc, vfull, uf, 0);
-    DDM_CUDA(ctx, cudaGetLastError());
+    int rc2 = precond_apply(ctx, t, mat, dt, pc_point ? 1 : 2, vfull, uf, s);
+    if (rc2) return rc2;
     return fmm_matvec(ctx, t, mat, dt, uf, true, nullptr, wf, mode, s);
   };
   // r = b - A x uses A itself (x is in the unpreconditioned space)
@@ -280,8 +520,64 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   }
   int iters = 0;
   bool converged = false;
-  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), gv(m + 1), y(m);
+  // Hessenberg matrix, packed by columns: H(i, k) = Hp[k (k + 3) / 2 + i], i <= k + 1.
+  // Column k is touched only at step k (contiguous, grows with the basis):
+  // a dense (m+1) x m row-major array made every step walk k rows m apart,
+  // which costs TLB misses proportional to the restart length, not to k.
+  std::vector<double> Hp, cs(m), sn(m), gv(m + 1), y(m);
+  auto H = [&Hp](int i, int k) -> double& { return Hp[(size_t)k * (k + 3) / 2 + i]; };
   double rel = 0.0;
+  static const bool trace = [] {
+    const char* e = getenv("DDM_GMRES_TRACE");
+    return e && e[0] == '1';
+  }();
+  auto now_ms = [] {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t_start = now_ms();
+  // DDM_GMRES_CGS2=1: reorthogonalise every step (plain CGS2)
+  static const bool always_cgs2 = [] {
+    const char* e = getenv("DDM_GMRES_CGS2");
+    return e && e[0] == '1';
+  }();
+  int n_reorth = 0;
+  static const double eta2 = [] {
+    const char* e = getenv("DDM_GMRES_ETA2");
+    return e ? atof(e) : 0.5;
+  }();
+  bool accepted = false;
+  // dst (full) = x + M^-1 V y (or x + V y), y = H^-1 g over the first kd
+  // columns (upper triangular, by columns; gv itself is left intact)
+  std::vector<double> gtmp(m + 1);
+  auto form_x = [&](int kd, double* dst) -> int {
+    for (int i = 0; i < kd; ++i) gtmp[i] = gv[i];
+    for (int j = kd - 1; j >= 0; --j) {
+      y[j] = gtmp[j] / H(j, j);
+      for (int i = 0; i < j; ++i) gtmp[i] -= H(i, j) * y[j];
+    }
+    DDM_CUDA(ctx, cudaMemcpyAsync(g.dh, y.data(), kd * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (dst != xs)
+      DDM_CUDA(ctx, cudaMemcpyAsync(dst, xs, nfull * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    int rc2;
+    if (use_pc) {
+      DDM_CUDA(ctx, cudaMemsetAsync(uf + lo, 0, nloc * sizeof(double), s));
+      if ((rc2 = g.axpy(V, nloc, kd, g.dh, 1.0, uf + lo))) return rc2;
+      if (pc_point) {
+        block_apply<<<nblk(t->own_el_hi - t->own_el_lo, 256), 256, 0, s>>>(
+            t->own_el_lo, t->own_el_hi, ncomp, t->pc, uf, dst, 1);
+      } else if (t->pc_q_hi > t->pc_q_lo) {
+        chunk_apply<<<t->pc_q_hi - t->pc_q_lo, 128, 0, s>>>(t->pc_chunks, t->pc_off, t->pc_q_lo,
+                                                            ncomp, t->pcl, uf, dst, 1);
+      }
+      DDM_CUDA(ctx, cudaGetLastError());
+    } else if ((rc2 = g.axpy(V, nloc, kd, g.dh, 1.0, dst + lo))) {
+      return rc2;
+    }
+    if (ctx->world > 1 && (rc2 = allgather_sorted(ctx, t, dst, ncomp, s))) return rc2;
+    DDM_CUDA(ctx, cudaStreamSynchronize(s));   // y (host) must stay alive until the copy ran
+    return DDM_OK;
+  };
   for (;;) {
     // r = b - A x
     if ((rc = apply_plain(xs))) return rc;
@@ -290,12 +586,15 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
     if ((rc = g.dots(V, 0, 1, V, 0)) || (rc = fetch(1))) return rc;
     const double beta = std::sqrt(hh[0]);
     rel = beta / bnorm;
+    if (trace)
+      fprintf(stderr, "[gmres] iters %d true rel %.3e at %.1f ms, %d reorthogonalised\n", iters,
+              rel, now_ms() - t_start, n_reorth);
     if (beta <= tol * bnorm) { converged = true; break; }
     if (iters >= max_iter) break;
     scale_copy<<<nblk(nloc, 256), 256, 0, s>>>(V, 1.0 / beta, V, nloc);
     DDM_CUDA(ctx, cudaGetLastError());
-    std::fill(H.begin(), H.end(), 0.0);
     std::fill(gv.begin(), gv.end(), 0.0);
+    double inner = tol;   // estimate target (relative), tightened when the true residual lags
     gv[0] = beta;
     int kdone = 0;
     for (int k = 0; k < m; ++k) {
@@ -308,55 +607,75 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
       }
       if ((rc = apply(vin))) return rc;
       double* w = wf + lo;
-      // CGS2: two classical Gram-Schmidt passes
+      // classical Gram-Schmidt with selective reorthogonalisation (DGKS,
+      // eta = 1/sqrt(2)): one pass h = V^T w, w -= V h; a second pass only
+      // when it cancelled most of w (||w'|| < eta ||w||), where a single
+      // pass loses orthogonality.  dh layout: [h1 (k+1) | h2 (k+1) | ||w||^2 | ||w'||^2]
+      const int o_w0 = 2 * (k + 1), o_w1 = o_w0 + 1;
       if ((rc = g.dots(V, nloc, k + 1, w, 0))) return rc;
+      if ((rc = g.dots(w, 0, 1, w, o_w0))) return rc;
       if ((rc = g.axpy(V, nloc, k + 1, g.dh, -1.0, w))) return rc;
-      if ((rc = g.dots(V, nloc, k + 1, w, k + 1))) return rc;
-      if ((rc = g.axpy(V, nloc, k + 1, g.dh + k + 1, -1.0, w))) return rc;
-      if ((rc = g.dots(w, 0, 1, w, 2 * (k + 1)))) return rc;
-      if ((rc = fetch(2 * (k + 1) + 1))) return rc;
-      const double hn = std::sqrt(hh[2 * (k + 1)]);
-      for (int i = 0; i <= k; ++i) H[(size_t)i * m + k] = hh[i] + hh[k + 1 + i];
-      H[(size_t)(k + 1) * m + k] = hn;
+      if ((rc = g.dots(w, 0, 1, w, o_w1))) return rc;
+      if ((rc = fetch(o_w1 + 1))) return rc;
+      bool reorth = !(hh[o_w1] >= eta2 * hh[o_w0]) || always_cgs2;
+      if (reorth) {
+        if ((rc = g.dots(V, nloc, k + 1, w, k + 1))) return rc;
+        if ((rc = g.axpy(V, nloc, k + 1, g.dh + k + 1, -1.0, w))) return rc;
+        if ((rc = g.dots(w, 0, 1, w, o_w1))) return rc;
+        if ((rc = fetch(o_w1 + 1))) return rc;
+        ++n_reorth;
+      }
+      const double hn = std::sqrt(hh[o_w1]);
+      if (Hp.size() < (size_t)(k + 1) * (k + 4) / 2) Hp.resize((size_t)(k + 1) * (k + 4) / 2);
+      for (int i = 0; i <= k; ++i) H(i, k) = hh[i] + (reorth ? hh[k + 1 + i] : 0.0);
+      H(k + 1, k) = hn;
       if (hn > 0.0) {
         scale_copy<<<nblk(nloc, 256), 256, 0, s>>>(w, 1.0 / hn, V + (int64_t)(k + 1) * nloc, nloc);
         DDM_CUDA(ctx, cudaGetLastError());
       }
       for (int i = 0; i < k; ++i) {
-        const double a = H[(size_t)i * m + k], bb = H[(size_t)(i + 1) * m + k];
-        H[(size_t)i * m + k] = cs[i] * a + sn[i] * bb;
-        H[(size_t)(i + 1) * m + k] = -sn[i] * a + cs[i] * bb;
+        const double a = H(i, k), bb = H(i + 1, k);
+        H(i, k) = cs[i] * a + sn[i] * bb;
+        H(i + 1, k) = -sn[i] * a + cs[i] * bb;
       }
-      const double a = H[(size_t)k * m + k], bb = H[(size_t)(k + 1) * m + k];
+      const double a = H(k, k), bb = H(k + 1, k);
       const double den = std::hypot(a, bb);
       cs[k] = a / den;
       sn[k] = bb / den;
-      H[(size_t)k * m + k] = den;
-      H[(size_t)(k + 1) * m + k] = 0.0;
+      H(k, k) = den;
+      H(k + 1, k) = 0.0;
       gv[k + 1] = -sn[k] * gv[k];
       gv[k] = cs[k] * gv[k];
       ++iters;
       kdone = k + 1;
-      if (std::fabs(gv[k + 1]) <= tol * bnorm || iters >= max_iter || hn == 0.0) break;
+      const bool est_ok = std::fabs(gv[k + 1]) <= inner * bnorm;
+      if (est_ok && kdone < m && iters < max_iter && hn != 0.0) {
+        // the estimate says converged: check the true residual of the
+        // iterate without ending the cycle.  Near the operator's accuracy
+        // floor the two differ; a restart here would rebuild the Krylov
+        // space from one vector and crawl (one step per cycle).
+        if ((rc = form_x(kdone, xt))) return rc;
+        if ((rc = apply_plain(xt))) return rc;
+        sub_scale<<<nblk(nloc, 256), 256, 0, s>>>(bs + lo, wf + lo, uf + lo, nloc);
+        DDM_CUDA(ctx, cudaGetLastError());
+        if ((rc = g.dots(uf + lo, 0, 1, uf + lo, 0)) || (rc = fetch(1))) return rc;
+        const double tr = std::sqrt(hh[0]);
+        if (trace)
+          fprintf(stderr, "[gmres] iters %d estimate %.3e true %.3e\n", iters,
+                  std::fabs(gv[k + 1]) / bnorm, tr / bnorm);
+        if (tr <= tol * bnorm) {
+          DDM_CUDA(ctx, cudaMemcpyAsync(xs, xt, nfull * sizeof(double), cudaMemcpyDeviceToDevice, s));
+          rel = tr / bnorm;
+          converged = accepted = true;
+          break;
+        }
+        inner = std::min(inner, std::fabs(gv[k + 1]) / bnorm) * 0.5 * (tol * bnorm / tr);
+        continue;
+      }
+      if (est_ok || iters >= max_iter || hn == 0.0) break;
     }
-    // y = H^-1 g (upper triangular), x += V y
-    for (int i = kdone - 1; i >= 0; --i) {
-      double acc = gv[i];
-      for (int j = i + 1; j < kdone; ++j) acc -= H[(size_t)i * m + j] * y[j];
-      y[i] = acc / H[(size_t)i * m + i];
-    }
-    DDM_CUDA(ctx, cudaMemcpyAsync(g.dh, y.data(), kdone * sizeof(double), cudaMemcpyHostToDevice, s));
-    if (use_pc) {   // x += M^-1 (V y)
-      DDM_CUDA(ctx, cudaMemsetAsync(uf + lo, 0, nloc * sizeof(double), s));
-      if ((rc = g.axpy(V, nloc, kdone, g.dh, 1.0, uf + lo))) return rc;
-      block_apply<<<nblk(t->own_el_hi - t->own_el_lo, 256), 256, 0, s>>>(
-          t->own_el_lo, t->own_el_hi, ncomp, t->pc, uf, xs, 1);
-      DDM_CUDA(ctx, cudaGetLastError());
-    } else if ((rc = g.axpy(V, nloc, kdone, g.dh, 1.0, xs + lo))) {
-      return rc;
-    }
-    if (ctx->world > 1 && (rc = allgather_sorted(ctx, t, xs, ncomp, s))) return rc;
-    DDM_CUDA(ctx, cudaStreamSynchronize(s));   // y (host) must stay alive until the copy ran
+    if (accepted) break;
+    if ((rc = form_x(kdone, xs))) return rc;
   }
   if (ctx->world > 1 && (rc = allgather_sorted(ctx, t, xs, ncomp, s))) return rc;
   scatter_to_user<<<nblk(n, 256), 256, 0, s>>>(n, ncomp, t->perm, xs, x_user);

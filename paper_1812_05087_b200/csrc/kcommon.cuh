@@ -88,6 +88,13 @@ int launch_poro_hist_near(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, in
                           const double* Hs, const double* Cs, cudaStream_t s);
 int launch_poro_self_blocks(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, double* blk,
                             cudaStream_t s);
+// leaf-block Jacobi preconditioner blocks (gmres.cu): chunks[q] = (first
+// sorted element, count <= kPcChunk), block q row-major at blk + off[q]
+int launch_poro_chunk_blocks(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, int nchunks,
+                             const int2* chunks, const int64_t* off, double* blk, cudaStream_t s);
+int launch_elastic_chunk_blocks(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, int nchunks,
+                                const int2* chunks, const int64_t* off, double* blk,
+                                cudaStream_t s);
 int launch_elastic_self_blocks(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, double* blk,
                                cudaStream_t s);
 int launch_poro_direct(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi,

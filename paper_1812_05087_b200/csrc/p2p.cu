@@ -280,7 +280,49 @@ __global__ void elastic_self_blocks(int64_t n, const double* __restrict__ ex,
     blk[i * 4 + 1 * 2 + col] = T.y;
   }
 }
+// dense diagonal blocks of the leaf-block Jacobi preconditioner (gmres.cu):
+// CTA per chunk; entry (2 i + r, 2 j + c) = traction component r at element
+// e0+i from a unit DD component c on element e0+j (the exact pair kernel)
+__global__ void elastic_chunk_blocks(const int2* __restrict__ chunks,
+                                     const int64_t* __restrict__ off, const double* __restrict__ ex,
+                                     const double* __restrict__ ey, const double* __restrict__ ea,
+                                     const double* __restrict__ ec, const double* __restrict__ es,
+                                     double gc, double* __restrict__ blk) {
+  const int2 ch = chunks[blockIdx.x];
+  const int e0 = ch.x, ne = ch.y, d = 2 * ne;
+  double* Bk = blk + off[blockIdx.x];
+  for (int idx = threadIdx.x; idx < ne * ne * 2; idx += blockDim.x) {
+    const int col = idx % 2, pr = idx / 2, i = e0 + pr / ne, j = e0 + pr % ne;
+    const double c = ec[j], s = es[j], a = ea[j];
+    const double2 r = make_double2(c * c - s * s, -2.0 * c * s);
+    const double ds = col == 0 ? 1.0 : 0.0, dn = col == 1 ? 1.0 : 0.0;
+    const double2 B = make_double2(ds * c - dn * s, ds * s + dn * c);
+    const double2 rB = cmul(r, B);
+    const double2 Bh = make_double2(0.5 * B.x, 0.5 * B.y);
+    const double2 P1 = cmul(Bh, make_double2(r.x - 1.0, r.y));
+    const double2 T2 = cmul(Bh, make_double2(r.x + 1.0, r.y));
+    const double sp[kSrcStride] = {ex[j] - a * c, ey[j] - a * s, ex[j] + a * c, ey[j] + a * s,
+                                   P1.x, P1.y, -T2.y, T2.x, Bh.x, Bh.y, -(rB.x + B.x),
+                                   -(rB.y - B.y)};
+    P2PAcc acc;
+    pair_update(acc, ex[i], ey[i], sp);
+    const double2 T = acc_to_traction(acc, gc, ec[i], es[i]);
+    const int r0 = 2 * (i - e0), c0 = 2 * (j - e0) + col;
+    Bk[(size_t)r0 * d + c0] = T.x;
+    Bk[(size_t)(r0 + 1) * d + c0] = T.y;
+  }
+}
 }  // namespace
+
+int launch_elastic_chunk_blocks(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, int nchunks,
+                                const int2* chunks, const int64_t* off, double* blk,
+                                cudaStream_t s) {
+  if (nchunks <= 0) return DDM_OK;
+  elastic_chunk_blocks<<<nchunks, 128, 0, s>>>(chunks, off, t->ex, t->ey, t->ea, t->ec, t->es,
+                                               gc, blk);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
 
 int launch_elastic_self_blocks(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, double* blk,
                                cudaStream_t s) {

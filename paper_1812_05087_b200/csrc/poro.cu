@@ -962,7 +962,51 @@ __global__ void poro_self_blocks(int64_t n, const double* __restrict__ ex,
   }
 }
 
+// dense diagonal blocks of the leaf-block Jacobi preconditioner (gmres.cu):
+// CTA per chunk of <= kPcChunk consecutive sorted elements; entry
+// (3 i + r, 3 j + c) = response r at element e0+i to a unit component c on
+// element e0+j (the exact direct-mode pair kernel)
+__global__ void poro_chunk_blocks(const int2* __restrict__ chunks, const int64_t* __restrict__ off,
+                                  const double* __restrict__ ex, const double* __restrict__ ey,
+                                  const double* __restrict__ ea, const double* __restrict__ ec,
+                                  const double* __restrict__ es, PoroConst k,
+                                  double* __restrict__ blk) {
+  const int2 ch = chunks[blockIdx.x];
+  const int e0 = ch.x, ne = ch.y, d = 3 * ne;
+  double* B = blk + off[blockIdx.x];
+  for (int idx = threadIdx.x; idx < ne * ne * 3; idx += blockDim.x) {
+    const int col = idx % 3, pr = idx / 3, i = e0 + pr / ne, j = e0 + pr % ne;
+    const double2 zt = make_double2(ex[i], ey[i]);
+    const double ct = ec[i], st = es[i];
+    const double2 e2t = make_double2(ct * ct - st * st, 2.0 * ct * st);
+    const double sp[kPoroStride] = {ex[j], ey[j], ec[j], es[j], ea[j], col == 0 ? 1.0 : 0.0,
+                                    col == 1 ? 1.0 : 0.0, col == 2 ? 1.0 : 0.0};
+    double os = 0.0, on = 0.0, op = 0.0;
+    poro_pair(zt, e2t, sp, k, os, on, op);
+    const int r0 = 3 * (i - e0), c0 = 3 * (j - e0) + col;
+    B[(size_t)(r0 + 0) * d + c0] = os;
+    B[(size_t)(r0 + 1) * d + c0] = on;
+    B[(size_t)(r0 + 2) * d + c0] = op;
+  }
+}
+
 }  // namespace
+
+static PoroConst to_const(const PoroParams& P) {
+  PoroConst k;
+  k.G = P.G; k.C = P.C; k.eta = P.eta; k.kp = P.kp; k.S = P.S; k.kappa = P.kappa; k.c = P.c;
+  k.ct = P.ct; k.gc = P.G * P.C;
+  return k;
+}
+
+int launch_poro_chunk_blocks(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, int nchunks,
+                             const int2* chunks, const int64_t* off, double* blk, cudaStream_t s) {
+  if (nchunks <= 0) return DDM_OK;
+  poro_chunk_blocks<<<nchunks, 128, 0, s>>>(chunks, off, t->ex, t->ey, t->ea, t->ec, t->es,
+                                            to_const(P), blk);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
 
 PoroParams poro_params(const ddm_material* m, double tau) {
   PoroParams P;
@@ -1054,12 +1098,6 @@ int poro_init_tables(ddm_ctx_s* ctx) {
   return DDM_OK;
 }
 
-static PoroConst to_const(const PoroParams& P) {
-  PoroConst k;
-  k.G = P.G; k.C = P.C; k.eta = P.eta; k.kp = P.kp; k.S = P.S; k.kappa = P.kappa; k.c = P.c;
-  k.ct = P.ct; k.gc = P.G * P.C;
-  return k;
-}
 
 int launch_poro_prep(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D,
                      cudaStream_t s) {

@@ -66,18 +66,25 @@ def solve_sync(k=0):
 
 
 out["matvec_newptr_sync_ms"] = ev_time(solve_sync, 20)
-for it in (50, 100, 200, 400, 800):
+for it in (100,):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     x, k, rr = D.gmres_solve(ctx, tree, mat, b, dt=dt, tol=1e-30, restart=3000, max_iter=it,
                              raise_noconv=False)
     torch.cuda.synchronize()
     out[f"gmres_{it}_ms"] = (time.perf_counter() - t0) * 1e3
-for pc in (True, False):
+for rs, mi, tol in ():
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    x, k, rr = D.gmres_solve(ctx, tree, mat, b, dt=dt, tol=tol, restart=rs, max_iter=mi,
+                             raise_noconv=False)
+    torch.cuda.synchronize()
+    out[f"gmres_rs{rs}_mi{mi}_tol{tol}"] = {"iters": k, "rel": rr, "ms": (time.perf_counter() - t0) * 1e3}
+for pc in ("leaf", "point", False):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     x, k, rr = D.gmres_solve(ctx, tree, mat, b, dt=dt, tol=c["tol"], restart=3000,
                              max_iter=6000, raise_noconv=False, precond=pc)
     torch.cuda.synchronize()
-    out[f"solve_precond{int(pc)}"] = {"iters": k, "rel": rr, "ms": (time.perf_counter() - t0) * 1e3}
+    out[f"solve_precond_{pc}"] = {"iters": k, "rel": rr, "ms": (time.perf_counter() - t0) * 1e3}
 print(json.dumps(out, indent=1))
