@@ -238,10 +238,12 @@ def run_ours(args):
     p2p_ms = stages["p2p"]
     achieved = owned_pairs * FLOP_PER_PAIR / (p2p_ms * 1e-3) / 1e12
     levels = cnt["LEVELS"]
-    # prep_sources, p2p_kernel, p2m_kernel, m2m_kernel, m2l_kernel, l2l_kernel,
-    # finalize_kernel
+    # per matvec: prep_sources, p2p_kernel, p2m_kernel, m2m_level_kernel per
+    # level 2..L-2 with parents, m2l_kernel, l2l_level_kernel per level 3..L-1,
+    # l2p_kernel, finalize_kernel = 2 L for L levels (24 at L = 12; the list in
+    # profiles/r1_launches_cfg5_summary.txt), replayed as one CUDA graph
     # (+ unpack_allgather and scatter_user when the rows are exchanged)
-    launches_per_step = 7
+    launches_per_step = 2 * levels
     if world > 1:
         launches_per_step += 2
 

@@ -1,5 +1,6 @@
 """Profiling driver: config-5 tree + a few FMM matvecs (for ncu launch lists /
---set full captures).  python scripts/profile_matvec.py [reps] [p] [cfg]"""
+--set full captures).  python scripts/profile_matvec.py [reps] [p] [cfg] [mode]
+(mode: "fmm" default, "bbfmm3", "bbfmm6", "direct")"""
 import os
 import sys
 
@@ -12,6 +13,7 @@ from synth import CONFIGS, make_config, random_dd
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 cfgn = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+mode = sys.argv[4] if len(sys.argv) > 4 else "fmm"
 c = CONFIGS[cfgn]
 p = int(sys.argv[2]) if len(sys.argv) > 2 else c["p"]
 ctx = D.Context(0)
@@ -22,6 +24,6 @@ mat = D.material_from_dict(c["material"])
 Dv = f(random_dd(g.n, 2, c.get("d_seed", 55)))
 y = torch.empty_like(Dv)
 for _ in range(reps):
-    D.matvec(ctx, tree, mat, Dv, y)
+    D.matvec(ctx, tree, mat, Dv, y, mode=mode)
 torch.cuda.synchronize()
 print("ok", tree.counts)
