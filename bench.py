@@ -29,8 +29,8 @@ sys.path.insert(0, ROOT)
 METRIC = ("FMM DDM matvec interactions/s and GMRES solve time (fp64) vs roofline, "
           "1/2/4/8 GPU")
 UNIT = "interactions/s"
-FLOP_PER_PAIR = 57          # P2P pair update: 21 DFMA (2 flop) + 9 DMUL + 6 DADD
-FP64_INSTR_PER_PAIR = 36    # fp64-pipe instructions per pair (+ 1 MUFU.RCP64H on the XU)
+FLOP_PER_PAIR = 45          # P2P record update as written: 16 FMA (2 flop) + 5 MUL + 8 ADD
+FP64_INSTR_PER_PAIR = 28    # fp64-pipe instructions per record and target in the SASS (+ 1 MUFU.RCP64H)
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 
 

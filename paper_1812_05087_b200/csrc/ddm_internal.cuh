@@ -25,7 +25,9 @@ constexpr int kTgtGroup = DDM_TGT_GROUP;   // targets per P2P work item (one war
 #define DDM_SRC_CHUNK 512
 #endif
 constexpr int kSrcChunk = DDM_SRC_CHUNK;  // max sources per P2P work item
-constexpr int kSrcStride = 12;  // doubles per P2P source record
+constexpr int kSrcStride = 12;  // doubles per direct-mode source record
+constexpr int kRecStride = 10;  // doubles per near-field stream record (node + 4 complex coefficients)
+constexpr int kChainMax = 256;  // leaves with more elements keep Morton order (no node sharing)
 constexpr int kPcChunk = 32;    // max elements per leaf-block preconditioner block
 
 struct Status {
@@ -168,7 +170,15 @@ struct ddm_tree_s {
   double2* mpole = nullptr;
   double2* local = nullptr;
   // per-matvec workspaces
-  double* src = nullptr;          // [n][10] P2P source coefficients
+  double* src = nullptr;          // [n][12] direct-mode source records
+  // near-field source stream (p2p.cu): each leaf's elements
+  // reordered along fracture chains; consecutive elements sharing a node
+  // share its reciprocal.  Built once per tree.
+  int* st_elem = nullptr;         // [n] stream slot -> sorted element (permutation within leaves)
+  unsigned char* st_code = nullptr;   // [n] bit 0: flipped (first node = z2), bit 1: linked to slot - 1
+  int* rbeg = nullptr;            // [n+1] first record of each slot (its break record if unlinked)
+  double* srec = nullptr;         // [nrec][kRecStride]; record 0 = pad
+  int64_t nrec = 0;
   double2* part = nullptr;        // [nitems*32] partial tractions
   double* d_sorted = nullptr;     // [n*3] D gathered into sorted order
   double* y_sorted = nullptr;     // [n*3]

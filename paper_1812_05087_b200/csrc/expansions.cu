@@ -804,14 +804,14 @@ int pass_grid(ddm_ctx_s* ctx, const void* kernel, size_t shm, int work) {
   }
   const int by_work = (work + kPassWarps - 1) / kPassWarps;
   // DDM_PASS_BLOCKS_PER_SM caps the grids of the pass kernels so the
-  // concurrent near field keeps SM slots (0 = occupancy limit); default: 1
+  // concurrent near field keeps SM slots (0 = occupancy limit); default: 2
   // block per SM when the near field runs concurrently, the occupancy limit
   // when everything is serial
   static const int env_cap = [] {
     const char* e = getenv("DDM_PASS_BLOCKS_PER_SM");
     return e ? atoi(e) : -1;
   }();
-  const int cap = env_cap >= 0 ? env_cap : (ctx->serial ? 0 : 1);
+  const int cap = env_cap >= 0 ? env_cap : (ctx->serial ? 0 : 2);
   if (cap > 0) per_sm = std::min(per_sm, cap);
   return std::max(1, std::min(std::max(per_sm, 1) * nsm, by_work));
 }

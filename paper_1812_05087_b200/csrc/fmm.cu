@@ -21,7 +21,7 @@ double binom(int n, int k) {
   return r;
 }
 
-int ensure_workspace(ddm_ctx_s* ctx, ddm_tree_s* t) {
+int ensure_workspace(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   int rc;
   if (!t->mpole) {
     if ((rc = dalloc(ctx, &t->mpole, (size_t)t->ncells * 2 * t->p))) return rc;
@@ -32,7 +32,7 @@ int ensure_workspace(ddm_ctx_s* ctx, ddm_tree_s* t) {
     if ((rc = dalloc(ctx, &t->y_sorted, (size_t)t->n * 3))) return rc;
     if ((rc = dalloc(ctx, &t->y_far, (size_t)t->n * 3))) return rc;
   }
-  return DDM_OK;
+  return build_source_stream(ctx, t, s);
 }
 
 }  // namespace
@@ -126,7 +126,7 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
 int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double elapsed,
                const double* D, bool d_sorted, double* y_user, double* y_sorted, int mode,
                cudaStream_t s) {
-  int rc = ensure_workspace(ctx, t);
+  int rc = ensure_workspace(ctx, t, s);
   if (rc) return rc;
   static const bool no_graph = [] {
     const char* e = getenv("DDM_NO_GRAPH");
@@ -218,8 +218,11 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
   }
 
   stage_begin(ctx, DDM_ST_PREP, s);
+  // elastic: the direct mode reads per-element source records, the near
+  // field of the FMM the node-sharing source stream (p2p.cu)
   rc = poro ? launch_poro_prep(ctx, t, perm_in, D, s)
-            : launch_prep_sources(ctx, t, perm_in, D, ncomp, s);
+       : mode == DDM_DIRECT ? launch_prep_sources(ctx, t, perm_in, D, ncomp, s)
+                            : launch_prep_stream(ctx, t, perm_in, D, ncomp, s);
   if (rc) return rc;
   stage_end(ctx, DDM_ST_PREP, s);
 
@@ -281,7 +284,7 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
 // order; writes the owned rows into y_user and/or y_sorted.
 int fmm_history(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt, int h,
                 const double* D_hist, double* y_user, double* y_sorted, cudaStream_t s) {
-  int rc = ensure_workspace(ctx, t);
+  int rc = ensure_workspace(ctx, t, s);
   if (rc) return rc;
   const PoroParams PP = poro_params(mat, dt);
   if (t->nlevels > 2) {

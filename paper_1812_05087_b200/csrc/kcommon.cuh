@@ -115,6 +115,11 @@ int launch_prep_sources(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const
                         int ncomp, cudaStream_t s);
 int launch_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, double gc,
                cudaStream_t s);
+// near-field source stream (p2p.cu): chain order + break records once per
+// tree; prep_stream writes the element records (and D in sorted order)
+int build_source_stream(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
+int launch_prep_stream(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D,
+                       int ncomp, cudaStream_t s);
 int launch_direct(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, int ncomp, double gc,
                   double* y_user, double* y_sorted, cudaStream_t s);
 

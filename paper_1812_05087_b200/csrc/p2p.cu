@@ -85,30 +85,246 @@ __device__ __forceinline__ double2 acc_to_traction(const P2PAcc& a, double gc, d
   return make_double2(T.y, T.x - 4.0 * gc * a.phi);            // (sigma_s, sigma_n)
 }
 
+// ---------------------------------------------------------------- stream
+// Near-field source stream.  Constant DD elements of one
+// fracture share their end nodes, and I2 = r2 - r1 only needs the reciprocal
+// r = 1/(z - node) of each NODE: an element whose first node is the previous
+// element's second node reuses that reciprocal.  The elements of each leaf are
+// therefore reordered along chains of node-sharing elements (a permutation
+// within the leaf, so every U-list range [lo, hi) of sorted elements is the
+// same range of stream slots); a chain start is preceded by a break record
+// (its first node, zero coefficients).  Record of slot q:
+//   {second node, P1, P2, Bh, Q'} (x sign: a flipped element, first node =
+//   z2, has I2 negated, so its coefficients are negated), 10 doubles.
+// Node sharing is decided by coordinates equal up to 8 ulp of the coordinate
+// magnitude; the shared node is then the previous element's computed node,
+// an O(ulp) change of the element's own endpoint (reading R22).
+
+__device__ __forceinline__ double2 end_node(const double* ex, const double* ey,
+                                            const double* ea, const double* ec,
+                                            const double* es, int i, int ep) {
+  const double a = ep ? ea[i] : -ea[i];
+  return make_double2(ex[i] + a * ec[i], ey[i] + a * es[i]);
+}
+
+// Thread per leaf: node-sharing neighbours (O(count^2) endpoint matching),
+// then chains walked from their free ends in sorted-index order (closed loops
+// last).  st_code bit 0: flipped, bit 1: linked to the previous slot.
+__global__ void chain_order_kernel(int nleaves, const int* __restrict__ leaves,
+                                   const int* __restrict__ c_start,
+                                   const int* __restrict__ c_count, const double* __restrict__ ex,
+                                   const double* __restrict__ ey, const double* __restrict__ ea,
+                                   const double* __restrict__ ec, const double* __restrict__ es,
+                                   int* __restrict__ st_elem, unsigned char* __restrict__ st_code) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nleaves) return;
+  const int c = leaves[k];
+  const int cs = c_start[c], cnt = c_count[c];
+  if (cnt > kChainMax) {   // Morton order, every element a chain of its own
+    for (int i = 0; i < cnt; ++i) {
+      st_elem[cs + i] = cs + i;
+      st_code[cs + i] = 0;
+    }
+    return;
+  }
+  // nb[i][ep] = 2 j + ep_j of the element endpoint coinciding with (i, ep), or -1
+  short nb[kChainMax][2];
+  unsigned char vis[kChainMax];
+  for (int i = 0; i < cnt; ++i) {
+    nb[i][0] = nb[i][1] = -1;
+    vis[i] = 0;
+  }
+  const double eps8 = 8.0 * 2.220446049250313e-16;
+  for (int i = 0; i < cnt; ++i)
+    for (int ei = 0; ei < 2; ++ei) {
+      if (nb[i][ei] >= 0) continue;
+      const double2 p = end_node(ex, ey, ea, ec, es, cs + i, ei);
+      const double tol = eps8 * (fabs(p.x) + fabs(p.y));
+      for (int j = i + 1; j < cnt && nb[i][ei] < 0; ++j)
+        for (int ej = 0; ej < 2; ++ej) {
+          if (nb[j][ej] >= 0) continue;
+          const double2 q = end_node(ex, ey, ea, ec, es, cs + j, ej);
+          if (fabs(p.x - q.x) <= tol && fabs(p.y - q.y) <= tol) {
+            nb[i][ei] = (short)(2 * j + ej);
+            nb[j][ej] = (short)(2 * i + ei);
+            break;
+          }
+        }
+    }
+  int out = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int s0 = 0; s0 < cnt; ++s0) {
+      if (vis[s0]) continue;
+      if (pass == 0 && nb[s0][0] >= 0 && nb[s0][1] >= 0) continue;   // interior of a chain
+      int cur = s0, first = (pass == 0 && nb[s0][0] >= 0) ? 1 : 0;
+      bool link = false;
+      while (true) {
+        vis[cur] = 1;
+        st_elem[cs + out] = cs + cur;
+        st_code[cs + out] = (unsigned char)((first ? 1 : 0) | (link ? 2 : 0));
+        ++out;
+        const int n = nb[cur][1 - first];
+        if (n < 0 || vis[n >> 1]) break;
+        cur = n >> 1;
+        first = n & 1;
+        link = true;
+      }
+    }
+}
+
+__global__ void chain_count_kernel(int64_t n, const unsigned char* __restrict__ st_code,
+                                   int* __restrict__ cntv) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q < n) cntv[q] = (st_code[q] & 2) ? 1 : 2;
+}
+
+// break records (first node, zero coefficients) of the unlinked slots, and
+// the pad record 0 (a node far outside the tree, zero coefficients)
+__global__ void break_records_kernel(int64_t n, const int* __restrict__ st_elem,
+                                     const unsigned char* __restrict__ st_code,
+                                     const int* __restrict__ rbeg, const double* __restrict__ ex,
+                                     const double* __restrict__ ey, const double* __restrict__ ea,
+                                     const double* __restrict__ ec, const double* __restrict__ es,
+                                     double2 pad, double* __restrict__ srec) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q == 0) {
+    double2* o = reinterpret_cast<double2*>(srec);
+    o[0] = pad;
+    for (int f = 1; f < kRecStride / 2; ++f) o[f] = make_double2(0.0, 0.0);
+  }
+  if (q >= n) return;
+  const unsigned char code = st_code[q];
+  if (code & 2) return;
+  double2* o = reinterpret_cast<double2*>(srec + (int64_t)rbeg[q] * kRecStride);
+  o[0] = end_node(ex, ey, ea, ec, es, st_elem[q], code & 1);
+  for (int f = 1; f < kRecStride / 2; ++f) o[f] = make_double2(0.0, 0.0);
+}
+
+// Per stream slot (every matvec): the element's record from its DDs,
+//   B = (D_s + i D_n) e, r = conj(e)^2, Bh = B/2, Q' = -(r B + conj B),
+//   P1 = Bh (r - 1), P2 = i Bh (r + 1)   (negated for a flipped element)
+// and D gathered to sorted order for the upward pass.
+__global__ void prep_stream(int64_t n, int ncomp, const int* __restrict__ perm,
+                            const int* __restrict__ st_elem,
+                            const unsigned char* __restrict__ st_code,
+                            const int* __restrict__ rbeg, const double* __restrict__ D,
+                            const double* __restrict__ ex, const double* __restrict__ ey,
+                            const double* __restrict__ ea, const double* __restrict__ ec,
+                            const double* __restrict__ es, double* __restrict__ srec,
+                            double* __restrict__ dsort) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int i = st_elem[q];
+  const unsigned char code = st_code[q];
+  const int j = perm ? perm[i] : i;
+  const double ds = D[(int64_t)j * ncomp + 0];
+  const double dn = D[(int64_t)j * ncomp + 1];
+  if (dsort) {
+    dsort[(int64_t)i * ncomp + 0] = ds;
+    dsort[(int64_t)i * ncomp + 1] = dn;
+  }
+  const double c = ec[i], s = es[i];
+  const double sg = (code & 1) ? -1.0 : 1.0;
+  const double2 B = make_double2(ds * c - dn * s, ds * s + dn * c);
+  const double2 r = make_double2(c * c - s * s, -2.0 * c * s);
+  const double2 rB = cmul(r, B);
+  const double2 Bh = make_double2(0.5 * sg * B.x, 0.5 * sg * B.y);
+  const double2 P1 = cmul(Bh, make_double2(r.x - 1.0, r.y));
+  const double2 T2 = cmul(Bh, make_double2(r.x + 1.0, r.y));
+  double2* o = reinterpret_cast<double2*>(srec + (int64_t)(rbeg[q] + ((code & 2) ? 0 : 1)) * kRecStride);
+  o[0] = end_node(ex, ey, ea, ec, es, i, (code & 1) ? 0 : 1);   // second node
+  o[1] = P1;
+  o[2] = make_double2(-T2.y, T2.x);   // P2 = i Bh (r + 1)
+  o[3] = Bh;
+  o[4] = make_double2(-sg * (rB.x + B.x), -sg * (rB.y - B.y));   // Q'
+}
+
+// Per target (z, with the carried reciprocal rp and offset wp of the
+// previous record's node) and record {node, P1, P2, Bh, Q'}:
+//   w = z - node, r = 1/w, I2 = r - rp, S = r + rp, d = w + wp = 2 (z - zc)
+//   phi += Im(Bh I2),  psi += I2 [Q' + (d.x P1 + d.y P2) S]
+// 29 fp64-pipe instructions + 1 MUFU.RCP64H per record.
+struct NodeCarry {
+  double rx, ry, wx, wy;
+};
+
+__device__ __forceinline__ void node_init(NodeCarry& n, double zx, double zy, const double* rec) {
+  n.wx = zx - rec[0];
+  n.wy = zy - rec[1];
+  const double inv = fast_rcp(fma(n.wx, n.wx, n.wy * n.wy));
+  n.rx = n.wx * inv;
+  n.ry = -n.wy * inv;
+}
+
+__device__ __forceinline__ void record_update(P2PAcc& acc, NodeCarry& n, double zx, double zy,
+                                              const double* sp) {
+  const double wx = zx - sp[0], wy = zy - sp[1];
+  const double inv = fast_rcp(fma(wx, wx, wy * wy));
+  const double rx = wx * inv, ry = -wy * inv;
+  const double I2x = rx - n.rx, I2y = ry - n.ry;
+  const double Sx = rx + n.rx, Sy = ry + n.ry;
+  const double dx = wx + n.wx, dy = wy + n.wy;
+  const double BXx = fma(dx, sp[2], dy * sp[4]);
+  const double BXy = fma(dx, sp[3], dy * sp[5]);
+  const double Vx = fma(BXx, Sx, fma(-BXy, Sy, sp[8]));
+  const double Vy = fma(BXx, Sy, fma(BXy, Sx, sp[9]));
+  acc.psi.x = fma(I2x, Vx, fma(-I2y, Vy, acc.psi.x));
+  acc.psi.y = fma(I2x, Vy, fma(I2y, Vx, acc.psi.y));
+  acc.phi = fma(sp[6], I2y, fma(sp[7], I2x, acc.phi));
+  n.rx = rx;
+  n.ry = ry;
+  n.wx = wx;
+  n.wy = wy;
+}
+
 // One warp per work item (leaf k, group of nt <= kTgtGroup targets, interval
-// of the leaf's concatenated source ranges).  Each lane owns kTPL targets
-// (independent chains sharing every source load); the tp = ceil(nt/kTPL)
-// lane-target slots are replicated over S = 32 / tp source slices: lane l
-// takes slot l % tp and the sources j = l / tp (mod S).  Source records are
-// read through L1 (the tp lanes of a slice broadcast one record).  The S slice
-// partials are summed in a fixed order (deterministic results).
-constexpr int kP2PWarps = 4;
+// [item.z, item.w) of the leaf's concatenated source-slot ranges).  Each lane
+// owns kTPL targets (independent chains sharing every record load); the
+// tp = ceil(nt/kTPL) lane-target slots are replicated over S = 32 / tp source
+// slices, and slice s takes the s-th contiguous part of each range's records
+// (a node carry needs consecutive records), starting from the node of the
+// record before it.  Records are read through L1 (the tp lanes of a slice
+// broadcast one record).  The S slice partials are summed in a fixed order
+// (deterministic results, independent of the rank count).
+#ifndef DDM_P2P_WARPS
+#define DDM_P2P_WARPS 4
+#endif
+constexpr int kP2PWarps = DDM_P2P_WARPS;
 #ifndef DDM_P2P_MINB
 #define DDM_P2P_MINB 6
 #endif
 #ifndef DDM_TPL
 #define DDM_TPL 2
 #endif
-constexpr int kTPL = DDM_TPL;   // targets per lane (independent chains sharing each source load)
+constexpr int kTPL = DDM_TPL;   // targets per lane (independent chains sharing each record load)
+#ifndef DDM_P2P_UNROLL
+#define DDM_P2P_UNROLL 2
+#endif
+constexpr int kP2PUnroll = DDM_P2P_UNROLL;
+#ifndef DDM_P2P_PREFETCH
+#define DDM_P2P_PREFETCH 0
+#endif
+constexpr int kP2PPrefetch = DDM_P2P_PREFETCH;   // records ahead (0 = off)
+
+__device__ __forceinline__ void load_rec(double (&sp)[kRecStride], const double* rec) {
+  const double2* g = reinterpret_cast<const double2*>(rec);
+#pragma unroll
+  for (int f = 0; f < kRecStride / 2; ++f) {
+    const double2 v = __ldg(g + f);
+    sp[2 * f] = v.x;
+    sp[2 * f + 1] = v.y;
+  }
+}
 
 __global__ void __launch_bounds__(kP2PWarps * 32, DDM_P2P_MINB)
 p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ items,
            const int* __restrict__ u_off, const int* __restrict__ u_lo,
            const int* __restrict__ u_hi, const int* __restrict__ leaves,
            const int* __restrict__ c_start, const int* __restrict__ c_count,
-           const double* __restrict__ src, const double* __restrict__ ex,
-           const double* __restrict__ ey, const double* __restrict__ ec,
-           const double* __restrict__ es, double gc, double2* __restrict__ part) {
+           const int* __restrict__ rbeg, const double* __restrict__ srec,
+           const double* __restrict__ ex, const double* __restrict__ ey,
+           const double* __restrict__ ec, const double* __restrict__ es, double gc,
+           double2* __restrict__ part) {
   __shared__ double red[kP2PWarps][3][32 * kTPL];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int oi = blockIdx.x * kP2PWarps + w; oi < nown; oi += gridDim.x * kP2PWarps) {
@@ -130,25 +346,35 @@ p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ ite
       zy[q] = ey[ti];
     }
     if (active) {
-      int pos = 0;   // position in the concatenated range space
+      int pos = 0;   // position in the concatenated slot space
       for (int r = u_off[k], rend = u_off[k + 1]; r < rend && pos < item.w; ++r) {
         const int lo = u_lo[r], len = u_hi[r] - lo;
         const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
-        const double* base = src + (int64_t)lo * kSrcStride;
-#pragma unroll 2
-        for (int j = b + slice; j < e; j += S) {
-          double sp[kSrcStride];
-          const double2* g = reinterpret_cast<const double2*>(base + (int64_t)j * kSrcStride);
-#pragma unroll
-          for (int f = 0; f < kSrcStride / 2; ++f) {
-            const double2 v = __ldg(g + f);
-            sp[2 * f] = v.x;
-            sp[2 * f + 1] = v.y;
-          }
-#pragma unroll
-          for (int q = 0; q < kTPL; ++q) pair_update(acc[q], zx[q], zy[q], sp);
-        }
         pos += len;
+        if (b >= e) continue;
+        const int rb = __ldg(rbeg + lo + b), L = __ldg(rbeg + lo + e) - rb;
+        const int q0 = rb + (int)(((int64_t)L * slice) / S);
+        const int q1 = rb + (int)(((int64_t)L * (slice + 1)) / S);
+        if (q0 >= q1) continue;
+        NodeCarry nc[kTPL];
+        {
+          double sp[kRecStride];
+          load_rec(sp, srec + (int64_t)(q0 - 1) * kRecStride);
+#pragma unroll
+          for (int q = 0; q < kTPL; ++q) node_init(nc[q], zx[q], zy[q], sp);
+        }
+#pragma unroll kP2PUnroll
+        for (int j = q0; j < q1; ++j) {
+          double sp[kRecStride];
+          if (kP2PPrefetch > 0) {   // L1 prefetch of the record kP2PPrefetch ahead (no registers)
+            const double* pf = srec + (int64_t)min(j + kP2PPrefetch, q1 - 1) * kRecStride;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pf + kRecStride - 1));
+          }
+          load_rec(sp, srec + (int64_t)j * kRecStride);
+#pragma unroll
+          for (int q = 0; q < kTPL; ++q) record_update(acc[q], nc[q], zx[q], zy[q], sp);
+        }
       }
     }
     // slot of (target t, slice s) = t + s * tp * kTPL
@@ -179,6 +405,11 @@ p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ ite
     }
     __syncwarp();
   }
+}
+
+__global__ void add_const_kernel(int64_t n, int v, int* __restrict__ a) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[i] += v;
 }
 
 // All pairs (mode DDM_DIRECT): thread per target, sources tiled through smem.
@@ -236,9 +467,49 @@ int launch_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, double g
   // high-priority far-field kernels interleave with the near field
   const unsigned nb = nblk(item_hi - item_lo, kP2PWarps);
   p2p_kernel<<<nb, kP2PWarps * 32, 0, s>>>(item_hi - item_lo, t->p2p_order, t->items, t->u_off,
-                                           t->u_lo,
-                                           t->u_hi, t->leaves, t->c_start, t->c_count, t->src,
-                                           t->ex, t->ey, t->ec, t->es, gc, t->part);
+                                           t->u_lo, t->u_hi, t->leaves, t->c_start, t->c_count,
+                                           t->rbeg, t->srec, t->ex, t->ey, t->ec, t->es, gc,
+                                           t->part);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+// Near-field source stream of the tree (once per tree, outside any capture)
+int build_source_stream(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
+  if (t->srec || t->n == 0) return DDM_OK;
+  const int64_t n = t->n;
+  int rc;
+  int* cntv = nullptr;
+  if ((rc = dalloc(ctx, &t->st_elem, (size_t)n)) || (rc = dalloc(ctx, &t->st_code, (size_t)n)) ||
+      (rc = dalloc(ctx, &t->rbeg, (size_t)n + 1)) || (rc = dalloc(ctx, &cntv, (size_t)n + 1)))
+    return rc;
+  chain_order_kernel<<<nblk(t->nleaves, 64), 64, 0, s>>>(t->nleaves, t->leaves, t->c_start,
+                                                         t->c_count, t->ex, t->ey, t->ea, t->ec,
+                                                         t->es, t->st_elem, t->st_code);
+  DDM_CUDA(ctx, cudaGetLastError());
+  chain_count_kernel<<<nblk(n, 256), 256, 0, s>>>(n, t->st_code, cntv);
+  DDM_CUDA(ctx, cudaMemsetAsync(cntv + n, 0, sizeof(int), s));
+  int total = 0;
+  if ((rc = exclusive_scan_i32(ctx, cntv, t->rbeg, (int)n + 1, &total, s))) return rc;
+  cudaFree(cntv);
+  // records: pad (0), then the slots' records; rbeg was counted from 0
+  add_const_kernel<<<nblk(n + 1, 256), 256, 0, s>>>(n + 1, 1, t->rbeg);
+  DDM_CUDA(ctx, cudaGetLastError());
+  t->nrec = (int64_t)total + 1;
+  if ((rc = dalloc(ctx, &t->srec, (size_t)t->nrec * kRecStride))) return rc;
+  const double2 pad = make_double2(t->x_min - 16.0 * t->W, t->y_min - 16.0 * t->W);
+  break_records_kernel<<<nblk(n, 256), 256, 0, s>>>(n, t->st_elem, t->st_code, t->rbeg, t->ex,
+                                                    t->ey, t->ea, t->ec, t->es, pad, t->srec);
+  DDM_CUDA(ctx, cudaGetLastError());
+  DDM_CUDA(ctx, cudaStreamSynchronize(s));
+  return DDM_OK;
+}
+
+int launch_prep_stream(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D,
+                       int ncomp, cudaStream_t s) {
+  prep_stream<<<nblk(t->n, 256), 256, 0, s>>>(t->n, ncomp, perm_in, t->st_elem, t->st_code,
+                                               t->rbeg, D, t->ex, t->ey, t->ea, t->ec, t->es,
+                                               t->srec, perm_in ? t->d_sorted : nullptr);
   DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;
 }

@@ -261,3 +261,55 @@ def test_no_w_lists_reproduce_survey_sizes_and_parity(ddm, monkeypatch):
     Dv = random_dd(g.n, 2, 102)
     y = _mv(D, ctx, torch, tree, Dv, "fmm")
     assert rel_l2(y, OE.matvec_dense(_A(2), Dv)) <= 1e-8
+
+
+def _polyline_elements(nodes_list):
+    """Constant elements between consecutive nodes of each polyline (beta in
+    [0, pi), so the element's own first endpoint may be either node)."""
+    xc, yc, a, b, fid = [], [], [], [], []
+    for f, P in enumerate(nodes_list):
+        P = np.asarray(P, dtype=np.float64)
+        d = P[1:] - P[:-1]
+        xc.append(0.5 * (P[1:, 0] + P[:-1, 0]))
+        yc.append(0.5 * (P[1:, 1] + P[:-1, 1]))
+        a.append(0.5 * np.hypot(d[:, 0], d[:, 1]))
+        b.append(np.mod(np.arctan2(d[:, 1], d[:, 0]), np.pi))
+        fid.append(np.full(len(d), f))
+    n = sum(len(v) for v in xc)
+    return Geometry(np.concatenate(xc), np.concatenate(yc), np.concatenate(a), np.concatenate(b),
+                    np.concatenate(fid), np.zeros((len(nodes_list), 2), int))
+
+
+def _node_sharing_cases():
+    rng = np.random.default_rng(7)
+    t = np.linspace(0, 1, 41)
+    square = np.concatenate([np.stack([t, 0 * t], 1)[:-1], np.stack([1 + 0 * t, t], 1)[:-1],
+                             np.stack([1 - t, 1 + 0 * t], 1)[:-1], np.stack([0 * t, 1 - t], 1)])
+    kink = np.stack([np.linspace(0, 2, 31), 0.3 * np.abs(np.linspace(-1, 1, 31))], 1)
+    star = [np.stack([0.5 + np.cos(th) * np.linspace(0, 0.8, 13),
+                      2.0 + np.sin(th) * np.linspace(0, 0.8, 13)], 1) for th in (0.3, 2.4, 4.4)]
+    zigzag = np.stack([np.linspace(3, 5, 50), 1.0 + 0.05 * (np.arange(50) % 2)], 1)
+    g = _polyline_elements([square, kink, *star, zigzag])
+    perm = rng.permutation(g.n)   # user order unrelated to the fracture order
+    return Geometry(g.xc[perm], g.yc[perm], g.half_len[perm], g.beta[perm], g.frac_id[perm],
+                    g.tips)
+
+
+@pytest.mark.parametrize("leaf", [8, 32, 300])
+def test_node_sharing_geometries(ddm, leaf):
+    """Near-field source stream (R22): closed loop, kinked and
+    star-shaped polylines (three elements meeting at a node), zig-zag, in a
+    shuffled user order; leaf 300 puts all 275 elements in one leaf, above the
+    chain-order cap (Morton order, no node sharing)."""
+    D, ctx, torch = ddm
+    g = _node_sharing_cases()
+    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+    tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=leaf, order_p=40)
+    A = OE.assemble_dense(g, G0, NU0)
+    rng = np.random.default_rng(leaf)
+    for _ in range(2):
+        Dv = rng.uniform(-1e-3, 1e-3, (g.n, 2))
+        ref = OE.matvec_dense(A, Dv)
+        assert rel_l2(_mv(D, ctx, torch, tree, Dv, "direct"), ref) <= 1e-12
+        assert rel_l2(_mv(D, ctx, torch, tree, Dv, "fmm"), ref) <= (1e-12 if leaf == 300 else 1e-10)
+    tree.free()
