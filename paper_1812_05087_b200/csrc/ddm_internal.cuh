@@ -188,6 +188,15 @@ struct ddm_tree_s {
   double2* bb_w = nullptr;
   double2* bb_f = nullptr;
   int bb_n = 0;
+  // poroelastic near-field matrix cache (poro.cu): 3x3
+  // blocks of every owned near pair for one (material, elapsed time), built
+  // on the second consecutive matvec with the same parameters
+  double* nc = nullptr;           // blocks, item by item: [(jpos * kTgtGroup + t) * 9 + 3 r + c]
+  int64_t* nc_off = nullptr;      // [owned items] first double of each item
+  int64_t nc_n = 0;               // doubles allocated
+  double nc_key[9] = {};          // PoroConst of the cached blocks
+  double nc_seen[9] = {};         // PoroConst of the previous poroelastic matvec
+  bool nc_valid = false, nc_seen_set = false;
   // matvec CUDA graphs (fmm.cu)
   std::vector<MatvecGraph> graphs = std::vector<MatvecGraph>(4);
   int graph_next = 0;

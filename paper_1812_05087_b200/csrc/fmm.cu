@@ -128,6 +128,10 @@ int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double el
                cudaStream_t s) {
   int rc = ensure_workspace(ctx, t, s);
   if (rc) return rc;
+  // poroelastic near-field blocks: cached for repeated matvecs at one elapsed
+  // time (GMRES), outside any capture
+  if (mat->kind == 1 && mode == DDM_FMM && elapsed > 0)
+    if ((rc = poro_near_cache_update(ctx, t, poro_params(mat, elapsed), s))) return rc;
   static const bool no_graph = [] {
     const char* e = getenv("DDM_NO_GRAPH");
     return e && e[0] == '1';

@@ -82,6 +82,9 @@ int launch_poro_prep(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const do
                      cudaStream_t s);
 int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, const PoroParams& P,
                     cudaStream_t s);
+// near-field matrix cache of the poroelastic operator (built on the second
+// consecutive matvec with the same parameters)
+int poro_near_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, cudaStream_t s);
 int launch_poro_hist_gather(ddm_ctx_s* ctx, ddm_tree_s* t, int h, const double* D_hist,
                             double* Hs, double* Cs, double* Ctot, cudaStream_t s);
 int launch_poro_hist_near(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, int h, double dt,
