@@ -233,6 +233,16 @@ int ddm_ctx_create(int device, const void* nccl_uid, int rank, int world, ddm_ct
     *out = ctx;
     return rc;
   }
+  {
+    // stream-ordered workspaces (cudaMallocAsync in history / GMRES calls)
+    // stay mapped in the device's default pool between calls instead of
+    // being unmapped at every synchronisation and remapped by the next call
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   e = cudaMalloc((void**)&ctx->d_scalar, 64 * sizeof(double));
   if (e != cudaSuccess) {
     int rc = cuda_error(ctx, e, "cudaMalloc(scratch)");

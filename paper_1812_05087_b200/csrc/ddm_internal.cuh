@@ -197,6 +197,16 @@ struct ddm_tree_s {
   double nc_key[9] = {};          // PoroConst of the cached blocks
   double nc_seen[9] = {};         // PoroConst of the previous poroelastic matvec
   bool nc_valid = false, nc_seen_set = false;
+  // history near-field lag cache (poro.cu): blocks of the
+  // poroelastic part K^p(j dt) of every owned near pair, in chunks of lags
+  // (nc_off item layout x kLagChunk), built as the history grows
+  std::vector<double*> hc_lag;    // device chunks of kLagChunk lags ([item][jpos][lag][t][9])
+  int hc_nlags = 0;               // lags built (1..hc_nlags)
+  int hc_max_chunks = 0;          // chunk budget (memory) fixed when the cache is keyed
+  double** hc_ptrs = nullptr;     // device copy of hc_lag
+  int hc_ptrs_n = 0;
+  double hc_key[9] = {}, hc_seen[9] = {};
+  bool hc_valid = false, hc_seen_set = false, hc_capped = false;
   // matvec CUDA graphs (fmm.cu)
   std::vector<MatvecGraph> graphs = std::vector<MatvecGraph>(4);
   int graph_next = 0;

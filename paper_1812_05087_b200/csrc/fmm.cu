@@ -300,6 +300,8 @@ int fmm_history(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
                        "tree too fine for the poroelastic far field at the history's longest lag: "
                        "build it with min_leaf_side >= sqrt(160 c (h+1) dt) + 2 max(a)");
   }
+  const bool cached = poro_hist_cache_update(ctx, t, mat, dt, h, s, &rc);
+  if (rc) return rc;
   const int64_t n = t->n;
   double *Hs = nullptr, *Cs = nullptr, *Ctot = nullptr;
   DDM_CUDA(ctx, cudaMallocAsync((void**)&Hs, (size_t)n * (h + 2) * 3 * sizeof(double), s));
@@ -314,7 +316,9 @@ int fmm_history(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   DDM_CUDA(ctx, cudaStreamWaitEvent(sf, ctx->ev_fork, 0));
   DDM_CUDA(ctx, cudaStreamWaitEvent(sn, ctx->ev_fork, 0));
   stage_begin(ctx, DDM_ST_P2P, sn);
-  if ((rc = launch_poro_hist_near(ctx, t, PP, h, dt, Hs, Cs, sn))) return rc;
+  rc = cached ? launch_poro_hist_cached(ctx, t, h, Hs, sn)
+              : launch_poro_hist_near(ctx, t, PP, h, dt, Hs, Cs, sn);
+  if (rc) return rc;
   stage_end(ctx, DDM_ST_P2P, sn);
   DDM_CUDA(ctx, cudaEventRecord(ctx->ev_near, sn));
   PoroFar pf = poro_far(PP);

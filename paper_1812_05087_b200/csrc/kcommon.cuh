@@ -85,6 +85,11 @@ int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, con
 // near-field matrix cache of the poroelastic operator (built on the second
 // consecutive matvec with the same parameters)
 int poro_near_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, cudaStream_t s);
+// history lag cache: true when lags 1..h+1 are cached
+bool poro_hist_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt,
+                            int h, cudaStream_t s, int* rc_out);
+int launch_poro_hist_cached(ddm_ctx_s* ctx, ddm_tree_s* t, int h, const double* Hs,
+                            cudaStream_t s);
 int launch_poro_hist_gather(ddm_ctx_s* ctx, ddm_tree_s* t, int h, const double* D_hist,
                             double* Hs, double* Cs, double* Ctot, cudaStream_t s);
 int launch_poro_hist_near(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, int h, double dt,

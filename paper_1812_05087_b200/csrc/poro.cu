@@ -16,6 +16,7 @@
 //             - mu f2(u) ob^2/(16 pi c tau) - q h2(u) ob^2/(16 pi kappa)
 //   K = -4 k_p i G C B e, B = (Ds + i Dn) e, mu = -(eta/S) Dn
 //   T^p = sigma_n + i sigma_s = -eta p + e^{2 i bt} (-4 eta d2Phi)
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -784,8 +785,8 @@ poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __re
                        const int* __restrict__ c_start, const int* __restrict__ c_count,
                        const double* __restrict__ ex, const double* __restrict__ ey,
                        const double* __restrict__ ea, const double* __restrict__ ec,
-                       const double* __restrict__ es, PoroConst k,
-                       const int64_t* __restrict__ ioff, double* __restrict__ cache) {
+                       const double* __restrict__ es, PoroConst k, int drained, int lstride,
+                       int lidx, const int64_t* __restrict__ ioff, double* __restrict__ cache) {
   __shared__ NearQueue nq[4];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   NearQueue& Q = nq[w];
@@ -803,7 +804,9 @@ poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __re
     const double2 zt = make_double2(ex[ti], ey[ti]);
     const double ctg = ec[ti], stg = es[ti];
     const double2 e2t = make_double2(ctg * ctg - stg * stg, 2.0 * ctg * stg);
-    double* blk0 = cache + ioff[it - item_lo];
+    // block (jpos, t) of lag slot lidx: ((jpos lstride + lidx) kTgtGroup + t) 9
+    double* blk0 = cache + ioff[it - item_lo] * lstride + (int64_t)lidx * kTgtGroup * 9;
+    const int64_t jstride = (int64_t)lstride * kTgtGroup * 9;
     int qn = 0;
     // queue entry: t = target slot, s = source element, j = 4 jpos + component
     auto desc = [&](int qi) {
@@ -824,7 +827,7 @@ poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __re
     };
     auto sink = [&](int qi, double2 T, double p) {
       const int comp = Q.j[qi] & 3, jpos = Q.j[qi] >> 2;
-      double* b = blk0 + ((int64_t)jpos * kTgtGroup + Q.t[qi]) * 9;
+      double* b = blk0 + jpos * jstride + Q.t[qi] * 9;
       b[comp] += T.y;
       b[3 + comp] += T.x;
       b[6 + comp] -= p;   // J: p_ABI = -p_formula
@@ -848,12 +851,24 @@ poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __re
         for (int comp = 0; comp < 3; ++comp) {
           bool near = false;
           if (have) {
-            sp[5] = comp == 0 ? 1.0 : 0.0;
-            sp[6] = comp == 1 ? 1.0 : 0.0;
-            sp[7] = comp == 2 ? 1.0 : 0.0;
+            const double Ds = comp == 0 ? 1.0 : 0.0, Dn = comp == 1 ? 1.0 : 0.0;
+            const double2 zc = make_double2(sp[0], sp[1]), e = make_double2(sp[2], sp[3]);
             double os = 0.0, on = 0.0, op = 0.0;
-            near = poro_pair_split(zt, e2t, sp, k, os, on, op);
-            double* bb = blk0 + ((int64_t)jpos * kTgtGroup + tl) * 9;
+            if (drained) {
+              const double2 Td = drained_traction(zt, zc, e, sp[4], Ds, Dn, k.gc, e2t);
+              os += Td.y;
+              on += Td.x;
+            }
+            near = poro_is_near(zt, zc, e, sp[4], k.ct);
+            if (!near) {   // analytic far form of the poroelastic part
+              double2 Tp;
+              double pp;
+              poro_element(zt, zc, e, sp[4], Ds, Dn, comp == 2 ? -1.0 : 0.0, k, e2t, Tp, pp);
+              os += Tp.y;
+              on += Tp.x;
+              op -= pp;   // J: p_ABI = -p_formula
+            }
+            double* bb = blk0 + jpos * jstride + tl * 9;
             bb[comp] = os;
             bb[3 + comp] = on;
             bb[6 + comp] = op;
@@ -937,6 +952,89 @@ poro_near_apply_kernel(int nown, const int* __restrict__ order, const int4* __re
       o[2] = s2;
     }
     __syncwarp();
+  }
+}
+
+// History near field from the lag cache:
+//   r_near(t) = sum_s sum_{j=1}^{h+1} K^p_ts(j dt) E_j(s),  E_j = D^(h+1-j) - D^(h-j)
+// with the cached blocks of every lag (the drained part cancels, sum_j E_j = 0).
+// Lags are stored in chunks of kLagChunk: in a chunk the blocks of one pair's
+// successive lags are adjacent ([item][jpos][lag][t][9]), so a lane streams
+// through contiguous memory and a warp touches few pages.  Warp per item,
+// lane = (target, source slice); per (pair, lag) 9 FMA on a 72-B block (HBM
+// bound).  Same partial layout as poro_hist_near_kernel.
+constexpr int kLagChunk = 16;
+constexpr int kHistWarps = 8;   // warps per item, splitting the lag chunks
+
+__global__ void __launch_bounds__(kHistWarps * 32)
+poro_hist_cached_kernel(const int* __restrict__ order, const int4* __restrict__ items,
+                        int item_lo, const int* __restrict__ u_off, const int* __restrict__ u_lo,
+                        const int* __restrict__ u_hi, const int* __restrict__ leaves,
+                        const int* __restrict__ c_start, const int* __restrict__ c_count,
+                        const double* __restrict__ Hs, int h, const int64_t* __restrict__ ioff,
+                        const double* const* __restrict__ chunks, double* __restrict__ part3) {
+  __shared__ double red[kHistWarps][3][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hs = (h + 2) * 3;
+  const int it = order[blockIdx.x];
+  const int4 item = items[it];
+  const int kk = item.x;
+  const int c = leaves[kk];
+  const int nt = min(kTgtGroup, c_start[c] + c_count[c] - item.y);
+  const int S = 32 / nt;
+  const int tl = lane % nt, slice = lane / nt;
+  const bool active = slice < S;
+  const int64_t off0 = ioff[it - item_lo] * kLagChunk;
+  double os = 0.0, on = 0.0, op = 0.0;
+  if (active) {
+    for (int l0 = w * kLagChunk; l0 <= h; l0 += kHistWarps * kLagChunk) {
+      const double* ch = chunks[l0 / kLagChunk] + off0;
+      const int ln = min(kLagChunk, h + 1 - l0);
+      int pos = 0;
+      for (int r = u_off[kk], rend = u_off[kk + 1]; r < rend && pos < item.w; ++r) {
+        const int lo = u_lo[r], len = u_hi[r] - lo;
+        const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
+        for (int j = b + slice; j < e; j += S) {
+          const double* bb0 =
+              ch + ((int64_t)(pos + j - item.z) * kLagChunk * kTgtGroup + tl) * 9;
+          // lags l = l0+1 .. l0+ln: E_l = D^(h+1-l) - D^(h-l) = H[h+2-l] - H[h+1-l]
+          const double* H = Hs + (int64_t)(lo + j) * hs + (h + 1 - l0) * 3;
+          double dp0 = __ldg(H), dp1 = __ldg(H + 1), dp2 = __ldg(H + 2);
+#pragma unroll 4
+          for (int li = 0; li < ln; ++li) {
+            const double* Db = H - 3 * (li + 1);
+            const double d0 = __ldg(Db), d1 = __ldg(Db + 1), d2 = __ldg(Db + 2);
+            const double e0 = dp0 - d0, e1 = dp1 - d1, e2 = dp2 - d2;
+            dp0 = d0;
+            dp1 = d1;
+            dp2 = d2;
+            const double* bb = bb0 + li * (kTgtGroup * 9);
+            os = fma(__ldg(bb + 0), e0, fma(__ldg(bb + 1), e1, fma(__ldg(bb + 2), e2, os)));
+            on = fma(__ldg(bb + 3), e0, fma(__ldg(bb + 4), e1, fma(__ldg(bb + 5), e2, on)));
+            op = fma(__ldg(bb + 6), e0, fma(__ldg(bb + 7), e1, fma(__ldg(bb + 8), e2, op)));
+          }
+        }
+        pos += len;
+      }
+    }
+  }
+  red[w][0][lane] = os;
+  red[w][1][lane] = on;
+  red[w][2][lane] = op;
+  __syncthreads();
+  if (w == 0 && lane < kTgtGroup) {   // fixed order: warps, then slices
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if (lane < nt)
+      for (int ww = 0; ww < kHistWarps; ++ww)
+        for (int q = 0; q < S; ++q) {
+          s0 += red[ww][0][lane + q * nt];
+          s1 += red[ww][1][lane + q * nt];
+          s2 += red[ww][2][lane + q * nt];
+        }
+    double* o = part3 + ((int64_t)it * kTgtGroup + lane) * 3;
+    o[0] = s0;
+    o[1] = s1;
+    o[2] = s2;
   }
 }
 
@@ -1298,6 +1396,30 @@ static bool key_eq(const double* a, const double* b) {
   return std::memcmp(a, b, 9 * sizeof(double)) == 0;
 }
 
+// Block offsets of the owned P2P items (window length x kTgtGroup x 9
+// doubles each), shared by the near-field cache and the history lag cache.
+static int item_block_offsets(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
+  if (t->nc_off) return DDM_OK;
+  const int nown = t->item_hi_owned - t->item_lo_owned;
+  std::vector<int4> it((size_t)nown);
+  DDM_CUDA(ctx, cudaMemcpyAsync(it.data(), t->items + t->item_lo_owned, nown * sizeof(int4),
+                                cudaMemcpyDeviceToHost, s));
+  DDM_CUDA(ctx, cudaStreamSynchronize(s));
+  std::vector<int64_t> off((size_t)nown);
+  int64_t tot = 0;
+  for (int i = 0; i < nown; ++i) {
+    off[i] = tot;
+    tot += (int64_t)(it[i].w - it[i].z) * kTgtGroup * 9;
+  }
+  int rc;
+  if ((rc = dalloc(ctx, &t->nc_off, (size_t)nown))) return rc;
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->nc_off, off.data(), nown * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, s));
+  DDM_CUDA(ctx, cudaStreamSynchronize(s));
+  t->nc_n = tot;
+  return DDM_OK;
+}
+
 // Near-field cache bookkeeping, called by fmm_matvec before any graph capture:
 // the blocks for these parameters are built on the second consecutive
 // poroelastic FMM matvec with them (a single matvec never pays the build),
@@ -1317,32 +1439,18 @@ int poro_near_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, c
   std::memcpy(t->nc_seen, key, sizeof(key));
   t->nc_seen_set = true;
   if (!repeat) return DDM_OK;
-  // block offsets of the owned items (window length x kTgtGroup x 9 doubles)
-  if (!t->nc_off) {
-    std::vector<int4> it((size_t)nown);
-    DDM_CUDA(ctx, cudaMemcpyAsync(it.data(), t->items + t->item_lo_owned, nown * sizeof(int4),
-                                  cudaMemcpyDeviceToHost, s));
-    DDM_CUDA(ctx, cudaStreamSynchronize(s));
-    std::vector<int64_t> off((size_t)nown);
-    int64_t tot = 0;
-    for (int i = 0; i < nown; ++i) {
-      off[i] = tot;
-      tot += (int64_t)(it[i].w - it[i].z) * kTgtGroup * 9;
-    }
+  int rc;
+  if ((rc = item_block_offsets(ctx, t, s))) return rc;
+  if (!t->nc) {
     size_t fr = 0, total = 0;
     DDM_CUDA(ctx, cudaMemGetInfo(&fr, &total));
-    if ((size_t)tot * sizeof(double) > fr / 2) return DDM_OK;   // does not fit: on the fly
-    int rc;
-    if ((rc = dalloc(ctx, &t->nc_off, (size_t)nown)) || (rc = dalloc(ctx, &t->nc, (size_t)tot)))
-      return rc;
-    DDM_CUDA(ctx, cudaMemcpyAsync(t->nc_off, off.data(), nown * sizeof(int64_t),
-                                  cudaMemcpyHostToDevice, s));
-    t->nc_n = tot;
+    if ((size_t)t->nc_n * sizeof(double) > fr / 2) return DDM_OK;   // does not fit: on the fly
+    if ((rc = dalloc(ctx, &t->nc, (size_t)t->nc_n))) return rc;
   }
   t->nc_valid = false;
   poro_near_build_kernel<<<nblk(nown, 4), 128, 0, s>>>(
       nown, t->p2p_order, t->items, t->item_lo_owned, t->u_off, t->u_lo, t->u_hi, t->leaves,
-      t->c_start, t->c_count, t->ex, t->ey, t->ea, t->ec, t->es, k, t->nc_off, t->nc);
+      t->c_start, t->c_count, t->ex, t->ey, t->ea, t->ec, t->es, k, 1, 1, 0, t->nc_off, t->nc);
   DDM_CUDA(ctx, cudaGetLastError());
   DDM_CUDA(ctx, cudaStreamSynchronize(s));
   std::memcpy(t->nc_key, key, sizeof(key));
@@ -1368,6 +1476,101 @@ int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, con
   poro_p2p_kernel<<<nblk(item_hi - item_lo, 4), 128, 0, s>>>(
       item_hi - item_lo, t->p2p_order, t->items, t->u_off, t->u_lo, t->u_hi, t->leaves, t->c_start, t->c_count,
       t->src, t->ex, t->ey, t->ec, t->es, to_const(P), reinterpret_cast<double*>(t->part));
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+// History lag cache bookkeeping (fmm_history, outside any capture): for the
+// (material, dt) of a history sum requested twice in a row, the blocks of
+// lags 1..h+1 are built (missing lags only, as the history grows) while the
+// device keeps a quarter of its memory free; returns true when every lag the
+// call needs is cached.  DDM_HIST_CACHE=0 disables.
+bool poro_hist_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt,
+                            int h, cudaStream_t s, int* rc_out) {
+  *rc_out = DDM_OK;
+  static const bool off = [] {
+    const char* e = getenv("DDM_HIST_CACHE");
+    return e && e[0] == '0';
+  }();
+  const int nown = t->item_hi_owned - t->item_lo_owned;
+  if (off || nown <= 0 || h < 1) return false;
+  double key[9];
+  const_key(to_const(poro_params(mat, dt)), key);
+  if (!(t->hc_valid && key_eq(key, t->hc_key))) {
+    const bool repeat = t->hc_seen_set && key_eq(key, t->hc_seen);
+    std::memcpy(t->hc_seen, key, sizeof(key));
+    t->hc_seen_set = true;
+    if (!repeat) return false;
+    for (double* p : t->hc_lag) cudaFree(p);
+    t->hc_lag.clear();
+    t->hc_nlags = 0;
+    // chunk budget, fixed at creation (no memory queries while the history
+    // grows): chunks that keep a quarter of the device memory free
+    int rc;
+    if ((rc = item_block_offsets(ctx, t, s))) {
+      *rc_out = rc;
+      return false;
+    }
+    size_t fr = 0, total = 0;
+    DDM_CUDA(ctx, cudaMemGetInfo(&fr, &total));
+    const size_t cbytes = (size_t)t->nc_n * kLagChunk * sizeof(double);
+    t->hc_max_chunks = fr > total / 4 && cbytes > 0 ? (int)((fr - total / 4) / cbytes) : 0;
+    std::memcpy(t->hc_key, key, sizeof(key));
+    t->hc_valid = true;
+    t->hc_capped = false;
+  }
+  if (t->hc_nlags < h + 1 && !t->hc_capped) {
+    int rc;
+    while (t->hc_nlags < h + 1) {
+      const int j = t->hc_nlags + 1;
+      const int ci = (j - 1) / kLagChunk;
+      if (ci == (int)t->hc_lag.size()) {
+        if (ci >= t->hc_max_chunks) {   // memory budget reached: on the fly from here on
+          t->hc_capped = true;
+          break;
+        }
+        // plain cudaMalloc (~4 ms at any size); growing the stream-ordered
+        // pool by a chunk stalled the host for 10-800 ms (scripts/micro/alloc.cu)
+        double* blk = nullptr;
+        if ((rc = dalloc(ctx, &blk, (size_t)t->nc_n * kLagChunk))) {
+          *rc_out = rc;
+          return false;
+        }
+        t->hc_lag.push_back(blk);
+      }
+      poro_near_build_kernel<<<nblk(nown, 4), 128, 0, s>>>(
+          nown, t->p2p_order, t->items, t->item_lo_owned, t->u_off, t->u_lo, t->u_hi, t->leaves,
+          t->c_start, t->c_count, t->ex, t->ey, t->ea, t->ec, t->es,
+          to_const(poro_params(mat, j * dt)), 0, kLagChunk, (j - 1) % kLagChunk, t->nc_off,
+          t->hc_lag[ci]);
+      DDM_CUDA(ctx, cudaGetLastError());
+      t->hc_nlags = j;
+    }
+    if (t->hc_ptrs_n < (int)t->hc_lag.size()) {
+      if (t->hc_ptrs) cudaFree(t->hc_ptrs);
+      t->hc_ptrs = nullptr;
+      t->hc_ptrs_n = 0;
+      const int cap = std::max(2 * (int)t->hc_lag.size(), 64);
+      if ((rc = dalloc(ctx, &t->hc_ptrs, (size_t)cap))) {
+        *rc_out = rc;
+        return false;
+      }
+      t->hc_ptrs_n = cap;
+    }
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->hc_ptrs, t->hc_lag.data(), t->hc_lag.size() * sizeof(double*),
+                                  cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaStreamSynchronize(s));
+  }
+  return t->hc_nlags >= h + 1;
+}
+
+int launch_poro_hist_cached(ddm_ctx_s* ctx, ddm_tree_s* t, int h, const double* Hs,
+                            cudaStream_t s) {
+  const int nown = t->item_hi_owned - t->item_lo_owned;
+  if (nown <= 0) return DDM_OK;
+  poro_hist_cached_kernel<<<nown, kHistWarps * 32, 0, s>>>(
+      t->p2p_order, t->items, t->item_lo_owned, t->u_off, t->u_lo, t->u_hi, t->leaves,
+      t->c_start, t->c_count, Hs, h, t->nc_off, t->hc_ptrs, reinterpret_cast<double*>(t->part));
   DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;
 }

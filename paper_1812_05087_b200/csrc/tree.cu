@@ -523,6 +523,9 @@ void free_tree(ddm_tree_s* t) {
                   t->pc_chunks, t->pc_off, t->pcl, t->st_elem, t->st_code, t->rbeg, t->srec, t->nc, t->nc_off};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (double* p : t->hc_lag)
+    if (p) cudaFree(p);
+  if (t->hc_ptrs) cudaFree(t->hc_ptrs);
   for (auto& g : t->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
 }

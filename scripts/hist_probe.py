@@ -29,3 +29,10 @@ for _ in range(30):
     evs.append(round(e0.elapsed_time(e1), 2))
 print("wall", walls)
 print("events", evs)
+# per-stage events of repeated history applications (profiling mode, concurrent)
+ctx.set_profiling(True)
+for _ in range(12):
+    D.history_rhs(ctx, tree, mat, dt, Dh[:9], b, rhs)
+    torch.cuda.synchronize()
+    print({k: round(v, 2) for k, v in ctx.stage_times().items() if v > 0})
+ctx.set_profiling(False)
