@@ -232,6 +232,10 @@ struct ddm_tree_s {
   double* gm_tmp = nullptr;
   double* gm_part = nullptr;
   int64_t gm_part_n = 0;
+  // device Arnoldi state of the batched GMRES (gmres.cu): packed Hessenberg,
+  // Givens rotations, rotated rhs, per-step estimates, 1/h(k+1,k), flags
+  double* gm_dev = nullptr;
+  int gm_dev_m = 0;
 };
 
 namespace ddm {

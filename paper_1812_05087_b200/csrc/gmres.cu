@@ -276,6 +276,52 @@ chunk_apply(const int2* __restrict__ chunks, const int64_t* __restrict__ off, in
   }
 }
 
+// One Arnoldi step's small work on the device (batched GMRES, no host round
+// trip per iteration).  dh = [h1 (k+1) | h2 (k+1) | -- | ||w||^2] of the CGS2
+// passes; column k of the packed Hessenberg Hp(i, k) = Hp[k (k+3)/2 + i]
+// becomes h1 + h2 with h(k+1,k) = ||w||, the previous Givens rotations are
+// applied, a new one zeroes h(k+1,k), and the rotated rhs g gives the
+// residual estimate est[k] = |g[k+1]|.  scal[0] = 1/h(k+1,k) (0 on
+// breakdown, which also sets flag[0] = k + 1 and makes later steps no-ops).
+// One thread: O(k) work.
+__global__ void arnoldi_finish(int k, const double* __restrict__ dh, double* __restrict__ Hp,
+                               double* __restrict__ cs, double* __restrict__ sn,
+                               double* __restrict__ g, double* __restrict__ est,
+                               double* __restrict__ scal, int* __restrict__ flag) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (flag[0]) {   // broken down earlier: nothing to add
+    est[k] = est[k > 0 ? k - 1 : 0];
+    scal[0] = 0.0;
+    return;
+  }
+  double* col = Hp + (size_t)k * (k + 3) / 2;
+  for (int i = 0; i <= k; ++i) col[i] = dh[i] + dh[k + 1 + i];
+  const double hn = sqrt(dh[2 * (k + 1) + 1]);
+  for (int i = 0; i < k; ++i) {
+    const double a = col[i], b = col[i + 1];
+    col[i] = cs[i] * a + sn[i] * b;
+    col[i + 1] = -sn[i] * a + cs[i] * b;
+  }
+  const double a = col[k], b = hn;
+  const double den = hypot(a, b);
+  cs[k] = a / den;
+  sn[k] = b / den;
+  col[k] = den;
+  col[k + 1] = 0.0;
+  g[k + 1] = -sn[k] * g[k];
+  g[k] = cs[k] * g[k];
+  est[k] = fabs(g[k + 1]);
+  scal[0] = hn > 0.0 ? 1.0 / hn : 0.0;
+  if (!(hn > 0.0)) flag[0] = k + 1;
+}
+
+// dst = a[0] * src with a device scalar
+__global__ void scale_copy_dev(const double* __restrict__ src, const double* __restrict__ a,
+                               double* __restrict__ dst, int64_t len) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < len) dst[j] = a[0] * src[j];
+}
+
 struct Gm {
   ddm_ctx_s* ctx;
   ddm_tree_s* t;
@@ -486,6 +532,32 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   double* xt = t->gm_w + 5 * nfull;   // trial iterate (true-residual check)
   double* V = t->krylov;
   Gm g{ctx, t, s, ncomp, nloc, lo, t->gm_part, t->gm_part_n, t->gm_tmp};
+  // DDM_GMRES_SYNC=1: the host takes every Arnoldi step's decisions (Givens,
+  // DGKS reorthogonalisation); default: batched device-side steps
+  static const bool sync_mode = [] {
+    const char* e = getenv("DDM_GMRES_SYNC");
+    return e && e[0] == '1';
+  }();
+  static const int batch = [] {
+    const char* e = getenv("DDM_GMRES_BATCH");
+    return e ? std::max(1, atoi(e)) : 8;
+  }();
+  const size_t hp_n = (size_t)(m + 1) * (m + 4) / 2;
+  const int dev_need = (int)std::min<size_t>(hp_n + 4 * (size_t)m + 8, (size_t)INT32_MAX);
+  if (!sync_mode && t->gm_dev_m < dev_need) {
+    if (t->gm_dev) cudaFree(t->gm_dev);
+    t->gm_dev = nullptr;
+    t->gm_dev_m = 0;
+    if ((rc = dalloc(ctx, &t->gm_dev, (size_t)dev_need))) return rc;
+    t->gm_dev_m = dev_need;
+  }
+  double* Hd = t->gm_dev;
+  double* csd = Hd + hp_n;
+  double* snd = csd + m;
+  double* gd = snd + m;
+  double* estd = gd + m + 1;
+  double* scald = estd + m;
+  int* flagd = reinterpret_cast<int*>(scald + 2);
 
   gather_sorted<<<nblk(n, 256), 256, 0, s>>>(n, ncomp, t->perm, b_user, bs);
   gather_sorted<<<nblk(n, 256), 256, 0, s>>>(n, ncomp, t->perm, x_user, xs);
@@ -597,6 +669,95 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
     double inner = tol;   // estimate target (relative), tightened when the true residual lags
     gv[0] = beta;
     int kdone = 0;
+    if (!sync_mode) {
+      // batched: the Arnoldi steps queue back to back on the stream; the
+      // host reads the residual estimates every `batch` steps and picks the
+      // first step that met the target (later steps of the batch are
+      // discarded work, not counted as iterations)
+      const int it0 = iters;
+      std::vector<double> g0(m + 1, 0.0);
+      g0[0] = beta;
+      DDM_CUDA(ctx, cudaMemcpyAsync(gd, g0.data(), (m + 1) * sizeof(double), cudaMemcpyHostToDevice, s));
+      DDM_CUDA(ctx, cudaMemsetAsync(flagd, 0, sizeof(int), s));
+      std::vector<double> hest(batch);
+      int kb = 0;
+      bool stop = false;
+      // H and g of the first kd steps from the device (for form_x)
+      auto fetch_state = [&](int kd) -> int {
+        const size_t hn_ = (size_t)kd * (kd + 3) / 2;
+        if (Hp.size() < hn_) Hp.resize(hn_);
+        DDM_CUDA(ctx, cudaMemcpyAsync(Hp.data(), Hd, hn_ * sizeof(double), cudaMemcpyDeviceToHost, s));
+        DDM_CUDA(ctx, cudaMemcpyAsync(gv.data(), gd, (kd + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        DDM_CUDA(ctx, cudaStreamSynchronize(s));
+        return DDM_OK;
+      };
+      for (int k = 0; k < m && iters < max_iter; ++k) {
+        const double* vk = V + (int64_t)k * nloc;
+        const double* vin = vk;
+        if (ctx->world > 1) {
+          DDM_CUDA(ctx, cudaMemcpyAsync(vf + lo, vk, nloc * sizeof(double), cudaMemcpyDeviceToDevice, s));
+          if ((rc = allgather_sorted(ctx, t, vf, ncomp, s))) return rc;
+          vin = vf;
+        }
+        if ((rc = apply(vin))) return rc;
+        double* w = wf + lo;
+        // CGS2 (two classical Gram-Schmidt passes, no host decision)
+        const int o_w1 = 2 * (k + 1) + 1;
+        if ((rc = g.dots(V, nloc, k + 1, w, 0))) return rc;
+        if ((rc = g.axpy(V, nloc, k + 1, g.dh, -1.0, w))) return rc;
+        if ((rc = g.dots(V, nloc, k + 1, w, k + 1))) return rc;
+        if ((rc = g.axpy(V, nloc, k + 1, g.dh + k + 1, -1.0, w))) return rc;
+        if ((rc = g.dots(w, 0, 1, w, o_w1))) return rc;
+        arnoldi_finish<<<1, 32, 0, s>>>(k, g.dh, Hd, csd, snd, gd, estd, scald, flagd);
+        scale_copy_dev<<<nblk(nloc, 256), 256, 0, s>>>(w, scald, V + (int64_t)(k + 1) * nloc, nloc);
+        DDM_CUDA(ctx, cudaGetLastError());
+        ++iters;
+        kdone = k + 1;
+        if (k + 1 - kb < batch && k + 1 < m && iters < max_iter) continue;
+        int hflag = 0;
+        DDM_CUDA(ctx, cudaMemcpyAsync(hest.data(), estd + kb, (k + 1 - kb) * sizeof(double),
+                                      cudaMemcpyDeviceToHost, s));
+        DDM_CUDA(ctx, cudaMemcpyAsync(&hflag, flagd, sizeof(int), cudaMemcpyDeviceToHost, s));
+        DDM_CUDA(ctx, cudaStreamSynchronize(s));
+        for (int kk = kb; kk <= k; ++kk) {
+          const bool brk = hflag && kk + 1 >= hflag;   // h(kk+1, kk) = 0
+          const bool est_ok = hest[kk - kb] <= inner * bnorm;
+          if (!est_ok && !brk) continue;
+          const int it_kk = it0 + kk + 1;
+          if (est_ok && !brk && kk + 1 < m && it_kk < max_iter) {
+            // the estimate says converged: check the true residual without
+            // ending the cycle (as in the synchronous path)
+            if ((rc = fetch_state(kk + 1)) || (rc = form_x(kk + 1, xt))) return rc;
+            if ((rc = apply_plain(xt))) return rc;
+            sub_scale<<<nblk(nloc, 256), 256, 0, s>>>(bs + lo, wf + lo, uf + lo, nloc);
+            DDM_CUDA(ctx, cudaGetLastError());
+            if ((rc = g.dots(uf + lo, 0, 1, uf + lo, 0)) || (rc = fetch(1))) return rc;
+            const double tr = std::sqrt(hh[0]);
+            if (trace)
+              fprintf(stderr, "[gmres] iters %d estimate %.3e true %.3e\n", it_kk,
+                      hest[kk - kb] / bnorm, tr / bnorm);
+            if (tr <= tol * bnorm) {
+              DDM_CUDA(ctx, cudaMemcpyAsync(xs, xt, nfull * sizeof(double), cudaMemcpyDeviceToDevice, s));
+              rel = tr / bnorm;
+              converged = accepted = true;
+              iters = it_kk;
+              break;
+            }
+            inner = std::min(inner, hest[kk - kb] / bnorm) * 0.5 * (tol * bnorm / tr);
+            continue;
+          }
+          // end of the cycle at step kk (estimate met at the cycle's end or
+          // max_iter, or breakdown): restart from x + M^-1 V y
+          kdone = kk + 1;
+          iters = it_kk;
+          stop = true;
+          break;
+        }
+        kb = k + 1;
+        if (accepted || stop) break;
+      }
+      if (!accepted && (rc = fetch_state(kdone))) return rc;
+    } else
     for (int k = 0; k < m; ++k) {
       const double* vk = V + (int64_t)k * nloc;
       const double* vin = vk;
