@@ -36,6 +36,7 @@ namespace {
     case 20: F(20); break;                \
     case 24: F(24); break;                \
     case 28: F(28); break;                \
+    case 30: F(30); break;                \
     case 32: F(32); break;                \
     default: F(0); break;                 \
   }
@@ -862,7 +863,7 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   if (t->nlevels <= 2) return DDM_OK;
   const int p = t->p;
   const int c0 = t->level_off[2], c1 = t->ncells;
-  const bool tc = (p == 8 || p == 12 || p == 16 || p == 20 || p == 24 || p == 28 || p == 32);
+  const bool tc = (p == 8 || p == 12 || p == 16 || p == 20 || p == 24 || p == 28 || p == 30 || p == 32);
   const size_t ndbl = tc ? (size_t)((p + 7) / 8) * ((p + 4) / 4) * 32 : (size_t)(p + 1) * p;
   const size_t wstride = tc ? (size_t)2 * kM2LBatch * kXStride : 3 * (size_t)p + 1;
   const size_t shm = ((tc ? 0 : (size_t)kNOffsets * (p + 2)) + (ndbl + 1) / 2 +

@@ -894,64 +894,66 @@ poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __re
   }
 }
 
-// y_near = blocks x D per owned item (warp per item, lane = (target, slice)),
-// the same partial layout as poro_p2p_kernel
-__global__ void __launch_bounds__(128)
-poro_near_apply_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ items,
+// y_near = blocks x D per owned item: block per item, its kApplyWarps warps
+// take interleaved groups of the source positions, lane = (target, slice);
+// partials reduced in a fixed order (deterministic).  Same partial layout as
+// poro_p2p_kernel.
+constexpr int kApplyWarps = 8;
+
+__global__ void __launch_bounds__(kApplyWarps * 32)
+poro_near_apply_kernel(const int* __restrict__ order, const int4* __restrict__ items,
                        int item_lo, const int* __restrict__ u_off, const int* __restrict__ u_lo,
                        const int* __restrict__ u_hi, const int* __restrict__ leaves,
                        const int* __restrict__ c_start, const int* __restrict__ c_count,
                        const double* __restrict__ src, const int64_t* __restrict__ ioff,
                        const double* __restrict__ cache, double* __restrict__ part3) {
-  __shared__ double red[4][3][32];
+  __shared__ double red[kApplyWarps][3][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int oi = blockIdx.x * 4 + w; oi < nown; oi += gridDim.x * 4) {
-    const int it = order[oi];
-    const int4 item = items[it];
-    const int kk = item.x;
-    const int c = leaves[kk];
-    const int nt = min(kTgtGroup, c_start[c] + c_count[c] - item.y);
-    const int S = 32 / nt;
-    const int tl = lane % nt, slice = lane / nt;
-    const bool active = slice < S;
-    const double* blk0 = cache + ioff[it - item_lo];
-    double os = 0.0, on = 0.0, op = 0.0;
-    if (active) {
-      int pos = 0;
-      for (int r = u_off[kk], rend = u_off[kk + 1]; r < rend && pos < item.w; ++r) {
-        const int lo = u_lo[r], len = u_hi[r] - lo;
-        const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
-#pragma unroll 4
-        for (int j = b + slice; j < e; j += S) {
-          const int jpos = pos + j - item.z;
-          const double* bb = blk0 + ((int64_t)jpos * kTgtGroup + tl) * 9;
-          const double* d = src + (int64_t)(lo + j) * kPoroStride + 5;
-          const double d0 = __ldg(d), d1 = __ldg(d + 1), d2 = __ldg(d + 2);
-          os = fma(__ldg(bb + 0), d0, fma(__ldg(bb + 1), d1, fma(__ldg(bb + 2), d2, os)));
-          on = fma(__ldg(bb + 3), d0, fma(__ldg(bb + 4), d1, fma(__ldg(bb + 5), d2, on)));
-          op = fma(__ldg(bb + 6), d0, fma(__ldg(bb + 7), d1, fma(__ldg(bb + 8), d2, op)));
-        }
-        pos += len;
+  const int it = order[blockIdx.x];
+  const int4 item = items[it];
+  const int kk = item.x;
+  const int c = leaves[kk];
+  const int nt = min(kTgtGroup, c_start[c] + c_count[c] - item.y);
+  const int S = 32 / nt;
+  const int tl = lane % nt, slice = lane / nt;
+  const bool active = slice < S;
+  const double* blk0 = cache + ioff[it - item_lo];
+  double os = 0.0, on = 0.0, op = 0.0;
+  if (active) {
+    int pos = 0;
+    for (int r = u_off[kk], rend = u_off[kk + 1]; r < rend && pos < item.w; ++r) {
+      const int lo = u_lo[r], len = u_hi[r] - lo;
+      const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
+#pragma unroll 2
+      for (int j = b + slice + S * w; j < e; j += S * kApplyWarps) {
+        const int jpos = pos + j - item.z;
+        const double* bb = blk0 + ((int64_t)jpos * kTgtGroup + tl) * 9;
+        const double* d = src + (int64_t)(lo + j) * kPoroStride + 5;
+        const double d0 = __ldg(d), d1 = __ldg(d + 1), d2 = __ldg(d + 2);
+        os = fma(__ldg(bb + 0), d0, fma(__ldg(bb + 1), d1, fma(__ldg(bb + 2), d2, os)));
+        on = fma(__ldg(bb + 3), d0, fma(__ldg(bb + 4), d1, fma(__ldg(bb + 5), d2, on)));
+        op = fma(__ldg(bb + 6), d0, fma(__ldg(bb + 7), d1, fma(__ldg(bb + 8), d2, op)));
       }
-      red[w][0][lane] = os;
-      red[w][1][lane] = on;
-      red[w][2][lane] = op;
+      pos += len;
     }
-    __syncwarp();
-    if (lane < kTgtGroup) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      if (lane < nt)
+  }
+  red[w][0][lane] = os;
+  red[w][1][lane] = on;
+  red[w][2][lane] = op;
+  __syncthreads();
+  if (w == 0 && lane < kTgtGroup) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if (lane < nt)
+      for (int ww = 0; ww < kApplyWarps; ++ww)
         for (int q = 0; q < S; ++q) {
-          s0 += red[w][0][lane + q * nt];
-          s1 += red[w][1][lane + q * nt];
-          s2 += red[w][2][lane + q * nt];
+          s0 += red[ww][0][lane + q * nt];
+          s1 += red[ww][1][lane + q * nt];
+          s2 += red[ww][2][lane + q * nt];
         }
-      double* o = part3 + ((int64_t)it * kTgtGroup + lane) * 3;
-      o[0] = s0;
-      o[1] = s1;
-      o[2] = s2;
-    }
-    __syncwarp();
+    double* o = part3 + ((int64_t)it * kTgtGroup + lane) * 3;
+    o[0] = s0;
+    o[1] = s1;
+    o[2] = s2;
   }
 }
 
@@ -1466,8 +1468,8 @@ int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, con
   const_key(k, key);
   if (t->nc_valid && key_eq(key, t->nc_key) && item_lo == t->item_lo_owned &&
       item_hi == t->item_hi_owned) {
-    poro_near_apply_kernel<<<nblk(item_hi - item_lo, 4), 128, 0, s>>>(
-        item_hi - item_lo, t->p2p_order, t->items, t->item_lo_owned, t->u_off, t->u_lo, t->u_hi,
+    poro_near_apply_kernel<<<item_hi - item_lo, kApplyWarps * 32, 0, s>>>(
+        t->p2p_order, t->items, t->item_lo_owned, t->u_off, t->u_lo, t->u_hi,
         t->leaves, t->c_start, t->c_count, t->src, t->nc_off, t->nc,
         reinterpret_cast<double*>(t->part));
     DDM_CUDA(ctx, cudaGetLastError());
