@@ -231,6 +231,27 @@ int ddm_farfield_rhs(ddm_ctx_t ctx, const double* beta, int64_t n, int ncomp, do
 int ddm_sif(ddm_ctx_t ctx, const double* w_tip, const double* ds_tip, const double* a_tip,
             int ntips, double E, double nu, double* KI, double* KII, void* stream);
 
+/* Fracture propagation step (Fig. 8 branch: "a fracture
+ * propagation criterion may be used ... an element will be added to the
+ * model if propagation happens, and in that case the quad-tree needs to be
+ * constructed again").  The paper names no criterion; reading
+ * R23: maximum tangential stress (Erdogan-Sih) in each tip's
+ * outward frame, kink angle theta = 2 atan((K_I - sqrt(K_I^2 + 8 K_II^2)) /
+ * (4 K_II)) (0 when K_II = 0), K_eq = cos(theta/2) (K_I cos^2(theta/2) -
+ * 3/2 K_II sin theta); a tip grows when K_I > 0 and K_eq >= K_IC, by one
+ * element of the tip element's length along phi = outward angle + theta.
+ * Per tip i (all arrays [device], length ntips): KI, KII (ddm_sif); the tip
+ * element's centre (x, y), half-length a, angle beta in [0, pi) and end
+ * (1: its (x, y) + a e^{i beta} endpoint is the tip, 0: the - endpoint).
+ * Outputs: grow[i] (0/1) and, where grow[i] = 1, the new element (new_x,
+ * new_y, new_a, new_beta in [0, pi)) and its outward end new_end.  The caller
+ * appends the new elements and rebuilds the tree (ddm_build_tree).  Errors:
+ * DDM_ERR_ARG for NULL arrays with ntips > 0 or K_IC < 0. */
+int ddm_tip_growth(ddm_ctx_t ctx, int ntips, const double* KI, const double* KII,
+                   const double* x, const double* y, const double* a, const double* beta,
+                   const int* end, double K_IC, int* grow, double* new_x, double* new_y,
+                   double* new_a, double* new_beta, int* new_end, void* stream);
+
 /* Per-stage timings of the last ddm_matvec on this tree (CUDA events, ms),
  * written into ms[DDM_NSTAGES] [host] when profiling is enabled
  * (ddm_set_profiling).  Stages: prep, p2m, m2m, m2l, l2l, p2p, finalize (near +

@@ -22,8 +22,10 @@ from .api import (  # noqa: F401
     precond_apply,
     sif,
     split_costs,
+    tip_growth,
 )
 
 from .march import march  # noqa: F401,E402
+from .propagate import propagate  # noqa: F401,E402
 
 __version__ = "0.1.0"

@@ -77,6 +77,8 @@ ddm_precond_apply = _proto("ddm_precond_apply", _i, _vp, _vp, C.POINTER(Material
 ddm_farfield_rhs = _proto("ddm_farfield_rhs", _i, _vp, _dp, _i64, _i, _d, _d, _d, _i, _d, _dp,
                           _vp)
 ddm_sif = _proto("ddm_sif", _i, _vp, _dp, _dp, _dp, _i, _d, _d, _dp, _dp, _vp)
+ddm_tip_growth = _proto("ddm_tip_growth", _i, _vp, _i, _dp, _dp, _dp, _dp, _dp, _dp, _vp, _d,
+                        _vp, _dp, _dp, _dp, _dp, _vp, _vp)
 ddm_set_profiling = _proto("ddm_set_profiling", _i, _vp, _i)
 ddm_stage_times = _proto("ddm_stage_times", _i, _vp, C.POINTER(_d))
 
@@ -84,5 +86,5 @@ EXPORTED = ["ddm_version", "ddm_last_error", "ddm_nccl_unique_id", "ddm_ctx_crea
             "ddm_ctx_destroy", "ddm_build_tree", "ddm_tree_free", "ddm_tree_counts",
             "ddm_tree_export", "ddm_tree_partition", "ddm_split_costs", "ddm_matvec",
             "ddm_history_apply", "ddm_history_rhs", "ddm_gmres_solve", "ddm_precond_apply",
-            "ddm_farfield_rhs", "ddm_sif",
+            "ddm_farfield_rhs", "ddm_sif", "ddm_tip_growth",
             "ddm_set_profiling", "ddm_stage_times"]

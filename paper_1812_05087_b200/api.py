@@ -266,6 +266,23 @@ def sif(ctx, w_tip: torch.Tensor, ds_tip: torch.Tensor, a_tip: torch.Tensor, E: 
     return KI, KII
 
 
+def tip_growth(ctx, KI: torch.Tensor, KII: torch.Tensor, x: torch.Tensor, y: torch.Tensor,
+               a: torch.Tensor, beta: torch.Tensor, end: torch.Tensor, K_IC: float, stream=None):
+    """ddm_tip_growth (Fig. 8 branch, reading R23): per tip, grow flag
+    and the new element (x, y, a, beta, outward end) of the tips that grow."""
+    n = KI.numel()
+    grow = torch.empty(n, dtype=torch.int32, device=KI.device)
+    ne = torch.empty(n, dtype=torch.int32, device=KI.device)
+    nx, ny, na, nb = (torch.empty_like(KI) for _ in range(4))
+    ctx.check(L.ddm_tip_growth(ctx._h, int(n), _dev(KI, "KI"), _dev(KII, "KII"), _dev(x, "x"),
+                               _dev(y, "y"), _dev(a, "a"), _dev(beta, "beta"),
+                               _dev(end, "end", torch.int32), float(K_IC),
+                               _dev(grow, "grow", torch.int32), _dev(nx, "nx"), _dev(ny, "ny"),
+                               _dev(na, "na"), _dev(nb, "nb"), _dev(ne, "ne", torch.int32),
+                               _stream_ptr(stream)))
+    return grow, nx, ny, na, nb, ne
+
+
 def split_costs(prefix_excl: np.ndarray, total: int, world: int) -> np.ndarray:
     """Host-only leaf partition (ddm_split_costs); no GPU needed."""
     pre = np.ascontiguousarray(prefix_excl, dtype=np.int64)

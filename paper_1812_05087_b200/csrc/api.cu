@@ -74,6 +74,38 @@ __global__ void sif_kernel(const double* __restrict__ w, const double* __restric
 }
 
 // DFMA throughput probe: 8 independent FMA chains per thread.
+// Maximum-tangential-stress growth of one tip (ddm_tip_growth, reading R23)
+__global__ void tip_growth_kernel(int ntips, const double* __restrict__ KI,
+                                  const double* __restrict__ KII, const double* __restrict__ x,
+                                  const double* __restrict__ y, const double* __restrict__ a,
+                                  const double* __restrict__ beta, const int* __restrict__ end,
+                                  double kic, int* __restrict__ grow, double* __restrict__ nx,
+                                  double* __restrict__ ny, double* __restrict__ na,
+                                  double* __restrict__ nb, int* __restrict__ ne) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntips) return;
+  const double k1 = KI[i], k2 = KII[i];
+  const double th = k2 == 0.0 ? 0.0 : 2.0 * atan((k1 - sqrt(k1 * k1 + 8.0 * k2 * k2)) / (4.0 * k2));
+  const double ch = cos(0.5 * th);
+  const double keq = ch * (k1 * ch * ch - 1.5 * k2 * sin(th));
+  const int g = (k1 > 0.0 && keq >= kic) ? 1 : 0;
+  grow[i] = g;
+  if (!g) return;
+  const double b = beta[i], ai = a[i];
+  const double sgn = end[i] ? 1.0 : -1.0;
+  const double ex = x[i] + sgn * ai * cos(b), ey = y[i] + sgn * ai * sin(b);   // tip point
+  double phi = (end[i] ? b : b + M_PI) + th;                                   // growth direction
+  phi = fmod(phi, 2.0 * M_PI);
+  if (phi < 0.0) phi += 2.0 * M_PI;
+  nx[i] = ex + ai * cos(phi);
+  ny[i] = ey + ai * sin(phi);
+  na[i] = ai;
+  // beta in [0, pi); the outward end is + e^{i beta} when phi < pi
+  const bool up = phi < M_PI;
+  nb[i] = up ? phi : phi - M_PI;
+  ne[i] = up ? 1 : 0;
+}
+
 __global__ void dfma_probe_kernel(int iters, double a, double b, double* out) {
   double x[8];
 #pragma unroll
@@ -580,6 +612,22 @@ int ddm_sif(ddm_ctx_t ctx, const double* w_tip, const double* ds_tip, const doub
   if (ntips == 0) return DDM_OK;
   sif_kernel<<<nblk(ntips, 128), 128, 0, (cudaStream_t)stream>>>(w_tip, ds_tip, a_tip, ntips, E,
                                                                  nu, KI, KII);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+int ddm_tip_growth(ddm_ctx_t ctx, int ntips, const double* KI, const double* KII,
+                   const double* x, const double* y, const double* a, const double* beta,
+                   const int* end, double K_IC, int* grow, double* new_x, double* new_y,
+                   double* new_a, double* new_beta, int* new_end, void* stream) {
+  if (!ctx) return DDM_ERR_ARG;
+  if (ntips < 0 || !(K_IC >= 0.0) ||
+      (ntips && (!KI || !KII || !x || !y || !a || !beta || !end || !grow || !new_x || !new_y ||
+                 !new_a || !new_beta || !new_end)))
+    return set_error(ctx, DDM_ERR_ARG, "bad argument");
+  if (ntips == 0) return DDM_OK;
+  tip_growth_kernel<<<nblk(ntips, 128), 128, 0, (cudaStream_t)stream>>>(
+      ntips, KI, KII, x, y, a, beta, end, K_IC, grow, new_x, new_y, new_a, new_beta, new_end);
   DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;
 }
