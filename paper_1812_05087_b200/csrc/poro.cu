@@ -158,6 +158,51 @@ __device__ __forceinline__ void point_add(double wx, double wy, double wq, const
   d2_acc.y = fma(wq, d2.y, d2_acc.y);
 }
 
+// point_add for the three unit source columns at once (near-field block
+// builds): column 0 = unit D_s (K0 = -4 k_p i G C e^2), column 1 = unit D_n
+// (K1 = i K0, mu = -eta/S), column 2 = unit q_ABI (q_formula = -1).  The
+// kernel functions of the node (f2, g2, h2, e^-u, E1) are evaluated once.
+__device__ __forceinline__ void point_add3(double wx, double wy, double wq, const PoroConst& k,
+                                           double2 K0, double mu1, bool q_split, double* p_acc,
+                                           double2* d2_acc) {
+  const double r2 = fma(wx, wx, wy * wy);
+  const double u = r2 / (4.0 * k.ct);
+  const double ir = rsqrt(r2);
+  const double obx = wx * ir, oby = -wy * ir;
+  const double2 ob2 = make_double2(obx * obx - oby * oby, 2.0 * obx * oby);
+  const double2 ob4 = cmul(ob2, ob2);
+  double f2, g2, h2, eu;
+  fgh(u, f2, g2, h2, eu);
+  const double c4 = 1.0 / (4.0 * k.ct), c16 = 1.0 / (16.0 * k.ct);
+  const double2 Kob2 = cmul(K0, ob2), Kob4 = cmul(K0, ob4);
+  // column 0
+  {
+    const double ReK = Kob2.x;
+    const double p = ReK * f2 * c4;
+    const double cb = eu * ReK * c16;
+    p_acc[0] = fma(wq, p, p_acc[0]);
+    d2_acc[0].x = fma(wq, Kob4.x * g2 * c4 - cb * ob2.x, d2_acc[0].x);
+    d2_acc[0].y = fma(wq, Kob4.y * g2 * c4 - cb * ob2.y, d2_acc[0].y);
+  }
+  // column 1: K1 ob^2 = i K0 ob^2, K1 ob^4 = i K0 ob^4
+  {
+    const double ReK = -Kob2.y;
+    const double p = ReK * f2 * c4 + mu1 * eu / (4.0 * M_PI * k.ct);
+    const double cb = eu * ReK * c16 + mu1 * f2 / (16.0 * M_PI * k.ct);
+    p_acc[1] = fma(wq, p, p_acc[1]);
+    d2_acc[1].x = fma(wq, -Kob4.y * g2 * c4 - cb * ob2.x, d2_acc[1].x);
+    d2_acc[1].y = fma(wq, Kob4.x * g2 * c4 - cb * ob2.y, d2_acc[1].y);
+  }
+  // column 2: q = -1
+  {
+    const double e1 = q_split ? expint_ein(u) : expint_e1(u);
+    const double cq = h2 / (16.0 * M_PI * k.kappa);
+    p_acc[2] = fma(wq, -e1 / (4.0 * M_PI * k.kappa), p_acc[2]);
+    d2_acc[2].x = fma(wq, cq * ob2.x, d2_acc[2].x);
+    d2_acc[2].y = fma(wq, cq * ob2.y, d2_acc[2].y);
+  }
+}
+
 // integral of (-gamma - ln(s^2/(4 c tau))) ds over [s0, s1], 0 <= s0 < s1
 __device__ __forceinline__ double e1_log_part(double s0, double s1, double ct) {
   auto prim = [&](double s) {
@@ -511,6 +556,44 @@ struct NearDesc {
   double a, Ds, Dn, q, ct;
 };
 
+// Phase A of a queue flush: graded panel breakpoints of entries [base,
+// base + ng), lane = (entry, side).
+template <class Desc>
+__device__ void near_queue_panels(NearQueue& Q, int base, int ng, int lane, const Desc& desc) {
+  {  // phase A: panel breakpoints, lane = (entry, side)
+    const int ei = lane >> 1, side = lane & 1;
+    if (ei < ng) {
+      const NearDesc d = desc(base + ei);
+      const double lt = sqrt(d.ct);
+      const double rx = d.zt.x - d.zc.x, ry = d.zt.y - d.zc.y;
+      const double sstar = rx * d.e.x + ry * d.e.y;
+      const double dperp = fabs(-rx * d.e.y + ry * d.e.x);
+      const double s0c = fmin(fmax(sstar, -d.a), d.a);
+      const double other = side ? d.a : -d.a;
+      const double sign = side ? 1.0 : -1.0;
+      double* b = Q.bp[ei][side];
+      double cur = s0c;
+      int np = 0;
+      b[0] = cur;
+      bool over = false;
+      if ((other - s0c) * sign > 0.0) {
+        while ((other - cur) * sign > 0.0) {
+          if (np == kBP) {
+            over = true;
+            break;
+          }
+          const double r = hypot(dperp, cur - sstar);
+          double snext = cur + sign * kPanelFraction * fmax(r, lt);
+          if ((other - snext) * sign <= 0.0) snext = other;
+          b[++np] = snext;
+          cur = snext;
+        }
+      }
+      Q.np[ei][side] = over ? -1 : np;
+    }
+  }
+}
+
 // Flush the queue: entries in batches of kBatchQ; lanes 2i, 2i+1 generate the
 // graded panels of entry i's two sides in parallel (the sequential recurrence
 // of poro_element), then the warp integrates the entries one at a time (32
@@ -523,38 +606,7 @@ __device__ void near_queue_flush(NearQueue& Q, int qn, int lane, const PoroConst
   __syncwarp();
   for (int base = 0; base < qn; base += kBatchQ) {
     const int ng = min(kBatchQ, qn - base);
-    {  // phase A: panel breakpoints, lane = (entry, side)
-      const int ei = lane >> 1, side = lane & 1;
-      if (ei < ng) {
-        const NearDesc d = desc(base + ei);
-        const double lt = sqrt(d.ct);
-        const double rx = d.zt.x - d.zc.x, ry = d.zt.y - d.zc.y;
-        const double sstar = rx * d.e.x + ry * d.e.y;
-        const double dperp = fabs(-rx * d.e.y + ry * d.e.x);
-        const double s0c = fmin(fmax(sstar, -d.a), d.a);
-        const double other = side ? d.a : -d.a;
-        const double sign = side ? 1.0 : -1.0;
-        double* b = Q.bp[ei][side];
-        double cur = s0c;
-        int np = 0;
-        b[0] = cur;
-        bool over = false;
-        if ((other - s0c) * sign > 0.0) {
-          while ((other - cur) * sign > 0.0) {
-            if (np == kBP) {
-              over = true;
-              break;
-            }
-            const double r = hypot(dperp, cur - sstar);
-            double snext = cur + sign * kPanelFraction * fmax(r, lt);
-            if ((other - snext) * sign <= 0.0) snext = other;
-            b[++np] = snext;
-            cur = snext;
-          }
-        }
-        Q.np[ei][side] = over ? -1 : np;
-      }
-    }
+    near_queue_panels(Q, base, ng, lane, desc);
     __syncwarp();
     for (int ei = 0; ei < ng; ++ei) {   // phase B: the warp integrates entry ei
       const NearDesc d = desc(base + ei);
@@ -607,6 +659,81 @@ __device__ void near_queue_flush(NearQueue& Q, int qn, int lane, const PoroConst
         const double2 t2 =
             cmul(d.e2t, make_double2(-4.0 * k.eta * d2acc.x, -4.0 * k.eta * d2acc.y));
         T = make_double2(-k.eta * pacc + t2.x, t2.y);
+      }
+      if (lane == 0) sink(base + ei, T, p);
+      __syncwarp();
+    }
+  }
+}
+
+// near_queue_flush for the three unit source columns of each entry (near-
+// field block builds, §4.5b/§4.6b): one quadrature pass per entry gives all
+// three columns (point_add3); sink(qi, T[3], p[3]).  desc(qi) supplies the
+// geometry and c tau (its strengths are ignored).
+template <class Desc, class Sink>
+__device__ void near_queue_flush3(NearQueue& Q, int qn, int lane, const PoroConst& k0,
+                                  const Desc& desc, const Sink& sink) {
+  __syncwarp();
+  for (int base = 0; base < qn; base += kBatchQ) {
+    const int ng = min(kBatchQ, qn - base);
+    near_queue_panels(Q, base, ng, lane, desc);
+    __syncwarp();
+    for (int ei = 0; ei < ng; ++ei) {
+      const NearDesc d = desc(base + ei);
+      PoroConst k = k0;
+      k.ct = d.ct;
+      double2 T[3];
+      double p[3];
+      const int n0 = Q.np[ei][0], n1 = Q.np[ei][1];
+      if (n0 < 0 || n1 < 0) {   // long panel lists: the per-column cooperative rule
+        for (int c = 0; c < 3; ++c)
+          poro_near_coop(d.zt, d.zc, d.e, d.a, c == 0 ? 1.0 : 0.0, c == 1 ? 1.0 : 0.0,
+                         c == 2 ? -1.0 : 0.0, k, d.e2t, Q.coop, lane, T[c], p[c]);
+      } else {
+        const double rx = d.zt.x - d.zc.x, ry = d.zt.y - d.zc.y;
+        const double sstar = rx * d.e.x + ry * d.e.y;
+        const double dperp = fabs(-rx * d.e.y + ry * d.e.x);
+        const double2 K0 = cscale(cmul(make_double2(0.0, k.gc), cmul(d.e, d.e)), -4.0 * k.kp);
+        const double mu1 = -(k.eta / k.S);
+        const bool on_line = (dperp == 0.0) && (fabs(sstar) < d.a);
+        const double s0c = fmin(fmax(sstar, -d.a), d.a);
+        double pacc[3] = {0.0, 0.0, 0.0};
+        double2 d2acc[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+        const int npts = 8 * (n0 + n1);
+        for (int t = lane; t < npts; t += 32) {
+          const int pan = t >> 3, g = t & 7;
+          const int side = pan < n0 ? 0 : 1;
+          const int pi = side ? pan - n0 : pan;
+          const double* b = Q.bp[ei][side];
+          const double s0 = b[pi], s1 = b[pi + 1];
+          const double mid = 0.5 * (s0 + s1), half = 0.5 * fabs(s1 - s0);
+          const double sq = mid + half * c_gl_x[g];
+          const double wx = d.zt.x - (d.zc.x + sq * d.e.x), wy = d.zt.y - (d.zc.y + sq * d.e.y);
+          point_add3(wx, wy, half * c_gl_w[g], k, K0, mu1, on_line, pacc, d2acc);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) {
+            pacc[c] += __shfl_xor_sync(0xffffffffu, pacc[c], o);
+            d2acc[c].x += __shfl_xor_sync(0xffffffffu, d2acc[c].x, o);
+            d2acc[c].y += __shfl_xor_sync(0xffffffffu, d2acc[c].y, o);
+          }
+        if (on_line) {   // analytic log part of E1 on the element, column 2 (q = -1)
+          for (int side = 0; side < 2; ++side) {
+            const double other = side ? d.a : -d.a;
+            const double sign = side ? 1.0 : -1.0;
+            if ((other - s0c) * sign <= 0.0) continue;
+            const double len = fabs(other - sstar);
+            pacc[2] -= e1_log_part(0.0, len, k.ct) / (4.0 * M_PI * k.kappa);
+          }
+        }
+        for (int c = 0; c < 3; ++c) {
+          p[c] = pacc[c];
+          const double2 t2 =
+              cmul(d.e2t, make_double2(-4.0 * k.eta * d2acc[c].x, -4.0 * k.eta * d2acc[c].y));
+          T[c] = make_double2(-k.eta * pacc[c] + t2.x, t2.y);
+        }
       }
       if (lane == 0) sink(base + ei, T, p);
       __syncwarp();
@@ -808,10 +935,11 @@ poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __re
     double* blk0 = cache + ioff[it - item_lo] * lstride + (int64_t)lidx * kTgtGroup * 9;
     const int64_t jstride = (int64_t)lstride * kTgtGroup * 9;
     int qn = 0;
-    // queue entry: t = target slot, s = source element, j = 4 jpos + component
+    // queue entry: t = target slot, s = source element, j = jpos (all three
+    // unit columns of the pair integrated together, near_queue_flush3)
     auto desc = [&](int qi) {
       const int tg = item.y + Q.t[qi];
-      const int sj = Q.s[qi], comp = Q.j[qi] & 3;
+      const int sj = Q.s[qi];
       const double cq = ec[tg], sq = es[tg];
       NearDesc d;
       d.zt = make_double2(ex[tg], ey[tg]);
@@ -819,18 +947,17 @@ poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __re
       d.zc = make_double2(ex[sj], ey[sj]);
       d.e = make_double2(ec[sj], es[sj]);
       d.a = ea[sj];
-      d.Ds = comp == 0 ? 1.0 : 0.0;
-      d.Dn = comp == 1 ? 1.0 : 0.0;
-      d.q = comp == 2 ? -1.0 : 0.0;   // J: q_formula = -q_ABI
+      d.Ds = d.Dn = d.q = 0.0;   // unused by near_queue_flush3
       d.ct = k.ct;
       return d;
     };
-    auto sink = [&](int qi, double2 T, double p) {
-      const int comp = Q.j[qi] & 3, jpos = Q.j[qi] >> 2;
-      double* b = blk0 + jpos * jstride + Q.t[qi] * 9;
-      b[comp] += T.y;
-      b[3 + comp] += T.x;
-      b[6 + comp] -= p;   // J: p_ABI = -p_formula
+    auto sink = [&](int qi, const double2* T, const double* p) {
+      double* b = blk0 + (int64_t)Q.j[qi] * jstride + Q.t[qi] * 9;
+      for (int comp = 0; comp < 3; ++comp) {
+        b[comp] += T[comp].y;
+        b[3 + comp] += T[comp].x;
+        b[6 + comp] -= p[comp];   // J: p_ABI = -p_formula
+      }
     };
     int pos = 0;
     for (int r = u_off[kk], rend = u_off[kk + 1]; r < rend && pos < item.w; ++r) {
@@ -848,18 +975,19 @@ poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __re
           sp[3] = es[lo + j];
           sp[4] = ea[lo + j];
         }
-        for (int comp = 0; comp < 3; ++comp) {
-          bool near = false;
-          if (have) {
+        bool near = false;
+        if (have) {
+          const double2 zc = make_double2(sp[0], sp[1]), e = make_double2(sp[2], sp[3]);
+          near = poro_is_near(zt, zc, e, sp[4], k.ct);
+          double* bb = blk0 + jpos * jstride + tl * 9;
+          for (int comp = 0; comp < 3; ++comp) {
             const double Ds = comp == 0 ? 1.0 : 0.0, Dn = comp == 1 ? 1.0 : 0.0;
-            const double2 zc = make_double2(sp[0], sp[1]), e = make_double2(sp[2], sp[3]);
             double os = 0.0, on = 0.0, op = 0.0;
             if (drained) {
               const double2 Td = drained_traction(zt, zc, e, sp[4], Ds, Dn, k.gc, e2t);
               os += Td.y;
               on += Td.x;
             }
-            near = poro_is_near(zt, zc, e, sp[4], k.ct);
             if (!near) {   // analytic far form of the poroelastic part
               double2 Tp;
               double pp;
@@ -868,28 +996,27 @@ poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __re
               on += Tp.x;
               op -= pp;   // J: p_ABI = -p_formula
             }
-            double* bb = blk0 + jpos * jstride + tl * 9;
             bb[comp] = os;
             bb[3 + comp] = on;
             bb[6 + comp] = op;
           }
-          const unsigned m = __ballot_sync(0xffffffffu, near);
-          if (near) {
-            const int idx = qn + __popc(m & lt_mask);
-            Q.t[idx] = tl;
-            Q.s[idx] = lo + j;
-            Q.j[idx] = 4 * jpos + comp;
-          }
-          qn += __popc(m);
-          if (qn >= 32) {
-            near_queue_flush(Q, qn, lane, k, desc, sink);
-            qn = 0;
-          }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, near);
+        if (near) {
+          const int idx = qn + __popc(m & lt_mask);
+          Q.t[idx] = tl;
+          Q.s[idx] = lo + j;
+          Q.j[idx] = jpos;
+        }
+        qn += __popc(m);
+        if (qn >= 32) {
+          near_queue_flush3(Q, qn, lane, k, desc, sink);
+          qn = 0;
         }
       }
       pos += len;
     }
-    near_queue_flush(Q, qn, lane, k, desc, sink);
+    near_queue_flush3(Q, qn, lane, k, desc, sink);
     __syncwarp();
   }
 }
