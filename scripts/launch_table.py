@@ -8,7 +8,7 @@ rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
 hdr = rows[0]
 ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
 recs = [(r[ki], float(r[vi].replace(",", ""))) for r in rows[1:]]
-last = max(i for i, (k, _) in enumerate(recs) if "prep_sources" in k or "poro_prep" in k)
+last = max(i for i, (k, _) in enumerate(recs) if "prep_sources" in k or "prep_stream" in k or "poro_prep" in k)
 end = next((i for i in range(last, len(recs)) if "finalize" in recs[i][0]), len(recs) - 1)
 agg = collections.OrderedDict()
 for k, v in recs[last:end + 1]:
