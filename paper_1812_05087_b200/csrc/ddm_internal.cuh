@@ -210,7 +210,8 @@ struct ddm_tree_s {
   // matvec CUDA graphs (fmm.cu)
   std::vector<MatvecGraph> graphs = std::vector<MatvecGraph>(4);
   int graph_next = 0;
-  MatvecKey last_key;
+  MatvecKey seen_keys[4];          // recently used argument sets (capture on a repeat)
+  int seen_next = 0;
   // GMRES block-Jacobi preconditioner: inverse self blocks [n][ncomp][ncomp]
   // (sorted order) for the material / elapsed time in pc_key
   double* pc = nullptr;

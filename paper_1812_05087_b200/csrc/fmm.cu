@@ -153,9 +153,13 @@ int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double el
       DDM_CUDA(ctx, cudaGraphLaunch(g.exec, s));
       return DDM_OK;
     }
-  // capture on the second consecutive use of the same arguments
-  if (!(t->last_key == key)) {
-    t->last_key = key;
+  // capture on the second use of the same arguments among the last four
+  // argument sets (alternating buffers, e.g. a pipelined caller, repeat too)
+  bool seen = false;
+  for (const auto& k : t->seen_keys) seen = seen || (k == key);
+  if (!seen) {
+    t->seen_keys[t->seen_next] = key;
+    t->seen_next = (t->seen_next + 1) % 4;
     return fmm_matvec_launch(ctx, t, mat, elapsed, D, d_sorted, y_user, y_sorted, mode, s);
   }
   // captured on the library's own stream (the caller's may be the legacy
