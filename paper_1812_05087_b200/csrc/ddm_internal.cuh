@@ -237,6 +237,8 @@ struct ddm_tree_s {
   // Givens rotations, rotated rhs, per-step estimates, 1/h(k+1,k), flags
   double* gm_dev = nullptr;
   int gm_dev_m = 0;
+  unsigned* gm_ticket = nullptr;  // zeroed tickets of the fused GMRES reductions
+  int gm_ticket_n = 0;
 };
 
 namespace ddm {

@@ -26,10 +26,21 @@ namespace {
 
 constexpr int kDotThreads = 256;
 
-// part[i * nb + b] = sum over chunk b of V[i * ld + j] * w[j]
+// part[i * nb + b] = sum over chunk b of V[i * ld + j] * w[j]; the last
+// block of vector i to finish (atomic ticket) sums the nb partials in a fixed
+// order into out[i] (deterministic, no second launch) and resets the ticket.
+__device__ __forceinline__ double fixed_order_sum(const double* part, int nb) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int b = lane; b < nb; b += 32) s += part[b];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
 __global__ void __launch_bounds__(kDotThreads)
 multi_dot(const double* __restrict__ V, int64_t ld, const double* __restrict__ w, int64_t len,
-          int nb, double* __restrict__ part) {
+          int nb, double* __restrict__ part, unsigned* __restrict__ ticket,
+          double* __restrict__ out) {
   const int i = blockIdx.y, b = blockIdx.x;
   const int64_t chunk = (len + nb - 1) / nb;
   const int64_t j0 = b * chunk, j1 = min(len, j0 + chunk);
@@ -38,25 +49,25 @@ multi_dot(const double* __restrict__ V, int64_t ld, const double* __restrict__ w
   for (int64_t j = j0 + threadIdx.x; j < j1; j += kDotThreads) acc = fma(v[j], w[j], acc);
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   __shared__ double sh[kDotThreads / 32];
+  __shared__ bool last;
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int k = 0; k < kDotThreads / 32; ++k) s += sh[k];
     part[(int64_t)i * nb + b] = s;
+    __threadfence();
+    last = atomicAdd(ticket + i, 1u) == (unsigned)(nb - 1);
   }
-}
-
-// out[i] = sum_b part[i * nb + b] in a fixed order (deterministic)
-__global__ void reduce_parts(const double* __restrict__ part, int nvec, int nb,
-                             double* __restrict__ out) {
-  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (i >= nvec) return;
-  double s = 0.0;
-  for (int b = lane; b < nb; b += 32) s += part[(int64_t)i * nb + b];
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) out[i] = s;
+  __syncthreads();
+  if (last && threadIdx.x < 32) {
+    __threadfence();
+    const double s = fixed_order_sum(part + (int64_t)i * nb, nb);
+    if (threadIdx.x == 0) {
+      out[i] = s;
+      ticket[i] = 0u;
+    }
+  }
 }
 
 // w[j] += sign * sum_i V[i * ld + j] c[i]: eight independent accumulators
@@ -79,6 +90,54 @@ __global__ void multi_axpy(const double* __restrict__ V, int64_t ld, int nvec,
     for (int q = 0; i < nvec; ++i, ++q) a[q] = fma(__ldg(v + (int64_t)i * ld), sc[i], a[q]);
     const double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     w[j] = fma(sign, acc, w[j]);
+  }
+}
+
+// multi_axpy followed by ||w||^2 of the result: per-block partial sums, the
+// last block (ticket) reduces them in a fixed order into out[0]
+__global__ void multi_axpy_norm(const double* __restrict__ V, int64_t ld, int nvec,
+                                const double* __restrict__ c, double sign, double* __restrict__ w,
+                                int64_t len, double* __restrict__ part,
+                                unsigned* __restrict__ ticket, double* __restrict__ out) {
+  extern __shared__ double sc[];
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) sc[i] = c[i];
+  __syncthreads();
+  double nrm = 0.0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < len;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    const double* v = V + j;
+    int i = 0;
+    for (; i + 8 <= nvec; i += 8) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = fma(__ldg(v + (int64_t)(i + q) * ld), sc[i + q], a[q]);
+    }
+    for (int q = 0; i < nvec; ++i, ++q) a[q] = fma(__ldg(v + (int64_t)i * ld), sc[i], a[q]);
+    const double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    const double wn = fma(sign, acc, w[j]);
+    w[j] = wn;
+    nrm = fma(wn, wn, nrm);
+  }
+  for (int o = 16; o; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+  __shared__ double sh[32];
+  __shared__ bool last;
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = nrm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += sh[k];
+    part[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x < 32) {
+    __threadfence();
+    const double s = fixed_order_sum(part, gridDim.x);
+    if (threadIdx.x == 0) {
+      out[0] = s;
+      ticket[0] = 0u;
+    }
   }
 }
 
@@ -277,49 +336,49 @@ chunk_apply(const int2* __restrict__ chunks, const int64_t* __restrict__ off, in
 }
 
 // One Arnoldi step's small work on the device (batched GMRES, no host round
-// trip per iteration).  dh = [h1 (k+1) | h2 (k+1) | -- | ||w||^2] of the CGS2
-// passes; column k of the packed Hessenberg Hp(i, k) = Hp[k (k+3)/2 + i]
+// trip per step), fused with the normalisation of the next basis vector.
+// dh = [h1 (k+1) | h2 (k+1) | -- | ||w||^2] of the CGS2 passes.  Block 0,
+// thread 0: column k of the packed Hessenberg Hp(i, k) = Hp[k (k+3)/2 + i]
 // becomes h1 + h2 with h(k+1,k) = ||w||, the previous Givens rotations are
 // applied, a new one zeroes h(k+1,k), and the rotated rhs g gives the
-// residual estimate est[k] = |g[k+1]|.  scal[0] = 1/h(k+1,k) (0 on
-// breakdown, which also sets flag[0] = k + 1 and makes later steps no-ops).
-// One thread: O(k) work.
-__global__ void arnoldi_finish(int k, const double* __restrict__ dh, double* __restrict__ Hp,
-                               double* __restrict__ cs, double* __restrict__ sn,
-                               double* __restrict__ g, double* __restrict__ est,
-                               double* __restrict__ scal, int* __restrict__ flag) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  if (flag[0]) {   // broken down earlier: nothing to add
-    est[k] = est[k > 0 ? k - 1 : 0];
-    scal[0] = 0.0;
-    return;
-  }
-  double* col = Hp + (size_t)k * (k + 3) / 2;
-  for (int i = 0; i <= k; ++i) col[i] = dh[i] + dh[k + 1 + i];
+// residual estimate est[k] = |g[k+1]|; a breakdown (h(k+1,k) = 0) sets
+// flag[0] = k + 1 and makes later steps no-ops.  All blocks: dst = w / h(k+1,k)
+// (0 after a breakdown).
+__global__ void finish_scale(int k, const double* __restrict__ dh, double* __restrict__ Hp,
+                             double* __restrict__ cs, double* __restrict__ sn,
+                             double* __restrict__ g, double* __restrict__ est,
+                             double* __restrict__ scal, int* __restrict__ flag,
+                             const double* __restrict__ w, double* __restrict__ dst, int64_t len) {
+  const bool broke = flag[0] != 0;
   const double hn = sqrt(dh[2 * (k + 1) + 1]);
-  for (int i = 0; i < k; ++i) {
-    const double a = col[i], b = col[i + 1];
-    col[i] = cs[i] * a + sn[i] * b;
-    col[i + 1] = -sn[i] * a + cs[i] * b;
-  }
-  const double a = col[k], b = hn;
-  const double den = hypot(a, b);
-  cs[k] = a / den;
-  sn[k] = b / den;
-  col[k] = den;
-  col[k + 1] = 0.0;
-  g[k + 1] = -sn[k] * g[k];
-  g[k] = cs[k] * g[k];
-  est[k] = fabs(g[k + 1]);
-  scal[0] = hn > 0.0 ? 1.0 / hn : 0.0;
-  if (!(hn > 0.0)) flag[0] = k + 1;
-}
-
-// dst = a[0] * src with a device scalar
-__global__ void scale_copy_dev(const double* __restrict__ src, const double* __restrict__ a,
-                               double* __restrict__ dst, int64_t len) {
+  const double a = (!broke && hn > 0.0) ? 1.0 / hn : 0.0;
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j < len) dst[j] = a[0] * src[j];
+  if (j < len) dst[j] = a * w[j];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (broke) {
+      est[k] = est[k > 0 ? k - 1 : 0];
+      scal[0] = 0.0;
+      return;
+    }
+    double* col = Hp + (size_t)k * (k + 3) / 2;
+    for (int i = 0; i <= k; ++i) col[i] = dh[i] + dh[k + 1 + i];
+    for (int i = 0; i < k; ++i) {
+      const double x = col[i], y = col[i + 1];
+      col[i] = cs[i] * x + sn[i] * y;
+      col[i + 1] = -sn[i] * x + cs[i] * y;
+    }
+    const double x = col[k];
+    const double den = hypot(x, hn);
+    cs[k] = x / den;
+    sn[k] = hn / den;
+    col[k] = den;
+    col[k + 1] = 0.0;
+    g[k + 1] = -sn[k] * g[k];
+    g[k] = cs[k] * g[k];
+    est[k] = fabs(g[k + 1]);
+    scal[0] = a;
+    if (!(hn > 0.0)) flag[0] = k + 1;
+  }
 }
 
 struct Gm {
@@ -335,15 +394,26 @@ struct Gm {
   int nb() const { return (int)std::max<int64_t>(1, std::min<int64_t>(256, nloc / 2048)); }
 
   // dots of V[0..nvec) (leading dim ld) with w over the owned rows -> dh[off..off+nvec)
+  unsigned* ticket;      // [>= nvec] zeroed tickets of the fused dot reductions
+  unsigned* ticket_norm; // zeroed ticket of axpy_norm
+
   int dots(const double* V, int64_t ld, int nvec, const double* w, int off) {
     const int b = nb();
     if ((int64_t)nvec * b > part_cap) return set_error(ctx, DDM_ERR_ARG, "gmres part buffer");
     dim3 grid(b, nvec);
-    multi_dot<<<grid, kDotThreads, 0, s>>>(V, ld, w, nloc, b, part);
-    DDM_CUDA(ctx, cudaGetLastError());
-    reduce_parts<<<nblk(nvec, 8), 256, 0, s>>>(part, nvec, b, dh + off);
+    multi_dot<<<grid, kDotThreads, 0, s>>>(V, ld, w, nloc, b, part, ticket, dh + off);
     DDM_CUDA(ctx, cudaGetLastError());
     return allreduce_sum(ctx, dh + off, nvec, s);
+  }
+  // w += sign V c, then dh[off] = ||w||^2 (owned rows, summed over ranks)
+  int axpy_norm(const double* V, int64_t ld, int nvec, const double* c, double sign, double* w,
+                int off) {
+    const unsigned g = std::min(nblk(nloc, 256), 148u * 8);
+    if ((int64_t)g > part_cap) return set_error(ctx, DDM_ERR_ARG, "gmres part buffer");
+    multi_axpy_norm<<<g, 256, nvec * sizeof(double), s>>>(V, ld, nvec, c, sign, w, nloc, part,
+                                                          ticket_norm, dh + off);
+    DDM_CUDA(ctx, cudaGetLastError());
+    return allreduce_sum(ctx, dh + off, 1, s);
   }
   int axpy(const double* V, int64_t ld, int nvec, const double* c, double sign, double* w) {
     const unsigned g = std::min(nblk(nloc, 256), 148u * 8);
@@ -531,7 +601,16 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   double* uf = t->gm_w + 4 * nfull;   // preconditioned operand M^-1 v (full) / update V y
   double* xt = t->gm_w + 5 * nfull;   // trial iterate (true-residual check)
   double* V = t->krylov;
-  Gm g{ctx, t, s, ncomp, nloc, lo, t->gm_part, t->gm_part_n, t->gm_tmp};
+  if (t->gm_ticket_n < m + 4) {
+    if (t->gm_ticket) cudaFree(t->gm_ticket);
+    t->gm_ticket = nullptr;
+    t->gm_ticket_n = 0;
+    DDM_CUDA(ctx, cudaMalloc((void**)&t->gm_ticket, (size_t)(m + 4) * sizeof(unsigned)));
+    DDM_CUDA(ctx, cudaMemsetAsync(t->gm_ticket, 0, (size_t)(m + 4) * sizeof(unsigned), s));
+    t->gm_ticket_n = m + 4;
+  }
+  Gm g{ctx, t, s, ncomp, nloc, lo, t->gm_part, t->gm_part_n, t->gm_tmp, t->gm_ticket,
+       t->gm_ticket + m + 3};
   // DDM_GMRES_SYNC=1: the host takes every Arnoldi step's decisions (Givens,
   // DGKS reorthogonalisation); default: batched device-side steps
   static const bool sync_mode = [] {
@@ -706,10 +785,9 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
         if ((rc = g.dots(V, nloc, k + 1, w, 0))) return rc;
         if ((rc = g.axpy(V, nloc, k + 1, g.dh, -1.0, w))) return rc;
         if ((rc = g.dots(V, nloc, k + 1, w, k + 1))) return rc;
-        if ((rc = g.axpy(V, nloc, k + 1, g.dh + k + 1, -1.0, w))) return rc;
-        if ((rc = g.dots(w, 0, 1, w, o_w1))) return rc;
-        arnoldi_finish<<<1, 32, 0, s>>>(k, g.dh, Hd, csd, snd, gd, estd, scald, flagd);
-        scale_copy_dev<<<nblk(nloc, 256), 256, 0, s>>>(w, scald, V + (int64_t)(k + 1) * nloc, nloc);
+        if ((rc = g.axpy_norm(V, nloc, k + 1, g.dh + k + 1, -1.0, w, o_w1))) return rc;
+        finish_scale<<<nblk(nloc, 256), 256, 0, s>>>(k, g.dh, Hd, csd, snd, gd, estd, scald, flagd,
+                                                     w, V + (int64_t)(k + 1) * nloc, nloc);
         DDM_CUDA(ctx, cudaGetLastError());
         ++iters;
         kdone = k + 1;
