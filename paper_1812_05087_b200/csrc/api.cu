@@ -181,10 +181,39 @@ int allreduce_sum(ddm_ctx_s* ctx, double* buf, int64_t count, cudaStream_t s) {
 #endif
 }
 
+// Everything derived from the owned range (captured matvec graphs, the
+// near-field and history caches of the owned items, the owned preconditioner
+// chunks) is dropped when the partition changes; it is rebuilt on demand.
+static void drop_owned_state(ddm_tree_s* t) {
+  for (auto& g : t->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+  }
+  for (auto& k : t->seen_keys) k = MatvecKey();
+  for (double* p : t->hc_lag) cudaFree(p);
+  t->hc_lag.clear();
+  t->hc_nlags = 0;
+  t->hc_valid = t->hc_seen_set = t->hc_capped = false;
+  void* ptrs[] = {t->nc, t->nc_off, t->pc_chunks, t->pc_off, t->pcl};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  t->nc = nullptr;
+  t->nc_off = nullptr;
+  t->nc_n = 0;
+  t->nc_valid = t->nc_seen_set = false;
+  t->pc_chunks = nullptr;
+  t->pc_off = nullptr;
+  t->pcl = nullptr;
+  t->pc_nchunks = t->pc_off_ncomp = 0;
+  std::memset(t->pcl_key, 0, sizeof(t->pcl_key));
+}
+
 int partition_tree(ddm_tree_s* t, int rank, int world, cudaStream_t s) {
   ddm_ctx_s* ctx = t->ctx;
   if (world < 1 || rank < 0 || rank >= world)
     return set_error(ctx, DDM_ERR_ARG, "bad rank/world");
+  DDM_CUDA(ctx, cudaStreamSynchronize(s));
+  drop_owned_state(t);
   std::vector<int> split(world + 1);
   split_costs(t->leaf_cost_prefix.data(), t->leaf_cost_prefix[t->nleaves], t->nleaves, world,
               split.data());
