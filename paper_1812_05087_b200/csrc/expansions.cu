@@ -258,8 +258,16 @@ __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* 
 }
 
 // P2M of every leaf: no dependencies, warp per leaf (grid-stride).
+#ifndef DDM_P2M_MINB
+#define DDM_P2M_MINB 0
+#endif
+#if DDM_P2M_MINB > 0
+#define DDM_P2M_BOUNDS __launch_bounds__(kPassWarps * 32, DDM_P2M_MINB)
+#else
+#define DDM_P2M_BOUNDS __launch_bounds__(kPassWarps * 32)
+#endif
 template <int PT>
-__global__ void __launch_bounds__(kPassWarps * 32)
+__global__ void DDM_P2M_BOUNDS
 p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ c_level,
            const int* __restrict__ c_ix, const int* __restrict__ c_iy,
            const int* __restrict__ c_start, const int* __restrict__ c_count, CellGeom cg,
@@ -503,8 +511,11 @@ __device__ void m2l_cell_dfma(int p, int vb, int ve, const int* __restrict__ v_i
 
 // M2L of every cell of level >= 2 whose subtree holds owned targets: no
 // dependencies (all multipoles are final), warp per cell (grid-stride).
+#ifndef DDM_M2L_MINB
+#define DDM_M2L_MINB 2
+#endif
 template <int PT>
-__global__ void __launch_bounds__(kPassWarps * 32, 2)
+__global__ void __launch_bounds__(kPassWarps * 32, DDM_M2L_MINB)
 m2l_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restrict__ v_off,
            const int* __restrict__ v_idx, const unsigned char* __restrict__ v_cls,
            const int* __restrict__ c_start, const int* __restrict__ c_count, int p_rt,
@@ -639,8 +650,16 @@ l2l_level_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __re
 // read through L1: the threads of a leaf share them), projected onto the
 // element's frame: y_far[i] = (sigma_s, sigma_n[, p]) in sorted order.
 //   W = i G C (conj(u) Phi' + Psi~),  T = sigma_n + i sigma_s = 2 Re(i G C Phi) + e^{2 i b} W
+#ifndef DDM_L2P_MINB
+#define DDM_L2P_MINB 4   // 64 registers, 32 warps per SM (measured: 161 -> 150 us on config 5)
+#endif
+#if DDM_L2P_MINB > 0
+#define DDM_L2P_BOUNDS __launch_bounds__(256, DDM_L2P_MINB)
+#else
+#define DDM_L2P_BOUNDS __launch_bounds__(256)
+#endif
 template <int PT>
-__global__ void __launch_bounds__(256)
+__global__ void DDM_L2P_BOUNDS
 l2p_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int* __restrict__ el_leaf,
            const int* __restrict__ leaves, const int* __restrict__ c_level,
            const int* __restrict__ c_ix, const int* __restrict__ c_iy,
