@@ -309,12 +309,19 @@ chunk_invert(const int2* __restrict__ chunks, const int64_t* __restrict__ off, i
   }
 }
 
-// y (+)= blockdiag(inv) x over the chunks [q0, q0 + gridDim.x) (sorted order)
-__global__ void __launch_bounds__(128)
+// y (+)= blockdiag(inv) x over the chunks [q0, q0 + gridDim.x) (sorted order).
+// CTA per chunk; the d columns are split over G = blockDim / d thread groups
+// (thread (r, g) sums columns c = g, g + G, ... of row r with eight
+// accumulators: coalesced over r, eight loads in flight), partials summed over
+// the groups in a fixed order.
+constexpr int kApplyThreads = 256;
+
+__global__ void __launch_bounds__(kApplyThreads)
 chunk_apply(const int2* __restrict__ chunks, const int64_t* __restrict__ off, int q0, int ncomp,
             const double* __restrict__ inv, const double* __restrict__ x, double* __restrict__ y,
             int add) {
   __shared__ double xs[kPcChunk * 3];
+  __shared__ double part[kApplyThreads];
   const int q = q0 + blockIdx.x;
   const int2 ch = chunks[q];
   const int d = ncomp * ch.y;
@@ -322,16 +329,28 @@ chunk_apply(const int2* __restrict__ chunks, const int64_t* __restrict__ off, in
   const double* Ai = inv + off[q];
   for (int t = threadIdx.x; t < d; t += blockDim.x) xs[t] = x[b0 + t];
   __syncthreads();
-  for (int r = threadIdx.x; r < d; r += blockDim.x) {
-    double a0 = 0.0, a1 = 0.0;
-    int c = 0;
-    for (; c + 1 < d; c += 2) {
-      a0 = fma(Ai[(size_t)c * d + r], xs[c], a0);
-      a1 = fma(Ai[(size_t)(c + 1) * d + r], xs[c + 1], a1);
+  if (d == 0) return;
+  const int G = max(1, (int)blockDim.x / d);
+  const int r = threadIdx.x % d, g = threadIdx.x / d;
+  if (g < G) {
+    // eight loads in flight per thread (all issued before the FMAs use them)
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int c = g;
+    for (; c + 7 * G < d; c += 8 * G) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(Ai + (size_t)(c + u * G) * d + r);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = fma(v[u], xs[c + u * G], a[u]);
     }
-    if (c < d) a0 = fma(Ai[(size_t)c * d + r], xs[c], a0);
-    const double v = a0 + a1;
-    y[b0 + r] = add ? y[b0 + r] + v : v;
+    for (int u = 0; c < d; c += G, ++u) a[u] = fma(__ldg(Ai + (size_t)c * d + r), xs[c], a[u]);
+    part[threadIdx.x] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  }
+  __syncthreads();
+  if (threadIdx.x < d) {
+    double v = 0.0;
+    for (int gg = 0; gg < G; ++gg) v += part[gg * d + threadIdx.x];
+    y[b0 + threadIdx.x] = add ? y[b0 + threadIdx.x] + v : v;
   }
 }
 
@@ -531,7 +550,7 @@ int precond_apply(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double
     block_apply<<<nblk(t->n, 256), 256, 0, s>>>(0, t->n, ncomp, t->pc, x_sorted, y_sorted, 0);
   } else {
     if ((rc = pc_leaf_blocks(ctx, t, mat, dt, s))) return rc;
-    chunk_apply<<<t->pc_nchunks, 128, 0, s>>>(t->pc_chunks, t->pc_off, 0, ncomp, t->pcl, x_sorted,
+    chunk_apply<<<t->pc_nchunks, kApplyThreads, 0, s>>>(t->pc_chunks, t->pc_off, 0, ncomp, t->pcl, x_sorted,
                                               y_sorted, 0);
   }
   DDM_CUDA(ctx, cudaGetLastError());
@@ -718,7 +737,7 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
         block_apply<<<nblk(t->own_el_hi - t->own_el_lo, 256), 256, 0, s>>>(
             t->own_el_lo, t->own_el_hi, ncomp, t->pc, uf, dst, 1);
       } else if (t->pc_q_hi > t->pc_q_lo) {
-        chunk_apply<<<t->pc_q_hi - t->pc_q_lo, 128, 0, s>>>(t->pc_chunks, t->pc_off, t->pc_q_lo,
+        chunk_apply<<<t->pc_q_hi - t->pc_q_lo, kApplyThreads, 0, s>>>(t->pc_chunks, t->pc_off, t->pc_q_lo,
                                                             ncomp, t->pcl, uf, dst, 1);
       }
       DDM_CUDA(ctx, cudaGetLastError());
