@@ -46,6 +46,16 @@ __host__ __device__ constexpr int pmax() { return PT ? PT : kMaxP; }
 
 constexpr int kPassWarps = 8;
 
+// Programmatic dependent launch (sm_90+): a far-chain kernel is launched with
+// programmatic stream serialisation, so its blocks are scheduled once every
+// block of the previous kernel has started (that kernel triggers at entry);
+// it waits for the previous kernel's results (griddepcontrol.wait) only where
+// it first reads them, after any prologue that does not depend on them.
+// Without the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+
 // ------------------------------------------------------------ P2M (a5)
 // Warp per leaf; lane = element of a 32-element round.
 //   alpha_n = (B/s) P_{n-1}
@@ -276,6 +286,7 @@ p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ 
            const double* __restrict__ ec, const double* __restrict__ es,
            double2* __restrict__ mpole, PoroFar pf) {
   const int p = PT ? PT : p_rt;
+  pdl_trigger();
   extern __shared__ double2 p2m_sh[];   // [kPassWarps][32 * 17] transposition buffers
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int k = blockIdx.x * kPassWarps + w; k < nleaves; k += gridDim.x * kPassWarps)
@@ -293,6 +304,8 @@ m2m_level_kernel(int u0, int u1, const int* __restrict__ up_list, const int* __r
                  const double2* __restrict__ eps_g, const double2* __restrict__ e2i_g,
                  double2* __restrict__ mpole) {
   const int p = PT ? PT : p_rt;
+  pdl_trigger();
+  pdl_wait();   // the children's multipoles (previous level / P2M)
   extern __shared__ double2 up_sh[];   // per warp: pre-scaled children [2][4][p]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* wb = up_sh + (size_t)w * 8 * p;
@@ -546,6 +559,8 @@ m2l_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restrict
     block_copy(sh_pm2l, pm2l_g, (p + 1) * p);
   }
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();   // all multipoles (the upward pass)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t wstride = TC ? (size_t)2 * kM2LBatch * kXStride : 3 * (size_t)p + 1;
   double2* ring = wbuf + (size_t)w * wstride;
@@ -578,6 +593,8 @@ l2l_level_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __re
   const int pw = p + 2;
   constexpr int NC = PT ? (PT + 31) / 32 : 2;   // coefficients per lane
   extern __shared__ double2 l2_sh[];   // per warp: xl [p] | xg [p]
+  pdl_trigger();
+  pdl_wait();   // the parents' final locals (previous level / M2L)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* xl = l2_sh + (size_t)w * 2 * p;
   double2* xg = xl + p;
@@ -669,6 +686,7 @@ l2p_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int* __restrict__ el_lea
            const double* __restrict__ ey, const double* __restrict__ ec,
            const double* __restrict__ es, double* __restrict__ y_far) {
   const int p = PT ? PT : p_rt;
+  pdl_wait();   // the leaves' final locals (L2L)
   const int64_t i = e_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= e_hi) return;
   const int k = __ldg(el_leaf + i);
@@ -838,6 +856,37 @@ int pass_grid(ddm_ctx_s* ctx, const void* kernel, size_t shm, int work) {
 
 }  // namespace
 
+// Launch with programmatic stream serialisation (PDL, see pdl_wait) when the
+// far chain is latency bound: small trees, where the chain is the matvec's
+// critical path (config 3: 114 -> 110 us, config 4: 64 -> 60 us).  On large
+// trees the early-resident dependent blocks take SM slots from the concurrent
+// near field (config 5: 1.16 -> 1.28 ms), so there it is off.  DDM_PDL=0/1
+// overrides.
+static bool use_pdl(const ddm_tree_s* t) {
+  static const int env = [] {
+    const char* e = getenv("DDM_PDL");
+    return e ? atoi(e) : -1;
+  }();
+  return env >= 0 ? env != 0 : t->n <= 200000;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(bool on, void (*kernel)(KArgs...), unsigned grid, unsigned block,
+                       size_t shm, cudaStream_t s, Args... args) {
+  const bool off = !on;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = shm;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // upward pass: P2M on all leaves, then M2M one level at a time (deepest
 // first), replicated on every rank
 int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
@@ -864,9 +913,12 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
       const int u0 = t->up_level_off[2 * lev], u1 = t->up_level_off[2 * lev + 1];               \
       if (u1 <= u0) continue;                                                                   \
       const int nb2 = pass_grid(ctx, (const void*)m2m_level_kernel<PT>, shm, u1 - u0);          \
-      m2m_level_kernel<PT><<<nb2, kPassWarps * 32, shm, s>>>(                                   \
-          u0, u1, t->up_list, t->c_ix, t->c_iy, t->c_first_child, t->c_nchild, p, t->op_pasT,    \
-          t->op_eps, t->op_e2i, t->mpole);                                                      \
+      DDM_CUDA(ctx, launch_pdl(use_pdl(t), m2m_level_kernel<PT>, nb2, kPassWarps * 32, shm, s, u0, u1,     \
+                               (const int*)t->up_list, (const int*)t->c_ix,                    \
+                               (const int*)t->c_iy, (const int*)t->c_first_child,              \
+                               (const int*)t->c_nchild, p, (const double*)t->op_pasT,          \
+                               (const double2*)t->op_eps, (const double2*)t->op_e2i,           \
+                               t->mpole));                                                     \
     }                                                                                           \
     stage_end(ctx, DDM_ST_M2M, s);                                                              \
   } while (0)
@@ -894,9 +946,12 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     if ((rc = set_smem(ctx, m2l_kernel<PT>, shm))) return rc;                                   \
     const int nb = pass_grid(ctx, (const void*)m2l_kernel<PT>, shm, c1 - c0);                   \
     stage_begin(ctx, DDM_ST_M2L, s);                                                            \
-    m2l_kernel<PT><<<nb, kPassWarps * 32, shm, s>>>(                                            \
-        c0, c1, t->own_el_lo, t->own_el_hi, t->v_off, t->v_idx, t->v_cls, t->c_start,           \
-        t->c_count, p, t->op_w, t->op_pm2l, t->mpole, t->local);                                \
+    DDM_CUDA(ctx, launch_pdl(use_pdl(t), m2l_kernel<PT>, nb, kPassWarps * 32, shm, s, c0, c1,              \
+                             (int64_t)t->own_el_lo, (int64_t)t->own_el_hi,                     \
+                             (const int*)t->v_off, (const int*)t->v_idx,                       \
+                             (const unsigned char*)t->v_cls, (const int*)t->c_start,           \
+                             (const int*)t->c_count, p, (const double2*)t->op_w,               \
+                             (const double*)t->op_pm2l, (const double2*)t->mpole, t->local));  \
     stage_end(ctx, DDM_ST_M2L, s);                                                              \
     if ((rc = set_smem(ctx, l2l_level_kernel<PT>, shm2))) return rc;                            \
     stage_begin(ctx, DDM_ST_L2L, s);                                                            \
@@ -904,9 +959,13 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
       const int a = t->level_off[lev], b = t->level_off[lev + 1];                               \
       if (b <= a) continue;                                                                     \
       const int nb2 = pass_grid(ctx, (const void*)l2l_level_kernel<PT>, shm2, b - a);           \
-      l2l_level_kernel<PT><<<nb2, kPassWarps * 32, shm2, s>>>(                                  \
-          a, b, t->own_el_lo, t->own_el_hi, t->c_ix, t->c_iy, t->c_start, t->c_count,           \
-          t->c_parent, p, t->op_eps, t->op_e2i, t->op_pas, t->local);                           \
+      DDM_CUDA(ctx, launch_pdl(use_pdl(t), l2l_level_kernel<PT>, nb2, kPassWarps * 32, shm2, s, a, b,      \
+                               (int64_t)t->own_el_lo, (int64_t)t->own_el_hi,                   \
+                               (const int*)t->c_ix, (const int*)t->c_iy,                       \
+                               (const int*)t->c_start, (const int*)t->c_count,                 \
+                               (const int*)t->c_parent, p, (const double2*)t->op_eps,          \
+                               (const double2*)t->op_e2i, (const double*)t->op_pas,            \
+                               t->local));                                                     \
     }                                                                                           \
     stage_end(ctx, DDM_ST_L2L, s);                                                              \
   } while (0)
@@ -925,9 +984,13 @@ int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFa
   const unsigned nb = nblk(hi - lo, 256);
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \
-    l2p_kernel<PT><<<nb, 256, 0, s>>>(lo, hi, ncomp, t->el_leaf, t->leaves, t->c_level,         \
-                                      t->c_ix, t->c_iy, t->local, t->w_off, t->w_idx, t->mpole, \
-                                      cg, t->p, gc, pf, t->ex, t->ey, t->ec, t->es, t->y_far);  \
+    DDM_CUDA(ctx, launch_pdl(use_pdl(t), l2p_kernel<PT>, nb, 256, 0, s, (int64_t)lo, (int64_t)hi, ncomp,    \
+                             (const int*)t->el_leaf, (const int*)t->leaves,                    \
+                             (const int*)t->c_level, (const int*)t->c_ix, (const int*)t->c_iy, \
+                             (const double2*)t->local, (const int*)t->w_off,                   \
+                             (const int*)t->w_idx, (const double2*)t->mpole, cg, t->p, gc, pf, \
+                             (const double*)t->ex, (const double*)t->ey,                       \
+                             (const double*)t->ec, (const double*)t->es, t->y_far));           \
   } while (0)
   DDM_P_DISPATCH(t->p, DDM_L);
 #undef DDM_L
