@@ -150,6 +150,11 @@ struct ddm_tree_s {
   int* p2p_order = nullptr;       // [item_hi_owned - item_lo_owned] owned items, most sources
                                   // first (longest-processing-time order: no tail)
   // persistent-pass scheduling (expansions.cu)
+  // subtree passes (small trees, expansions.cu): split level, roots = its cells,
+  // per (root, level >= Ls) ranges into up_list (M2M) and into the level's cells (L2L)
+  int sub_Ls = 0, sub_n = 0, sub_nsl = 0;
+  int2* sub_up = nullptr;
+  int2* sub_cells = nullptr;
   int* up_list = nullptr;         // non-leaf cells of level >= 2, deepest level first
   int n_up = 0;
   std::vector<int> up_level_off;  // [2 (nlevels+1)]: level l = up_list[off[2l], off[2l+1])

@@ -582,6 +582,78 @@ m2l_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restrict
 // L2L of the cells [c0, c1) of ONE level >= 3 whose subtree holds owned
 // targets: local[c] (its M2L result) += L2L(parent's final local).  Launched
 // top-down, one level at a time.
+// L2L of one cell c (its M2L result in local[c]) from its parent's final local
+// (separable form); one warp.
+template <int PT>
+__device__ __forceinline__ void l2l_cell(int c, int p, const int* __restrict__ c_ix,
+                                         const int* __restrict__ c_iy,
+                                         const int* __restrict__ c_parent,
+                                         const double2* __restrict__ eps_g,
+                                         const double2* __restrict__ e2i_g,
+                                         const double* __restrict__ pas_g,
+                                         double2* __restrict__ local, double2* xl, double2* xg,
+                                         int lane) {
+  const int pw = p + 2;
+  constexpr int NC = PT ? (PT + 31) / 32 : 2;   // coefficients per lane
+  const int P = c_parent[c];
+  const double2* lp = local + (size_t)P * 2 * p;
+  double2* out = local + (size_t)c * 2 * p;
+  const int quad = (c_ix[c] & 1) + 2 * (c_iy[c] & 1);
+  // loads first: parent coefficients (slots m, m+1 of lambda, m of gamma) and
+  // this cell's own M2L result
+  double2 pl[NC], pl1[NC], pg[NC], ol[NC], og[NC];
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc) {
+    const int m = lane + 32 * cc;
+    const bool ok = m < p;
+    const double2 z = make_double2(0.0, 0.0);
+    pl[cc] = ok ? lp[m] : z;
+    pl1[cc] = (ok && m + 1 < p) ? lp[m + 1] : z;
+    pg[cc] = ok ? lp[p + m] : z;
+    ol[cc] = ok ? out[m] : z;
+    og[cc] = ok ? out[p + m] : z;
+  }
+  const double2 epsb = make_double2(0.5 * ((quad & 1) - 0.5), -0.5 * ((quad >> 1) - 0.5));
+  const double2* E = eps_g + quad * pw;
+  const double2* Ei = e2i_g + quad * pw;
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc) {
+    const int m = lane + 32 * cc;
+    if (m < p) {
+      double2 gv = pg[cc];
+      cmac(gv, cscale(epsb, (double)(m + 1)), pl1[cc]);
+      const double2 em = __ldg(E + m);
+      xl[m] = cmul(pl[cc], em);
+      xg[m] = cmul(gv, em);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc) {
+    const int k = lane + 32 * cc;
+    if (k < p) {
+      double2 l = make_double2(0.0, 0.0), g = l;
+#pragma unroll
+      for (int m = 0; m < pmax<PT>(); ++m) {
+        if (!PT && m >= p) break;
+        const double pc = __ldg(pas_g + m * p + k);   // C(m, k)
+        const double2 x = xl[m], y = xg[m];
+        l.x = fma(x.x, pc, l.x);
+        l.y = fma(x.y, pc, l.y);
+        g.x = fma(y.x, pc, g.x);
+        g.y = fma(y.y, pc, g.y);
+      }
+      const double2 ek = __ldg(Ei + k);
+      double2 al = ol[cc], ag = og[cc];
+      cmac(al, l, ek);
+      cmac(ag, g, ek);
+      out[k] = al;
+      out[p + k] = ag;
+    }
+  }
+  __syncwarp();
+}
+
 template <int PT>
 __global__ void __launch_bounds__(kPassWarps * 32)
 l2l_level_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restrict__ c_ix,
@@ -590,8 +662,6 @@ l2l_level_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __re
                  const double2* __restrict__ eps_g, const double2* __restrict__ e2i_g,
                  const double* __restrict__ pas_g, double2* __restrict__ local) {
   const int p = PT ? PT : p_rt;
-  const int pw = p + 2;
-  constexpr int NC = PT ? (PT + 31) / 32 : 2;   // coefficients per lane
   extern __shared__ double2 l2_sh[];   // per warp: xl [p] | xg [p]
   pdl_trigger();
   pdl_wait();   // the parents' final locals (previous level / M2L)
@@ -601,63 +671,64 @@ l2l_level_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __re
   for (int c = c0 + blockIdx.x * kPassWarps + w; c < c1; c += gridDim.x * kPassWarps) {
     const int cs = c_start[c], ce = cs + c_count[c];
     if (ce <= own_lo || cs >= own_hi) continue;   // no owned target below c
-    const int P = c_parent[c];
-    const double2* lp = local + (size_t)P * 2 * p;
-    double2* out = local + (size_t)c * 2 * p;
-    const int quad = (c_ix[c] & 1) + 2 * (c_iy[c] & 1);
-    // loads first: parent coefficients (slots m, m+1 of lambda, m of gamma) and
-    // this cell's own M2L result
-    double2 pl[NC], pl1[NC], pg[NC], ol[NC], og[NC];
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc) {
-      const int m = lane + 32 * cc;
-      const bool ok = m < p;
-      const double2 z = make_double2(0.0, 0.0);
-      pl[cc] = ok ? lp[m] : z;
-      pl1[cc] = (ok && m + 1 < p) ? lp[m + 1] : z;
-      pg[cc] = ok ? lp[p + m] : z;
-      ol[cc] = ok ? out[m] : z;
-      og[cc] = ok ? out[p + m] : z;
+    l2l_cell<PT>(c, p, c_ix, c_iy, c_parent, eps_g, e2i_g, pas_g, local, xl, xg, lane);
+  }
+}
+
+// Subtree passes for small trees: CTA per cell R of the split
+// level Ls.  Upward: M2M of R's non-leaf descendants, deepest level first, and
+// of R itself (levels nlevels-1 .. Ls); downward: L2L of R's descendants,
+// levels Ls+1 .. nlevels-1 (R's local is final from the per-level kernels).
+// Levels are separated by __syncthreads (every cell of a level inside one
+// CTA): one launch per pass instead of one per level.  rng[R * nsl + (l - Ls)]
+// = the range of level l's entries below R: into up_list (upward) or into the
+// level's cells (downward).
+template <int PT>
+__global__ void __launch_bounds__(kPassWarps * 32)
+m2m_subtree_kernel(int Ls, int nlev, int nsl, const int2* __restrict__ rng,
+                   const int* __restrict__ up_list, const int* __restrict__ c_ix,
+                   const int* __restrict__ c_iy, const int* __restrict__ first_child,
+                   const int* __restrict__ nchild, int p_rt, const double* __restrict__ pasT_g,
+                   const double2* __restrict__ eps_g, const double2* __restrict__ e2i_g,
+                   double2* __restrict__ mpole) {
+  const int p = PT ? PT : p_rt;
+  pdl_trigger();
+  pdl_wait();   // leaf multipoles (P2M)
+  extern __shared__ double2 up_sh[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* wb = up_sh + (size_t)w * 8 * p;
+  for (int l = nlev - 1; l >= Ls; --l) {
+    const int2 r = rng[(size_t)blockIdx.x * nsl + (l - Ls)];
+    for (int k = r.x + w; k < r.y; k += kPassWarps)
+      m2m_cell<PT>(up_list[k], p, c_ix, c_iy, first_child, nchild, pasT_g, eps_g, e2i_g, mpole,
+                   wb, wb + 4 * p, lane);
+    __syncthreads();
+  }
+}
+
+template <int PT>
+__global__ void __launch_bounds__(kPassWarps * 32)
+l2l_subtree_kernel(int Ls, int nlev, int nsl, const int2* __restrict__ rng, int64_t own_lo,
+                   int64_t own_hi, const int* __restrict__ c_ix, const int* __restrict__ c_iy,
+                   const int* __restrict__ c_start, const int* __restrict__ c_count,
+                   const int* __restrict__ c_parent, int p_rt, const double2* __restrict__ eps_g,
+                   const double2* __restrict__ e2i_g, const double* __restrict__ pas_g,
+                   double2* __restrict__ local) {
+  const int p = PT ? PT : p_rt;
+  extern __shared__ double2 l2_sh[];
+  pdl_trigger();
+  pdl_wait();   // the roots' final locals
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* xl = l2_sh + (size_t)w * 2 * p;
+  double2* xg = xl + p;
+  for (int l = Ls + 1; l < nlev; ++l) {
+    const int2 r = rng[(size_t)blockIdx.x * nsl + (l - Ls)];
+    for (int c = r.x + w; c < r.y; c += kPassWarps) {
+      const int cs = c_start[c], ce = cs + c_count[c];
+      if (ce <= own_lo || cs >= own_hi) continue;
+      l2l_cell<PT>(c, p, c_ix, c_iy, c_parent, eps_g, e2i_g, pas_g, local, xl, xg, lane);
     }
-    const double2 epsb = make_double2(0.5 * ((quad & 1) - 0.5), -0.5 * ((quad >> 1) - 0.5));
-    const double2* E = eps_g + quad * pw;
-    const double2* Ei = e2i_g + quad * pw;
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc) {
-      const int m = lane + 32 * cc;
-      if (m < p) {
-        double2 gv = pg[cc];
-        cmac(gv, cscale(epsb, (double)(m + 1)), pl1[cc]);
-        const double2 em = __ldg(E + m);
-        xl[m] = cmul(pl[cc], em);
-        xg[m] = cmul(gv, em);
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc) {
-      const int k = lane + 32 * cc;
-      if (k < p) {
-        double2 l = make_double2(0.0, 0.0), g = l;
-#pragma unroll
-        for (int m = 0; m < pmax<PT>(); ++m) {
-          if (!PT && m >= p) break;
-          const double pc = __ldg(pas_g + m * p + k);   // C(m, k)
-          const double2 x = xl[m], y = xg[m];
-          l.x = fma(x.x, pc, l.x);
-          l.y = fma(x.y, pc, l.y);
-          g.x = fma(y.x, pc, g.x);
-          g.y = fma(y.y, pc, g.y);
-        }
-        const double2 ek = __ldg(Ei + k);
-        double2 al = ol[cc], ag = og[cc];
-        cmac(al, l, ek);
-        cmac(ag, g, ek);
-        out[k] = al;
-        out[p + k] = ag;
-      }
-    }
-    __syncwarp();
+    __syncthreads();
   }
 }
 
@@ -870,6 +941,18 @@ static bool use_pdl(const ddm_tree_s* t) {
   return env >= 0 ? env != 0 : t->n <= 200000;
 }
 
+// Subtree passes (one launch per pass below the split level) on small trees,
+// where the per-level launches are the chain's latency; DDM_SUBTREE=0/1
+// overrides.
+static bool use_subtrees(const ddm_tree_s* t) {
+  static const int env = [] {
+    const char* e = getenv("DDM_SUBTREE");
+    return e ? atoi(e) : -1;
+  }();
+  if (t->sub_n <= 0) return false;
+  return env >= 0 ? env != 0 : t->n <= 200000;
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(bool on, void (*kernel)(KArgs...), unsigned grid, unsigned block,
                        size_t shm, cudaStream_t s, Args... args) {
@@ -909,7 +992,19 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
     stage_end(ctx, DDM_ST_P2M, s);                                                              \
     if ((rc = set_smem(ctx, m2m_level_kernel<PT>, shm))) return rc;                             \
     stage_begin(ctx, DDM_ST_M2M, s);                                                            \
-    for (int lev = t->nlevels - 1; lev >= 2; --lev) {                                           \
+    int top = t->nlevels - 1;                                                                   \
+    if (use_subtrees(t)) {                                                                      \
+      if ((rc = set_smem(ctx, m2m_subtree_kernel<PT>, shm))) return rc;                         \
+      DDM_CUDA(ctx, launch_pdl(use_pdl(t), m2m_subtree_kernel<PT>, t->sub_n, kPassWarps * 32,   \
+                               shm, s, t->sub_Ls, t->nlevels, t->sub_nsl,                       \
+                               (const int2*)t->sub_up, (const int*)t->up_list,                  \
+                               (const int*)t->c_ix, (const int*)t->c_iy,                        \
+                               (const int*)t->c_first_child, (const int*)t->c_nchild, p,        \
+                               (const double*)t->op_pasT, (const double2*)t->op_eps,            \
+                               (const double2*)t->op_e2i, t->mpole));                           \
+      top = t->sub_Ls - 1;                                                                      \
+    }                                                                                           \
+    for (int lev = top; lev >= 2; --lev) {                                                      \
       const int u0 = t->up_level_off[2 * lev], u1 = t->up_level_off[2 * lev + 1];               \
       if (u1 <= u0) continue;                                                                   \
       const int nb2 = pass_grid(ctx, (const void*)m2m_level_kernel<PT>, shm, u1 - u0);          \
@@ -955,7 +1050,8 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     stage_end(ctx, DDM_ST_M2L, s);                                                              \
     if ((rc = set_smem(ctx, l2l_level_kernel<PT>, shm2))) return rc;                            \
     stage_begin(ctx, DDM_ST_L2L, s);                                                            \
-    for (int lev = 3; lev < t->nlevels; ++lev) {                                                \
+    const bool sub = use_subtrees(t);                                                           \
+    for (int lev = 3; lev < (sub ? t->sub_Ls + 1 : t->nlevels); ++lev) {                        \
       const int a = t->level_off[lev], b = t->level_off[lev + 1];                               \
       if (b <= a) continue;                                                                     \
       const int nb2 = pass_grid(ctx, (const void*)l2l_level_kernel<PT>, shm2, b - a);           \
@@ -966,6 +1062,17 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
                                (const int*)t->c_parent, p, (const double2*)t->op_eps,          \
                                (const double2*)t->op_e2i, (const double*)t->op_pas,            \
                                t->local));                                                     \
+    }                                                                                           \
+    if (sub) {                                                                                  \
+      if ((rc = set_smem(ctx, l2l_subtree_kernel<PT>, shm2))) return rc;                        \
+      DDM_CUDA(ctx, launch_pdl(use_pdl(t), l2l_subtree_kernel<PT>, t->sub_n, kPassWarps * 32,   \
+                               shm2, s, t->sub_Ls, t->nlevels, t->sub_nsl,                      \
+                               (const int2*)t->sub_cells, (int64_t)t->own_el_lo,                \
+                               (int64_t)t->own_el_hi, (const int*)t->c_ix,                      \
+                               (const int*)t->c_iy, (const int*)t->c_start,                     \
+                               (const int*)t->c_count, (const int*)t->c_parent, p,              \
+                               (const double2*)t->op_eps, (const double2*)t->op_e2i,            \
+                               (const double*)t->op_pas, t->local));                            \
     }                                                                                           \
     stage_end(ctx, DDM_ST_L2L, s);                                                              \
   } while (0)

@@ -520,7 +520,7 @@ void free_tree(ddm_tree_s* t) {
                   t->op_eps, t->op_e2i, t->mpole, t->local, t->src, t->part, t->d_sorted, t->y_sorted, t->y_far,
                   t->part_direct, t->up_list, t->ready_up, t->ready_down, t->tickets,
                   t->krylov, t->pc, t->gm_w, t->gm_tmp, t->gm_part, t->bb_w, t->bb_f,
-                  t->pc_chunks, t->pc_off, t->pcl, t->st_elem, t->st_code, t->rbeg, t->srec, t->nc, t->nc_off, t->gm_dev, t->gm_ticket};
+                  t->pc_chunks, t->pc_off, t->pcl, t->st_elem, t->st_code, t->rbeg, t->srec, t->nc, t->nc_off, t->gm_dev, t->gm_ticket, t->sub_up, t->sub_cells};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (double* p : t->hc_lag)
@@ -881,6 +881,69 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
                                     cudaMemcpyHostToDevice, s));
     DDM_CUDA(ctx, cudaMemsetAsync(t->ready_up, 0, ncells * sizeof(int), s));
     DDM_CUDA(ctx, cudaMemsetAsync(t->ready_down, 0, 2 * ncells * sizeof(int), s));
+
+    // subtree schedule (expansions.cu subtree passes): split level Ls = the
+    // first level >= 3 with >= 128 cells, if at least two levels lie below it
+    int Ls = -1;
+    for (int lev = 3; lev < t->nlevels; ++lev)
+      if (t->level_off[lev + 1] - t->level_off[lev] >= 128) {
+        Ls = lev;
+        break;
+      }
+    t->sub_n = 0;
+    std::vector<int2> sup, scell;
+    if (Ls > 0 && t->nlevels - 1 - Ls >= 2) {
+      std::vector<int> hpar(ncells);
+      DDM_CUDA(ctx, cudaMemcpyAsync(hpar.data(), C.parent, ncells * sizeof(int),
+                                    cudaMemcpyDeviceToHost, s));
+      DDM_CUDA(ctx, cudaStreamSynchronize(s));
+      const int nroot = t->level_off[Ls + 1] - t->level_off[Ls];
+      const int nsl = t->nlevels - Ls;
+      // root of every cell at level >= Ls (parents precede children by level)
+      std::vector<int> root(ncells, -1);
+      for (int c = t->level_off[Ls]; c < t->level_off[Ls + 1]; ++c) root[c] = c - t->level_off[Ls];
+      for (int lev = Ls + 1; lev < t->nlevels; ++lev)
+        for (int c = t->level_off[lev]; c < t->level_off[lev + 1]; ++c) root[c] = root[hpar[c]];
+      sup.assign((size_t)nroot * nsl, make_int2(0, 0));
+      scell.assign((size_t)nroot * nsl, make_int2(0, 0));
+      for (int lev = Ls; lev < t->nlevels; ++lev) {
+        const int L = lev - Ls;
+        for (int c = t->level_off[lev]; c < t->level_off[lev + 1]; ++c) {
+          int2& r = scell[(size_t)root[c] * nsl + L];
+          if (r.y == r.x) r = make_int2(c, c + 1); else r.y = c + 1;   // contiguous (Morton)
+        }
+        for (int k = t->up_level_off[2 * lev]; k < t->up_level_off[2 * lev + 1]; ++k) {
+          int2& r = sup[(size_t)root[up[k]] * nsl + L];
+          if (r.y == r.x) r = make_int2(k, k + 1); else r.y = k + 1;
+        }
+      }
+      // the ranges must be exactly the subtree's entries (Morton contiguity)
+      std::vector<int> cnt_c((size_t)nroot * nsl, 0), cnt_u((size_t)nroot * nsl, 0);
+      for (int lev = Ls; lev < t->nlevels; ++lev) {
+        for (int c = t->level_off[lev]; c < t->level_off[lev + 1]; ++c)
+          ++cnt_c[(size_t)root[c] * nsl + (lev - Ls)];
+        for (int k = t->up_level_off[2 * lev]; k < t->up_level_off[2 * lev + 1]; ++k)
+          ++cnt_u[(size_t)root[up[k]] * nsl + (lev - Ls)];
+      }
+      bool ok = true;
+      for (size_t i = 0; i < cnt_c.size(); ++i)
+        ok = ok && cnt_c[i] == scell[i].y - scell[i].x && cnt_u[i] == sup[i].y - sup[i].x;
+      if (!ok) Ls = -1;
+    }
+    if (Ls > 0 && t->nlevels - 1 - Ls >= 2) {
+      const int nroot = t->level_off[Ls + 1] - t->level_off[Ls];
+      const int nsl = t->nlevels - Ls;
+      if ((rc = dalloc(ctx, &t->sub_up, sup.size())) || (rc = dalloc(ctx, &t->sub_cells, scell.size())))
+        return rc;
+      DDM_CUDA(ctx, cudaMemcpyAsync(t->sub_up, sup.data(), sup.size() * sizeof(int2),
+                                    cudaMemcpyHostToDevice, s));
+      DDM_CUDA(ctx, cudaMemcpyAsync(t->sub_cells, scell.data(), scell.size() * sizeof(int2),
+                                    cudaMemcpyHostToDevice, s));
+      DDM_CUDA(ctx, cudaStreamSynchronize(s));
+      t->sub_Ls = Ls;
+      t->sub_n = nroot;
+      t->sub_nsl = nsl;
+    }
   }
   DDM_CUDA(ctx, cudaStreamSynchronize(s));
   return DDM_OK;
