@@ -1093,19 +1093,25 @@ poro_near_apply_kernel(const int* __restrict__ order, const int4* __restrict__ i
 // lane = (target, source slice); per (pair, lag) 9 FMA on a 72-B block (HBM
 // bound).  Same partial layout as poro_hist_near_kernel.
 constexpr int kLagChunk = 16;
-constexpr int kHistWarps = 8;   // warps per item, splitting the lag chunks
+constexpr int kHistWarps = 8;   // warps per (item, lag chunk) block, splitting the sources
 
+// grid (owned item i, lag chunk q): the block sums lags 16q+1 .. 16q+16 of
+// every pair of item order[i] (its warps take interleaved source groups) and
+// writes its per-target partial to hpart[q][i][t][3]; poro_hist_reduce sums
+// the chunks in order (deterministic).
 __global__ void __launch_bounds__(kHistWarps * 32)
 poro_hist_cached_kernel(const int* __restrict__ order, const int4* __restrict__ items,
-                        int item_lo, const int* __restrict__ u_off, const int* __restrict__ u_lo,
-                        const int* __restrict__ u_hi, const int* __restrict__ leaves,
-                        const int* __restrict__ c_start, const int* __restrict__ c_count,
-                        const double* __restrict__ Hs, int h, const int64_t* __restrict__ ioff,
-                        const double* const* __restrict__ chunks, double* __restrict__ part3) {
+                        int item_lo, int nown, const int* __restrict__ u_off,
+                        const int* __restrict__ u_lo, const int* __restrict__ u_hi,
+                        const int* __restrict__ leaves, const int* __restrict__ c_start,
+                        const int* __restrict__ c_count, const double* __restrict__ Hs, int h,
+                        const int64_t* __restrict__ ioff, const double* const* __restrict__ chunks,
+                        double* __restrict__ hpart) {
   __shared__ double red[kHistWarps][3][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hs = (h + 2) * 3;
-  const int it = order[blockIdx.x];
+  const int oi = blockIdx.x, q = blockIdx.y;
+  const int it = order[oi];
   const int4 item = items[it];
   const int kk = item.x;
   const int c = leaves[kk];
@@ -1113,38 +1119,35 @@ poro_hist_cached_kernel(const int* __restrict__ order, const int4* __restrict__ 
   const int S = 32 / nt;
   const int tl = lane % nt, slice = lane / nt;
   const bool active = slice < S;
-  const int64_t off0 = ioff[it - item_lo] * kLagChunk;
+  const int l0 = q * kLagChunk;
+  const int ln = min(kLagChunk, h + 1 - l0);
+  const double* ch = chunks[q] + ioff[it - item_lo] * kLagChunk;
   double os = 0.0, on = 0.0, op = 0.0;
   if (active) {
-    for (int l0 = w * kLagChunk; l0 <= h; l0 += kHistWarps * kLagChunk) {
-      const double* ch = chunks[l0 / kLagChunk] + off0;
-      const int ln = min(kLagChunk, h + 1 - l0);
-      int pos = 0;
-      for (int r = u_off[kk], rend = u_off[kk + 1]; r < rend && pos < item.w; ++r) {
-        const int lo = u_lo[r], len = u_hi[r] - lo;
-        const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
-        for (int j = b + slice; j < e; j += S) {
-          const double* bb0 =
-              ch + ((int64_t)(pos + j - item.z) * kLagChunk * kTgtGroup + tl) * 9;
-          // lags l = l0+1 .. l0+ln: E_l = D^(h+1-l) - D^(h-l) = H[h+2-l] - H[h+1-l]
-          const double* H = Hs + (int64_t)(lo + j) * hs + (h + 1 - l0) * 3;
-          double dp0 = __ldg(H), dp1 = __ldg(H + 1), dp2 = __ldg(H + 2);
+    int pos = 0;
+    for (int r = u_off[kk], rend = u_off[kk + 1]; r < rend && pos < item.w; ++r) {
+      const int lo = u_lo[r], len = u_hi[r] - lo;
+      const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
+      for (int j = b + slice + S * w; j < e; j += S * kHistWarps) {
+        const double* bb0 = ch + ((int64_t)(pos + j - item.z) * kLagChunk * kTgtGroup + tl) * 9;
+        // lags l = l0+1 .. l0+ln: E_l = D^(h+1-l) - D^(h-l) = H[h+2-l] - H[h+1-l]
+        const double* H = Hs + (int64_t)(lo + j) * hs + (h + 1 - l0) * 3;
+        double dp0 = __ldg(H), dp1 = __ldg(H + 1), dp2 = __ldg(H + 2);
 #pragma unroll 4
-          for (int li = 0; li < ln; ++li) {
-            const double* Db = H - 3 * (li + 1);
-            const double d0 = __ldg(Db), d1 = __ldg(Db + 1), d2 = __ldg(Db + 2);
-            const double e0 = dp0 - d0, e1 = dp1 - d1, e2 = dp2 - d2;
-            dp0 = d0;
-            dp1 = d1;
-            dp2 = d2;
-            const double* bb = bb0 + li * (kTgtGroup * 9);
-            os = fma(__ldg(bb + 0), e0, fma(__ldg(bb + 1), e1, fma(__ldg(bb + 2), e2, os)));
-            on = fma(__ldg(bb + 3), e0, fma(__ldg(bb + 4), e1, fma(__ldg(bb + 5), e2, on)));
-            op = fma(__ldg(bb + 6), e0, fma(__ldg(bb + 7), e1, fma(__ldg(bb + 8), e2, op)));
-          }
+        for (int li = 0; li < ln; ++li) {
+          const double* Db = H - 3 * (li + 1);
+          const double d0 = __ldg(Db), d1 = __ldg(Db + 1), d2 = __ldg(Db + 2);
+          const double e0 = dp0 - d0, e1 = dp1 - d1, e2 = dp2 - d2;
+          dp0 = d0;
+          dp1 = d1;
+          dp2 = d2;
+          const double* bb = bb0 + li * (kTgtGroup * 9);
+          os = fma(__ldg(bb + 0), e0, fma(__ldg(bb + 1), e1, fma(__ldg(bb + 2), e2, os)));
+          on = fma(__ldg(bb + 3), e0, fma(__ldg(bb + 4), e1, fma(__ldg(bb + 5), e2, on)));
+          op = fma(__ldg(bb + 6), e0, fma(__ldg(bb + 7), e1, fma(__ldg(bb + 8), e2, op)));
         }
-        pos += len;
       }
+      pos += len;
     }
   }
   red[w][0][lane] = os;
@@ -1155,16 +1158,28 @@ poro_hist_cached_kernel(const int* __restrict__ order, const int4* __restrict__ 
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     if (lane < nt)
       for (int ww = 0; ww < kHistWarps; ++ww)
-        for (int q = 0; q < S; ++q) {
-          s0 += red[ww][0][lane + q * nt];
-          s1 += red[ww][1][lane + q * nt];
-          s2 += red[ww][2][lane + q * nt];
+        for (int sl = 0; sl < S; ++sl) {
+          s0 += red[ww][0][lane + sl * nt];
+          s1 += red[ww][1][lane + sl * nt];
+          s2 += red[ww][2][lane + sl * nt];
         }
-    double* o = part3 + ((int64_t)it * kTgtGroup + lane) * 3;
+    double* o = hpart + (((int64_t)q * nown + oi) * kTgtGroup + lane) * 3;
     o[0] = s0;
     o[1] = s1;
     o[2] = s2;
   }
+}
+
+// part3[item order[i]][t] = sum over the lag chunks q (in order) of hpart[q][i][t]
+__global__ void poro_hist_reduce(int nown, int nch, const int* __restrict__ order,
+                                 const double* __restrict__ hpart, double* __restrict__ part3) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;   // (i, t, comp)
+  if (e >= (int64_t)nown * kTgtGroup * 3) return;
+  const int i = (int)(e / (kTgtGroup * 3));
+  const int rem = (int)(e - (int64_t)i * kTgtGroup * 3);
+  double s = 0.0;
+  for (int q = 0; q < nch; ++q) s += hpart[(int64_t)q * nown * kTgtGroup * 3 + e];
+  part3[(int64_t)order[i] * kTgtGroup * 3 + rem] = s;
 }
 
 // ---------------------------------------------------------------- fast history (f1)
@@ -1697,10 +1712,19 @@ int launch_poro_hist_cached(ddm_ctx_s* ctx, ddm_tree_s* t, int h, const double* 
                             cudaStream_t s) {
   const int nown = t->item_hi_owned - t->item_lo_owned;
   if (nown <= 0) return DDM_OK;
-  poro_hist_cached_kernel<<<nown, kHistWarps * 32, 0, s>>>(
-      t->p2p_order, t->items, t->item_lo_owned, t->u_off, t->u_lo, t->u_hi, t->leaves,
-      t->c_start, t->c_count, Hs, h, t->nc_off, t->hc_ptrs, reinterpret_cast<double*>(t->part));
+  const int nch = (h + 1 + kLagChunk - 1) / kLagChunk;
+  double* hpart = nullptr;
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&hpart, (size_t)nch * nown * kTgtGroup * 3 * sizeof(double),
+                                s));
+  poro_hist_cached_kernel<<<dim3(nown, nch), kHistWarps * 32, 0, s>>>(
+      t->p2p_order, t->items, t->item_lo_owned, nown, t->u_off, t->u_lo, t->u_hi, t->leaves,
+      t->c_start, t->c_count, Hs, h, t->nc_off, t->hc_ptrs, hpart);
   DDM_CUDA(ctx, cudaGetLastError());
+  const int64_t ne = (int64_t)nown * kTgtGroup * 3;
+  poro_hist_reduce<<<nblk(ne, 256), 256, 0, s>>>(nown, nch, t->p2p_order, hpart,
+                                                 reinterpret_cast<double*>(t->part));
+  DDM_CUDA(ctx, cudaGetLastError());
+  cudaFreeAsync(hpart, s);
   return DDM_OK;
 }
 
