@@ -28,7 +28,10 @@ constexpr int kSrcChunk = DDM_SRC_CHUNK;  // max sources per P2P work item
 constexpr int kSrcStride = 12;  // doubles per direct-mode source record
 constexpr int kRecStride = 10;  // doubles per near-field stream record (node + 4 complex coefficients)
 constexpr int kChainMax = 256;  // leaves with more elements keep Morton order (no node sharing)
-constexpr int kPcChunk = 32;    // max elements per leaf-block preconditioner block
+#ifndef DDM_PC_CHUNK
+#define DDM_PC_CHUNK 32
+#endif
+constexpr int kPcChunk = DDM_PC_CHUNK;   // max elements per leaf-block preconditioner block
 
 struct Status {
   int code = DDM_OK;

@@ -1,0 +1,8 @@
+# leaf-block Jacobi chunk size (elements per block): GMRES iterations / time, configs 3 and 4
+cd $GRAFT_REPO_ROOT
+for ch in 32 48 64; do
+  python -c "from paper_1812_05087_b200 import build as B; B.build(defines=['DDM_PC_CHUNK=$ch'], out='/tmp/ddm_pc$ch.so', force=True)" > /dev/null 2>&1
+  echo "chunk $ch"
+  DDM_LIB=/tmp/ddm_pc$ch.so python scripts/gmres_probe.py 2>&1 | grep "solve 2"
+  DDM_LIB=/tmp/ddm_pc$ch.so python scripts/march_guess.py 2>&1 | grep extrap3
+done
