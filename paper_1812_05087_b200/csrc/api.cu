@@ -190,7 +190,8 @@ static void drop_owned_state(ddm_tree_s* t) {
     g.exec = nullptr;
   }
   for (auto& k : t->seen_keys) k = MatvecKey();
-  for (double* p : t->hc_lag) cudaFree(p);
+  for (double* p : t->hc_alloc) cudaFree(p);
+  t->hc_alloc.clear();
   t->hc_lag.clear();
   t->hc_nlags = 0;
   t->hc_valid = t->hc_seen_set = t->hc_capped = false;

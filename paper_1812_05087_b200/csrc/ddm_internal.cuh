@@ -209,6 +209,7 @@ struct ddm_tree_s {
   // poroelastic part K^p(j dt) of every owned near pair, in chunks of lags
   // (nc_off item layout x kLagChunk), built as the history grows
   std::vector<double*> hc_lag;    // device chunks of kLagChunk lags ([item][jpos][lag][t][9])
+  std::vector<double*> hc_alloc;  // the allocations holding them (doubling groups of chunks)
   int hc_nlags = 0;               // lags built (1..hc_nlags)
   int hc_max_chunks = 0;          // chunk budget (memory) fixed when the cache is keyed
   double** hc_ptrs = nullptr;     // device copy of hc_lag

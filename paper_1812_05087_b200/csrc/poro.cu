@@ -1645,7 +1645,8 @@ bool poro_hist_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* m
     std::memcpy(t->hc_seen, key, sizeof(key));
     t->hc_seen_set = true;
     if (!repeat) return false;
-    for (double* p : t->hc_lag) cudaFree(p);
+    for (double* p : t->hc_alloc) cudaFree(p);
+    t->hc_alloc.clear();
     t->hc_lag.clear();
     t->hc_nlags = 0;
     // chunk budget, fixed at creation (no memory queries while the history
@@ -1673,14 +1674,17 @@ bool poro_hist_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* m
           t->hc_capped = true;
           break;
         }
-        // plain cudaMalloc (~4 ms at any size); growing the stream-ordered
-        // pool by a chunk stalled the host for 10-800 ms (scripts/micro/alloc.cu)
+        // plain cudaMalloc (~4 ms at any size; growing the stream-ordered
+        // pool by a chunk stalled the host for 10-800 ms, scripts/micro/alloc.cu),
+        // as many chunks as already exist (doubling: O(log) allocations)
+        const int k = std::min(std::max(1, (int)t->hc_lag.size()), t->hc_max_chunks - ci);
         double* blk = nullptr;
-        if ((rc = dalloc(ctx, &blk, (size_t)t->nc_n * kLagChunk))) {
+        if ((rc = dalloc(ctx, &blk, (size_t)t->nc_n * kLagChunk * k))) {
           *rc_out = rc;
           return false;
         }
-        t->hc_lag.push_back(blk);
+        t->hc_alloc.push_back(blk);
+        for (int q = 0; q < k; ++q) t->hc_lag.push_back(blk + (size_t)q * t->nc_n * kLagChunk);
       }
       poro_near_build_kernel<<<nblk(nown, 4), 128, 0, s>>>(
           nown, t->p2p_order, t->items, t->item_lo_owned, t->u_off, t->u_lo, t->u_hi, t->leaves,

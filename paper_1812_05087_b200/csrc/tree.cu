@@ -523,7 +523,7 @@ void free_tree(ddm_tree_s* t) {
                   t->pc_chunks, t->pc_off, t->pcl, t->st_elem, t->st_code, t->rbeg, t->srec, t->nc, t->nc_off, t->gm_dev, t->gm_ticket, t->sub_up, t->sub_cells};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  for (double* p : t->hc_lag)
+  for (double* p : t->hc_alloc)
     if (p) cudaFree(p);
   if (t->hc_ptrs) cudaFree(t->hc_ptrs);
   for (auto& g : t->graphs)
