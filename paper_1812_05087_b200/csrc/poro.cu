@@ -905,6 +905,8 @@ __global__ void poro_direct_kernel(int64_t n, int64_t t_lo, int64_t t_hi,
 // pair: HBM bound).  Layout per item: block (jpos, t) at
 // nc_off[item] + (jpos kTgtGroup + t) 9, row r = (sigma_s, sigma_n, p), column c =
 // (Ds, Dn, q), ABI convention.
+constexpr int kBuildGroups = 8;   // warps per item in the block builds
+
 __global__ void __launch_bounds__(128)
 poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ items,
                        int item_lo, const int* __restrict__ u_off, const int* __restrict__ u_lo,
@@ -918,7 +920,11 @@ poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __re
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   NearQueue& Q = nq[w];
   const unsigned lt_mask = (1u << lane) - 1u;
-  for (int oi = blockIdx.x * 4 + w; oi < nown; oi += gridDim.x * 4) {
+  // warp task = (owned item, source group grp of kBuildGroups): the item's
+  // rounds of S sources are dealt round-robin to its groups (the blocks of a
+  // pair are written by exactly one warp: disjoint, no ordering needed)
+  for (int task = blockIdx.x * 4 + w; task < nown * kBuildGroups; task += gridDim.x * 4) {
+    const int oi = task / kBuildGroups, grp = task - oi * kBuildGroups;
     const int it = order[oi];
     const int4 item = items[it];
     const int kk = item.x;
@@ -964,6 +970,7 @@ poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __re
       const int lo = u_lo[r], len = u_hi[r] - lo;
       const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
       for (int jb = b; jb < e; jb += S) {
+        if (((pos + jb - item.z) / S) % kBuildGroups != grp) continue;   // another warp's round
         const int j = jb + slice;
         const bool have = active && j < e;
         const int jpos = pos + j - item.z;
@@ -1592,7 +1599,7 @@ int poro_near_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, c
     if ((rc = dalloc(ctx, &t->nc, (size_t)t->nc_n))) return rc;
   }
   t->nc_valid = false;
-  poro_near_build_kernel<<<nblk(nown, 4), 128, 0, s>>>(
+  poro_near_build_kernel<<<nblk((int64_t)nown * kBuildGroups, 4), 128, 0, s>>>(
       nown, t->p2p_order, t->items, t->item_lo_owned, t->u_off, t->u_lo, t->u_hi, t->leaves,
       t->c_start, t->c_count, t->ex, t->ey, t->ea, t->ec, t->es, k, 1, 1, 0, t->nc_off, t->nc);
   DDM_CUDA(ctx, cudaGetLastError());
@@ -1686,7 +1693,7 @@ bool poro_hist_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* m
         t->hc_alloc.push_back(blk);
         for (int q = 0; q < k; ++q) t->hc_lag.push_back(blk + (size_t)q * t->nc_n * kLagChunk);
       }
-      poro_near_build_kernel<<<nblk(nown, 4), 128, 0, s>>>(
+      poro_near_build_kernel<<<nblk((int64_t)nown * kBuildGroups, 4), 128, 0, s>>>(
           nown, t->p2p_order, t->items, t->item_lo_owned, t->u_off, t->u_lo, t->u_hi, t->leaves,
           t->c_start, t->c_count, t->ex, t->ey, t->ea, t->ec, t->es,
           to_const(poro_params(mat, j * dt)), 0, kLagChunk, (j - 1) % kLagChunk, t->nc_off,
