@@ -187,6 +187,8 @@ struct ddm_tree_s {
   int* rbeg = nullptr;            // [n+1] first record of each slot (its break record if unlinked)
   double* srec = nullptr;         // [nrec][kRecStride]; record 0 = pad
   int64_t nrec = 0;
+  int* it_roff = nullptr;         // [nitems+1] first record range of each P2P item
+  int2* it_rng = nullptr;         // record ranges [rb, re) of each item's source window
   double2* part = nullptr;        // [nitems*32] partial tractions
   double* d_sorted = nullptr;     // [n*3] D gathered into sorted order
   double* y_sorted = nullptr;     // [n*3]

@@ -4,6 +4,8 @@
 // multiplication ... is used for points that are not well-separated"
 // (P:536-538), "P2P term, to account for the self and neighbor interactions"
 // (P:868-877).
+#include <algorithm>
+
 #include "kcommon.cuh"
 
 namespace ddm {
@@ -200,6 +202,46 @@ __global__ void break_records_kernel(int64_t n, const int* __restrict__ st_elem,
   for (int f = 1; f < kRecStride / 2; ++f) o[f] = make_double2(0.0, 0.0);
 }
 
+// Record ranges of every P2P item: the item's window [item.z, item.w) of
+// its leaf's concatenated U ranges, mapped to stream records (rbeg).  One
+// entry per intersecting U range; the P2P kernel reads one int2 per range
+// instead of chasing u_lo/u_hi -> rbeg -> records.
+__global__ void item_rng_count(int nitems, const int4* __restrict__ items,
+                               const int* __restrict__ u_off, const int* __restrict__ u_lo,
+                               const int* __restrict__ u_hi, int* __restrict__ cnt) {
+  const int it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it > nitems) return;
+  if (it == nitems) {
+    cnt[it] = 0;
+    return;
+  }
+  const int4 item = items[it];
+  int pos = 0, n = 0;
+  for (int r = u_off[item.x], rend = u_off[item.x + 1]; r < rend && pos < item.w; ++r) {
+    const int len = u_hi[r] - u_lo[r];
+    const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
+    if (b < e) ++n;
+    pos += len;
+  }
+  cnt[it] = n;
+}
+
+__global__ void item_rng_fill(int nitems, const int4* __restrict__ items,
+                              const int* __restrict__ u_off, const int* __restrict__ u_lo,
+                              const int* __restrict__ u_hi, const int* __restrict__ rbeg,
+                              const int* __restrict__ roff, int2* __restrict__ rng) {
+  const int it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= nitems) return;
+  const int4 item = items[it];
+  int pos = 0, o = roff[it];
+  for (int r = u_off[item.x], rend = u_off[item.x + 1]; r < rend && pos < item.w; ++r) {
+    const int lo = u_lo[r], len = u_hi[r] - lo;
+    const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
+    if (b < e) rng[o++] = make_int2(rbeg[lo + b], rbeg[lo + e]);
+    pos += len;
+  }
+}
+
 // Per stream slot (every matvec): the element's record from its DDs,
 //   B = (D_s + i D_n) e, r = conj(e)^2, Bh = B/2, Q' = -(r B + conj B),
 //   P1 = Bh (r - 1), P2 = i Bh (r + 1)   (negated for a flipped element)
@@ -278,7 +320,8 @@ __device__ __forceinline__ void record_update(P2PAcc& acc, NodeCarry& n, double 
 }
 
 // One warp per work item (leaf k, group of nt <= kTgtGroup targets, interval
-// [item.z, item.w) of the leaf's concatenated source-slot ranges).  Each lane
+// [item.z, item.w) of the leaf's concatenated source-slot ranges, read as the
+// item's record ranges it_rng[it_roff[it] .. it_roff[it+1])).  Each lane
 // owns kTPL targets (independent chains sharing every record load); the
 // tp = ceil(nt/kTPL) lane-target slots are replicated over S = 32 / tp source
 // slices, and slice s takes the s-th contiguous part of each range's records
@@ -318,10 +361,10 @@ __device__ __forceinline__ void load_rec(double (&sp)[kRecStride], const double*
 
 __global__ void __launch_bounds__(kP2PWarps * 32, DDM_P2P_MINB)
 p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ items,
-           const int* __restrict__ u_off, const int* __restrict__ u_lo,
-           const int* __restrict__ u_hi, const int* __restrict__ leaves,
+           const int* __restrict__ leaves,
            const int* __restrict__ c_start, const int* __restrict__ c_count,
-           const int* __restrict__ rbeg, const double* __restrict__ srec,
+           const int* __restrict__ it_roff, const int2* __restrict__ it_rng,
+           const double* __restrict__ srec,
            const double* __restrict__ ex, const double* __restrict__ ey,
            const double* __restrict__ ec, const double* __restrict__ es, double gc,
            double2* __restrict__ part) {
@@ -346,13 +389,11 @@ p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ ite
       zy[q] = ey[ti];
     }
     if (active) {
-      int pos = 0;   // position in the concatenated slot space
-      for (int r = u_off[k], rend = u_off[k + 1]; r < rend && pos < item.w; ++r) {
-        const int lo = u_lo[r], len = u_hi[r] - lo;
-        const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
-        pos += len;
-        if (b >= e) continue;
-        const int rb = __ldg(rbeg + lo + b), L = __ldg(rbeg + lo + e) - rb;
+      const int e0 = __ldg(it_roff + it), e1 = __ldg(it_roff + it + 1);
+      int2 rr = e0 < e1 ? __ldg(it_rng + e0) : make_int2(0, 0);
+      for (int ei = e0; ei < e1; ++ei) {
+        const int rb = rr.x, L = rr.y - rr.x;
+        if (ei + 1 < e1) rr = __ldg(it_rng + ei + 1);   // next range's bounds in flight
         const int q0 = rb + (int)(((int64_t)L * slice) / S);
         const int q1 = rb + (int)(((int64_t)L * (slice + 1)) / S);
         if (q0 >= q1) continue;
@@ -366,11 +407,6 @@ p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ ite
 #pragma unroll kP2PUnroll
         for (int j = q0; j < q1; ++j) {
           double sp[kRecStride];
-          if (kP2PPrefetch > 0) {   // L1 prefetch of the record kP2PPrefetch ahead (no registers)
-            const double* pf = srec + (int64_t)min(j + kP2PPrefetch, q1 - 1) * kRecStride;
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(pf + kRecStride - 1));
-          }
           load_rec(sp, srec + (int64_t)j * kRecStride);
 #pragma unroll
           for (int q = 0; q < kTPL; ++q) record_update(acc[q], nc[q], zx[q], zy[q], sp);
@@ -466,10 +502,10 @@ int launch_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, double g
   // short-lived blocks (4 items each): slots free up continuously, so the
   // high-priority far-field kernels interleave with the near field
   const unsigned nb = nblk(item_hi - item_lo, kP2PWarps);
-  p2p_kernel<<<nb, kP2PWarps * 32, 0, s>>>(item_hi - item_lo, t->p2p_order, t->items, t->u_off,
-                                           t->u_lo, t->u_hi, t->leaves, t->c_start, t->c_count,
-                                           t->rbeg, t->srec, t->ex, t->ey, t->ec, t->es, gc,
-                                           t->part);
+  p2p_kernel<<<nb, kP2PWarps * 32, 0, s>>>(item_hi - item_lo, t->p2p_order, t->items,
+                                           t->leaves, t->c_start, t->c_count,
+                                           t->it_roff, t->it_rng, t->srec, t->ex, t->ey, t->ec,
+                                           t->es, gc, t->part);
   DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;
 }
@@ -500,6 +536,20 @@ int build_source_stream(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   const double2 pad = make_double2(t->x_min - 16.0 * t->W, t->y_min - 16.0 * t->W);
   break_records_kernel<<<nblk(n, 256), 256, 0, s>>>(n, t->st_elem, t->st_code, t->rbeg, t->ex,
                                                     t->ey, t->ea, t->ec, t->es, pad, t->srec);
+  DDM_CUDA(ctx, cudaGetLastError());
+  // record ranges of every P2P item
+  const int ni = t->nitems;
+  int* icnt = nullptr;
+  if ((rc = dalloc(ctx, &t->it_roff, (size_t)ni + 1)) || (rc = dalloc(ctx, &icnt, (size_t)ni + 1)))
+    return rc;
+  item_rng_count<<<nblk(ni + 1, 128), 128, 0, s>>>(ni, t->items, t->u_off, t->u_lo, t->u_hi, icnt);
+  DDM_CUDA(ctx, cudaGetLastError());
+  int nr = 0;
+  if ((rc = exclusive_scan_i32(ctx, icnt, t->it_roff, ni + 1, &nr, s))) return rc;
+  cudaFree(icnt);
+  if ((rc = dalloc(ctx, &t->it_rng, (size_t)std::max(nr, 1)))) return rc;
+  item_rng_fill<<<nblk(ni, 128), 128, 0, s>>>(ni, t->items, t->u_off, t->u_lo, t->u_hi, t->rbeg,
+                                              t->it_roff, t->it_rng);
   DDM_CUDA(ctx, cudaGetLastError());
   DDM_CUDA(ctx, cudaStreamSynchronize(s));
   return DDM_OK;
