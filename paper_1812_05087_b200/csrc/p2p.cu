@@ -501,7 +501,10 @@ int launch_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, double g
   if (item_hi <= item_lo) return DDM_OK;
   // short-lived blocks (4 items each): slots free up continuously, so the
   // high-priority far-field kernels interleave with the near field
-  const unsigned nb = nblk(item_hi - item_lo, kP2PWarps);
+#ifndef DDM_P2P_IPW
+#define DDM_P2P_IPW 1
+#endif
+  const unsigned nb = nblk(item_hi - item_lo, kP2PWarps * DDM_P2P_IPW);   // items per warp
   p2p_kernel<<<nb, kP2PWarps * 32, 0, s>>>(item_hi - item_lo, t->p2p_order, t->items,
                                            t->leaves, t->c_start, t->c_count,
                                            t->it_roff, t->it_rng, t->srec, t->ex, t->ey, t->ec,
