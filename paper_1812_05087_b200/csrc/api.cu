@@ -135,7 +135,7 @@ int check_material(ddm_ctx_s* ctx, const ddm_material* m) {
 
 // all-gather of the owned sorted rows y_sorted[lo..hi) into the full vector
 int allgather_sorted(ddm_ctx_s* ctx, ddm_tree_s* t, double* buf, int ncomp, cudaStream_t s) {
-  if (ctx->world == 1) return DDM_OK;
+  if (!ctx->exchange) return DDM_OK;
 #ifdef DDM_WITH_NCCL
   int64_t maxrows = 0;
   for (int r = 0; r < ctx->world; ++r)
@@ -169,7 +169,7 @@ int allgather_sorted(ddm_ctx_s* ctx, ddm_tree_s* t, double* buf, int ncomp, cuda
 }
 
 int allreduce_sum(ddm_ctx_s* ctx, double* buf, int64_t count, cudaStream_t s) {
-  if (ctx->world == 1) return DDM_OK;
+  if (!ctx->exchange) return DDM_OK;
 #ifdef DDM_WITH_NCCL
   ncclResult_t nr = ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, ctx->comm, s);
   if (nr != ncclSuccess)
@@ -336,14 +336,26 @@ int ddm_ctx_create(int device, const void* nccl_uid, int rank, int world, ddm_ct
       return rc;
     }
   }
-  if (world > 1) {
+  const bool force_nccl = [] {
+    const char* e = getenv("DDM_FORCE_NCCL");
+    return e && e[0] == '1';
+  }();
+  if (world > 1 || force_nccl) {
 #ifdef DDM_WITH_NCCL
-    if (!nccl_uid) {
-      *out = ctx;
-      return set_error(ctx, DDM_ERR_ARG, "world > 1 needs an ncclUniqueId");
-    }
     ncclUniqueId id;
-    std::memcpy(&id, nccl_uid, sizeof(id));
+    if (world == 1) {   // one-rank communicator (exchange path test)
+      if (ncclGetUniqueId(&id) != ncclSuccess) {
+        *out = ctx;
+        return set_error(ctx, DDM_ERR_NCCL, "ncclGetUniqueId");
+      }
+    } else {
+      if (!nccl_uid) {
+        *out = ctx;
+        return set_error(ctx, DDM_ERR_ARG, "world > 1 needs an ncclUniqueId");
+      }
+      std::memcpy(&id, nccl_uid, sizeof(id));
+    }
+    ctx->exchange = true;
     ncclResult_t nr = ncclCommInitRank(&ctx->comm, world, id, rank);
     if (nr != ncclSuccess) {
       *out = ctx;
@@ -503,7 +515,8 @@ int ddm_matvec(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double elap
     return set_error(ctx, DDM_ERR_ARG, "bad mode");
   cudaStream_t s = (cudaStream_t)stream;
   const int ncomp = mat->kind == 1 ? 3 : 2;
-  if (ctx->world == 1) return fmm_matvec(ctx, t, mat, elapsed, D, false, y, nullptr, mode, s);
+  if (!ctx->exchange) return fmm_matvec(ctx, t, mat, elapsed, D, false, y, nullptr, mode, s);
+  if ((rc = fmm_workspace(ctx, t, s))) return rc;   // t->y_sorted exists before it is passed
   rc = fmm_matvec(ctx, t, mat, elapsed, D, false, nullptr, t->y_sorted, mode, s);
   if (rc) return rc;
   stage_begin(ctx, DDM_ST_COMM, s);
@@ -555,7 +568,8 @@ int ddm_history_apply(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, doub
   if (h == 0 || mat->kind == 0) return DDM_OK;   // empty sum / elastic (R10)
   if (!D_hist) return set_error(ctx, DDM_ERR_ARG, "NULL D_hist");
   if (mode == DDM_FMM) {   // fast form (f1)
-    if (ctx->world == 1) return fmm_history(ctx, t, mat, dt, h, D_hist, r, nullptr, s);
+    if (!ctx->exchange) return fmm_history(ctx, t, mat, dt, h, D_hist, r, nullptr, s);
+    if ((rc = fmm_workspace(ctx, t, s))) return rc;   // t->y_sorted exists before it is passed
     rc = fmm_history(ctx, t, mat, dt, h, D_hist, nullptr, t->y_sorted, s);
     if (rc) return rc;
     stage_begin(ctx, DDM_ST_COMM, s);

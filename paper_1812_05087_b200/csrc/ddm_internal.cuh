@@ -49,6 +49,9 @@ struct StageEvents {
 struct ddm_ctx_s {
   int device = 0;
   int rank = 0, world = 1;
+  // owned rows are exchanged with NCCL (world > 1, or DDM_FORCE_NCCL=1 on one
+  // rank: the exchange path run on a one-rank communicator, for tests)
+  bool exchange = false;
   std::string err;
   bool profiling = false;
   ddm::StageEvents stage;
@@ -298,6 +301,7 @@ int fmm_init_operators(ddm_tree_s* t, cudaStream_t s);
 // D: [n][ncomp], user order (d_sorted = false) or sorted order (true), full
 // length.  Writes the owned rows into y_user (user order, via perm) and/or
 // y_sorted.  ncomp = 2 (elastic) or 3 (poroelastic, elapsed = tau).
+int fmm_workspace(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
 int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double elapsed,
                const double* D, bool d_sorted, double* y_user, double* y_sorted, int mode,
                cudaStream_t s);

@@ -21,7 +21,11 @@ double binom(int n, int k) {
   return r;
 }
 
-int ensure_workspace(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
+}  // namespace
+
+// Per-tree FMM workspaces (expansions, source records, partials, sorted
+// outputs) and the near-field source stream; idempotent.
+int fmm_workspace(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   int rc;
   if (!t->mpole) {
     if ((rc = dalloc(ctx, &t->mpole, (size_t)t->ncells * 2 * t->p))) return rc;
@@ -35,7 +39,6 @@ int ensure_workspace(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   return build_source_stream(ctx, t, s);
 }
 
-}  // namespace
 
 // Translation operators (host, fp64), uploaded once per tree.  Every
 // translation of DESIGN.md §4 factors as  post-scale x (real Pascal matrix) x
@@ -126,7 +129,7 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
 int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double elapsed,
                const double* D, bool d_sorted, double* y_user, double* y_sorted, int mode,
                cudaStream_t s) {
-  int rc = ensure_workspace(ctx, t, s);
+  int rc = fmm_workspace(ctx, t, s);
   if (rc) return rc;
   // poroelastic near-field blocks: cached for repeated matvecs at one elapsed
   // time (GMRES), outside any capture
@@ -292,7 +295,7 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
 // order; writes the owned rows into y_user and/or y_sorted.
 int fmm_history(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt, int h,
                 const double* D_hist, double* y_user, double* y_sorted, cudaStream_t s) {
-  int rc = ensure_workspace(ctx, t, s);
+  int rc = fmm_workspace(ctx, t, s);
   if (rc) return rc;
   const PoroParams PP = poro_params(mat, dt);
   if (t->nlevels > 2) {

@@ -744,7 +744,7 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
     } else if ((rc2 = g.axpy(V, nloc, kd, g.dh, 1.0, dst + lo))) {
       return rc2;
     }
-    if (ctx->world > 1 && (rc2 = allgather_sorted(ctx, t, dst, ncomp, s))) return rc2;
+    if (ctx->exchange && (rc2 = allgather_sorted(ctx, t, dst, ncomp, s))) return rc2;
     DDM_CUDA(ctx, cudaStreamSynchronize(s));   // y (host) must stay alive until the copy ran
     return DDM_OK;
   };
@@ -792,7 +792,7 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
       for (int k = 0; k < m && iters < max_iter; ++k) {
         const double* vk = V + (int64_t)k * nloc;
         const double* vin = vk;
-        if (ctx->world > 1) {
+        if (ctx->exchange) {
           DDM_CUDA(ctx, cudaMemcpyAsync(vf + lo, vk, nloc * sizeof(double), cudaMemcpyDeviceToDevice, s));
           if ((rc = allgather_sorted(ctx, t, vf, ncomp, s))) return rc;
           vin = vf;
@@ -858,7 +858,7 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
     for (int k = 0; k < m; ++k) {
       const double* vk = V + (int64_t)k * nloc;
       const double* vin = vk;
-      if (ctx->world > 1) {
+      if (ctx->exchange) {
         DDM_CUDA(ctx, cudaMemcpyAsync(vf + lo, vk, nloc * sizeof(double), cudaMemcpyDeviceToDevice, s));
         if ((rc = allgather_sorted(ctx, t, vf, ncomp, s))) return rc;
         vin = vf;
@@ -935,7 +935,7 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
     if (accepted) break;
     if ((rc = form_x(kdone, xs))) return rc;
   }
-  if (ctx->world > 1 && (rc = allgather_sorted(ctx, t, xs, ncomp, s))) return rc;
+  if (ctx->exchange && (rc = allgather_sorted(ctx, t, xs, ncomp, s))) return rc;
   scatter_to_user<<<nblk(n, 256), 256, 0, s>>>(n, ncomp, t->perm, xs, x_user);
   DDM_CUDA(ctx, cudaGetLastError());
   DDM_CUDA(ctx, cudaStreamSynchronize(s));

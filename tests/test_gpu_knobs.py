@@ -68,6 +68,10 @@ print("RESULT " + json.dumps(out))
     {"DDM_PDL": "0", "DDM_SUBTREE": "0"},
     {"DDM_NO_GRAPH": "1", "DDM_SERIAL": "1"},
     {"DDM_PDL": "1", "DDM_SUBTREE": "1", "DDM_GMRES_BATCH": "3"},
+    # the multi-rank exchange path (NCCL all-gather of the owned rows, NCCL
+    # all-reduce of the GMRES dots) on a one-rank communicator
+    {"DDM_FORCE_NCCL": "1"},
+    {"DDM_FORCE_NCCL": "1", "DDM_GMRES_SYNC": "1"},
 ])
 def test_knob_paths_agree_with_oracle(env):
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=dict(os.environ, **env),
