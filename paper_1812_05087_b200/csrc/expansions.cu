@@ -931,14 +931,15 @@ int pass_grid(ddm_ctx_s* ctx, const void* kernel, size_t shm, int work) {
 // far chain is latency bound: small trees, where the chain is the matvec's
 // critical path (config 3: 114 -> 110 us, config 4: 64 -> 60 us).  On large
 // trees the early-resident dependent blocks take SM slots from the concurrent
-// near field (config 5: 1.16 -> 1.28 ms), so there it is off.  DDM_PDL=0/1
-// overrides.
+// near field (config 5: 1.16 -> 1.28 ms), so there it is off -- except on
+// several ranks, where each rank's near field shrinks by the rank count and the
+// replicated far chain becomes the critical path.  DDM_PDL=0/1 overrides.
 static bool use_pdl(const ddm_tree_s* t) {
   static const int env = [] {
     const char* e = getenv("DDM_PDL");
     return e ? atoi(e) : -1;
   }();
-  return env >= 0 ? env != 0 : t->n <= 200000;
+  return env >= 0 ? env != 0 : (t->n <= 200000 || t->ctx->world > 1);
 }
 
 // Subtree passes (one launch per pass below the split level) on small trees,
@@ -950,7 +951,7 @@ static bool use_subtrees(const ddm_tree_s* t) {
     return e ? atoi(e) : -1;
   }();
   if (t->sub_n <= 0) return false;
-  return env >= 0 ? env != 0 : t->n <= 200000;
+  return env >= 0 ? env != 0 : (t->n <= 200000 || t->ctx->world > 1);
 }
 
 template <typename... KArgs, typename... Args>
