@@ -334,7 +334,10 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
                : "d"(a), "d"(b));
 }
 
-constexpr int kM2LBatch = 4;     // V pairs per pipelined batch (2 DMMA n-tiles)
+#ifndef DDM_M2L_BATCH
+#define DDM_M2L_BATCH 4
+#endif
+constexpr int kM2LBatch = DDM_M2L_BATCH;   // V pairs per pipelined batch (2 pairs per DMMA n-tile)
 
 // Tensor-core M2L of cell c's V list [vb, ve) (PT <= 32).  Per batch of
 // kM2LBatch pairs: (1) every lane loads the source coefficients of its
