@@ -150,12 +150,10 @@ struct ddm_tree_s {
   int w_min = 24;                 // W(B) cells hold >= w_min elements (DDM_W_MIN, 0 = off)
   int4* items = nullptr;          // P2P work items: (leaf, tgt0, src_begin, src_end)
   int* item_off = nullptr;        // [nleaves+1] first item of each leaf
-  int* m2l_cells = nullptr;       // (reserved) cells whose subtree meets the owned range
-  int n_m2l_cells = 0;
   int item_lo_owned = 0, item_hi_owned = 0;   // P2P items of owned leaves
   int* p2p_order = nullptr;       // [item_hi_owned - item_lo_owned] owned items, most sources
                                   // first (longest-processing-time order: no tail)
-  // persistent-pass scheduling (expansions.cu)
+  // upward-pass schedule (expansions.cu)
   // subtree passes (small trees, expansions.cu): split level, roots = its cells,
   // per (root, level >= Ls) ranges into up_list (M2M) and into the level's cells (L2L)
   int sub_Ls = 0, sub_n = 0, sub_nsl = 0;
@@ -164,10 +162,6 @@ struct ddm_tree_s {
   int* up_list = nullptr;         // non-leaf cells of level >= 2, deepest level first
   int n_up = 0;
   std::vector<int> up_level_off;  // [2 (nlevels+1)]: level l = up_list[off[2l], off[2l+1])
-  int* ready_up = nullptr;        // [ncells] multipole-ready flags (epoch tagged)
-  int* ready_down = nullptr;      // [2 ncells] local-final flags | M2L-done flags (epoch tagged)
-  int* tickets = nullptr;         // [2] work counters (upward, downward)
-  int epoch = 0;
 
   // FMM operators (device, fmm.cu fmm_init_operators): every translation is
   // pre-scale (complex powers) x real Pascal matrix x post-scale
@@ -196,7 +190,6 @@ struct ddm_tree_s {
   double* d_sorted = nullptr;     // [n*3] D gathered into sorted order
   double* y_sorted = nullptr;     // [n*3]
   double* y_far = nullptr;        // [n*3] L2P far field of the owned elements (sorted order)
-  double* part_direct = nullptr;  // [n*2] direct-mode tractions (sorted)
   // bbFMM far field (bbfmm.cu): node weights W and node values F, [ncells][3][bb_n^2] complex
   double2* bb_w = nullptr;
   double2* bb_f = nullptr;

@@ -516,9 +516,9 @@ void free_tree(ddm_tree_s* t) {
                   t->el_leaf, t->c_level, t->c_ix, t->c_iy, t->c_start, t->c_count,
                   t->c_parent, t->c_first_child, t->c_nchild, t->c_leaf, t->colleagues,
                   t->v_off, t->v_idx, t->v_cls, t->leaves, t->u_off, t->u_lo, t->u_hi, t->w_off, t->w_idx,
-                  t->items, t->item_off, t->p2p_order, t->m2l_cells, t->op_pas, t->op_pasT, t->op_pm2l, t->op_w,
+                  t->items, t->item_off, t->p2p_order, t->op_pas, t->op_pasT, t->op_pm2l, t->op_w,
                   t->op_eps, t->op_e2i, t->mpole, t->local, t->src, t->part, t->d_sorted, t->y_sorted, t->y_far,
-                  t->part_direct, t->up_list, t->ready_up, t->ready_down, t->tickets,
+                  t->up_list,
                   t->krylov, t->pc, t->gm_w, t->gm_tmp, t->gm_part, t->bb_w, t->bb_f,
                   t->pc_chunks, t->pc_off, t->pcl, t->st_elem, t->st_code, t->rbeg, t->srec, t->nc, t->nc_off, t->gm_dev, t->gm_ticket, t->sub_up, t->sub_cells, t->it_roff, t->it_rng};
   for (void* p : ptrs)
@@ -857,8 +857,8 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
                                                 t->ea, t->ec, t->es);
   DDM_CUDA(ctx, cudaGetLastError());
 
-  // ---- schedule of the persistent upward pass: non-leaf cells of level >= 2,
-  // deepest level first (every parent after all of its children)
+  // ---- upward-pass schedule: non-leaf cells of level >= 2, deepest level
+  // first (every parent after all of its children), one range per level
   {
     std::vector<int> hleaf(ncells);
     DDM_CUDA(ctx, cudaMemcpyAsync(hleaf.data(), C.leaf, ncells * sizeof(int),
@@ -873,14 +873,10 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
       t->up_level_off[2 * lev + 1] = (int)up.size();
     }
     t->n_up = (int)up.size();
-    if ((rc = dalloc(ctx, &t->up_list, up.size())) || (rc = dalloc(ctx, &t->ready_up, ncells)) ||
-        (rc = dalloc(ctx, &t->ready_down, 2 * (size_t)ncells)) || (rc = dalloc(ctx, &t->tickets, 2)))
-      return rc;
+    if ((rc = dalloc(ctx, &t->up_list, up.size()))) return rc;
     if (!up.empty())
       DDM_CUDA(ctx, cudaMemcpyAsync(t->up_list, up.data(), up.size() * sizeof(int),
                                     cudaMemcpyHostToDevice, s));
-    DDM_CUDA(ctx, cudaMemsetAsync(t->ready_up, 0, ncells * sizeof(int), s));
-    DDM_CUDA(ctx, cudaMemsetAsync(t->ready_down, 0, 2 * ncells * sizeof(int), s));
 
     // subtree schedule (expansions.cu subtree passes): split level Ls = the
     // first level >= 3 with >= 128 cells, if at least two levels lie below it
