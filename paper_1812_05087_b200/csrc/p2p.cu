@@ -344,10 +344,6 @@ constexpr int kTPL = DDM_TPL;   // targets per lane (independent chains sharing 
 #define DDM_P2P_UNROLL 2
 #endif
 constexpr int kP2PUnroll = DDM_P2P_UNROLL;
-#ifndef DDM_P2P_PREFETCH
-#define DDM_P2P_PREFETCH 0
-#endif
-constexpr int kP2PPrefetch = DDM_P2P_PREFETCH;   // records ahead (0 = off)
 
 __device__ __forceinline__ void load_rec(double (&sp)[kRecStride], const double* rec) {
   const double2* g = reinterpret_cast<const double2*>(rec);
