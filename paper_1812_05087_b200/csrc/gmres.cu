@@ -657,6 +657,15 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   double* scald = estd + m;
   int* flagd = reinterpret_cast<int*>(scald + 2);
 
+  // GMRES applies the operator many times at one elapsed time: build the
+  // poroelastic near-field cache up front instead of on the
+  // second matvec
+  if (mat->kind == 1 && (mode & 0xff) == DDM_FMM && dt > 0) {
+    if ((rc = fmm_workspace(ctx, t, s))) return rc;
+    const PoroParams P = poro_params(mat, dt);
+    for (int k = 0; k < 2; ++k)
+      if ((rc = poro_near_cache_update(ctx, t, P, s))) return rc;
+  }
   gather_sorted<<<nblk(n, 256), 256, 0, s>>>(n, ncomp, t->perm, b_user, bs);
   gather_sorted<<<nblk(n, 256), 256, 0, s>>>(n, ncomp, t->perm, x_user, xs);
   DDM_CUDA(ctx, cudaGetLastError());
