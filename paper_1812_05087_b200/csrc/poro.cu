@@ -778,13 +778,18 @@ poro_p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict_
                 const int* __restrict__ c_start, const int* __restrict__ c_count,
                 const double* __restrict__ src, const double* __restrict__ ex,
                 const double* __restrict__ ey, const double* __restrict__ ec,
-                const double* __restrict__ es, PoroConst k, double* __restrict__ part3) {
+                const double* __restrict__ es, PoroConst k, int G, double* __restrict__ gpart,
+                double* __restrict__ part3) {
   __shared__ double red[4][3][32];
   __shared__ NearQueue nq[4];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   NearQueue& Q = nq[w];
   const unsigned lt_mask = (1u << lane) - 1u;
-  for (int oi = blockIdx.x * 4 + w; oi < nown; oi += gridDim.x * 4) {
+  // warp task = (owned item oi, source group grp of G): the item's rounds of S
+  // sources are dealt round-robin to the groups; G > 1 writes per-group
+  // partials gpart[grp][oi][t][3] (summed in order by poro_hist_reduce)
+  for (int task = blockIdx.x * 4 + w; task < nown * G; task += gridDim.x * 4) {
+    const int oi = task / G, grp = task - oi * G;
     const int it = order[oi];
     const int4 item = items[it];
     const int kk = item.x;
@@ -825,6 +830,7 @@ poro_p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict_
       const int lo = u_lo[r], len = u_hi[r] - lo;
       const int b = max(item.z - pos, 0), e = min(item.w - pos, len);
       for (int jb = b; jb < e; jb += S) {
+        if (G > 1 && ((pos + jb - item.z) / S) % G != grp) continue;   // another warp's round
         const int j = jb + slice;
         bool near = false;
         if (active && j < e)
@@ -859,7 +865,8 @@ poro_p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict_
         s1 += Q.acc[1][lane];
         s2 += Q.acc[2][lane];
       }
-      double* o = part3 + ((int64_t)it * kTgtGroup + lane) * 3;
+      double* o = G > 1 ? gpart + (((int64_t)grp * nown + oi) * kTgtGroup + lane) * 3
+                        : part3 + ((int64_t)it * kTgtGroup + lane) * 3;
       o[0] = s0;
       o[1] = s1;
       o[2] = s2;
@@ -1624,10 +1631,29 @@ int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, con
     DDM_CUDA(ctx, cudaGetLastError());
     return DDM_OK;
   }
-  poro_p2p_kernel<<<nblk(item_hi - item_lo, 4), 128, 0, s>>>(
-      item_hi - item_lo, t->p2p_order, t->items, t->u_off, t->u_lo, t->u_hi, t->leaves, t->c_start, t->c_count,
-      t->src, t->ex, t->ey, t->ec, t->es, to_const(P), reinterpret_cast<double*>(t->part));
+  // source groups per item (the near-rule work of an item is large and
+  // uneven; one warp per item left 181 warps for config 4's 181 items)
+  const int nown = item_hi - item_lo;
+  static const int g_env = [] {
+    const char* e = getenv("DDM_PORO_GROUPS");
+    return e ? atoi(e) : 0;
+  }();
+  // measured (DDM_NEAR_CACHE=0): config 4 0.59 -> 0.15 ms, config 3 0.93 -> 0.81 ms at G = 8
+  const int G = g_env > 0 ? g_env : 8;
+  double* gpart = nullptr;
+  if (G > 1)
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&gpart, (size_t)G * nown * kTgtGroup * 3 * sizeof(double), s));
+  poro_p2p_kernel<<<nblk((int64_t)nown * G, 4), 128, 0, s>>>(
+      nown, t->p2p_order, t->items, t->u_off, t->u_lo, t->u_hi, t->leaves, t->c_start, t->c_count,
+      t->src, t->ex, t->ey, t->ec, t->es, to_const(P), G, gpart, reinterpret_cast<double*>(t->part));
   DDM_CUDA(ctx, cudaGetLastError());
+  if (G > 1) {
+    const int64_t ne = (int64_t)nown * kTgtGroup * 3;
+    poro_hist_reduce<<<nblk(ne, 256), 256, 0, s>>>(nown, G, t->p2p_order, gpart,
+                                                   reinterpret_cast<double*>(t->part));
+    DDM_CUDA(ctx, cudaGetLastError());
+    cudaFreeAsync(gpart, s);
+  }
   return DDM_OK;
 }
 
