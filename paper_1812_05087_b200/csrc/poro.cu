@@ -1240,14 +1240,16 @@ poro_hist_near_kernel(int nown, const int* __restrict__ order, const int4* __res
                       const double* __restrict__ Cs, int h, double dt,
                       const double* __restrict__ ex, const double* __restrict__ ey,
                       const double* __restrict__ ec, const double* __restrict__ es, PoroConst k,
-                      double* __restrict__ part3) {
+                      int G, double* __restrict__ gpart, double* __restrict__ part3) {
   __shared__ double red[4][3][32];
   __shared__ NearQueue nq[4];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   NearQueue& Q = nq[w];
   const unsigned lt_mask = (1u << lane) - 1u;
   const int hs = (h + 2) * 3, cst = (h + 1) * 3;
-  for (int oi = blockIdx.x * 4 + w; oi < nown; oi += gridDim.x * 4) {
+  // warp task = (owned item oi, source group grp of G), as poro_p2p_kernel
+  for (int task = blockIdx.x * 4 + w; task < nown * G; task += gridDim.x * 4) {
+    const int oi = task / G, grp = task - oi * G;
     const int it = order[oi];
     const int4 item = items[it];
     const int kk = item.x;
@@ -1290,6 +1292,7 @@ poro_hist_near_kernel(int nown, const int* __restrict__ order, const int4* __res
       const int lo = u_lo[r], len = u_hi[r] - lo;
       const int b = max(item.z - pos, 0), e_ = min(item.w - pos, len);
       for (int jb = b; jb < e_; jb += S) {
+        if (G > 1 && ((pos + jb - item.z) / S) % G != grp) continue;   // another warp's round
         const int jj = jb + slice;
         const bool valid = active && jj < e_;
         const int sidx = lo + (valid ? jj : 0);
@@ -1369,7 +1372,8 @@ poro_hist_near_kernel(int nown, const int* __restrict__ order, const int4* __res
         s1 += Q.acc[1][lane];
         s2 += Q.acc[2][lane];
       }
-      double* o = part3 + ((int64_t)it * kTgtGroup + lane) * 3;
+      double* o = G > 1 ? gpart + (((int64_t)grp * nown + oi) * kTgtGroup + lane) * 3
+                        : part3 + ((int64_t)it * kTgtGroup + lane) * 3;
       o[0] = s0;
       o[1] = s1;
       o[2] = s2;
@@ -1786,11 +1790,19 @@ int launch_poro_hist_near(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, in
                           const double* Hs, const double* Cs, cudaStream_t s) {
   const int nown = t->item_hi_owned - t->item_lo_owned;
   if (nown <= 0) return DDM_OK;
-  poro_hist_near_kernel<<<nblk(nown, 4), 128, 0, s>>>(
+  constexpr int G = 8;   // source groups per item (as launch_poro_p2p)
+  double* gpart = nullptr;
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&gpart, (size_t)G * nown * kTgtGroup * 3 * sizeof(double), s));
+  poro_hist_near_kernel<<<nblk((int64_t)nown * G, 4), 128, 0, s>>>(
       nown, t->p2p_order, t->items, t->u_off, t->u_lo, t->u_hi, t->leaves, t->c_start,
-      t->c_count, t->src, Hs, Cs, h, dt, t->ex, t->ey, t->ec, t->es, to_const(P),
+      t->c_count, t->src, Hs, Cs, h, dt, t->ex, t->ey, t->ec, t->es, to_const(P), G, gpart,
       reinterpret_cast<double*>(t->part));
   DDM_CUDA(ctx, cudaGetLastError());
+  const int64_t ne = (int64_t)nown * kTgtGroup * 3;
+  poro_hist_reduce<<<nblk(ne, 256), 256, 0, s>>>(nown, G, t->p2p_order, gpart,
+                                                 reinterpret_cast<double*>(t->part));
+  DDM_CUDA(ctx, cudaGetLastError());
+  cudaFreeAsync(gpart, s);
   return DDM_OK;
 }
 
