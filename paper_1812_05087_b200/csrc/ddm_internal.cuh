@@ -186,6 +186,8 @@ struct ddm_tree_s {
   int64_t nrec = 0;
   int* it_roff = nullptr;         // [nitems+1] first record range of each P2P item
   int2* it_rng = nullptr;         // record ranges [rb, re) of each item's source window
+  double* gpart = nullptr;        // per-group partials of the on-the-fly poroelastic near field
+  int64_t gpart_n = 0;
   double2* part = nullptr;        // [nitems*32] partial tractions
   double* d_sorted = nullptr;     // [n*3] D gathered into sorted order
   double* y_sorted = nullptr;     // [n*3]

@@ -1620,6 +1620,22 @@ int poro_near_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, c
   return DDM_OK;
 }
 
+// per-tree buffer of the per-group partials of the on-the-fly near-field
+// kernels (grown with cudaMalloc; a first-use cudaMallocAsync pool growth
+// cost ~20 ms)
+static int group_partials(ddm_ctx_s* ctx, ddm_tree_s* t, size_t doubles, double** out) {
+  if (t->gpart_n < (int64_t)doubles) {
+    if (t->gpart) cudaFree(t->gpart);
+    t->gpart = nullptr;
+    t->gpart_n = 0;
+    int rc;
+    if ((rc = dalloc(ctx, &t->gpart, doubles))) return rc;
+    t->gpart_n = (int64_t)doubles;
+  }
+  *out = t->gpart;
+  return DDM_OK;
+}
+
 int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, const PoroParams& P,
                     cudaStream_t s) {
   if (item_hi <= item_lo) return DDM_OK;
@@ -1645,8 +1661,10 @@ int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, con
   // measured (DDM_NEAR_CACHE=0): config 4 0.59 -> 0.15 ms, config 3 0.93 -> 0.81 ms at G = 8
   const int G = g_env > 0 ? g_env : 8;
   double* gpart = nullptr;
-  if (G > 1)
-    DDM_CUDA(ctx, cudaMallocAsync((void**)&gpart, (size_t)G * nown * kTgtGroup * 3 * sizeof(double), s));
+  if (G > 1) {
+    int rc;
+    if ((rc = group_partials(ctx, t, (size_t)G * nown * kTgtGroup * 3, &gpart))) return rc;
+  }
   poro_p2p_kernel<<<nblk((int64_t)nown * G, 4), 128, 0, s>>>(
       nown, t->p2p_order, t->items, t->u_off, t->u_lo, t->u_hi, t->leaves, t->c_start, t->c_count,
       t->src, t->ex, t->ey, t->ec, t->es, to_const(P), G, gpart, reinterpret_cast<double*>(t->part));
@@ -1656,7 +1674,6 @@ int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, con
     poro_hist_reduce<<<nblk(ne, 256), 256, 0, s>>>(nown, G, t->p2p_order, gpart,
                                                    reinterpret_cast<double*>(t->part));
     DDM_CUDA(ctx, cudaGetLastError());
-    cudaFreeAsync(gpart, s);
   }
   return DDM_OK;
 }
@@ -1792,7 +1809,10 @@ int launch_poro_hist_near(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, in
   if (nown <= 0) return DDM_OK;
   constexpr int G = 8;   // source groups per item (as launch_poro_p2p)
   double* gpart = nullptr;
-  DDM_CUDA(ctx, cudaMallocAsync((void**)&gpart, (size_t)G * nown * kTgtGroup * 3 * sizeof(double), s));
+  {
+    int rc;
+    if ((rc = group_partials(ctx, t, (size_t)G * nown * kTgtGroup * 3, &gpart))) return rc;
+  }
   poro_hist_near_kernel<<<nblk((int64_t)nown * G, 4), 128, 0, s>>>(
       nown, t->p2p_order, t->items, t->u_off, t->u_lo, t->u_hi, t->leaves, t->c_start,
       t->c_count, t->src, Hs, Cs, h, dt, t->ex, t->ey, t->ec, t->es, to_const(P), G, gpart,
@@ -1802,7 +1822,6 @@ int launch_poro_hist_near(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, in
   poro_hist_reduce<<<nblk(ne, 256), 256, 0, s>>>(nown, G, t->p2p_order, gpart,
                                                  reinterpret_cast<double*>(t->part));
   DDM_CUDA(ctx, cudaGetLastError());
-  cudaFreeAsync(gpart, s);
   return DDM_OK;
 }
 
