@@ -437,9 +437,10 @@ def gmres_extra(D, ctx, torch, dev, march_steps: int):
         return (time.perf_counter() - t0) / reps * 1e3, r
 
     def steady_mv(fn):
-        # the first poroelastic matvec at an elapsed time (near field on the
-        # fly), then the second (builds the near-field cache); matvec_ms below
-        # is the steady state (cached blocks, graph replay)
+        # the first poroelastic matvec on the fresh tree (one-time workspace
+        # allocation, source stream build, first-use module loading, near
+        # field on the fly), then the second (builds the near-field cache);
+        # matvec_ms below is the steady state (cached blocks, graph replay)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         fn()
