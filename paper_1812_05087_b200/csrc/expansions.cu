@@ -281,7 +281,8 @@ __global__ void DDM_P2M_BOUNDS
 p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ c_level,
            const int* __restrict__ c_ix, const int* __restrict__ c_iy,
            const int* __restrict__ c_start, const int* __restrict__ c_count, CellGeom cg,
-           int p_rt, const double* __restrict__ D, int ncomp, const double* __restrict__ ex,
+           int p_rt, const int* __restrict__ perm, const double* __restrict__ D, int ncomp,
+           const double* __restrict__ ex,
            const double* __restrict__ ey, const double* __restrict__ ea,
            const double* __restrict__ ec, const double* __restrict__ es,
            double2* __restrict__ mpole, PoroFar pf) {
@@ -290,7 +291,7 @@ p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ 
   extern __shared__ double2 p2m_sh[];   // [kPassWarps][32 * 17] transposition buffers
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int k = blockIdx.x * kPassWarps + w; k < nleaves; k += gridDim.x * kPassWarps)
-    p2m_cell<PT>(leaves[k], p, c_level, c_ix, c_iy, c_start, c_count, cg, nullptr, D, ncomp, ex,
+    p2m_cell<PT>(leaves[k], p, c_level, c_ix, c_iy, c_start, c_count, cg, perm, D, ncomp, ex,
                  ey, ea, ec, es, mpole, p2m_sh + w * 32 * 17, lane, pf);
 }
 
@@ -978,7 +979,7 @@ cudaError_t launch_pdl(bool on, void (*kernel)(KArgs...), unsigned grid, unsigne
 // first), replicated on every rank
 int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
                   const PoroFar& pf, cudaStream_t s) {
-  (void)perm_in;   // D is in sorted order (prep gathered it)
+  // D in user order (perm_in = sorted -> user, read through it) or sorted (nullptr)
   const int p = t->p;
   const CellGeom cg{t->x_min, t->y_min, t->W};
   const size_t shm = (size_t)kPassWarps * 8 * p * sizeof(double2);
@@ -990,7 +991,8 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
     const int nb = pass_grid(ctx, (const void*)p2m_kernel<PT>, shp, t->nleaves);                \
     stage_begin(ctx, DDM_ST_P2M, s);                                                            \
     p2m_kernel<PT><<<nb, kPassWarps * 32, shp, s>>>(t->nleaves, t->leaves, t->c_level, t->c_ix, \
-                                                    t->c_iy, t->c_start, t->c_count, cg, p, D,  \
+                                                    t->c_iy, t->c_start, t->c_count, cg, p,     \
+                                                    perm_in, D,                                 \
                                                     ncomp, t->ex, t->ey, t->ea, t->ec, t->es,   \
                                                     t->mpole, pf);                              \
     stage_end(ctx, DDM_ST_P2M, s);                                                              \

@@ -228,14 +228,30 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
     if ((rc = bb_prepare(ctx, t, bb_n))) return rc;
   }
 
-  stage_begin(ctx, DDM_ST_PREP, s);
+  // The series far field reads D itself (P2M through perm), so it does not
+  // wait for the near field's source records: fork first, prep on the near
+  // stream (the far chain starts at once; it is the critical path on small
+  // trees).  DDM_EARLY_FAR=0: prep before the fork (P2M reads D sorted).
+  static const bool early_env = [] {
+    const char* e = getenv("DDM_EARLY_FAR");
+    return !(e && e[0] == '0');
+  }();
+  const bool early = early_env && !bb && mode != DDM_DIRECT;
+  cudaStream_t sf = ctx->serial ? s : ctx->s_hi, sn = ctx->serial ? s : ctx->s_lo;
+  if (early) {
+    DDM_CUDA(ctx, cudaEventRecord(ctx->ev_fork, s));
+    DDM_CUDA(ctx, cudaStreamWaitEvent(sf, ctx->ev_fork, 0));
+    DDM_CUDA(ctx, cudaStreamWaitEvent(sn, ctx->ev_fork, 0));
+  }
+  cudaStream_t sp = early ? sn : s;
+  stage_begin(ctx, DDM_ST_PREP, sp);
   // elastic: the direct mode reads per-element source records, the near
   // field of the FMM the node-sharing source stream (p2p.cu)
-  rc = poro ? launch_poro_prep(ctx, t, perm_in, D, s)
-       : mode == DDM_DIRECT ? launch_prep_sources(ctx, t, perm_in, D, ncomp, s)
-                            : launch_prep_stream(ctx, t, perm_in, D, ncomp, s);
+  rc = poro ? launch_poro_prep(ctx, t, perm_in, D, sp)
+       : mode == DDM_DIRECT ? launch_prep_sources(ctx, t, perm_in, D, ncomp, sp)
+                            : launch_prep_stream(ctx, t, perm_in, D, ncomp, sp);
   if (rc) return rc;
-  stage_end(ctx, DDM_ST_PREP, s);
+  stage_end(ctx, DDM_ST_PREP, sp);
 
   if (mode == DDM_DIRECT) {
     stage_begin(ctx, DDM_ST_P2P, s);
@@ -248,10 +264,11 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
   // fork: the near field (P2P, throughput bound) runs on the low-priority
   // stream concurrently with the latency-bound far-field chain on the
   // high-priority stream; both only read `src` / D and write disjoint buffers.
-  DDM_CUDA(ctx, cudaEventRecord(ctx->ev_fork, s));
-  cudaStream_t sf = ctx->serial ? s : ctx->s_hi, sn = ctx->serial ? s : ctx->s_lo;
-  DDM_CUDA(ctx, cudaStreamWaitEvent(sf, ctx->ev_fork, 0));
-  DDM_CUDA(ctx, cudaStreamWaitEvent(sn, ctx->ev_fork, 0));
+  if (!early) {
+    DDM_CUDA(ctx, cudaEventRecord(ctx->ev_fork, s));
+    DDM_CUDA(ctx, cudaStreamWaitEvent(sf, ctx->ev_fork, 0));
+    DDM_CUDA(ctx, cudaStreamWaitEvent(sn, ctx->ev_fork, 0));
+  }
 
   // near field: P2P work items of the owned leaves
   stage_begin(ctx, DDM_ST_P2P, sn);
@@ -266,7 +283,9 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
   } else {
   // upward pass: P2M on all leaves, M2M level by level (replicated on all
   // ranks); prep gathered D into sorted order, so it is read coalesced
-  if ((rc = launch_upward(ctx, t, nullptr, perm_in ? t->d_sorted : D, ncomp, pf, sf))) return rc;
+  if ((rc = early ? launch_upward(ctx, t, perm_in, D, ncomp, pf, sf)
+                  : launch_upward(ctx, t, nullptr, perm_in ? t->d_sorted : D, ncomp, pf, sf)))
+    return rc;
   // downward pass: M2L of every cell of level >= 2, L2L level by level (cells
   // whose subtree holds owned targets)
   if ((rc = launch_downward(ctx, t, sf))) return rc;
