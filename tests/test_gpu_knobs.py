@@ -65,7 +65,7 @@ print("RESULT " + json.dumps(out))
     {},
     {"DDM_GMRES_SYNC": "1"},
     {"DDM_NEAR_CACHE": "0", "DDM_HIST_CACHE": "0"},
-    {"DDM_PDL": "0", "DDM_SUBTREE": "0"},
+    {"DDM_PDL": "0", "DDM_SUBTREE": "0", "DDM_EARLY_FAR": "0"},
     {"DDM_NO_GRAPH": "1", "DDM_SERIAL": "1"},
     {"DDM_PDL": "1", "DDM_SUBTREE": "1", "DDM_GMRES_BATCH": "3"},
     # the multi-rank exchange path (NCCL all-gather of the owned rows, NCCL
