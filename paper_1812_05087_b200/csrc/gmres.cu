@@ -400,6 +400,84 @@ __global__ void finish_scale(int k, const double* __restrict__ dh, double* __res
   }
 }
 
+// finish_scale fused with the leaf-block preconditioner of the next step
+// (single rank, leaf blocks covering every row): CTA per chunk q scales its
+// rows of the next basis vector (dst = w / h(k+1,k)) and applies the chunk's
+// inverse block to them (uf = M^-1 dst), so the next operator apply skips a
+// separate preconditioner launch.  CTA 0, thread 0 also does the Givens step
+// (as finish_scale).
+__global__ void __launch_bounds__(kApplyThreads)
+finish_scale_pc(int k, const double* __restrict__ dh, double* __restrict__ Hp,
+                double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ g,
+                double* __restrict__ est, double* __restrict__ scal, int* __restrict__ flag,
+                const double* __restrict__ w, double* __restrict__ dst,
+                const int2* __restrict__ chunks, const int64_t* __restrict__ off, int ncomp,
+                const double* __restrict__ inv, double* __restrict__ uf) {
+  __shared__ double xs[kPcChunk * 3];
+  __shared__ double part[kApplyThreads];
+  const bool broke = flag[0] != 0;
+  const double hn = sqrt(dh[2 * (k + 1) + 1]);
+  const double a = (!broke && hn > 0.0) ? 1.0 / hn : 0.0;
+  const int2 ch = chunks[blockIdx.x];
+  const int d = ncomp * ch.y;
+  const int64_t b0 = (int64_t)ch.x * ncomp;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) {
+    const double v = a * w[b0 + t];
+    dst[b0 + t] = v;
+    xs[t] = v;
+  }
+  __syncthreads();
+  const double* Ai = inv + off[blockIdx.x];
+  if (d > 0) {
+    const int G = max(1, (int)blockDim.x / d);
+    const int r = threadIdx.x % d, gg = threadIdx.x / d;
+    if (gg < G) {
+      double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      int c = gg;
+      for (; c + 7 * G < d; c += 8 * G) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(Ai + (size_t)(c + u * G) * d + r);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = fma(v[u], xs[c + u * G], acc[u]);
+      }
+      for (int u = 0; c < d; c += G, ++u) acc[u] = fma(__ldg(Ai + (size_t)c * d + r), xs[c], acc[u]);
+      part[threadIdx.x] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    }
+    __syncthreads();
+    if (threadIdx.x < d) {
+      double v = 0.0;
+      for (int q = 0; q < G; ++q) v += part[q * d + threadIdx.x];
+      uf[b0 + threadIdx.x] = v;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (broke) {
+      est[k] = est[k > 0 ? k - 1 : 0];
+      scal[0] = 0.0;
+      return;
+    }
+    double* col = Hp + (size_t)k * (k + 3) / 2;
+    for (int i = 0; i <= k; ++i) col[i] = dh[i] + dh[k + 1 + i];
+    for (int i = 0; i < k; ++i) {
+      const double x = col[i], y = col[i + 1];
+      col[i] = cs[i] * x + sn[i] * y;
+      col[i + 1] = -sn[i] * x + cs[i] * y;
+    }
+    const double x = col[k];
+    const double den = hypot(x, hn);
+    cs[k] = x / den;
+    sn[k] = hn / den;
+    col[k] = den;
+    col[k + 1] = 0.0;
+    g[k + 1] = -sn[k] * g[k];
+    g[k] = cs[k] * g[k];
+    est[k] = fabs(g[k + 1]);
+    scal[0] = a;
+    if (!(hn > 0.0)) flag[0] = k + 1;
+  }
+}
+
 struct Gm {
   ddm_ctx_s* ctx;
   ddm_tree_s* t;
@@ -777,6 +855,14 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
     gv[0] = beta;
     int kdone = 0;
     if (!sync_mode) {
+      // the leaf-block preconditioner of the next step fused into the step's
+      // normalisation (one rank, leaf blocks built by the first apply)
+      bool uf_ready = false;
+      const bool fuse_pc_env = [] {
+        const char* e = getenv("DDM_GMRES_FUSE_PC");
+        return !(e && e[0] == '0');
+      }();
+      bool fuse_pc = false;
       // batched: the Arnoldi steps queue back to back on the stream; the
       // host reads the residual estimates every `batch` steps and picks the
       // first step that met the target (later steps of the batch are
@@ -806,7 +892,14 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
           if ((rc = allgather_sorted(ctx, t, vf, ncomp, s))) return rc;
           vin = vf;
         }
-        if ((rc = apply(vin))) return rc;
+        if (uf_ready) {   // M^-1 V_k came with the previous step's finish_scale_pc
+          if ((rc = fmm_matvec(ctx, t, mat, dt, uf, true, nullptr, wf, mode, s))) return rc;
+          uf_ready = false;
+        } else if ((rc = apply(vin))) {
+          return rc;
+        }
+        if (k == 0)   // the first apply built the leaf blocks for this material / dt
+          fuse_pc = fuse_pc_env && use_pc && !pc_point && !ctx->exchange && t->pc_nchunks > 0;
         double* w = wf + lo;
         // CGS2 (two classical Gram-Schmidt passes, no host decision)
         const int o_w1 = 2 * (k + 1) + 1;
@@ -814,8 +907,15 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
         if ((rc = g.axpy(V, nloc, k + 1, g.dh, -1.0, w))) return rc;
         if ((rc = g.dots(V, nloc, k + 1, w, k + 1))) return rc;
         if ((rc = g.axpy_norm(V, nloc, k + 1, g.dh + k + 1, -1.0, w, o_w1))) return rc;
-        finish_scale<<<nblk(nloc, 256), 256, 0, s>>>(k, g.dh, Hd, csd, snd, gd, estd, scald, flagd,
-                                                     w, V + (int64_t)(k + 1) * nloc, nloc);
+        if (fuse_pc) {
+          finish_scale_pc<<<t->pc_nchunks, kApplyThreads, 0, s>>>(
+              k, g.dh, Hd, csd, snd, gd, estd, scald, flagd, w, V + (int64_t)(k + 1) * nloc,
+              t->pc_chunks, t->pc_off, ncomp, t->pcl, uf);
+          uf_ready = true;   // uf = M^-1 V_{k+1} for the next step's operator apply
+        } else {
+          finish_scale<<<nblk(nloc, 256), 256, 0, s>>>(k, g.dh, Hd, csd, snd, gd, estd, scald,
+                                                       flagd, w, V + (int64_t)(k + 1) * nloc, nloc);
+        }
         DDM_CUDA(ctx, cudaGetLastError());
         ++iters;
         kdone = k + 1;
@@ -832,7 +932,9 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
           const int it_kk = it0 + kk + 1;
           if (est_ok && !brk && kk + 1 < m && it_kk < max_iter) {
             // the estimate says converged: check the true residual without
-            // ending the cycle (as in the synchronous path)
+            // ending the cycle (as in the synchronous path); uf is reused as
+            // scratch, so the next step applies the preconditioner itself
+            uf_ready = false;
             if ((rc = fetch_state(kk + 1)) || (rc = form_x(kk + 1, xt))) return rc;
             if ((rc = apply_plain(xt))) return rc;
             sub_scale<<<nblk(nloc, 256), 256, 0, s>>>(bs + lo, wf + lo, uf + lo, nloc);

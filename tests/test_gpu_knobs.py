@@ -64,6 +64,7 @@ print("RESULT " + json.dumps(out))
 @pytest.mark.parametrize("env", [
     {},
     {"DDM_GMRES_SYNC": "1"},
+    {"DDM_GMRES_FUSE_PC": "0"},
     {"DDM_NEAR_CACHE": "0", "DDM_HIST_CACHE": "0"},
     {"DDM_PDL": "0", "DDM_SUBTREE": "0", "DDM_EARLY_FAR": "0"},
     {"DDM_NO_GRAPH": "1", "DDM_SERIAL": "1"},
