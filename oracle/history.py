@@ -44,10 +44,13 @@ def history_sum(geom, mat, dt, D_hist, lags=None):
     return r.reshape(geom.n, 3)
 
 
-def march(geom, mat, dt, b, steps, solve=np.linalg.solve):
+def march(geom, mat, dt, b, steps, solve=np.linalg.solve, lags=None):
     """Direct time marching with a constant right-hand side b [N, 3]:
-    returns D [steps, N, 3]."""
-    lags = [lag_matrix(geom, mat, dt, m) for m in range(steps + 1)]
+    returns D [steps, N, 3].  Step h solves A^(0) D^h = b - r_h.
+    `lags` may pass the lag matrices A^(0..steps) (tests drive the recurrence
+    with synthetic lags whose solution has a closed form)."""
+    if lags is None:
+        lags = [lag_matrix(geom, mat, dt, m) for m in range(steps + 1)]
     D = np.zeros((steps, geom.n, 3))
     for h in range(steps):
         rhs = b.reshape(-1) - history_sum(geom, mat, dt, D[:h], lags).reshape(-1)

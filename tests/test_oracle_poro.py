@@ -109,6 +109,16 @@ def test_fluid_source_is_theis():
     # the DD -> p coupling vanishes with alpha (order alpha)
     pD, _ = _point_field(z, tau, kd, 0.0, 1.0, 0.0, 0.0)
     assert abs(pD) < 1e-3 * abs(_point_field(z, tau, K3, 0.0, 1.0, 0.0, 0.0)[0])
+    # ... and so does the q -> sigma coupling: the fluid source induces no
+    # stress (SURVEY §8c.3 pin 5), for the point kernel and for an element
+    def tq(kk, zz):
+        p, d2 = _point_field(zz, tau, kk, 0.0, 0.0, 1.0, 0.0)
+        return -kk["eta"] * p + np.exp(0.6j) * (-4 * kk["eta"] * d2)
+    for zz in (z, 0.3 - 0.1j, 2.0 + 1.0j):
+        assert abs(tq(kd, zz)) <= 1e-3 * abs(tq(K3, zz))
+    ss_d, sn_d, _ = P.influence(ZC + 0.04j, 0.6, ZC, BS, 0.02, tau, kd, 0.0, 0.0, 1.0)
+    ss_c, sn_c, _ = P.influence(ZC + 0.04j, 0.6, ZC, BS, 0.02, tau, K3, 0.0, 0.0, 1.0)
+    assert math.hypot(ss_d, sn_d) <= 1e-3 * math.hypot(ss_c, sn_c)
 
 
 @pytest.mark.parametrize("src", [(1.0, 0.0, 0.0), (0.0, 1.0, 0.0), (0.0, 0.0, 1.0)])
@@ -178,7 +188,12 @@ def test_element_rule_matches_adaptive_quadrature(where):
         def fk(s, part):
             pp, dd = P.point_kernel(np.array([zt - (ZC + s * e)]), tau, k, e, *src)
             return {"p": pp[0].real, "dr": dd[0].real, "di": dd[0].imag}[part]
-        pts = [rel.real] if abs(rel.real) < a else None
+        # break the adaptive rule at the foot of the perpendicular and at
+        # offsets of a few distances from it, where the integrand has its peak
+        foot = min(max(rel.real, -a), a)
+        dp = max(abs(rel.imag), 1e-3 * a)
+        pts = sorted({x for x in (foot, foot - dp, foot + dp, foot - 4 * dp, foot + 4 * dp)
+                      if -a < x < a}) or None
         ref = {part: integrate.quad(fk, -a, a, args=(part,), points=pts, epsabs=0,
                                     epsrel=1e-13, limit=400)[0] for part in ("p", "dr", "di")}
         # tolerance relative to the integral of the absolute integrand (the
@@ -236,3 +251,106 @@ def test_history_sum_pins():
     r2 = H.history_sum(g, mat, dt, Dh2)
     r0 = H.history_sum(g, mat, dt, np.concatenate([Dh[:1], 0 * Dh[1:]]))
     assert np.allclose(r2 - r1, r0, rtol=1e-12, atol=1e-12 * np.abs(r1).max())
+
+
+# --- reciprocity (SURVEY §8c.3 pin 4) ------------------------------------------
+#
+# Poroelastic reciprocal theorem (Laplace domain, zero initial state, sources
+# switched on at t = 0 and held; tension-positive stress, CS-convention DD
+# D = u(0-) - u(0+), q = fluid volume rate per unit length).  From the
+# constitutive law sigma = 2G eps + lambda eps_kk I - alpha p I and
+# zeta = alpha eps_kk + p/M, s zeta - kappa lap p = gamma:
+#     int sigma1:eps2 + p1 gamma2 / s  =  int sigma2:eps1 + p2 gamma1 / s .
+# State 1 = a held unit DD at x1 (no fluid source), state 2 = a held unit
+# source at x2 (no DD): int sigma2:eps1 = t2(x1) . D (the cut's two faces),
+# int sigma1:eps2 = 0, so with p1 = K_pD(s)/s, t2 = K_tq(s)/s ... in the time
+# domain
+#     sigma_(n|s)(x1, tau | q at x2)  =  int_0^tau p(x2, t | D_(n|s) at x1) dt
+# (the q -> traction kernel is the time integral of the DD -> pressure
+# kernel).  Dimensionally: the pressure pairs with the injected volume.
+# Neither side's formula appears in the other (DD -> p: order-2 part f2 and the
+# Gaussian monopole; q -> sigma: h2 and E1), so a dropped term, a wrong sign or
+# factor in either fails this.
+
+def _pD_point(w, t, e, Ds, Dn):
+    p, _ = P.point_kernel(np.array([w]), t, K3, e, Ds, Dn, 0.0)
+    return p[0].real
+
+
+def _tq_point(w, tau, bt):
+    p, d2 = P.point_kernel(np.array([w]), tau, K3, np.exp(1j * bt), 0.0, 0.0, 1.0)
+    return -K3["eta"] * p[0] + np.exp(2j * bt) * (-4 * K3["eta"] * d2[0])
+
+
+def _time_integral(f, tau):
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", integrate.IntegrationWarning)
+        return integrate.quad(f, 0.0, tau, epsabs=0, epsrel=1e-13, limit=400,
+                              points=[tau * 1e-6, tau * 1e-4, tau * 1e-2])[0]
+
+
+@pytest.mark.parametrize("x2", [0.03 + 0.02j, -0.01 + 0.05j, 0.1 - 0.02j])
+def test_reciprocity_point_kernels(x2):
+    b1 = 0.37
+    e1 = np.exp(1j * b1)
+    x1 = 0.0 + 0.0j
+    for tau in (10.0, 100.0, 1000.0):
+        T = _tq_point(x1 - x2, tau, b1)
+        for Ds, Dn, comp in ((0.0, 1.0, T.real), (1.0, 0.0, T.imag)):
+            lhs = _time_integral(lambda t: _pD_point(x2 - x1, t, e1, Ds, Dn), tau)
+            assert abs(lhs - comp) <= 1e-12 * abs(comp)
+
+
+@pytest.mark.parametrize("x2", [0.03 + 0.02j, 0.01 + 0.012j])
+def test_reciprocity_element_rule(x2):
+    # element level: the pressure at x2 from a DD element (the oracle's fixed
+    # element rule, near rule and analytic far form over the time range),
+    # time-integrated, equals the traction from a point source at x2
+    # integrated along the element (adaptive quadrature of the point kernel)
+    b1, a = 0.37, 0.02
+    e1 = np.exp(1j * b1)
+
+    def p_elem(t, Ds, Dn):
+        r = P.element_integral(x2, 0j, e1, a, t, K3, Ds, Dn, 0.0)
+        return (r[1] if r[0] == "near" else r[4]).real
+
+    for tau in (20.0, 200.0):
+        for Ds, Dn in ((0.0, 1.0), (1.0, 0.0)):
+            lhs = _time_integral(lambda t: p_elem(t, Ds, Dn), tau)
+            part = (lambda T: T.real) if Dn else (lambda T: T.imag)
+            rhs = integrate.quad(lambda s: part(_tq_point(s * e1 - x2, tau, b1)), -a, a,
+                                 epsabs=0, epsrel=1e-13, limit=200)[0]
+            assert abs(lhs - rhs) <= 1e-12 * abs(rhs)
+
+
+def test_fluid_source_far_field_is_centre_of_dilatation():
+    # outside the diffusion length the source's
+    # potential is V ln r / (2 pi), V = Q tau / S, so sigma^p = 2 eta Phi_,ij =
+    # (eta V / pi) d_ij ln r and the face traction is
+    #   T = sigma_n + i sigma_s = e^{2 i b_t} (eta V / pi) conj(w)^2 / |w|^4
+    # (d_ij ln r is trace-free; sigma_yy - sigma_xx + 2i sigma_xy = 2 conj(w)^2/|w|^4).
+    tau = 50.0
+    ell = math.sqrt(K3["c"] * tau)
+    V = tau / K3["S"]
+    for w in (25 * ell * np.exp(0.3j), 40 * ell * np.exp(2.2j), 60 * ell * np.exp(-1.0j)):
+        for bt in (0.0, 0.8, 2.5):
+            T = _tq_point(w, tau, bt)
+            ref = np.exp(2j * bt) * (K3["eta"] * V / np.pi) * np.conj(w) ** 2 / abs(w) ** 4
+            assert abs(T - ref) <= 1e-12 * abs(ref)
+    # element far form (analytic, u_min > 40) against the same exterior field
+    # integrated along the element
+    a, bs = 0.3, 0.4
+    e = np.exp(1j * bs)
+    for zt in (ZC + 40 * ell * np.exp(0.5j), ZC + 70 * ell * np.exp(-2.0j)):
+        for bt in (0.2, 1.3):
+            Phi, dPhi, Psi, p = P._far_element(zt, ZC, e, a, tau, K3, 0.0, 0.0, 1.0)
+            Tf = 2 * Phi.real + np.exp(2j * bt) * (np.conj(zt) * dPhi + Psi)
+
+            def part(s, f):
+                w = zt - (ZC + s * e)
+                return f(np.exp(2j * bt) * (K3["eta"] * V / np.pi) * np.conj(w) ** 2 / abs(w) ** 4)
+            ref = (integrate.quad(part, -a, a, args=(np.real,), epsabs=0, epsrel=1e-13)[0]
+                   + 1j * integrate.quad(part, -a, a, args=(np.imag,), epsabs=0, epsrel=1e-13)[0])
+            assert abs(Tf - ref) <= 1e-12 * abs(ref)
+            assert p == 0.0 or abs(p) <= 1e-30
