@@ -486,7 +486,7 @@ def gmres_extra(D, ctx, torch, dev, march_steps: int):
     mat = D.material_from_dict(c["material"])
     dt = c["dt"]
     tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=c["leaf"],
-                  order_p=c["p"], min_leaf_side=_poro_rc(c, g, (c["steps"] + 1) * dt))
+                  order_p=c["p_star"], min_leaf_side=_poro_rc(c, g, (c["steps"] + 1) * dt))
     ld = c["load"]
     b = D.farfield_rhs(ctx, f(g.beta), 3, ld["p_f"], ld["sH"], ld["sh"], net=False,
                        b_p=ld["p_f"] - ld["p0"])

@@ -185,11 +185,7 @@ int allreduce_sum(ddm_ctx_s* ctx, double* buf, int64_t count, cudaStream_t s) {
 // near-field and history caches of the owned items, the owned preconditioner
 // chunks) is dropped when the partition changes; it is rebuilt on demand.
 static void drop_owned_state(ddm_tree_s* t) {
-  for (auto& g : t->graphs) {
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    g.exec = nullptr;
-  }
-  for (auto& k : t->seen_keys) k = MatvecKey();
+  drop_graphs(t);
   for (double* p : t->hc_alloc) cudaFree(p);
   t->hc_alloc.clear();
   t->hc_lag.clear();

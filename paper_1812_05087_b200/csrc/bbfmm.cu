@@ -513,6 +513,7 @@ int bb_prepare(ddm_ctx_s* ctx, ddm_tree_s* t, int n) {
   int rc = bb_init_tables(ctx);
   if (rc) return rc;
   if (t->bb_n != n) {
+    drop_graphs(t);   // captured bbFMM graphs hold the old node arrays
     if (t->bb_w) cudaFree(t->bb_w);
     if (t->bb_f) cudaFree(t->bb_f);
     t->bb_w = t->bb_f = nullptr;

@@ -293,6 +293,12 @@ void split_costs(const int64_t* prefix_excl, int64_t total, int nleaves, int wor
 
 // fmm.cu
 int fmm_init_operators(ddm_tree_s* t, cudaStream_t s);
+// Destroy every captured matvec graph and forget the recently seen argument
+// sets.  Called whenever a buffer a captured graph may read or write is
+// rebuilt or reallocated (poroelastic near-field cache, bbFMM node arrays,
+// group partials, partition change): a graph holds raw pointers and would
+// otherwise replay against stale or freed memory.
+void drop_graphs(ddm_tree_s* t);
 // D: [n][ncomp], user order (d_sorted = false) or sorted order (true), full
 // length.  Writes the owned rows into y_user (user order, via perm) and/or
 // y_sorted.  ncomp = 2 (elastic) or 3 (poroelastic, elapsed = tau).

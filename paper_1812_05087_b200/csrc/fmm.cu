@@ -119,6 +119,16 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
                              double elapsed, const double* D, bool d_sorted, double* y_user,
                              double* y_sorted, int mode, cudaStream_t s);
 
+void drop_graphs(ddm_tree_s* t) {
+  for (auto& g : t->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+    g.key = MatvecKey();
+  }
+  for (auto& k : t->seen_keys) k = MatvecKey();
+  t->graph_next = t->seen_next = 0;
+}
+
 // CUDA-graph replay of the matvec launch sequence (23 launches for config 5,
 // fork/join across the two streams captured as graph edges): a call whose
 // arguments (pointers, material, elapsed time, mode, stream) repeat the
@@ -135,6 +145,10 @@ int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double el
   // time (GMRES), outside any capture
   if (mat->kind == 1 && mode == DDM_FMM && elapsed > 0)
     if ((rc = poro_near_cache_update(ctx, t, poro_params(mat, elapsed), s))) return rc;
+  // bbFMM node arrays sized for this order, also outside any capture (a
+  // change of order reallocates them and drops the graphs that used them)
+  if ((mode & DDM_BBFMM) && mat->kind == 0)
+    if ((rc = bb_prepare(ctx, t, (mode >> 8) & 0xff))) return rc;
   static const bool no_graph = [] {
     const char* e = getenv("DDM_NO_GRAPH");
     return e && e[0] == '1';

@@ -1610,6 +1610,9 @@ int poro_near_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, c
     if ((rc = dalloc(ctx, &t->nc, (size_t)t->nc_n))) return rc;
   }
   t->nc_valid = false;
+  // graphs captured against the previous blocks (another elapsed time) would
+  // replay the apply kernel on the blocks rebuilt here
+  drop_graphs(t);
   poro_near_build_kernel<<<nblk((int64_t)nown * kBuildGroups, 4), 128, 0, s>>>(
       nown, t->p2p_order, t->items, t->item_lo_owned, t->u_off, t->u_lo, t->u_hi, t->leaves,
       t->c_start, t->c_count, t->ex, t->ey, t->ea, t->ec, t->es, k, 1, 1, 0, t->nc_off, t->nc);
@@ -1625,6 +1628,7 @@ int poro_near_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const PoroParams& P, c
 // cost ~20 ms)
 static int group_partials(ddm_ctx_s* ctx, ddm_tree_s* t, size_t doubles, double** out) {
   if (t->gpart_n < (int64_t)doubles) {
+    drop_graphs(t);   // captured on-the-fly graphs hold the old buffer
     if (t->gpart) cudaFree(t->gpart);
     t->gpart = nullptr;
     t->gpart_n = 0;
@@ -1663,7 +1667,10 @@ int launch_poro_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, con
   double* gpart = nullptr;
   if (G > 1) {
     int rc;
-    if ((rc = group_partials(ctx, t, (size_t)G * nown * kTgtGroup * 3, &gpart))) return rc;
+    // sized for at least the history kernels' 8 groups, so a later history
+    // call never reallocates the buffer under a captured matvec graph
+    if ((rc = group_partials(ctx, t, (size_t)std::max(G, 8) * nown * kTgtGroup * 3, &gpart)))
+      return rc;
   }
   poro_p2p_kernel<<<nblk((int64_t)nown * G, 4), 128, 0, s>>>(
       nown, t->p2p_order, t->items, t->u_off, t->u_lo, t->u_hi, t->leaves, t->c_start, t->c_count,
@@ -1714,6 +1721,10 @@ bool poro_hist_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* m
     DDM_CUDA(ctx, cudaMemGetInfo(&fr, &total));
     const size_t cbytes = (size_t)t->nc_n * kLagChunk * sizeof(double);
     t->hc_max_chunks = fr > total / 4 && cbytes > 0 ? (int)((fr - total / 4) / cbytes) : 0;
+    // DDM_HIST_CHUNKS=k caps the budget at k chunks (tests of the fallback;
+    // read whenever a cache is keyed, so a test can change it in-process)
+    const char* cap_env = getenv("DDM_HIST_CHUNKS");
+    if (cap_env && cap_env[0]) t->hc_max_chunks = std::min(t->hc_max_chunks, atoi(cap_env));
     std::memcpy(t->hc_key, key, sizeof(key));
     t->hc_valid = true;
     t->hc_capped = false;
@@ -1733,9 +1744,12 @@ bool poro_hist_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* m
         // as many chunks as already exist (doubling: O(log) allocations)
         const int k = std::min(std::max(1, (int)t->hc_lag.size()), t->hc_max_chunks - ci);
         double* blk = nullptr;
-        if ((rc = dalloc(ctx, &blk, (size_t)t->nc_n * kLagChunk * k))) {
-          *rc_out = rc;
-          return false;
+        if (dalloc(ctx, &blk, (size_t)t->nc_n * kLagChunk * k)) {
+          // out of memory while growing: keep the lags built so far and
+          // evaluate this and later history sums on the fly (not an error)
+          ctx->err.clear();
+          t->hc_capped = true;
+          break;
         }
         t->hc_alloc.push_back(blk);
         for (int q = 0; q < k; ++q) t->hc_lag.push_back(blk + (size_t)q * t->nc_n * kLagChunk);
@@ -1753,8 +1767,9 @@ bool poro_hist_cache_update(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* m
       t->hc_ptrs = nullptr;
       t->hc_ptrs_n = 0;
       const int cap = std::max(2 * (int)t->hc_lag.size(), 64);
-      if ((rc = dalloc(ctx, &t->hc_ptrs, (size_t)cap))) {
-        *rc_out = rc;
+      if (dalloc(ctx, &t->hc_ptrs, (size_t)cap)) {
+        ctx->err.clear();
+        t->hc_capped = true;
         return false;
       }
       t->hc_ptrs_n = cap;

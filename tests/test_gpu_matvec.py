@@ -101,16 +101,53 @@ def test_fmm_parity_cfg4_geometry_elastic(ddm):
     assert rel_l2(yd, OE.matvec_dense(A, Dv)) <= 1e-12
 
 
+def _cfg5_hard_rows(tree, rng):
+    """User-order rows of config 5's hardest targets: every element of the leaf
+    with the most near-field sources (its P2P work splits into several
+    512-source items), of the largest leaf (> kChainMax = 256 elements keeps
+    Morton order in the near-field stream, if any), of the leaf with the most W
+    cells, and one element from each of 64 random leaves with W cells."""
+    leaves = tree.export("LEAVES")
+    start, count = tree.export("START"), tree.export("COUNT")
+    uoff, ulo, uhi = tree.export("U_OFF"), tree.export("U_LO"), tree.export("U_HI")
+    woff = tree.export("W_OFF")
+    perm = tree.export("PERM")
+    near = np.add.reduceat(uhi - ulo, uoff[:-1]) if ulo.size else np.zeros(leaves.size)
+    near = np.where(np.diff(uoff) > 0, near, 0)
+    nw = np.diff(woff)
+    picks = [int(np.argmax(near)), int(np.argmax(count[leaves])), int(np.argmax(nw))]
+    rows = []
+    for k in picks:
+        c = leaves[k]
+        rows.extend(perm[start[c]:start[c] + count[c]].tolist())
+    withw = np.nonzero(nw > 0)[0]
+    for k in rng.choice(withw, min(64, withw.size), replace=False):
+        c = leaves[k]
+        rows.append(int(perm[start[c] + rng.integers(count[c])]))
+    return np.unique(np.array(rows)), int(near.max()), int(count[leaves].max()), int(nw.max())
+
+
 def test_fmm_parity_cfg5_sampled_rows(ddm):
     # full size (N = 1e6, leaf 64, p = 20), in the launch configuration bench.py
     # times; the oracle evaluates sampled rows one by one against all sources
+    # (all host cores): 512 random rows plus the hardest leaves' targets
+    from . import _pool
     D, ctx, torch = ddm
     g, tree = _setup(D, ctx, torch, 5)
     Dv = random_dd(g.n, 2, CONFIGS[5]["d_seed"])
     y = _mv(D, ctx, torch, tree, Dv, "fmm")
-    rows = np.random.default_rng(5).choice(g.n, 48, replace=False)
-    ref = OE.matvec_rows(g, G0, NU0, Dv, rows)
+    rng = np.random.default_rng(5)
+    hard, max_near, max_count, max_w = _cfg5_hard_rows(tree, rng)
+    assert max_near > 512 and max_w > 0          # the cases the rows are meant to hit
+    rows = np.unique(np.concatenate([rng.choice(g.n, 512, replace=False), hard]))
+    ref = _pool.elastic_rows(g, G0, NU0, Dv, rows)
     assert rel_l2(y[rows], ref) <= 1e-8
+    # the hard rows on their own, and every sampled row within 1e-6 of its own
+    # scale (no single target is badly wrong inside a good aggregate)
+    sel = np.isin(rows, hard)
+    assert rel_l2(y[rows[sel]], ref[sel]) <= 1e-8
+    scale = np.linalg.norm(ref, axis=1).mean()
+    assert np.abs(y[rows] - ref).max() <= 1e-6 * scale
     # and deterministic: a second call is bitwise identical
     y2 = _mv(D, ctx, torch, tree, Dv, "fmm")
     assert np.array_equal(y, y2)

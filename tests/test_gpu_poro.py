@@ -368,3 +368,127 @@ def test_poro_march_vs_oracle(ddm):
             assert rel_l2(Dg[h, :, comp], ref[h, :, comp]) <= 1e-6, (h, comp)
     # the solution changes over time (poroelastic relaxation), so the history matters
     assert rel_l2(Dg[-1], Dg[0]) > 1e-4
+
+
+def test_graphs_follow_rebuilt_caches(ddm):
+    """Captured matvec graphs hold raw pointers to per-tree buffers; when a
+    buffer is rebuilt (the poroelastic near-field cache at a new elapsed time,
+    the bbFMM node arrays at a new order) the graphs that used it are dropped.
+    Alternating elapsed times and bbFMM orders on one tree, with fixed input and
+    output buffers (so every repeat is a graph replay): each result equals the
+    DIRECT evaluation of the same operator."""
+    D, ctx, torch = ddm
+    g = _subset(make_config(4), 8)
+    dt = CONFIGS[4]["dt"]
+    mat = D.material_from_dict(MAT)
+    tree = _tree(D, ctx, torch, g, leaf=16, p=28, min_side=_rc(3 * dt, g))
+    Dv = random_dd(g.n, 3, 77)
+    Dv[:, 2] *= 1e-9
+    Din = torch.tensor(Dv, device="cuda")
+    y = torch.empty_like(Din)
+    ref = {t: D.matvec(ctx, tree, mat, Din, mode="direct", elapsed=t).cpu().numpy()
+           for t in (dt, 3 * dt)}
+    for t in (dt, dt, dt, 3 * dt, 3 * dt, 3 * dt, dt, dt, 3 * dt, dt):
+        D.matvec(ctx, tree, mat, Din, y, mode="fmm", elapsed=t)
+        yy = y.cpu().numpy()
+        for c in range(3):
+            assert rel_l2(yy[:, c], ref[t][:, c]) <= 1e-8, (t, c)
+    # elastic tree: series and bbFMM orders alternate on the same buffers
+    ge = make_config(2)
+    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+    te = D.Tree(ctx, f(ge.xc), f(ge.yc), f(ge.half_len), f(ge.beta), leaf_size=32, order_p=20)
+    me = D.material(0, 8e9, 0.25)
+    De = f(random_dd(ge.n, 2, 78))
+    ye = torch.empty_like(De)
+    yd = D.matvec(ctx, te, me, De, mode="direct").cpu().numpy()
+    tol = {"fmm": 1e-8, "bbfmm3": 1e-3, "bbfmm6": 1e-5}
+    for mode in ("bbfmm3", "bbfmm3", "bbfmm3", "bbfmm6", "bbfmm6", "bbfmm6", "bbfmm3", "bbfmm3",
+                 "fmm", "fmm", "bbfmm6", "bbfmm3"):
+        D.matvec(ctx, te, me, De, ye, mode=mode)
+        assert rel_l2(ye.cpu().numpy(), yd) <= tol[mode], mode
+    tree.free()
+    te.free()
+
+
+def _history_series(g, dt, H, seed):
+    rng = np.random.default_rng(seed)
+    Dh = rng.uniform(-1e-3, 1e-3, (H, g.n, 3))
+    Dh[:, :, 2] *= 1e-9
+    return Dh
+
+
+@pytest.mark.parametrize("cap", [None, "2", "0"])
+def test_poro_history_lag_cache_long(ddm, monkeypatch, cap):
+    """History lag cache past one chunk (kLagChunk = 16): as
+    in a march, h = 1..40 on one tree (41 lags = three chunks, allocated by
+    doubling).  cap = "2" limits the chunk budget (DDM_HIST_CHUNKS) so lags
+    beyond 32 fall back to the on-the-fly near kernel; "0" never caches.
+    Every h against the oracle's direct double sum (dense lags)."""
+    from . import _pool
+    if cap is not None:
+        monkeypatch.setenv("DDM_HIST_CHUNKS", cap)
+    D, ctx, torch = ddm
+    g = _subset(make_config(4), 4)
+    dt = CONFIGS[4]["dt"]
+    H = 40
+    Dh = _history_series(g, dt, H, 4040)
+    K = [None] + _pool.poro_dense_many(g, MAT, [j * dt for j in range(1, H + 2)])
+    lags = [None] + [K[m + 1] - K[m] for m in range(1, H + 1)]
+    mat = D.material_from_dict(MAT)
+    Dt = torch.tensor(Dh, device="cuda")
+    tree = _tree(D, ctx, torch, g, leaf=16, p=28, min_side=_rc((H + 1) * dt, g))
+    assert tree.counts["LEVELS"] >= 4
+    for h in range(1, H + 1):
+        r = D.history_apply(ctx, tree, mat, dt, Dt[:h], mode="fmm").cpu().numpy()
+        ref = OH.history_sum(g, dict(MAT, kind=1), dt, Dh[:h], lags)
+        for c in range(3):
+            assert rel_l2(r[:, c], ref[:, c]) <= 1e-8, (cap, h, c)
+    tree.free()
+
+
+def test_poro_history_cfg4_h199_sampled_rows(ddm):
+    """Config 4 at its stated length (N = 2000, 200 steps of 60 s): the history
+    sum applied for h = 1..199 as the march does (lag cache over 13 chunks),
+    checked at h = 64 and h = 199 on 16 sampled rows against
+    the oracle's row blocks of every lag kernel; p* = 28
+    as benched."""
+    from . import _pool
+    D, ctx, torch = ddm
+    g = make_config(4)
+    c = CONFIGS[4]
+    dt, H = c["dt"], c["steps"] - 1
+    Dh = _history_series(g, dt, H, 199)
+    mat = D.material_from_dict(MAT)
+    tree = _tree(D, ctx, torch, g, leaf=c["leaf"], p=c["p_star"], min_side=_rc((H + 1) * dt, g))
+    Dt = torch.tensor(Dh, device="cuda")
+    rows = np.random.default_rng(199).choice(g.n, 16, replace=False)
+    blocks = _pool.poro_row_blocks_many(g, MAT, [j * dt for j in range(1, H + 2)], rows)
+    got = {}
+    for h in range(1, H + 1):
+        r = D.history_apply(ctx, tree, mat, dt, Dt[:h], mode="fmm")
+        if h in (64, H):
+            got[h] = r.cpu().numpy()
+    for h, r in got.items():
+        ref = np.zeros((rows.size, 3))
+        for m in range(1, h + 1):      # A^(m) = K((m+1) dt) - K(m dt), on D^(h-m)
+            ref += np.einsum("ijrc,jc->ir", blocks[m] - blocks[m - 1], Dh[h - m])
+        for comp in range(3):
+            assert rel_l2(r[rows, comp], ref[:, comp]) <= 1e-8, (h, comp)
+
+
+def test_poro_fmm_pstar_solution_vector_cfg4(ddm):
+    """Reading R7 on the poroelastic path: the FMM operator applied to config
+    4's step-0 solution (near and far fields cancel) must stay within
+    1e-8 of b per component.  Measured: p = 20 gives 2.8e-7 on the shear row, so
+    the config-4 march (tests and bench.py) runs at p* = 28."""
+    D, ctx, torch = ddm
+    g = make_config(4)
+    c = CONFIGS[4]
+    tau = c["dt"]
+    bref = OH.poro_rhs(g, c["load"])
+    A = _A(4, tau)
+    x = np.linalg.solve(A, bref.reshape(-1)).reshape(-1, 3)
+    tree = _tree(D, ctx, torch, g, p=c["p_star"], min_side=_rc(c["steps"] * tau, g))
+    y = _mv(D, ctx, torch, tree, x, "fmm", tau)
+    for comp in range(3):
+        assert rel_l2(y[:, comp], bref[:, comp]) <= 1e-8, comp
