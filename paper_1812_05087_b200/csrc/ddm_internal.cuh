@@ -186,6 +186,10 @@ struct ddm_tree_s {
   int64_t nrec = 0;
   int* it_roff = nullptr;         // [nitems+1] first record range of each P2P item
   int2* it_rng = nullptr;         // record ranges [rb, re) of each item's source window
+  int2* lr_rng = nullptr;         // [nu] record range [rbeg[u_lo], rbeg[u_hi]) of every U range
+                                  // (leaf k's ranges: u_off[k] .. u_off[k+1]; p2p_leaf_kernel)
+  int4* leaf_info = nullptr;      // [nleaves] (c_start, c_count, u_off[k], u_off[k+1]) of each leaf
+  double* y_near = nullptr;       // [n][2] elastic near field of the owned elements (sorted order)
   double* gpart = nullptr;        // per-group partials of the on-the-fly poroelastic near field
   int64_t gpart_n = 0;
   double2* part = nullptr;        // [nitems*32] partial tractions

@@ -35,6 +35,7 @@ int fmm_workspace(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     if ((rc = dalloc(ctx, &t->d_sorted, (size_t)t->n * 3))) return rc;
     if ((rc = dalloc(ctx, &t->y_sorted, (size_t)t->n * 3))) return rc;
     if ((rc = dalloc(ctx, &t->y_far, (size_t)t->n * 3))) return rc;
+    if ((rc = dalloc(ctx, &t->y_near, (size_t)t->n * 2))) return rc;
   }
   return build_source_stream(ctx, t, s);
 }
@@ -285,9 +286,11 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
   }
 
   // near field: P2P work items of the owned leaves
+  const bool leaf_p2p = !poro && use_leaf_p2p();
   stage_begin(ctx, DDM_ST_P2P, sn);
-  rc = poro ? launch_poro_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, PP, sn)
-            : launch_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, gc, sn);
+  rc = poro       ? launch_poro_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, PP, sn)
+       : leaf_p2p ? launch_p2p_leaf(ctx, t, gc, sn)
+                  : launch_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, gc, sn);
   if (rc) return rc;
   stage_end(ctx, DDM_ST_P2P, sn);
   DDM_CUDA(ctx, cudaEventRecord(ctx->ev_near, sn));
@@ -314,7 +317,8 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
   DDM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_near, 0));
   DDM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_far, 0));
   stage_begin(ctx, DDM_ST_FINAL, s);
-  rc = launch_finalize(ctx, t, lo, hi, ncomp, gc, pf, y_user, y_sorted, s);
+  rc = leaf_p2p ? launch_finalize_near(ctx, t, lo, hi, y_user, y_sorted, s)
+                : launch_finalize(ctx, t, lo, hi, ncomp, gc, pf, y_user, y_sorted, s);
   stage_end(ctx, DDM_ST_FINAL, s);
   return rc;
 }

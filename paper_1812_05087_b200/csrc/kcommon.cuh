@@ -123,6 +123,13 @@ int launch_prep_sources(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const
                         int ncomp, cudaStream_t s);
 int launch_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, double gc,
                cudaStream_t s);
+// leaf-block near field (records staged in shared memory by bulk copies) into
+// t->y_near, and the matching assembly y = y_near + y_far; DDM_P2P_LEAF=0
+// selects the item kernel (launch_p2p + launch_finalize) instead
+bool use_leaf_p2p();
+int launch_p2p_leaf(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, cudaStream_t s);
+int launch_finalize_near(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, double* y_user,
+                         double* y_sorted, cudaStream_t s);
 // near-field source stream (p2p.cu): chain order + break records once per
 // tree; prep_stream writes the element records (and D in sorted order)
 int build_source_stream(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);

@@ -439,6 +439,283 @@ p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ ite
   }
 }
 
+// ---------------------------------------------------------------- leaf blocks
+// Near field with the source records staged in shared memory:
+// one CTA (4 warps) per owned leaf B.  B's source records are the U(B) ranges
+// of the node-sharing stream, contiguous in srec, so each range (with the
+// record before it, which carries the previous node) is ONE 1-D bulk copy
+// (cp.async.bulk on the TMA engine) into shared memory, completing on an
+// mbarrier: warp 0 reads the leaf's range table, prefix-sums the staged sizes
+// with shuffles and its lanes issue one copy each.  (A leaf whose ranges
+// exceed the buffer is processed in chunks, built by thread 0.)  Every staged
+// record is then read by all targets of the leaf: 2 targets per lane, tp =
+// ceil(nt/2) lanes per slice, S slices (S <= 128/tp and about >= 16 records per
+// slice), slice s taking the s-th contiguous part of the chunk's records (a
+// node carry is re-initialised where a range starts).  Slice partials are
+// summed in a fixed order: deterministic, independent of the rank count.
+constexpr int kLeafThreads = 128;
+constexpr int kLeafMaxTg = 64;      // targets per pass (2 per lane, >= 4 slices)
+constexpr int kLeafMaxPieces = 32;  // ranges per chunk
+constexpr int kLeafMinRec = 16;     // records per slice (at least, where possible)
+#ifndef DDM_LEAF_RMAX
+#define DDM_LEAF_RMAX 384           // staged records per chunk (30 KB)
+#endif
+#ifndef DDM_LEAF_MINB
+#define DDM_LEAF_MINB 6
+#endif
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "DDM_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra DDM_WAIT_%=;\n}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes,
+                                         unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void load_rec_s(double (&sp)[kRecStride], const double* rec) {
+  const double2* g = reinterpret_cast<const double2*>(rec);
+#pragma unroll
+  for (int f = 0; f < kRecStride / 2; ++f) {
+    const double2 v = g[f];
+    sp[2 * f] = v.x;
+    sp[2 * f + 1] = v.y;
+  }
+}
+
+__global__ void __launch_bounds__(kLeafThreads, DDM_LEAF_MINB)
+p2p_leaf_kernel(int leaf_lo, const int4* __restrict__ leaf_info, const int2* __restrict__ lr_rng,
+                const double* __restrict__ srec, const double* __restrict__ ex,
+                const double* __restrict__ ey, const double* __restrict__ ec,
+                const double* __restrict__ es, double gc, int rmax, double* __restrict__ y_near) {
+  extern __shared__ __align__(128) double recs[];   // [rmax][kRecStride]
+  __shared__ __align__(8) unsigned long long bar;
+  // pieces of the current chunk: (first staged record = the carry, first real
+  // record in srec, real records, real-record prefix)
+  __shared__ int4 pcs[kLeafMaxPieces];
+  __shared__ int s_np, s_R, s_last, s_cur_r, s_cur_off;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const unsigned bar_a = smem_u32(&bar);
+  // (cs, nt, first range, end range) of the leaf
+  const int4 li = __ldg(leaf_info + leaf_lo + blockIdx.x);
+  const int cs = li.x, nt = li.y, rg0 = li.z, rg1 = li.w;
+  if (tid == 0) mbar_init(bar_a, 1);
+  __syncthreads();
+  unsigned phase = 0;
+  for (int tg0 = 0; tg0 < nt; tg0 += kLeafMaxTg) {
+    const int tg = min(kLeafMaxTg, nt - tg0);
+    const int tp = (tg + 1) >> 1, Smax = kLeafThreads / tp;
+    double zx[2], zy[2];
+    P2PAcc acc[2];
+    const int tl0 = tid % tp;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int ti = cs + tg0 + min(2 * tl0 + q, tg - 1);
+      zx[q] = __ldg(ex + ti);
+      zy[q] = __ldg(ey + ti);
+    }
+    int S = 1;
+    bool first_chunk = true;
+    if (tid == 0) {
+      s_cur_r = rg0;
+      s_cur_off = 0;
+    }
+    while (true) {
+      // ---- stage the next chunk
+      bool fast = false;
+      if (first_chunk && tid < 32 && rg1 - rg0 <= 32) {
+        // all ranges at once: lane r takes range rg0 + r
+        const int nr = rg1 - rg0;
+        int2 rg = make_int2(0, 0);
+        if (lane < nr) rg = __ldg(lr_rng + rg0 + lane);
+        const int L = rg.y - rg.x;
+        int incl = lane < nr ? L + 1 : 0;   // staged records of range `lane` (with its carry)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int used = __shfl_sync(0xffffffffu, incl, 31);
+        fast = used <= rmax;
+        if (fast) {
+          const int st0 = incl - (lane < nr ? L + 1 : 0);
+          if (lane < nr) pcs[lane] = make_int4(st0, rg.x, L, st0 - lane);
+          if (lane == 0) {
+            s_np = nr;
+            s_R = used - nr;
+            s_last = 1;
+            if (nr > 0) mbar_expect_tx(bar_a, (unsigned)used * kRecStride * 8u);
+          }
+          __syncwarp();
+          if (lane < nr)
+            bulk_g2s(smem_u32(recs + (size_t)st0 * kRecStride), srec + (int64_t)(rg.x - 1) * kRecStride,
+                     (unsigned)(L + 1) * kRecStride * 8u, bar_a);
+        }
+      }
+      fast = __syncthreads_or(fast);
+      if (!fast && tid == 0) {   // general case: greedy chunk from the cursor
+        int cur_r = s_cur_r, cur_off = s_cur_off;
+        int np = 0, used = 0, R = 0;
+        while (cur_r < rg1 && np < kLeafMaxPieces) {
+          const int2 rg = __ldg(lr_rng + cur_r);
+          const int L = rg.y - rg.x - cur_off;
+          const int room = rmax - used - 1;
+          if (room <= 0) break;
+          const int take = min(L, room);
+          pcs[np++] = make_int4(used, rg.x + cur_off, take, R);
+          used += take + 1;
+          R += take;
+          if (take < L) {
+            cur_off += take;
+            break;
+          }
+          ++cur_r;
+          cur_off = 0;
+        }
+        s_cur_r = cur_r;
+        s_cur_off = cur_off;
+        s_np = np;
+        s_R = R;
+        s_last = cur_r >= rg1;
+        if (np > 0) {
+          mbar_expect_tx(bar_a, (unsigned)used * kRecStride * 8u);
+          for (int q = 0; q < np; ++q) {
+            const int4 pc = pcs[q];
+            bulk_g2s(smem_u32(recs + (size_t)pc.x * kRecStride), srec + (int64_t)(pc.y - 1) * kRecStride,
+                     (unsigned)(pc.z + 1) * kRecStride * 8u, bar_a);
+          }
+        }
+      }
+      if (!fast) __syncthreads();
+      const int np = s_np, R = s_R;
+      const bool last = s_last;
+      if (first_chunk) {   // slices: >= kLeafMinRec records each where the leaf allows
+        S = max(1, min(Smax, R / kLeafMinRec));
+        first_chunk = false;
+      }
+      if (np == 0) break;
+      mbar_wait(bar_a, phase);
+      phase ^= 1u;
+      // ---- evaluate: slice `slice` of the chunk's records for 2 targets per lane
+      const int slice = tid / tp, tl = tid - slice * tp;
+      if (slice < S) {
+        const int a = (int)(((int64_t)R * slice) / S);
+        const int b = (int)(((int64_t)R * (slice + 1)) / S);
+        if (a < b) {
+          int p = 0;
+          while (p + 1 < np && pcs[p + 1].w <= a) ++p;
+          int4 pc = pcs[p];
+          int sidx = pc.x + 1 + (a - pc.w);
+          int nxt = pc.w + pc.z;
+          NodeCarry ncr[2];
+          {
+            double sp[kRecStride];
+            load_rec_s(sp, recs + (size_t)(sidx - 1) * kRecStride);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) node_init(ncr[q], zx[q], zy[q], sp);
+          }
+#pragma unroll 2
+          for (int r = a; r < b; ++r) {
+            if (r == nxt) {   // a new range: carry from its staged predecessor
+              ++p;
+              pc = pcs[p];
+              sidx = pc.x + 1;
+              nxt = pc.w + pc.z;
+              double sp[kRecStride];
+              load_rec_s(sp, recs + (size_t)(sidx - 1) * kRecStride);
+#pragma unroll
+              for (int q = 0; q < 2; ++q) node_init(ncr[q], zx[q], zy[q], sp);
+            }
+            double sp[kRecStride];
+            load_rec_s(sp, recs + (size_t)sidx * kRecStride);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) record_update(acc[q], ncr[q], zx[q], zy[q], sp);
+            ++sidx;
+          }
+        }
+      }
+      __syncthreads();   // the buffer is free for the next chunk
+      if (last) break;
+    }
+    // ---- slice partials -> per target, summed in slice order
+    const int slice = tid / tp, tl = tid - slice * tp;
+    double* red = recs;   // [S][2 tp][3] (<= 256 entries)
+    if (slice < S) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        double* o = red + ((size_t)slice * 2 * tp + 2 * tl + q) * 3;
+        o[0] = acc[q].phi;
+        o[1] = acc[q].psi.x;
+        o[2] = acc[q].psi.y;
+      }
+    }
+    __syncthreads();
+    if (tid < tg) {
+      P2PAcc tot;
+      for (int s2 = 0; s2 < S; ++s2) {
+        const double* o = red + ((size_t)s2 * 2 * tp + tid) * 3;
+        tot.phi += o[0];
+        tot.psi.x += o[1];
+        tot.psi.y += o[2];
+      }
+      const int ti = cs + tg0 + tid;
+      reinterpret_cast<double2*>(y_near)[ti] = acc_to_traction(tot, gc, ec[ti], es[ti]);
+    }
+    __syncthreads();
+  }
+}
+
+// per leaf: (first sorted element, count, first U range, end U range)
+__global__ void leaf_info_fill(int nleaves, const int* __restrict__ leaves,
+                               const int* __restrict__ c_start, const int* __restrict__ c_count,
+                               const int* __restrict__ u_off, int4* __restrict__ info) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nleaves) return;
+  const int c = leaves[k];
+  info[k] = make_int4(c_start[c], c_count[c], u_off[k], u_off[k + 1]);
+}
+
+// the record range of every U range (once per tree): lr_rng[r] = [rbeg[u_lo[r]], rbeg[u_hi[r]])
+__global__ void leaf_rng_fill(int64_t nu, const int* __restrict__ u_lo, const int* __restrict__ u_hi,
+                              const int* __restrict__ rbeg, int2* __restrict__ lr_rng) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r < nu) lr_rng[r] = make_int2(rbeg[u_lo[r]], rbeg[u_hi[r]]);
+}
+
+// elastic FMM assembly: y = near (p2p_leaf_kernel) + far (L2P), sorted and/or user order
+__global__ void finalize_near_kernel(int64_t e_lo, int64_t e_hi, const double2* __restrict__ y_near,
+                                     const double2* __restrict__ y_far,
+                                     const int* __restrict__ perm, double2* __restrict__ y_user,
+                                     double2* __restrict__ y_sorted) {
+  const int64_t i = e_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= e_hi) return;
+  const double2 a = y_near[i], b = y_far[i];
+  const double2 t = make_double2(a.x + b.x, a.y + b.y);
+  if (y_sorted) y_sorted[i] = t;
+  if (y_user) y_user[perm[i]] = t;
+}
+
 __global__ void add_const_kernel(int64_t n, int v, int* __restrict__ a) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) a[i] += v;
@@ -509,6 +786,44 @@ int launch_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, double g
   return DDM_OK;
 }
 
+// Elastic near field, leaf blocks: owned leaves in Morton
+// order (consecutive CTAs share source records in L2); writes y_near.
+bool use_leaf_p2p() {
+  static const bool on = [] {
+    const char* e = getenv("DDM_P2P_LEAF");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+int launch_p2p_leaf(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, cudaStream_t s) {
+  const int nlv = t->own_leaf_hi - t->own_leaf_lo;
+  if (nlv <= 0) return DDM_OK;
+  const int rmax = DDM_LEAF_RMAX;
+  const size_t shm = (size_t)rmax * kRecStride * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    DDM_CUDA(ctx, cudaFuncSetAttribute(p2p_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)shm));
+    attr = true;
+  }
+  p2p_leaf_kernel<<<nlv, kLeafThreads, shm, s>>>(t->own_leaf_lo, t->leaf_info, t->lr_rng, t->srec,
+                                                t->ex, t->ey, t->ec, t->es, gc, rmax, t->y_near);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+int launch_finalize_near(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, double* y_user,
+                         double* y_sorted, cudaStream_t s) {
+  if (hi <= lo) return DDM_OK;
+  finalize_near_kernel<<<nblk(hi - lo, 256), 256, 0, s>>>(
+      lo, hi, reinterpret_cast<const double2*>(t->y_near),
+      reinterpret_cast<const double2*>(t->y_far), t->perm, reinterpret_cast<double2*>(y_user),
+      reinterpret_cast<double2*>(y_sorted));
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
 // Near-field source stream of the tree (once per tree, outside any capture)
 int build_source_stream(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   if (t->srec || t->n == 0) return DDM_OK;
@@ -549,6 +864,16 @@ int build_source_stream(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   if ((rc = dalloc(ctx, &t->it_rng, (size_t)std::max(nr, 1)))) return rc;
   item_rng_fill<<<nblk(ni, 128), 128, 0, s>>>(ni, t->items, t->u_off, t->u_lo, t->u_hi, t->rbeg,
                                               t->it_roff, t->it_rng);
+  DDM_CUDA(ctx, cudaGetLastError());
+  // record ranges of the U ranges (leaf-block near field)
+  if ((rc = dalloc(ctx, &t->lr_rng, (size_t)std::max<int64_t>(t->nu, 1)))) return rc;
+  if (t->nu > 0) {
+    leaf_rng_fill<<<nblk(t->nu, 256), 256, 0, s>>>(t->nu, t->u_lo, t->u_hi, t->rbeg, t->lr_rng);
+    DDM_CUDA(ctx, cudaGetLastError());
+  }
+  if ((rc = dalloc(ctx, &t->leaf_info, (size_t)t->nleaves))) return rc;
+  leaf_info_fill<<<nblk(t->nleaves, 256), 256, 0, s>>>(t->nleaves, t->leaves, t->c_start, t->c_count,
+                                                       t->u_off, t->leaf_info);
   DDM_CUDA(ctx, cudaGetLastError());
   DDM_CUDA(ctx, cudaStreamSynchronize(s));
   return DDM_OK;
