@@ -834,6 +834,176 @@ l2p_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int* __restrict__ el_lea
   if (ncomp == 3) y_far[i * ncomp + 2] = pf.on ? -4.0 * pf.kp * gc * phi_t.y / pf.fu : 0.0;
 }
 
+// Block-staged L2P: a CTA of 128 threads takes 128
+// consecutive owned elements (a few leaves).  The leaves' geometry and local
+// series and the multipoles of their W cells (contiguous in the W CSR) are
+// first copied into shared memory by all threads at once -- the per-element
+// chain el_leaf -> leaves -> cell geometry -> coefficients becomes a few
+// block-wide load stages -- then every thread evaluates its element exactly
+// as l2p_kernel does (same Horner order: bitwise identical results) from
+// shared memory.  Runs of elements with more than kL2PLeaves leaves or
+// kL2PW W cells take the global-memory path of l2p_kernel.
+constexpr int kL2PThreads = 128;
+constexpr int kL2PLeaves = 16;
+constexpr int kL2PW = 32;
+
+template <int PT>
+__device__ __forceinline__ void l2p_eval(int p, double x, double y, bool has_local, double2 z0,
+                                         double is, const double2* L, int nwc,
+                                         const double4* wg, const double2* WM, int wstride,
+                                         double2& phi_t, double2& X_t) {
+  phi_t = make_double2(0.0, 0.0);
+  X_t = phi_t;
+  if (has_local) {
+    const double2 u = make_double2((x - z0.x) * is, (y - z0.y) * is);
+    double2 phi = make_double2(0, 0), dphi = phi, psi = phi;
+    // Horner for Phi and, by synthetic division, Phi' (dphi = dphi u + phi
+    // before phi takes its next coefficient)
+#pragma unroll
+    for (int mm = pmax<PT>() - 1; mm >= 0; --mm) {
+      if (!PT && mm >= p) continue;
+      const double2 lm = L[mm], gm = L[p + mm];
+      if (mm <= p - 2)
+        dphi = make_double2(fma(dphi.x, u.x, fma(-dphi.y, u.y, phi.x)),
+                            fma(dphi.x, u.y, fma(dphi.y, u.x, phi.y)));
+      phi = make_double2(fma(phi.x, u.x, fma(-phi.y, u.y, lm.x)),
+                         fma(phi.x, u.y, fma(phi.y, u.x, lm.y)));
+      psi = make_double2(fma(psi.x, u.x, fma(-psi.y, u.y, gm.x)),
+                         fma(psi.x, u.y, fma(psi.y, u.x, gm.y)));
+    }
+    phi_t = phi;
+    X_t = cadd(cmul(cconj(u), dphi), psi);
+  }
+  for (int wi = 0; wi < nwc; ++wi) {
+    const double4 g = wg[wi];
+    const double2 u = make_double2((x - g.x) * g.z, (y - g.y) * g.z);
+    const double inn = 1.0 / fma(u.x, u.x, u.y * u.y);
+    const double2 v = make_double2(u.x * inn, -u.y * inn);
+    const double2* M = WM + (size_t)wi * wstride;
+    double2 f = make_double2(0, 0), fd = f, g2 = f;
+#pragma unroll
+    for (int n = pmax<PT>(); n >= 1; --n) {
+      if (!PT && n > p) continue;
+      const double2 an = M[n - 1], cn = M[p + n - 1];
+      fd = make_double2(fma(fd.x, v.x, fma(-fd.y, v.y, f.x)), fma(fd.x, v.y, fma(fd.y, v.x, f.y)));
+      f = make_double2(fma(f.x, v.x, fma(-f.y, v.y, an.x)), fma(f.x, v.y, fma(f.y, v.x, an.y)));
+      g2 = make_double2(fma(g2.x, v.x, fma(-g2.y, v.y, cn.x)), fma(g2.x, v.y, fma(g2.y, v.x, cn.y)));
+    }
+    const double2 dPdv = cadd(f, cmul(v, fd));
+    const double2 v2 = cmul(v, v);
+    const double2 dPdu = make_double2(-(v2.x * dPdv.x - v2.y * dPdv.y),
+                                      -(v2.x * dPdv.y + v2.y * dPdv.x));
+    phi_t = cadd(phi_t, cmul(f, v));
+    X_t = cadd(X_t, cadd(cmul(cconj(u), dPdu), cmul(g2, v)));
+  }
+}
+
+#ifndef DDM_L2PB_MINB
+#define DDM_L2PB_MINB 8
+#endif
+template <int PT>
+__global__ void __launch_bounds__(kL2PThreads, DDM_L2PB_MINB)
+l2p_block_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int* __restrict__ el_leaf,
+                 const int* __restrict__ leaves, const int* __restrict__ c_level,
+                 const int* __restrict__ c_ix, const int* __restrict__ c_iy,
+                 const double2* __restrict__ local, const int* __restrict__ w_off,
+                 const int* __restrict__ w_idx, const double2* __restrict__ mpole, CellGeom cg,
+                 int p_rt, double gc, PoroFar pf, const double* __restrict__ ex,
+                 const double* __restrict__ ey, const double* __restrict__ ec,
+                 const double* __restrict__ es, double* __restrict__ y_far) {
+  const int p = PT ? PT : p_rt;
+  const int P2 = 2 * p;
+  extern __shared__ double2 l2p_sh[];   // [kL2PLeaves][2p] locals | [kL2PW][2p] W multipoles
+  double2* shL = l2p_sh;
+  double2* shW = l2p_sh + (size_t)kL2PLeaves * P2;
+  __shared__ double4 kgeo[kL2PLeaves];   // (z0.x, z0.y, 1/s, has local)
+  __shared__ double4 wgeo[kL2PW];        // (z_D.x, z_D.y, 1/s_D, -)
+  __shared__ int kcell[kL2PLeaves], kw[kL2PLeaves + 1], wcell[kL2PW];
+  __shared__ int s_k0, s_nk, s_w0, s_nw;
+  const int tid = threadIdx.x;
+  const int64_t i0 = e_lo + (int64_t)blockIdx.x * kL2PThreads;
+  const int64_t i = i0 + tid;
+  const bool valid = i < e_hi;
+  pdl_wait();   // the leaves' final locals (L2L)
+  const int k = valid ? __ldg(el_leaf + i) : -1;
+  if (tid == 0) {
+    const int k0 = k, k1 = __ldg(el_leaf + min(i0 + kL2PThreads, e_hi) - 1);
+    s_k0 = k0;
+    s_nk = k1 - k0 + 1;
+    s_w0 = __ldg(w_off + k0);
+    s_nw = __ldg(w_off + k1 + 1) - s_w0;
+  }
+  __syncthreads();
+  const int k0 = s_k0, nk = s_nk, w0 = s_w0, nw = s_nw;
+  const bool staged = nk <= kL2PLeaves && nw <= kL2PW;
+  if (staged) {
+    if (tid < nk) {
+      const int c = __ldg(leaves + k0 + tid);
+      const int lev = __ldg(c_level + c);
+      kcell[tid] = c;
+      const double2 z0 = cg.centre(lev, __ldg(c_ix + c), __ldg(c_iy + c));
+      kgeo[tid] = make_double4(z0.x, z0.y, 1.0 / cg.side(lev), lev >= 2 ? 1.0 : 0.0);
+      kw[tid] = __ldg(w_off + k0 + tid) - w0;
+      if (tid == nk - 1) kw[nk] = nw;
+    } else if (tid >= 64 && tid - 64 < nw) {
+      const int D = __ldg(w_idx + w0 + tid - 64);
+      const int ld = __ldg(c_level + D);
+      wcell[tid - 64] = D;
+      const double2 zd = cg.centre(ld, __ldg(c_ix + D), __ldg(c_iy + D));
+      wgeo[tid - 64] = make_double4(zd.x, zd.y, ldexp(1.0 / cg.W, ld), 0.0);
+    }
+    __syncthreads();
+    for (int e = tid; e < nk * P2; e += kL2PThreads) {
+      const int kl = e / P2, m = e - kl * P2;
+      shL[e] = __ldg(local + (size_t)kcell[kl] * P2 + m);
+    }
+    for (int e = tid; e < nw * P2; e += kL2PThreads) {
+      const int wl = e / P2, m = e - wl * P2;
+      shW[e] = __ldg(mpole + (size_t)wcell[wl] * P2 + m);
+    }
+    __syncthreads();
+  }
+  if (!valid) return;
+  const double x = ex[i], y = ey[i];
+  double2 phi_t, X_t;
+  if (staged) {
+    const int kl = k - k0;
+    const double4 g = kgeo[kl];
+    const int wa = kw[kl], wb = kw[kl + 1];
+    l2p_eval<PT>(p, x, y, g.w != 0.0, make_double2(g.x, g.y), g.z, shL + (size_t)kl * P2, wb - wa,
+                 wgeo + wa, shW + (size_t)wa * P2, P2, phi_t, X_t);
+  } else {
+    // global-memory path (rare: many tiny leaves or W cells in one run)
+    const int c = __ldg(leaves + k);
+    const int lev = __ldg(c_level + c);
+    const double2 z0 = cg.centre(lev, __ldg(c_ix + c), __ldg(c_iy + c));
+    phi_t = make_double2(0.0, 0.0);
+    X_t = phi_t;
+    double2 ph, Xl;
+    l2p_eval<PT>(p, x, y, lev >= 2, z0, 1.0 / cg.side(lev), local + (size_t)c * P2, 0, nullptr,
+                 nullptr, P2, ph, Xl);
+    phi_t = ph;
+    X_t = Xl;
+    for (int wi = __ldg(w_off + k), we = __ldg(w_off + k + 1); wi < we; ++wi) {
+      const int D = __ldg(w_idx + wi);
+      const int ld = __ldg(c_level + D);
+      const double2 zd = cg.centre(ld, __ldg(c_ix + D), __ldg(c_iy + D));
+      const double4 wg1 = make_double4(zd.x, zd.y, ldexp(1.0 / cg.W, ld), 0.0);
+      double2 pw, Xw;
+      l2p_eval<PT>(p, x, y, false, z0, 0.0, nullptr, 1, &wg1, mpole + (size_t)D * P2, P2, pw, Xw);
+      phi_t = cadd(phi_t, pw);
+      X_t = cadd(X_t, Xw);
+    }
+  }
+  const double2 W = make_double2(-gc * X_t.y, gc * X_t.x);
+  const double ct = ec[i], st = es[i];
+  const double2 e2 = make_double2(ct * ct - st * st, 2.0 * ct * st);
+  const double2 t2 = cmul(e2, W);
+  y_far[i * ncomp + 0] = t2.y;
+  y_far[i * ncomp + 1] = t2.x - 2.0 * gc * phi_t.y;
+  if (ncomp == 3) y_far[i * ncomp + 2] = pf.on ? -4.0 * pf.kp * gc * phi_t.y / pf.fu : 0.0;
+}
+
 // ------------------------------------------------------------ finalize (a11)
 // per owned sorted element: near field (sum of the P2P partials of its target
 // group, in item order) + far field (y_far), written in user and/or sorted order
@@ -1088,22 +1258,43 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   return DDM_OK;
 }
 
-// L2P of the owned elements into t->y_far (far-field stream)
+// L2P of the owned elements into t->y_far (far-field stream): block-staged
+// kernel by default, DDM_L2P_BLOCK=0 the thread-per-element kernel
 int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFar& pf,
                cudaStream_t s) {
   const int64_t lo = t->own_el_lo, hi = t->own_el_hi;
   if (hi <= lo) return DDM_OK;
   const CellGeom cg{t->x_min, t->y_min, t->W};
+  static const bool blk = [] {
+    const char* e = getenv("DDM_L2P_BLOCK");
+    return !(e && e[0] == '0');
+  }();
   const unsigned nb = nblk(hi - lo, 256);
+  const unsigned nbb = nblk(hi - lo, kL2PThreads);
+  const size_t shb = (size_t)(kL2PLeaves + kL2PW) * 2 * t->p * sizeof(double2);
+  int rc = DDM_OK;
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \
-    DDM_CUDA(ctx, launch_pdl(use_pdl(t), l2p_kernel<PT>, nb, 256, 0, s, (int64_t)lo, (int64_t)hi, ncomp,    \
-                             (const int*)t->el_leaf, (const int*)t->leaves,                    \
-                             (const int*)t->c_level, (const int*)t->c_ix, (const int*)t->c_iy, \
-                             (const double2*)t->local, (const int*)t->w_off,                   \
-                             (const int*)t->w_idx, (const double2*)t->mpole, cg, t->p, gc, pf, \
-                             (const double*)t->ex, (const double*)t->ey,                       \
-                             (const double*)t->ec, (const double*)t->es, t->y_far));           \
+    if (blk) {                                                                                  \
+      if ((rc = set_smem(ctx, l2p_block_kernel<PT>, shb))) return rc;                           \
+      DDM_CUDA(ctx, launch_pdl(use_pdl(t), l2p_block_kernel<PT>, nbb, kL2PThreads, shb, s,      \
+                               (int64_t)lo, (int64_t)hi, ncomp, (const int*)t->el_leaf,         \
+                               (const int*)t->leaves, (const int*)t->c_level,                  \
+                               (const int*)t->c_ix, (const int*)t->c_iy,                       \
+                               (const double2*)t->local, (const int*)t->w_off,                 \
+                               (const int*)t->w_idx, (const double2*)t->mpole, cg, t->p, gc,   \
+                               pf, (const double*)t->ex, (const double*)t->ey,                 \
+                               (const double*)t->ec, (const double*)t->es, t->y_far));         \
+    } else {                                                                                    \
+      DDM_CUDA(ctx, launch_pdl(use_pdl(t), l2p_kernel<PT>, nb, 256, 0, s, (int64_t)lo,          \
+                               (int64_t)hi, ncomp, (const int*)t->el_leaf,                     \
+                               (const int*)t->leaves, (const int*)t->c_level,                  \
+                               (const int*)t->c_ix, (const int*)t->c_iy,                       \
+                               (const double2*)t->local, (const int*)t->w_off,                 \
+                               (const int*)t->w_idx, (const double2*)t->mpole, cg, t->p, gc,   \
+                               pf, (const double*)t->ex, (const double*)t->ey,                 \
+                               (const double*)t->ec, (const double*)t->es, t->y_far));         \
+    }                                                                                           \
   } while (0)
   DDM_P_DISPATCH(t->p, DDM_L);
 #undef DDM_L
