@@ -114,6 +114,15 @@ enum {
 };
 int ddm_tree_counts(ddm_tree_t tree, int64_t* counts);
 
+/* Timing of the last ddm_build_tree of `tree` (keys, sort, cells,
+ * interaction lists; built once per geometry), written into
+ * ms[DDM_TB_N] [host], milliseconds: stage spans from CUDA events on the build
+ * stream (host gaps included) and the host wall time of the whole call
+ * (operators and partition included).  Always available; no profiling mode. */
+enum { DDM_TB_KEYS = 0, DDM_TB_SORT, DDM_TB_CELLS, DDM_TB_LISTS, DDM_TB_SCHED, DDM_TB_TOTAL,
+       DDM_TB_N };
+int ddm_tree_build_times(ddm_tree_t tree, double* ms);
+
 /* Copy one exported array into dst [host] (capacity in bytes).  Arrays:
  *   KEYS    u64[n]   Morton key of each element, user order
  *   PERM    i32[n]   sorted position -> user index

@@ -62,6 +62,8 @@ ddm_build_tree = _proto("ddm_build_tree", _i, _vp, _dp, _dp, _dp, _dp, _i64, _i,
                         C.POINTER(_vp))
 ddm_tree_free = _proto("ddm_tree_free", None, _vp)
 ddm_tree_counts = _proto("ddm_tree_counts", _i, _vp, C.POINTER(_i64))
+ddm_tree_build_times = _proto("ddm_tree_build_times", _i, _vp, C.POINTER(C.c_double))
+TB = ["keys", "sort", "cells", "lists", "sched", "total"]
 ddm_tree_export = _proto("ddm_tree_export", _i, _vp, _i, _vp, _i64)
 ddm_tree_partition = _proto("ddm_tree_partition", _i, _vp, _i, _i)
 ddm_split_costs = _proto("ddm_split_costs", _i, C.POINTER(_i64), _i64, _i, _i, C.POINTER(_i))
@@ -87,4 +89,4 @@ EXPORTED = ["ddm_version", "ddm_last_error", "ddm_nccl_unique_id", "ddm_ctx_crea
             "ddm_tree_export", "ddm_tree_partition", "ddm_split_costs", "ddm_matvec",
             "ddm_history_apply", "ddm_history_rhs", "ddm_gmres_solve", "ddm_precond_apply",
             "ddm_farfield_rhs", "ddm_sif", "ddm_tip_growth",
-            "ddm_set_profiling", "ddm_stage_times"]
+            "ddm_set_profiling", "ddm_stage_times", "ddm_tree_build_times"]

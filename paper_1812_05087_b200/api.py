@@ -124,6 +124,13 @@ class Tree:
         self.ctx.check(L.ddm_tree_counts(self._h, arr))
         return {k: int(arr[v]) for k, v in L.TC.items()}
 
+    def build_times(self) -> dict:
+        """ddm_tree_build_times: ms per build stage (keys, sort, cells, lists,
+        sched) and the host wall time of the build call (total)."""
+        arr = (C.c_double * len(L.TB))()
+        self.ctx.check(L.ddm_tree_build_times(self._h, arr))
+        return {k: float(arr[i]) for i, k in enumerate(L.TB)}
+
     def export(self, what: str) -> np.ndarray:
         c = self.counts
         n, nc, nl = c["N"], c["CELLS"], c["LEAVES"]

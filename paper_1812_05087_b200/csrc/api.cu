@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <new>
 
@@ -417,9 +418,12 @@ int ddm_build_tree(ddm_ctx_t ctx, const double* xc, const double* yc, const doub
   cudaStream_t s = (cudaStream_t)stream;
   ddm_tree_s* t = new (std::nothrow) ddm_tree_s();
   if (!t) return set_error(ctx, DDM_ERR_OOM, "host allocation");
+  const auto t0 = std::chrono::steady_clock::now();
   int rc = build_tree(ctx, xc, yc, half_len, beta, n, leaf_size, order_p, min_leaf_side, s, t);
   if (!rc) rc = fmm_init_operators(t, s);
   if (!rc) rc = partition_tree(t, ctx->rank, ctx->world, s);
+  t->build_ms[DDM_TB_TOTAL] =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (rc) {
     cudaStreamSynchronize(s);
     cudaGetLastError();
@@ -459,6 +463,12 @@ int ddm_tree_counts(ddm_tree_t t, int64_t* c) {
   c[DDM_TC_P] = t->p;
   c[DDM_TC_W] = t->nw;
   c[DDM_TC_W_MIN] = t->w_min;
+  return DDM_OK;
+}
+
+int ddm_tree_build_times(ddm_tree_t t, double* ms) {
+  if (!t || !ms) return DDM_ERR_ARG;
+  for (int i = 0; i < DDM_TB_N; ++i) ms[i] = t->build_ms[i];
   return DDM_OK;
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include <string>
 #include <vector>
@@ -99,6 +100,7 @@ struct MatvecGraph {
 
 struct ddm_tree_s {
   ddm_ctx_s* ctx = nullptr;
+  double build_ms[DDM_TB_N] = {};   // ddm_tree_build_times
   int64_t n = 0;
   int leaf = 0, p = 0;
   int nlevels = 0;           // number of levels (max level + 1)
@@ -277,6 +279,26 @@ int dalloc(ddm_ctx_s* ctx, T** p, size_t count) {
   if (e != cudaSuccess) {
     cudaGetLastError();
     return set_error(ctx, DDM_ERR_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+  }
+  return DDM_OK;
+}
+
+// Tree-lifetime allocation from the stream-ordered pool (the context keeps
+// the pool's memory mapped): no device-wide synchronisation per array, unlike
+// cudaMalloc.  Freed by free_tree with cudaFree (valid for pool memory).
+template <class T>
+int talloc(ddm_ctx_s* ctx, T** p, size_t count, cudaStream_t s) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  static const bool pool = [] {
+    const char* v = getenv("DDM_TREE_POOL");
+    return !(v && v[0] == '0');
+  }();
+  cudaError_t e = pool ? cudaMallocAsync((void**)p, count * sizeof(T), s)
+                       : cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(ctx, DDM_ERR_OOM, std::string("cudaMallocAsync failed: ") + cudaGetErrorString(e));
   }
   return DDM_OK;
 }

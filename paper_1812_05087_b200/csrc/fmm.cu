@@ -28,14 +28,14 @@ double binom(int n, int k) {
 int fmm_workspace(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   int rc;
   if (!t->mpole) {
-    if ((rc = dalloc(ctx, &t->mpole, (size_t)t->ncells * 2 * t->p))) return rc;
-    if ((rc = dalloc(ctx, &t->local, (size_t)t->ncells * 2 * t->p))) return rc;
-    if ((rc = dalloc(ctx, &t->src, (size_t)t->n * kSrcStride))) return rc;
-    if ((rc = dalloc(ctx, &t->part, (size_t)t->nitems * kTgtGroup * 2))) return rc;  // <= 4 doubles/slot
-    if ((rc = dalloc(ctx, &t->d_sorted, (size_t)t->n * 3))) return rc;
-    if ((rc = dalloc(ctx, &t->y_sorted, (size_t)t->n * 3))) return rc;
-    if ((rc = dalloc(ctx, &t->y_far, (size_t)t->n * 3))) return rc;
-    if ((rc = dalloc(ctx, &t->y_near, (size_t)t->n * 2))) return rc;
+    if ((rc = talloc(ctx, &t->mpole, (size_t)t->ncells * 2 * t->p, s))) return rc;
+    if ((rc = talloc(ctx, &t->local, (size_t)t->ncells * 2 * t->p, s))) return rc;
+    if ((rc = talloc(ctx, &t->src, (size_t)t->n * kSrcStride, s))) return rc;
+    if ((rc = talloc(ctx, &t->part, (size_t)t->nitems * kTgtGroup * 2, s))) return rc;  // <= 4 doubles/slot
+    if ((rc = talloc(ctx, &t->d_sorted, (size_t)t->n * 3, s))) return rc;
+    if ((rc = talloc(ctx, &t->y_sorted, (size_t)t->n * 3, s))) return rc;
+    if ((rc = talloc(ctx, &t->y_far, (size_t)t->n * 3, s))) return rc;
+    if ((rc = talloc(ctx, &t->y_near, (size_t)t->n * 2, s))) return rc;
   }
   return build_source_stream(ctx, t, s);
 }
@@ -92,9 +92,9 @@ int fmm_init_operators(ddm_tree_s* t, cudaStream_t s) {
     }
   }
   int rc;
-  if ((rc = dalloc(ctx, &t->op_pas, pas.size())) || (rc = dalloc(ctx, &t->op_pasT, pasT.size())) ||
-      (rc = dalloc(ctx, &t->op_pm2l, pm2l.size())) || (rc = dalloc(ctx, &t->op_w, w.size())) ||
-      (rc = dalloc(ctx, &t->op_eps, eps.size())) || (rc = dalloc(ctx, &t->op_e2i, e2i.size())))
+  if ((rc = talloc(ctx, &t->op_pas, pas.size(), s)) || (rc = talloc(ctx, &t->op_pasT, pasT.size(), s)) ||
+      (rc = talloc(ctx, &t->op_pm2l, pm2l.size(), s)) || (rc = talloc(ctx, &t->op_w, w.size(), s)) ||
+      (rc = talloc(ctx, &t->op_eps, eps.size(), s)) || (rc = talloc(ctx, &t->op_e2i, e2i.size(), s)))
     return rc;
   DDM_CUDA(ctx, cudaMemcpyAsync(t->op_pas, pas.data(), pas.size() * sizeof(double),
                                 cudaMemcpyHostToDevice, s));

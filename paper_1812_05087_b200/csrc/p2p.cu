@@ -830,8 +830,8 @@ int build_source_stream(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   const int64_t n = t->n;
   int rc;
   int* cntv = nullptr;
-  if ((rc = dalloc(ctx, &t->st_elem, (size_t)n)) || (rc = dalloc(ctx, &t->st_code, (size_t)n)) ||
-      (rc = dalloc(ctx, &t->rbeg, (size_t)n + 1)) || (rc = dalloc(ctx, &cntv, (size_t)n + 1)))
+  if ((rc = talloc(ctx, &t->st_elem, (size_t)n, s)) || (rc = talloc(ctx, &t->st_code, (size_t)n, s)) ||
+      (rc = talloc(ctx, &t->rbeg, (size_t)n + 1, s)) || (rc = talloc(ctx, &cntv, (size_t)n + 1, s)))
     return rc;
   chain_order_kernel<<<nblk(t->nleaves, 64), 64, 0, s>>>(t->nleaves, t->leaves, t->c_start,
                                                          t->c_count, t->ex, t->ey, t->ea, t->ec,
@@ -841,12 +841,12 @@ int build_source_stream(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   DDM_CUDA(ctx, cudaMemsetAsync(cntv + n, 0, sizeof(int), s));
   int total = 0;
   if ((rc = exclusive_scan_i32(ctx, cntv, t->rbeg, (int)n + 1, &total, s))) return rc;
-  cudaFree(cntv);
+  cudaFreeAsync(cntv, s);
   // records: pad (0), then the slots' records; rbeg was counted from 0
   add_const_kernel<<<nblk(n + 1, 256), 256, 0, s>>>(n + 1, 1, t->rbeg);
   DDM_CUDA(ctx, cudaGetLastError());
   t->nrec = (int64_t)total + 1;
-  if ((rc = dalloc(ctx, &t->srec, (size_t)t->nrec * kRecStride))) return rc;
+  if ((rc = talloc(ctx, &t->srec, (size_t)t->nrec * kRecStride, s))) return rc;
   const double2 pad = make_double2(t->x_min - 16.0 * t->W, t->y_min - 16.0 * t->W);
   break_records_kernel<<<nblk(n, 256), 256, 0, s>>>(n, t->st_elem, t->st_code, t->rbeg, t->ex,
                                                     t->ey, t->ea, t->ec, t->es, pad, t->srec);
@@ -854,24 +854,24 @@ int build_source_stream(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   // record ranges of every P2P item
   const int ni = t->nitems;
   int* icnt = nullptr;
-  if ((rc = dalloc(ctx, &t->it_roff, (size_t)ni + 1)) || (rc = dalloc(ctx, &icnt, (size_t)ni + 1)))
+  if ((rc = talloc(ctx, &t->it_roff, (size_t)ni + 1, s)) || (rc = talloc(ctx, &icnt, (size_t)ni + 1, s)))
     return rc;
   item_rng_count<<<nblk(ni + 1, 128), 128, 0, s>>>(ni, t->items, t->u_off, t->u_lo, t->u_hi, icnt);
   DDM_CUDA(ctx, cudaGetLastError());
   int nr = 0;
   if ((rc = exclusive_scan_i32(ctx, icnt, t->it_roff, ni + 1, &nr, s))) return rc;
-  cudaFree(icnt);
-  if ((rc = dalloc(ctx, &t->it_rng, (size_t)std::max(nr, 1)))) return rc;
+  cudaFreeAsync(icnt, s);
+  if ((rc = talloc(ctx, &t->it_rng, (size_t)std::max(nr, 1), s))) return rc;
   item_rng_fill<<<nblk(ni, 128), 128, 0, s>>>(ni, t->items, t->u_off, t->u_lo, t->u_hi, t->rbeg,
                                               t->it_roff, t->it_rng);
   DDM_CUDA(ctx, cudaGetLastError());
   // record ranges of the U ranges (leaf-block near field)
-  if ((rc = dalloc(ctx, &t->lr_rng, (size_t)std::max<int64_t>(t->nu, 1)))) return rc;
+  if ((rc = talloc(ctx, &t->lr_rng, (size_t)std::max<int64_t>(t->nu, 1), s))) return rc;
   if (t->nu > 0) {
     leaf_rng_fill<<<nblk(t->nu, 256), 256, 0, s>>>(t->nu, t->u_lo, t->u_hi, t->rbeg, t->lr_rng);
     DDM_CUDA(ctx, cudaGetLastError());
   }
-  if ((rc = dalloc(ctx, &t->leaf_info, (size_t)t->nleaves))) return rc;
+  if ((rc = talloc(ctx, &t->leaf_info, (size_t)t->nleaves, s))) return rc;
   leaf_info_fill<<<nblk(t->nleaves, 256), 256, 0, s>>>(t->nleaves, t->leaves, t->c_start, t->c_count,
                                                        t->u_off, t->leaf_info);
   DDM_CUDA(ctx, cudaGetLastError());

@@ -42,34 +42,49 @@ __device__ __forceinline__ uint32_t compact_bits(uint64_t x) {
 }
 
 // ---------------------------------------------------------------- a1
+// Root square and input validation in one pass (a1): per block the min/max
+// of the centres and the largest half-length; bad |= 1 for a non-finite
+// centre, 2 for a half-length that is not finite and > 0.
 __global__ void minmax_partial(const double* __restrict__ x, const double* __restrict__ y,
-                               int64_t n, double4* __restrict__ part, int* __restrict__ bad) {
-  double xmn = INFINITY, xmx = -INFINITY, ymn = INFINITY, ymx = -INFINITY;
-  int nonfinite = 0;
+                               const double* __restrict__ ha, int64_t n,
+                               double4* __restrict__ part, double* __restrict__ pamax,
+                               int* __restrict__ bad) {
+  double xmn = INFINITY, xmx = -INFINITY, ymn = INFINITY, ymx = -INFINITY, am = 0.0;
+  int flags = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double a = x[i], b = y[i];
-    if (!isfinite(a) || !isfinite(b)) nonfinite = 1;
+    const double a = x[i], b = y[i], h = ha[i];
+    if (!isfinite(a) || !isfinite(b)) flags |= 1;
+    if (!(isfinite(h) && h > 0.0)) flags |= 2;
     xmn = fmin(xmn, a); xmx = fmax(xmx, a); ymn = fmin(ymn, b); ymx = fmax(ymx, b);
+    am = fmax(am, h);
   }
   for (int o = 16; o; o >>= 1) {
     xmn = fmin(xmn, __shfl_xor_sync(0xffffffffu, xmn, o));
     xmx = fmax(xmx, __shfl_xor_sync(0xffffffffu, xmx, o));
     ymn = fmin(ymn, __shfl_xor_sync(0xffffffffu, ymn, o));
     ymx = fmax(ymx, __shfl_xor_sync(0xffffffffu, ymx, o));
+    am = fmax(am, __shfl_xor_sync(0xffffffffu, am, o));
   }
   __shared__ double4 sh[32];
+  __shared__ double sa[32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) sh[w] = make_double4(xmn, xmx, ymn, ymx);
-  if (nonfinite) atomicOr(bad, 1);
+  if (lane == 0) {
+    sh[w] = make_double4(xmn, xmx, ymn, ymx);
+    sa[w] = am;
+  }
+  if (flags) atomicOr(bad, flags);
   __syncthreads();
   if (threadIdx.x == 0) {
     double4 r = sh[0];
+    double ra = sa[0];
     for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
       r.x = fmin(r.x, sh[k].x); r.y = fmax(r.y, sh[k].y);
       r.z = fmin(r.z, sh[k].z); r.w = fmax(r.w, sh[k].w);
+      ra = fmax(ra, sa[k]);
     }
     part[blockIdx.x] = r;
+    pamax[blockIdx.x] = ra;
   }
 }
 
@@ -159,14 +174,11 @@ int cells_reserve(ddm_ctx_s* ctx, Cells& c, int need, int used, cudaStream_t s) 
                      &c.nchild, &c.leaf};
   for (int f = 0; f < 9; ++f) {
     int* nb = nullptr;
-    int rc = dalloc(ctx, &nb, ncap);
+    int rc = talloc(ctx, &nb, ncap, s);
     if (rc) return rc;
     if (*fields[f] && used) DDM_CUDA(ctx, cudaMemcpyAsync(nb, *fields[f], sizeof(int) * used,
                                                           cudaMemcpyDeviceToDevice, s));
-    if (*fields[f]) {
-      DDM_CUDA(ctx, cudaStreamSynchronize(s));
-      cudaFree(*fields[f]);
-    }
+    if (*fields[f]) cudaFreeAsync(*fields[f], s);   // stream-ordered after the copy
     *fields[f] = nb;
   }
   c.cap = ncap;
@@ -530,6 +542,33 @@ void free_tree(ddm_tree_s* t) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
 }
 
+// CUDA events at the stage boundaries of build_tree (ddm_tree_build_times)
+struct BuildEvents {
+  cudaEvent_t ev[DDM_TB_TOTAL + 1] = {};
+  void record(int k, cudaStream_t s) {
+    if (!ev[k] && cudaEventCreate(&ev[k]) != cudaSuccess) {
+      cudaGetLastError();
+      ev[k] = nullptr;
+      return;
+    }
+    cudaEventRecord(ev[k], s);
+  }
+  void store(double* ms) {
+    for (int k = 0; k < DDM_TB_TOTAL; ++k) {
+      float v = 0.f;
+      if (ev[k] && ev[k + 1] && cudaEventElapsedTime(&v, ev[k], ev[k + 1]) != cudaSuccess) {
+        cudaGetLastError();
+        v = 0.f;
+      }
+      ms[k] = v;
+    }
+  }
+  ~BuildEvents() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
 int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double* a,
                const double* beta, int64_t n, int leaf, int p, double min_side,
                cudaStream_t s, ddm_tree_s* t) {
@@ -542,42 +581,45 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
   t->leaf = leaf;
   t->p = p;
 
-  // ---- a1: root square
+  // ---- a1: root square, validation and the largest half-length (one pass,
+  // one small read-back)
+  BuildEvents bev;
+  bev.record(0, s);
   const int mmb = 148;
   double4* part = nullptr;
+  double* pamax = nullptr;
   int* dbad = nullptr;
   DDM_CUDA(ctx, cudaMallocAsync((void**)&part, mmb * sizeof(double4), s));
+  DDM_CUDA(ctx, cudaMallocAsync((void**)&pamax, mmb * sizeof(double), s));
   DDM_CUDA(ctx, cudaMallocAsync((void**)&dbad, sizeof(int), s));
   DDM_CUDA(ctx, cudaMemsetAsync(dbad, 0, sizeof(int), s));
-  minmax_partial<<<mmb, 256, 0, s>>>(xc, yc, n, part, dbad);
+  minmax_partial<<<mmb, 256, 0, s>>>(xc, yc, a, n, part, pamax, dbad);
   DDM_CUDA(ctx, cudaGetLastError());
   std::vector<double4> hpart(mmb);
+  std::vector<double> hamax(mmb);
   int hbad = 0;
   DDM_CUDA(ctx, cudaMemcpyAsync(hpart.data(), part, mmb * sizeof(double4),
+                                cudaMemcpyDeviceToHost, s));
+  DDM_CUDA(ctx, cudaMemcpyAsync(hamax.data(), pamax, mmb * sizeof(double),
                                 cudaMemcpyDeviceToHost, s));
   DDM_CUDA(ctx, cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
   DDM_CUDA(ctx, cudaStreamSynchronize(s));
   cudaFreeAsync(part, s);
+  cudaFreeAsync(pamax, s);
   cudaFreeAsync(dbad, s);
-  if (hbad) return set_error(ctx, DDM_ERR_GEOM, "non-finite element coordinates");
+  if (hbad & 1) return set_error(ctx, DDM_ERR_GEOM, "non-finite element coordinates");
+  if (hbad & 2) return set_error(ctx, DDM_ERR_GEOM, "element half-lengths must be finite and > 0");
   double xmn = INFINITY, xmx = -INFINITY, ymn = INFINITY, ymx = -INFINITY;
-  for (auto& v : hpart) {
+  t->a_max = 0.0;
+  for (int b = 0; b < mmb; ++b) {
+    const double4 v = hpart[b];
     xmn = std::min(xmn, v.x); xmx = std::max(xmx, v.y);
     ymn = std::min(ymn, v.z); ymx = std::max(ymx, v.w);
+    t->a_max = std::max(t->a_max, hamax[b]);
   }
   double W = std::max(xmx - xmn, ymx - ymn);
   if (W == 0.0) W = 1.0;
   const double scale = 1073741824.0 / W;  // 2^30 / W, one IEEE division
-  {
-    std::vector<double> ha(n);
-    DDM_CUDA(ctx, cudaMemcpy(ha.data(), a, n * sizeof(double), cudaMemcpyDeviceToHost));
-    t->a_max = 0.0;
-    for (double v : ha) {
-      if (!(std::isfinite(v) && v > 0))
-        return set_error(ctx, DDM_ERR_GEOM, "element half-lengths must be finite and > 0");
-      t->a_max = std::max(t->a_max, v);
-    }
-  }
   t->x_min = xmn;
   t->y_min = ymn;
   t->W = W;
@@ -588,14 +630,15 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
   uint64_t* k2 = nullptr;
   int* v2 = nullptr;
   int* vin = nullptr;
-  if ((rc = dalloc(ctx, &t->keys_user, n)) || (rc = dalloc(ctx, &t->keys, n)) ||
-      (rc = dalloc(ctx, &t->perm, n)))
+  if ((rc = talloc(ctx, &t->keys_user, n, s)) || (rc = talloc(ctx, &t->keys, n, s)) ||
+      (rc = talloc(ctx, &t->perm, n, s)))
     return rc;
   DDM_CUDA(ctx, cudaMallocAsync((void**)&k2, n * sizeof(uint64_t), s));
   DDM_CUDA(ctx, cudaMallocAsync((void**)&v2, n * sizeof(int), s));
   DDM_CUDA(ctx, cudaMallocAsync((void**)&vin, n * sizeof(int), s));
   morton_kernel<<<nblk(n, 256), 256, 0, s>>>(xc, yc, n, xmn, ymn, scale, t->keys_user, vin);
   DDM_CUDA(ctx, cudaGetLastError());
+  bev.record(DDM_TB_SORT, s);
   DDM_CUDA(ctx, cudaMemcpyAsync(t->keys, t->keys_user, n * sizeof(uint64_t),
                                 cudaMemcpyDeviceToDevice, s));
   {
@@ -628,6 +671,7 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
   cudaFreeAsync(vin, s);
 
   // ---- a3 cells, level by level
+  bev.record(DDM_TB_CELLS, s);
   Cells C;
   if ((rc = cells_reserve(ctx, C, (int)std::max<int64_t>(64, 4 * (n / leaf + 1) + 8), 0, s)))
     return rc;
@@ -701,11 +745,12 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
   t->c_nchild = C.nchild; t->c_leaf = C.leaf;
 
   // ---- a4 colleagues and V lists
+  bev.record(DDM_TB_LISTS, s);
   int* vtmp = nullptr;
   unsigned char* vcls_tmp = nullptr;
   int* vcnt = nullptr;
-  if ((rc = dalloc(ctx, &t->colleagues, (size_t)ncells * 9))) return rc;
-  if ((rc = dalloc(ctx, &t->v_off, ncells + 1))) return rc;
+  if ((rc = talloc(ctx, &t->colleagues, (size_t)ncells * 9, s))) return rc;
+  if ((rc = talloc(ctx, &t->v_off, ncells + 1, s))) return rc;
   DDM_CUDA(ctx, cudaMallocAsync((void**)&vtmp, (size_t)ncells * 27 * sizeof(int), s));
   DDM_CUDA(ctx, cudaMallocAsync((void**)&vcls_tmp, (size_t)ncells * 27, s));
   DDM_CUDA(ctx, cudaMallocAsync((void**)&vcnt, (size_t)(ncells + 1) * sizeof(int), s));
@@ -727,7 +772,7 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
     if ((rc = exclusive_scan_i32(ctx, vcnt, t->v_off, ncells, &nv, s))) return rc;
     DDM_CUDA(ctx, cudaMemcpyAsync(t->v_off + ncells, &nv, sizeof(int), cudaMemcpyHostToDevice, s));
     t->nv = nv;
-    if ((rc = dalloc(ctx, &t->v_idx, nv)) || (rc = dalloc(ctx, &t->v_cls, nv))) return rc;
+    if ((rc = talloc(ctx, &t->v_idx, nv, s)) || (rc = talloc(ctx, &t->v_cls, nv, s))) return rc;
     compact_v<<<nblk(ncells, 128), 128, 0, s>>>(ncells, vtmp, vcls_tmp, vcnt, t->v_off,
                                                 t->v_idx, t->v_cls);
     DDM_CUDA(ctx, cudaGetLastError());
@@ -750,7 +795,7 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
     int nl = 0;
     if ((rc = exclusive_scan_i32(ctx, flag, pos, (int)n, &nl, s))) return rc;
     t->nleaves = nl;
-    if ((rc = dalloc(ctx, &t->leaves, nl)) || (rc = dalloc(ctx, &t->el_leaf, n))) return rc;
+    if ((rc = talloc(ctx, &t->leaves, nl, s)) || (rc = talloc(ctx, &t->el_leaf, n, s))) return rc;
     gather_leaves<<<nblk(n, 256), 256, 0, s>>>(n, lbs, flag, pos, t->leaves);
     DDM_CUDA(ctx, cudaGetLastError());
     element_leaf<<<nl, 64, 0, s>>>(nl, t->leaves, C.start, C.count, t->el_leaf);
@@ -782,11 +827,11 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
     DDM_CUDA(ctx, cudaMallocAsync((void**)&utmp, (size_t)std::max(tot, 1) * sizeof(int2), s));
     // W lists: offsets per leaf, cells
     int nwt = 0;
-    if ((rc = dalloc(ctx, &t->w_off, nl + 1))) return rc;
+    if ((rc = talloc(ctx, &t->w_off, nl + 1, s))) return rc;
     if ((rc = exclusive_scan_i32(ctx, wcnt, t->w_off, nl, &nwt, s))) return rc;
     DDM_CUDA(ctx, cudaMemcpyAsync(t->w_off + nl, &nwt, sizeof(int), cudaMemcpyHostToDevice, s));
     t->nw = nwt;
-    if ((rc = dalloc(ctx, &t->w_idx, std::max(nwt, 1)))) return rc;
+    if ((rc = talloc(ctx, &t->w_idx, std::max(nwt, 1), s))) return rc;
     u_fill<<<nblk(nl, 64), 64, 0, s>>>(nl, t->leaves, C.parent, t->colleagues, C.leaf, C.start,
                                        C.count, C.level, C.ix, C.iy, C.first_child, C.nchild,
                                        t->w_min, uoff, utmp, mcnt, nsrc, t->w_off, t->w_idx);
@@ -795,8 +840,8 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
     int nu = 0;
     if ((rc = exclusive_scan_i32(ctx, mcnt, moff, nl, &nu, s))) return rc;
     t->nu = nu;
-    if ((rc = dalloc(ctx, &t->u_off, nl + 1)) || (rc = dalloc(ctx, &t->u_lo, nu)) ||
-        (rc = dalloc(ctx, &t->u_hi, nu)))
+    if ((rc = talloc(ctx, &t->u_off, nl + 1, s)) || (rc = talloc(ctx, &t->u_lo, nu, s)) ||
+        (rc = talloc(ctx, &t->u_hi, nu, s)))
       return rc;
     DDM_CUDA(ctx, cudaMemcpyAsync(t->u_off, moff, nl * sizeof(int), cudaMemcpyDeviceToDevice, s));
     DDM_CUDA(ctx, cudaMemcpyAsync(t->u_off + nl, &nu, sizeof(int), cudaMemcpyHostToDevice, s));
@@ -815,12 +860,12 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
     if ((rc = exclusive_scan_i64(ctx, (const int64_t*)pairs, (int64_t*)pairs_scan, nl, &np, s)))
       return rc;
     t->near_pairs = np;
-    if ((rc = dalloc(ctx, &t->item_off, nl + 1))) return rc;
+    if ((rc = talloc(ctx, &t->item_off, nl + 1, s))) return rc;
     int ni = 0;
     if ((rc = exclusive_scan_i32(ctx, icnt, t->item_off, nl, &ni, s))) return rc;
     DDM_CUDA(ctx, cudaMemcpyAsync(t->item_off + nl, &ni, sizeof(int), cudaMemcpyHostToDevice, s));
     t->nitems = ni;
-    if ((rc = dalloc(ctx, &t->items, ni))) return rc;
+    if ((rc = talloc(ctx, &t->items, ni, s))) return rc;
     item_fill<<<nblk(nl, 128), 128, 0, s>>>(nl, t->leaves, C.start, C.count, nsrc, t->item_off,
                                             t->items);
     DDM_CUDA(ctx, cudaGetLastError());
@@ -849,9 +894,10 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
   }
 
   // ---- element data in Morton order
-  if ((rc = dalloc(ctx, &t->ex, n)) || (rc = dalloc(ctx, &t->ey, n)) ||
-      (rc = dalloc(ctx, &t->ea, n)) || (rc = dalloc(ctx, &t->ec, n)) ||
-      (rc = dalloc(ctx, &t->es, n)))
+  bev.record(DDM_TB_SCHED, s);
+  if ((rc = talloc(ctx, &t->ex, n, s)) || (rc = talloc(ctx, &t->ey, n, s)) ||
+      (rc = talloc(ctx, &t->ea, n, s)) || (rc = talloc(ctx, &t->ec, n, s)) ||
+      (rc = talloc(ctx, &t->es, n, s)))
     return rc;
   permute_elements<<<nblk(n, 256), 256, 0, s>>>(n, t->perm, xc, yc, a, beta, t->ex, t->ey,
                                                 t->ea, t->ec, t->es);
@@ -873,7 +919,7 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
       t->up_level_off[2 * lev + 1] = (int)up.size();
     }
     t->n_up = (int)up.size();
-    if ((rc = dalloc(ctx, &t->up_list, up.size()))) return rc;
+    if ((rc = talloc(ctx, &t->up_list, up.size(), s))) return rc;
     if (!up.empty())
       DDM_CUDA(ctx, cudaMemcpyAsync(t->up_list, up.data(), up.size() * sizeof(int),
                                     cudaMemcpyHostToDevice, s));
@@ -929,7 +975,7 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
     if (Ls > 0 && t->nlevels - 1 - Ls >= 2) {
       const int nroot = t->level_off[Ls + 1] - t->level_off[Ls];
       const int nsl = t->nlevels - Ls;
-      if ((rc = dalloc(ctx, &t->sub_up, sup.size())) || (rc = dalloc(ctx, &t->sub_cells, scell.size())))
+      if ((rc = talloc(ctx, &t->sub_up, sup.size(), s)) || (rc = talloc(ctx, &t->sub_cells, scell.size(), s)))
         return rc;
       DDM_CUDA(ctx, cudaMemcpyAsync(t->sub_up, sup.data(), sup.size() * sizeof(int2),
                                     cudaMemcpyHostToDevice, s));
@@ -941,7 +987,9 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
       t->sub_nsl = nsl;
     }
   }
+  bev.record(DDM_TB_TOTAL, s);
   DDM_CUDA(ctx, cudaStreamSynchronize(s));
+  bev.store(t->build_ms);
   return DDM_OK;
 }
 
