@@ -79,15 +79,65 @@ class Clocks:
                 "samples": len(rows)}
 
 
-def cpu_baseline_oracle(g, mat, Dv, rows: int):
-    """The oracle (numpy, fp64, as it stands) on a bounded sample: `rows` target
-    rows of config 5 against all N sources (oracle/elastic.matvec_rows)."""
+def _host_info() -> dict:
+    info = {"nproc": os.cpu_count()}
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                info["cpu_model"] = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return info
+
+
+def _oracle_rows(args):
     from oracle import elastic as OE
+    g, G, nu, Dv, idx = args
+    return OE.matvec_rows(g, G, nu, Dv, idx)
+
+
+def cpu_baseline_oracle(g, mat, Dv, rows: int, workers: int | None = None):
+    """The oracle (numpy, fp64, as it stands) on a bounded sample: `rows` target
+    rows of config 5 against all N sources (oracle/elastic.matvec_rows), the
+    rows split over `workers` processes (default: every host core).  Returns
+    (interactions/s, seconds, workers)."""
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+    workers = workers or os.cpu_count() or 1
     idx = np.random.default_rng(1234).choice(g.n, rows, replace=False)
+    chunks = [c for c in np.array_split(idx, workers) if c.size]
+    jobs = [(g, mat["G"], mat["nu"], Dv, c) for c in chunks]
+    with ProcessPoolExecutor(max_workers=len(jobs), mp_context=mp.get_context("spawn")) as ex:
+        list(ex.map(_oracle_rows, jobs[:1]))        # worker start-up outside the timing
+        t0 = time.perf_counter()
+        list(ex.map(_oracle_rows, jobs))
+        dt = time.perf_counter() - t0
+    return rows * g.n / dt, dt, len(jobs)
+
+
+def oracle_gmres_cfg2():
+    """The oracle's dense GMRES on config 2 (oracle/gmres.py: CGS2, Givens,
+    unpreconditioned, tol 1e-10) beside the GPU solve: assembly and solve
+    times, iterations; numpy BLAS threads as configured on the host."""
+    from oracle import elastic as OE
+    from oracle import gmres as OG
+    from synth import CONFIGS, make_config
+    c = CONFIGS[2]
+    g = make_config(2)
     t0 = time.perf_counter()
-    OE.matvec_rows(g, mat["G"], mat["nu"], Dv, idx)
-    dt = time.perf_counter() - t0
-    return rows * g.n / dt, dt
+    A = OE.assemble_dense(g, c["material"]["G"], c["material"]["nu"])
+    t1 = time.perf_counter()
+    b = OE.farfield_rhs(g, c["load"]).reshape(-1)
+    x, it, rr, ok = OG.gmres(lambda v: A @ v, b, tol=c["tol"], restart=2000, max_iter=10000)
+    t2 = time.perf_counter()
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((d.get("num_threads", 1) for d in threadpool_info()), default=1)
+    except Exception:
+        threads = None
+    return {"assembly_s": t1 - t0, "solve_s": t2 - t1, "iters": it, "rel_resid": rr,
+            "blas_threads": threads, "precond": "none (the oracle follows the paper's plain GMRES)"}
 
 
 def run_reference(args):
@@ -100,23 +150,24 @@ def run_reference(args):
     g = make_config(args.config)
     Dv = random_dd(g.n, 2, c["d_seed"])
     rows = args.ref_rows
+    cores = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_baseline_oracle(g, c["material"], Dv, max(1, rows // 4))
+        cpu_baseline_oracle(g, c["material"], Dv, max(cores, rows // 4))
     times = []
     for _ in range(args.steps):
-        v, dt = cpu_baseline_oracle(g, c["material"], Dv, rows)
+        v, dt, cores = cpu_baseline_oracle(g, c["material"], Dv, rows)
         times.append(dt)
     tot = sum(times)
     value = args.steps * rows * g.n / tot
-    sample = (f"{rows} seeded target rows x all {g.n} sources per step "
-              f"(oracle.elastic.matvec_rows, numpy fp64)")
+    sample = (f"{rows} seeded target rows x all {g.n} sources per step, split over {cores} "
+              f"processes (oracle.elastic.matvec_rows, numpy fp64)")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": c["name"], "N": g.n, "leaf": c["leaf"], "p": c["p"]},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                            "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": sample, "host": _host_info()},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -150,14 +201,21 @@ def run_ours(args):
     mat = D.material_from_dict(c["material"])
     stream = torch.cuda.current_stream()
 
-    # tree (built once per geometry)
+    # tree (built once per geometry): the first build in the
+    # process includes one-time kernel-module loading; the tree used below is
+    # the second build (steady state), timed per stage by the library
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    t0 = time.perf_counter()
     tree = D.Tree(ctx, xc, yc, hl, be, leaf_size=c["leaf"], order_p=p)
-    e1.record()
     torch.cuda.synchronize()
-    tree_ms = e0.elapsed_time(e1)
+    tree_first_ms = (time.perf_counter() - t0) * 1e3
+    tree.free()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tree = D.Tree(ctx, xc, yc, hl, be, leaf_size=c["leaf"], order_p=p)
+    torch.cuda.synchronize()
+    tree_ms = (time.perf_counter() - t0) * 1e3
+    tree_stages = tree.build_times()
     cnt = tree.counts
 
     Dv_host = random_dd(n, 2, c["d_seed"])
@@ -269,6 +327,7 @@ def run_ours(args):
         p2p_conc += ctx.stage_times()["p2p"] / nprof
     ctx.set_profiling(False)
     fp64_peak = ctx_probe_fp64(ctx)
+    kern = kernel_rooflines(tree, cnt, stages, tree_stages, p, fp64_peak, world)
     owned_pairs = cnt["NEAR_PAIRS"] / world   # approx. per rank for N > 1
     p2p_ms = stages["p2p"]
     achieved = owned_pairs * FLOP_PER_PAIR / (p2p_ms * 1e-3) / 1e12
@@ -290,13 +349,16 @@ def run_ours(args):
                       "elements_per_fracture": 100, "fractures": 10000, "box_m": 2000,
                       "parallelism": f"morton-leaf-partition x{world}",
                       "l2": "flushed between steps (256 MiB write, outside the step events)",
-                      "tree_build_ms": tree_ms, "cells": cnt["CELLS"], "leaves": cnt["LEAVES"],
+                      "tree_build_ms": tree_ms, "tree_build_first_ms": tree_first_ms,
+                      "tree_build_stage_ms": tree_stages,
+                      "cells": cnt["CELLS"], "leaves": cnt["LEAVES"],
                       "levels": levels, "v_pairs": cnt["V"], "near_pairs": cnt["NEAR_PAIRS"]},
            "stage_ms": stages,
-           "roofline": {"bound": "alu", "kernel": "p2p_kernel (fp64 pipe)",
+           "kernels": kern,
+           "roofline": {"bound": "alu", "kernel": "p2p_leaf_kernel (fp64 pipe)",
                         "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                         "frac": achieved / fp64_peak if fp64_peak else None,
-                        "traffic": _ncu_traffic("p2p_kernel"),
+                        "traffic": _ncu_traffic("p2p_leaf_kernel"),
                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one "
                                           "ncu --set full capture (profiles/ncu_traffic.json)",
                         "peak_source": "measured DFMA-chain probe (ddm_probe_fp64) on this GPU",
@@ -328,15 +390,106 @@ def run_ours(args):
         out["bbfmm"] = bbfmm_extra(D, ctx, torch, tree, mat, Dd, y, flush, cnt, fp64_peak)
         # GMRES solve time on config 2 (the metric's second half), at p and p*
         out["gmres"] = gmres_extra(D, ctx, torch, dev, args.march_steps)
-        gv, gdt = cpu_baseline_oracle(g, c["material"], Dv_host, args.cpu_rows)
-        out["cpu_baseline"] = {"value": gv, "unit": UNIT, "cores": 1, "kind": "oracle",
-                               "sample": f"{args.cpu_rows} seeded target rows x all {n} sources "
-                                         f"(oracle.elastic.matvec_rows, numpy fp64, {gdt:.1f} s)"}
+        gv, gdt, gw = cpu_baseline_oracle(g, c["material"], Dv_host, args.cpu_rows)
+        out["cpu_baseline"] = {"value": gv, "unit": UNIT, "cores": gw, "kind": "oracle",
+                               "sample": f"{args.cpu_rows} seeded target rows x all {n} sources, "
+                                         f"split over {gw} processes (oracle.elastic.matvec_rows, "
+                                         f"numpy fp64, {gdt:.1f} s)",
+                               "host": _host_info(),
+                               "gmres_cfg2": oracle_gmres_cfg2()}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+HBM_PEAK_FALLBACK = 6530.0   # GB/s, MEASURED_PEAKS.json on this pool
+
+
+def _hbm_peak() -> tuple:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy)"
+    except Exception:
+        return HBM_PEAK_FALLBACK, "fallback 6530 GB/s (MEASURED_PEAKS.json of this pool, round 1)"
+
+
+def kernel_rooflines(tree, cnt, stages, tree_stages, p, fp64_peak, world):
+    """Roofline fraction of every stage of the step (serial instrumented
+    matvecs, CUDA events on the launching stream) and of the tree build
+    stages, in SURVEY.md §8(d).2 work units (DESIGN.md §7.1 states each unit
+    and where the implementation executes a different amount of work):
+      fp64 stages: algorithmic flop / time / measured fp64 peak (DFMA probe);
+      HBM stages : algorithmic bytes / time / measured HBM copy bandwidth."""
+    n = cnt["N"]
+    lev = tree.export("LEVEL")
+    leaves = tree.export("LEAVES")
+    count = tree.export("COUNT")
+    woff = tree.export("W_OFF")
+    n_l3 = int((lev >= 3).sum())                 # cells with a parent of level >= 2
+    el_w = int((count[leaves] * np.diff(woff)).sum())   # (element, W cell) pairs
+    T = 12800                                      # flop per translation: dense 80 x 80 real operator
+    hbm, hbm_src = _hbm_peak()
+    depth = cnt["LEVELS"] - 1
+    sort_passes = max(1, -(-2 * depth // 8))
+    rows = {
+        "prep": ("hbm", 165.0 * n, "B", "165 B/elem: D (16, gathered through perm), geometry "
+                 "(40), stream tables (13) in; 80-B near-field record and D sorted (16) out"),
+        "p2m": ("fp64", 40.0 * p * n, "flop", "SURVEY 40 p flop/elem (exact segment moments)"),
+        "m2m": ("fp64", float(T) * n_l3, "flop", "SURVEY 12 800 flop per child translation "
+                "(executed: separable Pascal form, about half)"),
+        "m2l": ("fp64", float(T) * cnt["V"], "flop", "SURVEY 12 800 flop per V pair (executed on "
+                "DMMA: 9 x DMMA.8x8x4 = 4 608 flop per pair, Pascal form)"),
+        "l2l": ("fp64", float(T) * n_l3, "flop", "SURVEY 12 800 flop per parent-to-child "
+                "translation"),
+        "l2p": ("fp64", (24.0 * p + 20) * n + (24.0 * p + 30) * el_w, "flop",
+                f"(24 p + 20) flop/elem local + (24 p + 30) per (element, W cell) M2P pair "
+                f"({el_w} pairs)"),
+        "p2p": ("fp64", FLOP_PER_PAIR * cnt["NEAR_PAIRS"] / world, "flop",
+                "45 flop per near pair (node-sharing record update as written)"),
+        "final": ("hbm", 52.0 * n, "B", "52 B/elem: near (16) + far (16) + perm (4) in, y (16) out"),
+    }
+    out = {}
+    for k, (bound, work, unit, note) in rows.items():
+        ms = stages.get(k, 0.0)
+        if ms <= 0:
+            continue
+        if bound == "fp64":
+            ach = work / (ms * 1e-3) / 1e12
+            out[k] = {"bound": "alu", "unit": "TFLOP/s", "achieved": ach, "peak": fp64_peak,
+                      "frac": ach / fp64_peak if fp64_peak else None, "kernel_ms": ms,
+                      "work": work, "work_unit": unit, "note": note}
+        else:
+            ach = work / (ms * 1e-3) / 1e9
+            out[k] = {"bound": "hbm", "unit": "GB/s", "achieved": ach, "peak": hbm,
+                      "frac": ach / hbm, "kernel_ms": ms, "work": work, "work_unit": unit,
+                      "note": note}
+    m2l_exec = 4608.0 * cnt["V"] / (stages["m2l"] * 1e-3) / 1e12 if stages.get("m2l") else None
+    if m2l_exec and "m2l" in out:
+        out["m2l"]["executed_dmma_tflops"] = m2l_exec
+        out["m2l"]["executed_dmma_frac"] = m2l_exec / fp64_peak if fp64_peak else None
+    tb = {
+        "keys": (28.0 * n, "SURVEY 28 B/elem (centres in, key + index out)"),
+        "sort": ((24.0 * sort_passes + 8.0) * n, f"SURVEY {sort_passes} passes x 24 B/elem + 8 "
+                 "B/elem histogram (executed: 8 passes of 8-bit digits over the 60-bit key, "
+                 "for the bit-exact full-key order)"),
+        "cells": (24.0 * n * depth, "24 B/elem per level"),
+        "lists": (48.0 * cnt["CELLS"] + 4.0 * (cnt["V"] + 2 * cnt["URANGES"] + cnt["W"]),
+                  "48 B/cell + 4 B per V, U-range bound and W entry"),
+    }
+    tree_out = {}
+    for k, (byt, note) in tb.items():
+        ms = tree_stages.get(k, 0.0)
+        if ms > 0:
+            ach = byt / (ms * 1e-3) / 1e9
+            tree_out[k] = {"bound": "hbm", "unit": "GB/s", "achieved": ach, "peak": hbm,
+                           "frac": ach / hbm, "kernel_ms": ms, "work": byt, "work_unit": "B",
+                           "note": note + " (stage span incl. host gaps)"}
+    return {"step": out, "tree_build": tree_out, "fp64_peak_source":
+            "measured DFMA-chain probe (ddm_probe_fp64) on this GPU", "hbm_peak_source": hbm_src,
+            "time_source": "CUDA events around each stage's kernels, serial schedule, after the "
+                           "timed region (profiles/r2_kernel_ncu_summary.txt has the ncu rows)"}
 
 
 def _ncu_traffic(kernel: str):
@@ -522,8 +675,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--p", type=int, default=0)
-    ap.add_argument("--cpu-rows", type=int, default=64)
-    ap.add_argument("--ref-rows", type=int, default=16)
+    ap.add_argument("--cpu-rows", type=int, default=256)
+    ap.add_argument("--ref-rows", type=int, default=64)
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--march-steps", type=int, default=200)
     args = ap.parse_args()

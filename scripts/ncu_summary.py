@@ -16,6 +16,9 @@ METRICS = [
     "dram__bytes_read.sum",
     "dram__bytes_write.sum",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "smsp__inst_executed_pipe_fp64.sum",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.sum",
     "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "smsp__inst_executed.sum",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
