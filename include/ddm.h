@@ -114,6 +114,19 @@ enum {
 };
 int ddm_tree_counts(ddm_tree_t tree, int64_t* counts);
 
+/* Multi-rank matvec emulated on ONE device (tests of the sharded path,
+ * DESIGN.md §6): trees[r] [host array of handles] is one geometry built on
+ * this context and partitioned (ddm_tree_partition) as rank r of `world`.
+ * Runs the elastic FMM matvec exactly as `world` ranks would (each rank's
+ * near field, P2M of its leaves and M2M of its complete cells, the multipole
+ * all-gather, the straddling cells' M2M, the downward pass and assembly of
+ * its owned rows), rank by rank on `stream`, with device copies in place of
+ * the NCCL all-gathers.  D, y: device [n][2], user order.  Elastic only
+ * (DDM_ERR_ARG otherwise).  The result equals ddm_matvec on the unpartitioned
+ * tree bitwise: every row is summed in the same order. */
+int ddm_matvec_sim(ddm_ctx_t ctx, const ddm_tree_t* trees, int world, const ddm_material* mat,
+                   const double* D, double* y, void* stream);
+
 /* Timing of the last ddm_build_tree of `tree` (keys, sort, cells,
  * interaction lists; built once per geometry), written into
  * ms[DDM_TB_N] [host], milliseconds: stage spans from CUDA events on the build
@@ -149,6 +162,16 @@ int ddm_tree_export(ddm_tree_t tree, int what, void* dst, int64_t capacity_bytes
  * near-equal estimated cost (P2P pairs + M2L work) and keep rank's range.
  * Called automatically by ddm_build_tree with the context's rank/world. */
 int ddm_tree_partition(ddm_tree_t tree, int rank, int world);
+
+/* Host-only helper (no GPU needed) of the sharded upward pass:
+ * owner[c] = the rank r whose sorted-element range [rank_el_lo[r],
+ * rank_el_lo[r+1]) contains cell c's whole range [c_start[c], c_start[c] +
+ * c_count[c]) (a COMPLETE cell: r computes its multipole from its own
+ * elements), or -1 for a straddling cell (its range crosses a rank boundary;
+ * completed on every rank from its children after the multipole
+ * all-gather).  All arrays host memory; rank_el_lo has world+1 entries. */
+int ddm_shard_owner(const int* c_start, const int* c_count, int ncells,
+                    const int64_t* rank_el_lo, int world, int* owner);
 
 /* Host-only helper (no GPU needed): split leaves with exclusive cost prefix
  * prefix_excl[nleaves] (total = sum of costs) into `world` contiguous ranges:

@@ -18,9 +18,11 @@ from .api import (  # noqa: F401
     material,
     material_from_dict,
     matvec,
+    matvec_sim,
     nccl_unique_id,
     precond_apply,
     sif,
+    shard_owner,
     split_costs,
     tip_growth,
 )

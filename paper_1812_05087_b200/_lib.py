@@ -68,6 +68,10 @@ ddm_tree_export = _proto("ddm_tree_export", _i, _vp, _i, _vp, _i64)
 ddm_tree_partition = _proto("ddm_tree_partition", _i, _vp, _i, _i)
 ddm_split_costs = _proto("ddm_split_costs", _i, C.POINTER(_i64), _i64, _i, _i, C.POINTER(_i))
 ddm_matvec = _proto("ddm_matvec", _i, _vp, _vp, C.POINTER(Material), _d, _dp, _dp, _i, _vp)
+ddm_shard_owner = _proto("ddm_shard_owner", _i, C.POINTER(_i), C.POINTER(_i), _i, C.POINTER(_i64), _i,
+                          C.POINTER(_i))
+ddm_matvec_sim = _proto("ddm_matvec_sim", _i, _vp, C.POINTER(_vp), _i, C.POINTER(Material), _dp,
+                        _dp, _vp)
 ddm_history_apply = _proto("ddm_history_apply", _i, _vp, _vp, C.POINTER(Material), _d, _i, _dp,
                            _dp, _i, _vp)
 ddm_history_rhs = _proto("ddm_history_rhs", _i, _vp, _vp, C.POINTER(Material), _d, _i, _dp, _dp,
@@ -86,7 +90,7 @@ ddm_stage_times = _proto("ddm_stage_times", _i, _vp, C.POINTER(_d))
 
 EXPORTED = ["ddm_version", "ddm_last_error", "ddm_nccl_unique_id", "ddm_ctx_create",
             "ddm_ctx_destroy", "ddm_build_tree", "ddm_tree_free", "ddm_tree_counts",
-            "ddm_tree_export", "ddm_tree_partition", "ddm_split_costs", "ddm_matvec",
+            "ddm_tree_export", "ddm_tree_partition", "ddm_split_costs", "ddm_matvec", "ddm_matvec_sim", "ddm_shard_owner",
             "ddm_history_apply", "ddm_history_rhs", "ddm_gmres_solve", "ddm_precond_apply",
             "ddm_farfield_rhs", "ddm_sif", "ddm_tip_growth",
             "ddm_set_profiling", "ddm_stage_times", "ddm_tree_build_times"]

@@ -182,6 +182,18 @@ def matvec(ctx: Context, tree: Tree, mat, D: torch.Tensor, y: torch.Tensor | Non
     return y
 
 
+def matvec_sim(ctx: Context, trees, mat, D: torch.Tensor, y: torch.Tensor | None = None,
+               stream=None) -> torch.Tensor:
+    """ddm_matvec_sim: the sharded multi-rank elastic FMM matvec emulated on one
+    device; trees[r] is the geometry partitioned as rank r of len(trees)."""
+    if y is None:
+        y = torch.empty_like(D)
+    arr = (C.c_void_p * len(trees))(*[t._h.value for t in trees])
+    ctx.check(L.ddm_matvec_sim(ctx._h, arr, len(trees), C.byref(mat), _dev(D, "D"), _dev(y, "y"),
+                               _stream_ptr(stream)))
+    return y
+
+
 def history_apply(ctx, tree, mat, dt: float, D_hist: torch.Tensor, r: torch.Tensor | None = None,
                   mode="fmm", stream=None) -> torch.Tensor:
     """ddm_history_apply: r = sum_{m=1}^{h} A^(m) D^(h-m); D_hist [h, n, 3].
@@ -288,6 +300,21 @@ def tip_growth(ctx, KI: torch.Tensor, KII: torch.Tensor, x: torch.Tensor, y: tor
                                _dev(na, "na"), _dev(nb, "nb"), _dev(ne, "ne", torch.int32),
                                _stream_ptr(stream)))
     return grow, nx, ny, na, nb, ne
+
+
+def shard_owner(c_start: np.ndarray, c_count: np.ndarray, rank_el_lo: np.ndarray) -> np.ndarray:
+    """Host-only ddm_shard_owner: the rank on which each cell is complete, or -1
+    (straddling cell)."""
+    st = np.ascontiguousarray(c_start, dtype=np.int32)
+    ct = np.ascontiguousarray(c_count, dtype=np.int32)
+    lo = np.ascontiguousarray(rank_el_lo, dtype=np.int64)
+    out = np.empty(st.size, dtype=np.int32)
+    rc = L.ddm_shard_owner(st.ctypes.data_as(C.POINTER(C.c_int)), ct.ctypes.data_as(C.POINTER(C.c_int)),
+                           int(st.size), lo.ctypes.data_as(C.POINTER(C.c_int64)), int(lo.size - 1),
+                           out.ctypes.data_as(C.POINTER(C.c_int)))
+    if rc != L.OK:
+        raise DDMError(rc, "ddm_shard_owner")
+    return out
 
 
 def split_costs(prefix_excl: np.ndarray, total: int, world: int) -> np.ndarray:

@@ -135,38 +135,52 @@ int check_material(ddm_ctx_s* ctx, const ddm_material* m) {
 }  // namespace
 
 // all-gather of the owned sorted rows y_sorted[lo..hi) into the full vector
+// (persistent buffers from the partition: no allocation per call)
 int allgather_sorted(ddm_ctx_s* ctx, ddm_tree_s* t, double* buf, int ncomp, cudaStream_t s) {
   if (!ctx->exchange) return DDM_OK;
 #ifdef DDM_WITH_NCCL
-  int64_t maxrows = 0;
-  for (int r = 0; r < ctx->world; ++r)
-    maxrows = std::max(maxrows, t->rank_el_lo[r + 1] - t->rank_el_lo[r]);
-  double* send = nullptr;
-  double* recv = nullptr;
-  int64_t* dlo = nullptr;
+  if (!t->ag_send) return set_error(ctx, DDM_ERR_ARG, "tree not partitioned for the exchange");
+  const int64_t maxrows = t->ag_max;
   const size_t cnt = (size_t)maxrows * ncomp;
-  DDM_CUDA(ctx, cudaMallocAsync((void**)&send, std::max<size_t>(cnt, 1) * sizeof(double), s));
-  DDM_CUDA(ctx, cudaMallocAsync((void**)&recv, std::max<size_t>(cnt * ctx->world, 1) * sizeof(double), s));
-  DDM_CUDA(ctx, cudaMallocAsync((void**)&dlo, (ctx->world + 1) * sizeof(int64_t), s));
-  DDM_CUDA(ctx, cudaMemcpyAsync(dlo, t->rank_el_lo.data(), (ctx->world + 1) * sizeof(int64_t),
-                                cudaMemcpyHostToDevice, s));
   const int64_t lo = t->own_el_lo, hi = t->own_el_hi;
-  DDM_CUDA(ctx, cudaMemcpyAsync(send, buf + lo * ncomp, (hi - lo) * ncomp * sizeof(double),
-                                cudaMemcpyDeviceToDevice, s));
-  ncclResult_t nr = ncclAllGather(send, recv, cnt, ncclDouble, ctx->comm, s);
+  if (hi > lo)
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->ag_send, buf + lo * ncomp, (hi - lo) * ncomp * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, s));
+  ncclResult_t nr = ncclAllGather(t->ag_send, t->ag_recv, cnt, ncclDouble, ctx->comm, s);
   if (nr != ncclSuccess)
     return set_error(ctx, DDM_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
   dim3 grid(std::max(1u, nblk(maxrows * ncomp, 256)), ctx->world);
-  unpack_allgather<<<grid, 256, 0, s>>>(recv, dlo, ctx->world, maxrows, ncomp, buf);
+  unpack_allgather<<<grid, 256, 0, s>>>(t->ag_recv, t->ag_lo, ctx->world, maxrows, ncomp, buf);
   DDM_CUDA(ctx, cudaGetLastError());
-  cudaFreeAsync(send, s);
-  cudaFreeAsync(recv, s);
-  cudaFreeAsync(dlo, s);
   return DDM_OK;
 #else
   (void)t; (void)buf; (void)ncomp; (void)s;
   return set_error(ctx, DDM_ERR_NCCL, "libddm built without NCCL");
 #endif
+}
+
+// all-gather of the packed multipoles of every rank's complete cells (the
+// sharded upward pass), padded to xr_max cells per rank
+int allgather_mpole(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
+#ifdef DDM_WITH_NCCL
+  const size_t cnt = (size_t)t->xr_max * 2 * t->p * 2;   // doubles
+  if (cnt == 0) return DDM_OK;
+  ncclResult_t nr = ncclAllGather(t->xsend, t->xrecv, cnt, ncclDouble, ctx->comm, s);
+  if (nr != ncclSuccess)
+    return set_error(ctx, DDM_ERR_NCCL, std::string("ncclAllGather (multipoles): ") +
+                                            ncclGetErrorString(nr));
+  return DDM_OK;
+#else
+  (void)t; (void)s;
+  return set_error(ctx, DDM_ERR_NCCL, "libddm built without NCCL");
+#endif
+}
+
+int launch_scatter_user(ddm_ctx_s* ctx, ddm_tree_s* t, const double* ys, int ncomp, double* y,
+                        cudaStream_t s) {
+  scatter_user<<<nblk(t->n, 256), 256, 0, s>>>(t->n, ncomp, t->perm, ys, y);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
 }
 
 int allreduce_sum(ddm_ctx_s* ctx, double* buf, int64_t count, cudaStream_t s) {
@@ -187,6 +201,26 @@ int allreduce_sum(ddm_ctx_s* ctx, double* buf, int64_t count, cudaStream_t s) {
 // chunks) is dropped when the partition changes; it is rebuilt on demand.
 static void drop_owned_state(ddm_tree_s* t) {
   drop_graphs(t);
+  {
+    void* sh[] = {t->xr_cells, t->xr_off_dev, t->up_own, t->up_strad, t->xsend, t->xrecv,
+                  t->ag_send, t->ag_recv, t->ag_lo, t->halo_rng, t->halo_pre, t->dn_own};
+    t->dn_own = nullptr;
+    t->halo_rng = nullptr;
+    t->halo_pre = nullptr;
+    t->nhalo = 0;
+    t->halo_slots = 0;
+    for (void* p : sh)
+      if (p) cudaFree(p);
+    t->xr_cells = nullptr;
+    t->xr_off_dev = nullptr;
+    t->up_own = t->up_strad = nullptr;
+    t->xsend = t->xrecv = nullptr;
+    t->ag_send = t->ag_recv = nullptr;
+    t->ag_lo = nullptr;
+    t->xr_max = 0;
+    t->ag_max = 0;
+    t->shard_up = false;
+  }
   for (double* p : t->hc_alloc) cudaFree(p);
   t->hc_alloc.clear();
   t->hc_lag.clear();
@@ -206,8 +240,162 @@ static void drop_owned_state(ddm_tree_s* t) {
   std::memset(t->pcl_key, 0, sizeof(t->pcl_key));
 }
 
+void shard_owner(const int* c_start, const int* c_count, int ncells, const int64_t* lo, int world,
+                 int* owner) {
+  for (int c = 0; c < ncells; ++c) {
+    const int64_t a = c_start[c], b = a + c_count[c];
+    // the rank whose range contains the cell's first element
+    const int r = (int)(std::upper_bound(lo, lo + world + 1, a) - lo) - 1;
+    owner[c] = (r >= 0 && r < world && a >= lo[r] && b <= lo[r + 1]) ? r : -1;
+  }
+}
+
+// Sharded upward pass metadata and the persistent exchange
+// buffers: per rank the cells whose element range lies inside its range
+// (complete cells), this rank's complete non-leaf cells and the straddling
+// non-leaf cells as per-level M2M lists (deepest level first).
+static int shard_metadata(ddm_tree_s* t, int rank, int world, const std::vector<int>& h_start,
+                          cudaStream_t s) {
+  ddm_ctx_s* ctx = t->ctx;
+  const int nc = t->ncells;
+  std::vector<int> h_count(nc);
+  DDM_CUDA(ctx, cudaMemcpyAsync(h_count.data(), t->c_count, nc * sizeof(int),
+                                cudaMemcpyDeviceToHost, s));
+  DDM_CUDA(ctx, cudaStreamSynchronize(s));
+  const std::vector<int64_t>& lo = t->rank_el_lo;
+  std::vector<int> owner(nc, -1);
+  shard_owner(h_start.data(), h_count.data(), nc, lo.data(), world, owner.data());
+  std::vector<std::vector<int>> per(world);
+  for (int c = 0; c < nc; ++c)
+    if (owner[c] >= 0) per[owner[c]].push_back(c);
+  std::vector<int> cells;
+  t->xr_off.assign(world + 1, 0);
+  t->xr_max = 0;
+  for (int r = 0; r < world; ++r) {
+    t->xr_off[r] = (int)cells.size();
+    cells.insert(cells.end(), per[r].begin(), per[r].end());
+    t->xr_max = std::max(t->xr_max, (int)per[r].size());
+  }
+  t->xr_off[world] = (int)cells.size();
+  std::vector<int> own, strad;
+  t->up_own_off.assign(2 * (t->nlevels + 1), 0);
+  t->up_strad_off.assign(2 * (t->nlevels + 1), 0);
+  for (int lev = t->nlevels - 1; lev >= 2; --lev) {
+    t->up_own_off[2 * lev] = (int)own.size();
+    t->up_strad_off[2 * lev] = (int)strad.size();
+    for (int k = t->up_level_off[2 * lev]; k < t->up_level_off[2 * lev + 1]; ++k) {
+      const int c = t->h_up[k];
+      if (owner[c] == rank) own.push_back(c);
+      else if (owner[c] < 0) strad.push_back(c);
+    }
+    t->up_own_off[2 * lev + 1] = (int)own.size();
+    t->up_strad_off[2 * lev + 1] = (int)strad.size();
+  }
+  t->shard_up = world > 1;
+  int rc0;
+  // downward-pass cell list of this rank (cells whose range meets the owned range)
+  std::vector<int> dn;
+  t->dn_own_off.assign(t->nlevels + 1, 0);
+  for (int lev = 0; lev < t->nlevels; ++lev) {
+    t->dn_own_off[lev] = (int)dn.size();
+    if (lev < 2) continue;
+    for (int c = t->level_off[lev]; c < t->level_off[lev + 1]; ++c)
+      if ((int64_t)h_start[c] < t->own_el_hi && (int64_t)h_start[c] + h_count[c] > t->own_el_lo)
+        dn.push_back(c);
+  }
+  t->dn_own_off[t->nlevels] = (int)dn.size();
+  if (world > 1) {
+    if ((rc0 = dalloc(ctx, &t->dn_own, dn.size()))) return rc0;
+    if (!dn.empty())
+      DDM_CUDA(ctx, cudaMemcpyAsync(t->dn_own, dn.data(), dn.size() * sizeof(int),
+                                    cudaMemcpyHostToDevice, s));
+  }
+  // near-field halo: the slots of the owned leaves' U ranges, plus the slot
+  // before them (its record carries the node of a linked first record)
+  t->halo_lo = 0;
+  t->halo_hi = t->n;
+  if (world > 1) {
+    const int l0 = t->own_leaf_lo, l1 = t->own_leaf_hi;
+    if (l1 > l0) {
+      std::vector<int> uoff(l1 - l0 + 1);
+      DDM_CUDA(ctx, cudaMemcpyAsync(uoff.data(), t->u_off + l0, uoff.size() * sizeof(int),
+                                    cudaMemcpyDeviceToHost, s));
+      DDM_CUDA(ctx, cudaStreamSynchronize(s));
+      const int r0 = uoff.front(), r1 = uoff.back();
+      std::vector<int> ulo(std::max(r1 - r0, 1)), uhi(std::max(r1 - r0, 1));
+      if (r1 > r0) {
+        DDM_CUDA(ctx, cudaMemcpyAsync(ulo.data(), t->u_lo + r0, (r1 - r0) * sizeof(int),
+                                      cudaMemcpyDeviceToHost, s));
+        DDM_CUDA(ctx, cudaMemcpyAsync(uhi.data(), t->u_hi + r0, (r1 - r0) * sizeof(int),
+                                      cudaMemcpyDeviceToHost, s));
+        DDM_CUDA(ctx, cudaStreamSynchronize(s));
+        int64_t a = t->n, b = 0;
+        std::vector<std::pair<int, int>> iv(r1 - r0);
+        for (int k = 0; k < r1 - r0; ++k) {
+          a = std::min<int64_t>(a, ulo[k]);
+          b = std::max<int64_t>(b, uhi[k]);
+          iv[k] = {std::max(0, ulo[k] - 1), uhi[k]};
+        }
+        t->halo_lo = std::max<int64_t>(0, a - 1);
+        t->halo_hi = b;
+        std::sort(iv.begin(), iv.end());
+        std::vector<int2> mr;
+        for (const auto& v : iv) {
+          if (!mr.empty() && v.first <= mr.back().y) mr.back().y = std::max(mr.back().y, v.second);
+          else mr.push_back(make_int2(v.first, v.second));
+        }
+        std::vector<int64_t> pre(mr.size() + 1, 0);
+        for (size_t k = 0; k < mr.size(); ++k) pre[k + 1] = pre[k] + (mr[k].y - mr[k].x);
+        t->nhalo = (int)mr.size();
+        t->halo_slots = pre.back();
+        if ((rc0 = dalloc(ctx, &t->halo_rng, mr.size())) || (rc0 = dalloc(ctx, &t->halo_pre, pre.size())))
+          return rc0;
+        DDM_CUDA(ctx, cudaMemcpyAsync(t->halo_rng, mr.data(), mr.size() * sizeof(int2),
+                                      cudaMemcpyHostToDevice, s));
+        DDM_CUDA(ctx, cudaMemcpyAsync(t->halo_pre, pre.data(), pre.size() * sizeof(int64_t),
+                                      cudaMemcpyHostToDevice, s));
+      }
+    } else {
+      t->halo_lo = t->halo_hi = 0;
+    }
+  }
+  int rc;
+  const size_t P2 = 2 * (size_t)t->p;
+  if ((rc = dalloc(ctx, &t->xr_cells, cells.size())) || (rc = dalloc(ctx, &t->xr_off_dev, world + 1)) ||
+      (rc = dalloc(ctx, &t->up_own, own.size())) || (rc = dalloc(ctx, &t->up_strad, strad.size())))
+    return rc;
+  if (world > 1 && ((rc = dalloc(ctx, &t->xsend, (size_t)std::max(t->xr_max, 1) * P2)) ||
+                    (rc = dalloc(ctx, &t->xrecv, (size_t)std::max(t->xr_max, 1) * P2 * world))))
+    return rc;
+  if (!cells.empty())
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->xr_cells, cells.data(), cells.size() * sizeof(int),
+                                  cudaMemcpyHostToDevice, s));
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->xr_off_dev, t->xr_off.data(), (world + 1) * sizeof(int),
+                                cudaMemcpyHostToDevice, s));
+  if (!own.empty())
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->up_own, own.data(), own.size() * sizeof(int),
+                                  cudaMemcpyHostToDevice, s));
+  if (!strad.empty())
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->up_strad, strad.data(), strad.size() * sizeof(int),
+                                  cudaMemcpyHostToDevice, s));
+  // all-gather buffers of the owned output rows (<= 3 components)
+  t->ag_max = 0;
+  for (int r = 0; r < world; ++r) t->ag_max = std::max(t->ag_max, lo[r + 1] - lo[r]);
+  if (world > 1 || ctx->exchange) {
+  if ((rc = dalloc(ctx, &t->ag_send, (size_t)std::max<int64_t>(t->ag_max, 1) * 3)) ||
+      (rc = dalloc(ctx, &t->ag_recv, (size_t)std::max<int64_t>(t->ag_max, 1) * 3 * world)) ||
+      (rc = dalloc(ctx, &t->ag_lo, world + 1)))
+    return rc;
+  DDM_CUDA(ctx, cudaMemcpyAsync(t->ag_lo, lo.data(), (world + 1) * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, s));
+  }
+  DDM_CUDA(ctx, cudaStreamSynchronize(s));
+  return DDM_OK;
+}
+
 int partition_tree(ddm_tree_s* t, int rank, int world, cudaStream_t s) {
   ddm_ctx_s* ctx = t->ctx;
+  int rc0;
   if (world < 1 || rank < 0 || rank >= world)
     return set_error(ctx, DDM_ERR_ARG, "bad rank/world");
   DDM_CUDA(ctx, cudaStreamSynchronize(s));
@@ -235,6 +423,7 @@ int partition_tree(ddm_tree_s* t, int rank, int world, cudaStream_t s) {
   t->own_el_hi = t->rank_el_lo[rank + 1];
   t->item_lo_owned = h_ioff[split[rank]];
   t->item_hi_owned = h_ioff[split[rank + 1]];
+  if ((rc0 = shard_metadata(t, rank, world, h_start, s))) return rc0;
   // execution order of the owned P2P items: Morton order (consecutive warps
   // share source records in L2; measured: a longest-first order doubled the
   // DRAM traffic of p2p_kernel for no time gain -- items are capped at
@@ -508,6 +697,24 @@ int ddm_tree_export(ddm_tree_t t, int what, void* dst, int64_t cap) {
   if ((int64_t)bytes > cap) return set_error(ctx, DDM_ERR_ARG, "capacity too small");
   if (bytes) DDM_CUDA(ctx, cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
   return DDM_OK;
+}
+
+int ddm_shard_owner(const int* c_start, const int* c_count, int ncells, const int64_t* rank_el_lo,
+                    int world, int* owner) {
+  if (!c_start || !c_count || !rank_el_lo || !owner || ncells < 0 || world < 1) return DDM_ERR_ARG;
+  shard_owner(c_start, c_count, ncells, rank_el_lo, world, owner);
+  return DDM_OK;
+}
+
+int ddm_matvec_sim(ddm_ctx_t ctx, const ddm_tree_t* trees, int world, const ddm_material* mat,
+                   const double* D, double* y, void* stream) {
+  if (!ctx || !trees || !D || !y || world < 1)
+    return ctx ? set_error(ctx, DDM_ERR_ARG, "NULL argument") : DDM_ERR_ARG;
+  int rc = check_material(ctx, mat);
+  if (rc) return rc;
+  for (int r = 0; r < world; ++r)
+    if (!trees[r]) return set_error(ctx, DDM_ERR_ARG, "NULL tree");
+  return fmm_matvec_sim(ctx, trees, world, mat, D, y, (cudaStream_t)stream);
 }
 
 int ddm_matvec(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double elapsed,

@@ -164,6 +164,36 @@ struct ddm_tree_s {
   int* up_list = nullptr;         // non-leaf cells of level >= 2, deepest level first
   int n_up = 0;
   std::vector<int> up_level_off;  // [2 (nlevels+1)]: level l = up_list[off[2l], off[2l+1])
+  std::vector<int> h_up;          // host copy of up_list
+  // sharded upward pass (several ranks): a cell is COMPLETE on
+  // rank r when its element range lies inside r's range; r computes P2M of
+  // its leaves and M2M of its complete cells, the packed multipoles of every
+  // rank's complete cells are all-gathered, and the STRADDLING cells (ranges
+  // across a rank boundary: ancestors of the boundaries) are completed on
+  // every rank by M2M from the gathered children.
+  bool shard_up = false;          // partition has several ranks
+  int64_t halo_lo = 0, halo_hi = 0;   // hull of the stream slots the owned leaves read
+  int2* halo_rng = nullptr;           // those slots as merged ranges [a, b) (sharded prep)
+  int64_t* halo_pre = nullptr;        // [nhalo + 1] exclusive prefix of the range lengths
+  int nhalo = 0;
+  int64_t halo_slots = 0;
+  int* xr_cells = nullptr;        // complete cells of every rank, rank-major, ascending
+  std::vector<int> xr_off;        // [world+1]
+  int* xr_off_dev = nullptr;      // device copy of xr_off
+  int xr_max = 0;                 // max complete cells of one rank
+  int* up_own = nullptr;          // this rank's complete non-leaf cells (level >= 2), deepest level first
+  std::vector<int> up_own_off;    // [2 (nlevels+1)] as up_level_off
+  int* dn_own = nullptr;          // cells of level >= 2 holding owned targets (ascending = level-major)
+  std::vector<int> dn_own_off;    // [nlevels+1] first entry of each level (M2L / L2L lists)
+  int* up_strad = nullptr;        // straddling non-leaf cells (level >= 2), deepest level first
+  std::vector<int> up_strad_off;
+  double2* xsend = nullptr;       // [xr_max][2p] packed multipoles of this rank
+  double2* xrecv = nullptr;       // [world][xr_max][2p] gathered
+  // persistent buffers of the all-gather of the owned output rows
+  double* ag_send = nullptr;
+  double* ag_recv = nullptr;
+  int64_t* ag_lo = nullptr;       // device copy of rank_el_lo
+  int64_t ag_max = 0;             // max owned rows of one rank
 
   // FMM operators (device, fmm.cu fmm_init_operators): every translation is
   // pre-scale (complex powers) x real Pascal matrix x post-scale
@@ -315,6 +345,8 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
                cudaStream_t s, ddm_tree_s* t);
 void free_tree(ddm_tree_s* t);
 int partition_tree(ddm_tree_s* t, int rank, int world, cudaStream_t s);
+void shard_owner(const int* c_start, const int* c_count, int ncells, const int64_t* lo, int world,
+                 int* owner);
 void split_costs(const int64_t* prefix_excl, int64_t total, int nleaves, int world, int* split);
 
 // fmm.cu
@@ -332,6 +364,12 @@ int fmm_workspace(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
 int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double elapsed,
                const double* D, bool d_sorted, double* y_user, double* y_sorted, int mode,
                cudaStream_t s);
+
+// several ranks emulated on one device (fmm.cu; tests)
+int fmm_matvec_sim(ddm_ctx_s* ctx, ddm_tree_s* const* trees, int world, const ddm_material* mat,
+                   const double* D, double* y, cudaStream_t s);
+int launch_scatter_user(ddm_ctx_s* ctx, ddm_tree_s* t, const double* ys, int ncomp, double* y,
+                        cudaStream_t s);
 
 // fast history sum (poroelastic): r = sum_{m=1}^{h} A^(m) D^(h-m), D_hist user order
 int fmm_history(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double dt, int h,
@@ -353,6 +391,7 @@ int precond_apply_user(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, d
 
 // comm (api.cu)
 int allgather_sorted(ddm_ctx_s* ctx, ddm_tree_s* t, double* buf, int ncomp, cudaStream_t s);
+int allgather_mpole(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
 int allreduce_sum(ddm_ctx_s* ctx, double* buf, int64_t count, cudaStream_t s);
 
 // profiling helpers

@@ -533,7 +533,8 @@ __device__ void m2l_cell_dfma(int p, int vb, int ve, const int* __restrict__ v_i
 #endif
 template <int PT>
 __global__ void __launch_bounds__(kPassWarps * 32, DDM_M2L_MINB)
-m2l_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restrict__ v_off,
+m2l_kernel(int c0, int c1, const int* __restrict__ clist, int64_t own_lo, int64_t own_hi,
+           const int* __restrict__ v_off,
            const int* __restrict__ v_idx, const unsigned char* __restrict__ v_cls,
            const int* __restrict__ c_start, const int* __restrict__ c_count, int p_rt,
            const double2* __restrict__ w_g, const double* __restrict__ pm2l_g,
@@ -568,7 +569,8 @@ m2l_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restrict
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t wstride = TC ? (size_t)2 * kM2LBatch * kXStride : 3 * (size_t)p + 1;
   double2* ring = wbuf + (size_t)w * wstride;
-  for (int c = c0 + blockIdx.x * kPassWarps + w; c < c1; c += gridDim.x * kPassWarps) {
+  for (int k = c0 + blockIdx.x * kPassWarps + w; k < c1; k += gridDim.x * kPassWarps) {
+    const int c = clist ? clist[k] : k;   // clist: this rank's cells (several ranks)
     const int cs = c_start[c], ce = cs + c_count[c];
     if (ce <= own_lo || cs >= own_hi) continue;   // subtree outside this rank's targets
     double2* out = local + (size_t)c * 2 * p;
@@ -660,7 +662,8 @@ __device__ __forceinline__ void l2l_cell(int c, int p, const int* __restrict__ c
 
 template <int PT>
 __global__ void __launch_bounds__(kPassWarps * 32)
-l2l_level_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __restrict__ c_ix,
+l2l_level_kernel(int c0, int c1, const int* __restrict__ clist, int64_t own_lo, int64_t own_hi,
+                 const int* __restrict__ c_ix,
                  const int* __restrict__ c_iy, const int* __restrict__ c_start,
                  const int* __restrict__ c_count, const int* __restrict__ c_parent, int p_rt,
                  const double2* __restrict__ eps_g, const double2* __restrict__ e2i_g,
@@ -672,7 +675,8 @@ l2l_level_kernel(int c0, int c1, int64_t own_lo, int64_t own_hi, const int* __re
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* xl = l2_sh + (size_t)w * 2 * p;
   double2* xg = xl + p;
-  for (int c = c0 + blockIdx.x * kPassWarps + w; c < c1; c += gridDim.x * kPassWarps) {
+  for (int k = c0 + blockIdx.x * kPassWarps + w; k < c1; k += gridDim.x * kPassWarps) {
+    const int c = clist ? clist[k] : k;
     const int cs = c_start[c], ce = cs + c_count[c];
     if (ce <= own_lo || cs >= own_hi) continue;   // no owned target below c
     l2l_cell<PT>(c, p, c_ix, c_iy, c_parent, eps_g, e2i_g, pas_g, local, xl, xg, lane);
@@ -1150,28 +1154,36 @@ cudaError_t launch_pdl(bool on, void (*kernel)(KArgs...), unsigned grid, unsigne
 // upward pass: P2M on all leaves, then M2M one level at a time (deepest
 // first), replicated on every rank
 int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
-                  const PoroFar& pf, cudaStream_t s) {
+                  const PoroFar& pf, cudaStream_t s, int scope) {
   // D in user order (perm_in = sorted -> user, read through it) or sorted (nullptr)
   const int p = t->p;
+  const bool do_p2m = scope != kUpStrad;
+  const int leaf0 = scope == kUpOwn ? t->own_leaf_lo : 0;
+  const int nlv = scope == kUpOwn ? t->own_leaf_hi - t->own_leaf_lo : t->nleaves;
+  const int* ulist = scope == kUpFull ? t->up_list : scope == kUpOwn ? t->up_own : t->up_strad;
+  const std::vector<int>& uoff =
+      scope == kUpFull ? t->up_level_off : scope == kUpOwn ? t->up_own_off : t->up_strad_off;
   const CellGeom cg{t->x_min, t->y_min, t->W};
   const size_t shm = (size_t)kPassWarps * 8 * p * sizeof(double2);
   const size_t shp = (size_t)kPassWarps * 32 * 17 * sizeof(double2);
   int rc = DDM_OK;
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \
-    if ((rc = set_smem(ctx, p2m_kernel<PT>, shp))) return rc;                                   \
-    const int nb = pass_grid(ctx, (const void*)p2m_kernel<PT>, shp, t->nleaves);                \
-    stage_begin(ctx, DDM_ST_P2M, s);                                                            \
-    p2m_kernel<PT><<<nb, kPassWarps * 32, shp, s>>>(t->nleaves, t->leaves, t->c_level, t->c_ix, \
-                                                    t->c_iy, t->c_start, t->c_count, cg, p,     \
-                                                    perm_in, D,                                 \
-                                                    ncomp, t->ex, t->ey, t->ea, t->ec, t->es,   \
-                                                    t->mpole, pf);                              \
-    stage_end(ctx, DDM_ST_P2M, s);                                                              \
+    if (do_p2m && nlv > 0) {                                                                    \
+      if ((rc = set_smem(ctx, p2m_kernel<PT>, shp))) return rc;                                 \
+      const int nb = pass_grid(ctx, (const void*)p2m_kernel<PT>, shp, nlv);                     \
+      stage_begin(ctx, DDM_ST_P2M, s);                                                          \
+      p2m_kernel<PT><<<nb, kPassWarps * 32, shp, s>>>(nlv, t->leaves + leaf0, t->c_level,       \
+                                                      t->c_ix, t->c_iy, t->c_start, t->c_count, \
+                                                      cg, p, perm_in, D,                        \
+                                                      ncomp, t->ex, t->ey, t->ea, t->ec, t->es, \
+                                                      t->mpole, pf);                            \
+      stage_end(ctx, DDM_ST_P2M, s);                                                            \
+    }                                                                                           \
     if ((rc = set_smem(ctx, m2m_level_kernel<PT>, shm))) return rc;                             \
     stage_begin(ctx, DDM_ST_M2M, s);                                                            \
     int top = t->nlevels - 1;                                                                   \
-    if (use_subtrees(t)) {                                                                      \
+    if (scope == kUpFull && use_subtrees(t)) {                                                  \
       if ((rc = set_smem(ctx, m2m_subtree_kernel<PT>, shm))) return rc;                         \
       DDM_CUDA(ctx, launch_pdl(use_pdl(t), m2m_subtree_kernel<PT>, t->sub_n, kPassWarps * 32,   \
                                shm, s, t->sub_Ls, t->nlevels, t->sub_nsl,                       \
@@ -1183,11 +1195,11 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
       top = t->sub_Ls - 1;                                                                      \
     }                                                                                           \
     for (int lev = top; lev >= 2; --lev) {                                                      \
-      const int u0 = t->up_level_off[2 * lev], u1 = t->up_level_off[2 * lev + 1];               \
+      const int u0 = uoff[2 * lev], u1 = uoff[2 * lev + 1];                                     \
       if (u1 <= u0) continue;                                                                   \
       const int nb2 = pass_grid(ctx, (const void*)m2m_level_kernel<PT>, shm, u1 - u0);          \
       DDM_CUDA(ctx, launch_pdl(use_pdl(t), m2m_level_kernel<PT>, nb2, kPassWarps * 32, shm, s, u0, u1,     \
-                               (const int*)t->up_list, (const int*)t->c_ix,                    \
+                               (const int*)ulist, (const int*)t->c_ix,                         \
                                (const int*)t->c_iy, (const int*)t->c_first_child,              \
                                (const int*)t->c_nchild, p, (const double*)t->op_pasT,          \
                                (const double2*)t->op_eps, (const double2*)t->op_e2i,           \
@@ -1201,12 +1213,62 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
   return DDM_OK;
 }
 
+// Multipole exchange of the sharded upward pass: pack this
+// rank's complete cells (xr_cells[xr_off[rank] ..]) into xsend; after the
+// all-gather (xrecv = every rank's pack, padded to xr_max cells), scatter the
+// other ranks' cells into mpole.
+__global__ void mpole_pack_kernel(int ncell, const int* __restrict__ cells, int P2,
+                                  const double2* __restrict__ mpole, double2* __restrict__ out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)ncell * P2) return;
+  const int k = (int)(e / P2), m = (int)(e - (int64_t)k * P2);
+  out[e] = mpole[(size_t)cells[k] * P2 + m];
+}
+
+__global__ void mpole_unpack_kernel(const int* __restrict__ cells, const int* __restrict__ xr_off,
+                                    int world, int rank, int xr_max, int P2,
+                                    const double2* __restrict__ in, double2* __restrict__ mpole) {
+  const int r = blockIdx.y;
+  if (r == rank) return;   // own cells are already in place
+  const int c0 = xr_off[r], nc = xr_off[r + 1] - c0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)nc * P2;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(e / P2), m = (int)(e - (int64_t)k * P2);
+    mpole[(size_t)cells[c0 + k] * P2 + m] = in[((size_t)r * xr_max + k) * P2 + m];
+  }
+}
+
+int launch_mpole_pack(ddm_ctx_s* ctx, ddm_tree_s* t, int rank, cudaStream_t s) {
+  const int P2 = 2 * t->p;
+  const int c0 = t->xr_off[rank], nc = t->xr_off[rank + 1] - c0;
+  if (nc <= 0) return DDM_OK;
+  if (!t->xsend) return set_error(ctx, DDM_ERR_ARG, "no multipole exchange buffers (one rank)");
+  mpole_pack_kernel<<<nblk((int64_t)nc * P2, 256), 256, 0, s>>>(nc, t->xr_cells + c0, P2, t->mpole,
+                                                                t->xsend);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+int launch_mpole_unpack(ddm_ctx_s* ctx, ddm_tree_s* t, int rank, int world, cudaStream_t s) {
+  const int P2 = 2 * t->p;
+  if (t->xr_max <= 0) return DDM_OK;
+  if (!t->xrecv) return set_error(ctx, DDM_ERR_ARG, "no multipole exchange buffers (one rank)");
+  dim3 grid(std::max(1u, std::min(nblk((int64_t)t->xr_max * P2, 256), 1184u)), world);
+  mpole_unpack_kernel<<<grid, 256, 0, s>>>(t->xr_cells, t->xr_off_dev, world, rank, t->xr_max, P2,
+                                           t->xrecv, t->mpole);
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
 // downward pass: M2L of every cell of level >= 2, then L2L one level at a
 // time (top-down), both restricted to subtrees holding owned targets
 int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   if (t->nlevels <= 2) return DDM_OK;
   const int p = t->p;
-  const int c0 = t->level_off[2], c1 = t->ncells;
+  // several ranks: iterate this rank's cell list instead of every cell
+  const int* cl = t->dn_own;
+  const int c0 = cl ? t->dn_own_off[2] : t->level_off[2];
+  const int c1 = cl ? t->dn_own_off[t->nlevels] : t->ncells;
   const bool tc = (p == 8 || p == 12 || p == 16 || p == 20 || p == 24 || p == 28 || p == 30 || p == 32);
   const size_t ndbl = tc ? (size_t)((p + 7) / 8) * ((p + 4) / 4) * 32 : (size_t)(p + 1) * p;
   const size_t wstride = tc ? (size_t)2 * kM2LBatch * kXStride : 3 * (size_t)p + 1;
@@ -1220,7 +1282,7 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     const int nb = pass_grid(ctx, (const void*)m2l_kernel<PT>, shm, c1 - c0);                   \
     stage_begin(ctx, DDM_ST_M2L, s);                                                            \
     DDM_CUDA(ctx, launch_pdl(use_pdl(t), m2l_kernel<PT>, nb, kPassWarps * 32, shm, s, c0, c1,              \
-                             (int64_t)t->own_el_lo, (int64_t)t->own_el_hi,                     \
+                             (const int*)cl, (int64_t)t->own_el_lo, (int64_t)t->own_el_hi,     \
                              (const int*)t->v_off, (const int*)t->v_idx,                       \
                              (const unsigned char*)t->v_cls, (const int*)t->c_start,           \
                              (const int*)t->c_count, p, (const double2*)t->op_w,               \
@@ -1230,11 +1292,12 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     stage_begin(ctx, DDM_ST_L2L, s);                                                            \
     const bool sub = use_subtrees(t);                                                           \
     for (int lev = 3; lev < (sub ? t->sub_Ls + 1 : t->nlevels); ++lev) {                        \
-      const int a = t->level_off[lev], b = t->level_off[lev + 1];                               \
+      const int a = cl ? t->dn_own_off[lev] : t->level_off[lev];                                \
+      const int b = cl ? t->dn_own_off[lev + 1] : t->level_off[lev + 1];                        \
       if (b <= a) continue;                                                                     \
       const int nb2 = pass_grid(ctx, (const void*)l2l_level_kernel<PT>, shm2, b - a);           \
       DDM_CUDA(ctx, launch_pdl(use_pdl(t), l2l_level_kernel<PT>, nb2, kPassWarps * 32, shm2, s, a, b,      \
-                               (int64_t)t->own_el_lo, (int64_t)t->own_el_hi,                   \
+                               (const int*)cl, (int64_t)t->own_el_lo, (int64_t)t->own_el_hi,   \
                                (const int*)t->c_ix, (const int*)t->c_iy,                       \
                                (const int*)t->c_start, (const int*)t->c_count,                 \
                                (const int*)t->c_parent, p, (const double2*)t->op_eps,          \

@@ -154,7 +154,9 @@ int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double el
     const char* e = getenv("DDM_NO_GRAPH");
     return e && e[0] == '1';
   }();
-  if (ctx->profiling || no_graph || !ctx->s_cap)
+  // several ranks: the sharded upward pass all-gathers multipoles inside the
+  // far chain (NCCL), launched directly rather than captured
+  if (ctx->profiling || no_graph || !ctx->s_cap || ctx->world > 1)
     return fmm_matvec_launch(ctx, t, mat, elapsed, D, d_sorted, y_user, y_sorted, mode, s);
   MatvecKey key;
   key.D = D;
@@ -235,6 +237,14 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
     }
   }
 
+  // DDM_SHARD_NOEXCHANGE=1 (scripts/rank_timing.py only): one process times
+  // a rank's sharded work on a partitioned tree WITHOUT the multipole
+  // exchange -- the far field is then incomplete, the result invalid
+  static const bool noexch = [] {
+    const char* e = getenv("DDM_SHARD_NOEXCHANGE");
+    return e && e[0] == '1';
+  }();
+
   // Chebyshev far field (f2, bbfmm.cu): mode DDM_BBFMM | n << 8, elastic
   const bool bb = (mode & DDM_BBFMM) != 0;
   const int bb_n = (mode >> 8) & 0xff;
@@ -264,7 +274,8 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
   // field of the FMM the node-sharing source stream (p2p.cu)
   rc = poro ? launch_poro_prep(ctx, t, perm_in, D, sp)
        : mode == DDM_DIRECT ? launch_prep_sources(ctx, t, perm_in, D, ncomp, sp)
-                            : launch_prep_stream(ctx, t, perm_in, D, ncomp, sp);
+                            : launch_prep_stream(ctx, t, perm_in, D, ncomp, sp,
+                                                 early && (ctx->world > 1 || noexch) && t->shard_up);
   if (rc) return rc;
   stage_end(ctx, DDM_ST_PREP, sp);
 
@@ -298,11 +309,24 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
   if (bb) {
     if ((rc = launch_bb_far(ctx, t, bb_n, perm_in ? t->d_sorted : D, ncomp, gc, sf))) return rc;
   } else {
-  // upward pass: P2M on all leaves, M2M level by level (replicated on all
-  // ranks); prep gathered D into sorted order, so it is read coalesced
-  if ((rc = early ? launch_upward(ctx, t, perm_in, D, ncomp, pf, sf)
-                  : launch_upward(ctx, t, nullptr, perm_in ? t->d_sorted : D, ncomp, pf, sf)))
+  // upward pass: P2M on all leaves, M2M level by level; on several ranks
+  // sharded: this rank's leaves and complete cells, the
+  // multipole all-gather (overlapping the near field on the other stream),
+  // then the straddling cells on every rank
+  const bool sharded = (ctx->world > 1 || noexch) && t->shard_up;
+  const int scope = sharded ? kUpOwn : kUpFull;
+  if ((rc = early ? launch_upward(ctx, t, perm_in, D, ncomp, pf, sf, scope)
+                  : launch_upward(ctx, t, nullptr, perm_in ? t->d_sorted : D, ncomp, pf, sf,
+                                  scope)))
     return rc;
+  if (sharded) {
+    if ((rc = launch_mpole_pack(ctx, t, ctx->rank, sf))) return rc;
+    stage_begin(ctx, DDM_ST_COMM, sf);
+    if (!noexch && (rc = allgather_mpole(ctx, t, sf))) return rc;
+    stage_end(ctx, DDM_ST_COMM, sf);
+    if ((rc = launch_mpole_unpack(ctx, t, ctx->rank, ctx->world, sf))) return rc;
+    if ((rc = launch_upward(ctx, t, nullptr, nullptr, ncomp, pf, sf, kUpStrad))) return rc;
+  }
   // downward pass: M2L of every cell of level >= 2, L2L level by level (cells
   // whose subtree holds owned targets)
   if ((rc = launch_downward(ctx, t, sf))) return rc;
@@ -383,6 +407,57 @@ int fmm_history(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   cudaFreeAsync(Cs, s);
   cudaFreeAsync(Ctot, s);
   return rc;
+}
+
+// Several ranks emulated on one device (tests): the elastic FMM
+// matvec of the sharded path for trees[r] partitioned as rank r of `world`,
+// every phase run rank by rank on stream s, with device copies standing in
+// for the two NCCL all-gathers (multipoles, owned output rows).  Writes the
+// full y in user order.
+int fmm_matvec_sim(ddm_ctx_s* ctx, ddm_tree_s* const* trees, int world, const ddm_material* mat,
+                   const double* D, double* y, cudaStream_t s) {
+  int rc;
+  if (world < 1) return set_error(ctx, DDM_ERR_ARG, "world < 1");
+  if (mat->kind != 0) return set_error(ctx, DDM_ERR_ARG, "the emulation is elastic only");
+  ddm_tree_s* t0 = trees[0];
+  for (int r = 0; r < world; ++r) {
+    ddm_tree_s* t = trees[r];
+    if (t->n != t0->n || t->ncells != t0->ncells || t->p != t0->p || (int)t->xr_off.size() != world + 1 ||
+        t->own_leaf_lo != t->rank_leaf_lo[r])
+      return set_error(ctx, DDM_ERR_ARG, "trees[r] must be one geometry partitioned as rank r of world");
+    if ((rc = fmm_workspace(ctx, t, s))) return rc;
+  }
+  const double gc = mat->G / (4.0 * M_PI * (1.0 - mat->nu));
+  const PoroFar pf;
+  for (int r = 0; r < world; ++r) {   // phase A: near field, local upward pass, pack
+    ddm_tree_s* t = trees[r];
+    if ((rc = launch_prep_stream(ctx, t, t->perm, D, 2, s, world > 1))) return rc;
+    if ((rc = launch_p2p_leaf(ctx, t, gc, s))) return rc;
+    if ((rc = launch_upward(ctx, t, t->perm, D, 2, pf, s, world > 1 ? kUpOwn : kUpFull))) return rc;
+    if (world > 1 && (rc = launch_mpole_pack(ctx, t, r, s))) return rc;
+  }
+  const size_t P2 = 2 * (size_t)t0->p;
+  for (int r = 0; r < world && world > 1; ++r)   // the multipole all-gather
+    for (int q = 0; q < world; ++q) {
+      const int nc = trees[q]->xr_off[q + 1] - trees[q]->xr_off[q];
+      if (nc > 0)
+        DDM_CUDA(ctx, cudaMemcpyAsync(trees[r]->xrecv + (size_t)q * trees[r]->xr_max * P2,
+                                      trees[q]->xsend, nc * P2 * sizeof(double2),
+                                      cudaMemcpyDeviceToDevice, s));
+    }
+  double* ys = t0->y_sorted;
+  for (int r = 0; r < world; ++r) {   // phase B: straddling cells, downward pass, assembly
+    ddm_tree_s* t = trees[r];
+    if (world > 1) {
+      if ((rc = launch_mpole_unpack(ctx, t, r, world, s))) return rc;
+      if ((rc = launch_upward(ctx, t, nullptr, nullptr, 2, pf, s, kUpStrad))) return rc;
+    }
+    if ((rc = launch_downward(ctx, t, s))) return rc;
+    if ((rc = launch_l2p(ctx, t, 2, gc, pf, s))) return rc;
+    // owned rows straight into the shared sorted vector (the row all-gather)
+    if ((rc = launch_finalize_near(ctx, t, t->own_el_lo, t->own_el_hi, nullptr, ys, s))) return rc;
+  }
+  return launch_scatter_user(ctx, t0, ys, 2, y, s);
 }
 
 }  // namespace ddm

@@ -110,8 +110,15 @@ int launch_poro_direct(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi,
 
 // ---- launchers (expansions.cu): upward / downward passes
 struct PoroFar;
+// scope 0: P2M of all leaves + M2M of every non-leaf cell (replicated);
+// 1: P2M of the owned leaves + M2M of this rank's complete cells; 2: M2M of
+// the straddling cells (after the multipole exchange)
+enum { kUpFull = 0, kUpOwn = 1, kUpStrad = 2 };
 int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
-                  const PoroFar& pf, cudaStream_t s);
+                  const PoroFar& pf, cudaStream_t s, int scope = kUpFull);
+// multipoles of this rank's complete cells -> t->xsend; gathered -> mpole
+int launch_mpole_pack(ddm_ctx_s* ctx, ddm_tree_s* t, int rank, cudaStream_t s);
+int launch_mpole_unpack(ddm_ctx_s* ctx, ddm_tree_s* t, int rank, int world, cudaStream_t s);
 int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
 int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFar& pf,
                cudaStream_t s);
@@ -133,8 +140,9 @@ int launch_finalize_near(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, 
 // near-field source stream (p2p.cu): chain order + break records once per
 // tree; prep_stream writes the element records (and D in sorted order)
 int build_source_stream(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
+// halo: only the slots the owned leaves read (sharded multi-rank matvec)
 int launch_prep_stream(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D,
-                       int ncomp, cudaStream_t s);
+                       int ncomp, cudaStream_t s, bool halo = false);
 int launch_direct(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, int ncomp, double gc,
                   double* y_user, double* y_sorted, cudaStream_t s);
 

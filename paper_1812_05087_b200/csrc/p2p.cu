@@ -246,7 +246,9 @@ __global__ void item_rng_fill(int nitems, const int4* __restrict__ items,
 //   B = (D_s + i D_n) e, r = conj(e)^2, Bh = B/2, Q' = -(r B + conj B),
 //   P1 = Bh (r - 1), P2 = i Bh (r + 1)   (negated for a flipped element)
 // and D gathered to sorted order for the upward pass.
-__global__ void prep_stream(int64_t n, int ncomp, const int* __restrict__ perm,
+__global__ void prep_stream(int64_t q_lo, int64_t n, const int2* __restrict__ hrng,
+                            const int64_t* __restrict__ hpre, int nh, int ncomp,
+                            const int* __restrict__ perm,
                             const int* __restrict__ st_elem,
                             const unsigned char* __restrict__ st_code,
                             const int* __restrict__ rbeg, const double* __restrict__ D,
@@ -254,8 +256,16 @@ __global__ void prep_stream(int64_t n, int ncomp, const int* __restrict__ perm,
                             const double* __restrict__ ea, const double* __restrict__ ec,
                             const double* __restrict__ es, double* __restrict__ srec,
                             double* __restrict__ dsort) {
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t q = q_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= n) return;
+  if (hrng) {   // q numbers the slots of the merged halo ranges
+    int lo = 0, hi = nh - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (hpre[mid] <= q) lo = mid; else hi = mid - 1;
+    }
+    q = hrng[lo].x + (q - hpre[lo]);
+  }
   const int i = st_elem[q];
   const unsigned char code = st_code[q];
   const int j = perm ? perm[i] : i;
@@ -880,8 +890,15 @@ int build_source_stream(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
 }
 
 int launch_prep_stream(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D,
-                       int ncomp, cudaStream_t s) {
-  prep_stream<<<nblk(t->n, 256), 256, 0, s>>>(t->n, ncomp, perm_in, t->st_elem, t->st_code,
+                       int ncomp, cudaStream_t s, bool halo) {
+  // slots [halo_lo, halo_hi): every record the owned leaves' near field reads
+  // (all slots on one rank)
+  const bool h = halo && t->halo_rng;
+  const int64_t q0 = 0, q1 = h ? t->halo_slots : (halo ? 0 : t->n);
+  if (q1 <= q0) return DDM_OK;
+  prep_stream<<<nblk(q1 - q0, 256), 256, 0, s>>>(q0, q1, h ? t->halo_rng : nullptr,
+                                               h ? t->halo_pre : nullptr, t->nhalo, ncomp, perm_in,
+                                               t->st_elem, t->st_code,
                                                t->rbeg, D, t->ex, t->ey, t->ea, t->ec, t->es,
                                                t->srec, perm_in ? t->d_sorted : nullptr);
   DDM_CUDA(ctx, cudaGetLastError());

@@ -95,3 +95,44 @@ def test_partition_poro_cached_and_history(ddm):
     _rows_by_rank(D, ctx, torch, tree, run_mv, worlds=(2, 3))
     _rows_by_rank(D, ctx, torch, tree, run_hist, worlds=(2, 3))
     tree.free()
+
+
+def _sim_case(D, ctx, torch, g, leaf, p, worlds, seed):
+    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+    args = (f(g.xc), f(g.yc), f(g.half_len), f(g.beta))
+    mat = D.material(0, 8e9, 0.25)
+    x = f(random_dd(g.n, 2, seed))
+    ref_tree = D.Tree(ctx, *args, leaf_size=leaf, order_p=p)
+    ref = D.matvec(ctx, ref_tree, mat, x).cpu().numpy()
+    ref_tree.free()
+    for world in worlds:
+        trees = [D.Tree(ctx, *args, leaf_size=leaf, order_p=p) for _ in range(world)]
+        for r, t in enumerate(trees):
+            t.partition(r, world)
+        y = D.matvec_sim(ctx, trees, mat, x).cpu().numpy()
+        assert np.array_equal(y, ref), world
+        for t in trees:
+            t.free()
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_sharded_upward_pass_emulated(ddm, cfg):
+    """The sharded multi-rank matvec (P2M of each rank's leaves,
+    M2M of its complete cells, multipole all-gather -- played here by device
+    copies between the ranks' trees --, M2M of the straddling cells, downward
+    pass and assembly of the owned rows) equals the unpartitioned matvec
+    bitwise for W = 1, 2, 3, 5, 8."""
+    D, ctx, torch = ddm
+    g = make_config(cfg)
+    _sim_case(D, ctx, torch, g, CONFIGS[cfg]["leaf"], 20, (1, 2, 3, 5, 8), 30 + cfg)
+
+
+def test_sharded_upward_pass_emulated_cfg5_cut(ddm):
+    # a 100 000-element cut of config 5 (leaf 64, p 20: the headline tree's
+    # shape, deep enough for straddling cells at many levels), W = 2 and 8
+    D, ctx, torch = ddm
+    g5 = make_config(5)
+    keep = g5.frac_id < 1000
+    g = Geometry(g5.xc[keep], g5.yc[keep], g5.half_len[keep], g5.beta[keep], g5.frac_id[keep],
+                 g5.tips[:1000])
+    _sim_case(D, ctx, torch, g, 64, 20, (2, 8), 55)
