@@ -284,6 +284,9 @@ struct ddm_tree_s {
   int gm_dev_m = 0;
   unsigned* gm_ticket = nullptr;  // zeroed tickets of the fused GMRES reductions
   int gm_ticket_n = 0;
+  // captured Arnoldi step (gmres.cu): one graph per argument set
+  cudaGraphExec_t gm_exec = nullptr;
+  uintptr_t gm_key[12] = {};
 };
 
 namespace ddm {
@@ -301,6 +304,18 @@ int cuda_error_if(ddm_ctx_s* ctx, cudaError_t e, const char* what);
 
 #define DDM_CHECK_LAUNCH(ctx, name) DDM_CUDA(ctx, cudaGetLastError())
 
+// DDM_POISON=1 (tests; compute-sanitizer is not available on the GPU pool):
+// every library allocation is filled with 0xFF bytes (NaN doubles, -1
+// indices), so a kernel that reads memory no kernel wrote shows up as NaN in
+// a checked result (or as a fault)
+inline bool poison_allocs() {
+  static const bool on = [] {
+    const char* v = getenv("DDM_POISON");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 template <class T>
 int dalloc(ddm_ctx_s* ctx, T** p, size_t count) {
   *p = nullptr;
@@ -310,6 +325,7 @@ int dalloc(ddm_ctx_s* ctx, T** p, size_t count) {
     cudaGetLastError();
     return set_error(ctx, DDM_ERR_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
   }
+  if (poison_allocs()) cudaMemset(*p, 0xff, count * sizeof(T));
   return DDM_OK;
 }
 
@@ -330,6 +346,7 @@ int talloc(ddm_ctx_s* ctx, T** p, size_t count, cudaStream_t s) {
     cudaGetLastError();
     return set_error(ctx, DDM_ERR_OOM, std::string("cudaMallocAsync failed: ") + cudaGetErrorString(e));
   }
+  if (poison_allocs()) cudaMemsetAsync(*p, 0xff, count * sizeof(T), s);
   return DDM_OK;
 }
 

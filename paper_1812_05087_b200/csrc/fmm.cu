@@ -121,6 +121,8 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
                              double* y_sorted, int mode, cudaStream_t s);
 
 void drop_graphs(ddm_tree_s* t) {
+  if (t->gm_exec) cudaGraphExecDestroy(t->gm_exec);
+  t->gm_exec = nullptr;
   for (auto& g : t->graphs) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
     g.exec = nullptr;
@@ -156,7 +158,14 @@ int fmm_matvec(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double el
   }();
   // several ranks: the sharded upward pass all-gathers multipoles inside the
   // far chain (NCCL), launched directly rather than captured
-  if (ctx->profiling || no_graph || !ctx->s_cap || ctx->world > 1)
+  // inside a capture (the GMRES step graph) the launches become its nodes
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cst) != cudaSuccess) {
+    cudaGetLastError();
+    cst = cudaStreamCaptureStatusNone;
+  }
+  if (ctx->profiling || no_graph || !ctx->s_cap || ctx->world > 1 ||
+      cst != cudaStreamCaptureStatusNone)
     return fmm_matvec_launch(ctx, t, mat, elapsed, D, d_sorted, y_user, y_sorted, mode, s);
   MatvecKey key;
   key.D = D;

@@ -37,36 +37,48 @@ __device__ __forceinline__ double fixed_order_sum(const double* part, int nb) {
   return s;
 }
 
+// kd != nullptr (captured Arnoldi step): the step index k
+// is read from device memory, nvec = k + 1 and out += (pass ? k + 1 : 0);
+// vectors i = blockIdx.y, blockIdx.y + gridDim.y, ...
 __global__ void __launch_bounds__(kDotThreads)
 multi_dot(const double* __restrict__ V, int64_t ld, const double* __restrict__ w, int64_t len,
           int nb, double* __restrict__ part, unsigned* __restrict__ ticket,
-          double* __restrict__ out) {
-  const int i = blockIdx.y, b = blockIdx.x;
+          double* __restrict__ out, const int* __restrict__ kd, int pass) {
+  const int b = blockIdx.x;
+  int nvec = gridDim.y;
+  if (kd) {
+    const int k = *kd;
+    nvec = k + 1;
+    out += pass ? k + 1 : 0;
+  }
   const int64_t chunk = (len + nb - 1) / nb;
   const int64_t j0 = b * chunk, j1 = min(len, j0 + chunk);
-  const double* v = V + (int64_t)i * ld;
-  double acc = 0.0;
-  for (int64_t j = j0 + threadIdx.x; j < j1; j += kDotThreads) acc = fma(v[j], w[j], acc);
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   __shared__ double sh[kDotThreads / 32];
   __shared__ bool last;
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int k = 0; k < kDotThreads / 32; ++k) s += sh[k];
-    part[(int64_t)i * nb + b] = s;
-    __threadfence();
-    last = atomicAdd(ticket + i, 1u) == (unsigned)(nb - 1);
-  }
-  __syncthreads();
-  if (last && threadIdx.x < 32) {
-    __threadfence();
-    const double s = fixed_order_sum(part + (int64_t)i * nb, nb);
+  for (int i = blockIdx.y; i < nvec; i += gridDim.y) {
+    const double* v = V + (int64_t)i * ld;
+    double acc = 0.0;
+    for (int64_t j = j0 + threadIdx.x; j < j1; j += kDotThreads) acc = fma(v[j], w[j], acc);
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
     if (threadIdx.x == 0) {
-      out[i] = s;
-      ticket[i] = 0u;
+      double s = 0.0;
+      for (int k = 0; k < kDotThreads / 32; ++k) s += sh[k];
+      part[(int64_t)i * nb + b] = s;
+      __threadfence();
+      last = atomicAdd(ticket + i, 1u) == (unsigned)(nb - 1);
     }
+    __syncthreads();
+    if (last && threadIdx.x < 32) {
+      __threadfence();
+      const double s = fixed_order_sum(part + (int64_t)i * nb, nb);
+      if (threadIdx.x == 0) {
+        out[i] = s;
+        ticket[i] = 0u;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -74,8 +86,13 @@ multi_dot(const double* __restrict__ V, int64_t ld, const double* __restrict__ w
 // per thread (eight loads of the basis in flight), summed in a fixed order
 __global__ void multi_axpy(const double* __restrict__ V, int64_t ld, int nvec,
                            const double* __restrict__ c, double sign, double* __restrict__ w,
-                           int64_t len) {
+                           int64_t len, const int* __restrict__ kd, int pass) {
   extern __shared__ double sc[];
+  if (kd) {   // captured step: nvec = k + 1, coefficients at c + (pass ? k + 1 : 0)
+    const int k = *kd;
+    nvec = k + 1;
+    c += pass ? k + 1 : 0;
+  }
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) sc[i] = c[i];
   __syncthreads();
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < len;
@@ -98,8 +115,15 @@ __global__ void multi_axpy(const double* __restrict__ V, int64_t ld, int nvec,
 __global__ void multi_axpy_norm(const double* __restrict__ V, int64_t ld, int nvec,
                                 const double* __restrict__ c, double sign, double* __restrict__ w,
                                 int64_t len, double* __restrict__ part,
-                                unsigned* __restrict__ ticket, double* __restrict__ out) {
+                                unsigned* __restrict__ ticket, double* __restrict__ out,
+                                const int* __restrict__ kd) {
   extern __shared__ double sc[];
+  if (kd) {   // captured step: second CGS pass, ||w||^2 into out[2 (k+1) + 1]
+    const int k = *kd;
+    nvec = k + 1;
+    c += k + 1;
+    out += 2 * (k + 1) + 1;
+  }
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) sc[i] = c[i];
   __syncthreads();
   double nrm = 0.0;
@@ -379,14 +403,17 @@ __global__ void finish_scale(int k, const double* __restrict__ dh, double* __res
       scal[0] = 0.0;
       return;
     }
+    // column k of H (h1 + h2) with the previous rotations applied; the
+    // running entry stays in a register (a store -> load round trip through
+    // global memory per rotation made this serial loop ~300 cycles a step)
     double* col = Hp + (size_t)k * (k + 3) / 2;
-    for (int i = 0; i <= k; ++i) col[i] = dh[i] + dh[k + 1 + i];
+    double x = dh[0] + dh[k + 1];
     for (int i = 0; i < k; ++i) {
-      const double x = col[i], y = col[i + 1];
-      col[i] = cs[i] * x + sn[i] * y;
-      col[i + 1] = -sn[i] * x + cs[i] * y;
+      const double y = dh[i + 1] + dh[k + 2 + i];
+      const double c = cs[i], sv = sn[i];
+      col[i] = c * x + sv * y;
+      x = -sv * x + c * y;
     }
-    const double x = col[k];
     const double den = hypot(x, hn);
     cs[k] = x / den;
     sn[k] = hn / den;
@@ -406,15 +433,22 @@ __global__ void finish_scale(int k, const double* __restrict__ dh, double* __res
 // inverse block to them (uf = M^-1 dst), so the next operator apply skips a
 // separate preconditioner launch.  CTA 0, thread 0 also does the Givens step
 // (as finish_scale).
+// kd != nullptr (captured step): k = *kd, dst = V + (k + 1) nloc, and the
+// last CTA to finish (ticket) advances *kd for the next step.
 __global__ void __launch_bounds__(kApplyThreads)
 finish_scale_pc(int k, const double* __restrict__ dh, double* __restrict__ Hp,
                 double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ g,
                 double* __restrict__ est, double* __restrict__ scal, int* __restrict__ flag,
                 const double* __restrict__ w, double* __restrict__ dst,
                 const int2* __restrict__ chunks, const int64_t* __restrict__ off, int ncomp,
-                const double* __restrict__ inv, double* __restrict__ uf) {
+                const double* __restrict__ inv, double* __restrict__ uf, int* __restrict__ kd,
+                int64_t nloc, unsigned* __restrict__ kd_ticket) {
   __shared__ double xs[kPcChunk * 3];
   __shared__ double part[kApplyThreads];
+  if (kd) {
+    k = *kd;
+    dst += (int64_t)(k + 1) * nloc;
+  }
   const bool broke = flag[0] != 0;
   const double hn = sqrt(dh[2 * (k + 1) + 1]);
   const double a = (!broke && hn > 0.0) ? 1.0 / hn : 0.0;
@@ -457,14 +491,17 @@ finish_scale_pc(int k, const double* __restrict__ dh, double* __restrict__ Hp,
       scal[0] = 0.0;
       return;
     }
+    // column k of H (h1 + h2) with the previous rotations applied; the
+    // running entry stays in a register (a store -> load round trip through
+    // global memory per rotation made this serial loop ~300 cycles a step)
     double* col = Hp + (size_t)k * (k + 3) / 2;
-    for (int i = 0; i <= k; ++i) col[i] = dh[i] + dh[k + 1 + i];
+    double x = dh[0] + dh[k + 1];
     for (int i = 0; i < k; ++i) {
-      const double x = col[i], y = col[i + 1];
-      col[i] = cs[i] * x + sn[i] * y;
-      col[i + 1] = -sn[i] * x + cs[i] * y;
+      const double y = dh[i + 1] + dh[k + 2 + i];
+      const double c = cs[i], sv = sn[i];
+      col[i] = c * x + sv * y;
+      x = -sv * x + c * y;
     }
-    const double x = col[k];
     const double den = hypot(x, hn);
     cs[k] = x / den;
     sn[k] = hn / den;
@@ -476,7 +513,19 @@ finish_scale_pc(int k, const double* __restrict__ dh, double* __restrict__ Hp,
     scal[0] = a;
     if (!(hn > 0.0)) flag[0] = k + 1;
   }
+  if (kd) {   // every CTA has read k: the last one advances it
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(kd_ticket, 1u) == gridDim.x - 1) {
+        *kd = k + 1;
+        *kd_ticket = 0u;
+      }
+    }
+  }
 }
+
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
 
 struct Gm {
   ddm_ctx_s* ctx;
@@ -498,7 +547,7 @@ struct Gm {
     const int b = nb();
     if ((int64_t)nvec * b > part_cap) return set_error(ctx, DDM_ERR_ARG, "gmres part buffer");
     dim3 grid(b, nvec);
-    multi_dot<<<grid, kDotThreads, 0, s>>>(V, ld, w, nloc, b, part, ticket, dh + off);
+    multi_dot<<<grid, kDotThreads, 0, s>>>(V, ld, w, nloc, b, part, ticket, dh + off, nullptr, 0);
     DDM_CUDA(ctx, cudaGetLastError());
     return allreduce_sum(ctx, dh + off, nvec, s);
   }
@@ -508,13 +557,29 @@ struct Gm {
     const unsigned g = std::min(nblk(nloc, 256), 148u * 8);
     if ((int64_t)g > part_cap) return set_error(ctx, DDM_ERR_ARG, "gmres part buffer");
     multi_axpy_norm<<<g, 256, nvec * sizeof(double), s>>>(V, ld, nvec, c, sign, w, nloc, part,
-                                                          ticket_norm, dh + off);
+                                                          ticket_norm, dh + off, nullptr);
     DDM_CUDA(ctx, cudaGetLastError());
     return allreduce_sum(ctx, dh + off, 1, s);
   }
+  // one Arnoldi step with the step index in device memory (captured once,
+  // replayed for every step of a cycle): CGS2 over V[0..k] and w, then
+  // finish_scale_pc writes V[k+1], M^-1 V[k+1] and advances *kd
+  int cgs2_k(const double* V, int m, double* w, const int* kd) {
+    const int b = nb();
+    const int gy = std::min(m + 1, 64);
+    if ((int64_t)(m + 1) * b > part_cap) return set_error(ctx, DDM_ERR_ARG, "gmres part buffer");
+    const unsigned ga = std::min(nblk(nloc, 256), 148u * 8);
+    const size_t shc = (size_t)(m + 1) * sizeof(double);
+    multi_dot<<<dim3(b, gy), kDotThreads, 0, s>>>(V, nloc, w, nloc, b, part, ticket, dh, kd, 0);
+    multi_axpy<<<ga, 256, shc, s>>>(V, nloc, 0, dh, -1.0, w, nloc, kd, 0);
+    multi_dot<<<dim3(b, gy), kDotThreads, 0, s>>>(V, nloc, w, nloc, b, part, ticket, dh, kd, 1);
+    multi_axpy_norm<<<ga, 256, shc, s>>>(V, nloc, 0, dh, -1.0, w, nloc, part, ticket_norm, dh, kd);
+    DDM_CUDA(ctx, cudaGetLastError());
+    return DDM_OK;
+  }
   int axpy(const double* V, int64_t ld, int nvec, const double* c, double sign, double* w) {
     const unsigned g = std::min(nblk(nloc, 256), 148u * 8);
-    multi_axpy<<<g, 256, nvec * sizeof(double), s>>>(V, ld, nvec, c, sign, w, nloc);
+    multi_axpy<<<g, 256, nvec * sizeof(double), s>>>(V, ld, nvec, c, sign, w, nloc, nullptr, 0);
     DDM_CUDA(ctx, cudaGetLastError());
     return DDM_OK;
   }
@@ -875,6 +940,59 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
       std::vector<double> hest(batch);
       int kb = 0;
       bool stop = false;
+      // captured Arnoldi step: from step 1 on, one CUDA
+      // graph per step -- operator apply on M^-1 V_k, CGS2 and the fused
+      // normalisation + preconditioner -- with k in device memory, so the
+      // same graph serves every step (one rank, leaf blocks; DDM_GMRES_GRAPH=0
+      // launches the kernels one by one)
+      static const bool graph_env = [] {
+        const char* e = getenv("DDM_GMRES_GRAPH");
+        return !(e && e[0] == '0');
+      }();
+      int* kdd = reinterpret_cast<int*>(scald + 3);
+      unsigned* kd_tick = t->gm_ticket + m + 2;
+      bool graph_on = false;
+      auto get_step_graph = [&]() -> int {
+        const uintptr_t key[12] = {(uintptr_t)V, (uintptr_t)wf, (uintptr_t)uf, (uintptr_t)nloc,
+                                   (uintptr_t)m, (uintptr_t)mode, (uintptr_t)t->pcl,
+                                   (uintptr_t)mat->kind, 0, 0, 0, 0};
+        uintptr_t kk[12];
+        std::memcpy(kk, key, sizeof(kk));
+        double dd[2] = {dt, mat->G * 1e-9 + mat->nu + mat->nu_u + mat->alpha + mat->kappa * 1e12};
+        std::memcpy(&kk[8], &dd[0], sizeof(double));
+        std::memcpy(&kk[9], &dd[1], sizeof(double));
+        kk[10] = (uintptr_t)Hd;
+        kk[11] = (uintptr_t)g.dh;
+        if (t->gm_exec && std::memcmp(kk, t->gm_key, sizeof(kk)) == 0) return DDM_OK;
+        if (t->gm_exec) cudaGraphExecDestroy(t->gm_exec);
+        t->gm_exec = nullptr;
+        const cudaStream_t sc = ctx->s_cap;
+        cudaGraph_t graph = nullptr;
+        DDM_CUDA(ctx, cudaStreamBeginCapture(sc, cudaStreamCaptureModeThreadLocal));
+        Gm gc = g;
+        gc.s = sc;
+        int rc2 = fmm_matvec(ctx, t, mat, dt, uf, true, nullptr, wf, mode, sc);
+        if (!rc2) rc2 = gc.cgs2_k(V, m, wf + lo, kdd);
+        if (!rc2)
+          finish_scale_pc<<<t->pc_nchunks, kApplyThreads, 0, sc>>>(
+              0, g.dh, Hd, csd, snd, gd, estd, scald, flagd, wf + lo, V, t->pc_chunks, t->pc_off,
+              ncomp, t->pcl, uf, kdd, nloc, kd_tick);
+        const cudaError_t ce = cudaStreamEndCapture(sc, &graph);
+        if (rc2) {
+          if (graph) cudaGraphDestroy(graph);
+          return rc2;
+        }
+        if (ce != cudaSuccess) return cuda_error(ctx, ce, "cudaStreamEndCapture (gmres step)");
+        const cudaError_t ie =
+            cudaGraphInstantiateWithFlags(&t->gm_exec, graph, cudaGraphInstantiateFlagUseNodePriority);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) {
+          t->gm_exec = nullptr;
+          return cuda_error(ctx, ie, "cudaGraphInstantiate (gmres step)");
+        }
+        std::memcpy(t->gm_key, kk, sizeof(kk));
+        return DDM_OK;
+      };
       // H and g of the first kd steps from the device (for form_x)
       auto fetch_state = [&](int kd) -> int {
         const size_t hn_ = (size_t)kd * (kd + 3) / 2;
@@ -887,6 +1005,18 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
       for (int k = 0; k < m && iters < max_iter; ++k) {
         const double* vk = V + (int64_t)k * nloc;
         const double* vin = vk;
+        if (graph_on) {
+          if (!uf_ready) {   // uf served as scratch of a true-residual check
+            if ((rc = precond_apply(ctx, t, mat, dt, 2, vk, uf, s))) return rc;
+            set_int_kernel<<<1, 1, 0, s>>>(kdd, k);
+            DDM_CUDA(ctx, cudaGetLastError());
+          }
+          DDM_CUDA(ctx, cudaGraphLaunch(t->gm_exec, s));
+          uf_ready = true;
+          ++iters;
+          kdone = k + 1;
+          if (k + 1 - kb < batch && k + 1 < m && iters < max_iter) continue;
+        } else {
         if (ctx->exchange) {
           DDM_CUDA(ctx, cudaMemcpyAsync(vf + lo, vk, nloc * sizeof(double), cudaMemcpyDeviceToDevice, s));
           if ((rc = allgather_sorted(ctx, t, vf, ncomp, s))) return rc;
@@ -910,7 +1040,7 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
         if (fuse_pc) {
           finish_scale_pc<<<t->pc_nchunks, kApplyThreads, 0, s>>>(
               k, g.dh, Hd, csd, snd, gd, estd, scald, flagd, w, V + (int64_t)(k + 1) * nloc,
-              t->pc_chunks, t->pc_off, ncomp, t->pcl, uf);
+              t->pc_chunks, t->pc_off, ncomp, t->pcl, uf, nullptr, 0, nullptr);
           uf_ready = true;   // uf = M^-1 V_{k+1} for the next step's operator apply
         } else {
           finish_scale<<<nblk(nloc, 256), 256, 0, s>>>(k, g.dh, Hd, csd, snd, gd, estd, scald,
@@ -919,7 +1049,15 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
         DDM_CUDA(ctx, cudaGetLastError());
         ++iters;
         kdone = k + 1;
+        if (k == 0 && fuse_pc && graph_env && ctx->world == 1 && !ctx->exchange && !ctx->profiling &&
+            ctx->s_cap && m > 1) {
+          if ((rc = get_step_graph())) return rc;
+          set_int_kernel<<<1, 1, 0, s>>>(kdd, 1);
+          DDM_CUDA(ctx, cudaGetLastError());
+          graph_on = true;
+        }
         if (k + 1 - kb < batch && k + 1 < m && iters < max_iter) continue;
+        }
         int hflag = 0;
         DDM_CUDA(ctx, cudaMemcpyAsync(hest.data(), estd + kb, (k + 1 - kb) * sizeof(double),
                                       cudaMemcpyDeviceToHost, s));

@@ -540,6 +540,7 @@ void free_tree(ddm_tree_s* t) {
   if (t->hc_ptrs) cudaFree(t->hc_ptrs);
   for (auto& g : t->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (t->gm_exec) cudaGraphExecDestroy(t->gm_exec);
 }
 
 // CUDA events at the stage boundaries of build_tree (ddm_tree_build_times)

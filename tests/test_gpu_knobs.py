@@ -73,6 +73,10 @@ print("RESULT " + json.dumps(out))
     # all-reduce of the GMRES dots) on a one-rank communicator
     {"DDM_FORCE_NCCL": "1"},
     {"DDM_FORCE_NCCL": "1", "DDM_GMRES_SYNC": "1"},
+    # every library allocation poisoned with NaN / -1 (uninitialised reads
+    # surface in the checked results; compute-sanitizer is closed on the pool)
+    {"DDM_POISON": "1"},
+    {"DDM_POISON": "1", "DDM_GMRES_GRAPH": "0", "DDM_P2P_LEAF": "0", "DDM_L2P_BLOCK": "0"},
 ])
 def test_knob_paths_agree_with_oracle(env):
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=dict(os.environ, **env),
