@@ -1062,8 +1062,8 @@ std::vector<LaunchCfg> g_cfg;
 template <class K>
 int set_smem(ddm_ctx_s* ctx, K kernel, size_t shm) {
   // dynamic + static shared memory above 48 KB needs the opt-in attribute
-  // (static use of these kernels stays below 8 KB)
-  if (shm <= 40 * 1024) return DDM_OK;
+  // (static use of these kernels stays below 17 KB)
+  if (shm <= 30 * 1024) return DDM_OK;
   std::lock_guard<std::mutex> lk(g_cfg_mu);
   for (const auto& c : g_cfg)
     if (c.kernel == (const void*)kernel && c.shm >= shm && c.device == ctx->device && c.per_sm < 0)
