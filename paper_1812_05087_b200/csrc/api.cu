@@ -205,6 +205,10 @@ static void drop_owned_state(ddm_tree_s* t) {
     void* sh[] = {t->xr_cells, t->xr_off_dev, t->up_own, t->up_strad, t->xsend, t->xrecv,
                   t->ag_send, t->ag_recv, t->ag_lo, t->halo_rng, t->halo_pre, t->dn_own};
     t->dn_own = nullptr;
+    if (t->l2p_runs) cudaFree(t->l2p_runs);
+    t->l2p_runs = nullptr;
+    t->l2p_nruns = 0;
+    t->l2p_lo = t->l2p_hi = -1;
     t->halo_rng = nullptr;
     t->halo_pre = nullptr;
     t->nhalo = 0;

@@ -221,6 +221,13 @@ struct ddm_tree_s {
   int2* lr_rng = nullptr;         // [nu] record range [rbeg[u_lo], rbeg[u_hi]) of every U range
                                   // (leaf k's ranges: u_off[k] .. u_off[k+1]; p2p_leaf_kernel)
   int4* leaf_info = nullptr;      // [nleaves] (c_start, c_count, u_off[k], u_off[k+1]) of each leaf
+  // block-staged L2P (expansions.cu): static geometry tables and the runs of
+  // 128 owned elements (first leaf, leaves, first W entry, W entries)
+  double4* leaf_geo = nullptr;    // [nleaves] (z0.x, z0.y, 1/s, has a local expansion)
+  double4* w_geo = nullptr;       // [nw] (z_D.x, z_D.y, 1/s_D, 0) of every W entry
+  int4* l2p_runs = nullptr;
+  int l2p_nruns = 0;
+  int64_t l2p_lo = -1, l2p_hi = -1;   // owned range the runs were built for
   double* y_near = nullptr;       // [n][2] elastic near field of the owned elements (sorted order)
   double* gpart = nullptr;        // per-group partials of the on-the-fly poroelastic near field
   int64_t gpart_n = 0;

@@ -907,7 +907,9 @@ __device__ __forceinline__ void l2p_eval(int p, double x, double y, bool has_loc
 #endif
 template <int PT>
 __global__ void __launch_bounds__(kL2PThreads, DDM_L2PB_MINB)
-l2p_block_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int* __restrict__ el_leaf,
+l2p_block_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int4* __restrict__ runs,
+                 const double4* __restrict__ leaf_geo, const double4* __restrict__ w_geo,
+                 const int* __restrict__ el_leaf,
                  const int* __restrict__ leaves, const int* __restrict__ c_level,
                  const int* __restrict__ c_ix, const int* __restrict__ c_iy,
                  const double2* __restrict__ local, const int* __restrict__ w_off,
@@ -923,52 +925,46 @@ l2p_block_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int* __restrict__ 
   __shared__ double4 kgeo[kL2PLeaves];   // (z0.x, z0.y, 1/s, has local)
   __shared__ double4 wgeo[kL2PW];        // (z_D.x, z_D.y, 1/s_D, -)
   __shared__ int kcell[kL2PLeaves], kw[kL2PLeaves + 1], wcell[kL2PW];
-  __shared__ int s_k0, s_nk, s_w0, s_nw;
   const int tid = threadIdx.x;
   const int64_t i0 = e_lo + (int64_t)blockIdx.x * kL2PThreads;
   const int64_t i = i0 + tid;
   const bool valid = i < e_hi;
-  pdl_wait();   // the leaves' final locals (L2L)
+  // the run's descriptor (precomputed per owned range): the staging is two
+  // block-wide load rounds -- the leaves' / W cells' ids and geometry, then
+  // their coefficients -- independent of the element loads
+  const int4 rd = __ldg(runs + blockIdx.x);
+  const int k0 = rd.x, nk = rd.y, w0 = rd.z, nw = rd.w;
   const int k = valid ? __ldg(el_leaf + i) : -1;
-  if (tid == 0) {
-    const int k0 = k, k1 = __ldg(el_leaf + min(i0 + kL2PThreads, e_hi) - 1);
-    s_k0 = k0;
-    s_nk = k1 - k0 + 1;
-    s_w0 = __ldg(w_off + k0);
-    s_nw = __ldg(w_off + k1 + 1) - s_w0;
-  }
-  __syncthreads();
-  const int k0 = s_k0, nk = s_nk, w0 = s_w0, nw = s_nw;
+  // the element's own data, loaded before the staging (their latency would
+  // otherwise be exposed after the evaluation)
+  const double x = valid ? __ldg(ex + i) : 0.0, y = valid ? __ldg(ey + i) : 0.0;
+  const double ct = valid ? __ldg(ec + i) : 1.0, st = valid ? __ldg(es + i) : 0.0;
   const bool staged = nk <= kL2PLeaves && nw <= kL2PW;
   if (staged) {
     if (tid < nk) {
-      const int c = __ldg(leaves + k0 + tid);
-      const int lev = __ldg(c_level + c);
-      kcell[tid] = c;
-      const double2 z0 = cg.centre(lev, __ldg(c_ix + c), __ldg(c_iy + c));
-      kgeo[tid] = make_double4(z0.x, z0.y, 1.0 / cg.side(lev), lev >= 2 ? 1.0 : 0.0);
+      kcell[tid] = __ldg(leaves + k0 + tid);
+      kgeo[tid] = leaf_geo[k0 + tid];
       kw[tid] = __ldg(w_off + k0 + tid) - w0;
       if (tid == nk - 1) kw[nk] = nw;
     } else if (tid >= 64 && tid - 64 < nw) {
-      const int D = __ldg(w_idx + w0 + tid - 64);
-      const int ld = __ldg(c_level + D);
-      wcell[tid - 64] = D;
-      const double2 zd = cg.centre(ld, __ldg(c_ix + D), __ldg(c_iy + D));
-      wgeo[tid - 64] = make_double4(zd.x, zd.y, ldexp(1.0 / cg.W, ld), 0.0);
+      wcell[tid - 64] = __ldg(w_idx + w0 + tid - 64);
+      wgeo[tid - 64] = w_geo[w0 + tid - 64];
     }
     __syncthreads();
+    pdl_wait();   // the leaves' final locals (L2L)
     for (int e = tid; e < nk * P2; e += kL2PThreads) {
       const int kl = e / P2, m = e - kl * P2;
-      shL[e] = __ldg(local + (size_t)kcell[kl] * P2 + m);
+      shL[e] = local[(size_t)kcell[kl] * P2 + m];
     }
     for (int e = tid; e < nw * P2; e += kL2PThreads) {
       const int wl = e / P2, m = e - wl * P2;
       shW[e] = __ldg(mpole + (size_t)wcell[wl] * P2 + m);
     }
     __syncthreads();
+  } else {
+    pdl_wait();
   }
   if (!valid) return;
-  const double x = ex[i], y = ey[i];
   double2 phi_t, X_t;
   if (staged) {
     const int kl = k - k0;
@@ -1000,7 +996,6 @@ l2p_block_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int* __restrict__ 
     }
   }
   const double2 W = make_double2(-gc * X_t.y, gc * X_t.x);
-  const double ct = ec[i], st = es[i];
   const double2 e2 = make_double2(ct * ct - st * st, 2.0 * ct * st);
   const double2 t2 = cmul(e2, W);
   y_far[i * ncomp + 0] = t2.y;
@@ -1323,6 +1318,72 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   return DDM_OK;
 }
 
+// static geometry of every leaf and every W entry (block-staged L2P)
+__global__ void l2p_geo_kernel(int nleaves, int64_t nw, const int* __restrict__ leaves,
+                               const int* __restrict__ w_idx, const int* __restrict__ c_level,
+                               const int* __restrict__ c_ix, const int* __restrict__ c_iy,
+                               CellGeom cg, double4* __restrict__ leaf_geo,
+                               double4* __restrict__ w_geo) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < nleaves) {
+    const int c = leaves[j];
+    const int lev = c_level[c];
+    const double2 z0 = cg.centre(lev, c_ix[c], c_iy[c]);
+    leaf_geo[j] = make_double4(z0.x, z0.y, 1.0 / cg.side(lev), lev >= 2 ? 1.0 : 0.0);
+  } else if (j - nleaves < nw) {
+    const int D = w_idx[j - nleaves];
+    const int ld = c_level[D];
+    const double2 zd = cg.centre(ld, c_ix[D], c_iy[D]);
+    w_geo[j - nleaves] = make_double4(zd.x, zd.y, ldexp(1.0 / cg.W, ld), 0.0);
+  }
+}
+
+// run r = elements [e_lo + 128 r, ...) of the owned range: (first leaf,
+// leaves, first W entry, W entries)
+__global__ void l2p_runs_kernel(int nruns, int64_t e_lo, int64_t e_hi, const int* __restrict__ el_leaf,
+                                const int* __restrict__ w_off, int4* __restrict__ runs) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nruns) return;
+  const int64_t a = e_lo + (int64_t)r * kL2PThreads;
+  const int64_t b = min(e_hi, a + kL2PThreads) - 1;
+  const int k0 = el_leaf[a], k1 = el_leaf[b];
+  runs[r] = make_int4(k0, k1 - k0 + 1, w_off[k0], w_off[k1 + 1] - w_off[k0]);
+}
+
+static int l2p_tables(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
+  int rc;
+  const CellGeom cg{t->x_min, t->y_min, t->W};
+  if (!t->leaf_geo) {
+    if ((rc = talloc(ctx, &t->leaf_geo, (size_t)t->nleaves, s)) ||
+        (rc = talloc(ctx, &t->w_geo, (size_t)std::max<int64_t>(t->nw, 1), s)))
+      return rc;
+    const int64_t tot = t->nleaves + t->nw;
+    l2p_geo_kernel<<<nblk(tot, 256), 256, 0, s>>>(t->nleaves, t->nw, t->leaves, t->w_idx,
+                                                   t->c_level, t->c_ix, t->c_iy, cg, t->leaf_geo,
+                                                   t->w_geo);
+    DDM_CUDA(ctx, cudaGetLastError());
+  }
+  if (t->l2p_lo != t->own_el_lo || t->l2p_hi != t->own_el_hi) {
+    if (t->l2p_runs) cudaFree(t->l2p_runs);
+    t->l2p_runs = nullptr;
+    const int64_t ne = t->own_el_hi - t->own_el_lo;
+    t->l2p_nruns = (int)((ne + kL2PThreads - 1) / kL2PThreads);
+    if ((rc = talloc(ctx, &t->l2p_runs, (size_t)std::max(t->l2p_nruns, 1), s))) return rc;
+    if (t->l2p_nruns > 0) {
+      l2p_runs_kernel<<<nblk(t->l2p_nruns, 256), 256, 0, s>>>(t->l2p_nruns, t->own_el_lo,
+                                                               t->own_el_hi, t->el_leaf, t->w_off,
+                                                               t->l2p_runs);
+      DDM_CUDA(ctx, cudaGetLastError());
+    }
+    t->l2p_lo = t->own_el_lo;
+    t->l2p_hi = t->own_el_hi;
+  }
+  return DDM_OK;
+}
+
+// prepare the static L2P tables (called from fmm_workspace, outside captures)
+int l2p_prepare(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) { return l2p_tables(ctx, t, s); }
+
 // L2P of the owned elements into t->y_far (far-field stream): block-staged
 // kernel by default, DDM_L2P_BLOCK=0 the thread-per-element kernel
 int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFar& pf,
@@ -1330,10 +1391,12 @@ int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFa
   const int64_t lo = t->own_el_lo, hi = t->own_el_hi;
   if (hi <= lo) return DDM_OK;
   const CellGeom cg{t->x_min, t->y_min, t->W};
-  static const bool blk = [] {
+  static const bool blk_env = [] {
     const char* e = getenv("DDM_L2P_BLOCK");
     return !(e && e[0] == '0');
   }();
+  // the runs must match the owned range (built by l2p_prepare, outside captures)
+  const bool blk = blk_env && t->l2p_runs && t->l2p_lo == lo && t->l2p_hi == hi;
   const unsigned nb = nblk(hi - lo, 256);
   const unsigned nbb = nblk(hi - lo, kL2PThreads);
   const size_t shb = (size_t)(kL2PLeaves + kL2PW) * 2 * t->p * sizeof(double2);
@@ -1343,7 +1406,9 @@ int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFa
     if (blk) {                                                                                  \
       if ((rc = set_smem(ctx, l2p_block_kernel<PT>, shb))) return rc;                           \
       DDM_CUDA(ctx, launch_pdl(use_pdl(t), l2p_block_kernel<PT>, nbb, kL2PThreads, shb, s,      \
-                               (int64_t)lo, (int64_t)hi, ncomp, (const int*)t->el_leaf,         \
+                               (int64_t)lo, (int64_t)hi, ncomp, (const int4*)t->l2p_runs,       \
+                               (const double4*)t->leaf_geo, (const double4*)t->w_geo,           \
+                               (const int*)t->el_leaf,                                          \
                                (const int*)t->leaves, (const int*)t->c_level,                  \
                                (const int*)t->c_ix, (const int*)t->c_iy,                       \
                                (const double2*)t->local, (const int*)t->w_off,                 \

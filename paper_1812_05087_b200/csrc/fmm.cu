@@ -37,7 +37,8 @@ int fmm_workspace(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     if ((rc = talloc(ctx, &t->y_far, (size_t)t->n * 3, s))) return rc;
     if ((rc = talloc(ctx, &t->y_near, (size_t)t->n * 2, s))) return rc;
   }
-  return build_source_stream(ctx, t, s);
+  if ((rc = build_source_stream(ctx, t, s))) return rc;
+  return l2p_prepare(ctx, t, s);
 }
 
 

@@ -122,6 +122,9 @@ int launch_mpole_unpack(ddm_ctx_s* ctx, ddm_tree_s* t, int rank, int world, cuda
 int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
 int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFar& pf,
                cudaStream_t s);
+// static tables of the block-staged L2P (geometry of leaves / W entries, runs
+// of the owned range); idempotent, outside any capture
+int l2p_prepare(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
 int launch_finalize(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, int ncomp, double gc,
                     const PoroFar& pf, double* y_user, double* y_sorted, cudaStream_t s);
 
