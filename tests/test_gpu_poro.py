@@ -492,3 +492,40 @@ def test_poro_fmm_pstar_solution_vector_cfg4(ddm):
     y = _mv(D, ctx, torch, tree, x, "fmm", tau)
     for comp in range(3):
         assert rel_l2(y[:, comp], bref[:, comp]) <= 1e-8, comp
+
+
+def test_poro_gmres_cfg3_fmm_vs_direct_operator(ddm):
+    """Config 3 at full size: the solution of the FMM-operator GMRES against
+    the solution of the same GMRES with the exact (DIRECT-mode) operator --
+    which equals the oracle's dense matrix to 1e-12 (test_poro_direct_parity_*)
+    -- bounds the solution error itself, not only the residual on sampled rows
+    (north-star bar 1e-6 on the GMRES solution)."""
+    D, ctx, torch = ddm
+    g = make_config(3)
+    c = CONFIGS[3]
+    tau, ld = c["dt"], c["load"]
+    tree = _tree(D, ctx, torch, g, p=c["p_star"], min_side=_rc(tau, g))
+    mat = D.material_from_dict(MAT)
+    beta = torch.tensor(g.beta, device="cuda")
+    b = D.farfield_rhs(ctx, beta, 3, ld["p_f"], ld["sH"], ld["sh"], net=True,
+                       b_p=ld["sh"] + ld["p_f"] - ld["p0"])
+    xf, itf, rrf = D.gmres_solve(ctx, tree, mat, b, dt=tau, tol=1e-10, restart=3000, max_iter=6000)
+    xd, itd, rrd = D.gmres_solve(ctx, tree, mat, b, dt=tau, tol=1e-10, restart=3000, max_iter=6000,
+                                 mode="direct")
+    assert rrf <= 1e-10 and rrd <= 1e-10
+    xf, xd = xf.cpu().numpy(), xd.cpu().numpy()
+    errs = [rel_l2(xf[:, comp], xd[:, comp]) for comp in range(3)]
+    print(f"config 3 GMRES: FMM vs exact operator solution {errs}, iterations {itf} / {itd}")
+    assert max(errs) <= 1e-6, errs
+    # and the FMM matvec on EVERY row against the exact operator (random D and
+    # the solution, where near and far fields cancel)
+    Dv = random_dd(g.n, 3, 303)
+    Dv[:, 2] *= 1e-9
+    for v in (Dv, xd):
+        yf = _mv(D, ctx, torch, tree, v, "fmm", tau)
+        yd = _mv(D, ctx, torch, tree, v, "direct", tau)
+        # tractions (shear and normal rows, same units) on their joint scale --
+        # the solution's shear row is ~0 (b_s = 0) -- and the pressure row on its own
+        trac = np.linalg.norm(yf[:, :2] - yd[:, :2]) / np.linalg.norm(yd[:, :2])
+        assert trac <= 1e-8, trac
+        assert rel_l2(yf[:, 2], yd[:, 2]) <= 1e-8
