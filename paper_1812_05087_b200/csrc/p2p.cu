@@ -627,41 +627,36 @@ p2p_leaf_kernel(int leaf_lo, const int4* __restrict__ leaf_info, const int2* __r
       if (np == 0) break;
       mbar_wait(bar_a, phase);
       phase ^= 1u;
-      // ---- evaluate: slice `slice` of the chunk's records for 2 targets per lane
+      // each range's staged predecessor (its carry record) keeps its node and
+      // gets zero coefficients: it then acts as a break record, and every
+      // slice walks ONE contiguous run of staged records with a single node
+      // carry initialised from the record before it (no branch per record)
+      if (tid < np) {
+        double* cr = recs + (size_t)pcs[tid].x * kRecStride;
+#pragma unroll
+        for (int f = 2; f < kRecStride; ++f) cr[f] = 0.0;
+      }
+      __syncthreads();
+      // ---- evaluate: slice `slice` of the chunk's staged records 1 .. used-1
+      const int used = R + np;   // staged records (the first, index 0, is a carry)
       const int slice = tid / tp, tl = tid - slice * tp;
       if (slice < S) {
-        const int a = (int)(((int64_t)R * slice) / S);
-        const int b = (int)(((int64_t)R * (slice + 1)) / S);
+        const int a = 1 + (int)(((int64_t)(used - 1) * slice) / S);
+        const int b = 1 + (int)(((int64_t)(used - 1) * (slice + 1)) / S);
         if (a < b) {
-          int p = 0;
-          while (p + 1 < np && pcs[p + 1].w <= a) ++p;
-          int4 pc = pcs[p];
-          int sidx = pc.x + 1 + (a - pc.w);
-          int nxt = pc.w + pc.z;
           NodeCarry ncr[2];
           {
             double sp[kRecStride];
-            load_rec_s(sp, recs + (size_t)(sidx - 1) * kRecStride);
+            load_rec_s(sp, recs + (size_t)(a - 1) * kRecStride);
 #pragma unroll
             for (int q = 0; q < 2; ++q) node_init(ncr[q], zx[q], zy[q], sp);
           }
 #pragma unroll 2
-          for (int r = a; r < b; ++r) {
-            if (r == nxt) {   // a new range: carry from its staged predecessor
-              ++p;
-              pc = pcs[p];
-              sidx = pc.x + 1;
-              nxt = pc.w + pc.z;
-              double sp[kRecStride];
-              load_rec_s(sp, recs + (size_t)(sidx - 1) * kRecStride);
-#pragma unroll
-              for (int q = 0; q < 2; ++q) node_init(ncr[q], zx[q], zy[q], sp);
-            }
+          for (int j = a; j < b; ++j) {
             double sp[kRecStride];
-            load_rec_s(sp, recs + (size_t)sidx * kRecStride);
+            load_rec_s(sp, recs + (size_t)j * kRecStride);
 #pragma unroll
             for (int q = 0; q < 2; ++q) record_update(acc[q], ncr[q], zx[q], zy[q], sp);
-            ++sidx;
           }
         }
       }
