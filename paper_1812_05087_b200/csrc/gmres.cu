@@ -313,7 +313,8 @@ chunk_invert(const int2* __restrict__ chunks, const int64_t* __restrict__ off, i
     __syncthreads();
   }
   if (singular) {
-    for (int f = tid; f < d * d; f += nt) B[f] = (f / d == f % d) ? 1.0 : 0.0;
+    const int ld = d + (d & 1);
+    for (int f = tid; f < ld * d; f += nt) B[f] = (f / ld == f % ld) ? 1.0 : 0.0;
     return;
   }
   for (int k = d - 1; k >= 0; --k) {   // undo the row interchanges as column swaps
@@ -326,10 +327,13 @@ chunk_invert(const int2* __restrict__ chunks, const int64_t* __restrict__ off, i
       }
     __syncthreads();
   }
-  // (R A)^-1 R: column c scaled by rs[c]; stored column-major
-  for (int f = tid; f < d * d; f += nt) {
-    const int c = f / d, r = f % d;
-    B[f] = A[r * d + c] * rs[c];
+  // (R A)^-1 R: column c scaled by rs[c]; stored column-major with the even
+  // leading dimension ld = d + (d & 1) (16-byte aligned columns for the
+  // double2 loads of chunk_mv; the padding row is 0)
+  const int ld = d + (d & 1);
+  for (int f = tid; f < ld * d; f += nt) {
+    const int c = f / ld, r = f % ld;
+    B[f] = r < d ? A[r * d + c] * rs[c] : 0.0;
   }
 }
 
@@ -340,42 +344,70 @@ chunk_invert(const int2* __restrict__ chunks, const int64_t* __restrict__ off, i
 // the groups in a fixed order.
 constexpr int kApplyThreads = 256;
 
+// y_rows (+)= Ai xs for one chunk (d rows, column-major inverse with even
+// leading dimension ld): thread (row pair rp, column group g) accumulates
+// double2 rows (2 rp, 2 rp + 1) over the columns c = g, g + G, ... with four
+// 16-byte loads in flight; the G group partials are summed in a fixed order.
+__device__ __forceinline__ void chunk_mv(const double* __restrict__ Ai, int d,
+                                         const double* xs, double2* part,
+                                         double* __restrict__ y, int add) {
+  const int ld = d + (d & 1), RP = ld >> 1;
+  const int G = max(1, (int)blockDim.x / RP);
+  const int rp = threadIdx.x % RP, g = threadIdx.x / RP;
+  if (g < G) {
+    const double2* A2 = reinterpret_cast<const double2*>(Ai);
+    double2 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = make_double2(0.0, 0.0);
+    int c = g;
+    for (; c + 3 * G < d; c += 4 * G) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(A2 + (size_t)(c + u * G) * RP + rp);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double xv = xs[c + u * G];
+        a[u].x = fma(v[u].x, xv, a[u].x);
+        a[u].y = fma(v[u].y, xv, a[u].y);
+      }
+    }
+    for (int u = 0; c < d; c += G, ++u) {
+      const double2 v = __ldg(A2 + (size_t)c * RP + rp);
+      const double xv = xs[c];
+      a[u & 3].x = fma(v.x, xv, a[u & 3].x);
+      a[u & 3].y = fma(v.y, xv, a[u & 3].y);
+    }
+    part[threadIdx.x] = make_double2((a[0].x + a[1].x) + (a[2].x + a[3].x),
+                                     (a[0].y + a[1].y) + (a[2].y + a[3].y));
+  }
+  __syncthreads();
+  if (threadIdx.x < RP) {
+    double2 v = make_double2(0.0, 0.0);
+    for (int gg = 0; gg < G; ++gg) {
+      const double2 q = part[gg * RP + threadIdx.x];
+      v.x += q.x;
+      v.y += q.y;
+    }
+    const int r0 = 2 * threadIdx.x;
+    y[r0] = add ? y[r0] + v.x : v.x;
+    if (r0 + 1 < d) y[r0 + 1] = add ? y[r0 + 1] + v.y : v.y;
+  }
+}
+
 __global__ void __launch_bounds__(kApplyThreads)
 chunk_apply(const int2* __restrict__ chunks, const int64_t* __restrict__ off, int q0, int ncomp,
             const double* __restrict__ inv, const double* __restrict__ x, double* __restrict__ y,
             int add) {
   __shared__ double xs[kPcChunk * 3];
-  __shared__ double part[kApplyThreads];
+  __shared__ double2 part[kApplyThreads];
   const int q = q0 + blockIdx.x;
   const int2 ch = chunks[q];
   const int d = ncomp * ch.y;
   const int64_t b0 = (int64_t)ch.x * ncomp;
-  const double* Ai = inv + off[q];
   for (int t = threadIdx.x; t < d; t += blockDim.x) xs[t] = x[b0 + t];
   __syncthreads();
   if (d == 0) return;
-  const int G = max(1, (int)blockDim.x / d);
-  const int r = threadIdx.x % d, g = threadIdx.x / d;
-  if (g < G) {
-    // eight loads in flight per thread (all issued before the FMAs use them)
-    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    int c = g;
-    for (; c + 7 * G < d; c += 8 * G) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldg(Ai + (size_t)(c + u * G) * d + r);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) a[u] = fma(v[u], xs[c + u * G], a[u]);
-    }
-    for (int u = 0; c < d; c += G, ++u) a[u] = fma(__ldg(Ai + (size_t)c * d + r), xs[c], a[u]);
-    part[threadIdx.x] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-  }
-  __syncthreads();
-  if (threadIdx.x < d) {
-    double v = 0.0;
-    for (int gg = 0; gg < G; ++gg) v += part[gg * d + threadIdx.x];
-    y[b0 + threadIdx.x] = add ? y[b0 + threadIdx.x] + v : v;
-  }
+  chunk_mv(inv + off[q], d, xs, part, y + b0, add);
 }
 
 // One Arnoldi step's small work on the device (batched GMRES, no host round
@@ -444,7 +476,7 @@ finish_scale_pc(int k, const double* __restrict__ dh, double* __restrict__ Hp,
                 const double* __restrict__ inv, double* __restrict__ uf, int* __restrict__ kd,
                 int64_t nloc, unsigned* __restrict__ kd_ticket) {
   __shared__ double xs[kPcChunk * 3];
-  __shared__ double part[kApplyThreads];
+  __shared__ double2 part[kApplyThreads];
   if (kd) {
     k = *kd;
     dst += (int64_t)(k + 1) * nloc;
@@ -461,36 +493,11 @@ finish_scale_pc(int k, const double* __restrict__ dh, double* __restrict__ Hp,
     xs[t] = v;
   }
   __syncthreads();
-  const double* Ai = inv + off[blockIdx.x];
-  if (d > 0) {
-    const int G = max(1, (int)blockDim.x / d);
-    const int r = threadIdx.x % d, gg = threadIdx.x / d;
-    if (gg < G) {
-      double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      int c = gg;
-      for (; c + 7 * G < d; c += 8 * G) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldg(Ai + (size_t)(c + u * G) * d + r);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc[u] = fma(v[u], xs[c + u * G], acc[u]);
-      }
-      for (int u = 0; c < d; c += G, ++u) acc[u] = fma(__ldg(Ai + (size_t)c * d + r), xs[c], acc[u]);
-      part[threadIdx.x] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-    }
-    __syncthreads();
-    if (threadIdx.x < d) {
-      double v = 0.0;
-      for (int q = 0; q < G; ++q) v += part[q * d + threadIdx.x];
-      uf[b0 + threadIdx.x] = v;
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (broke) {
-      est[k] = est[k > 0 ? k - 1 : 0];
-      scal[0] = 0.0;
-      return;
-    }
+  if (d > 0) chunk_mv(inv + off[blockIdx.x], d, xs, part, uf + b0, 0);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && broke) {
+    est[k] = est[k > 0 ? k - 1 : 0];
+    scal[0] = 0.0;
+  } else if (blockIdx.x == 0 && threadIdx.x == 0) {
     // column k of H (h1 + h2) with the previous rotations applied; the
     // running entry stays in a register (a store -> load round trip through
     // global memory per rotation made this serial loop ~300 cycles a step)
@@ -619,7 +626,8 @@ static int pc_build_chunks(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, cudaStream_
       }
       ch.push_back(make_int2(a, b - a));
       off.push_back(tot);
-      tot += (int64_t)(ncomp * (b - a)) * (ncomp * (b - a));
+      const int64_t d = ncomp * (b - a);
+      tot += (d + (d & 1)) * d;   // inverse stored with an even leading dimension (chunk_mv)
     }
   }
   if (t->pc_q_lo < 0) t->pc_q_lo = t->pc_q_hi = 0;
