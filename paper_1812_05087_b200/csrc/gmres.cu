@@ -82,84 +82,78 @@ multi_dot(const double* __restrict__ V, int64_t ld, const double* __restrict__ w
   }
 }
 
-// w[j] += sign * sum_i V[i * ld + j] c[i]: eight independent accumulators
-// per thread (eight loads of the basis in flight), summed in a fixed order
-__global__ void multi_axpy(const double* __restrict__ V, int64_t ld, int nvec,
-                           const double* __restrict__ c, double sign, double* __restrict__ w,
-                           int64_t len, const int* __restrict__ kd, int pass) {
+// w[j] += sign * sum_i V[i * ld + j] c[i] (and optionally ||w||^2 of the
+// result).  Block = 64 rows x 4 vector groups: thread (j, q) sums the vectors
+// i = q, q + 4, ... with four accumulators (loads of four vectors in flight),
+// the four group partials are added in a fixed order, so every row's sum has
+// the same order whatever the row range (deterministic, rank independent).
+// With kd (captured step): nvec = *kd + 1, c += pass ? k + 1 : 0, and the
+// norm goes to out[2 (k+1) + 1].
+constexpr int kAxRows = 64, kAxGroups = 4;
+
+template <bool NORM>
+__global__ void __launch_bounds__(kAxRows * kAxGroups)
+cgs_axpy(const double* __restrict__ V, int64_t ld, int nvec, const double* __restrict__ c,
+         double sign, double* __restrict__ w, int64_t len, double* __restrict__ part,
+         unsigned* __restrict__ ticket, double* __restrict__ out, const int* __restrict__ kd,
+         int pass) {
   extern __shared__ double sc[];
-  if (kd) {   // captured step: nvec = k + 1, coefficients at c + (pass ? k + 1 : 0)
+  __shared__ double red[kAxGroups][kAxRows];
+  __shared__ double wsum[kAxRows / 32 > 0 ? kAxRows / 32 : 1];
+  __shared__ bool last;
+  if (kd) {
     const int k = *kd;
     nvec = k + 1;
     c += pass ? k + 1 : 0;
+    if (NORM) out += 2 * (k + 1) + 1;
   }
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) sc[i] = c[i];
   __syncthreads();
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < len;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const int r = threadIdx.x % kAxRows, q = threadIdx.x / kAxRows;
+  const int64_t j = blockIdx.x * (int64_t)kAxRows + r;
+  double acc = 0.0;
+  if (j < len) {
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
     const double* v = V + j;
-    int i = 0;
-    for (; i + 8 <= nvec; i += 8) {
+    int i = q;
+    for (; i + 3 * kAxGroups < nvec; i += 4 * kAxGroups) {
+      double t[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) a[q] = fma(__ldg(v + (int64_t)(i + q) * ld), sc[i + q], a[q]);
+      for (int u = 0; u < 4; ++u) t[u] = __ldg(v + (int64_t)(i + u * kAxGroups) * ld);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = fma(t[u], sc[i + u * kAxGroups], a[u]);
     }
-    for (int q = 0; i < nvec; ++i, ++q) a[q] = fma(__ldg(v + (int64_t)i * ld), sc[i], a[q]);
-    const double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-    w[j] = fma(sign, acc, w[j]);
+    for (int u = 0; i < nvec; i += kAxGroups, ++u) a[u] = fma(__ldg(v + (int64_t)i * ld), sc[i], a[u]);
+    acc = (a[0] + a[1]) + (a[2] + a[3]);
   }
-}
-
-// multi_axpy followed by ||w||^2 of the result: per-block partial sums, the
-// last block (ticket) reduces them in a fixed order into out[0]
-__global__ void multi_axpy_norm(const double* __restrict__ V, int64_t ld, int nvec,
-                                const double* __restrict__ c, double sign, double* __restrict__ w,
-                                int64_t len, double* __restrict__ part,
-                                unsigned* __restrict__ ticket, double* __restrict__ out,
-                                const int* __restrict__ kd) {
-  extern __shared__ double sc[];
-  if (kd) {   // captured step: second CGS pass, ||w||^2 into out[2 (k+1) + 1]
-    const int k = *kd;
-    nvec = k + 1;
-    c += k + 1;
-    out += 2 * (k + 1) + 1;
-  }
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) sc[i] = c[i];
+  red[q][r] = acc;
   __syncthreads();
   double nrm = 0.0;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < len;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    const double* v = V + j;
-    int i = 0;
-    for (; i + 8 <= nvec; i += 8) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) a[q] = fma(__ldg(v + (int64_t)(i + q) * ld), sc[i + q], a[q]);
-    }
-    for (int q = 0; i < nvec; ++i, ++q) a[q] = fma(__ldg(v + (int64_t)i * ld), sc[i], a[q]);
-    const double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-    const double wn = fma(sign, acc, w[j]);
+  if (q == 0 && j < len) {
+    const double tot = ((red[0][r] + red[1][r]) + (red[2][r] + red[3][r]));
+    const double wn = fma(sign, tot, w[j]);
     w[j] = wn;
-    nrm = fma(wn, wn, nrm);
+    nrm = wn * wn;
   }
-  for (int o = 16; o; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
-  __shared__ double sh[32];
-  __shared__ bool last;
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = nrm;
+  if (!NORM) return;
+  if (q == 0) {   // warps 0, 1: the block's rows
+    for (int o = 16; o; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = nrm;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += sh[k];
-    part[blockIdx.x] = s;
+    double t = 0.0;
+    for (int k2 = 0; k2 < kAxRows / 32; ++k2) t += wsum[k2];
+    part[blockIdx.x] = t;
     __threadfence();
     last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (last && threadIdx.x < 32) {
     __threadfence();
-    const double s = fixed_order_sum(part, gridDim.x);
+    const double t = fixed_order_sum(part, gridDim.x);
     if (threadIdx.x == 0) {
-      out[0] = s;
+      out[0] = t;
       ticket[0] = 0u;
     }
   }
@@ -410,6 +404,56 @@ chunk_apply(const int2* __restrict__ chunks, const int64_t* __restrict__ off, in
   chunk_mv(inv + off[q], d, xs, part, y + b0, add);
 }
 
+// The Givens part of an Arnoldi step (block 0 of finish_scale*, all its
+// threads): column k of H = h1 + h2 with the previous rotations applied, a
+// new rotation zeroing h(k+1,k) = hn, the rotated rhs and the residual
+// estimate.  The rotations and the column are staged in shared memory in
+// chunks of 256 by the whole block (the serial recurrence of thread 0 used to
+// wait on a global load per rotation: ~35 us at k = 180 on config 3).
+__device__ void givens_block(int k, double hn, double a, bool broke, const double* __restrict__ dh,
+                             double* __restrict__ Hp, double* __restrict__ cs,
+                             double* __restrict__ sn, double* __restrict__ g,
+                             double* __restrict__ est, double* __restrict__ scal,
+                             int* __restrict__ flag) {
+  __shared__ double sc[256], ss[256], sy[256];
+  double* col = Hp + (size_t)k * (k + 3) / 2;
+  double x = 0.0;
+  if (threadIdx.x == 0 && !broke) x = dh[0] + dh[k + 1];
+  for (int i0 = 0; i0 < k && !broke; i0 += 256) {
+    const int n = min(256, k - i0);
+    __syncthreads();
+    if ((int)threadIdx.x < n) {
+      const int i = i0 + threadIdx.x;
+      sc[threadIdx.x] = cs[i];
+      ss[threadIdx.x] = sn[i];
+      sy[threadIdx.x] = dh[i + 1] + dh[k + 2 + i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int u = 0; u < n; ++u) {
+        const double c = sc[u], sv = ss[u], y = sy[u];
+        col[i0 + u] = c * x + sv * y;
+        x = -sv * x + c * y;
+      }
+  }
+  if (threadIdx.x != 0) return;
+  if (broke) {
+    est[k] = est[k > 0 ? k - 1 : 0];
+    scal[0] = 0.0;
+    return;
+  }
+  const double den = hypot(x, hn);
+  cs[k] = x / den;
+  sn[k] = hn / den;
+  col[k] = den;
+  col[k + 1] = 0.0;
+  g[k + 1] = -sn[k] * g[k];
+  g[k] = cs[k] * g[k];
+  est[k] = fabs(g[k + 1]);
+  scal[0] = a;
+  if (!(hn > 0.0)) flag[0] = k + 1;
+}
+
 // One Arnoldi step's small work on the device (batched GMRES, no host round
 // trip per step), fused with the normalisation of the next basis vector.
 // dh = [h1 (k+1) | h2 (k+1) | -- | ||w||^2] of the CGS2 passes.  Block 0,
@@ -429,34 +473,7 @@ __global__ void finish_scale(int k, const double* __restrict__ dh, double* __res
   const double a = (!broke && hn > 0.0) ? 1.0 / hn : 0.0;
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j < len) dst[j] = a * w[j];
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (broke) {
-      est[k] = est[k > 0 ? k - 1 : 0];
-      scal[0] = 0.0;
-      return;
-    }
-    // column k of H (h1 + h2) with the previous rotations applied; the
-    // running entry stays in a register (a store -> load round trip through
-    // global memory per rotation made this serial loop ~300 cycles a step)
-    double* col = Hp + (size_t)k * (k + 3) / 2;
-    double x = dh[0] + dh[k + 1];
-    for (int i = 0; i < k; ++i) {
-      const double y = dh[i + 1] + dh[k + 2 + i];
-      const double c = cs[i], sv = sn[i];
-      col[i] = c * x + sv * y;
-      x = -sv * x + c * y;
-    }
-    const double den = hypot(x, hn);
-    cs[k] = x / den;
-    sn[k] = hn / den;
-    col[k] = den;
-    col[k + 1] = 0.0;
-    g[k + 1] = -sn[k] * g[k];
-    g[k] = cs[k] * g[k];
-    est[k] = fabs(g[k + 1]);
-    scal[0] = a;
-    if (!(hn > 0.0)) flag[0] = k + 1;
-  }
+  if (blockIdx.x == 0) givens_block(k, hn, a, broke, dh, Hp, cs, sn, g, est, scal, flag);
 }
 
 // finish_scale fused with the leaf-block preconditioner of the next step
@@ -494,32 +511,7 @@ finish_scale_pc(int k, const double* __restrict__ dh, double* __restrict__ Hp,
   }
   __syncthreads();
   if (d > 0) chunk_mv(inv + off[blockIdx.x], d, xs, part, uf + b0, 0);
-  if (blockIdx.x == 0 && threadIdx.x == 0 && broke) {
-    est[k] = est[k > 0 ? k - 1 : 0];
-    scal[0] = 0.0;
-  } else if (blockIdx.x == 0 && threadIdx.x == 0) {
-    // column k of H (h1 + h2) with the previous rotations applied; the
-    // running entry stays in a register (a store -> load round trip through
-    // global memory per rotation made this serial loop ~300 cycles a step)
-    double* col = Hp + (size_t)k * (k + 3) / 2;
-    double x = dh[0] + dh[k + 1];
-    for (int i = 0; i < k; ++i) {
-      const double y = dh[i + 1] + dh[k + 2 + i];
-      const double c = cs[i], sv = sn[i];
-      col[i] = c * x + sv * y;
-      x = -sv * x + c * y;
-    }
-    const double den = hypot(x, hn);
-    cs[k] = x / den;
-    sn[k] = hn / den;
-    col[k] = den;
-    col[k + 1] = 0.0;
-    g[k + 1] = -sn[k] * g[k];
-    g[k] = cs[k] * g[k];
-    est[k] = fabs(g[k + 1]);
-    scal[0] = a;
-    if (!(hn > 0.0)) flag[0] = k + 1;
-  }
+  if (blockIdx.x == 0) givens_block(k, hn, a, broke, dh, Hp, cs, sn, g, est, scal, flag);
   if (kd) {   // every CTA has read k: the last one advances it
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -561,10 +553,10 @@ struct Gm {
   // w += sign V c, then dh[off] = ||w||^2 (owned rows, summed over ranks)
   int axpy_norm(const double* V, int64_t ld, int nvec, const double* c, double sign, double* w,
                 int off) {
-    const unsigned g = std::min(nblk(nloc, 256), 148u * 8);
+    const unsigned g = nblk(nloc, kAxRows);
     if ((int64_t)g > part_cap) return set_error(ctx, DDM_ERR_ARG, "gmres part buffer");
-    multi_axpy_norm<<<g, 256, nvec * sizeof(double), s>>>(V, ld, nvec, c, sign, w, nloc, part,
-                                                          ticket_norm, dh + off, nullptr);
+    cgs_axpy<true><<<g, kAxRows * kAxGroups, nvec * sizeof(double), s>>>(
+        V, ld, nvec, c, sign, w, nloc, part, ticket_norm, dh + off, nullptr, 0);
     DDM_CUDA(ctx, cudaGetLastError());
     return allreduce_sum(ctx, dh + off, 1, s);
   }
@@ -575,18 +567,22 @@ struct Gm {
     const int b = nb();
     const int gy = std::min(m + 1, 64);
     if ((int64_t)(m + 1) * b > part_cap) return set_error(ctx, DDM_ERR_ARG, "gmres part buffer");
-    const unsigned ga = std::min(nblk(nloc, 256), 148u * 8);
+    const unsigned ga = nblk(nloc, kAxRows);
+    if ((int64_t)ga > part_cap) return set_error(ctx, DDM_ERR_ARG, "gmres part buffer");
     const size_t shc = (size_t)(m + 1) * sizeof(double);
     multi_dot<<<dim3(b, gy), kDotThreads, 0, s>>>(V, nloc, w, nloc, b, part, ticket, dh, kd, 0);
-    multi_axpy<<<ga, 256, shc, s>>>(V, nloc, 0, dh, -1.0, w, nloc, kd, 0);
+    cgs_axpy<false><<<ga, kAxRows * kAxGroups, shc, s>>>(V, nloc, 0, dh, -1.0, w, nloc, nullptr,
+                                                        nullptr, nullptr, kd, 0);
     multi_dot<<<dim3(b, gy), kDotThreads, 0, s>>>(V, nloc, w, nloc, b, part, ticket, dh, kd, 1);
-    multi_axpy_norm<<<ga, 256, shc, s>>>(V, nloc, 0, dh, -1.0, w, nloc, part, ticket_norm, dh, kd);
+    cgs_axpy<true><<<ga, kAxRows * kAxGroups, shc, s>>>(V, nloc, 0, dh, -1.0, w, nloc, part,
+                                                       ticket_norm, dh, kd, 1);
     DDM_CUDA(ctx, cudaGetLastError());
     return DDM_OK;
   }
   int axpy(const double* V, int64_t ld, int nvec, const double* c, double sign, double* w) {
-    const unsigned g = std::min(nblk(nloc, 256), 148u * 8);
-    multi_axpy<<<g, 256, nvec * sizeof(double), s>>>(V, ld, nvec, c, sign, w, nloc, nullptr, 0);
+    const unsigned g = nblk(nloc, kAxRows);
+    cgs_axpy<false><<<g, kAxRows * kAxGroups, nvec * sizeof(double), s>>>(
+        V, ld, nvec, c, sign, w, nloc, nullptr, nullptr, nullptr, nullptr, 0);
     DDM_CUDA(ctx, cudaGetLastError());
     return DDM_OK;
   }
@@ -756,7 +752,7 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   }
   if (use_pc && mat->kind == 1 && !(dt > 0))
     return set_error(ctx, DDM_ERR_ARG, "poroelastic GMRES needs dt > 0");
-  const int64_t part_need = (int64_t)(m + 2) * 256;
+  const int64_t part_need = std::max<int64_t>((int64_t)(m + 2) * 256, nloc / 64 + 2);
   if (t->gm_part_n < part_need) {
     if (t->gm_part) cudaFree(t->gm_part);
     if ((rc = dalloc(ctx, &t->gm_part, part_need))) return rc;
