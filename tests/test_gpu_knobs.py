@@ -76,6 +76,7 @@ print("RESULT " + json.dumps(out))
     # every library allocation poisoned with NaN / -1 (uninitialised reads
     # surface in the checked results; compute-sanitizer is closed on the pool)
     {"DDM_POISON": "1"},
+    {"DDM_GMRES_DGKS": "1"},
     {"DDM_POISON": "1", "DDM_GMRES_GRAPH": "0", "DDM_P2P_LEAF": "0", "DDM_L2P_BLOCK": "0"},
 ])
 def test_knob_paths_agree_with_oracle(env):
