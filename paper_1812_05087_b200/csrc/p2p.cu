@@ -464,7 +464,11 @@ p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ ite
 // node carry is re-initialised where a range starts).  Slice partials are
 // summed in a fixed order: deterministic, independent of the rank count.
 constexpr int kLeafThreads = 128;
-constexpr int kLeafMaxTg = 64;      // targets per pass (2 per lane, >= 4 slices)
+#ifndef DDM_LEAF_TPL
+#define DDM_LEAF_TPL 2
+#endif
+constexpr int kLT = DDM_LEAF_TPL;           // targets per lane
+constexpr int kLeafMaxTg = 32 * kLT;        // targets per pass (tp <= 32: >= 4 slices)
 constexpr int kLeafMaxPieces = 32;  // ranges per chunk
 constexpr int kLeafMinRec = 16;     // records per slice (at least, where possible)
 #ifndef DDM_LEAF_RMAX
@@ -535,13 +539,13 @@ p2p_leaf_kernel(int leaf_lo, const int4* __restrict__ leaf_info, const int2* __r
   unsigned phase = 0;
   for (int tg0 = 0; tg0 < nt; tg0 += kLeafMaxTg) {
     const int tg = min(kLeafMaxTg, nt - tg0);
-    const int tp = (tg + 1) >> 1, Smax = kLeafThreads / tp;
-    double zx[2], zy[2];
-    P2PAcc acc[2];
+    const int tp = (tg + kLT - 1) / kLT, Smax = kLeafThreads / tp;
+    double zx[kLT], zy[kLT];
+    P2PAcc acc[kLT];
     const int tl0 = tid % tp;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int ti = cs + tg0 + min(2 * tl0 + q, tg - 1);
+    for (int q = 0; q < kLT; ++q) {
+      const int ti = cs + tg0 + min(kLT * tl0 + q, tg - 1);
       zx[q] = __ldg(ex + ti);
       zy[q] = __ldg(ey + ti);
     }
@@ -644,19 +648,19 @@ p2p_leaf_kernel(int leaf_lo, const int4* __restrict__ leaf_info, const int2* __r
         const int a = 1 + (int)(((int64_t)(used - 1) * slice) / S);
         const int b = 1 + (int)(((int64_t)(used - 1) * (slice + 1)) / S);
         if (a < b) {
-          NodeCarry ncr[2];
+          NodeCarry ncr[kLT];
           {
             double sp[kRecStride];
             load_rec_s(sp, recs + (size_t)(a - 1) * kRecStride);
 #pragma unroll
-            for (int q = 0; q < 2; ++q) node_init(ncr[q], zx[q], zy[q], sp);
+            for (int q = 0; q < kLT; ++q) node_init(ncr[q], zx[q], zy[q], sp);
           }
 #pragma unroll 2
           for (int j = a; j < b; ++j) {
             double sp[kRecStride];
             load_rec_s(sp, recs + (size_t)j * kRecStride);
 #pragma unroll
-            for (int q = 0; q < 2; ++q) record_update(acc[q], ncr[q], zx[q], zy[q], sp);
+            for (int q = 0; q < kLT; ++q) record_update(acc[q], ncr[q], zx[q], zy[q], sp);
           }
         }
       }
@@ -665,11 +669,11 @@ p2p_leaf_kernel(int leaf_lo, const int4* __restrict__ leaf_info, const int2* __r
     }
     // ---- slice partials -> per target, summed in slice order
     const int slice = tid / tp, tl = tid - slice * tp;
-    double* red = recs;   // [S][2 tp][3] (<= 256 entries)
+    double* red = recs;   // [S][kLT tp][3] (<= kLT * 128 entries)
     if (slice < S) {
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        double* o = red + ((size_t)slice * 2 * tp + 2 * tl + q) * 3;
+      for (int q = 0; q < kLT; ++q) {
+        double* o = red + ((size_t)slice * kLT * tp + kLT * tl + q) * 3;
         o[0] = acc[q].phi;
         o[1] = acc[q].psi.x;
         o[2] = acc[q].psi.y;
@@ -679,7 +683,7 @@ p2p_leaf_kernel(int leaf_lo, const int4* __restrict__ leaf_info, const int2* __r
     if (tid < tg) {
       P2PAcc tot;
       for (int s2 = 0; s2 < S; ++s2) {
-        const double* o = red + ((size_t)s2 * 2 * tp + tid) * 3;
+        const double* o = red + ((size_t)s2 * kLT * tp + tid) * 3;
         tot.phi += o[0];
         tot.psi.x += o[1];
         tot.psi.y += o[2];
