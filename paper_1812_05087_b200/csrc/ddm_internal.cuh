@@ -225,6 +225,10 @@ struct ddm_tree_s {
   // 128 owned elements (first leaf, leaves, first W entry, W entries)
   double4* leaf_geo = nullptr;    // [nleaves] (z0.x, z0.y, 1/s, has a local expansion)
   double4* w_geo = nullptr;       // [nw] (z_D.x, z_D.y, 1/s_D, 0) of every W entry
+  int2* p2m_runs = nullptr;       // P2M runs (first leaf, leaves) over all leaves
+  int2* p2m_runs_own = nullptr;   // ... over the owned leaves
+  int p2m_nruns = 0, p2m_nruns_own = 0;
+  int p2m_own_lo = -1, p2m_own_hi = -1;
   int4* l2p_runs = nullptr;
   int l2p_nruns = 0;
   int64_t l2p_lo = -1, l2p_hi = -1;   // owned range the runs were built for

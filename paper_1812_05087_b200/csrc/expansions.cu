@@ -57,28 +57,43 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 
 // ------------------------------------------------------------ P2M (a5)
-// Warp per leaf; lane = element of a 32-element round.
+// Warp per RUN of leaves: one leaf (lanes = the elements of a 32-element
+// round, rounds accumulated), or several consecutive small leaves packed into
+// one 32-lane round (their elements are contiguous in sorted order; each lane
+// uses its own leaf's centre and scale) -- leaves of <= 32 elements no longer
+// leave most lanes idle.
 //   alpha_n = (B/s) P_{n-1}
 //   gamma_n = (1/s)[Q P_{n-1} + B((n-1) A P_{n-2} + (n-2) r P_{n-1})]
 // zeta_{1,2} = (z_{1,2} - z0)/s, P_m = zeta2^m - zeta1^m, A = conj(zc - z0)/s - r (zc - z0)/s.
-// Coefficients are produced in chunks of 8 and summed over the elements of
-// the round through a padded [32][17] shared-memory transpose (fixed order).
+// Coefficients are produced in chunks of 8 and summed over each leaf's
+// elements through a padded [32][17] shared-memory transpose, in the same
+// order whether the leaf is packed or not (rows [0, 16) and [16, count) of
+// the leaf, then their sum): results do not depend on the packing.
 template <int PT>
-__device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const int* __restrict__ c_ix,
-                         const int* __restrict__ c_iy, const int* __restrict__ c_start,
-                         const int* __restrict__ c_count, const CellGeom& cg,
-                         const int* __restrict__ perm, const double* __restrict__ D, int ncomp,
-                         const double* __restrict__ ex, const double* __restrict__ ey,
-                         const double* __restrict__ ea, const double* __restrict__ ec,
-                         const double* __restrict__ es, double2* __restrict__ mpole, double2* buf,
-                         int lane, const PoroFar& pf) {
+__device__ void p2m_run(int kk0, int nseg, int p, const int* __restrict__ leaves,
+                        const int* __restrict__ c_level, const int* __restrict__ c_ix,
+                        const int* __restrict__ c_iy, const int* __restrict__ c_start,
+                        const int* __restrict__ c_count, const CellGeom& cg,
+                        const int* __restrict__ perm, const double* __restrict__ D, int ncomp,
+                        const double* __restrict__ ex, const double* __restrict__ ey,
+                        const double* __restrict__ ea, const double* __restrict__ ec,
+                        const double* __restrict__ es, double2* __restrict__ mpole, double2* buf,
+                        int lane, const PoroFar& pf) {
   constexpr int NCH = (pmax<PT>() + 7) / 8;
   const int nchunk = (p + 7) / 8;
-  const int lev = c_level[c];
-  const double s = cg.side(lev);
-  const double is = 1.0 / s;
-  const double2 z0 = cg.centre(lev, c_ix[c], c_iy[c]);
-  const int e0 = c_start[c], ne = c_count[c];
+  // segment table, one leaf per lane (lanes < nseg)
+  int sg_c = 0, sg_start = 0, sg_cnt = 0, sg_lev = 0, sg_ix = 0, sg_iy = 0;
+  if (lane < nseg) {
+    sg_c = leaves[kk0 + lane];
+    sg_start = c_start[sg_c];
+    sg_cnt = c_count[sg_c];
+    sg_lev = c_level[sg_c];
+    sg_ix = c_ix[sg_c];
+    sg_iy = c_iy[sg_c];
+  }
+  const unsigned full = 0xffffffffu;
+  const int e0 = __shfl_sync(full, sg_start, 0);
+  const int ne = __shfl_sync(full, sg_start, nseg - 1) + __shfl_sync(full, sg_cnt, nseg - 1) - e0;
   // lane < 16 owns column `lane` of every chunk:
   // column j < 8 -> alpha slot 8 ch + j, column j >= 8 -> gamma slot 8 ch + j - 8
   double2 acc[NCH];
@@ -87,6 +102,14 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
   for (int r0 = 0; r0 < ne; r0 += 32) {
     const int i = e0 + r0 + lane;
     const bool valid = r0 + lane < ne;
+    // this lane's leaf (packed runs: the segment holding element i)
+    int seg = 0;
+    for (int q = 1; q < nseg; ++q)
+      if (i >= __shfl_sync(full, sg_start, q)) seg = q;
+    const int lev = __shfl_sync(full, sg_lev, seg);
+    const double s = cg.side(lev);
+    const double is = 1.0 / s;
+    const double2 z0 = cg.centre(lev, __shfl_sync(full, sg_ix, seg), __shfl_sync(full, sg_iy, seg));
     double2 B = make_double2(0, 0), Q = B, rr = B, A = B, z1 = B, z2 = B;
     // poroelastic far field: B-part of Phi and Psi~ scaled by
     // fu, plus Wm conj(e) I2 and Wc B I4 in Psi~ (iGC factored out)
@@ -131,7 +154,6 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
     double2 Pm2 = make_double2(0.0, 0.0);   // P_{n-3}
     double2 Pm1 = make_double2(0.0, 0.0);   // P_{n-2}
     double2 Pm = make_double2(0.0, 0.0);    // P_{n-1}
-    const int rows = min(32, ne - r0);
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
       if (ch < nchunk) {
@@ -159,18 +181,31 @@ __device__ void p2m_cell(int c, int p, const int* __restrict__ c_level, const in
         }
         __syncwarp();
         const int col = lane & 15, h0 = (lane >> 4) * 16;
-        double2 sum = make_double2(0.0, 0.0);
-        const int hend = min(rows, h0 + 16);
-        for (int e = h0; e < hend; ++e) sum = cadd(sum, buf[e * 17 + col]);
-        sum.x += __shfl_down_sync(0xffffffffu, sum.x, 16);
-        sum.y += __shfl_down_sync(0xffffffffu, sum.y, 16);
-        acc[ch] = cadd(acc[ch], sum);
+        const int slot = 8 * ch + (lane & 7);
+        for (int q = 0; q < nseg; ++q) {
+          // this segment's rows of the round, halves counted from its start
+          const int sa = __shfl_sync(full, sg_start, q) - e0 - r0;
+          const int sc = __shfl_sync(full, sg_cnt, q);
+          const int lo = max(sa, 0), hi = min(sa + sc, 32);
+          double2 sum = make_double2(0.0, 0.0);
+          const int hb = lo + h0, he = min(hi, hb + 16);
+          for (int e = hb; e < he; ++e) sum = cadd(sum, buf[e * 17 + col]);
+          sum.x += __shfl_down_sync(full, sum.x, 16);
+          sum.y += __shfl_down_sync(full, sum.y, 16);
+          const int cq = __shfl_sync(full, sg_c, q);
+          if (nseg == 1) {
+            acc[ch] = cadd(acc[ch], sum);
+          } else if (lane < 16 && slot < p) {   // packed leaves fit one round
+            mpole[(size_t)cq * 2 * p + (lane < 8 ? 0 : p) + slot] = cadd(make_double2(0.0, 0.0), sum);
+          }
+        }
         __syncwarp();
       }
     }
   }
-  double2* out = mpole + (size_t)c * 2 * p;
-  if (lane < 16) {
+  const int c0 = __shfl_sync(full, sg_c, 0);
+  if (nseg == 1 && lane < 16) {
+    double2* out = mpole + (size_t)c0 * 2 * p;
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
       const int slot = 8 * ch + (lane & 7);
@@ -278,7 +313,8 @@ __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* 
 #endif
 template <int PT>
 __global__ void DDM_P2M_BOUNDS
-p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ c_level,
+p2m_kernel(int nruns, const int2* __restrict__ runs, const int* __restrict__ leaves,
+           const int* __restrict__ c_level,
            const int* __restrict__ c_ix, const int* __restrict__ c_iy,
            const int* __restrict__ c_start, const int* __restrict__ c_count, CellGeom cg,
            int p_rt, const int* __restrict__ perm, const double* __restrict__ D, int ncomp,
@@ -290,9 +326,11 @@ p2m_kernel(int nleaves, const int* __restrict__ leaves, const int* __restrict__ 
   pdl_trigger();
   extern __shared__ double2 p2m_sh[];   // [kPassWarps][32 * 17] transposition buffers
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int k = blockIdx.x * kPassWarps + w; k < nleaves; k += gridDim.x * kPassWarps)
-    p2m_cell<PT>(leaves[k], p, c_level, c_ix, c_iy, c_start, c_count, cg, perm, D, ncomp, ex,
-                 ey, ea, ec, es, mpole, p2m_sh + w * 32 * 17, lane, pf);
+  for (int k = blockIdx.x * kPassWarps + w; k < nruns; k += gridDim.x * kPassWarps) {
+    const int2 rn = runs[k];   // (first leaf, leaves)
+    p2m_run<PT>(rn.x, rn.y, p, leaves, c_level, c_ix, c_iy, c_start, c_count, cg, perm, D, ncomp,
+                ex, ey, ea, ec, es, mpole, p2m_sh + w * 32 * 17, lane, pf);
+  }
 }
 
 // M2M of the non-leaf cells up_list[u0, u1) of ONE level (launched deepest
@@ -1153,7 +1191,8 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
   // D in user order (perm_in = sorted -> user, read through it) or sorted (nullptr)
   const int p = t->p;
   const bool do_p2m = scope != kUpStrad;
-  const int leaf0 = scope == kUpOwn ? t->own_leaf_lo : 0;
+  if (do_p2m && (!t->p2m_runs || t->p2m_own_lo != t->own_leaf_lo || t->p2m_own_hi != t->own_leaf_hi))
+    return set_error(ctx, DDM_ERR_ARG, "internal: P2M runs not prepared (fmm_workspace)");
   const int nlv = scope == kUpOwn ? t->own_leaf_hi - t->own_leaf_lo : t->nleaves;
   const int* ulist = scope == kUpFull ? t->up_list : scope == kUpOwn ? t->up_own : t->up_strad;
   const std::vector<int>& uoff =
@@ -1166,9 +1205,11 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
   do {                                                                                          \
     if (do_p2m && nlv > 0) {                                                                    \
       if ((rc = set_smem(ctx, p2m_kernel<PT>, shp))) return rc;                                 \
-      const int nb = pass_grid(ctx, (const void*)p2m_kernel<PT>, shp, nlv);                     \
+      const int nrun = scope == kUpOwn ? t->p2m_nruns_own : t->p2m_nruns;                       \
+      const int2* rtab = scope == kUpOwn ? t->p2m_runs_own : t->p2m_runs;                       \
+      const int nb = pass_grid(ctx, (const void*)p2m_kernel<PT>, shp, nrun);                    \
       stage_begin(ctx, DDM_ST_P2M, s);                                                          \
-      p2m_kernel<PT><<<nb, kPassWarps * 32, shp, s>>>(nlv, t->leaves + leaf0, t->c_level,       \
+      p2m_kernel<PT><<<nb, kPassWarps * 32, shp, s>>>(nrun, rtab, t->leaves, t->c_level,        \
                                                       t->c_ix, t->c_iy, t->c_start, t->c_count, \
                                                       cg, p, perm_in, D,                        \
                                                       ncomp, t->ex, t->ey, t->ea, t->ec, t->es, \
@@ -1362,6 +1403,53 @@ static int l2p_tables(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
                                                    t->c_level, t->c_ix, t->c_iy, cg, t->leaf_geo,
                                                    t->w_geo);
     DDM_CUDA(ctx, cudaGetLastError());
+  }
+  // P2M runs: consecutive leaves of <= 32 elements packed into one warp round
+  // (DESIGN.md §4.12); a leaf above 32 elements is a run of its own.  For all
+  // leaves (replicated upward pass) and for the owned leaves (sharded pass)
+  if (!t->p2m_runs || t->p2m_own_lo != t->own_leaf_lo || t->p2m_own_hi != t->own_leaf_hi) {
+    std::vector<int> hl(t->nleaves), hc(t->ncells);
+    DDM_CUDA(ctx, cudaMemcpyAsync(hl.data(), t->leaves, t->nleaves * sizeof(int),
+                                  cudaMemcpyDeviceToHost, s));
+    DDM_CUDA(ctx, cudaMemcpyAsync(hc.data(), t->c_count, t->ncells * sizeof(int),
+                                  cudaMemcpyDeviceToHost, s));
+    DDM_CUDA(ctx, cudaStreamSynchronize(s));
+    auto build = [&](int l0, int l1, std::vector<int2>& out) {
+      out.clear();
+      int k = l0;
+      while (k < l1) {
+        const int c = hc[hl[k]];
+        if (c > 32) {
+          out.push_back(make_int2(k, 1));
+          ++k;
+          continue;
+        }
+        int tot = c, m = 1;
+        while (k + m < l1 && hc[hl[k + m]] <= 32 && tot + hc[hl[k + m]] <= 32) tot += hc[hl[k + m++]];
+        out.push_back(make_int2(k, m));
+        k += m;
+      }
+    };
+    std::vector<int2> rf, ro;
+    build(0, t->nleaves, rf);
+    build(t->own_leaf_lo, t->own_leaf_hi, ro);
+    if (t->p2m_runs) cudaFree(t->p2m_runs);
+    if (t->p2m_runs_own) cudaFree(t->p2m_runs_own);
+    t->p2m_runs = t->p2m_runs_own = nullptr;
+    if ((rc = talloc(ctx, &t->p2m_runs, std::max<size_t>(rf.size(), 1), s)) ||
+        (rc = talloc(ctx, &t->p2m_runs_own, std::max<size_t>(ro.size(), 1), s)))
+      return rc;
+    if (!rf.empty())
+      DDM_CUDA(ctx, cudaMemcpyAsync(t->p2m_runs, rf.data(), rf.size() * sizeof(int2),
+                                    cudaMemcpyHostToDevice, s));
+    if (!ro.empty())
+      DDM_CUDA(ctx, cudaMemcpyAsync(t->p2m_runs_own, ro.data(), ro.size() * sizeof(int2),
+                                    cudaMemcpyHostToDevice, s));
+    DDM_CUDA(ctx, cudaStreamSynchronize(s));
+    t->p2m_nruns = (int)rf.size();
+    t->p2m_nruns_own = (int)ro.size();
+    t->p2m_own_lo = t->own_leaf_lo;
+    t->p2m_own_hi = t->own_leaf_hi;
   }
   if (t->l2p_lo != t->own_el_lo || t->l2p_hi != t->own_el_hi) {
     if (t->l2p_runs) cudaFree(t->l2p_runs);
