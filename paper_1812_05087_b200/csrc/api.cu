@@ -206,7 +206,9 @@ static void drop_owned_state(ddm_tree_s* t) {
                   t->ag_send, t->ag_recv, t->ag_lo, t->halo_rng, t->halo_pre, t->dn_own};
     t->dn_own = nullptr;
     if (t->l2p_runs) cudaFree(t->l2p_runs);
+    if (t->l2p_order) cudaFree(t->l2p_order);
     t->l2p_runs = nullptr;
+    t->l2p_order = nullptr;
     t->l2p_nruns = 0;
     t->l2p_lo = t->l2p_hi = -1;
     t->halo_rng = nullptr;

@@ -940,12 +940,16 @@ __device__ __forceinline__ void l2p_eval(int p, double x, double y, bool has_loc
   }
 }
 
+#ifndef DDM_L2P_TMA
+#define DDM_L2P_TMA 1
+#endif
 #ifndef DDM_L2PB_MINB
 #define DDM_L2PB_MINB 8
 #endif
 template <int PT>
 __global__ void __launch_bounds__(kL2PThreads, DDM_L2PB_MINB)
 l2p_block_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int4* __restrict__ runs,
+                 const int* __restrict__ order,
                  const double4* __restrict__ leaf_geo, const double4* __restrict__ w_geo,
                  const int* __restrict__ el_leaf,
                  const int* __restrict__ leaves, const int* __restrict__ c_level,
@@ -963,14 +967,19 @@ l2p_block_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int4* __restrict__
   __shared__ double4 kgeo[kL2PLeaves];   // (z0.x, z0.y, 1/s, has local)
   __shared__ double4 wgeo[kL2PW];        // (z_D.x, z_D.y, 1/s_D, -)
   __shared__ int kcell[kL2PLeaves], kw[kL2PLeaves + 1], wcell[kL2PW];
+  __shared__ __align__(8) unsigned long long l2p_bar;
   const int tid = threadIdx.x;
-  const int64_t i0 = e_lo + (int64_t)blockIdx.x * kL2PThreads;
+#if DDM_L2P_TMA
+  if (tid == 0) mbar_init(smem_u32(&l2p_bar), 1);
+#endif
+  const int rb = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
+  const int64_t i0 = e_lo + (int64_t)rb * kL2PThreads;
   const int64_t i = i0 + tid;
   const bool valid = i < e_hi;
   // the run's descriptor (precomputed per owned range): the staging is two
   // block-wide load rounds -- the leaves' / W cells' ids and geometry, then
   // their coefficients -- independent of the element loads
-  const int4 rd = __ldg(runs + blockIdx.x);
+  const int4 rd = __ldg(runs + rb);
   const int k0 = rd.x, nk = rd.y, w0 = rd.z, nw = rd.w;
   const int k = valid ? __ldg(el_leaf + i) : -1;
   // the element's own data, loaded before the staging (their latency would
@@ -990,6 +999,24 @@ l2p_block_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int4* __restrict__
     }
     __syncthreads();
     pdl_wait();   // the leaves' final locals (L2L)
+#if DDM_L2P_TMA
+    // coefficient rows by 1-D bulk copies (one per leaf / W cell, 2p double2
+    // each) issued by warp 0, completion counted on one mbarrier
+    if (tid < 32) {
+      const unsigned rowb = (unsigned)P2 * sizeof(double2);
+      if (tid == 0) mbar_expect_tx(smem_u32(&l2p_bar), (unsigned)(nk + nw) * rowb);
+      __syncwarp();
+      for (int r = tid; r < nk + nw; r += 32) {
+        if (r < nk)
+          bulk_g2s(smem_u32(shL + (size_t)r * P2), local + (size_t)kcell[r] * P2, rowb,
+                   smem_u32(&l2p_bar));
+        else
+          bulk_g2s(smem_u32(shW + (size_t)(r - nk) * P2), mpole + (size_t)wcell[r - nk] * P2,
+                   rowb, smem_u32(&l2p_bar));
+      }
+    }
+    mbar_wait(smem_u32(&l2p_bar), 0);
+#else
     for (int e = tid; e < nk * P2; e += kL2PThreads) {
       const int kl = e / P2, m = e - kl * P2;
       shL[e] = local[(size_t)kcell[kl] * P2 + m];
@@ -999,6 +1026,7 @@ l2p_block_kernel(int64_t e_lo, int64_t e_hi, int ncomp, const int4* __restrict__
       shW[e] = __ldg(mpole + (size_t)wcell[wl] * P2 + m);
     }
     __syncthreads();
+#endif
   } else {
     pdl_wait();
   }
@@ -1382,13 +1410,21 @@ __global__ void l2p_geo_kernel(int nleaves, int64_t nw, const int* __restrict__ 
 // run r = elements [e_lo + 128 r, ...) of the owned range: (first leaf,
 // leaves, first W entry, W entries)
 __global__ void l2p_runs_kernel(int nruns, int64_t e_lo, int64_t e_hi, const int* __restrict__ el_leaf,
-                                const int* __restrict__ w_off, int4* __restrict__ runs) {
+                                const int* __restrict__ w_off, int4* __restrict__ runs,
+                                int* __restrict__ work) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nruns) return;
   const int64_t a = e_lo + (int64_t)r * kL2PThreads;
   const int64_t b = min(e_hi, a + kL2PThreads) - 1;
   const int k0 = el_leaf[a], k1 = el_leaf[b];
   runs[r] = make_int4(k0, k1 - k0 + 1, w_off[k0], w_off[k1 + 1] - w_off[k0]);
+  // work estimate (series evaluations) of the run, for the launch order
+  int wk = 0;
+  for (int64_t i = a; i <= b; ++i) {
+    const int k = el_leaf[i];
+    wk += 1 + w_off[k + 1] - w_off[k];
+  }
+  work[r] = wk;
 }
 
 static int l2p_tables(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
@@ -1457,11 +1493,33 @@ static int l2p_tables(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     const int64_t ne = t->own_el_hi - t->own_el_lo;
     t->l2p_nruns = (int)((ne + kL2PThreads - 1) / kL2PThreads);
     if ((rc = talloc(ctx, &t->l2p_runs, (size_t)std::max(t->l2p_nruns, 1), s))) return rc;
+    if (t->l2p_order) cudaFree(t->l2p_order);
+    t->l2p_order = nullptr;
     if (t->l2p_nruns > 0) {
+      int* work = nullptr;
+      if ((rc = talloc(ctx, &work, (size_t)t->l2p_nruns, s))) return rc;
       l2p_runs_kernel<<<nblk(t->l2p_nruns, 256), 256, 0, s>>>(t->l2p_nruns, t->own_el_lo,
                                                                t->own_el_hi, t->el_leaf, t->w_off,
-                                                               t->l2p_runs);
+                                                               t->l2p_runs, work);
       DDM_CUDA(ctx, cudaGetLastError());
+      // longest runs first: the launch's tail is short runs
+      static const bool ord_env = [] {
+        const char* e = getenv("DDM_L2P_ORDER");
+        return !(e && e[0] == '0');
+      }();
+      if (ord_env) {
+        std::vector<int> hw(t->l2p_nruns), ord(t->l2p_nruns);
+        DDM_CUDA(ctx, cudaMemcpyAsync(hw.data(), work, hw.size() * sizeof(int),
+                                      cudaMemcpyDeviceToHost, s));
+        DDM_CUDA(ctx, cudaStreamSynchronize(s));
+        for (int r = 0; r < t->l2p_nruns; ++r) ord[r] = r;
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return hw[a] > hw[b]; });
+        if ((rc = talloc(ctx, &t->l2p_order, ord.size(), s))) return rc;
+        DDM_CUDA(ctx, cudaMemcpyAsync(t->l2p_order, ord.data(), ord.size() * sizeof(int),
+                                      cudaMemcpyHostToDevice, s));
+        DDM_CUDA(ctx, cudaStreamSynchronize(s));
+      }
+      DDM_CUDA(ctx, cudaFreeAsync(work, s));
     }
     t->l2p_lo = t->own_el_lo;
     t->l2p_hi = t->own_el_hi;
@@ -1495,6 +1553,7 @@ int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFa
       if ((rc = set_smem(ctx, l2p_block_kernel<PT>, shb))) return rc;                           \
       DDM_CUDA(ctx, launch_pdl(use_pdl(t), l2p_block_kernel<PT>, nbb, kL2PThreads, shb, s,      \
                                (int64_t)lo, (int64_t)hi, ncomp, (const int4*)t->l2p_runs,       \
+                               (const int*)t->l2p_order,                                        \
                                (const double4*)t->leaf_geo, (const double4*)t->w_geo,           \
                                (const int*)t->el_leaf,                                          \
                                (const int*)t->leaves, (const int*)t->c_level,                  \
