@@ -207,6 +207,9 @@ static void drop_owned_state(ddm_tree_s* t) {
     t->dn_own = nullptr;
     if (t->l2p_runs) cudaFree(t->l2p_runs);
     if (t->l2p_order) cudaFree(t->l2p_order);
+    if (t->p2p_leaf_order) cudaFree(t->p2p_leaf_order);
+    t->p2p_leaf_order = nullptr;
+    t->p2m_own_lo = t->p2m_own_hi = -1;
     t->l2p_runs = nullptr;
     t->l2p_order = nullptr;
     t->l2p_nruns = 0;

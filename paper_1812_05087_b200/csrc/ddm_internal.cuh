@@ -230,7 +230,8 @@ struct ddm_tree_s {
   int p2m_nruns = 0, p2m_nruns_own = 0;
   int p2m_own_lo = -1, p2m_own_hi = -1;
   int4* l2p_runs = nullptr;
-  int* l2p_order = nullptr;       // L2P run launch order (longest first), or null
+  int* l2p_order = nullptr;
+  int* p2p_leaf_order = nullptr;  // near-field leaf launch order (owned-relative), or null       // L2P run launch order (longest first), or null
   int l2p_nruns = 0;
   int64_t l2p_lo = -1, l2p_hi = -1;   // owned range the runs were built for
   double* y_near = nullptr;       // [n][2] elastic near field of the owned elements (sorted order)

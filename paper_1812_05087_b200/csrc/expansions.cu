@@ -1486,6 +1486,39 @@ static int l2p_tables(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     t->p2m_nruns_own = (int)ro.size();
     t->p2m_own_lo = t->own_leaf_lo;
     t->p2m_own_hi = t->own_leaf_hi;
+    // near-field leaf blocks longest-first (targets x staged records), so the
+    // launch does not end on a heavy leaf; DDM_P2P_ORDER=0 keeps Morton order
+    if (t->p2p_leaf_order) cudaFree(t->p2p_leaf_order);
+    t->p2p_leaf_order = nullptr;
+    static const bool p2p_ord = [] {
+      const char* e = getenv("DDM_P2P_ORDER");
+      return !(e && e[0] == '0');
+    }();
+    const int nlo = t->own_leaf_hi - t->own_leaf_lo;
+    if (p2p_ord && nlo > 0 && t->leaf_info && t->lr_rng) {
+      std::vector<int4> li(t->nleaves);
+      std::vector<int2> lr(std::max<int64_t>(t->nu, 1));
+      DDM_CUDA(ctx, cudaMemcpyAsync(li.data(), t->leaf_info, li.size() * sizeof(int4),
+                                    cudaMemcpyDeviceToHost, s));
+      if (t->nu > 0)
+        DDM_CUDA(ctx, cudaMemcpyAsync(lr.data(), t->lr_rng, t->nu * sizeof(int2),
+                                      cudaMemcpyDeviceToHost, s));
+      DDM_CUDA(ctx, cudaStreamSynchronize(s));
+      std::vector<int64_t> wk(nlo);
+      std::vector<int> ord(nlo);
+      for (int k = 0; k < nlo; ++k) {
+        const int4 v = li[t->own_leaf_lo + k];
+        int64_t rec = 0;
+        for (int r = v.z; r < v.w; ++r) rec += lr[r].y - lr[r].x + 1;
+        wk[k] = (int64_t)v.y * rec;
+        ord[k] = k;
+      }
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return wk[a] > wk[b]; });
+      if ((rc = talloc(ctx, &t->p2p_leaf_order, (size_t)nlo, s))) return rc;
+      DDM_CUDA(ctx, cudaMemcpyAsync(t->p2p_leaf_order, ord.data(), nlo * sizeof(int),
+                                    cudaMemcpyHostToDevice, s));
+      DDM_CUDA(ctx, cudaStreamSynchronize(s));
+    }
   }
   if (t->l2p_lo != t->own_el_lo || t->l2p_hi != t->own_el_hi) {
     if (t->l2p_runs) cudaFree(t->l2p_runs);

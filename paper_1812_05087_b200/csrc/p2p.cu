@@ -489,7 +489,8 @@ __device__ __forceinline__ void load_rec_s(double (&sp)[kRecStride], const doubl
 }
 
 __global__ void __launch_bounds__(kLeafThreads, DDM_LEAF_MINB)
-p2p_leaf_kernel(int leaf_lo, const int4* __restrict__ leaf_info, const int2* __restrict__ lr_rng,
+p2p_leaf_kernel(int leaf_lo, const int* __restrict__ order, const int4* __restrict__ leaf_info,
+                const int2* __restrict__ lr_rng,
                 const double* __restrict__ srec, const double* __restrict__ ex,
                 const double* __restrict__ ey, const double* __restrict__ ec,
                 const double* __restrict__ es, double gc, int rmax, double* __restrict__ y_near) {
@@ -502,7 +503,7 @@ p2p_leaf_kernel(int leaf_lo, const int4* __restrict__ leaf_info, const int2* __r
   const int tid = threadIdx.x, lane = tid & 31;
   const unsigned bar_a = smem_u32(&bar);
   // (cs, nt, first range, end range) of the leaf
-  const int4 li = __ldg(leaf_info + leaf_lo + blockIdx.x);
+  const int4 li = __ldg(leaf_info + leaf_lo + (order ? __ldg(order + blockIdx.x) : (int)blockIdx.x));
   const int cs = li.x, nt = li.y, rg0 = li.z, rg1 = li.w;
   if (tid == 0) mbar_init(bar_a, 1);
   __syncthreads();
@@ -786,7 +787,8 @@ int launch_p2p_leaf(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, cudaStream_t s) {
                                        (int)shm));
     attr = true;
   }
-  p2p_leaf_kernel<<<nlv, kLeafThreads, shm, s>>>(t->own_leaf_lo, t->leaf_info, t->lr_rng, t->srec,
+  p2p_leaf_kernel<<<nlv, kLeafThreads, shm, s>>>(t->own_leaf_lo, t->p2p_leaf_order, t->leaf_info,
+                                                t->lr_rng, t->srec,
                                                 t->ex, t->ey, t->ec, t->es, gc, rmax, t->y_near);
   DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;
