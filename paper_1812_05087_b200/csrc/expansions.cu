@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "kcommon.cuh"
@@ -57,18 +58,18 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 
 // ------------------------------------------------------------ P2M (a5)
-// Warp per RUN of leaves: one leaf (lanes = the elements of a 32-element
-// round, rounds accumulated), or several consecutive small leaves packed into
-// one 32-lane round (their elements are contiguous in sorted order; each lane
-// uses its own leaf's centre and scale) -- leaves of <= 32 elements no longer
-// leave most lanes idle.
+// Warp per RUN of consecutive whole leaves.  A leaf's
+// elements are cut into half-blocks of 16 (rows [16h, 16h + 16) from the leaf
+// start); the run's half-blocks are processed two per 32-lane round (lane
+// slot = lane / 16), so a leaf of 40 elements takes 3 half-block slots
+// instead of two full rounds.  Each lane uses its own leaf's centre and scale.
 //   alpha_n = (B/s) P_{n-1}
 //   gamma_n = (1/s)[Q P_{n-1} + B((n-1) A P_{n-2} + (n-2) r P_{n-1})]
 // zeta_{1,2} = (z_{1,2} - z0)/s, P_m = zeta2^m - zeta1^m, A = conj(zc - z0)/s - r (zc - z0)/s.
-// Coefficients are produced in chunks of 8 and summed over each leaf's
-// elements through a padded [32][17] shared-memory transpose, in the same
-// order whether the leaf is packed or not (rows [0, 16) and [16, count) of
-// the leaf, then their sum): results do not depend on the packing.
+// Coefficients are produced in chunks of 8 and summed over each half-block
+// through a padded [32][17] shared-memory transpose; a leaf's moments are
+// then (((h_0 + h_1) + h_2) + ...) in half-block order -- the same bits
+// whatever run the leaf is in (replicated vs sharded upward pass).
 template <int PT>
 __device__ void p2m_run(int kk0, int nseg, int p, const int* __restrict__ leaves,
                         const int* __restrict__ c_level, const int* __restrict__ c_ix,
@@ -81,8 +82,10 @@ __device__ void p2m_run(int kk0, int nseg, int p, const int* __restrict__ leaves
                         int lane, const PoroFar& pf) {
   constexpr int NCH = (pmax<PT>() + 7) / 8;
   const int nchunk = (p + 7) / 8;
-  // segment table, one leaf per lane (lanes < nseg)
-  int sg_c = 0, sg_start = 0, sg_cnt = 0, sg_lev = 0, sg_ix = 0, sg_iy = 0;
+  const unsigned full = 0xffffffffu;
+  // segment table, one leaf per lane (lanes < nseg); sg_h0 = the leaf's
+  // first half-block in the run
+  int sg_c = 0, sg_start = 0, sg_cnt = 0, sg_lev = 0, sg_ix = 0, sg_iy = 0, sg_nh = 0;
   if (lane < nseg) {
     sg_c = leaves[kk0 + lane];
     sg_start = c_start[sg_c];
@@ -90,26 +93,42 @@ __device__ void p2m_run(int kk0, int nseg, int p, const int* __restrict__ leaves
     sg_lev = c_level[sg_c];
     sg_ix = c_ix[sg_c];
     sg_iy = c_iy[sg_c];
+    sg_nh = (sg_cnt + 15) >> 4;
   }
-  const unsigned full = 0xffffffffu;
-  const int e0 = __shfl_sync(full, sg_start, 0);
-  const int ne = __shfl_sync(full, sg_start, nseg - 1) + __shfl_sync(full, sg_cnt, nseg - 1) - e0;
-  // lane < 16 owns column `lane` of every chunk:
-  // column j < 8 -> alpha slot 8 ch + j, column j >= 8 -> gamma slot 8 ch + j - 8
+  int sg_h0 = sg_nh;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(full, sg_h0, o);
+    if (lane >= o) sg_h0 += v;
+  }
+  const int NH = __shfl_sync(full, sg_h0, 31);   // half-blocks of the run
+  sg_h0 -= sg_nh;
+  if (lane < nseg && sg_cnt == 0)   // an empty leaf (no half-block): zero moments
+    for (int m = 0; m < 2 * p; ++m) mpole[(size_t)sg_c * 2 * p + m] = make_double2(0.0, 0.0);
+  // lane < 16 owns column `lane` of every chunk (the running sum of the open
+  // leaf): column j < 8 -> alpha slot 8 ch + j, column j >= 8 -> gamma slot 8 ch + j - 8
   double2 acc[NCH];
 #pragma unroll
   for (int q = 0; q < NCH; ++q) acc[q] = make_double2(0.0, 0.0);
-  for (int r0 = 0; r0 < ne; r0 += 32) {
-    const int i = e0 + r0 + lane;
-    const bool valid = r0 + lane < ne;
-    // this lane's leaf (packed runs: the segment holding element i)
+  const int slot2 = lane >> 4, row16 = lane & 15;
+  for (int hb0 = 0; hb0 < NH; hb0 += 2) {
+    const int hb = hb0 + slot2;
+    // this lane's leaf: the last segment with sg_h0 <= hb
     int seg = 0;
     for (int q = 1; q < nseg; ++q)
-      if (i >= __shfl_sync(full, sg_start, q)) seg = q;
+      if (hb >= __shfl_sync(full, sg_h0, q)) seg = q;
+    const int s_start = __shfl_sync(full, sg_start, seg);
+    const int s_cnt = __shfl_sync(full, sg_cnt, seg);
+    const int row = 16 * (hb - __shfl_sync(full, sg_h0, seg)) + row16;
+    const bool valid = hb < NH && row < s_cnt;
+    const int i = s_start + row;
     const int lev = __shfl_sync(full, sg_lev, seg);
     const double s = cg.side(lev);
     const double is = 1.0 / s;
     const double2 z0 = cg.centre(lev, __shfl_sync(full, sg_ix, seg), __shfl_sync(full, sg_iy, seg));
+    // rows of each slot's half-block, and whether it ends its leaf
+    const int nrow = hb < NH ? min(16, s_cnt - (row - row16)) : 0;
+    const bool closes = hb < NH && (row - row16) + 16 >= s_cnt;
     double2 B = make_double2(0, 0), Q = B, rr = B, A = B, z1 = B, z2 = B;
     // poroelastic far field: B-part of Phi and Psi~ scaled by
     // fu, plus Wm conj(e) I2 and Wc B I4 in Psi~ (iGC factored out)
@@ -142,6 +161,11 @@ __device__ void p2m_run(int kk0, int nseg, int p, const int* __restrict__ leaves
       B = cscale(B, is);
       Q = cscale(Q, is);
     }
+    // the two slots' leaves, row counts and closing flags, at lanes < 16
+    const int cA = __shfl_sync(full, sg_c, __shfl_sync(full, seg, 0));
+    const int cB = __shfl_sync(full, sg_c, __shfl_sync(full, seg, 16));
+    const int nA = __shfl_sync(full, nrow, 0), nB = __shfl_sync(full, nrow, 16);
+    const bool clA = __shfl_sync(full, closes, 0), clB = __shfl_sync(full, closes, 16);
     // per-element weights of the power sums (elastic: fu = 1, Wme = Bc = 0):
     //   alpha_n = ub P_{n-1},  gamma_n = y_n P_{n-1} + (n-1) x P_{n-2} [+ Bc (n-1)(n-2)/6 P_{n-3}]
     //   ub = fu B, wr = fu B r, x = fu B A, y_n = Q + (n-2) wr + Wme (y_1 = Q - wr + Wme)
@@ -180,36 +204,32 @@ __device__ void p2m_run(int kk0, int nseg, int p, const int* __restrict__ leaves
           buf[lane * 17 + 8 + j] = gam;
         }
         __syncwarp();
-        const int col = lane & 15, h0 = (lane >> 4) * 16;
+        // column row16 of half-block slot2: rows 16 slot2 + [0, nrow)
+        double2 sum = make_double2(0.0, 0.0);
+        for (int e = 0; e < nrow; ++e) sum = cadd(sum, buf[(16 * slot2 + e) * 17 + row16]);
+        double2 sB;
+        sB.x = __shfl_down_sync(full, sum.x, 16);
+        sB.y = __shfl_down_sync(full, sum.y, 16);
         const int slot = 8 * ch + (lane & 7);
-        for (int q = 0; q < nseg; ++q) {
-          // this segment's rows of the round, halves counted from its start
-          const int sa = __shfl_sync(full, sg_start, q) - e0 - r0;
-          const int sc = __shfl_sync(full, sg_cnt, q);
-          const int lo = max(sa, 0), hi = min(sa + sc, 32);
-          double2 sum = make_double2(0.0, 0.0);
-          const int hb = lo + h0, he = min(hi, hb + 16);
-          for (int e = hb; e < he; ++e) sum = cadd(sum, buf[e * 17 + col]);
-          sum.x += __shfl_down_sync(full, sum.x, 16);
-          sum.y += __shfl_down_sync(full, sum.y, 16);
-          const int cq = __shfl_sync(full, sg_c, q);
-          if (nseg == 1) {
+        if (lane < 16) {
+          const int off = (lane < 8 ? 0 : p) + slot;
+          if (nA > 0) {
             acc[ch] = cadd(acc[ch], sum);
-          } else if (lane < 16 && slot < p) {   // packed leaves fit one round
-            mpole[(size_t)cq * 2 * p + (lane < 8 ? 0 : p) + slot] = cadd(make_double2(0.0, 0.0), sum);
+            if (clA) {
+              if (slot < p) mpole[(size_t)cA * 2 * p + off] = acc[ch];
+              acc[ch] = make_double2(0.0, 0.0);
+            }
+          }
+          if (nB > 0) {
+            acc[ch] = cadd(acc[ch], sB);
+            if (clB) {
+              if (slot < p) mpole[(size_t)cB * 2 * p + off] = acc[ch];
+              acc[ch] = make_double2(0.0, 0.0);
+            }
           }
         }
         __syncwarp();
       }
-    }
-  }
-  const int c0 = __shfl_sync(full, sg_c, 0);
-  if (nseg == 1 && lane < 16) {
-    double2* out = mpole + (size_t)c0 * 2 * p;
-#pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) {
-      const int slot = 8 * ch + (lane & 7);
-      if (ch < nchunk && slot < p) out[(lane < 8 ? 0 : p) + slot] = acc[ch];
     }
   }
 }
@@ -1134,7 +1154,20 @@ int set_smem(ddm_ctx_s* ctx, K kernel, size_t shm) {
   return DDM_OK;
 }
 
-int pass_grid(ddm_ctx_s* ctx, const void* kernel, size_t shm, int work) {
+// integer environment knob, read once per name
+static int env_int(const char* name, int dflt) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::string, int>> seen;
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& kv : seen)
+    if (kv.first == name) return kv.second;
+  const char* e = getenv(name);
+  const int v = e ? atoi(e) : dflt;
+  seen.emplace_back(name, v);
+  return v;
+}
+
+int pass_grid(ddm_ctx_s* ctx, const void* kernel, size_t shm, int work, int kcap = -1) {
   int per_sm = -1, nsm = 148;
   {
     std::lock_guard<std::mutex> lk(g_cfg_mu);
@@ -1161,7 +1194,7 @@ int pass_grid(ddm_ctx_s* ctx, const void* kernel, size_t shm, int work) {
     const char* e = getenv("DDM_PASS_BLOCKS_PER_SM");
     return e ? atoi(e) : -1;
   }();
-  const int cap = env_cap >= 0 ? env_cap : (ctx->serial ? 0 : 2);
+  const int cap = (kcap >= 0 && !ctx->serial) ? kcap : env_cap >= 0 ? env_cap : (ctx->serial ? 0 : 2);
   if (cap > 0) per_sm = std::min(per_sm, cap);
   return std::max(1, std::min(std::max(per_sm, 1) * nsm, by_work));
 }
@@ -1235,7 +1268,7 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
       if ((rc = set_smem(ctx, p2m_kernel<PT>, shp))) return rc;                                 \
       const int nrun = scope == kUpOwn ? t->p2m_nruns_own : t->p2m_nruns;                       \
       const int2* rtab = scope == kUpOwn ? t->p2m_runs_own : t->p2m_runs;                       \
-      const int nb = pass_grid(ctx, (const void*)p2m_kernel<PT>, shp, nrun);                    \
+      const int nb = pass_grid(ctx, (const void*)p2m_kernel<PT>, shp, nrun, env_int("DDM_P2M_CAP", -1)); \
       stage_begin(ctx, DDM_ST_P2M, s);                                                          \
       p2m_kernel<PT><<<nb, kPassWarps * 32, shp, s>>>(nrun, rtab, t->leaves, t->c_level,        \
                                                       t->c_ix, t->c_iy, t->c_start, t->c_count, \
@@ -1343,7 +1376,7 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \
     if ((rc = set_smem(ctx, m2l_kernel<PT>, shm))) return rc;                                   \
-    const int nb = pass_grid(ctx, (const void*)m2l_kernel<PT>, shm, c1 - c0);                   \
+    const int nb = pass_grid(ctx, (const void*)m2l_kernel<PT>, shm, c1 - c0, env_int("DDM_M2L_CAP", -1)); \
     stage_begin(ctx, DDM_ST_M2L, s);                                                            \
     DDM_CUDA(ctx, launch_pdl(use_pdl(t), m2l_kernel<PT>, nb, kPassWarps * 32, shm, s, c0, c1,              \
                              (const int*)cl, (int64_t)t->own_el_lo, (int64_t)t->own_el_hi,     \
@@ -1440,9 +1473,10 @@ static int l2p_tables(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
                                                    t->w_geo);
     DDM_CUDA(ctx, cudaGetLastError());
   }
-  // P2M runs: consecutive leaves of <= 32 elements packed into one warp round
-  // (DESIGN.md §4.12); a leaf above 32 elements is a run of its own.  For all
-  // leaves (replicated upward pass) and for the owned leaves (sharded pass)
+  // P2M runs: consecutive whole leaves of at most DDM_P2M_RUN_HB half-blocks
+  // of 16 elements in all (a larger leaf is a run of its own; DESIGN.md
+  // §4.12).  For all leaves (replicated upward pass) and for the owned leaves
+  // (sharded pass)
   if (!t->p2m_runs || t->p2m_own_lo != t->own_leaf_lo || t->p2m_own_hi != t->own_leaf_hi) {
     std::vector<int> hl(t->nleaves), hc(t->ncells);
     DDM_CUDA(ctx, cudaMemcpyAsync(hl.data(), t->leaves, t->nleaves * sizeof(int),
@@ -1453,15 +1487,11 @@ static int l2p_tables(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     auto build = [&](int l0, int l1, std::vector<int2>& out) {
       out.clear();
       int k = l0;
+      const int hbmax = env_int("DDM_P2M_RUN_HB", 8);   // half-blocks per run (at most)
+      auto nh = [&](int kk) { return (hc[hl[kk]] + 15) / 16; };
       while (k < l1) {
-        const int c = hc[hl[k]];
-        if (c > 32) {
-          out.push_back(make_int2(k, 1));
-          ++k;
-          continue;
-        }
-        int tot = c, m = 1;
-        while (k + m < l1 && hc[hl[k + m]] <= 32 && tot + hc[hl[k + m]] <= 32) tot += hc[hl[k + m++]];
+        int tot = nh(k), m = 1;
+        while (k + m < l1 && m < 32 && tot + nh(k + m) <= hbmax) tot += nh(k + m++);
         out.push_back(make_int2(k, m));
         k += m;
       }
