@@ -361,6 +361,11 @@ def run_ours(args):
                         "traffic": _ncu_traffic("p2p_leaf_kernel"),
                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one "
                                           "ncu --set full capture (profiles/ncu_traffic.json)",
+                        "traffic_note": "algorithmic: 80-B source records once (~85 MB) + targets "
+                                        "(~48 MB); leaf CTAs launched heaviest-first re-read "
+                                        "shared U-list records from DRAM (~200 MB; 127 MB in "
+                                        "Morton order, DDM_P2P_ORDER=0, 1.2 % slower step): "
+                                        "the kernel is fp64-bound, ~0.34 TB/s of DRAM",
                         "peak_source": "measured DFMA-chain probe (ddm_probe_fp64) on this GPU",
                         "flop_per_pair": FLOP_PER_PAIR,
                         "fp64_pipe_frac": (owned_pairs * FP64_INSTR_PER_PAIR / (p2p_ms * 1e-3)

@@ -19,6 +19,7 @@
 // Every kernel is a template on the expansion order PT (PT = 0: runtime p) so
 // that, for the instantiated orders, inner loops unroll and loads pipeline.
 #include <algorithm>
+#include <functional>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -1520,12 +1521,12 @@ static int l2p_tables(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     // launch does not end on a heavy leaf; DDM_P2P_ORDER=0 keeps Morton order
     if (t->p2p_leaf_order) cudaFree(t->p2p_leaf_order);
     t->p2p_leaf_order = nullptr;
-    static const bool p2p_ord = [] {
-      const char* e = getenv("DDM_P2P_ORDER");
-      return !(e && e[0] == '0');
-    }();
+    // 1: by work; 2: by work in power-of-two classes, Morton order within a
+    // class (keeps neighbouring leaves, which share source records in L2,
+    // close in launch order); 3: the heaviest tenth first, then Morton order
+    const int p2p_ord = env_int("DDM_P2P_ORDER", 1);
     const int nlo = t->own_leaf_hi - t->own_leaf_lo;
-    if (p2p_ord && nlo > 0 && t->leaf_info && t->lr_rng) {
+    if (p2p_ord > 0 && nlo > 0 && t->leaf_info && t->lr_rng) {
       std::vector<int4> li(t->nleaves);
       std::vector<int2> lr(std::max<int64_t>(t->nu, 1));
       DDM_CUDA(ctx, cudaMemcpyAsync(li.data(), t->leaf_info, li.size() * sizeof(int4),
@@ -1542,6 +1543,14 @@ static int l2p_tables(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
         for (int r = v.z; r < v.w; ++r) rec += lr[r].y - lr[r].x + 1;
         wk[k] = (int64_t)v.y * rec;
         ord[k] = k;
+      }
+      if (p2p_ord == 2) {
+        for (auto& v : wk) v = v > 0 ? 63 - __builtin_clzll((unsigned long long)v) : 0;
+      } else if (p2p_ord == 3) {
+        std::vector<int64_t> srt(wk);
+        std::nth_element(srt.begin(), srt.begin() + nlo / 10, srt.end(), std::greater<int64_t>());
+        const int64_t thr = srt[nlo / 10];
+        for (auto& v : wk) v = v >= thr ? 1 : 0;
       }
       std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return wk[a] > wk[b]; });
       if ((rc = talloc(ctx, &t->p2p_leaf_order, (size_t)nlo, s))) return rc;
