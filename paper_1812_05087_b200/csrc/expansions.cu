@@ -1488,8 +1488,15 @@ static int l2p_tables(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     auto build = [&](int l0, int l1, std::vector<int2>& out) {
       out.clear();
       int k = l0;
-      const int hbmax = env_int("DDM_P2M_RUN_HB", 8);   // half-blocks per run (at most)
       auto nh = [&](int kk) { return (hc[hl[kk]] + 15) / 16; };
+      // half-blocks per run (at most): up to 8 while that leaves >= 4 runs per
+      // resident warp of the GPU (config 5), 2 = one round on small trees
+      // (latency bound: one run per warp)
+      int64_t tot_hb = 0;
+      for (int kk = l0; kk < l1; ++kk) tot_hb += nh(kk);
+      const int hb_env = env_int("DDM_P2M_RUN_HB", 0);
+      const int hbmax = hb_env > 0 ? hb_env
+                                   : (int)std::min<int64_t>(8, std::max<int64_t>(2, tot_hb / (4 * 148 * 16)));
       while (k < l1) {
         int tot = nh(k), m = 1;
         while (k + m < l1 && m < 32 && tot + nh(k + m) <= hbmax) tot += nh(k + m++);
