@@ -192,6 +192,140 @@ cgs_axpy(const double* __restrict__ V, int64_t ld, int nvec, const double* __res
   }
 }
 
+// Row-blocked CGS passes of the captured Arnoldi step:
+// a CTA of 512 threads owns 512 consecutive rows (thread = row) and ALL k+1
+// basis vectors, so w is read once per pass and -- in the fused kernel -- the
+// first pass's update w -= V c and the second pass's dots V^T w share one
+// sweep over the CTA's rows of V (the dots re-read the rows from L2).
+// Dots: groups of 8 vectors with 32 loads in flight per thread, a warp
+// reduce-scatter (9 shuffles for 8 sums), the 32 warps' sums added in warp
+// order into one partial per (vector, CTA); the last CTA (ticket) sums each
+// vector's <= 128 partials in CTA order.  Deterministic.
+constexpr int kRowT = 512, kRowsCta = kRowT, kRowMaxCta = 128, kRowChunk = 256;
+
+// 8 per-lane values -> lane l holds the warp sum of value
+// v = 4 ((l >> 4) & 1) + 2 ((l >> 3) & 1) + ((l >> 2) & 1)
+__device__ __forceinline__ double warp_rs8(const double (&a)[8], int lane) {
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+  double b[4], c[2];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const double send = h16 ? a[v] : a[v + 4];
+    b[v] = (h16 ? a[v + 4] : a[v]) + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int v = 0; v < 2; ++v) {
+    const double send = h8 ? b[v] : b[v + 2];
+    c[v] = (h8 ? b[v + 2] : b[v]) + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const double send = h4 ? c[0] : c[1];
+  double d = (h4 ? c[1] : c[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
+  d += __shfl_xor_sync(0xffffffffu, d, 2);
+  d += __shfl_xor_sync(0xffffffffu, d, 1);
+  return d;
+}
+
+// MODE 0: out = V^T w (pass 0 dots -> dh[0 .. k]).
+// MODE 1: w -= V c with c = dh[0 .. k], then out = V^T w -> dh[k+1 .. 2k+1].
+// (The second update + norm stays on cgs_axpy: a row-blocked version measured
+// slower, config 3 39.2 -> 41.0 ms.)
+template <int MODE>
+__global__ void __launch_bounds__(kRowT)
+cgs_rows(const double* __restrict__ V, int64_t ld, int64_t len, double* __restrict__ w,
+         const int* __restrict__ kd, double* __restrict__ dh, double* __restrict__ part,
+         unsigned* __restrict__ ticket) {
+  __shared__ double red[kRowT / 32][kRowChunk];   // per-warp sums of a chunk of vectors
+  __shared__ bool last;
+  const int k = *kd, nvec = k + 1, nb = gridDim.x;
+  const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
+  const int64_t j = (int64_t)blockIdx.x * kRowsCta + t;
+  const bool ok = j < len;
+  const double* Vj = V + (ok ? j : 0);
+  double wr;
+  if constexpr (MODE > 0) {
+    const double* sc = dh;   // pass-0 coefficients (broadcast loads)
+    double a0 = 0.0, a1 = 0.0;
+    int i = 0;
+#pragma unroll 8
+    for (; i + 1 < nvec; i += 2) {
+      a0 = fma(__ldg(Vj + (int64_t)i * ld), __ldg(sc + i), a0);
+      a1 = fma(__ldg(Vj + (int64_t)(i + 1) * ld), __ldg(sc + i + 1), a1);
+    }
+    if (i < nvec) a0 = fma(__ldg(Vj + (int64_t)i * ld), __ldg(sc + i), a0);
+    wr = 0.0;
+    if (ok) {
+      wr = w[j] - (a0 + a1);
+      w[j] = wr;
+    }
+  } else {
+    wr = ok ? w[j] : 0.0;
+  }
+  if (!ok) wr = 0.0;
+  double* out = dh + (MODE == 1 ? nvec : 0);
+  const int vsel = 4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1);
+  for (int c0 = 0; c0 < nvec; c0 += kRowChunk) {   // chunks of vectors (one for k < 256)
+    const int c1 = min(nvec, c0 + kRowChunk);
+    // groups of 8 vectors, four groups' loads in flight at once
+    for (int g0 = c0; g0 < c1; g0 += 32) {
+      double a[4][8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int i = g0 + 8 * q + v;
+          a[q][v] = i < c1 ? __ldg(Vj + (int64_t)i * ld) : 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) a[q][v] *= wr;
+        const double d = warp_rs8(a[q], lane);
+        const int i = g0 + 8 * q + vsel;
+        if ((lane & 3) == 0 && i < c1) red[wp][i - c0] = d;
+      }
+    }
+    __syncthreads();
+    for (int i = c0 + t; i < c1; i += kRowT) {
+      double sum = 0.0;
+#pragma unroll
+      for (int q = 0; q < kRowT / 32; ++q) sum += red[q][i - c0];
+      part[(int64_t)i * nb + blockIdx.x] = sum;
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == (unsigned)(nb - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    // warp wp: vectors wp + NW r; lane: CTAs lane + 32 q (4 vectors' loads
+    // in flight at once)
+    constexpr int NW = kRowT / 32, Q = kRowMaxCta / 32;
+    for (int r0 = 0; wp + NW * r0 < nvec; r0 += 4) {
+      double v[4][Q];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int i = wp + NW * (r0 + r), b = lane + 32 * q;
+          v[r][q] = (i < nvec && b < nb) ? __ldcg(part + (int64_t)i * nb + b) : 0.0;
+        }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        double sum = v[r][0];
+#pragma unroll
+        for (int q = 1; q < Q; ++q) sum += v[r][q];
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const int i = wp + NW * (r0 + r);
+        if (lane == 0 && i < nvec) out[i] = sum;
+      }
+    }
+    if (t == 0) *ticket = 0u;
+  }
+}
+
 __global__ void sub_scale(const double* __restrict__ b, const double* __restrict__ w,
                           double* __restrict__ r, int64_t len) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -607,6 +741,26 @@ struct Gm {
     // the device (eta^2 = dgks_eta2: the second pass runs only when the
     // first cancelled most of ||w||^2); dgks_eta2 = 0 keeps plain CGS2
     const int use_dgks = dgks_eta2 > 0.0 ? 1 : 0;
+    static const int rows_env = [] {
+      const char* e = getenv("DDM_GMRES_ROWS");
+      return e ? atoi(e) : 1;
+    }();
+    const int nbr = (int)((nloc + kRowsCta - 1) / kRowsCta);
+    // (small systems keep the vector-parallel kernels: a few row CTAs cannot
+    // keep enough loads in flight)
+    if (rows_env && !use_dgks && nbr >= 32 && nbr <= kRowMaxCta && (int64_t)(m + 1) * nbr <= part_cap) {
+      // row-blocked: dots, fused (update + second-pass dots), update + norm
+      if (getenv("DDM_GMRES_TRACE")) fprintf(stderr, "[gmres] row-blocked CGS2, %d CTAs, m %d\n", nbr, m);
+      if (rows_env == 2)
+        multi_dot<<<dim3(b, gy), kDotThreads, 0, s>>>(V, nloc, w, nloc, b, part, ticket, dh, kd, 0);
+      else
+        cgs_rows<0><<<nbr, kRowT, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket);
+      cgs_rows<1><<<nbr, kRowT, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket);
+      cgs_axpy<true><<<ga, kAxRows * kAxGroups, shc, s>>>(V, nloc, 0, dh, -1.0, w, nloc, part,
+                                                         ticket_norm, dh, kd, 1, 0.0);
+      DDM_CUDA(ctx, cudaGetLastError());
+      return DDM_OK;
+    }
     multi_dot<<<dim3(b, gy), kDotThreads, 0, s>>>(V, nloc, w, nloc, b, part, ticket, dh, kd, 0);
     if (use_dgks)
       cgs_axpy<true><<<ga, kAxRows * kAxGroups, shc, s>>>(V, nloc, 0, dh, -1.0, w, nloc, part,
@@ -616,6 +770,10 @@ struct Gm {
                                                           nullptr, nullptr, kd, 0);
     multi_dot<<<dim3(b, gy), kDotThreads, 0, s>>>(V, nloc, w, nloc, b, part, ticket, dh, kd, 1,
                                                   use_dgks);
+#ifdef DDM_EXP_DOT2   // timing experiment: the second-pass dots twice
+    multi_dot<<<dim3(b, gy), kDotThreads, 0, s>>>(V, nloc, w, nloc, b, part, ticket, dh, kd, 1,
+                                                  use_dgks);
+#endif
     cgs_axpy<true><<<ga, kAxRows * kAxGroups, shc, s>>>(V, nloc, 0, dh, -1.0, w, nloc, part,
                                                        ticket_norm, dh, kd, 1, dgks_eta2);
     DDM_CUDA(ctx, cudaGetLastError());
@@ -794,7 +952,8 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   }
   if (use_pc && mat->kind == 1 && !(dt > 0))
     return set_error(ctx, DDM_ERR_ARG, "poroelastic GMRES needs dt > 0");
-  const int64_t part_need = std::max<int64_t>((int64_t)(m + 2) * 256, 2 * (nloc / 64 + 2));
+  const int64_t part_need = std::max<int64_t>((int64_t)(m + 2) * std::max<int64_t>(256, nloc / kRowsCta + 1),
+                                              2 * (nloc / 64 + 2));
   if (t->gm_part_n < part_need) {
     if (t->gm_part) cudaFree(t->gm_part);
     if ((rc = dalloc(ctx, &t->gm_part, part_need))) return rc;

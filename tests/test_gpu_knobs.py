@@ -78,6 +78,8 @@ print("RESULT " + json.dumps(out))
     {"DDM_POISON": "1"},
     {"DDM_GMRES_DGKS": "1"},
     {"DDM_POISON": "1", "DDM_GMRES_GRAPH": "0", "DDM_P2P_LEAF": "0", "DDM_L2P_BLOCK": "0"},
+    # vector-parallel CGS kernels instead of the row-blocked ones
+    {"DDM_GMRES_ROWS": "0", "DDM_P2P_ORDER": "0", "DDM_L2P_ORDER": "0"},
 ])
 def test_knob_paths_agree_with_oracle(env):
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=dict(os.environ, **env),
