@@ -222,6 +222,19 @@ int ddm_history_apply(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, d
 int ddm_history_rhs(ddm_ctx_t ctx, ddm_tree_t tree, const ddm_material* mat, double dt, int h,
                     const double* D_hist, const double* b, double* rhs, int mode, void* stream);
 
+/* GMRES initial guess for step h of the time marching (not part of the
+ * paper's method, which solves every step from its own start; DESIGN.md §4.7c:
+ * it only changes the iteration count, every step is still solved to the
+ * same true residual).  x = polynomial extrapolation in time of the previous
+ * solutions: order 3: 4 D^{h-1} - 6 D^{h-2} + 4 D^{h-3} - D^{h-4}; 2:
+ * 3 (D^{h-1} - D^{h-2}) + D^{h-3}; 1: 2 D^{h-1} - D^{h-2}; 0: D^{h-1}; the
+ * order is lowered to h - 1 while fewer steps exist; h = 0 -> x = 0.
+ * D_hist [device] [h][len] (D^0 .. D^{h-1}, only read), x [device] [len],
+ * written.  Errors: h < 0, len < 0, order < 0, NULL x (or NULL D_hist with
+ * h > 0) -> DDM_ERR_ARG. */
+int ddm_march_guess(ddm_ctx_t ctx, int h, const double* D_hist, int64_t len, int order, double* x,
+                    void* stream);
+
 /* GMRES (reading R11): solve A(dt) x = b with classical
  * Gram-Schmidt Arnoldi (second pass when the first cancels more than half of
  * ||w||^2), Givens rotations, restart `restart`, relative tolerance tol on

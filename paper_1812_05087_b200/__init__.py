@@ -15,6 +15,7 @@ from .api import (  # noqa: F401
     gmres_solve,
     history_apply,
     history_rhs,
+    march_guess,
     material,
     material_from_dict,
     matvec,

@@ -76,6 +76,7 @@ ddm_history_apply = _proto("ddm_history_apply", _i, _vp, _vp, C.POINTER(Material
                            _dp, _i, _vp)
 ddm_history_rhs = _proto("ddm_history_rhs", _i, _vp, _vp, C.POINTER(Material), _d, _i, _dp, _dp,
                          _dp, _i, _vp)
+ddm_march_guess = _proto("ddm_march_guess", _i, _vp, _i, _dp, _i64, _i, _dp, _vp)
 ddm_gmres_solve = _proto("ddm_gmres_solve", _i, _vp, _vp, C.POINTER(Material), _d, _dp, _dp, _d,
                          _i, _i, _i, C.POINTER(_i), C.POINTER(_d), _vp)
 ddm_precond_apply = _proto("ddm_precond_apply", _i, _vp, _vp, C.POINTER(Material), _d, _dp, _dp,
@@ -91,6 +92,6 @@ ddm_stage_times = _proto("ddm_stage_times", _i, _vp, C.POINTER(_d))
 EXPORTED = ["ddm_version", "ddm_last_error", "ddm_nccl_unique_id", "ddm_ctx_create",
             "ddm_ctx_destroy", "ddm_build_tree", "ddm_tree_free", "ddm_tree_counts",
             "ddm_tree_export", "ddm_tree_partition", "ddm_split_costs", "ddm_matvec", "ddm_matvec_sim", "ddm_shard_owner",
-            "ddm_history_apply", "ddm_history_rhs", "ddm_gmres_solve", "ddm_precond_apply",
+            "ddm_history_apply", "ddm_history_rhs", "ddm_march_guess", "ddm_gmres_solve", "ddm_precond_apply",
             "ddm_farfield_rhs", "ddm_sif", "ddm_tip_growth",
             "ddm_set_profiling", "ddm_stage_times", "ddm_tree_build_times"]

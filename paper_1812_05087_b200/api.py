@@ -220,6 +220,16 @@ def history_rhs(ctx, tree, mat, dt: float, D_hist: torch.Tensor, b: torch.Tensor
     return rhs
 
 
+def march_guess(ctx, D_hist: torch.Tensor, order: int, x: torch.Tensor, stream=None) -> torch.Tensor:
+    """ddm_march_guess: x = polynomial extrapolation (order <= 3) of the last
+    solutions in D_hist [h, ...] (h = 0 -> x = 0)."""
+    h = D_hist.shape[0]
+    ptr = _dev(D_hist, "D_hist") if h > 0 else 0
+    ctx.check(L.ddm_march_guess(ctx._h, int(h), ptr, int(x.numel()), int(order), _dev(x, "x"),
+                                _stream_ptr(stream)))
+    return x
+
+
 def _pc_flags(precond) -> int:
     if precond is None or precond is False:
         return L.GMRES_NO_PRECOND

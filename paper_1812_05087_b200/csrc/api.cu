@@ -768,6 +768,27 @@ __global__ void sub_kernel(int64_t len, const double* a, const double* __restric
   if (i < len) out[i] = a[i] - b[i];
 }
 
+// GMRES initial guess of step h of the march: polynomial extrapolation in
+// time of D^{h-1} .. D^{h-1-q} (q = order, lowered while fewer steps exist),
+// each product and sum rounded separately in the listed order
+__global__ void march_guess_kernel(int64_t len, int q, const double* __restrict__ d1,
+                                   const double* __restrict__ d2, const double* __restrict__ d3,
+                                   const double* __restrict__ d4, double* __restrict__ x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  double v;
+  if (q == 3)        // 4 D1 - 6 D2 + 4 D3 - D4
+    v = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(4.0, d1[i]), __dmul_rn(6.0, d2[i])),
+                            __dmul_rn(4.0, d3[i])), d4[i]);
+  else if (q == 2)   // 3 (D1 - D2) + D3
+    v = __dadd_rn(__dmul_rn(__dsub_rn(d1[i], d2[i]), 3.0), d3[i]);
+  else if (q == 1)   // 2 D1 - D2
+    v = __dsub_rn(__dmul_rn(d1[i], 2.0), d2[i]);
+  else
+    v = d1[i];
+  x[i] = v;
+}
+
 __global__ void axpy_kernel(int64_t len, const double* __restrict__ x, double* __restrict__ y) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < len) y[i] += x[i];
@@ -835,6 +856,23 @@ int ddm_history_rhs(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double
   }
   cudaFreeAsync(r, s);
   return rc;
+}
+
+int ddm_march_guess(ddm_ctx_t ctx, int h, const double* D_hist, int64_t len, int order,
+                    double* x, void* stream) {
+  if (!ctx) return DDM_ERR_ARG;
+  if (h < 0 || len < 0 || order < 0 || !x || (h > 0 && !D_hist))
+    return set_error(ctx, DDM_ERR_ARG, "march_guess: bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (len == 0) return DDM_OK;
+  if (h == 0) {
+    DDM_CUDA(ctx, cudaMemsetAsync(x, 0, (size_t)len * sizeof(double), s));
+    return DDM_OK;
+  }
+  const int q = std::min(order, h - 1);
+  auto prev = [&](int j) { return D_hist + (int64_t)(h - 1 - std::min(j, h - 1)) * len; };
+  march_guess_kernel<<<nblk(len, 256), 256, 0, s>>>(len, q, prev(0), prev(1), prev(2), prev(3), x);
+  return cuda_error_if(ctx, cudaGetLastError(), "march_guess_kernel");
 }
 
 int ddm_precond_apply(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double dt,

@@ -14,17 +14,20 @@ from . import api
 
 def march(ctx, tree, mat, dt: float, b: torch.Tensor, steps: int, tol: float = 1e-10,
           restart: int = 2000, max_iter: int = 10000, history_mode: str = "fmm",
-          warm_start="extrap3", stream=None):
+          warm_start="extrap3", stream=None, timing: bool = False):
     """Returns (D, stats): D [steps, n, 3] device tensor of the per-step
-    solutions D^0..D^{steps-1}; stats = per-step dicts (iters, rel_resid,
-    history_s, gmres_s) with host wall times around synchronised calls.
-    warm_start: GMRES initial guess -- polynomial extrapolation in time of
-    the previous solutions, "extrap3" (cubic, 4 D^{h-1} - 6 D^{h-2} +
-    4 D^{h-3} - D^{h-4}, lower orders while fewer steps exist), "extrap2"
-    (quadratic), "extrap" (linear); True / "prev" (D^{h-1}); False (zero).
-    The guess only changes the iteration count: every step is solved to the
-    same relative residual.  Config 4, 200 steps: 21 721 GMRES iterations
-    from D^{h-1}, 17 609 linear, 11 892 quadratic, 10 085 cubic."""
+    solutions D^0..D^{steps-1}; stats = per-step dicts (iters, rel_resid;
+    with timing=True also history_s, gmres_s: host wall times around calls
+    that are then synchronised -- measurement only, the march itself only
+    waits where GMRES reads its residuals).
+    warm_start: GMRES initial guess (ddm_march_guess) -- polynomial
+    extrapolation in time of the previous solutions, "extrap3" (cubic,
+    4 D^{h-1} - 6 D^{h-2} + 4 D^{h-3} - D^{h-4}, lower orders while fewer steps
+    exist), "extrap2" (quadratic), "extrap" (linear); True / "prev" (D^{h-1});
+    False (zero).  The guess only changes the iteration count: every step is
+    solved to the same relative residual.  Config 4, 200 steps: 21 721 GMRES
+    iterations from D^{h-1}, 17 609 linear, 11 892 quadratic, 10 085 cubic."""
+    order = {"extrap3": 3, "extrap2": 2, "extrap": 1}.get(warm_start, 0 if warm_start else -1)
     n = tree.n
     D = torch.zeros((steps, n, 3), dtype=torch.float64, device=b.device)
     rhs = torch.empty_like(b)
@@ -32,19 +35,16 @@ def march(ctx, tree, mat, dt: float, b: torch.Tensor, steps: int, tol: float = 1
     for h in range(steps):
         t0 = time.perf_counter()
         api.history_rhs(ctx, tree, mat, dt, D[:h], b, rhs, mode=history_mode, stream=stream)
-        torch.cuda.synchronize()
+        if timing:
+            torch.cuda.synchronize()
         t1 = time.perf_counter()
-        if warm_start == "extrap3" and h > 3:   # cubic extrapolation
-            D[h].copy_(4.0 * D[h - 1] - 6.0 * D[h - 2] + 4.0 * D[h - 3] - D[h - 4])
-        elif warm_start in ("extrap2", "extrap3") and h > 2:   # quadratic extrapolation
-            torch.add(torch.sub(D[h - 1], D[h - 2]) * 3.0, D[h - 3], out=D[h])
-        elif warm_start in ("extrap", "extrap2", "extrap3") and h > 1:
-            torch.sub(D[h - 1] * 2.0, D[h - 2], out=D[h])   # guess only: GMRES decides the solution
-        elif warm_start and h > 0:
-            D[h].copy_(D[h - 1])
+        if order >= 0 and h > 0:   # guess only: GMRES decides the solution
+            api.march_guess(ctx, D[:h], order, D[h], stream=stream)
         _, it, rr = api.gmres_solve(ctx, tree, mat, rhs, x=D[h], dt=dt, tol=tol, restart=restart,
                                     max_iter=max_iter, stream=stream)
-        torch.cuda.synchronize()
-        t2 = time.perf_counter()
-        stats.append({"iters": it, "rel_resid": rr, "history_s": t1 - t0, "gmres_s": t2 - t1})
+        st = {"iters": it, "rel_resid": rr}
+        if timing:
+            torch.cuda.synchronize()
+            st.update(history_s=t1 - t0, gmres_s=time.perf_counter() - t1)
+        stats.append(st)
     return D, stats

@@ -366,3 +366,25 @@ def test_node_sharing_geometries(ddm, leaf):
         assert rel_l2(_mv(D, ctx, torch, tree, Dv, "direct"), ref) <= 1e-12
         assert rel_l2(_mv(D, ctx, torch, tree, Dv, "fmm"), ref) <= (1e-12 if leaf == 300 else 1e-10)
     tree.free()
+
+
+def test_march_guess_extrapolation(ddm):
+    """ddm_march_guess (GMRES initial guess of the time march): the
+    polynomial extrapolations, each product and sum rounded in the documented
+    order (numpy's elementwise operations round the same way), the order
+    lowered while fewer steps exist, h = 0 -> zero."""
+    D, ctx, torch = ddm
+    rng = np.random.default_rng(5)
+    H = rng.standard_normal((5, 37, 3))
+    Ht = torch.tensor(H, device="cuda")
+    x = torch.empty((37, 3), dtype=torch.float64, device="cuda")
+    D.march_guess(ctx, Ht[:0], 3, x)
+    assert not x.cpu().numpy().any()
+    exp = {0: lambda d: d[-1], 1: lambda d: d[-1] * 2.0 - d[-2],
+           2: lambda d: (d[-1] - d[-2]) * 3.0 + d[-3],
+           3: lambda d: ((4.0 * d[-1] - 6.0 * d[-2]) + 4.0 * d[-3]) - d[-4]}
+    for h in range(1, 6):
+        for order in range(4):
+            D.march_guess(ctx, Ht[:h], order, x)
+            ref = exp[min(order, h - 1)](H[:h])
+            assert np.array_equal(x.cpu().numpy(), ref), (h, order)
