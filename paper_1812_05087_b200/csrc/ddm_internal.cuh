@@ -299,6 +299,8 @@ struct ddm_tree_s {
   int gm_ticket_n = 0;
   // captured Arnoldi step (gmres.cu): one graph per argument set
   cudaGraphExec_t gm_exec = nullptr;
+  double* gm_pin = nullptr;       // pinned host: GMRES residual estimates + breakdown flag
+  int gm_pin_n = 0;
   uintptr_t gm_key[12] = {};
 };
 

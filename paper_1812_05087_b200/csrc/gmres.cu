@@ -1142,7 +1142,16 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
       g0[0] = beta;
       DDM_CUDA(ctx, cudaMemcpyAsync(gd, g0.data(), (m + 1) * sizeof(double), cudaMemcpyHostToDevice, s));
       DDM_CUDA(ctx, cudaMemsetAsync(flagd, 0, sizeof(int), s));
-      std::vector<double> hest(batch);
+      // residual estimates and breakdown flag read back into pinned host memory
+      if (t->gm_pin_n < batch + 2) {
+        if (t->gm_pin) cudaFreeHost(t->gm_pin);
+        t->gm_pin = nullptr;
+        t->gm_pin_n = 0;
+        DDM_CUDA(ctx, cudaMallocHost((void**)&t->gm_pin, (size_t)(batch + 2) * sizeof(double)));
+        t->gm_pin_n = batch + 2;
+      }
+      double* hest = t->gm_pin;
+      int* hflagp = reinterpret_cast<int*>(t->gm_pin + batch);
       int kb = 0;
       bool stop = false;
       // captured Arnoldi step: from step 1 on, one CUDA
@@ -1270,11 +1279,11 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
         }
         if (k + 1 - kb < batch && k + 1 < m && iters < max_iter) continue;
         }
-        int hflag = 0;
-        DDM_CUDA(ctx, cudaMemcpyAsync(hest.data(), estd + kb, (k + 1 - kb) * sizeof(double),
+        DDM_CUDA(ctx, cudaMemcpyAsync(hest, estd + kb, (k + 1 - kb) * sizeof(double),
                                       cudaMemcpyDeviceToHost, s));
-        DDM_CUDA(ctx, cudaMemcpyAsync(&hflag, flagd, sizeof(int), cudaMemcpyDeviceToHost, s));
+        DDM_CUDA(ctx, cudaMemcpyAsync(hflagp, flagd, sizeof(int), cudaMemcpyDeviceToHost, s));
         DDM_CUDA(ctx, cudaStreamSynchronize(s));
+        const int hflag = *hflagp;
         for (int kk = kb; kk <= k; ++kk) {
           const bool brk = hflag && kk + 1 >= hflag;   // h(kk+1, kk) = 0
           const bool est_ok = hest[kk - kb] <= inner * bnorm;

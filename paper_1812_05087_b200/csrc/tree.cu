@@ -535,6 +535,7 @@ void free_tree(ddm_tree_s* t) {
                   t->pc_chunks, t->pc_off, t->pcl, t->st_elem, t->st_code, t->rbeg, t->srec, t->nc, t->nc_off, t->gm_dev, t->gm_ticket, t->sub_up, t->sub_cells, t->it_roff, t->it_rng, t->gpart, t->lr_rng, t->y_near, t->leaf_info, t->xr_cells, t->xr_off_dev, t->up_own, t->up_strad, t->xsend, t->xrecv, t->ag_send, t->ag_recv, t->ag_lo, t->halo_rng, t->halo_pre, t->dn_own, t->leaf_geo, t->w_geo, t->l2p_runs, t->l2p_order, t->p2p_leaf_order, t->p2m_runs, t->p2m_runs_own};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (t->gm_pin) cudaFreeHost(t->gm_pin);
   for (double* p : t->hc_alloc)
     if (p) cudaFree(p);
   if (t->hc_ptrs) cudaFree(t->hc_ptrs);
