@@ -27,13 +27,19 @@ Exact readings (R5/R8):
                 parent(b) and a not adjacent-or-equal to b (levels >= 2).
   U(B), leaf B  leaves A whose ancestors at level min(lev A, lev B) are
                 adjacent-or-equal (includes B), minus the leaves below a W(B)
-                cell; X-type pairs go to P2P.
+                cell and (x_min > 0) the leaves of X(B).
   W(B), leaf B  (w_min > 0) cells D deeper than B whose
                 ancestor at B's level is adjacent-or-equal to B, with D not
                 touching B (closed boxes disjoint), every ancestor of D below
                 B's level touching B, and count(D) >= w_min: D's multipole is
                 evaluated at B's targets (M2P).  A non-touching D with fewer
                 than w_min elements stays in U (P2P is cheaper).
+  X(B), leaf B  (x_min > 0, the dual of W) leaves A coarser
+                than B and adjacent-or-equal to B's ancestor at A's level
+                (so (A, B) is a U pair), with A not
+                touching B, when count(B) >= x_min: A's elements are expanded
+                into B's local series (P2L) instead of evaluated at each of
+                B's targets.
 Cell numbering is canonical: level-major, Morton prefix order within a level.
 """
 from __future__ import annotations
@@ -260,15 +266,36 @@ def w_lists(t: OracleTree, w_min: int, targets=None) -> dict:
     return out
 
 
-def u_lists(t: OracleTree, targets=None, w_min: int = 0) -> dict:
+def x_lists(t: OracleTree, x_min: int, targets=None) -> dict:
+    """Brute force X(B) for each target leaf B: sorted canonical indices of
+    the coarser, non-touching U-pair leaves (definition in the module
+    docstring; empty when x_min <= 0 or count(B) < x_min)."""
+    leaves = [c for c in t.cells if c.leaf]
+    tg = leaves if targets is None else [t.cells[i] for i in targets]
+    out = {}
+    for B in tg:
+        lst = []
+        if x_min > 0 and len(B.points) >= x_min:
+            for A in leaves:
+                if (A.level < B.level and adjacent_or_equal(A, ancestor(B, A.level))
+                        and not touching(A, B)):
+                    lst.append(A.index)
+        out[B.index] = sorted(lst)
+    return out
+
+
+def u_lists(t: OracleTree, targets=None, w_min: int = 0, x_min: int = 0) -> dict:
     """Brute force U(B) for each target leaf B: sorted canonical leaf indices
-    (w_min > 0: without the leaves below a W(B) cell)."""
+    (w_min > 0: without the leaves below a W(B) cell; x_min > 0: without the
+    leaves of X(B))."""
     leaves = [c for c in t.cells if c.leaf]
     tg = leaves if targets is None else [t.cells[i] for i in targets]
     W = w_lists(t, w_min, [B.index for B in tg]) if w_min > 0 else {}
+    X = x_lists(t, x_min, [B.index for B in tg]) if x_min > 0 else {}
     out = {}
     for B in tg:
         wset = set(W.get(B.index, []))
+        xset = set(X.get(B.index, []))
         lst = []
         for A in leaves:
             m = min(A.level, B.level)
@@ -277,17 +304,18 @@ def u_lists(t: OracleTree, targets=None, w_min: int = 0) -> dict:
                 while c is not None and c.level > B.level:
                     under_w = under_w or c.index in wset
                     c = c.parent
-                if not under_w:
+                if not under_w and A.index not in xset:
                     lst.append(A.index)
         out[B.index] = sorted(lst)
     return out
 
 
-def pair_coverage(t: OracleTree, U: dict, V: dict, W: dict | None = None) -> np.ndarray:
+def pair_coverage(t: OracleTree, U: dict, V: dict, W: dict | None = None,
+                  X: dict | None = None) -> np.ndarray:
     """For every ordered pair of leaves (B target, A source) count how many
-    times it is handled: once by U(B), once per W(B) cell above-or-at A, or
-    once per level l where anc_l(A) in V(anc_l(B)).  The partition property
-    requires all ones."""
+    times it is handled: once by U(B), once by X(B), once per W(B) cell
+    above-or-at A, or once per level l where anc_l(A) in V(anc_l(B)).  The
+    partition property requires all ones."""
     leaves = [c for c in t.cells if c.leaf]
     Vs = {k: set(v) for k, v in V.items()}
     cnt = np.zeros((len(leaves), len(leaves)), dtype=np.int64)
@@ -296,6 +324,7 @@ def pair_coverage(t: OracleTree, U: dict, V: dict, W: dict | None = None) -> np.
         wset = set(W[B.index]) if W is not None else set()
         for j, A in enumerate(leaves):
             n = 1 if A.index in uset else 0
+            n += 1 if X is not None and A.index in X[B.index] else 0
             c = A
             while c is not None:
                 n += 1 if c.index in wset else 0

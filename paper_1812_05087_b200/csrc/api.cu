@@ -596,9 +596,16 @@ int ddm_set_profiling(ddm_ctx_t ctx, int enable) {
 int ddm_stage_times(ddm_ctx_t ctx, double* ms) {
   if (!ctx || !ms) return DDM_ERR_ARG;
   if (!ctx->profiling) return set_error(ctx, DDM_ERR_ARG, "profiling not enabled");
+  // DDM_STAGE_ENDS=1 (scripts/timeline.py): each stage's END relative to the
+  // start of prep instead of its duration -- the concurrent schedule's timeline
+  static const bool ends = [] {
+    const char* e = getenv("DDM_STAGE_ENDS");
+    return e && e[0] == '1';
+  }();
   for (int st = 0; st < DDM_NSTAGES; ++st) {
     float v = 0.f;
-    if (cudaEventElapsedTime(&v, ctx->stage.ev[2 * st], ctx->stage.ev[2 * st + 1]) != cudaSuccess) {
+    if (cudaEventElapsedTime(&v, ctx->stage.ev[ends ? 2 * DDM_ST_PREP : 2 * st],
+                             ctx->stage.ev[2 * st + 1]) != cudaSuccess) {
       cudaGetLastError();
       v = 0.f;
     }

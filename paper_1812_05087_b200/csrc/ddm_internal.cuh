@@ -27,7 +27,14 @@ constexpr int kTgtGroup = DDM_TGT_GROUP;   // targets per P2P work item (one war
 #endif
 constexpr int kSrcChunk = DDM_SRC_CHUNK;  // max sources per P2P work item
 constexpr int kSrcStride = 12;  // doubles per direct-mode source record
-constexpr int kRecStride = 10;  // doubles per near-field stream record (node + 4 complex coefficients)
+// near-field stream record (p2p.cu): node + 5 complex coefficients
+// {node, 2 P1, 2 P2, B/2, Q', K} (DDM_REC_K = 1, the default), or the round-1
+// 10-double form {node, P1, P2, B/2, Q'} that rebuilds 2 (z - zc) from the
+// carried node offsets (DDM_REC_K = 0)
+#ifndef DDM_REC_K
+#define DDM_REC_K 1
+#endif
+constexpr int kRecStride = DDM_REC_K ? 12 : 10;  // doubles per record
 constexpr int kChainMax = 256;  // leaves with more elements keep Morton order (no node sharing)
 #ifndef DDM_PC_CHUNK
 #define DDM_PC_CHUNK 32

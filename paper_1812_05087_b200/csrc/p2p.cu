@@ -285,27 +285,50 @@ __global__ void prep_stream(int64_t q_lo, int64_t n, const int2* __restrict__ hr
   const double2 T2 = cmul(Bh, make_double2(r.x + 1.0, r.y));
   double2* o = reinterpret_cast<double2*>(srec + (int64_t)(rbeg[q] + ((code & 2) ? 0 : 1)) * kRecStride);
   o[0] = end_node(ex, ey, ea, ec, es, i, (code & 1) ? 0 : 1);   // second node
+#if DDM_REC_K
+  // 2 (z - zc).x P1 + 2 (z - zc).y P2 = z.x P1' + z.y P2' - K with P1' = 2 P1,
+  // P2' = 2 P2, K = zc.x P1' + zc.y P2' (zc = the element centre)
+  const double2 P1d = make_double2(2.0 * P1.x, 2.0 * P1.y);
+  const double2 P2d = make_double2(-2.0 * T2.y, 2.0 * T2.x);   // 2 P2 = 2 i Bh (r + 1)
+  const double xc = ex[i], yc = ey[i];
+  o[1] = P1d;
+  o[2] = P2d;
+  o[3] = Bh;
+  o[4] = make_double2(-sg * (rB.x + B.x), -sg * (rB.y - B.y));   // Q'
+  o[5] = make_double2(fma(xc, P1d.x, yc * P2d.x), fma(xc, P1d.y, yc * P2d.y));   // K
+#else
   o[1] = P1;
   o[2] = make_double2(-T2.y, T2.x);   // P2 = i Bh (r + 1)
   o[3] = Bh;
   o[4] = make_double2(-sg * (rB.x + B.x), -sg * (rB.y - B.y));   // Q'
+#endif
 }
 
 // Per target (z, with the carried reciprocal rp and offset wp of the
 // previous record's node) and record {node, P1, P2, Bh, Q'}:
 //   w = z - node, r = 1/w, I2 = r - rp, S = r + rp, d = w + wp = 2 (z - zc)
 //   phi += Im(Bh I2),  psi += I2 [Q' + (d.x P1 + d.y P2) S]
-// 29 fp64-pipe instructions + 1 MUFU.RCP64H per record.
+// 29 fp64-pipe instructions + 1 MUFU.RCP64H per record.  With DDM_REC_K the
+// record carries P1' = 2 P1, P2' = 2 P2 and K = zc.x P1' + zc.y P2', so
+//   d.x P1 + d.y P2 = z.x P1' + z.y P2' - K
+// (4 DFMA instead of 2 DADD + 2 DMUL + 2 DFMA, and no offset carry): 27.
 struct NodeCarry {
+#if DDM_REC_K
+  double rx, ry;
+#else
   double rx, ry, wx, wy;
+#endif
 };
 
 __device__ __forceinline__ void node_init(NodeCarry& n, double zx, double zy, const double* rec) {
-  n.wx = zx - rec[0];
-  n.wy = zy - rec[1];
-  const double inv = fast_rcp(fma(n.wx, n.wx, n.wy * n.wy));
-  n.rx = n.wx * inv;
-  n.ry = -n.wy * inv;
+  const double wx = zx - rec[0], wy = zy - rec[1];
+  const double inv = fast_rcp(fma(wx, wx, wy * wy));
+  n.rx = wx * inv;
+  n.ry = -wy * inv;
+#if !DDM_REC_K
+  n.wx = wx;
+  n.wy = wy;
+#endif
 }
 
 __device__ __forceinline__ void record_update(P2PAcc& acc, NodeCarry& n, double zx, double zy,
@@ -315,9 +338,14 @@ __device__ __forceinline__ void record_update(P2PAcc& acc, NodeCarry& n, double 
   const double rx = wx * inv, ry = -wy * inv;
   const double I2x = rx - n.rx, I2y = ry - n.ry;
   const double Sx = rx + n.rx, Sy = ry + n.ry;
+#if DDM_REC_K
+  const double BXx = fma(zx, sp[2], fma(zy, sp[4], -sp[10]));
+  const double BXy = fma(zx, sp[3], fma(zy, sp[5], -sp[11]));
+#else
   const double dx = wx + n.wx, dy = wy + n.wy;
   const double BXx = fma(dx, sp[2], dy * sp[4]);
   const double BXy = fma(dx, sp[3], dy * sp[5]);
+#endif
   const double Vx = fma(BXx, Sx, fma(-BXy, Sy, sp[8]));
   const double Vy = fma(BXx, Sy, fma(BXy, Sx, sp[9]));
   acc.psi.x = fma(I2x, Vx, fma(-I2y, Vy, acc.psi.x));
@@ -325,8 +353,10 @@ __device__ __forceinline__ void record_update(P2PAcc& acc, NodeCarry& n, double 
   acc.phi = fma(sp[6], I2y, fma(sp[7], I2x, acc.phi));
   n.rx = rx;
   n.ry = ry;
+#if !DDM_REC_K
   n.wx = wx;
   n.wy = wy;
+#endif
 }
 
 // One warp per work item (leaf k, group of nt <= kTgtGroup targets, interval
@@ -472,7 +502,7 @@ constexpr int kLeafMaxTg = 32 * kLT;        // targets per pass (tp <= 32: >= 4 
 constexpr int kLeafMaxPieces = 32;  // ranges per chunk
 constexpr int kLeafMinRec = 16;     // records per slice (at least, where possible)
 #ifndef DDM_LEAF_RMAX
-#define DDM_LEAF_RMAX 384           // staged records per chunk (30 KB)
+#define DDM_LEAF_RMAX (DDM_REC_K ? 352 : 384)   // staged records per chunk (33 / 30 KB: 6 CTAs per SM)
 #endif
 #ifndef DDM_LEAF_MINB
 #define DDM_LEAF_MINB 6

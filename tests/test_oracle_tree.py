@@ -101,6 +101,20 @@ def test_pair_coverage_on_random_trees():
         for b, lst in Ww.items():   # W cells never touch their target leaf
             for d in lst:
                 assert not T.touching(t.cells[d], t.cells[b])
+        # the X split (P2L leaves) with it: still every pair exactly once; X
+        # leaves are coarser than, and do not touch, their target leaf, which
+        # holds >= x_min elements; X(B) is exactly the coarser non-touching
+        # part of the unsplit U(B)
+        xm = int(rng.integers(1, 4))
+        Ux, Xx = T.u_lists(t, w_min=wm, x_min=xm), T.x_lists(t, xm)
+        assert (T.pair_coverage(t, Ux, V, Ww, Xx) == 1).all(), (trial, wm, xm)
+        for b, lst in Xx.items():
+            B = t.cells[b]
+            assert not lst or t.count[b] >= xm
+            expect = [a for a in Uw[b] if t.cells[a].level < B.level
+                      and not T.touching(t.cells[a], B)] if t.count[b] >= xm else []
+            assert lst == expect, (trial, b)
+            assert sorted(Ux[b] + lst) == Uw[b]
         # every element sits in exactly one leaf; leaves hold <= leaf points
         assert t.count[t.is_leaf].sum() == n
         assert (t.count[t.is_leaf] <= leaf).all()
