@@ -106,11 +106,18 @@ int ddm_build_tree(ddm_ctx_t ctx, const double* xc, const double* yc, const doub
                    double min_leaf_side, void* stream, ddm_tree_t* out);
 void ddm_tree_free(ddm_tree_t tree);
 
-/* Sizes of the tree's arrays, written into counts[DDM_TREE_NCOUNTS] [host]. */
+/* Sizes of the tree's arrays, written into counts[DDM_TREE_NCOUNTS] [host].
+ * X = X-list entries (P2L source leaves), X_MIN = the target
+ * leaf size from which X lists are built (env DDM_X_MIN at build time,
+ * default 0 = off: measured slower on config 5),
+ * UXRANGES = merged ranges of U minus X, and
+ * NEAR_PAIRS_P2P = the (target, source) pairs the elastic series-FMM near
+ * field evaluates (NEAR_PAIRS minus the X pairs). */
 enum {
   DDM_TC_N = 0, DDM_TC_CELLS, DDM_TC_LEAVES, DDM_TC_LEVELS, DDM_TC_V, DDM_TC_URANGES,
   DDM_TC_NEAR_PAIRS, DDM_TC_P2P_ITEMS, DDM_TC_OWNED_LO, DDM_TC_OWNED_HI, DDM_TC_P,
-  DDM_TC_W, DDM_TC_W_MIN, DDM_TREE_NCOUNTS = 16
+  DDM_TC_W, DDM_TC_W_MIN, DDM_TC_X, DDM_TC_X_MIN, DDM_TC_UXRANGES, DDM_TC_NEAR_PAIRS_P2P,
+  DDM_TREE_NCOUNTS = 20
 };
 int ddm_tree_counts(ddm_tree_t tree, int64_t* counts);
 
@@ -149,12 +156,18 @@ int ddm_tree_build_times(ddm_tree_t tree, double* ms);
  *   W_OFF   i32[nl+1], W_IDX i32[nw]   (CSR of M2P source cells per leaf,
  *           ascending, the W split of R5: cells deeper than the
  *           leaf, not touching it, with >= w_min elements; env DDM_W_MIN at
- *           build time, default 24, 0 = no W lists) */
+ *           build time, default 24, 0 = no W lists)
+ *   X_OFF   i32[nl+1], X_IDX i32[nx]   (CSR of P2L source leaves per target
+ *           leaf, ascending element start, the dual of W:
+ *           leaves of U coarser than the target leaf and not touching it,
+ *           for target leaves of >= x_min elements)
+ *   UX_OFF  i32[nl+1], UX_LO i32[nux], UX_HI i32[nux]   (U minus X, as U) */
 enum {
   DDM_EX_KEYS = 0, DDM_EX_PERM, DDM_EX_ROOT, DDM_EX_LEVEL, DDM_EX_IX, DDM_EX_IY,
   DDM_EX_START, DDM_EX_COUNT, DDM_EX_PARENT, DDM_EX_FIRST_CHILD, DDM_EX_NCHILD,
   DDM_EX_LEAF, DDM_EX_V_OFF, DDM_EX_V_IDX, DDM_EX_LEAVES, DDM_EX_U_OFF, DDM_EX_U_LO,
-  DDM_EX_U_HI, DDM_EX_W_OFF, DDM_EX_W_IDX
+  DDM_EX_U_HI, DDM_EX_W_OFF, DDM_EX_W_IDX, DDM_EX_X_OFF, DDM_EX_X_IDX, DDM_EX_UX_OFF,
+  DDM_EX_UX_LO, DDM_EX_UX_HI
 };
 int ddm_tree_export(ddm_tree_t tree, int what, void* dst, int64_t capacity_bytes);
 
@@ -300,12 +313,12 @@ int ddm_tip_growth(ddm_ctx_t ctx, int ntips, const double* KI, const double* KII
 /* Per-stage timings of the last ddm_matvec on this tree (CUDA events, ms),
  * written into ms[DDM_NSTAGES] [host] when profiling is enabled
  * (ddm_set_profiling).  Stages: prep, p2m, m2m, m2l, l2l, p2p, finalize (near +
- * far sum and scatter), exchange, l2p.  enable = 0: off; 1: events on the normal schedule (the near
+ * far sum and scatter), exchange, l2p, p2l (X lists).  enable = 0: off; 1: events on the normal schedule (the near
  * field runs concurrently with the far-field chain, so stage times overlap);
  * 2: events + serial schedule (every stage on the caller's stream, one after
  * another: each stage time is that stage's kernels alone, for rooflines). */
 enum { DDM_ST_PREP = 0, DDM_ST_P2M, DDM_ST_M2M, DDM_ST_M2L, DDM_ST_L2L, DDM_ST_P2P,
-       DDM_ST_FINAL, DDM_ST_COMM, DDM_ST_L2P, DDM_NSTAGES };
+       DDM_ST_FINAL, DDM_ST_COMM, DDM_ST_L2P, DDM_ST_P2L, DDM_NSTAGES };
 int ddm_set_profiling(ddm_ctx_t ctx, int enable);
 int ddm_stage_times(ddm_ctx_t ctx, double* ms);
 

@@ -26,12 +26,13 @@ GMRES_PC_POINT = 32   # point-block Jacobi instead of the default leaf blocks
 BBFMM = 16   # | n << 8: Chebyshev (bbFMM) far field with n nodes per dimension
 
 TC = dict(N=0, CELLS=1, LEAVES=2, LEVELS=3, V=4, URANGES=5, NEAR_PAIRS=6, P2P_ITEMS=7,
-          OWNED_LO=8, OWNED_HI=9, P=10, W=11, W_MIN=12)
-NCOUNTS = 16
+          OWNED_LO=8, OWNED_HI=9, P=10, W=11, W_MIN=12, X=13, X_MIN=14, UXRANGES=15,
+          NEAR_PAIRS_P2P=16)
+NCOUNTS = 20
 EX = dict(KEYS=0, PERM=1, ROOT=2, LEVEL=3, IX=4, IY=5, START=6, COUNT=7, PARENT=8,
           FIRST_CHILD=9, NCHILD=10, LEAF=11, V_OFF=12, V_IDX=13, LEAVES=14, U_OFF=15, U_LO=16,
-          U_HI=17, W_OFF=18, W_IDX=19)
-STAGES = ["prep", "p2m", "m2m", "m2l", "l2l", "p2p", "final", "comm", "l2p"]
+          U_HI=17, W_OFF=18, W_IDX=19, X_OFF=20, X_IDX=21, UX_OFF=22, UX_LO=23, UX_HI=24)
+STAGES = ["prep", "p2m", "m2m", "m2l", "l2l", "p2p", "final", "comm", "l2p", "p2l"]
 
 
 class Material(C.Structure):

@@ -138,7 +138,10 @@ class Tree:
                 "V_OFF": (np.int32, nc + 1), "V_IDX": (np.int32, c["V"]),
                 "LEAVES": (np.int32, nl), "U_OFF": (np.int32, nl + 1),
                 "U_LO": (np.int32, c["URANGES"]), "U_HI": (np.int32, c["URANGES"]),
-                "W_OFF": (np.int32, nl + 1), "W_IDX": (np.int32, c["W"])}
+                "W_OFF": (np.int32, nl + 1), "W_IDX": (np.int32, c["W"]),
+                "X_OFF": (np.int32, nl + 1), "X_IDX": (np.int32, c["X"]),
+                "UX_OFF": (np.int32, nl + 1), "UX_LO": (np.int32, c["UXRANGES"]),
+                "UX_HI": (np.int32, c["UXRANGES"])}
         dt, size = spec.get(what, (np.int32, nc))
         out = np.empty(max(size, 1), dtype=dt)
         self.ctx.check(L.ddm_tree_export(self._h, L.EX[what], out.ctypes.data_as(C.c_void_p),

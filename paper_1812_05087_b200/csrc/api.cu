@@ -525,7 +525,8 @@ int ddm_ctx_create(int device, const void* nccl_uid, int rank, int world, ddm_ct
         (e = cudaStreamCreateWithFlags(&ctx->s_cap, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_far, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&ctx->ev_near, cudaEventDisableTiming)) != cudaSuccess) {
+        (e = cudaEventCreateWithFlags(&ctx->ev_near, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_p2l, cudaEventDisableTiming)) != cudaSuccess) {
       int rc = cuda_error(ctx, e, "stream/event creation");
       *out = ctx;
       return rc;
@@ -572,7 +573,7 @@ void ddm_ctx_destroy(ddm_ctx_t ctx) {
 #endif
   if (ctx->stage.created)
     for (auto& ev : ctx->stage.ev) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {ctx->ev_fork, ctx->ev_far, ctx->ev_near})
+  for (cudaEvent_t ev : {ctx->ev_fork, ctx->ev_far, ctx->ev_near, ctx->ev_p2l})
     if (ev) cudaEventDestroy(ev);
   for (cudaStream_t st : {ctx->s_hi, ctx->s_lo, ctx->s_cap})
     if (st) cudaStreamDestroy(st);
@@ -668,6 +669,10 @@ int ddm_tree_counts(ddm_tree_t t, int64_t* c) {
   c[DDM_TC_P] = t->p;
   c[DDM_TC_W] = t->nw;
   c[DDM_TC_W_MIN] = t->w_min;
+  c[DDM_TC_X] = t->nx;
+  c[DDM_TC_X_MIN] = t->xl_min;
+  c[DDM_TC_UXRANGES] = t->nux;
+  c[DDM_TC_NEAR_PAIRS_P2P] = t->nx > 0 ? t->near_pairs_x : t->near_pairs;
   return DDM_OK;
 }
 
@@ -708,6 +713,11 @@ int ddm_tree_export(ddm_tree_t t, int what, void* dst, int64_t cap) {
     case DDM_EX_U_HI: src = t->u_hi; bytes = t->nu * 4; break;
     case DDM_EX_W_OFF: src = t->w_off; bytes = ((size_t)t->nleaves + 1) * 4; break;
     case DDM_EX_W_IDX: src = t->w_idx; bytes = t->nw * 4; break;
+    case DDM_EX_X_OFF: src = t->x_off; bytes = ((size_t)t->nleaves + 1) * 4; break;
+    case DDM_EX_X_IDX: src = t->x_idx; bytes = t->nx * 4; break;
+    case DDM_EX_UX_OFF: src = t->ux_off; bytes = ((size_t)t->nleaves + 1) * 4; break;
+    case DDM_EX_UX_LO: src = t->ux_lo; bytes = t->nux * 4; break;
+    case DDM_EX_UX_HI: src = t->ux_hi; bytes = t->nux * 4; break;
     default: return set_error(ctx, DDM_ERR_ARG, "unknown export id");
   }
   if ((int64_t)bytes > cap) return set_error(ctx, DDM_ERR_ARG, "capacity too small");

@@ -73,7 +73,7 @@ struct ddm_ctx_s {
   cudaStream_t s_cap = nullptr;   // capture stream of the matvec graphs (fmm.cu)
   bool serial = false;            // DDM_SERIAL=1: everything on the caller's stream (profiling)
   bool serial_env = false;        // the DDM_SERIAL setting (restored when profiling mode 2 ends)
-  cudaEvent_t ev_fork = nullptr, ev_far = nullptr, ev_near = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_far = nullptr, ev_near = nullptr, ev_p2l = nullptr;
   // persistent scratch
   double* d_scalar = nullptr;     // small device scratch (reductions)
   double* h_pinned = nullptr;     // small pinned host scratch
@@ -157,6 +157,23 @@ struct ddm_tree_s {
   int* w_idx = nullptr;           // [nw] canonical cell ids, ascending per leaf
   int64_t nw = 0;
   int w_min = 24;                 // W(B) cells hold >= w_min elements (DDM_W_MIN, 0 = off)
+  // X lists (P2L, the dual of W): per target leaf B with
+  // count(B) >= x_min, the coarser leaves of U(B) that do not touch B; their
+  // elements are expanded into B's local series (p2l_kernel) by the elastic
+  // series FMM, whose near field then reads the U ranges minus X (ux_*).
+  // Every other path (poroelastic, bbFMM, history, direct) keeps U whole.
+  int xl_min = 0;                 // DDM_X_MIN at build time, 0 = off (the default: DESIGN §4.13)
+  int* x_off = nullptr;           // [nleaves+1]
+  int* x_idx = nullptr;           // [nx] X leaves (cell ids), ascending element start
+  int64_t nx = 0;
+  int* ux_off = nullptr;          // [nleaves+1] U minus X: merged element ranges per leaf
+  int* ux_lo = nullptr;           // [nux]
+  int* ux_hi = nullptr;           // [nux]
+  int64_t nux = 0, near_pairs_x = 0;   // ranges, and the P2P pairs of U minus X
+  int2* lr_rng_x = nullptr;       // [nux] record ranges of the ux ranges
+  int4* leaf_info_x = nullptr;    // [nleaves] (c_start, c_count, ux_off[k], ux_off[k+1])
+  double2* local_x = nullptr;     // [nleaves][2p] P2L local series of the leaves with X
+  int* x_slot = nullptr;          // [ncells] leaf index k of a leaf with an X list, else -1
   int4* items = nullptr;          // P2P work items: (leaf, tgt0, src_begin, src_end)
   int* item_off = nullptr;        // [nleaves+1] first item of each leaf
   int item_lo_owned = 0, item_hi_owned = 0;   // P2P items of owned leaves

@@ -354,6 +354,156 @@ p2m_kernel(int nruns, const int2* __restrict__ runs, const int* __restrict__ lea
   }
 }
 
+// ------------------------------------------------------------ P2L (f3, X lists)
+// Warp per owned target leaf B with a nonempty X list (tree.cu
+// x_count): the elements of B's X leaves (coarser, not touching B) are
+// expanded into B's local series about z0 = B's centre, written to
+// local_x[k] and added to B's local by the L2P.  In P2M's notation (zeta_1,2
+// the element's nodes, normalised by B's centre and side s; ub = B/s, wr = ub
+// r, x = ub A, Q), the element's fields are the rational functions
+//   Phi(t)  = ub sum_k sig_k / (t - zeta_k)
+//   Psi~(t) = sum_k sig_k [(Q - wr)/(t - zeta_k) + (wr zeta_k + x)/(t - zeta_k)^2]
+// (sig = +1 at zeta_2, -1 at zeta_1: their Laurent coefficients are exactly
+// P2M's alpha_n and gamma_n), and with u_k = 1/zeta_k, R_j = u_2^j - u_1^j the
+// Taylor coefficients about t = 0 (|t| < |zeta_k|: B's targets are closer to
+// z0 than any node of a non-touching leaf) are
+//   l^Phi_m  = -ub R_{m+1}
+//   l^Psi~_m = (-Q + (m + 2) wr) R_{m+1} + (m + 1) x R_{m+2}.
+// Lanes take the concatenated X elements 32 at a time; coefficient chunks of 8
+// are summed over the 32 rows through the [32][17] transpose of P2M, rounds
+// in order: deterministic.  Elastic only (the poroelastic paths keep U whole).
+#ifndef DDM_P2L_MINB
+#define DDM_P2L_MINB 1
+#endif
+template <int PT>
+__global__ void __launch_bounds__(kPassWarps * 32, DDM_P2L_MINB)
+p2l_kernel(int k_lo, int k_hi, const int* __restrict__ x_off, const int* __restrict__ x_idx,
+           const int* __restrict__ leaves, const int* __restrict__ c_level,
+           const int* __restrict__ c_ix, const int* __restrict__ c_iy,
+           const int* __restrict__ c_start, const int* __restrict__ c_count, CellGeom cg, int p_rt,
+           const int* __restrict__ perm, const double* __restrict__ D, int ncomp,
+           const double* __restrict__ ex, const double* __restrict__ ey,
+           const double* __restrict__ ea, const double* __restrict__ ec,
+           const double* __restrict__ es, double2* __restrict__ local_x) {
+  const int p = PT ? PT : p_rt;
+  constexpr int NCH = (pmax<PT>() + 7) / 8;
+  const int nchunk = (p + 7) / 8;
+  const unsigned full = 0xffffffffu;
+  extern __shared__ double2 p2m_sh[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* buf = p2m_sh + w * 32 * 17;
+  for (int k = k_lo + blockIdx.x * kPassWarps + w; k < k_hi; k += gridDim.x * kPassWarps) {
+    const int x0 = __ldg(x_off + k), x1 = __ldg(x_off + k + 1);
+    if (x1 <= x0) continue;
+    const int c = __ldg(leaves + k);
+    const int lev = __ldg(c_level + c);
+    const double s = cg.side(lev);
+    const double is = 1.0 / s;
+    const double2 z0 = cg.centre(lev, __ldg(c_ix + c), __ldg(c_iy + c));
+    double2 acc[NCH];
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) acc[q] = make_double2(0.0, 0.0);
+    // X leaves in batches of 32: lane j holds leaf x0 + j's start and the
+    // inclusive prefix of the element counts
+    for (int xb = x0; xb < x1; xb += 32) {
+      const int nb = min(32, x1 - xb);
+      int ls = 0, lc = 0;
+      if (lane < nb) {
+        const int A = __ldg(x_idx + xb + lane);
+        ls = __ldg(c_start + A);
+        lc = __ldg(c_count + A);
+      }
+      int pre = lc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(full, pre, o);
+        if (lane >= o) pre += v;
+      }
+      const int NE = __shfl_sync(full, pre, 31);
+      for (int e0 = 0; e0 < NE; e0 += 32) {
+        const int f = e0 + lane;
+        // this lane's X leaf: the first with inclusive prefix > f
+        int seg = 0;
+        for (int q = 0; q < nb; ++q)
+          if (__shfl_sync(full, pre, q) <= f) seg = q + 1;
+        const bool valid = f < NE;
+        seg = min(seg, nb - 1);
+        const int sstart = __shfl_sync(full, ls, seg);
+        const int sexcl = __shfl_sync(full, pre - lc, seg);
+        double2 ub = make_double2(0, 0), Q = ub, wr = ub, xw = ub;
+        double2 u1 = make_double2(1.0, 0.0), u2 = u1;
+        if (valid) {
+          const int i = sstart + (f - sexcl);
+          const int j = perm ? perm[i] : i;
+          const double ds = D[(int64_t)j * ncomp], dn = D[(int64_t)j * ncomp + 1];
+          const double cb = ec[i], sb = es[i], a = ea[i];
+          double2 B = make_double2(ds * cb - dn * sb, ds * sb + dn * cb);
+          const double2 rr = make_double2(cb * cb - sb * sb, -2.0 * cb * sb);
+          Q = cscale(csub(cmul(rr, B), cconj(B)), is);
+          const double2 d = make_double2((ex[i] - z0.x) * is, (ey[i] - z0.y) * is);
+          const double2 A = csub(cconj(d), cmul(rr, d));
+          const double2 z1 = make_double2(d.x - a * cb * is, d.y - a * sb * is);
+          const double2 z2 = make_double2(d.x + a * cb * is, d.y + a * sb * is);
+          ub = cscale(B, is);
+          wr = cmul(ub, rr);
+          xw = cmul(ub, A);
+          const double n1 = 1.0 / fma(z1.x, z1.x, z1.y * z1.y);
+          const double n2 = 1.0 / fma(z2.x, z2.x, z2.y * z2.y);
+          u1 = make_double2(z1.x * n1, -z1.y * n1);
+          u2 = make_double2(z2.x * n2, -z2.y * n2);
+        }
+        const double2 nub = make_double2(-ub.x, -ub.y);
+        double2 yv = csub(cscale(wr, 2.0), Q);   // -Q + (m + 2) wr at m = 0
+        double2 xm = xw;                          // (m + 1) x at m = 0
+        double2 pw1 = u1, pw2 = u2;
+        double2 Ra = csub(u2, u1);                // R_{m+1}
+        pw1 = cmul(pw1, u1);
+        pw2 = cmul(pw2, u2);
+        double2 Rb = csub(pw2, pw1);              // R_{m+2}
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          if (ch < nchunk) {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const int m = 8 * ch + jj;
+              double2 lphi = make_double2(0.0, 0.0), lpsi = lphi;
+              if (m < p) {
+                lphi = cmul(nub, Ra);
+                lpsi = cmul(yv, Ra);
+                cmac(lpsi, xm, Rb);
+                yv = cadd(yv, wr);
+                xm = cadd(xm, xw);
+                Ra = Rb;
+                pw1 = cmul(pw1, u1);
+                pw2 = cmul(pw2, u2);
+                Rb = csub(pw2, pw1);
+              }
+              buf[lane * 17 + jj] = lphi;
+              buf[lane * 17 + 8 + jj] = lpsi;
+            }
+            __syncwarp();
+            if (lane < 16) {
+              double2 sum = make_double2(0.0, 0.0);
+#pragma unroll 8
+              for (int r = 0; r < 32; ++r) sum = cadd(sum, buf[r * 17 + lane]);
+              acc[ch] = cadd(acc[ch], sum);
+            }
+            __syncwarp();
+          }
+        }
+      }
+    }
+    if (lane < 16) {
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int slot = 8 * ch + (lane & 7);
+        if (ch < nchunk && slot < p)
+          local_x[(size_t)k * 2 * p + (lane < 8 ? 0 : p) + slot] = acc[ch];
+      }
+    }
+  }
+}
+
 // M2M of the non-leaf cells up_list[u0, u1) of ONE level (launched deepest
 // level first: every child is final when its parent's level runs).
 template <int PT>
@@ -597,7 +747,8 @@ m2l_kernel(int c0, int c1, const int* __restrict__ clist, int64_t own_lo, int64_
            const int* __restrict__ v_idx, const unsigned char* __restrict__ v_cls,
            const int* __restrict__ c_start, const int* __restrict__ c_count, int p_rt,
            const double2* __restrict__ w_g, const double* __restrict__ pm2l_g,
-           const double2* __restrict__ mpole, double2* __restrict__ local) {
+           const double2* __restrict__ mpole, double2* __restrict__ local,
+           const int* __restrict__ x_slot, const double2* __restrict__ local_x) {
   const int p = PT ? PT : p_rt;
   constexpr bool TC = PT > 0 && PT <= 32;   // tensor-core M2L
   constexpr int MT = TC ? (PT + 7) / 8 : 1, KS = TC ? (PT + 4) / 4 : 1;
@@ -640,6 +791,13 @@ m2l_kernel(int c0, int c1, const int* __restrict__ clist, int64_t own_lo, int64_
     } else {
       m2l_cell_dfma(p, vb, ve, v_idx, v_cls, mpole, sh_w, sh_pm2l, ring, ring + p, ring + 2 * p,
                     out, out + p, lane);
+    }
+    // a leaf with an X list: + its P2L series (p2l_kernel, finished before this launch)
+    const int xs = local_x ? __ldg(x_slot + c) : -1;
+    if (xs >= 0) {
+      const double2* lx = local_x + (size_t)xs * 2 * p;
+      for (int m = lane; m < 2 * p; m += 32) out[m] = cadd(out[m], lx[m]);
+      __syncwarp();
     }
   }
 }
@@ -1360,8 +1518,12 @@ int launch_mpole_unpack(ddm_ctx_s* ctx, ddm_tree_s* t, int rank, int world, cuda
 
 // downward pass: M2L of every cell of level >= 2, then L2L one level at a
 // time (top-down), both restricted to subtrees holding owned targets
-int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
+int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s, bool use_x) {
   if (t->nlevels <= 2) return DDM_OK;
+  // use_x: the M2L adds the P2L series of the leaves with X lists (the caller
+  // made s wait for the P2L; the M2L is then launched without PDL)
+  const int* xsl = use_x ? t->x_slot : nullptr;
+  const double2* lxp = use_x ? t->local_x : nullptr;
   const int p = t->p;
   // several ranks: iterate this rank's cell list instead of every cell
   const int* cl = t->dn_own;
@@ -1379,12 +1541,14 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     if ((rc = set_smem(ctx, m2l_kernel<PT>, shm))) return rc;                                   \
     const int nb = pass_grid(ctx, (const void*)m2l_kernel<PT>, shm, c1 - c0, env_int("DDM_M2L_CAP", -1)); \
     stage_begin(ctx, DDM_ST_M2L, s);                                                            \
-    DDM_CUDA(ctx, launch_pdl(use_pdl(t), m2l_kernel<PT>, nb, kPassWarps * 32, shm, s, c0, c1,              \
+    DDM_CUDA(ctx, launch_pdl(use_pdl(t) && !use_x, m2l_kernel<PT>, nb, kPassWarps * 32, shm, s, \
+                             c0, c1,                                                           \
                              (const int*)cl, (int64_t)t->own_el_lo, (int64_t)t->own_el_hi,     \
                              (const int*)t->v_off, (const int*)t->v_idx,                       \
                              (const unsigned char*)t->v_cls, (const int*)t->c_start,           \
                              (const int*)t->c_count, p, (const double2*)t->op_w,               \
-                             (const double*)t->op_pm2l, (const double2*)t->mpole, t->local));  \
+                             (const double*)t->op_pm2l, (const double2*)t->mpole, t->local,    \
+                             xsl, lxp));                                                       \
     stage_end(ctx, DDM_ST_M2L, s);                                                              \
     if ((rc = set_smem(ctx, l2l_level_kernel<PT>, shm2))) return rc;                            \
     stage_begin(ctx, DDM_ST_L2L, s);                                                            \
@@ -1534,12 +1698,15 @@ static int l2p_tables(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
     const int p2p_ord = env_int("DDM_P2P_ORDER", 1);
     const int nlo = t->own_leaf_hi - t->own_leaf_lo;
     if (p2p_ord > 0 && nlo > 0 && t->leaf_info && t->lr_rng) {
+      // the work of the elastic series path: U minus X when there are X lists
+      const bool ux = t->nx > 0 && t->leaf_info_x && t->lr_rng_x;
+      const int64_t nur = ux ? t->nux : t->nu;
       std::vector<int4> li(t->nleaves);
-      std::vector<int2> lr(std::max<int64_t>(t->nu, 1));
-      DDM_CUDA(ctx, cudaMemcpyAsync(li.data(), t->leaf_info, li.size() * sizeof(int4),
-                                    cudaMemcpyDeviceToHost, s));
-      if (t->nu > 0)
-        DDM_CUDA(ctx, cudaMemcpyAsync(lr.data(), t->lr_rng, t->nu * sizeof(int2),
+      std::vector<int2> lr(std::max<int64_t>(nur, 1));
+      DDM_CUDA(ctx, cudaMemcpyAsync(li.data(), ux ? t->leaf_info_x : t->leaf_info,
+                                    li.size() * sizeof(int4), cudaMemcpyDeviceToHost, s));
+      if (nur > 0)
+        DDM_CUDA(ctx, cudaMemcpyAsync(lr.data(), ux ? t->lr_rng_x : t->lr_rng, nur * sizeof(int2),
                                       cudaMemcpyDeviceToHost, s));
       DDM_CUDA(ctx, cudaStreamSynchronize(s));
       std::vector<int64_t> wk(nlo);
@@ -1651,6 +1818,32 @@ int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFa
                                pf, (const double*)t->ex, (const double*)t->ey,                 \
                                (const double*)t->ec, (const double*)t->es, t->y_far));         \
     }                                                                                           \
+  } while (0)
+  DDM_P_DISPATCH(t->p, DDM_L);
+#undef DDM_L
+  DDM_CUDA(ctx, cudaGetLastError());
+  return DDM_OK;
+}
+
+// P2L of the owned leaves' X lists into t->local_x (elastic; D read through
+// perm_in when given, as the early P2M)
+int launch_p2l(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
+               cudaStream_t s) {
+  if (t->nx <= 0 || t->own_leaf_hi <= t->own_leaf_lo) return DDM_OK;
+  int rc = DDM_OK;
+  if (!t->local_x && (rc = talloc(ctx, &t->local_x, (size_t)t->nleaves * 2 * t->p, s))) return rc;
+  const CellGeom cg{t->x_min, t->y_min, t->W};
+  const size_t shp = (size_t)kPassWarps * 32 * 17 * sizeof(double2);
+  const int nl = t->own_leaf_hi - t->own_leaf_lo;
+#define DDM_L(PT)                                                                               \
+  do {                                                                                          \
+    if ((rc = set_smem(ctx, p2l_kernel<PT>, shp))) return rc;                                   \
+    const int nb = pass_grid(ctx, (const void*)p2l_kernel<PT>, shp, nl);                         \
+    p2l_kernel<PT><<<nb, kPassWarps * 32, shp, s>>>(t->own_leaf_lo, t->own_leaf_hi, t->x_off,   \
+                                                    t->x_idx, t->leaves, t->c_level, t->c_ix,   \
+                                                    t->c_iy, t->c_start, t->c_count, cg, t->p,  \
+                                                    perm_in, D, ncomp, t->ex, t->ey, t->ea,     \
+                                                    t->ec, t->es, t->local_x);                  \
   } while (0)
   DDM_P_DISPATCH(t->p, DDM_L);
 #undef DDM_L

@@ -308,9 +308,20 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
 
   // near field: P2P work items of the owned leaves
   const bool leaf_p2p = !poro && use_leaf_p2p();
+  // X lists: the elastic series FMM expands the coarser
+  // non-touching U leaves of a large target leaf into its local series (P2L,
+  // on the near stream ahead of the P2P; the L2P waits for it) and the P2P
+  // reads U minus X; the M2L adds the P2L series to the leaves' locals
+  const bool use_x = leaf_p2p && !bb && t->nx > 0;
+  if (use_x) {
+    stage_begin(ctx, DDM_ST_P2L, sn);
+    if ((rc = launch_p2l(ctx, t, perm_in, D, ncomp, sn))) return rc;
+    stage_end(ctx, DDM_ST_P2L, sn);
+    DDM_CUDA(ctx, cudaEventRecord(ctx->ev_p2l, sn));
+  }
   stage_begin(ctx, DDM_ST_P2P, sn);
   rc = poro       ? launch_poro_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, PP, sn)
-       : leaf_p2p ? launch_p2p_leaf(ctx, t, gc, sn)
+       : leaf_p2p ? launch_p2p_leaf(ctx, t, gc, sn, use_x)
                   : launch_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, gc, sn);
   if (rc) return rc;
   stage_end(ctx, DDM_ST_P2P, sn);
@@ -339,7 +350,8 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
   }
   // downward pass: M2L of every cell of level >= 2, L2L level by level (cells
   // whose subtree holds owned targets)
-  if ((rc = launch_downward(ctx, t, sf))) return rc;
+  if (use_x) DDM_CUDA(ctx, cudaStreamWaitEvent(sf, ctx->ev_p2l, 0));
+  if ((rc = launch_downward(ctx, t, sf, use_x))) return rc;
   // L2P of the owned leaves (far field at the targets), still on the far stream
   stage_begin(ctx, DDM_ST_L2P, sf);
   if ((rc = launch_l2p(ctx, t, ncomp, gc, pf, sf))) return rc;
@@ -439,10 +451,12 @@ int fmm_matvec_sim(ddm_ctx_s* ctx, ddm_tree_s* const* trees, int world, const dd
   }
   const double gc = mat->G / (4.0 * M_PI * (1.0 - mat->nu));
   const PoroFar pf;
+  const bool use_x = t0->nx > 0 && use_leaf_p2p();
   for (int r = 0; r < world; ++r) {   // phase A: near field, local upward pass, pack
     ddm_tree_s* t = trees[r];
     if ((rc = launch_prep_stream(ctx, t, t->perm, D, 2, s, world > 1))) return rc;
-    if ((rc = launch_p2p_leaf(ctx, t, gc, s))) return rc;
+    if (use_x && (rc = launch_p2l(ctx, t, t->perm, D, 2, s))) return rc;
+    if ((rc = launch_p2p_leaf(ctx, t, gc, s, use_x))) return rc;
     if ((rc = launch_upward(ctx, t, t->perm, D, 2, pf, s, world > 1 ? kUpOwn : kUpFull))) return rc;
     if (world > 1 && (rc = launch_mpole_pack(ctx, t, r, s))) return rc;
   }
@@ -462,7 +476,7 @@ int fmm_matvec_sim(ddm_ctx_s* ctx, ddm_tree_s* const* trees, int world, const dd
       if ((rc = launch_mpole_unpack(ctx, t, r, world, s))) return rc;
       if ((rc = launch_upward(ctx, t, nullptr, nullptr, 2, pf, s, kUpStrad))) return rc;
     }
-    if ((rc = launch_downward(ctx, t, s))) return rc;
+    if ((rc = launch_downward(ctx, t, s, use_x))) return rc;
     if ((rc = launch_l2p(ctx, t, 2, gc, pf, s))) return rc;
     // owned rows straight into the shared sorted vector (the row all-gather)
     if ((rc = launch_finalize_near(ctx, t, t->own_el_lo, t->own_el_hi, nullptr, ys, s))) return rc;

@@ -150,8 +150,12 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
 // multipoles of this rank's complete cells -> t->xsend; gathered -> mpole
 int launch_mpole_pack(ddm_ctx_s* ctx, ddm_tree_s* t, int rank, cudaStream_t s);
 int launch_mpole_unpack(ddm_ctx_s* ctx, ddm_tree_s* t, int rank, int world, cudaStream_t s);
-int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s);
+// use_x: the M2L adds the P2L series (local_x) of the leaves with X lists
+int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s, bool use_x = false);
 int launch_l2p(ddm_ctx_s* ctx, ddm_tree_s* t, int ncomp, double gc, const PoroFar& pf,
+               cudaStream_t s);
+// P2L of the owned leaves' X lists into t->local_x, elastic
+int launch_p2l(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const double* D, int ncomp,
                cudaStream_t s);
 // static tables of the block-staged L2P (geometry of leaves / W entries, runs
 // of the owned range); idempotent, outside any capture
@@ -168,7 +172,7 @@ int launch_p2p(ddm_ctx_s* ctx, ddm_tree_s* t, int item_lo, int item_hi, double g
 // t->y_near, and the matching assembly y = y_near + y_far; DDM_P2P_LEAF=0
 // selects the item kernel (launch_p2p + launch_finalize) instead
 bool use_leaf_p2p();
-int launch_p2p_leaf(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, cudaStream_t s);
+int launch_p2p_leaf(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, cudaStream_t s, bool use_x = false);
 int launch_finalize_near(ddm_ctx_s* ctx, ddm_tree_s* t, int64_t lo, int64_t hi, double* y_user,
                          double* y_sorted, cudaStream_t s);
 // near-field source stream (p2p.cu): chain order + break records once per

@@ -806,7 +806,7 @@ bool use_leaf_p2p() {
   return on;
 }
 
-int launch_p2p_leaf(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, cudaStream_t s) {
+int launch_p2p_leaf(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, cudaStream_t s, bool use_x) {
   const int nlv = t->own_leaf_hi - t->own_leaf_lo;
   if (nlv <= 0) return DDM_OK;
   const int rmax = DDM_LEAF_RMAX;
@@ -817,8 +817,10 @@ int launch_p2p_leaf(ddm_ctx_s* ctx, ddm_tree_s* t, double gc, cudaStream_t s) {
                                        (int)shm));
     attr = true;
   }
-  p2p_leaf_kernel<<<nlv, kLeafThreads, shm, s>>>(t->own_leaf_lo, t->p2p_leaf_order, t->leaf_info,
-                                                t->lr_rng, t->srec,
+  const bool ux = use_x && t->nx > 0;
+  p2p_leaf_kernel<<<nlv, kLeafThreads, shm, s>>>(t->own_leaf_lo, t->p2p_leaf_order,
+                                                ux ? t->leaf_info_x : t->leaf_info,
+                                                ux ? t->lr_rng_x : t->lr_rng, t->srec,
                                                 t->ex, t->ey, t->ec, t->es, gc, rmax, t->y_near);
   DDM_CUDA(ctx, cudaGetLastError());
   return DDM_OK;
@@ -886,6 +888,19 @@ int build_source_stream(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s) {
   leaf_info_fill<<<nblk(t->nleaves, 256), 256, 0, s>>>(t->nleaves, t->leaves, t->c_start, t->c_count,
                                                        t->u_off, t->leaf_info);
   DDM_CUDA(ctx, cudaGetLastError());
+  // the same tables for U minus X (elastic series FMM with X lists)
+  if (t->nx > 0) {
+    if ((rc = talloc(ctx, &t->lr_rng_x, (size_t)std::max<int64_t>(t->nux, 1), s))) return rc;
+    if (t->nux > 0) {
+      leaf_rng_fill<<<nblk(t->nux, 256), 256, 0, s>>>(t->nux, t->ux_lo, t->ux_hi, t->rbeg,
+                                                      t->lr_rng_x);
+      DDM_CUDA(ctx, cudaGetLastError());
+    }
+    if ((rc = talloc(ctx, &t->leaf_info_x, (size_t)t->nleaves, s))) return rc;
+    leaf_info_fill<<<nblk(t->nleaves, 256), 256, 0, s>>>(t->nleaves, t->leaves, t->c_start,
+                                                         t->c_count, t->ux_off, t->leaf_info_x);
+    DDM_CUDA(ctx, cudaGetLastError());
+  }
   DDM_CUDA(ctx, cudaStreamSynchronize(s));
   return DDM_OK;
 }

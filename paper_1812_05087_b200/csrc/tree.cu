@@ -446,6 +446,102 @@ __global__ void u_compact(int nleaves, const int* __restrict__ uoff, const int2*
   }
 }
 
+// X(B) of leaf B (oracle/tree.py x_lists): the leaf
+// colleagues of B's proper ancestors (coarser U-pair leaves) that do not
+// touch B, when count(B) >= x_min.  Filled in ascending element start.
+__global__ void x_count(int nleaves, const int* __restrict__ leaves, const int* parent,
+                        const int* coll, const int* leaf, const int* count, const int* level,
+                        const int* ix, const int* iy, int x_min, int* __restrict__ xcnt) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nleaves) return;
+  const int B = leaves[k];
+  int n = 0;
+  if (x_min > 0 && count[B] >= x_min) {
+    const int lB = level[B], xB = ix[B], yB = iy[B];
+    for (int A = parent[B]; A >= 0; A = parent[A])
+      for (int q = 0; q < 9; ++q) {
+        const int Q = coll[A * 9 + q];
+        if (Q < 0) break;
+        if (leaf[Q] && !cells_touch(lB, xB, yB, level[Q], ix[Q], iy[Q])) ++n;
+      }
+  }
+  xcnt[k] = n;
+}
+
+__global__ void x_fill(int nleaves, const int* __restrict__ leaves, const int* parent,
+                       const int* coll, const int* leaf, const int* start, const int* count,
+                       const int* level, const int* ix, const int* iy, int x_min,
+                       const int* __restrict__ xoff, int* __restrict__ xidx) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nleaves) return;
+  const int B = leaves[k];
+  int* out = xidx + xoff[k];
+  const int n = xoff[k + 1] - xoff[k];
+  if (n == 0) return;
+  const int lB = level[B], xB = ix[B], yB = iy[B];
+  int m = 0;
+  for (int A = parent[B]; A >= 0; A = parent[A])
+    for (int q = 0; q < 9; ++q) {
+      const int Q = coll[A * 9 + q];
+      if (Q < 0) break;
+      if (leaf[Q] && !cells_touch(lB, xB, yB, level[Q], ix[Q], iy[Q])) out[m++] = Q;
+    }
+  for (int a = 1; a < m; ++a) {   // ascending element start (disjoint leaves)
+    const int v = out[a];
+    int b = a - 1;
+    while (b >= 0 && start[out[b]] > start[v]) { out[b + 1] = out[b]; --b; }
+    out[b + 1] = v;
+  }
+}
+
+__global__ void x_slot_fill(int nleaves, const int* __restrict__ leaves,
+                            const int* __restrict__ xoff, int* __restrict__ x_slot) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nleaves && xoff[k + 1] > xoff[k]) x_slot[leaves[k]] = k;
+}
+
+// U(B) minus the element ranges of X(B) (each X leaf lies inside one merged
+// U range): kFill = false counts the ranges and the P2P pairs, true writes them
+template <bool kFill>
+__global__ void ux_ranges(int nleaves, const int* __restrict__ leaves, const int* __restrict__ count,
+                          const int* __restrict__ start, const int* __restrict__ u_off,
+                          const int* __restrict__ u_lo, const int* __restrict__ u_hi,
+                          const int* __restrict__ xoff, const int* __restrict__ xidx,
+                          int* __restrict__ cnt, long long* __restrict__ pairs,
+                          const int* __restrict__ ux_off, int* __restrict__ ux_lo,
+                          int* __restrict__ ux_hi) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nleaves) return;
+  const int x0 = xoff[k], x1 = xoff[k + 1];
+  int n = 0;
+  long long src = 0;
+  int xi = x0;
+  int o = kFill ? ux_off[k] : 0;
+  for (int r = u_off[k]; r < u_off[k + 1]; ++r) {
+    int cur = u_lo[r];
+    const int hi = u_hi[r];
+    while (xi < x1 && start[xidx[xi]] < hi) {
+      const int a = start[xidx[xi]], b = a + count[xidx[xi]];
+      if (a > cur) {
+        if (kFill) { ux_lo[o] = cur; ux_hi[o] = a; ++o; }
+        ++n;
+        src += a - cur;
+      }
+      cur = b;
+      ++xi;
+    }
+    if (cur < hi) {
+      if (kFill) { ux_lo[o] = cur; ux_hi[o] = hi; ++o; }
+      ++n;
+      src += hi - cur;
+    }
+  }
+  if (!kFill) {
+    cnt[k] = n;
+    pairs[k] = src * count[leaves[k]];
+  }
+}
+
 __global__ void item_count(int nleaves, const int* __restrict__ leaves,
                            const int* __restrict__ count, const int* __restrict__ nsrc,
                            int* __restrict__ icnt, long long* __restrict__ pairs) {
@@ -532,7 +628,7 @@ void free_tree(ddm_tree_s* t) {
                   t->op_eps, t->op_e2i, t->mpole, t->local, t->src, t->part, t->d_sorted, t->y_sorted, t->y_far,
                   t->up_list,
                   t->krylov, t->pc, t->gm_w, t->gm_tmp, t->gm_part, t->bb_w, t->bb_f,
-                  t->pc_chunks, t->pc_off, t->pcl, t->st_elem, t->st_code, t->rbeg, t->srec, t->nc, t->nc_off, t->gm_dev, t->gm_ticket, t->sub_up, t->sub_cells, t->it_roff, t->it_rng, t->gpart, t->lr_rng, t->y_near, t->leaf_info, t->xr_cells, t->xr_off_dev, t->up_own, t->up_strad, t->xsend, t->xrecv, t->ag_send, t->ag_recv, t->ag_lo, t->halo_rng, t->halo_pre, t->dn_own, t->leaf_geo, t->w_geo, t->l2p_runs, t->l2p_order, t->p2p_leaf_order, t->p2m_runs, t->p2m_runs_own};
+                  t->pc_chunks, t->pc_off, t->pcl, t->st_elem, t->st_code, t->rbeg, t->srec, t->nc, t->nc_off, t->gm_dev, t->gm_ticket, t->sub_up, t->sub_cells, t->it_roff, t->it_rng, t->gpart, t->lr_rng, t->y_near, t->leaf_info, t->xr_cells, t->xr_off_dev, t->up_own, t->up_strad, t->xsend, t->xrecv, t->ag_send, t->ag_recv, t->ag_lo, t->halo_rng, t->halo_pre, t->dn_own, t->leaf_geo, t->w_geo, t->l2p_runs, t->l2p_order, t->p2p_leaf_order, t->p2m_runs, t->p2m_runs_own, t->x_off, t->x_idx, t->ux_off, t->ux_lo, t->ux_hi, t->lr_rng_x, t->leaf_info_x, t->local_x, t->x_slot};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (t->gm_pin) cudaFreeHost(t->gm_pin);
@@ -891,6 +987,59 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
     cudaFreeAsync(nsrc, s);
     cudaFreeAsync(utmp, s);
     cudaFreeAsync(icnt, s);
+    cudaFreeAsync(pairs, s);
+    cudaFreeAsync(pairs_scan, s);
+  }
+
+  // ---- X lists and the U ranges without them (elastic series FMM only)
+  if (const char* e = getenv("DDM_X_MIN")) t->xl_min = atoi(e);
+  {
+    const int nl = t->nleaves;
+    int *xcnt = nullptr, *uxcnt = nullptr;
+    long long *pairs = nullptr, *pairs_scan = nullptr;
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&xcnt, nl * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&uxcnt, nl * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&pairs, nl * sizeof(long long), s));
+    DDM_CUDA(ctx, cudaMallocAsync((void**)&pairs_scan, nl * sizeof(long long), s));
+    x_count<<<nblk(nl, 128), 128, 0, s>>>(nl, t->leaves, C.parent, t->colleagues, C.leaf, C.count,
+                                          C.level, C.ix, C.iy, t->xl_min, xcnt);
+    DDM_CUDA(ctx, cudaGetLastError());
+    int nxt = 0;
+    if ((rc = talloc(ctx, &t->x_off, nl + 1, s))) return rc;
+    if ((rc = exclusive_scan_i32(ctx, xcnt, t->x_off, nl, &nxt, s))) return rc;
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->x_off + nl, &nxt, sizeof(int), cudaMemcpyHostToDevice, s));
+    t->nx = nxt;
+    if ((rc = talloc(ctx, &t->x_idx, std::max(nxt, 1), s))) return rc;
+    x_fill<<<nblk(nl, 128), 128, 0, s>>>(nl, t->leaves, C.parent, t->colleagues, C.leaf, C.start,
+                                         C.count, C.level, C.ix, C.iy, t->xl_min, t->x_off,
+                                         t->x_idx);
+    DDM_CUDA(ctx, cudaGetLastError());
+    if ((rc = talloc(ctx, &t->x_slot, (size_t)t->ncells, s))) return rc;
+    DDM_CUDA(ctx, cudaMemsetAsync(t->x_slot, 0xFF, (size_t)t->ncells * sizeof(int), s));
+    x_slot_fill<<<nblk(nl, 128), 128, 0, s>>>(nl, t->leaves, t->x_off, t->x_slot);
+    DDM_CUDA(ctx, cudaGetLastError());
+    ux_ranges<false><<<nblk(nl, 128), 128, 0, s>>>(nl, t->leaves, C.count, C.start, t->u_off,
+                                                   t->u_lo, t->u_hi, t->x_off, t->x_idx, uxcnt,
+                                                   pairs, nullptr, nullptr, nullptr);
+    DDM_CUDA(ctx, cudaGetLastError());
+    int nux = 0;
+    if ((rc = talloc(ctx, &t->ux_off, nl + 1, s))) return rc;
+    if ((rc = exclusive_scan_i32(ctx, uxcnt, t->ux_off, nl, &nux, s))) return rc;
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->ux_off + nl, &nux, sizeof(int), cudaMemcpyHostToDevice, s));
+    t->nux = nux;
+    if ((rc = talloc(ctx, &t->ux_lo, std::max(nux, 1), s)) ||
+        (rc = talloc(ctx, &t->ux_hi, std::max(nux, 1), s)))
+      return rc;
+    ux_ranges<true><<<nblk(nl, 128), 128, 0, s>>>(nl, t->leaves, C.count, C.start, t->u_off,
+                                                  t->u_lo, t->u_hi, t->x_off, t->x_idx, nullptr,
+                                                  nullptr, t->ux_off, t->ux_lo, t->ux_hi);
+    DDM_CUDA(ctx, cudaGetLastError());
+    int64_t npx = 0;
+    if ((rc = exclusive_scan_i64(ctx, (const int64_t*)pairs, (int64_t*)pairs_scan, nl, &npx, s)))
+      return rc;
+    t->near_pairs_x = npx;
+    cudaFreeAsync(xcnt, s);
+    cudaFreeAsync(uxcnt, s);
     cudaFreeAsync(pairs, s);
     cudaFreeAsync(pairs_scan, s);
   }

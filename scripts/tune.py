@@ -60,7 +60,7 @@ def main():
             continue
         d = json.loads(line[0][7:])
         print(f"{v:40s} " + " ".join(f"{k}={d[k]:.3f}" for k in
-                                      ("total", "prep", "p2p", "p2m", "m2m", "m2l", "l2l", "l2p", "final")),
+                                      ("total", "prep", "p2p", "p2l", "p2m", "m2m", "m2l", "l2l", "l2p", "final")),
               flush=True)
 
 

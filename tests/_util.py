@@ -28,12 +28,23 @@ def oracle_u_ranges(t, U: dict) -> dict:
     return out
 
 
-def gpu_u_ranges(tree) -> dict:
+def gpu_u_ranges(tree, prefix="U") -> dict:
+    """U ranges per leaf (prefix "UX": U minus the X lists)."""
     leaves = tree.export("LEAVES")
-    off = tree.export("U_OFF")
-    lo = tree.export("U_LO")
-    hi = tree.export("U_HI")
+    off = tree.export(prefix + "_OFF")
+    lo = tree.export(prefix + "_LO")
+    hi = tree.export(prefix + "_HI")
     return {int(leaves[k]): [(int(lo[r]), int(hi[r])) for r in range(off[k], off[k + 1])]
+            for k in range(leaves.size)}
+
+
+def gpu_x_lists(tree) -> dict:
+    """X lists per leaf as sorted canonical cell indices (the library keeps
+    them in element order)."""
+    leaves = tree.export("LEAVES")
+    off = tree.export("X_OFF")
+    idx = tree.export("X_IDX")
+    return {int(leaves[k]): sorted(int(v) for v in idx[off[k]:off[k + 1]])
             for k in range(leaves.size)}
 
 

@@ -316,6 +316,83 @@ def test_no_w_lists_reproduce_survey_sizes_and_parity(ddm, monkeypatch):
     assert rel_l2(y, OE.matvec_dense(_A(2), Dv)) <= 1e-8
 
 
+@pytest.mark.parametrize("xmin,leaf,p", [(0, 32, 20), (1, 32, 20), (8, 32, 20), (1, 12, 28),
+                                         (1, 100, 20)])
+def test_fmm_x_lists_p2l(ddm, monkeypatch, xmin, leaf, p):
+    """X lists: with DDM_X_MIN = xmin the elastic series FMM
+    expands the coarser non-touching U leaves of every target leaf of >= xmin
+    elements into its local series (P2L) and the P2P reads U minus X.  Config
+    2 at several leaf sizes against the dense oracle (1e-8); xmin = 0 is the
+    plain U split.  The near field with X removed evaluates exactly
+    NEAR_PAIRS_P2P pairs."""
+    D, ctx, torch = ddm
+    monkeypatch.setenv("DDM_X_MIN", str(xmin))
+    g = make_config(2)
+    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+    tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=leaf, order_p=p)
+    c = tree.counts
+    assert c["X_MIN"] == xmin
+    if xmin == 0:
+        assert c["X"] == 0 and c["NEAR_PAIRS_P2P"] == c["NEAR_PAIRS"]
+    elif xmin == 1:
+        assert c["X"] > 0 and c["NEAR_PAIRS_P2P"] < c["NEAR_PAIRS"]
+    for seed in (0, 1):
+        Dv = random_dd(g.n, 2, 700 + seed)
+        y = _mv(D, ctx, torch, tree, Dv, "fmm")
+        assert rel_l2(y, OE.matvec_dense(_A(2), Dv)) <= 1e-8, (xmin, leaf, seed)
+    # deterministic
+    assert np.array_equal(y, _mv(D, ctx, torch, tree, Dv, "fmm"))
+    tree.free()
+
+
+def test_fmm_x_lists_cfg5_sampled_rows(ddm, monkeypatch):
+    """X lists on the full-size config 5 (leaf 64, p = 20; DDM_X_MIN = 20):
+    the P2L route against the oracle on sampled rows, including every target
+    of the leaf with the most X sources."""
+    from . import _pool
+    D, ctx, torch = ddm
+    monkeypatch.setenv("DDM_X_MIN", "20")
+    g = make_config(5)
+    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+    tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=64, order_p=20)
+    assert tree.counts["X"] > 0
+    Dv = random_dd(g.n, 2, CONFIGS[5]["d_seed"])
+    y = _mv(D, ctx, torch, tree, Dv, "fmm")
+    leaves, xoff, xidx = tree.export("LEAVES"), tree.export("X_OFF"), tree.export("X_IDX")
+    start, count, perm = tree.export("START"), tree.export("COUNT"), tree.export("PERM")
+    xsrc = np.array([count[xidx[xoff[k]:xoff[k + 1]]].sum() for k in range(leaves.size)])
+    kmax = int(np.argmax(xsrc))
+    c = leaves[kmax]
+    rng = np.random.default_rng(55)
+    rows = np.unique(np.concatenate([rng.choice(g.n, 96, replace=False),
+                                     perm[start[c]:start[c] + count[c]]]))
+    ref = _pool.elastic_rows(g, G0, NU0, Dv, rows)
+    assert rel_l2(y[rows], ref) <= 1e-8
+    tree.free()
+
+
+def test_fmm_x_lists_match_plain_split(ddm, monkeypatch):
+    """The P2L route and the plain P2P route compute the same operator: on
+    config 4's geometry (elastic) with every leaf a P2L target the two
+    results agree to 1e-10 (the far-field truncation of the expansions),
+    and each agrees with the dense oracle to 1e-8."""
+    D, ctx, torch = ddm
+    g = make_config(4)
+    f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+    ys = {}
+    Dv = random_dd(g.n, 2, 711)
+    for xmin in (0, 1):
+        monkeypatch.setenv("DDM_X_MIN", str(xmin))
+        tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=16, order_p=30)
+        assert (tree.counts["X"] > 0) == (xmin > 0)
+        ys[xmin] = _mv(D, ctx, torch, tree, Dv, "fmm")
+        tree.free()
+    ref = OE.matvec_dense(OE.assemble_dense(g, G0, NU0), Dv)
+    assert rel_l2(ys[1], ys[0]) <= 1e-10
+    for y in ys.values():
+        assert rel_l2(y, ref) <= 1e-8
+
+
 def _polyline_elements(nodes_list):
     """Constant elements between consecutive nodes of each polyline (beta in
     [0, pi), so the element's own first endpoint may be either node)."""

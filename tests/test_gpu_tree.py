@@ -7,7 +7,7 @@ from oracle import tree as OT
 from synth import make_config
 from synth.geometry import Geometry
 
-from ._util import gpu_w_lists, gpu_u_ranges, gpu_v_lists, oracle_u_ranges
+from ._util import gpu_u_ranges, gpu_v_lists, gpu_w_lists, gpu_x_lists, oracle_u_ranges
 
 pytestmark = pytest.mark.gpu
 
@@ -41,11 +41,13 @@ def _compare(D, ctx, torch, g, leaf, lists=True, sample=None, min_side=0.0):
     leaves_by_start = sorted(np.nonzero(ot.is_leaf)[0], key=lambda c: ot.start[c])
     assert np.array_equal(tree.export("LEAVES"), np.array(leaves_by_start, dtype=np.int32))
     if lists:
-        wm = tree.counts["W_MIN"]
+        wm, xm = tree.counts["W_MIN"], tree.counts["X_MIN"]
         if sample is None:
             V = OT.v_lists(ot)
             U = OT.u_lists(ot, w_min=wm)
             Wl = OT.w_lists(ot, wm)
+            Xl = OT.x_lists(ot, xm)
+            UX = OT.u_lists(ot, w_min=wm, x_min=xm)
         else:
             rng = np.random.default_rng(0)
             cells = rng.choice(ot.n_cells, size=min(sample, ot.n_cells), replace=False)
@@ -54,6 +56,19 @@ def _compare(D, ctx, torch, g, leaf, lists=True, sample=None, min_side=0.0):
             V = OT.v_lists(ot, cells)
             U = OT.u_lists(ot, leaves, w_min=wm)
             Wl = OT.w_lists(ot, wm, leaves)
+            Xl = OT.x_lists(ot, xm, leaves)
+            UX = OT.u_lists(ot, leaves, w_min=wm, x_min=xm)
+        # X lists (P2L leaves) and the U ranges without them: bit-exact
+        gx = gpu_x_lists(tree)
+        for b, lst in Xl.items():
+            assert gx[b] == lst, b
+        gux = gpu_u_ranges(tree, "UX")
+        for b, rs in oracle_u_ranges(ot, UX).items():
+            assert gux[b] == rs, b
+        if sample is None:
+            pairs = sum(int(ot.count[b]) * (hi - lo) for b, rs in oracle_u_ranges(ot, UX).items()
+                        for lo, hi in rs)
+            assert tree.counts["NEAR_PAIRS_P2P"] == pairs
         gv = gpu_v_lists(tree)
         for c, lst in V.items():
             assert gv[c] == lst, c
@@ -102,6 +117,28 @@ def test_tree_bitexact_random_ragged(ddm, seed, n, leaf):
     except OT.GeometryError:
         with pytest.raises(D.DDMError):
             D.Tree(ctx, *_tensors(torch, g), leaf_size=leaf)
+
+
+@pytest.mark.parametrize("seed,n,leaf,xmin", [(3, 33, 1, 1), (4, 257, 3, 2), (5, 1000, 7, 3),
+                                              (6, 4097, 16, 4), (7, 5000, 64, 20)])
+def test_tree_x_lists_random(ddm, monkeypatch, seed, n, leaf, xmin):
+    """X lists and U minus X bit-exact on ragged / clustered random trees
+    with a small X threshold (DDM_X_MIN), so that most leaves are P2L targets."""
+    D, ctx, torch = ddm
+    monkeypatch.setenv("DDM_X_MIN", str(xmin))
+    rng = np.random.default_rng(seed)
+    if seed % 2:
+        x, y = rng.uniform(-5, 5, n), rng.uniform(0, 1, n)
+    else:
+        x = np.round(rng.normal(size=n), 2)
+        y = 0.5 * x + 0.01 * rng.integers(4, size=n)
+    g = Geometry(x, y, np.full(n, 1e-3), rng.uniform(0, np.pi, n), np.zeros(n, int),
+                 np.zeros((1, 2), int))
+    try:
+        tree, _ = _compare(D, ctx, torch, g, leaf)
+    except OT.GeometryError:
+        return
+    assert tree.counts["X_MIN"] == xmin
 
 
 def test_depth_cap(ddm):
