@@ -29,8 +29,8 @@ sys.path.insert(0, ROOT)
 METRIC = ("FMM DDM matvec interactions/s and GMRES solve time (fp64) vs roofline, "
           "1/2/4/8 GPU")
 UNIT = "interactions/s"
-FLOP_PER_PAIR = 45          # P2P record update as written: 16 FMA (2 flop) + 5 MUL + 8 ADD
-FP64_INSTR_PER_PAIR = 28    # fp64-pipe instructions per record and target in the SASS (+ 1 MUFU.RCP64H)
+FLOP_PER_PAIR = 45          # P2P algorithmic unit, fixed since round 1: the record update as first written (16 FMA + 5 MUL + 8 ADD, cubic reciprocal refinement); the round-2 kernel executes 43 (K-form record, one-step reciprocal)
+FP64_INSTR_PER_PAIR = 25    # fp64-pipe instructions per record and target in the SASS of p2p_leaf_kernel's loop (21 DFMA + 2 DADD + 2 DMUL, + 1 MUFU.RCP64H; 28 in round 1)
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 
 
@@ -308,7 +308,8 @@ def run_ours(args):
     # serial schedule: every stage's events bracket that stage's kernels alone
     # (in the timed step the near field overlaps the far-field chain)
     ctx.set_profiling(True, serial=True)
-    stages = {k: 0.0 for k in ("prep", "p2m", "m2m", "m2l", "l2l", "l2p", "p2p", "final", "comm")}
+    stages = {k: 0.0 for k in ("prep", "p2m", "m2m", "m2l", "l2l", "l2p", "p2p", "final", "comm",
+                               "p2l")}
     nprof = max(3, min(args.steps, 10))
     for _ in range(nprof):
         flush.zero_()
@@ -328,7 +329,7 @@ def run_ours(args):
     ctx.set_profiling(False)
     fp64_peak = ctx_probe_fp64(ctx)
     kern = kernel_rooflines(tree, cnt, stages, tree_stages, p, fp64_peak, world)
-    owned_pairs = cnt["NEAR_PAIRS"] / world   # approx. per rank for N > 1
+    owned_pairs = cnt["NEAR_PAIRS_P2P"] / world   # approx. per rank for N > 1 (U minus X)
     p2p_ms = stages["p2p"]
     achieved = owned_pairs * FLOP_PER_PAIR / (p2p_ms * 1e-3) / 1e12
     levels = cnt["LEVELS"]
@@ -451,8 +452,9 @@ def kernel_rooflines(tree, cnt, stages, tree_stages, p, fp64_peak, world):
         "l2p": ("fp64", (24.0 * p + 20) * n + (24.0 * p + 30) * el_w, "flop",
                 f"(24 p + 20) flop/elem local + (24 p + 30) per (element, W cell) M2P pair "
                 f"({el_w} pairs)"),
-        "p2p": ("fp64", FLOP_PER_PAIR * cnt["NEAR_PAIRS"] / world, "flop",
-                "45 flop per near pair (node-sharing record update as written)"),
+        "p2p": ("fp64", FLOP_PER_PAIR * cnt["NEAR_PAIRS_P2P"] / world, "flop",
+                "45 flop per near pair (the round-1 node-sharing record update as written; "
+                "the round-2 kernel executes 43 with 26 fp64 instructions)"),
         "final": ("hbm", 52.0 * n, "B", "52 B/elem: near (16) + far (16) + perm (4) in, y (16) out"),
     }
     out = {}

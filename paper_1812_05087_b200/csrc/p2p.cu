@@ -311,7 +311,28 @@ __global__ void prep_stream(int64_t q_lo, int64_t n, const int2* __restrict__ hr
 // 29 fp64-pipe instructions + 1 MUFU.RCP64H per record.  With DDM_REC_K the
 // record carries P1' = 2 P1, P2' = 2 P2 and K = zc.x P1' + zc.y P2', so
 //   d.x P1 + d.y P2 = z.x P1' + z.y P2' - K
-// (4 DFMA instead of 2 DADD + 2 DMUL + 2 DFMA, and no offset carry): 27.
+// (4 DFMA instead of 2 DADD + 2 DMUL + 2 DFMA, and no offset carry): 27, and
+// 26 with the one-step reciprocal below.
+
+// DDM_P2P_RCP2=1 (default): the near-field reciprocal takes ONE Newton step
+// on the MUFU seed instead of fast_rcp's cubic refinement.  Measured
+// (scripts/micro/rcp_probe.cu, x over 1e-12..1e12): seed 9.9e-7, one step
+// 9.9e-13, cubic 2.2e-16 max relative error.  The FMM bar is 1e-8 (the
+// direct mode keeps the cubic form for its 1e-12 bar); one DFMA fewer per
+// pair: P2P 0.579 -> 0.564 ms, concurrent step 0.976 -> 0.957 ms (config 5).
+#ifndef DDM_P2P_RCP2
+#define DDM_P2P_RCP2 1
+#endif
+__device__ __forceinline__ double p2p_rcp(double x) {
+#if DDM_P2P_RCP2
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return fma(r, fma(-x, r, 1.0), r);
+#else
+  return fast_rcp(x);
+#endif
+}
+
 struct NodeCarry {
 #if DDM_REC_K
   double rx, ry;
@@ -322,7 +343,7 @@ struct NodeCarry {
 
 __device__ __forceinline__ void node_init(NodeCarry& n, double zx, double zy, const double* rec) {
   const double wx = zx - rec[0], wy = zy - rec[1];
-  const double inv = fast_rcp(fma(wx, wx, wy * wy));
+  const double inv = p2p_rcp(fma(wx, wx, wy * wy));
   n.rx = wx * inv;
   n.ry = -wy * inv;
 #if !DDM_REC_K
@@ -331,10 +352,11 @@ __device__ __forceinline__ void node_init(NodeCarry& n, double zx, double zy, co
 #endif
 }
 
+
 __device__ __forceinline__ void record_update(P2PAcc& acc, NodeCarry& n, double zx, double zy,
                                               const double* sp) {
   const double wx = zx - sp[0], wy = zy - sp[1];
-  const double inv = fast_rcp(fma(wx, wx, wy * wy));
+  const double inv = p2p_rcp(fma(wx, wx, wy * wy));
   const double rx = wx * inv, ry = -wy * inv;
   const double I2x = rx - n.rx, I2y = ry - n.ry;
   const double Sx = rx + n.rx, Sy = ry + n.ry;
@@ -508,6 +530,10 @@ constexpr int kLeafMinRec = 16;     // records per slice (at least, where possib
 #define DDM_LEAF_MINB 6
 #endif
 
+#ifndef DDM_LEAF_UNROLL
+#define DDM_LEAF_UNROLL 2
+#endif
+constexpr int kLeafUnroll = DDM_LEAF_UNROLL;
 __device__ __forceinline__ void load_rec_s(double (&sp)[kRecStride], const double* rec) {
   const double2* g = reinterpret_cast<const double2*>(rec);
 #pragma unroll
@@ -656,7 +682,7 @@ p2p_leaf_kernel(int leaf_lo, const int* __restrict__ order, const int4* __restri
 #pragma unroll
             for (int q = 0; q < kLT; ++q) node_init(ncr[q], zx[q], zy[q], sp);
           }
-#pragma unroll 2
+#pragma unroll kLeafUnroll
           for (int j = a; j < b; ++j) {
             double sp[kRecStride];
             load_rec_s(sp, recs + (size_t)j * kRecStride);
