@@ -235,29 +235,71 @@ __device__ void p2m_run(int kk0, int nseg, int p, const int* __restrict__ leaves
   }
 }
 
+// Tree-static part of a parent's M2M (loaded before the PDL wait where the
+// launch allows it): the cell, its children and their quadrants.
+struct M2MStatic {
+  int c, f, nc;
+  int quad[4];
+};
+__device__ __forceinline__ M2MStatic m2m_static(int c, const int* __restrict__ c_ix,
+                                                const int* __restrict__ c_iy,
+                                                const int* __restrict__ first_child,
+                                                const int* __restrict__ nchild) {
+  M2MStatic st;
+  st.c = c;
+  st.f = first_child[c];
+  st.nc = nchild[c];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int q = st.f + min(i, st.nc - 1);
+    st.quad[i] = (c_ix[q] & 1) + 2 * (c_iy[q] & 1);
+  }
+  return st;
+}
+
+// The operator tables of the M2M / L2L passes staged in shared memory by the
+// whole CTA (before the PDL wait): the real Pascal matrix [p][p] and the
+// quadrant powers eps^k, (2 eps)^-k [4][p + 2]; tbl_doubles() = their size.
+__host__ __device__ __forceinline__ int tbl_pas(int p) { return (p * p + 1) & ~1; }
+__host__ __device__ __forceinline__ int tbl_doubles(int p) { return tbl_pas(p) + 16 * (p + 2); }
+struct OpTables {
+  const double* pas;    // pasT (M2M: C(m, n) at n p + m) or pas (L2L: C(m, k) at m p + k)
+  const double2* eps;   // [4][p + 2]
+  const double2* e2i;   // [4][p + 2]
+};
+__device__ __forceinline__ OpTables stage_tables(double* sh, int p, const double* __restrict__ pas_g,
+                                                 const double2* __restrict__ eps_g,
+                                                 const double2* __restrict__ e2i_g) {
+  const int np = tbl_pas(p), pw4 = 4 * (p + 2);
+  double2* e = reinterpret_cast<double2*>(sh + np);
+  for (int i = threadIdx.x; i < p * p; i += blockDim.x) sh[i] = pas_g[i];
+  for (int i = threadIdx.x; i < pw4; i += blockDim.x) {
+    e[i] = eps_g[i];
+    e[pw4 + i] = e2i_g[i];
+  }
+  return OpTables{sh, e, e + pw4};
+}
+
 // ------------------------------------------------------------ M2M (a6)
 // Parent c from its children q (all ready), separable form (fmm.cu):
 //   c^q_{n+1} = gamma^q_{n+1} - n conj(e)/s_q alpha^q_n,   e = z_c - z_q
 //   xa^q_n = (2 eps_q)^{-(n+1)} alpha^q_{n+1},  xc^q_n = (2 eps_q)^{-(n+1)} c^q_{n+1}
 //   alpha^c_{m+1} = sum_q eps_q^{m+1} sum_n C(m, n) xa^q_n     (gamma^c likewise from xc)
 // Lane m reads the real Pascal entry C(m, n) (consecutive per lane) and the
-// pre-scaled child coefficients (shared-memory broadcasts).
+// pre-scaled child coefficients (shared-memory broadcasts); the operator
+// tables are in shared memory (stage_tables), so after the children's loads
+// the cell's chain has no global round trip.
 template <int PT>
-__device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* __restrict__ c_iy,
-                         const int* __restrict__ first_child, const int* __restrict__ nchild,
-                         const double* __restrict__ pasT, const double2* __restrict__ eps,
-                         const double2* __restrict__ e2i, double2* __restrict__ mpole, double2* xa,
-                         double2* xc, int lane) {
-  const int f = first_child[c], nc = nchild[c];
+__device__ void m2m_cell(const M2MStatic& st, int p, const OpTables& T,
+                         double2* __restrict__ mpole, double2* xa, double2* xc, int lane) {
+  const int f = st.f, nc = st.nc;
   const int pw = p + 2;
   constexpr int NC = PT ? (PT + 31) / 32 : 2;   // coefficients per lane
   // all children's coefficients in flight at once (lane n: slots n, n-1 of both series)
   double2 an[4][NC], gn[4][NC], ap[4][NC];
-  int quad[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int q = f + min(i, nc - 1);
-    quad[i] = (c_ix[q] & 1) + 2 * (c_iy[q] & 1);
     const double2* mq = mpole + (size_t)q * 2 * p;
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc) {
@@ -271,16 +313,16 @@ __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* 
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     if (i < nc) {
-      const int xb = quad[i] & 1, yb = quad[i] >> 1;
+      const int xb = st.quad[i] & 1, yb = st.quad[i] >> 1;
       const double2 eb = make_double2(-(xb - 0.5), (yb - 0.5));   // conj(e)/s_q
-      const double2* Ei = e2i + quad[i] * pw;
+      const double2* Ei = T.e2i + st.quad[i] * pw;
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         const int n = lane + 32 * cc;
         if (n < p) {
           double2 cv = gn[i][cc];
           cmac(cv, cscale(eb, -(double)n), ap[i][cc]);
-          const double2 sc = __ldg(Ei + n + 1);
+          const double2 sc = Ei[n + 1];
           xa[i * p + n] = cmul(an[i][cc], sc);
           xc[i * p + n] = cmul(cv, sc);
         }
@@ -288,7 +330,7 @@ __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* 
     }
   }
   __syncwarp();
-  double2* out = mpole + (size_t)c * 2 * p;
+  double2* out = mpole + (size_t)st.c * 2 * p;
   for (int m = lane; m < p; m += 32) {
     double2 a[4], g[4];
 #pragma unroll
@@ -296,7 +338,7 @@ __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* 
 #pragma unroll
     for (int n = 0; n < pmax<PT>(); ++n) {
       if (!PT && n >= p) break;
-      const double cm = __ldg(pasT + n * p + m);   // C(m, n)
+      const double cm = T.pas[n * p + m];   // C(m, n)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         if (i < nc) {
@@ -312,7 +354,7 @@ __device__ void m2m_cell(int c, int p, const int* __restrict__ c_ix, const int* 
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (i < nc) {
-        const double2 em = __ldg(eps + quad[i] * pw + m + 1);
+        const double2 em = T.eps[st.quad[i] * pw + m + 1];
         cmac(sa, a[i], em);
         cmac(sg, g[i], em);
       }
@@ -515,13 +557,23 @@ m2m_level_kernel(int u0, int u1, const int* __restrict__ up_list, const int* __r
                  double2* __restrict__ mpole) {
   const int p = PT ? PT : p_rt;
   pdl_trigger();
-  pdl_wait();   // the children's multipoles (previous level / P2M)
-  extern __shared__ double2 up_sh[];   // per warp: pre-scaled children [2][4][p]
+  // tables | per warp: pre-scaled children [2][4][p]
+  extern __shared__ double2 up_sh[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* wb = up_sh + (size_t)w * 8 * p;
-  for (int k = u0 + blockIdx.x * kPassWarps + w; k < u1; k += gridDim.x * kPassWarps)
-    m2m_cell<PT>(up_list[k], p, c_ix, c_iy, first_child, nchild, pasT_g, eps_g, e2i_g, mpole, wb,
-                 wb + 4 * p, lane);
+  double2* wb = up_sh + tbl_doubles(p) / 2 + (size_t)w * 8 * p;
+  // tree-static data first (operator tables, this warp's first parent and
+  // its children), then wait for the children's multipoles (previous level
+  // / P2M): with PDL only the coefficient loads follow the wait
+  const OpTables T = stage_tables(reinterpret_cast<double*>(up_sh), p, pasT_g, eps_g, e2i_g);
+  int k = u0 + blockIdx.x * kPassWarps + w;
+  M2MStatic st{};
+  if (k < u1) st = m2m_static(up_list[k], c_ix, c_iy, first_child, nchild);
+  __syncthreads();
+  pdl_wait();
+  for (; k < u1; k += gridDim.x * kPassWarps) {
+    if (k != u0 + blockIdx.x * kPassWarps + w) st = m2m_static(up_list[k], c_ix, c_iy, first_child, nchild);
+    m2m_cell<PT>(st, p, T, mpole, wb, wb + 4 * p, lane);
+  }
 }
 
 // ------------------------------------------------------------ M2L (a7) + L2L (a8)
@@ -807,21 +859,36 @@ m2l_kernel(int c0, int c1, const int* __restrict__ clist, int64_t own_lo, int64_
 // top-down, one level at a time.
 // L2L of one cell c (its M2L result in local[c]) from its parent's final local
 // (separable form); one warp.
+// Tree-static part of a cell's L2L: the cell, its parent and its quadrant
+// (skip: no owned target below the cell).
+struct L2LStatic {
+  int c, P, quad;
+  bool skip;
+};
+__device__ __forceinline__ L2LStatic l2l_static(int c, int64_t own_lo, int64_t own_hi,
+                                                const int* __restrict__ c_start,
+                                                const int* __restrict__ c_count,
+                                                const int* __restrict__ c_ix,
+                                                const int* __restrict__ c_iy,
+                                                const int* __restrict__ c_parent) {
+  L2LStatic st;
+  st.c = c;
+  const int cs = c_start[c], ce = cs + c_count[c];
+  st.skip = ce <= own_lo || cs >= own_hi;
+  st.P = c_parent[c];
+  st.quad = (c_ix[c] & 1) + 2 * (c_iy[c] & 1);
+  return st;
+}
+
 template <int PT>
-__device__ __forceinline__ void l2l_cell(int c, int p, const int* __restrict__ c_ix,
-                                         const int* __restrict__ c_iy,
-                                         const int* __restrict__ c_parent,
-                                         const double2* __restrict__ eps_g,
-                                         const double2* __restrict__ e2i_g,
-                                         const double* __restrict__ pas_g,
+__device__ __forceinline__ void l2l_cell(const L2LStatic& st, int p, const OpTables& T,
                                          double2* __restrict__ local, double2* xl, double2* xg,
                                          int lane) {
   const int pw = p + 2;
   constexpr int NC = PT ? (PT + 31) / 32 : 2;   // coefficients per lane
-  const int P = c_parent[c];
-  const double2* lp = local + (size_t)P * 2 * p;
-  double2* out = local + (size_t)c * 2 * p;
-  const int quad = (c_ix[c] & 1) + 2 * (c_iy[c] & 1);
+  const double2* lp = local + (size_t)st.P * 2 * p;
+  double2* out = local + (size_t)st.c * 2 * p;
+  const int quad = st.quad;
   // loads first: parent coefficients (slots m, m+1 of lambda, m of gamma) and
   // this cell's own M2L result
   double2 pl[NC], pl1[NC], pg[NC], ol[NC], og[NC];
@@ -837,15 +904,15 @@ __device__ __forceinline__ void l2l_cell(int c, int p, const int* __restrict__ c
     og[cc] = ok ? out[p + m] : z;
   }
   const double2 epsb = make_double2(0.5 * ((quad & 1) - 0.5), -0.5 * ((quad >> 1) - 0.5));
-  const double2* E = eps_g + quad * pw;
-  const double2* Ei = e2i_g + quad * pw;
+  const double2* E = T.eps + quad * pw;
+  const double2* Ei = T.e2i + quad * pw;
 #pragma unroll
   for (int cc = 0; cc < NC; ++cc) {
     const int m = lane + 32 * cc;
     if (m < p) {
       double2 gv = pg[cc];
       cmac(gv, cscale(epsb, (double)(m + 1)), pl1[cc]);
-      const double2 em = __ldg(E + m);
+      const double2 em = E[m];
       xl[m] = cmul(pl[cc], em);
       xg[m] = cmul(gv, em);
     }
@@ -859,14 +926,14 @@ __device__ __forceinline__ void l2l_cell(int c, int p, const int* __restrict__ c
 #pragma unroll
       for (int m = 0; m < pmax<PT>(); ++m) {
         if (!PT && m >= p) break;
-        const double pc = __ldg(pas_g + m * p + k);   // C(m, k)
+        const double pc = T.pas[m * p + k];   // C(m, k)
         const double2 x = xl[m], y = xg[m];
         l.x = fma(x.x, pc, l.x);
         l.y = fma(x.y, pc, l.y);
         g.x = fma(y.x, pc, g.x);
         g.y = fma(y.y, pc, g.y);
       }
-      const double2 ek = __ldg(Ei + k);
+      const double2 ek = Ei[k];
       double2 al = ol[cc], ag = og[cc];
       cmac(al, l, ek);
       cmac(ag, g, ek);
@@ -886,17 +953,24 @@ l2l_level_kernel(int c0, int c1, const int* __restrict__ clist, int64_t own_lo, 
                  const double2* __restrict__ eps_g, const double2* __restrict__ e2i_g,
                  const double* __restrict__ pas_g, double2* __restrict__ local) {
   const int p = PT ? PT : p_rt;
-  extern __shared__ double2 l2_sh[];   // per warp: xl [p] | xg [p]
+  extern __shared__ double2 l2_sh[];   // tables | per warp: xl [p] | xg [p]
   pdl_trigger();
-  pdl_wait();   // the parents' final locals (previous level / M2L)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* xl = l2_sh + (size_t)w * 2 * p;
+  double2* xl = l2_sh + tbl_doubles(p) / 2 + (size_t)w * 2 * p;
   double2* xg = xl + p;
-  for (int k = c0 + blockIdx.x * kPassWarps + w; k < c1; k += gridDim.x * kPassWarps) {
-    const int c = clist ? clist[k] : k;
-    const int cs = c_start[c], ce = cs + c_count[c];
-    if (ce <= own_lo || cs >= own_hi) continue;   // no owned target below c
-    l2l_cell<PT>(c, p, c_ix, c_iy, c_parent, eps_g, e2i_g, pas_g, local, xl, xg, lane);
+  // tree-static data before the wait for the parents' final locals
+  const OpTables T = stage_tables(reinterpret_cast<double*>(l2_sh), p, pas_g, eps_g, e2i_g);
+  const int k0 = c0 + blockIdx.x * kPassWarps + w;
+  L2LStatic st{};
+  if (k0 < c1)
+    st = l2l_static(clist ? clist[k0] : k0, own_lo, own_hi, c_start, c_count, c_ix, c_iy, c_parent);
+  __syncthreads();
+  pdl_wait();   // the parents' final locals (previous level / M2L)
+  for (int k = k0; k < c1; k += gridDim.x * kPassWarps) {
+    if (k != k0)
+      st = l2l_static(clist ? clist[k] : k, own_lo, own_hi, c_start, c_count, c_ix, c_iy, c_parent);
+    if (st.skip) continue;   // no owned target below c
+    l2l_cell<PT>(st, p, T, local, xl, xg, lane);
   }
 }
 
@@ -918,15 +992,17 @@ m2m_subtree_kernel(int Ls, int nlev, int nsl, const int2* __restrict__ rng,
                    double2* __restrict__ mpole) {
   const int p = PT ? PT : p_rt;
   pdl_trigger();
-  pdl_wait();   // leaf multipoles (P2M)
   extern __shared__ double2 up_sh[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* wb = up_sh + (size_t)w * 8 * p;
+  double2* wb = up_sh + tbl_doubles(p) / 2 + (size_t)w * 8 * p;
+  const OpTables T = stage_tables(reinterpret_cast<double*>(up_sh), p, pasT_g, eps_g, e2i_g);
+  __syncthreads();
+  pdl_wait();   // leaf multipoles (P2M)
   for (int l = nlev - 1; l >= Ls; --l) {
     const int2 r = rng[(size_t)blockIdx.x * nsl + (l - Ls)];
     for (int k = r.x + w; k < r.y; k += kPassWarps)
-      m2m_cell<PT>(up_list[k], p, c_ix, c_iy, first_child, nchild, pasT_g, eps_g, e2i_g, mpole,
-                   wb, wb + 4 * p, lane);
+      m2m_cell<PT>(m2m_static(up_list[k], c_ix, c_iy, first_child, nchild), p, T, mpole, wb,
+                   wb + 4 * p, lane);
     __syncthreads();
   }
 }
@@ -942,16 +1018,18 @@ l2l_subtree_kernel(int Ls, int nlev, int nsl, const int2* __restrict__ rng, int6
   const int p = PT ? PT : p_rt;
   extern __shared__ double2 l2_sh[];
   pdl_trigger();
-  pdl_wait();   // the roots' final locals
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* xl = l2_sh + (size_t)w * 2 * p;
+  double2* xl = l2_sh + tbl_doubles(p) / 2 + (size_t)w * 2 * p;
   double2* xg = xl + p;
+  const OpTables T = stage_tables(reinterpret_cast<double*>(l2_sh), p, pas_g, eps_g, e2i_g);
+  __syncthreads();
+  pdl_wait();   // the roots' final locals
   for (int l = Ls + 1; l < nlev; ++l) {
     const int2 r = rng[(size_t)blockIdx.x * nsl + (l - Ls)];
     for (int c = r.x + w; c < r.y; c += kPassWarps) {
-      const int cs = c_start[c], ce = cs + c_count[c];
-      if (ce <= own_lo || cs >= own_hi) continue;
-      l2l_cell<PT>(c, p, c_ix, c_iy, c_parent, eps_g, e2i_g, pas_g, local, xl, xg, lane);
+      const L2LStatic st = l2l_static(c, own_lo, own_hi, c_start, c_count, c_ix, c_iy, c_parent);
+      if (st.skip) continue;
+      l2l_cell<PT>(st, p, T, local, xl, xg, lane);
     }
     __syncthreads();
   }
@@ -1418,7 +1496,7 @@ int launch_upward(ddm_ctx_s* ctx, ddm_tree_s* t, const int* perm_in, const doubl
   const std::vector<int>& uoff =
       scope == kUpFull ? t->up_level_off : scope == kUpOwn ? t->up_own_off : t->up_strad_off;
   const CellGeom cg{t->x_min, t->y_min, t->W};
-  const size_t shm = (size_t)kPassWarps * 8 * p * sizeof(double2);
+  const size_t shm = (size_t)tbl_doubles(p) * sizeof(double) + (size_t)kPassWarps * 8 * p * sizeof(double2);
   const size_t shp = (size_t)kPassWarps * 32 * 17 * sizeof(double2);
   int rc = DDM_OK;
 #define DDM_L(PT)                                                                               \
@@ -1534,7 +1612,7 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s, bool use_x) {
   const size_t wstride = tc ? (size_t)2 * kM2LBatch * kXStride : 3 * (size_t)p + 1;
   const size_t shm = ((tc ? 0 : (size_t)kNOffsets * (p + 2)) + (ndbl + 1) / 2 +
                       (size_t)kPassWarps * wstride) * sizeof(double2);
-  const size_t shm2 = (size_t)kPassWarps * 2 * p * sizeof(double2);
+  const size_t shm2 = (size_t)tbl_doubles(p) * sizeof(double) + (size_t)kPassWarps * 2 * p * sizeof(double2);
   int rc = DDM_OK;
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \

@@ -5,6 +5,7 @@
 // over interaction lists, L2L), final L2P + P2P for self and neighbour cells.
 // The paper's Chebyshev interpolation (bbFMM) is replaced by complex-variable
 // (Kolosov–Muskhelishvili) expansions of the constant-element influence.
+#include <cstring>
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -306,6 +307,12 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
     DDM_CUDA(ctx, cudaStreamWaitEvent(sn, ctx->ev_fork, 0));
   }
 
+  // DDM_TIMING_SKIP=near|far (scripts/timeline.py only; the result is then
+  // wrong): launch one side of the fork alone, to time the other's span
+  static const int skip = [] {
+    const char* e = getenv("DDM_TIMING_SKIP");
+    return !e ? 0 : !strcmp(e, "near") ? 1 : !strcmp(e, "far") ? 2 : 0;
+  }();
   // near field: P2P work items of the owned leaves
   const bool leaf_p2p = !poro && use_leaf_p2p();
   // X lists: the elastic series FMM expands the coarser
@@ -320,14 +327,16 @@ static int fmm_matvec_launch(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* 
     DDM_CUDA(ctx, cudaEventRecord(ctx->ev_p2l, sn));
   }
   stage_begin(ctx, DDM_ST_P2P, sn);
-  rc = poro       ? launch_poro_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, PP, sn)
+  rc = skip == 1  ? DDM_OK
+       : poro     ? launch_poro_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, PP, sn)
        : leaf_p2p ? launch_p2p_leaf(ctx, t, gc, sn, use_x)
                   : launch_p2p(ctx, t, t->item_lo_owned, t->item_hi_owned, gc, sn);
   if (rc) return rc;
   stage_end(ctx, DDM_ST_P2P, sn);
   DDM_CUDA(ctx, cudaEventRecord(ctx->ev_near, sn));
 
-  if (bb) {
+  if (skip == 2) {
+  } else if (bb) {
     if ((rc = launch_bb_far(ctx, t, bb_n, perm_in ? t->d_sorted : D, ncomp, gc, sf))) return rc;
   } else {
   // upward pass: P2M on all leaves, M2M level by level; on several ranks

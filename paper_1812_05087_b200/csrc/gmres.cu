@@ -94,7 +94,36 @@ multi_dot(const double* __restrict__ V, int64_t ld, const double* __restrict__ w
 // the same order whatever the row range (deterministic, rank independent).
 // With kd (captured step): nvec = *kd + 1, c += pass ? k + 1 : 0, and the
 // norm goes to out[2 (k+1) + 1].
+// DDM_V_KEEP=1: the CGS passes read the Krylov basis with an L2 evict_last
+// cache policy (createpolicy + ld.L2::cache_hint), so the basis stays in L2
+// across the operator apply, whose streamed data (the poroelastic near-field
+// cache, the preconditioner blocks) is read evict-first
+#ifndef DDM_V_KEEP
+#define DDM_V_KEEP 1
+#endif
+__device__ __forceinline__ uint64_t v_policy() {
+  uint64_t pol = 0;
+#if DDM_V_KEEP
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  return pol;
+}
+__device__ __forceinline__ double v_ld(const double* a, uint64_t pol) {
+#if DDM_V_KEEP
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+#else
+  (void)pol;
+  return __ldg(a);
+#endif
+}
+
 constexpr int kAxRows = 64, kAxGroups = 4;
+#ifndef DDM_AX_UNROLL
+#define DDM_AX_UNROLL 4
+#endif
+constexpr int kAxU = DDM_AX_UNROLL;   // loads in flight per thread (multiple of 4)
 
 // DGKS (captured step, kd != nullptr, dgks > 0): pass 0 also sums ||w||^2
 // before the update into out[2 (k+1)] and sets out[2 (k+1) + 2] = 1 when the
@@ -123,6 +152,7 @@ cgs_axpy(const double* __restrict__ V, int64_t ld, int nvec, const double* __res
     }
   }
   const bool track0 = NORM && dgks > 0.0 && pass == 0 && kd;
+  const uint64_t pol = v_policy();
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) sc[i] = c[i];
   __syncthreads();
   const int r = threadIdx.x % kAxRows, q = threadIdx.x / kAxRows;
@@ -132,14 +162,14 @@ cgs_axpy(const double* __restrict__ V, int64_t ld, int nvec, const double* __res
     double a[4] = {0.0, 0.0, 0.0, 0.0};
     const double* v = V + j;
     int i = q;
-    for (; i + 3 * kAxGroups < nvec; i += 4 * kAxGroups) {
-      double t[4];
+    for (; i + (kAxU - 1) * kAxGroups < nvec; i += kAxU * kAxGroups) {
+      double t[kAxU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) t[u] = __ldg(v + (int64_t)(i + u * kAxGroups) * ld);
+      for (int u = 0; u < kAxU; ++u) t[u] = v_ld(v + (int64_t)(i + u * kAxGroups) * ld, pol);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = fma(t[u], sc[i + u * kAxGroups], a[u]);
+      for (int u = 0; u < kAxU; ++u) a[u & 3] = fma(t[u], sc[i + u * kAxGroups], a[u & 3]);
     }
-    for (int u = 0; i < nvec; i += kAxGroups, ++u) a[u] = fma(__ldg(v + (int64_t)i * ld), sc[i], a[u]);
+    for (int u = 0; i < nvec; i += kAxGroups, ++u) a[u & 3] = fma(v_ld(v + (int64_t)i * ld, pol), sc[i], a[u & 3]);
     acc = (a[0] + a[1]) + (a[2] + a[3]);
   }
   red[q][r] = acc;
@@ -201,7 +231,14 @@ cgs_axpy(const double* __restrict__ V, int64_t ld, int nvec, const double* __res
 // reduce-scatter (9 shuffles for 8 sums), the 32 warps' sums added in warp
 // order into one partial per (vector, CTA); the last CTA (ticket) sums each
 // vector's <= 128 partials in CTA order.  Deterministic.
-constexpr int kRowT = 512, kRowsCta = kRowT, kRowMaxCta = 128, kRowChunk = 256;
+#ifndef DDM_ROW_T
+#define DDM_ROW_T 512
+#endif
+#ifndef DDM_ROW_UPD
+#define DDM_ROW_UPD 16   // 0: the update loop of cgs_rows<1> as 2 chains x unroll 8; U > 0: U loads at once
+#endif
+constexpr int kRowT = DDM_ROW_T, kRowsCta = kRowT, kRowMaxCta = kRowT >= 512 ? 128 : 256,
+              kRowChunk = 256;
 
 // 8 per-lane values -> lane l holds the warp sum of value
 // v = 4 ((l >> 4) & 1) + 2 ((l >> 3) & 1) + ((l >> 2) & 1)
@@ -238,6 +275,7 @@ cgs_rows(const double* __restrict__ V, int64_t ld, int64_t len, double* __restri
   __shared__ bool last;
   const int k = *kd, nvec = k + 1, nb = gridDim.x;
   const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
+  const uint64_t pol = v_policy();
   const int64_t j = (int64_t)blockIdx.x * kRowsCta + t;
   const bool ok = j < len;
   const double* Vj = V + (ok ? j : 0);
@@ -246,12 +284,31 @@ cgs_rows(const double* __restrict__ V, int64_t ld, int64_t len, double* __restri
     const double* sc = dh;   // pass-0 coefficients (broadcast loads)
     double a0 = 0.0, a1 = 0.0;
     int i = 0;
+#if DDM_ROW_UPD > 0
+    {
+      double a2 = 0.0, a3 = 0.0;
+      for (; i + DDM_ROW_UPD <= nvec; i += DDM_ROW_UPD) {
+        double tv[DDM_ROW_UPD];
+#pragma unroll
+        for (int u = 0; u < DDM_ROW_UPD; ++u) tv[u] = v_ld(Vj + (int64_t)(i + u) * ld, pol);
+#pragma unroll
+        for (int u = 0; u < DDM_ROW_UPD; u += 4) {
+          a0 = fma(tv[u], __ldg(sc + i + u), a0);
+          a1 = fma(tv[u + 1], __ldg(sc + i + u + 1), a1);
+          a2 = fma(tv[u + 2], __ldg(sc + i + u + 2), a2);
+          a3 = fma(tv[u + 3], __ldg(sc + i + u + 3), a3);
+        }
+      }
+      a0 += a2;
+      a1 += a3;
+    }
+#endif
 #pragma unroll 8
     for (; i + 1 < nvec; i += 2) {
-      a0 = fma(__ldg(Vj + (int64_t)i * ld), __ldg(sc + i), a0);
-      a1 = fma(__ldg(Vj + (int64_t)(i + 1) * ld), __ldg(sc + i + 1), a1);
+      a0 = fma(v_ld(Vj + (int64_t)i * ld, pol), __ldg(sc + i), a0);
+      a1 = fma(v_ld(Vj + (int64_t)(i + 1) * ld, pol), __ldg(sc + i + 1), a1);
     }
-    if (i < nvec) a0 = fma(__ldg(Vj + (int64_t)i * ld), __ldg(sc + i), a0);
+    if (i < nvec) a0 = fma(v_ld(Vj + (int64_t)i * ld, pol), __ldg(sc + i), a0);
     wr = 0.0;
     if (ok) {
       wr = w[j] - (a0 + a1);
@@ -273,7 +330,7 @@ cgs_rows(const double* __restrict__ V, int64_t ld, int64_t len, double* __restri
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
           const int i = g0 + 8 * q + v;
-          a[q][v] = i < c1 ? __ldg(Vj + (int64_t)i * ld) : 0.0;
+          a[q][v] = i < c1 ? v_ld(Vj + (int64_t)i * ld, pol) : 0.0;
         }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -505,6 +562,20 @@ chunk_invert(const int2* __restrict__ chunks, const int64_t* __restrict__ off, i
 // the groups in a fixed order.
 constexpr int kApplyThreads = 256;
 
+// DDM_PC_STREAM=1: the inverse blocks are read with the streaming (evict-first)
+// cache hint, so the once-per-step 46 MB (config 3) does not push the Krylov
+// basis out of L2
+#ifndef DDM_PC_STREAM
+#define DDM_PC_STREAM 1
+#endif
+__device__ __forceinline__ double2 pc_ld(const double2* p) {
+#if DDM_PC_STREAM
+  return __ldcs(p);
+#else
+  return __ldg(p);
+#endif
+}
+
 // y_rows (+)= Ai xs for one chunk (d rows, column-major inverse with even
 // leading dimension ld): thread (row pair rp, column group g) accumulates
 // double2 rows (2 rp, 2 rp + 1) over the columns c = g, g + G, ... with four
@@ -524,7 +595,7 @@ __device__ __forceinline__ void chunk_mv(const double* __restrict__ Ai, int d,
     for (; c + 3 * G < d; c += 4 * G) {
       double2 v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldg(A2 + (size_t)(c + u * G) * RP + rp);
+      for (int u = 0; u < 4; ++u) v[u] = pc_ld(A2 + (size_t)(c + u * G) * RP + rp);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const double xv = xs[c + u * G];
@@ -533,7 +604,7 @@ __device__ __forceinline__ void chunk_mv(const double* __restrict__ Ai, int d,
       }
     }
     for (int u = 0; c < d; c += G, ++u) {
-      const double2 v = __ldg(A2 + (size_t)c * RP + rp);
+      const double2 v = pc_ld(A2 + (size_t)c * RP + rp);
       const double xv = xs[c];
       a[u & 3].x = fma(v.x, xv, a[u & 3].x);
       a[u & 3].y = fma(v.y, xv, a[u & 3].y);

@@ -1041,6 +1041,20 @@ poro_near_build_kernel(int nown, const int* __restrict__ order, const int4* __re
 // poro_p2p_kernel.
 constexpr int kApplyWarps = 8;
 
+// DDM_NC_STREAM=1: the near-field matrix cache (134 MB on config 3, read once
+// per matvec) is read with the streaming (evict-first) cache hint, so it does
+// not push the GMRES Krylov basis out of L2 between Arnoldi steps
+#ifndef DDM_NC_STREAM
+#define DDM_NC_STREAM 1
+#endif
+__device__ __forceinline__ double nc_ld(const double* p) {
+#if DDM_NC_STREAM
+  return __ldcs(p);
+#else
+  return __ldg(p);
+#endif
+}
+
 __global__ void __launch_bounds__(kApplyWarps * 32)
 poro_near_apply_kernel(const int* __restrict__ order, const int4* __restrict__ items,
                        int item_lo, const int* __restrict__ u_off, const int* __restrict__ u_lo,
@@ -1071,9 +1085,9 @@ poro_near_apply_kernel(const int* __restrict__ order, const int4* __restrict__ i
         const double* bb = blk0 + ((int64_t)jpos * kTgtGroup + tl) * 9;
         const double* d = src + (int64_t)(lo + j) * kPoroStride + 5;
         const double d0 = __ldg(d), d1 = __ldg(d + 1), d2 = __ldg(d + 2);
-        os = fma(__ldg(bb + 0), d0, fma(__ldg(bb + 1), d1, fma(__ldg(bb + 2), d2, os)));
-        on = fma(__ldg(bb + 3), d0, fma(__ldg(bb + 4), d1, fma(__ldg(bb + 5), d2, on)));
-        op = fma(__ldg(bb + 6), d0, fma(__ldg(bb + 7), d1, fma(__ldg(bb + 8), d2, op)));
+        os = fma(nc_ld(bb + 0), d0, fma(nc_ld(bb + 1), d1, fma(nc_ld(bb + 2), d2, os)));
+        on = fma(nc_ld(bb + 3), d0, fma(nc_ld(bb + 4), d1, fma(nc_ld(bb + 5), d2, on)));
+        op = fma(nc_ld(bb + 6), d0, fma(nc_ld(bb + 7), d1, fma(nc_ld(bb + 8), d2, op)));
       }
       pos += len;
     }

@@ -1,2 +1,3 @@
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/rcp_probe scripts/micro/rcp_probe.cu && /tmp/rcp_probe
-TUNE_SERIAL=0 python scripts/tune.py base DDM_P2P_RCP2=1 base DDM_P2P_RCP2=1 2>&1 | grep -v Warn
+timeout 900 python -m pytest tests/test_gpu_matvec.py tests/test_gpu_partition.py tests/test_gpu_poro.py -x -q -k "parity or partition or sim or history_small or gmres_cfg4" 2>&1 | tail -2
+for cfg in 3 4 5; do echo "cfg $cfg"; python scripts/timeline.py $cfg 2>&1 | grep step; done
+GMRES_CFGS=2,3 python scripts/gmres_timing.py 3 2>&1 | grep solve

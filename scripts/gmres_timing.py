@@ -14,7 +14,7 @@ from synth import CONFIGS, make_config
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 ctx = D.Context(0)
 f = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
-for cfg in (2, 3):
+for cfg in [int(c) for c in os.environ.get("GMRES_CFGS", "2,3").split(",")]:
     c = CONFIGS[cfg]
     g = make_config(cfg)
     mat = D.material_from_dict(c["material"])
