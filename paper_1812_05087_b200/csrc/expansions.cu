@@ -630,7 +630,7 @@ __device__ void m2l_cell_tc(int vb, int ve, const int* __restrict__ v_idx,
                             const unsigned char* __restrict__ v_cls,
                             const double2* __restrict__ mpole, const double2* __restrict__ w_g,
                             const double* sh_afr, double* X, double2* out_l, double2* out_g,
-                            int lane) {
+                            int lane, int sub = 0, int S = 1) {
   constexpr int p = PT, pw = PT + 2, P2 = 2 * PT;
   constexpr int MT = (PT + 7) / 8, KS = (PT + 4) / 4, KB = 4 * KS;
   double2 acc[MT];
@@ -644,7 +644,8 @@ __device__ void m2l_cell_tc(int vb, int ve, const int* __restrict__ v_idx,
       my_src = v_idx[vc + lane];
       my_cls = v_cls[vc + lane];
     }
-    for (int b0 = 0; b0 < K; b0 += kM2LBatch) {
+    // S warps share the cell: warp `sub` takes batches sub, sub + S, ...
+    for (int b0 = sub * kM2LBatch; b0 < K; b0 += S * kM2LBatch) {
       const int nb = min(kM2LBatch, K - b0);
       // phase 1: lane n (rounds of 32 over n < KB) loads slots n, n-1 of every
       // pair of the batch at once (coalesced across lanes), then writes the
@@ -800,9 +801,10 @@ m2l_kernel(int c0, int c1, const int* __restrict__ clist, int64_t own_lo, int64_
            const int* __restrict__ c_start, const int* __restrict__ c_count, int p_rt,
            const double2* __restrict__ w_g, const double* __restrict__ pm2l_g,
            const double2* __restrict__ mpole, double2* __restrict__ local,
-           const int* __restrict__ x_slot, const double2* __restrict__ local_x) {
+           const int* __restrict__ x_slot, const double2* __restrict__ local_x, int S) {
   const int p = PT ? PT : p_rt;
   constexpr bool TC = PT > 0 && PT <= 32;   // tensor-core M2L
+  if (!TC) S = 1;
   constexpr int MT = TC ? (PT + 7) / 8 : 1, KS = TC ? (PT + 4) / 4 : 1;
   const int pw = p + 2;
   extern __shared__ double2 dn_sh[];
@@ -831,15 +833,38 @@ m2l_kernel(int c0, int c1, const int* __restrict__ clist, int64_t own_lo, int64_
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t wstride = TC ? (size_t)2 * kM2LBatch * kXStride : 3 * (size_t)p + 1;
   double2* ring = wbuf + (size_t)w * wstride;
-  for (int k = c0 + blockIdx.x * kPassWarps + w; k < c1; k += gridDim.x * kPassWarps) {
+  // S > 1 (small trees): S consecutive warps share a cell,
+  // each takes every S-th batch of its V list; their partial series meet in
+  // shared memory and the first warp sums them in warp order (named barrier
+  // per cell slot).  S is fixed per tree: results do not depend on the rank.
+  const int slot = w / S, sub = w - slot * S, per_cta = kPassWarps / S;
+  double2* psum = wbuf + (size_t)kPassWarps * wstride + (size_t)w * 2 * p;
+  for (int k = c0 + blockIdx.x * per_cta + slot; k < c1; k += gridDim.x * per_cta) {
     const int c = clist ? clist[k] : k;   // clist: this rank's cells (several ranks)
     const int cs = c_start[c], ce = cs + c_count[c];
     if (ce <= own_lo || cs >= own_hi) continue;   // subtree outside this rank's targets
     double2* out = local + (size_t)c * 2 * p;
     const int vb = v_off[c], ve = v_off[c + 1];
     if constexpr (TC) {
-      m2l_cell_tc<PT>(vb, ve, v_idx, v_cls, mpole, w_g, sh_pm2l, reinterpret_cast<double*>(ring),
-                      out, out + p, lane);
+      if (S == 1) {
+        m2l_cell_tc<PT>(vb, ve, v_idx, v_cls, mpole, w_g, sh_pm2l, reinterpret_cast<double*>(ring),
+                        out, out + p, lane);
+      } else {
+        m2l_cell_tc<PT>(vb, ve, v_idx, v_cls, mpole, w_g, sh_pm2l, reinterpret_cast<double*>(ring),
+                        psum, psum + p, lane, sub, S);
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * S) : "memory");
+        if (sub == 0) {
+          const double2* p0 = psum;
+          for (int m = lane; m < 2 * p; m += 32) {
+            double2 v = p0[m];
+            for (int s2 = 1; s2 < S; ++s2) v = cadd(v, p0[(size_t)s2 * 2 * p + m]);
+            out[m] = v;
+          }
+          __syncwarp();
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * S) : "memory");
+        if (sub != 0) continue;
+      }
     } else {
       m2l_cell_dfma(p, vb, ve, v_idx, v_cls, mpole, sh_w, sh_pm2l, ring, ring + p, ring + 2 * p,
                     out, out + p, lane);
@@ -1611,13 +1636,20 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s, bool use_x) {
   const size_t ndbl = tc ? (size_t)((p + 7) / 8) * ((p + 4) / 4) * 32 : (size_t)(p + 1) * p;
   const size_t wstride = tc ? (size_t)2 * kM2LBatch * kXStride : 3 * (size_t)p + 1;
   const size_t shm = ((tc ? 0 : (size_t)kNOffsets * (p + 2)) + (ndbl + 1) / 2 +
-                      (size_t)kPassWarps * wstride) * sizeof(double2);
+                      (size_t)kPassWarps * wstride + (tc ? (size_t)kPassWarps * 2 * p : 0)) *
+                     sizeof(double2);
+  // warps per cell (small trees: a cell's V list over S warps, §4.4d); a
+  // property of the whole tree, so every rank sums the same way
+  static const int m2l_s_env = env_int("DDM_M2L_SPLIT", -1);
+  const int64_t ncell2 = (int64_t)t->ncells - t->level_off[2];
+  const int S = !tc ? 1 : m2l_s_env >= 0 ? std::max(1, std::min(4, m2l_s_env))
+                        : ncell2 <= 768 ? 4 : 1;
   const size_t shm2 = (size_t)tbl_doubles(p) * sizeof(double) + (size_t)kPassWarps * 2 * p * sizeof(double2);
   int rc = DDM_OK;
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \
     if ((rc = set_smem(ctx, m2l_kernel<PT>, shm))) return rc;                                   \
-    const int nb = pass_grid(ctx, (const void*)m2l_kernel<PT>, shm, c1 - c0, env_int("DDM_M2L_CAP", -1)); \
+    const int nb = pass_grid(ctx, (const void*)m2l_kernel<PT>, shm, (c1 - c0) * S, env_int("DDM_M2L_CAP", -1)); \
     stage_begin(ctx, DDM_ST_M2L, s);                                                            \
     DDM_CUDA(ctx, launch_pdl(use_pdl(t) && !use_x, m2l_kernel<PT>, nb, kPassWarps * 32, shm, s, \
                              c0, c1,                                                           \
@@ -1626,7 +1658,7 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s, bool use_x) {
                              (const unsigned char*)t->v_cls, (const int*)t->c_start,           \
                              (const int*)t->c_count, p, (const double2*)t->op_w,               \
                              (const double*)t->op_pm2l, (const double2*)t->mpole, t->local,    \
-                             xsl, lxp));                                                       \
+                             xsl, lxp, S));                                                    \
     stage_end(ctx, DDM_ST_M2L, s);                                                              \
     if ((rc = set_smem(ctx, l2l_level_kernel<PT>, shm2))) return rc;                            \
     stage_begin(ctx, DDM_ST_L2L, s);                                                            \
