@@ -50,6 +50,14 @@ def main(cfg):
         b = D.farfield_rhs(ctx, f(g.beta), 3, ld["p_f"], ld["sH"], ld["sh"], net=True,
                            b_p=ld["sh"] + ld["p_f"] - ld["p0"])
         kw = dict(dt=tau, restart=3000, max_iter=6000)
+    elif cfg == 4:   # the first solve of the config-4 march
+        dt = c["dt"]
+        tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=c["leaf"],
+                      order_p=c["p_star"],
+                      min_leaf_side=bench._poro_rc(c, g, (c["steps"] + 1) * dt))
+        b = D.farfield_rhs(ctx, f(g.beta), 3, ld["p_f"], ld["sH"], ld["sh"], net=False,
+                           b_p=ld["p_f"] - ld["p0"])
+        kw = dict(dt=dt, restart=3000, max_iter=6000)
     else:
         tree = D.Tree(ctx, f(g.xc), f(g.yc), f(g.half_len), f(g.beta), leaf_size=c["leaf"],
                       order_p=20)
