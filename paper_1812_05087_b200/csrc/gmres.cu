@@ -266,17 +266,17 @@ __device__ __forceinline__ double warp_rs8(const double (&a)[8], int lane) {
 // MODE 1: w -= V c with c = dh[0 .. k], then out = V^T w -> dh[k+1 .. 2k+1].
 // (The second update + norm stays on cgs_axpy: a row-blocked version measured
 // slower, config 3 39.2 -> 41.0 ms.)
-template <int MODE>
-__global__ void __launch_bounds__(kRowT)
+template <int MODE, int RT = kRowT>
+__global__ void __launch_bounds__(RT)
 cgs_rows(const double* __restrict__ V, int64_t ld, int64_t len, double* __restrict__ w,
          const int* __restrict__ kd, double* __restrict__ dh, double* __restrict__ part,
          unsigned* __restrict__ ticket) {
-  __shared__ double red[kRowT / 32][kRowChunk];   // per-warp sums of a chunk of vectors
+  __shared__ double red[RT / 32][kRowChunk];   // per-warp sums of a chunk of vectors
   __shared__ bool last;
   const int k = *kd, nvec = k + 1, nb = gridDim.x;
   const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
   const uint64_t pol = v_policy();
-  const int64_t j = (int64_t)blockIdx.x * kRowsCta + t;
+  const int64_t j = (int64_t)blockIdx.x * RT + t;
   const bool ok = j < len;
   const double* Vj = V + (ok ? j : 0);
   double wr;
@@ -342,10 +342,10 @@ cgs_rows(const double* __restrict__ V, int64_t ld, int64_t len, double* __restri
       }
     }
     __syncthreads();
-    for (int i = c0 + t; i < c1; i += kRowT) {
+    for (int i = c0 + t; i < c1; i += RT) {
       double sum = 0.0;
 #pragma unroll
-      for (int q = 0; q < kRowT / 32; ++q) sum += red[q][i - c0];
+      for (int q = 0; q < RT / 32; ++q) sum += red[q][i - c0];
       part[(int64_t)i * nb + blockIdx.x] = sum;
     }
     __syncthreads();
@@ -359,7 +359,7 @@ cgs_rows(const double* __restrict__ V, int64_t ld, int64_t len, double* __restri
     __threadfence();
     // warp wp: vectors wp + NW r; lane: CTAs lane + 32 q (4 vectors' loads
     // in flight at once)
-    constexpr int NW = kRowT / 32, Q = kRowMaxCta / 32;
+    constexpr int NW = RT / 32, Q = (RT >= 512 ? 128 : 256) / 32;
     for (int r0 = 0; wp + NW * r0 < nvec; r0 += 4) {
       double v[4][Q];
 #pragma unroll
@@ -816,17 +816,31 @@ struct Gm {
       const char* e = getenv("DDM_GMRES_ROWS");
       return e ? atoi(e) : 1;
     }();
-    const int nbr = (int)((nloc + kRowsCta - 1) / kRowsCta);
+    // rows per CTA: 512, or 256 / 128 on smaller systems (>= 32 CTAs)
+    static const int rowt_env = [] {
+      const char* e = getenv("DDM_GMRES_ROWT");
+      return e ? atoi(e) : 0;
+    }();
+    int rt = rowt_env > 0 ? rowt_env
+             : nloc >= 32 * 512 ? 512 : nloc >= 32 * 256 ? 256 : 128;
+    if (rt != 128 && rt != 256) rt = 512;
+    const int nbr = (int)((nloc + rt - 1) / rt);
+    const int rmax = rt >= 512 ? 128 : 256;
     // (small systems keep the vector-parallel kernels: a few row CTAs cannot
     // keep enough loads in flight)
-    if (rows_env && !use_dgks && nbr >= 32 && nbr <= kRowMaxCta && (int64_t)(m + 1) * nbr <= part_cap) {
+    if (rows_env && !use_dgks && nbr >= (rt == 512 ? 32 : 24) && nbr <= rmax &&
+        (int64_t)(m + 1) * nbr <= part_cap) {
       // row-blocked: dots, fused (update + second-pass dots), update + norm
       if (getenv("DDM_GMRES_TRACE")) fprintf(stderr, "[gmres] row-blocked CGS2, %d CTAs, m %d\n", nbr, m);
       if (rows_env == 2)
         multi_dot<<<dim3(b, gy), kDotThreads, 0, s>>>(V, nloc, w, nloc, b, part, ticket, dh, kd, 0);
       else
-        cgs_rows<0><<<nbr, kRowT, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket);
-      cgs_rows<1><<<nbr, kRowT, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket);
+        rt == 512 ? cgs_rows<0, 512><<<nbr, 512, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket)
+        : rt == 256 ? cgs_rows<0, 256><<<nbr, 256, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket)
+                    : cgs_rows<0, 128><<<nbr, 128, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket);
+      rt == 512 ? cgs_rows<1, 512><<<nbr, 512, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket)
+      : rt == 256 ? cgs_rows<1, 256><<<nbr, 256, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket)
+                  : cgs_rows<1, 128><<<nbr, 128, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket);
       cgs_axpy<true><<<ga, kAxRows * kAxGroups, shc, s>>>(V, nloc, 0, dh, -1.0, w, nloc, part,
                                                          ticket_norm, dh, kd, 1, 0.0);
       DDM_CUDA(ctx, cudaGetLastError());
@@ -1023,7 +1037,7 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
   }
   if (use_pc && mat->kind == 1 && !(dt > 0))
     return set_error(ctx, DDM_ERR_ARG, "poroelastic GMRES needs dt > 0");
-  const int64_t part_need = std::max<int64_t>((int64_t)(m + 2) * std::max<int64_t>(256, nloc / kRowsCta + 1),
+  const int64_t part_need = std::max<int64_t>((int64_t)(m + 2) * std::max<int64_t>(256, nloc / 128 + 1),
                                               2 * (nloc / 64 + 2));
   if (t->gm_part_n < part_need) {
     if (t->gm_part) cudaFree(t->gm_part);
