@@ -362,11 +362,12 @@ def run_ours(args):
                         "traffic": _ncu_traffic("p2p_leaf_kernel"),
                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one "
                                           "ncu --set full capture (profiles/ncu_traffic.json)",
-                        "traffic_note": "algorithmic: 80-B source records once (~85 MB) + targets "
-                                        "(~48 MB); leaf CTAs launched heaviest-first re-read "
-                                        "shared U-list records from DRAM (~200 MB; 127 MB in "
-                                        "Morton order, DDM_P2P_ORDER=0, 1.2 % slower step): "
-                                        "the kernel is fp64-bound, ~0.34 TB/s of DRAM",
+                        "traffic_note": "algorithmic: 96-B source records once (~100 MB) + "
+                                        "targets (~48 MB); leaf CTAs launched heaviest-first "
+                                        "re-read shared U-list records from DRAM (~264 MB; "
+                                        "Morton order, DDM_P2P_ORDER=0, reads about the "
+                                        "algorithmic bytes at a 1.2 % slower step): the kernel "
+                                        "is fp64-bound, ~0.45 TB/s of DRAM",
                         "peak_source": "measured DFMA-chain probe (ddm_probe_fp64) on this GPU",
                         "flop_per_pair": FLOP_PER_PAIR,
                         "fp64_pipe_frac": (owned_pairs * FP64_INSTR_PER_PAIR / (p2p_ms * 1e-3)
@@ -454,7 +455,7 @@ def kernel_rooflines(tree, cnt, stages, tree_stages, p, fp64_peak, world):
                 f"({el_w} pairs)"),
         "p2p": ("fp64", FLOP_PER_PAIR * cnt["NEAR_PAIRS_P2P"] / world, "flop",
                 "45 flop per near pair (the round-1 node-sharing record update as written; "
-                "the round-2 kernel executes 43 with 26 fp64 instructions)"),
+                "the round-2 kernel executes 43 with 25 fp64 instructions, DESIGN.md §4.2c)"),
         "final": ("hbm", 52.0 * n, "B", "52 B/elem: near (16) + far (16) + perm (4) in, y (16) out"),
     }
     out = {}
