@@ -224,7 +224,7 @@ def history_rhs(ctx, tree, mat, dt: float, D_hist: torch.Tensor, b: torch.Tensor
 
 
 def march_guess(ctx, D_hist: torch.Tensor, order: int, x: torch.Tensor, stream=None) -> torch.Tensor:
-    """ddm_march_guess: x = polynomial extrapolation (order <= 3) of the last
+    """ddm_march_guess: x = polynomial extrapolation (order <= 5) of the last
     solutions in D_hist [h, ...] (h = 0 -> x = 0)."""
     h = D_hist.shape[0]
     ptr = _dev(D_hist, "D_hist") if h > 0 else 0

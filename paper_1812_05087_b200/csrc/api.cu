@@ -790,11 +790,23 @@ __global__ void sub_kernel(int64_t len, const double* a, const double* __restric
 // each product and sum rounded separately in the listed order
 __global__ void march_guess_kernel(int64_t len, int q, const double* __restrict__ d1,
                                    const double* __restrict__ d2, const double* __restrict__ d3,
-                                   const double* __restrict__ d4, double* __restrict__ x) {
+                                   const double* __restrict__ d4, const double* __restrict__ d5,
+                                   const double* __restrict__ d6, double* __restrict__ x) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= len) return;
   double v;
-  if (q == 3)        // 4 D1 - 6 D2 + 4 D3 - D4
+  if (q == 5)        // 6 D1 - 15 D2 + 20 D3 - 15 D4 + 6 D5 - D6
+    v = __dsub_rn(__dadd_rn(__dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(6.0, d1[i]), __dmul_rn(15.0, d2[i])),
+                                                __dmul_rn(20.0, d3[i])),
+                                      __dmul_rn(15.0, d4[i])),
+                            __dmul_rn(6.0, d5[i])),
+                  d6[i]);
+  else if (q == 4)   // 5 D1 - 10 D2 + 10 D3 - 5 D4 + D5
+    v = __dadd_rn(__dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(5.0, d1[i]), __dmul_rn(10.0, d2[i])),
+                                      __dmul_rn(10.0, d3[i])),
+                            __dmul_rn(5.0, d4[i])),
+                  d5[i]);
+  else if (q == 3)   // 4 D1 - 6 D2 + 4 D3 - D4
     v = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(4.0, d1[i]), __dmul_rn(6.0, d2[i])),
                             __dmul_rn(4.0, d3[i])), d4[i]);
   else if (q == 2)   // 3 (D1 - D2) + D3
@@ -878,7 +890,7 @@ int ddm_history_rhs(ddm_ctx_t ctx, ddm_tree_t t, const ddm_material* mat, double
 int ddm_march_guess(ddm_ctx_t ctx, int h, const double* D_hist, int64_t len, int order,
                     double* x, void* stream) {
   if (!ctx) return DDM_ERR_ARG;
-  if (h < 0 || len < 0 || order < 0 || !x || (h > 0 && !D_hist))
+  if (h < 0 || len < 0 || order < 0 || order > 5 || !x || (h > 0 && !D_hist))
     return set_error(ctx, DDM_ERR_ARG, "march_guess: bad argument");
   cudaStream_t s = (cudaStream_t)stream;
   if (len == 0) return DDM_OK;
@@ -888,7 +900,8 @@ int ddm_march_guess(ddm_ctx_t ctx, int h, const double* D_hist, int64_t len, int
   }
   const int q = std::min(order, h - 1);
   auto prev = [&](int j) { return D_hist + (int64_t)(h - 1 - std::min(j, h - 1)) * len; };
-  march_guess_kernel<<<nblk(len, 256), 256, 0, s>>>(len, q, prev(0), prev(1), prev(2), prev(3), x);
+  march_guess_kernel<<<nblk(len, 256), 256, 0, s>>>(len, q, prev(0), prev(1), prev(2), prev(3),
+                                                     prev(4), prev(5), x);
   return cuda_error_if(ctx, cudaGetLastError(), "march_guess_kernel");
 }
 

@@ -27,7 +27,8 @@ def march(ctx, tree, mat, dt: float, b: torch.Tensor, steps: int, tol: float = 1
     False (zero).  The guess only changes the iteration count: every step is
     solved to the same relative residual.  Config 4, 200 steps: 21 721 GMRES
     iterations from D^{h-1}, 17 609 linear, 11 892 quadratic, 10 085 cubic."""
-    order = {"extrap3": 3, "extrap2": 2, "extrap": 1}.get(warm_start, 0 if warm_start else -1)
+    order = {"extrap5": 5, "extrap4": 4, "extrap3": 3, "extrap2": 2,
+             "extrap": 1}.get(warm_start, 0 if warm_start else -1)
     n = tree.n
     D = torch.zeros((steps, n, 3), dtype=torch.float64, device=b.device)
     rhs = torch.empty_like(b)

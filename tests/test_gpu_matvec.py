@@ -452,16 +452,19 @@ def test_march_guess_extrapolation(ddm):
     lowered while fewer steps exist, h = 0 -> zero."""
     D, ctx, torch = ddm
     rng = np.random.default_rng(5)
-    H = rng.standard_normal((5, 37, 3))
+    H = rng.standard_normal((7, 37, 3))
     Ht = torch.tensor(H, device="cuda")
     x = torch.empty((37, 3), dtype=torch.float64, device="cuda")
     D.march_guess(ctx, Ht[:0], 3, x)
     assert not x.cpu().numpy().any()
     exp = {0: lambda d: d[-1], 1: lambda d: d[-1] * 2.0 - d[-2],
            2: lambda d: (d[-1] - d[-2]) * 3.0 + d[-3],
-           3: lambda d: ((4.0 * d[-1] - 6.0 * d[-2]) + 4.0 * d[-3]) - d[-4]}
-    for h in range(1, 6):
-        for order in range(4):
+           3: lambda d: ((4.0 * d[-1] - 6.0 * d[-2]) + 4.0 * d[-3]) - d[-4],
+           4: lambda d: (((5.0 * d[-1] - 10.0 * d[-2]) + 10.0 * d[-3]) - 5.0 * d[-4]) + d[-5],
+           5: lambda d: ((((6.0 * d[-1] - 15.0 * d[-2]) + 20.0 * d[-3]) - 15.0 * d[-4])
+                         + 6.0 * d[-5]) - d[-6]}
+    for h in range(1, 8):
+        for order in range(6):
             D.march_guess(ctx, Ht[:h], order, x)
             ref = exp[min(order, h - 1)](H[:h])
             assert np.array_equal(x.cpu().numpy(), ref), (h, order)
