@@ -1360,6 +1360,9 @@ __global__ void finalize_kernel(int64_t e_lo, int64_t e_hi, int ncomp,
                                 const int* __restrict__ item_off, const double* __restrict__ part,
                                 const double* __restrict__ y_far, const int* __restrict__ perm,
                                 double* __restrict__ y_user, double* __restrict__ y_sorted) {
+  // a PDL-launched successor (the GMRES step's first CGS kernel) may start early;
+  // it waits for this grid before reading anything
+  asm volatile("griddepcontrol.launch_dependents;");
   const int64_t i = e_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= e_hi) return;
   const int k = el_leaf[i];

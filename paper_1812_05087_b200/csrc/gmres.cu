@@ -21,6 +21,38 @@
 
 #include "kcommon.cuh"
 
+namespace {
+// Programmatic dependent launch inside the captured Arnoldi step (DESIGN.md
+// §4.7h): the CGS and finish kernels are launched with programmatic stream
+// serialisation, trigger their dependents at entry and wait for their
+// predecessor before touching anything (no-ops without the attribute).
+__device__ __forceinline__ void step_pdl() {
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// launch with programmatic stream serialisation (DDM_GMRES_PDL=0: plain)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_step(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t shm,
+                        cudaStream_t s, Args... args) {
+  static const bool on = [] {
+    const char* e = getenv("DDM_GMRES_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = shm;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+}  // namespace
+
 namespace ddm {
 namespace {
 
@@ -135,6 +167,7 @@ cgs_axpy(const double* __restrict__ V, int64_t ld, int nvec, const double* __res
          double sign, double* __restrict__ w, int64_t len, double* __restrict__ part,
          unsigned* __restrict__ ticket, double* __restrict__ out, const int* __restrict__ kd,
          int pass, double dgks = 0.0) {
+  step_pdl();
   extern __shared__ double sc[];
   __shared__ double red[kAxGroups][kAxRows];
   __shared__ double wsum[kAxRows / 32 > 0 ? kAxRows / 32 : 1];
@@ -271,6 +304,7 @@ __global__ void __launch_bounds__(RT)
 cgs_rows(const double* __restrict__ V, int64_t ld, int64_t len, double* __restrict__ w,
          const int* __restrict__ kd, double* __restrict__ dh, double* __restrict__ part,
          unsigned* __restrict__ ticket) {
+  step_pdl();
   __shared__ double red[RT / 32][kRowChunk];   // per-warp sums of a chunk of vectors
   __shared__ bool last;
   const int k = *kd, nvec = k + 1, nb = gridDim.x;
@@ -730,6 +764,7 @@ finish_scale_pc(int k, const double* __restrict__ dh, double* __restrict__ Hp,
                 const int2* __restrict__ chunks, const int64_t* __restrict__ off, int ncomp,
                 const double* __restrict__ inv, double* __restrict__ uf, int* __restrict__ kd,
                 int64_t nloc, unsigned* __restrict__ kd_ticket) {
+  step_pdl();
   __shared__ double xs[kPcChunk * 3];
   __shared__ double2 part[kApplyThreads];
   if (kd) {
@@ -832,17 +867,23 @@ struct Gm {
         (int64_t)(m + 1) * nbr <= part_cap) {
       // row-blocked: dots, fused (update + second-pass dots), update + norm
       if (getenv("DDM_GMRES_TRACE")) fprintf(stderr, "[gmres] row-blocked CGS2, %d CTAs, m %d\n", nbr, m);
-      if (rows_env == 2)
-        multi_dot<<<dim3(b, gy), kDotThreads, 0, s>>>(V, nloc, w, nloc, b, part, ticket, dh, kd, 0);
-      else
-        rt == 512 ? cgs_rows<0, 512><<<nbr, 512, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket)
-        : rt == 256 ? cgs_rows<0, 256><<<nbr, 256, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket)
-                    : cgs_rows<0, 128><<<nbr, 128, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket);
-      rt == 512 ? cgs_rows<1, 512><<<nbr, 512, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket)
-      : rt == 256 ? cgs_rows<1, 256><<<nbr, 256, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket)
-                  : cgs_rows<1, 128><<<nbr, 128, 0, s>>>(V, nloc, nloc, w, kd, dh, part, ticket);
-      cgs_axpy<true><<<ga, kAxRows * kAxGroups, shc, s>>>(V, nloc, 0, dh, -1.0, w, nloc, part,
-                                                         ticket_norm, dh, kd, 1, 0.0);
+      {
+        const int64_t ln = nloc;
+        cudaError_t e0;
+        if (rows_env == 2) {
+          multi_dot<<<dim3(b, gy), kDotThreads, 0, s>>>(V, nloc, w, nloc, b, part, ticket, dh, kd, 0);
+          e0 = cudaGetLastError();
+        } else
+          e0 = rt == 512 ? launch_step(cgs_rows<0, 512>, nbr, 512, 0, s, V, ln, ln, w, kd, dh, part, ticket)
+               : rt == 256 ? launch_step(cgs_rows<0, 256>, nbr, 256, 0, s, V, ln, ln, w, kd, dh, part, ticket)
+                           : launch_step(cgs_rows<0, 128>, nbr, 128, 0, s, V, ln, ln, w, kd, dh, part, ticket);
+        DDM_CUDA(ctx, e0);
+        DDM_CUDA(ctx, rt == 512 ? launch_step(cgs_rows<1, 512>, nbr, 512, 0, s, V, ln, ln, w, kd, dh, part, ticket)
+                      : rt == 256 ? launch_step(cgs_rows<1, 256>, nbr, 256, 0, s, V, ln, ln, w, kd, dh, part, ticket)
+                                  : launch_step(cgs_rows<1, 128>, nbr, 128, 0, s, V, ln, ln, w, kd, dh, part, ticket));
+        DDM_CUDA(ctx, launch_step(cgs_axpy<true>, ga, kAxRows * kAxGroups, shc, s, V, ln, 0,
+                                  (const double*)dh, -1.0, w, ln, part, ticket_norm, dh, kd, 1, 0.0));
+      }
       DDM_CUDA(ctx, cudaGetLastError());
       return DDM_OK;
     }
@@ -1280,9 +1321,13 @@ int gmres_solve(ddm_ctx_s* ctx, ddm_tree_s* t, const ddm_material* mat, double d
         }();
         if (!rc2) rc2 = gc.cgs2_k(V, m, wf + lo, kdd, dgks_eta2);
         if (!rc2)
-          finish_scale_pc<<<t->pc_nchunks, kApplyThreads, 0, sc>>>(
-              0, g.dh, Hd, csd, snd, gd, estd, scald, flagd, wf + lo, V, t->pc_chunks, t->pc_off,
-              ncomp, t->pcl, uf, kdd, nloc, kd_tick);
+          rc2 = cuda_error_if(ctx, launch_step(finish_scale_pc, (unsigned)t->pc_nchunks, kApplyThreads,
+                                              0, sc, 0, (const double*)g.dh, Hd, csd, snd, gd, estd,
+                                              scald, flagd, (const double*)(wf + lo), V,
+                                              (const int2*)t->pc_chunks, (const int64_t*)t->pc_off,
+                                              ncomp, (const double*)t->pcl, uf, kdd, (int64_t)nloc,
+                                              kd_tick),
+                              "finish_scale_pc");
         const cudaError_t ce = cudaStreamEndCapture(sc, &graph);
         if (rc2) {
           if (graph) cudaGraphDestroy(graph);

@@ -744,6 +744,9 @@ __global__ void finalize_near_kernel(int64_t e_lo, int64_t e_hi, const double2* 
                                      const double2* __restrict__ y_far,
                                      const int* __restrict__ perm, double2* __restrict__ y_user,
                                      double2* __restrict__ y_sorted) {
+  // a PDL-launched successor (the GMRES step's first CGS kernel) may start early;
+  // it waits for this grid before reading anything
+  asm volatile("griddepcontrol.launch_dependents;");
   const int64_t i = e_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= e_hi) return;
   const double2 a = y_near[i], b = y_far[i];

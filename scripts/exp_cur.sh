@@ -1,2 +1,3 @@
-timeout 600 python -m pytest tests/test_gpu_matvec.py -x -q -k march_guess 2>&1 | tail -1
-for ws in extrap3 extrap4 extrap5; do python scripts/march_probe.py 200 $ws 2>&1 | grep march; done
+timeout 900 python -m pytest tests/test_gpu_matvec.py tests/test_gpu_poro.py -x -q -k "gmres or march" 2>&1 | tail -1
+GMRES_CFGS=2,3 python scripts/gmres_timing.py 3 2>&1 | grep solve
+python scripts/march_probe.py 2>&1 | grep march
