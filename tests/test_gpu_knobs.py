@@ -80,6 +80,10 @@ print("RESULT " + json.dumps(out))
     {"DDM_POISON": "1", "DDM_GMRES_GRAPH": "0", "DDM_P2P_LEAF": "0", "DDM_L2P_BLOCK": "0"},
     # vector-parallel CGS kernels instead of the row-blocked ones
     {"DDM_GMRES_ROWS": "0", "DDM_P2P_ORDER": "0", "DDM_L2P_ORDER": "0"},
+    # round 2 (late): CGS row blocks of 512 / 256 rows, GMRES step without PDL,
+    # M2L with one warp per cell; X lists on (§4.13)
+    {"DDM_GMRES_ROWT": "512", "DDM_GMRES_PDL": "0", "DDM_M2L_SPLIT": "1"},
+    {"DDM_GMRES_ROWT": "256", "DDM_M2L_SPLIT": "2", "DDM_X_MIN": "1", "DDM_POISON": "1"},
 ])
 def test_knob_paths_agree_with_oracle(env):
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=dict(os.environ, **env),
