@@ -993,7 +993,30 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
 
   // ---- X lists and the U ranges without them (elastic series FMM only)
   if (const char* e = getenv("DDM_X_MIN")) t->xl_min = atoi(e);
-  {
+  if (t->xl_min <= 0) {
+    // X lists off (the default): no X entries, U minus X = U -- device copies,
+    // no host round trip in the build
+    const int nl = t->nleaves;
+    t->nx = 0;
+    t->nux = t->nu;
+    t->near_pairs_x = t->near_pairs;
+    if ((rc = talloc(ctx, &t->x_off, nl + 1, s)) || (rc = talloc(ctx, &t->x_idx, 1, s)) ||
+        (rc = talloc(ctx, &t->x_slot, (size_t)t->ncells, s)) ||
+        (rc = talloc(ctx, &t->ux_off, nl + 1, s)) ||
+        (rc = talloc(ctx, &t->ux_lo, std::max<int64_t>(t->nu, 1), s)) ||
+        (rc = talloc(ctx, &t->ux_hi, std::max<int64_t>(t->nu, 1), s)))
+      return rc;
+    DDM_CUDA(ctx, cudaMemsetAsync(t->x_off, 0, (size_t)(nl + 1) * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMemsetAsync(t->x_slot, 0xFF, (size_t)t->ncells * sizeof(int), s));
+    DDM_CUDA(ctx, cudaMemcpyAsync(t->ux_off, t->u_off, (size_t)(nl + 1) * sizeof(int),
+                                  cudaMemcpyDeviceToDevice, s));
+    if (t->nu > 0) {
+      DDM_CUDA(ctx, cudaMemcpyAsync(t->ux_lo, t->u_lo, (size_t)t->nu * sizeof(int),
+                                    cudaMemcpyDeviceToDevice, s));
+      DDM_CUDA(ctx, cudaMemcpyAsync(t->ux_hi, t->u_hi, (size_t)t->nu * sizeof(int),
+                                    cudaMemcpyDeviceToDevice, s));
+    }
+  } else {
     const int nl = t->nleaves;
     int *xcnt = nullptr, *uxcnt = nullptr;
     long long *pairs = nullptr, *pairs_scan = nullptr;
