@@ -323,8 +323,12 @@ cgs_rows(const double* __restrict__ V, int64_t ld, int64_t len, double* __restri
       double a2 = 0.0, a3 = 0.0;
       for (; i + DDM_ROW_UPD <= nvec; i += DDM_ROW_UPD) {
         double tv[DDM_ROW_UPD];
+        const double* vp = Vj + (int64_t)i * ld;
 #pragma unroll
-        for (int u = 0; u < DDM_ROW_UPD; ++u) tv[u] = v_ld(Vj + (int64_t)(i + u) * ld, pol);
+        for (int u = 0; u < DDM_ROW_UPD; ++u) {
+          tv[u] = v_ld(vp, pol);
+          vp += ld;
+        }
 #pragma unroll
         for (int u = 0; u < DDM_ROW_UPD; u += 4) {
           a0 = fma(tv[u], __ldg(sc + i + u), a0);
@@ -359,13 +363,24 @@ cgs_rows(const double* __restrict__ V, int64_t ld, int64_t len, double* __restri
     // groups of 8 vectors, four groups' loads in flight at once
     for (int g0 = c0; g0 < c1; g0 += 32) {
       double a[4][8];
+      if (g0 + 32 <= c1) {   // full group: a running pointer, no bounds checks
+        const double* vp = Vj + (int64_t)g0 * ld;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const int i = g0 + 8 * q + v;
-          a[q][v] = i < c1 ? v_ld(Vj + (int64_t)i * ld, pol) : 0.0;
-        }
+          for (int v = 0; v < 8; ++v) {
+            a[q][v] = v_ld(vp, pol);
+            vp += ld;
+          }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const int i = g0 + 8 * q + v;
+            a[q][v] = i < c1 ? v_ld(Vj + (int64_t)i * ld, pol) : 0.0;
+          }
+      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
 #pragma unroll

@@ -1,1 +1,2 @@
-for cfg in 3 4; do echo "cfg $cfg"; python scripts/timeline.py $cfg 2>&1 | grep step; DDM_L2P_BLOCK=0 python scripts/timeline.py $cfg 2>&1 | grep step; DDM_P2M_RUN_HB=1 python scripts/timeline.py $cfg 2>&1 | grep step; DDM_PDL=0 python scripts/timeline.py $cfg 2>&1 | grep step; DDM_EARLY_FAR=0 python scripts/timeline.py $cfg 2>&1 | grep step; done
+GMRES_CFGS=2,3 python scripts/gmres_timing.py 3 2>&1 | grep solve
+timeout 900 ncu --profile-from-start off --clock-control none --cache-control none --metrics gpu__time_duration.sum,smsp__inst_executed.sum -k regex:"cgs_rows" --launch-skip 300 -c 4 --csv python scripts/gmres_ncu.py 3 2>/dev/null | grep -E "cgs_rows" | cut -d, -f5,13-15
