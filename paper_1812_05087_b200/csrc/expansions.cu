@@ -1644,6 +1644,11 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s, bool use_x) {
   // warps per cell (small trees: a cell's V list over S warps, §4.4d); a
   // property of the whole tree, so every rank sums the same way
   static const int m2l_s_env = env_int("DDM_M2L_SPLIT", -1);
+  // M2L blocks per SM: on large trees (no PDL: the M2L overlaps the near
+  // field) one block per SM leaves the near field its slots (config 5 step
+  // 0.951 -> 0.941 ms); DDM_M2L_CAP overrides
+  static const int m2l_cap_env = env_int("DDM_M2L_CAP", -1);
+  const int m2l_cap = m2l_cap_env >= 0 ? m2l_cap_env : (use_pdl(t) ? -1 : 1);
   const int64_t ncell2 = (int64_t)t->ncells - t->level_off[2];
   const int S = !tc ? 1 : m2l_s_env >= 0 ? std::max(1, std::min(4, m2l_s_env))
                         : ncell2 <= 768 ? 4 : 1;
@@ -1652,7 +1657,7 @@ int launch_downward(ddm_ctx_s* ctx, ddm_tree_s* t, cudaStream_t s, bool use_x) {
 #define DDM_L(PT)                                                                               \
   do {                                                                                          \
     if ((rc = set_smem(ctx, m2l_kernel<PT>, shm))) return rc;                                   \
-    const int nb = pass_grid(ctx, (const void*)m2l_kernel<PT>, shm, (c1 - c0) * S, env_int("DDM_M2L_CAP", -1)); \
+    const int nb = pass_grid(ctx, (const void*)m2l_kernel<PT>, shm, (c1 - c0) * S, m2l_cap);  \
     stage_begin(ctx, DDM_ST_M2L, s);                                                            \
     DDM_CUDA(ctx, launch_pdl(use_pdl(t) && !use_x, m2l_kernel<PT>, nb, kPassWarps * 32, shm, s, \
                              c0, c1,                                                           \

@@ -1,5 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_matvec.py tests/test_gpu_poro.py tests/test_gpu_precond.py -x -q -k "gmres or march or precond" 2>&1 | tail -1
-GMRES_CFGS=2,3 python scripts/gmres_timing.py 3 2>&1 | grep solve
-GMRES_CFGS=2,3 DDM_GMRES_RPT=1 python scripts/gmres_timing.py 3 2>&1 | grep solve
-python scripts/march_probe.py 2>&1 | grep march
-DDM_GMRES_RPT=1 python scripts/march_probe.py 2>&1 | grep march
+for i in 1 2; do python scripts/timeline.py 5 2>&1 | grep step; DDM_M2L_CAP=2 python scripts/timeline.py 5 2>&1 | grep step; done
+python scripts/timeline.py 3 2>&1 | grep step
+DDM_L2P_CAP=1 python scripts/timeline.py 5 2>&1 | grep step
