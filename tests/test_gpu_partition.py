@@ -136,3 +136,13 @@ def test_sharded_upward_pass_emulated_cfg5_cut(ddm):
     g = Geometry(g5.xc[keep], g5.yc[keep], g5.half_len[keep], g5.beta[keep], g5.frac_id[keep],
                  g5.tips[:1000])
     _sim_case(D, ctx, torch, g, 64, 20, (2, 8), 55)
+
+
+def test_sharded_emulated_with_x_lists(ddm, monkeypatch):
+    """The same bitwise equality with X lists on (DDM_X_MIN = 8, SURVEY §8f
+    f3): each rank runs the P2L of its own leaves, its M2L adds the series of
+    the leaves in its cell list, and its near field reads U minus X."""
+    D, ctx, torch = ddm
+    monkeypatch.setenv("DDM_X_MIN", "8")
+    g = make_config(2)
+    _sim_case(D, ctx, torch, g, 16, 20, (1, 2, 5), 77)
