@@ -515,7 +515,10 @@ p2p_kernel(int nown, const int* __restrict__ order, const int4* __restrict__ ite
 // slice), slice s taking the s-th contiguous part of the chunk's records (a
 // node carry is re-initialised where a range starts).  Slice partials are
 // summed in a fixed order: deterministic, independent of the rank count.
-constexpr int kLeafThreads = 128;
+#ifndef DDM_LEAF_THREADS
+#define DDM_LEAF_THREADS 128
+#endif
+constexpr int kLeafThreads = DDM_LEAF_THREADS;
 #ifndef DDM_LEAF_TPL
 #define DDM_LEAF_TPL 2
 #endif
