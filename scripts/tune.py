@@ -50,18 +50,20 @@ def main():
         defs = [] if v == "base" else v.split(",")
         out = f"/tmp/ddm_var_{abs(hash(v))}.so"
         B.build(defines=defs, out=out, force=True)
-        env = dict(os.environ, DDM_LIB=out)
-        serial = os.environ.get("TUNE_SERIAL", "1")
-        env["DDM_SERIAL"] = serial
-        r = subprocess.run([sys.executable, "-c", MEASURE], env=env, capture_output=True, text=True)
-        line = [ln for ln in r.stdout.splitlines() if ln.startswith("RESULT ")]
-        if not line:
-            print(v, "FAILED", r.stderr[-2000:])
-            continue
-        d = json.loads(line[0][7:])
-        print(f"{v:40s} " + " ".join(f"{k}={d[k]:.3f}" for k in
-                                      ("total", "prep", "p2p", "p2l", "p2m", "m2m", "m2l", "l2l", "l2p", "final")),
-              flush=True)
+        # TUNE_SERIAL=1 (serial stages), 0 (concurrent schedule) or "both"
+        mode = os.environ.get("TUNE_SERIAL", "1")
+        for serial in (["1", "0"] if mode == "both" else [mode]):
+            env = dict(os.environ, DDM_LIB=out, DDM_SERIAL=serial)
+            r = subprocess.run([sys.executable, "-c", MEASURE], env=env, capture_output=True, text=True)
+            line = [ln for ln in r.stdout.splitlines() if ln.startswith("RESULT ")]
+            if not line:
+                print(v, "FAILED", r.stderr[-2000:])
+                continue
+            d = json.loads(line[0][7:])
+            tag = f"{v} [{'serial' if serial == '1' else 'concurrent'}]"
+            print(f"{tag:52s} " + " ".join(f"{k}={d[k]:.3f}" for k in
+                                          ("total", "prep", "p2p", "p2l", "p2m", "m2m", "m2l", "l2l", "l2p", "final")),
+                  flush=True)
 
 
 if __name__ == "__main__":

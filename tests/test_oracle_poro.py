@@ -174,8 +174,30 @@ def test_stress_equilibrium(src):
         assert abs(divx) <= 1e-5 * scale and abs(divy) <= 1e-5 * scale
 
 
+def _tanh_sinh(lo, hi, h, tmax=4.0):
+    """Double-exponential (tanh-sinh) nodes and weights on [lo, hi] with step
+    h: a quadrature family independent of the oracle's graded Gauss-Legendre
+    rule, exponentially convergent for integrands analytic inside the interval
+    with integrable endpoint singularities.  Nodes are placed by their distance
+    from the nearer endpoint (no rounding onto the endpoint)."""
+    t = np.arange(-tmax, tmax + h / 2, h)
+    u = 0.5 * np.pi * np.sinh(t)
+    w = h * 0.5 * np.pi * np.cosh(t) / np.cosh(u) ** 2
+    d = 1.0 / (np.exp(np.abs(u)) * np.cosh(u))   # 1 - |x| for x = tanh(u)
+    r = 0.5 * (hi - lo)
+    s = np.where(u >= 0, hi - r * d, lo + r * d)
+    keep = (r * d > 0) & (s > lo) & (s < hi)
+    return s[keep], r * w[keep]
+
+
 @pytest.mark.parametrize("where", ["self", "near_off_line", "collinear", "close_parallel"])
-def test_element_rule_matches_adaptive_quadrature(where):
+def test_element_rule_matches_double_exponential_quadrature(where):
+    """The fixed element rule (graded Gauss-Legendre, oracle/poro.py
+    element_integral) against a converged tanh-sinh integral of the point
+    kernel over the element, split at the foot of the perpendicular and at a
+    few distances from it.  The reference is converged when steps h = 1/16
+    and 1/32 agree; the offsets are formed as (rel - s) e, so nodes next to
+    the target keep their relative accuracy."""
     k = K3
     e = np.exp(1j * BS)
     a = 0.025
@@ -183,27 +205,31 @@ def test_element_rule_matches_adaptive_quadrature(where):
     zt = {"self": ZC, "near_off_line": ZC + 0.03 * np.exp(1j * (BS + 1.2)),
           "collinear": ZC + 0.05 * e, "close_parallel": ZC + 0.01 * e + 0.02j * e}[where]
     rel = (zt - ZC) * np.conj(e)
+    foot = min(max(rel.real, -a), a)
+    dp = max(abs(rel.imag), 1e-3 * a)
+    pts = sorted({x for x in (-a, a, foot, foot - dp, foot + dp, foot - 4 * dp, foot + 4 * dp)
+                  if -a <= x <= a})
     for src in ((1.0, 0.0, 0.0), (0.0, 1.0, 0.0), (0.0, 0.0, 1.0)):
         _, p, d2 = P.element_integral(zt, ZC, e, a, tau, k, *src)
-        def fk(s, part):
-            pp, dd = P.point_kernel(np.array([zt - (ZC + s * e)]), tau, k, e, *src)
-            return {"p": pp[0].real, "dr": dd[0].real, "di": dd[0].imag}[part]
-        # break the adaptive rule at the foot of the perpendicular and at
-        # offsets of a few distances from it, where the integrand has its peak
-        foot = min(max(rel.real, -a), a)
-        dp = max(abs(rel.imag), 1e-3 * a)
-        pts = sorted({x for x in (foot, foot - dp, foot + dp, foot - 4 * dp, foot + 4 * dp)
-                      if -a < x < a}) or None
-        ref = {part: integrate.quad(fk, -a, a, args=(part,), points=pts, epsabs=0,
-                                    epsrel=1e-13, limit=400)[0] for part in ("p", "dr", "di")}
-        # tolerance relative to the integral of the absolute integrand (the
-        # antisymmetric cases integrate to ~0)
-        mag = {part: integrate.quad(lambda s: abs(fk(s, part)), -a, a, points=pts,
-                                    limit=400)[0] for part in ("p", "dr", "di")}
+        ref = []
+        for h in (1 / 16, 1 / 32):
+            tp, td, mag = 0.0, 0.0, 0.0
+            for lo, hi in zip(pts[:-1], pts[1:]):
+                s, w = _tanh_sinh(lo, hi, h)
+                off = (rel - s) * e
+                m = np.abs(off) > 1e-140          # r^2 would underflow
+                pp, dd = P.point_kernel(off[m], tau, k, e, *src)
+                tp += np.sum(w[m] * pp.real)
+                td += np.sum(w[m] * dd)
+                mag += np.sum(w[m] * (np.abs(pp.real) + np.abs(dd)))
+            ref.append((tp, td, mag))
+        (p16, d16, mag), (p32, d32, _) = ref
         floor = 1e-12 * k["G"] * a      # rounding floor of fields that vanish by symmetry
-        assert abs(p.real - ref["p"]) <= 1e-11 * mag["p"] + floor
-        assert abs(d2.real - ref["dr"]) <= 1e-11 * (mag["dr"] + mag["di"]) + floor
-        assert abs(d2.imag - ref["di"]) <= 1e-11 * (mag["dr"] + mag["di"]) + floor
+        # the reference is converged ...
+        assert abs(p16 - p32) <= 1e-14 * mag and abs(d16 - d32) <= 1e-14 * mag
+        # ... and the element rule reproduces it (measured <= 3e-16 of mag)
+        assert abs(p.real - p32) <= 1e-13 * mag + floor, (where, src)
+        assert abs(d2 - d32) <= 1e-13 * mag + floor, (where, src)
 
 
 def test_abi_matrix_convention_and_undrained_block():
@@ -347,10 +373,9 @@ def test_fluid_source_far_field_is_centre_of_dilatation():
             Phi, dPhi, Psi, p = P._far_element(zt, ZC, e, a, tau, K3, 0.0, 0.0, 1.0)
             Tf = 2 * Phi.real + np.exp(2j * bt) * (np.conj(zt) * dPhi + Psi)
 
-            def part(s, f):
-                w = zt - (ZC + s * e)
-                return f(np.exp(2j * bt) * (K3["eta"] * V / np.pi) * np.conj(w) ** 2 / abs(w) ** 4)
-            ref = (integrate.quad(part, -a, a, args=(np.real,), epsabs=0, epsrel=1e-13)[0]
-                   + 1j * integrate.quad(part, -a, a, args=(np.imag,), epsabs=0, epsrel=1e-13)[0])
+            # conj(w)^2 / |w|^4 = 1 / w^2 and dw/ds = -e, so the integral over
+            # the element is closed-form: (1/e) [1/w(a) - 1/w(-a)]
+            wa, wb = zt - (ZC + a * e), zt - (ZC - a * e)
+            ref = np.exp(2j * bt) * (K3["eta"] * V / np.pi) * (1 / wa - 1 / wb) / e
             assert abs(Tf - ref) <= 1e-12 * abs(ref)
             assert p == 0.0 or abs(p) <= 1e-30
