@@ -76,7 +76,7 @@ def test_fmm_parity_random_vector(ddm, cfg):
     assert rel_l2(y, ref) <= 1e-8
 
 
-@pytest.mark.parametrize("leaf,p", [(12, 28), (48, 20), (100, 20)])
+@pytest.mark.parametrize("leaf,p", [(12, 28), (48, 20), (100, 20), (500, 20)])
 def test_fmm_parity_leaf_sizes(ddm, leaf, p):
     """Config 2 with other leaf sizes: leaves of 1-12 elements (many leaves
     per P2M run), up to 48 (runs mixing one- to three-half-block leaves) and
@@ -84,9 +84,15 @@ def test_fmm_parity_leaf_sizes(ddm, leaf, p):
     DESIGN.md §4.12), against the dense oracle.  Leaf 12 makes an 8-level tree
     whose deepest cells are not much larger than the elements: the series
     converge more slowly there (measured 5.8e-8 / 5.4e-9 / 1.5e-10 at p = 20 /
-    24 / 30, the same with one leaf per P2M run), so it is checked at p* = 28."""
+    24 / 30, the same with one leaf per P2M run), so it is checked at p* = 28.
+    Leaf 500 (a 13-leaf tree, largest leaf 407 elements): leaves above
+    kChainMax = 256 elements keep Morton order in the
+    near-field stream (no node sharing), and their P2P leaf blocks run several
+    64-target passes over several staged record chunks."""
     D, ctx, torch = ddm
     g, tree = _setup(D, ctx, torch, 2, leaf=leaf, p=p)
+    if leaf == 500:
+        assert tree.export("COUNT")[tree.export("LEAVES")].max() > 256
     Dv = random_dd(g.n, 2, 300 + leaf)
     y = _mv(D, ctx, torch, tree, Dv, "fmm")
     assert rel_l2(y, OE.matvec_dense(_A(2), Dv)) <= 1e-8
