@@ -214,6 +214,19 @@ __global__ void create_cells(const uint64_t* __restrict__ keys, const int* __res
   if (i == c.start[par]) c.first_child[par] = id;
 }
 
+// the root cell (index 0): level 0, the whole sorted range
+__global__ void root_cell_init(Cells c, int n, int root_leaf) {
+  c.level[0] = 0;
+  c.ix[0] = 0;
+  c.iy[0] = 0;
+  c.start[0] = 0;
+  c.count[0] = n;
+  c.parent[0] = -1;
+  c.first_child[0] = -1;
+  c.nchild[0] = 0;
+  c.leaf[0] = root_leaf;
+}
+
 __global__ void finish_cells(int base, int m, int leaf, int lev, int lmax, Cells c,
                              int* __restrict__ nsplit, int* __restrict__ geom_bad) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -773,22 +786,8 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
   Cells C;
   if ((rc = cells_reserve(ctx, C, (int)std::max<int64_t>(64, 4 * (n / leaf + 1) + 8), 0, s)))
     return rc;
-  {
-    const int zero = 0, one = 1, m1 = -1;
-    const int nn = (int)n;
-    const int root_leaf = (n <= leaf || lmax == 0) ? 1 : 0;
-    DDM_CUDA(ctx, cudaMemcpyAsync(C.level, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
-    DDM_CUDA(ctx, cudaMemcpyAsync(C.ix, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
-    DDM_CUDA(ctx, cudaMemcpyAsync(C.iy, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
-    DDM_CUDA(ctx, cudaMemcpyAsync(C.start, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
-    DDM_CUDA(ctx, cudaMemcpyAsync(C.count, &nn, sizeof(int), cudaMemcpyHostToDevice, s));
-    DDM_CUDA(ctx, cudaMemcpyAsync(C.parent, &m1, sizeof(int), cudaMemcpyHostToDevice, s));
-    DDM_CUDA(ctx, cudaMemcpyAsync(C.first_child, &m1, sizeof(int), cudaMemcpyHostToDevice, s));
-    DDM_CUDA(ctx, cudaMemcpyAsync(C.nchild, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
-    DDM_CUDA(ctx, cudaMemcpyAsync(C.leaf, &root_leaf, sizeof(int), cudaMemcpyHostToDevice, s));
-    DDM_CUDA(ctx, cudaStreamSynchronize(s));
-    (void)one;
-  }
+  root_cell_init<<<1, 1, 0, s>>>(C, (int)n, (n <= leaf || lmax == 0) ? 1 : 0);
+  DDM_CUDA(ctx, cudaGetLastError());
   t->level_off.assign(1, 0);
   t->level_off.push_back(1);
   int ncells = 1;
@@ -802,13 +801,23 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
     DDM_CUDA(ctx, cudaMemsetAsync(dgeom, 0, sizeof(int), s));
     const bool root_split = !(n <= leaf || lmax == 0);
     DDM_CUDA(ctx, cudaMemsetAsync(cur, root_split ? 0 : 0xff, n * sizeof(int), s));
+    // A level is processed while the previous one split a cell.  Whether it
+    // did is read from the next level's scan total (no cell splits <=> no
+    // element is flagged, m = 0), so each level costs one host read-back
+    // (the scan total) instead of two; the split counter of the last level is
+    // read once after the loop, for the depth check.
     int nsplit = root_split ? 1 : 0;
-    for (int lev = 0; nsplit > 0 && lev < kLBits; ++lev) {
+    int lev = 0;
+    for (; nsplit > 0 && lev < kLBits; ++lev) {
       const int sh = 2 * (kLBits - lev - 1);
       split_flags<<<nblk(n, 256), 256, 0, s>>>(t->keys, cur, C.start, n, sh, flag);
       DDM_CUDA(ctx, cudaGetLastError());
       int m = 0;
       if ((rc = exclusive_scan_i32(ctx, flag, pos, (int)n, &m, s))) return rc;
+      if (m == 0) {   // the previous level split nothing
+        nsplit = 0;
+        break;
+      }
       if ((rc = cells_reserve(ctx, C, ncells + m, ncells, s))) return rc;
       create_cells<<<nblk(n, 256), 256, 0, s>>>(t->keys, cur, flag, pos, n, sh, lev + 1,
                                                 ncells, C);
@@ -819,13 +828,13 @@ int build_tree(ddm_ctx_s* ctx, const double* xc, const double* yc, const double*
       DDM_CUDA(ctx, cudaGetLastError());
       update_cur<<<nblk(n, 256), 256, 0, s>>>(cur, flag, pos, n, ncells, C.leaf);
       DDM_CUDA(ctx, cudaGetLastError());
-      DDM_CUDA(ctx, cudaMemcpyAsync(&nsplit, dsplit, sizeof(int), cudaMemcpyDeviceToHost, s));
-      DDM_CUDA(ctx, cudaStreamSynchronize(s));
       ncells += m;
       t->level_off.push_back(ncells);
     }
     int hgeom = 0;
     DDM_CUDA(ctx, cudaMemcpyAsync(&hgeom, dgeom, sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (nsplit > 0)   // the loop stopped at kLBits levels: did the last one still split?
+      DDM_CUDA(ctx, cudaMemcpyAsync(&nsplit, dsplit, sizeof(int), cudaMemcpyDeviceToHost, s));
     DDM_CUDA(ctx, cudaStreamSynchronize(s));
     cudaFreeAsync(cur, s);
     cudaFreeAsync(flag, s);
