@@ -10,6 +10,8 @@ from oracle import elastic as E
 from oracle import poro as P
 from synth.geometry import Geometry
 
+from ._quad import element_integral_ts
+
 MAT = dict(G=6e9, nu=0.2, nu_u=0.33, alpha=0.8, kappa=1e-15)     # BASELINE configs[2]
 WESTERLY = dict(G=15e9, nu=0.25, nu_u=0.331, alpha=0.449, kappa=4e-19 / 1e-3)
 K3 = P.constants(**MAT)
@@ -174,22 +176,6 @@ def test_stress_equilibrium(src):
         assert abs(divx) <= 1e-5 * scale and abs(divy) <= 1e-5 * scale
 
 
-def _tanh_sinh(lo, hi, h, tmax=4.0):
-    """Double-exponential (tanh-sinh) nodes and weights on [lo, hi] with step
-    h: a quadrature family independent of the oracle's graded Gauss-Legendre
-    rule, exponentially convergent for integrands analytic inside the interval
-    with integrable endpoint singularities.  Nodes are placed by their distance
-    from the nearer endpoint (no rounding onto the endpoint)."""
-    t = np.arange(-tmax, tmax + h / 2, h)
-    u = 0.5 * np.pi * np.sinh(t)
-    w = h * 0.5 * np.pi * np.cosh(t) / np.cosh(u) ** 2
-    d = 1.0 / (np.exp(np.abs(u)) * np.cosh(u))   # 1 - |x| for x = tanh(u)
-    r = 0.5 * (hi - lo)
-    s = np.where(u >= 0, hi - r * d, lo + r * d)
-    keep = (r * d > 0) & (s > lo) & (s < hi)
-    return s[keep], r * w[keep]
-
-
 @pytest.mark.parametrize("where", ["self", "near_off_line", "collinear", "close_parallel"])
 def test_element_rule_matches_double_exponential_quadrature(where):
     """The fixed element rule (graded Gauss-Legendre, oracle/poro.py
@@ -204,25 +190,9 @@ def test_element_rule_matches_double_exponential_quadrature(where):
     tau = 100.0
     zt = {"self": ZC, "near_off_line": ZC + 0.03 * np.exp(1j * (BS + 1.2)),
           "collinear": ZC + 0.05 * e, "close_parallel": ZC + 0.01 * e + 0.02j * e}[where]
-    rel = (zt - ZC) * np.conj(e)
-    foot = min(max(rel.real, -a), a)
-    dp = max(abs(rel.imag), 1e-3 * a)
-    pts = sorted({x for x in (-a, a, foot, foot - dp, foot + dp, foot - 4 * dp, foot + 4 * dp)
-                  if -a <= x <= a})
     for src in ((1.0, 0.0, 0.0), (0.0, 1.0, 0.0), (0.0, 0.0, 1.0)):
         _, p, d2 = P.element_integral(zt, ZC, e, a, tau, k, *src)
-        ref = []
-        for h in (1 / 16, 1 / 32):
-            tp, td, mag = 0.0, 0.0, 0.0
-            for lo, hi in zip(pts[:-1], pts[1:]):
-                s, w = _tanh_sinh(lo, hi, h)
-                off = (rel - s) * e
-                m = np.abs(off) > 1e-140          # r^2 would underflow
-                pp, dd = P.point_kernel(off[m], tau, k, e, *src)
-                tp += np.sum(w[m] * pp.real)
-                td += np.sum(w[m] * dd)
-                mag += np.sum(w[m] * (np.abs(pp.real) + np.abs(dd)))
-            ref.append((tp, td, mag))
+        ref = [element_integral_ts(zt, ZC, e, a, tau, k, *src, h=h) for h in (1 / 16, 1 / 32)]
         (p16, d16, mag), (p32, d32, _) = ref
         floor = 1e-12 * k["G"] * a      # rounding floor of fields that vanish by symmetry
         # the reference is converged ...
