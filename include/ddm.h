@@ -104,6 +104,10 @@ const char* ddm_version(void);
 int ddm_build_tree(ddm_ctx_t ctx, const double* xc, const double* yc, const double* half_len,
                    const double* beta, int64_t n, int leaf_size, int order_p,
                    double min_leaf_side, void* stream, ddm_tree_t* out);
+/* Releases every device buffer, captured graph and pinned host buffer of the
+ * tree.  The tree may still be in use on any stream of the caller's, so the
+ * call waits for the device to go idle first (cudaFree would synchronise
+ * anyway); NULL is a no-op. */
 void ddm_tree_free(ddm_tree_t tree);
 
 /* Sizes of the tree's arrays, written into counts[DDM_TREE_NCOUNTS] [host].
