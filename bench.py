@@ -411,7 +411,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-HBM_PEAK_FALLBACK = 6530.0   # GB/s, MEASURED_PEAKS.json on this pool
+HBM_PEAK_FALLBACK = 6650.0   # GB/s, the fallback B200_PROFILING.md states when MEASURED_PEAKS.json is absent
 
 
 def _hbm_peak() -> tuple:
@@ -419,7 +419,7 @@ def _hbm_peak() -> tuple:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy)"
     except Exception:
-        return HBM_PEAK_FALLBACK, "fallback 6530 GB/s (MEASURED_PEAKS.json of this pool, round 1)"
+        return HBM_PEAK_FALLBACK, "of fallback: 6650 GB/s (B200_PROFILING.md, MEASURED_PEAKS.json absent)"
 
 
 def kernel_rooflines(tree, cnt, stages, tree_stages, p, fp64_peak, world):
@@ -497,7 +497,7 @@ def kernel_rooflines(tree, cnt, stages, tree_stages, p, fp64_peak, world):
     return {"step": out, "tree_build": tree_out, "fp64_peak_source":
             "measured DFMA-chain probe (ddm_probe_fp64) on this GPU", "hbm_peak_source": hbm_src,
             "time_source": "CUDA events around each stage's kernels, serial schedule, after the "
-                           "timed region (profiles/r2_kernel_ncu_summary.txt has the ncu rows)"}
+                           "timed region (profiles/r2_step_ncu_summary.txt has the ncu rows)"}
 
 
 def _ncu_traffic(kernel: str):
@@ -640,6 +640,22 @@ def gmres_extra(D, ctx, torch, dev, march_steps: int):
     res["cfg3_poro"] = {"solve_ms": ms, "iters": it, "rel_resid": rr, "matvec_ms": mv_ms,
                         "matvec_first_ms": first_ms,
                         "p": c["p_star"], "near_pairs": tree.counts["NEAR_PAIRS"]}
+    # CGS2 roofline (SURVEY 8(d).2 unit, DESIGN 4.1 a12): Arnoldi step k reads the
+    # k+1 basis vectors four times (dot + axpy, two passes) = 4 (k+1) dof 8 B.  The
+    # time is everything in the solve that is not a matvec (CGS2, preconditioner,
+    # Givens, residual read-backs), so the fraction is a lower bound for the passes.
+    dof = int(b.numel())
+    cgs_bytes = 32.0 * dof * it * (it + 1) / 2
+    rest_ms = max(ms - it * mv_ms, 1e-9)
+    hbm, hbm_src = _hbm_peak()
+    res["cfg3_poro"]["cgs2"] = {
+        "bound": "hbm", "unit": "GB/s", "achieved": cgs_bytes / (rest_ms * 1e-3) / 1e9,
+        "peak": hbm, "frac": cgs_bytes / (rest_ms * 1e-3) / 1e9 / hbm,
+        "bytes_per_iter_mean": cgs_bytes / max(it, 1), "non_matvec_ms_per_iter": rest_ms / max(it, 1),
+        "peak_source": hbm_src,
+        "note": "time = solve - iters x steady matvec (CGS2 + preconditioner + Givens + "
+                "read-backs); the basis (iters x dof x 8 B) stays in the 126 MB L2, the HBM "
+                "copy peak is the conservative denominator"}
     tree.free()
     # config 4: poroelastic time marching (first march_steps of the 200 steps)
     g = make_config(4)
