@@ -71,6 +71,12 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // through a padded [32][17] shared-memory transpose; a leaf's moments are
 // then (((h_0 + h_1) + h_2) + ...) in half-block order -- the same bits
 // whatever run the leaf is in (replicated vs sharded upward pass).
+#ifndef DDM_P2M_PREFETCH
+#define DDM_P2M_PREFETCH 0
+#endif
+__device__ __forceinline__ void prefetch_l1(const void* a) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+}
 template <int PT>
 __device__ void p2m_run(int kk0, int nseg, int p, const int* __restrict__ leaves,
                         const int* __restrict__ c_level, const int* __restrict__ c_ix,
@@ -130,6 +136,29 @@ __device__ void p2m_run(int kk0, int nseg, int p, const int* __restrict__ leaves
     // rows of each slot's half-block, and whether it ends its leaf
     const int nrow = hb < NH ? min(16, s_cnt - (row - row16)) : 0;
     const bool closes = hb < NH && (row - row16) + 16 >= s_cnt;
+#if DDM_P2M_PREFETCH
+    // next round's rows (half-blocks hb + 2): their geometry lines are asked
+    // for now and the user index is held, so D can be asked for once it has
+    // arrived (after this round's arithmetic).  Hints only: no result changes.
+    int jn = -1;
+    {
+      const int hb2 = hb + 2;
+      int seg2 = 0;
+      for (int q = 1; q < nseg; ++q)
+        if (hb2 >= __shfl_sync(full, sg_h0, q)) seg2 = q;
+      const int row2 = 16 * (hb2 - __shfl_sync(full, sg_h0, seg2)) + row16;
+      const int i2 = __shfl_sync(full, sg_start, seg2) + row2;
+      const int cnt2 = __shfl_sync(full, sg_cnt, seg2);
+      if (hb2 < NH && row2 < cnt2) {
+        prefetch_l1(ex + i2);
+        prefetch_l1(ey + i2);
+        prefetch_l1(ea + i2);
+        prefetch_l1(ec + i2);
+        prefetch_l1(es + i2);
+        jn = perm ? perm[i2] : i2;
+      }
+    }
+#endif
     double2 B = make_double2(0, 0), Q = B, rr = B, A = B, z1 = B, z2 = B;
     // poroelastic far field: B-part of Phi and Psi~ scaled by
     // fu, plus Wm conj(e) I2 and Wc B I4 in Psi~ (iGC factored out)
@@ -230,6 +259,9 @@ __device__ void p2m_run(int kk0, int nseg, int p, const int* __restrict__ leaves
           }
         }
         __syncwarp();
+#if DDM_P2M_PREFETCH
+        if (ch == 0 && jn >= 0) prefetch_l1(D + (int64_t)jn * ncomp);
+#endif
       }
     }
   }
