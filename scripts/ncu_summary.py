@@ -15,6 +15,8 @@ METRICS = [
     "gpu__time_duration.sum",
     "dram__bytes_read.sum",
     "dram__bytes_write.sum",
+    "lts__t_bytes.sum",
+    "lts__t_sector_hit_rate.pct",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
     "smsp__inst_executed_pipe_fp64.sum",
